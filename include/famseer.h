@@ -1,0 +1,142 @@
+/* famseer.h - C ABI of the B200-native FamilySeer cost-model hot path (libfamseer.so).
+ *
+ * The reference (/root/reference/proj, "famtune") has no plugin ABI: its hot path is the static
+ * C++ API in namespace famtune. This header is the thin extern "C" layer
+ * underneath the drop-in C++ API (include/famtune/ headers): plain pointers and sizes, no C++ or
+ * torch types, int status codes, one thread-local error string. Each entry point names the
+ * reference function it replaces.
+ *
+ * Conventions
+ *   - Every call is ordered on the device's stream. Entry points taking HOST pointers copy in,
+ *     run, copy out and synchronize before returning (the reference's value semantics). Entry
+ *     points with the suffix _d take DEVICE pointers and are asynchronous; call
+ *     fs_device_check() to synchronize and surface deferred kernel-side errors (non-finite
+ *     features, out-of-range knob indices) as FS_EINVAL.
+ *   - Status: FS_OK on success, otherwise the code of the reference exception it stands for:
+ *       FS_EINVAL  std::invalid_argument  (costmodel.cpp:178-182,226-231,239; searchspace.cpp:95-100)
+ *       FS_EDOMAIN std::domain_error      (costmodel.cpp:273-275)
+ *       FS_ERANGE  std::out_of_range      (family.cpp:81-93)
+ *     plus FS_ECUDA / FS_ENOMEM / FS_ENCCL for device failures. fs_last_error() returns the
+ *     message of the last failing call on this thread.
+ *   - Model layout (costmodel.hpp:27-57): trees concatenated in pre-order; tree t owns nodes
+ *     [offsets[t], offsets[t+1]); feature < 0 marks a leaf; left/right are tree-local.
+ *   - Feature matrices are row-major FP64 [rows][d]; candidate assignments are int32
+ *     [rows][FS_MAX_KNOBS] (knob value indices, unused slots ignored).
+ */
+#ifndef FAMSEER_H
+#define FAMSEER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_MAX_KNOBS 16 /* searchspace.hpp:18 kMaxKnobs */
+
+enum fs_status {
+  FS_OK = 0,
+  FS_EINVAL = 1,
+  FS_EDOMAIN = 2,
+  FS_ERANGE = 3,
+  FS_ECUDA = 4,
+  FS_ENOMEM = 5,
+  FS_ENCCL = 6
+};
+
+typedef struct fs_device fs_device;   /* one per GPU: stream, scratch arena, error word */
+typedef struct fs_spaces fs_spaces;   /* device-resident knob-space table */
+typedef struct fs_forest fs_forest;   /* device-resident ensembles, one per family */
+
+/* GbtParams (costmodel.hpp:20-25). */
+typedef struct fs_gbt_params {
+  int32_t trees;             /* default 50 */
+  int32_t depth;             /* default 3 */
+  double learning_rate;      /* default 0.1 */
+  int32_t min_samples_split; /* default 2 */
+} fs_gbt_params;
+
+const char* fs_last_error(void);
+const char* fs_version(void);
+
+/* ---- device ------------------------------------------------------------------------------ */
+int fs_device_create(int ordinal, fs_device** out);
+int fs_device_destroy(fs_device* dev);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream. */
+int fs_device_set_stream(fs_device* dev, void* cuda_stream);
+void* fs_device_stream(fs_device* dev);
+/* Synchronize the stream and report deferred kernel-side errors. */
+int fs_device_check(fs_device* dev);
+/* Kernels launched by this device since creation (evidence counter for bench.py). */
+int64_t fs_device_launches(const fs_device* dev);
+
+/* ---- knob spaces + featurize (searchspace.cpp:90-118, feature_dim :86-88) -------------------
+ * n_knobs[s] in [1,16]; n_values[s*16+k] = |values| of knob k; values concatenated space by
+ * space, knob by knob. log2 tables are computed once on the host with the C library's log2, the
+ * function the reference calls, so features are bit-identical. */
+int fs_feature_dim(int32_t knob_count);
+int fs_spaces_create(fs_device* dev, int32_t n_spaces, const int32_t* n_knobs,
+                     const int32_t* n_values, const int64_t* values, fs_spaces** out);
+int fs_spaces_destroy(fs_spaces* sp);
+int32_t fs_spaces_max_feature_dim(const fs_spaces* sp); /* max_feature_dim (graph.cpp:346-352) */
+
+/* out[i*pad_dim + j] = featurize(space[space_of[i]], assign[i*16 .. +K], pad_dim)[j].
+ * FS_EINVAL when pad_dim < feature_dim(K) of any referenced space or an index is out of range. */
+int fs_featurize(fs_device* dev, const fs_spaces* sp, int64_t n, const int32_t* space_of,
+                 const int32_t* assign, int32_t pad_dim, double* out);
+int fs_featurize_d(fs_device* dev, const fs_spaces* sp, int64_t n, const int32_t* space_of_d,
+                   const int32_t* assign_d, int32_t pad_dim, double* out_d);
+
+/* ---- forests (CostModelState trees, costmodel.hpp:48-57) -------------------------------------
+ * A forest holds F family ensembles. fs_forest_upload replaces family f's ensemble with
+ * host-built trees (the tests' hand-built models, or a CostModelState the caller owns). */
+int fs_forest_create(fs_device* dev, int32_t n_families, fs_forest** out);
+int fs_forest_destroy(fs_forest* fo);
+int fs_forest_upload(fs_forest* fo, int32_t family, double base, double learning_rate,
+                     int32_t n_trees, const int32_t* offsets, const int32_t* feature,
+                     const double* threshold, const int32_t* left, const int32_t* right,
+                     const double* value);
+/* Two-call export: pass NULL arrays to learn n_trees / n_nodes, then fill. gain (per node, 0
+ * for leaves) and mse (train_mse_by_round) are only produced by fs_fit; may be NULL. */
+int fs_forest_export(const fs_forest* fo, int32_t family, double* base, int32_t* n_trees,
+                     int32_t* n_nodes, int32_t* offsets, int32_t* feature, double* threshold,
+                     int32_t* left, int32_t* right, double* value, double* gain, double* mse);
+
+/* ---- predict (costmodel.cpp:135-143, 237-246) ------------------------------------------------
+ * Rows [seg[f], seg[f+1]) are scored with family f's ensemble: score = base, then for every tree
+ * in order score = score + lr*leaf (separately rounded, no FMA). leaf_ids (optional, uint8
+ * [rows][n_trees_of_family], pre-order node index) is written row-major per segment at
+ * leaf_offset[f] (bytes). Non-finite features -> FS_EINVAL. */
+int fs_predict(fs_device* dev, const fs_forest* fo, int32_t n_segments, const int64_t* seg,
+               int32_t d, const double* x, double* scores, uint8_t* leaf_ids);
+int fs_predict_d(fs_device* dev, const fs_forest* fo, int32_t n_segments, const int64_t* seg_h,
+                 int32_t d, const double* x_d, double* scores_d, uint8_t* leaf_ids_d);
+
+/* ---- rank (scheduler.cpp:187-192) ------------------------------------------------------------
+ * perm[seg[f] + i] = segment-local index of the i-th smallest (score, index) pair: the order
+ * std::sort gives vector<pair<double,size_t>>. -0.0 and +0.0 compare equal. */
+int fs_rank(fs_device* dev, int32_t n_segments, const int64_t* seg, const double* scores,
+            int32_t* perm);
+int fs_rank_d(fs_device* dev, int32_t n_segments, const int64_t* seg_h, const double* scores_d,
+              int32_t* perm_d);
+
+/* ---- fit (costmodel.cpp:152-222; train_cost_model :224-235 appends log-latency rows first) ---
+ * Refit family f's ensemble from scratch on rows [seg[f], seg[f+1]) of x/target with params[f].
+ * Trees are bit-identical to the reference's (canonical row order, reference-order sums for every
+ * value that reaches a tree, exact tie resolution). gains: the reference's split gain per
+ * internal node. Non-finite features -> FS_EINVAL. */
+int fs_fit(fs_device* dev, fs_forest* fo, int32_t n_segments, const int64_t* seg, int32_t d,
+           const double* x, const double* target, const fs_gbt_params* params);
+int fs_fit_d(fs_device* dev, fs_forest* fo, int32_t n_segments, const int64_t* seg_h, int32_t d,
+             const double* x_d, const double* target_d, const fs_gbt_params* params);
+
+/* Fit diagnostics of the last fs_fit on this forest family: internal nodes resolved by the
+ * histogram screen alone / by exact reference-order re-evaluation of the tie window. */
+int fs_forest_fit_stats(const fs_forest* fo, int32_t family, int64_t* screened,
+                        int64_t* exact_resolved);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAMSEER_H */

@@ -1,0 +1,303 @@
+"""paper_2201_00194_b200 - B200-native FamilySeer cost-model hot path.
+
+Python face of libfamseer.so (C ABI in include/famseer.h) used by the tests and bench.py. The
+product API mirrors the reference's cost-model interface (famtune, /root/reference/proj/core):
+
+  featurize           searchspace.cpp:90-118      Device.featurize / Spaces
+  predict             costmodel.cpp:237-246       Forest.predict
+  tune_step ranking   scheduler.cpp:187-192       Device.rank
+  fit / train         costmodel.cpp:152-235       Forest.fit / Forest.train
+  family grouping     family.cpp:22-140           paper_2201_00194_b200.families
+
+Everything runs on the GPU through the C ABI; there is no CPU fallback. Host numpy arrays go
+through the host-pointer entry points (copies inside the call); torch CUDA tensors go through the
+``_d`` entry points on the device's stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from ._capi import FS_MAX_KNOBS, GbtParams
+
+__all__ = ["Device", "Spaces", "Forest", "Ensemble", "GbtParams", "FamseerError", "InvalidArgument",
+           "DomainError", "OutOfRange", "feature_dim", "FS_MAX_KNOBS"]
+
+
+class FamseerError(RuntimeError):
+    pass
+
+
+class InvalidArgument(FamseerError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DomainError(FamseerError, ArithmeticError):
+    """std::domain_error in the reference."""
+
+
+class OutOfRange(FamseerError, IndexError):
+    """std::out_of_range in the reference."""
+
+
+_EXC = {_capi.FS_EINVAL: InvalidArgument, _capi.FS_EDOMAIN: DomainError, _capi.FS_ERANGE: OutOfRange}
+
+
+def _lib():
+    return _capi.load()
+
+
+def _check(rc: int):
+    if rc != _capi.FS_OK:
+        msg = _lib().fs_last_error().decode()
+        raise _EXC.get(rc, FamseerError)(msg)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _seg(seg):
+    s = np.ascontiguousarray(seg, np.int64)
+    return s, s.ctypes.data_as(_capi._i64p)
+
+
+def feature_dim(k: int) -> int:
+    """searchspace.cpp:86-88."""
+    return int(_lib().fs_feature_dim(k))
+
+
+@dataclass
+class Ensemble:
+    """One family's ensemble in the CostModelState pre-order layout (costmodel.hpp:27-57)."""
+
+    base: float
+    lr: float
+    offsets: np.ndarray
+    feature: np.ndarray
+    threshold: np.ndarray
+    left: np.ndarray
+    right: np.ndarray
+    value: np.ndarray
+    gain: np.ndarray | None = None
+    mse: np.ndarray | None = None
+
+    @property
+    def n_trees(self) -> int:
+        return len(self.offsets) - 1
+
+
+class Device:
+    """fs_device: one per GPU (stream, scratch, deferred errors)."""
+
+    def __init__(self, ordinal: int = 0):
+        h = _capi._vp()
+        _check(_lib().fs_device_create(ordinal, C.byref(h)))
+        self.h = h
+        self.ordinal = ordinal
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().fs_device_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(_lib().fs_device_set_stream(self.h, stream_ptr))
+
+    @property
+    def stream(self) -> int:
+        return _lib().fs_device_stream(self.h) or 0
+
+    def check(self):
+        _check(_lib().fs_device_check(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(_lib().fs_device_launches(self.h))
+
+    # -- ranking (scheduler.cpp:187-192) --------------------------------------------------------
+    def rank(self, scores, seg=None):
+        s = np.ascontiguousarray(scores, np.float64)
+        if seg is None:
+            seg = [0, len(s)]
+        sg, sp = _seg(seg)
+        perm = np.zeros(len(s), np.int32)
+        _check(_lib().fs_rank(self.h, len(sg) - 1, sp, _p(s, _capi._dp), _p(perm, _capi._i32p)))
+        return perm
+
+    def rank_d(self, scores_t, seg, perm_t):
+        sg, sp = _seg(seg)
+        _check(_lib().fs_rank_d(self.h, len(sg) - 1, sp, scores_t.data_ptr(), perm_t.data_ptr()))
+
+
+class Spaces:
+    """fs_spaces: knob-space table; featurize (searchspace.cpp:90-118) over a population."""
+
+    def __init__(self, dev: Device, spaces):
+        """spaces: list (one per space) of lists of knob value lists."""
+        self.dev = dev
+        self.k = [len(s) for s in spaces]
+        nk = np.array(self.k, np.int32)
+        nv = np.zeros((len(spaces), FS_MAX_KNOBS), np.int32)
+        vals = []
+        for i, s in enumerate(spaces):
+            for j, v in enumerate(s):
+                nv[i, j] = len(v)
+                vals.extend(int(a) for a in v)
+        va = np.array(vals if vals else [1], np.int64)
+        h = _capi._vp()
+        _check(_lib().fs_spaces_create(dev.h, len(spaces), _p(nk, _capi._i32p), _p(nv, _capi._i32p),
+                                       _p(va, _capi._i64p), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().fs_spaces_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def max_feature_dim(self) -> int:
+        return int(_lib().fs_spaces_max_feature_dim(self.h))
+
+    def featurize(self, space_of, assign, pad_dim: int):
+        so = np.ascontiguousarray(space_of, np.int32)
+        a = np.zeros((len(so), FS_MAX_KNOBS), np.int32)
+        src = np.asarray(assign, np.int32)
+        if src.ndim == 1:
+            src = src[None]
+        a[:, : src.shape[1]] = src
+        out = np.zeros((len(so), pad_dim))
+        _check(_lib().fs_featurize(self.dev.h, self.h, len(so), _p(so, _capi._i32p), _p(a, _capi._i32p), pad_dim,
+                                   _p(out, _capi._dp)))
+        return out
+
+    def featurize_d(self, space_of_t, assign_t, pad_dim: int, out_t):
+        _check(_lib().fs_featurize_d(self.dev.h, self.h, space_of_t.numel(), space_of_t.data_ptr(),
+                                     assign_t.data_ptr(), pad_dim, out_t.data_ptr()))
+
+
+class Forest:
+    """fs_forest: one ensemble per family (TuningEngine::models_, scheduler.cpp:123-130)."""
+
+    def __init__(self, dev: Device, n_families: int):
+        self.dev = dev
+        self.n = n_families
+        h = _capi._vp()
+        _check(_lib().fs_forest_create(dev.h, n_families, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().fs_forest_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, family: int, ens):
+        off = np.ascontiguousarray(ens.offsets, np.int32)
+        feat = np.ascontiguousarray(ens.feature, np.int32)
+        thr = np.ascontiguousarray(ens.threshold, np.float64)
+        le = np.ascontiguousarray(ens.left, np.int32)
+        ri = np.ascontiguousarray(ens.right, np.int32)
+        va = np.ascontiguousarray(ens.value, np.float64)
+        _check(_lib().fs_forest_upload(self.h, family, float(ens.base), float(ens.lr), len(off) - 1,
+                                       _p(off, _capi._i32p), _p(feat, _capi._i32p), _p(thr, _capi._dp),
+                                       _p(le, _capi._i32p), _p(ri, _capi._i32p), _p(va, _capi._dp)))
+
+    def export(self, family: int, lr: float = 0.1) -> Ensemble:
+        L = _lib()
+        base = C.c_double()
+        nt, nn = C.c_int32(), C.c_int32()
+        _check(L.fs_forest_export(self.h, family, C.byref(base), C.byref(nt), C.byref(nn), *([None] * 9)))
+        t, n = nt.value, nn.value
+        off = np.zeros(t + 1, np.int32)
+        feat = np.zeros(n, np.int32)
+        thr = np.zeros(n)
+        le = np.zeros(n, np.int32)
+        ri = np.zeros(n, np.int32)
+        va = np.zeros(n)
+        gain = np.zeros(n)
+        mse = np.zeros(max(t, 1))
+        _check(L.fs_forest_export(self.h, family, C.byref(base), None, None, _p(off, _capi._i32p),
+                                  _p(feat, _capi._i32p), _p(thr, _capi._dp), _p(le, _capi._i32p),
+                                  _p(ri, _capi._i32p), _p(va, _capi._dp), _p(gain, _capi._dp), _p(mse, _capi._dp)))
+        return Ensemble(base.value, lr, off, feat, thr, le, ri, va, gain, mse[:t])
+
+    def predict(self, x, seg=None, leaves: bool = False):
+        x = np.ascontiguousarray(x, np.float64)
+        if x.ndim == 1:
+            x = x[None]
+        if seg is None:
+            seg = [0, x.shape[0]]
+        sg, sp = _seg(seg)
+        out = np.zeros(x.shape[0])
+        lo = None
+        if leaves:
+            total = 0
+            for f in range(len(sg) - 1):
+                total += int(sg[f + 1] - sg[f]) * self.export_n_trees(f)
+            lo = np.zeros(max(total, 1), np.uint8)
+        _check(_lib().fs_predict(self.dev.h, self.h, len(sg) - 1, sp, x.shape[1], _p(x, _capi._dp),
+                                 _p(out, _capi._dp), _p(lo, _capi._u8p)))
+        return (out, lo) if leaves else out
+
+    def predict_d(self, x_t, seg, scores_t, leaves_t=None):
+        sg, sp = _seg(seg)
+        _check(_lib().fs_predict_d(self.dev.h, self.h, len(sg) - 1, sp, x_t.shape[1], x_t.data_ptr(),
+                                   scores_t.data_ptr(), None if leaves_t is None else leaves_t.data_ptr()))
+
+    def export_n_trees(self, family: int) -> int:
+        nt = C.c_int32()
+        _check(_lib().fs_forest_export(self.h, family, None, C.byref(nt), *([None] * 10)))
+        return nt.value
+
+    def fit(self, x, target, seg=None, params=None):
+        """Refit each family segment from scratch (costmodel.cpp:152-222)."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(target, np.float64)
+        if seg is None:
+            seg = [0, x.shape[0]]
+        sg, sp = _seg(seg)
+        nf = len(sg) - 1
+        pa = _params_array(params, nf)
+        d = x.shape[1] if x.ndim == 2 else 0
+        _check(_lib().fs_fit(self.dev.h, self.h, nf, sp, d, _p(x, _capi._dp), _p(y, _capi._dp), pa))
+
+    def fit_d(self, x_t, target_t, seg, params=None):
+        sg, sp = _seg(seg)
+        nf = len(sg) - 1
+        pa = _params_array(params, nf)
+        _check(_lib().fs_fit_d(self.dev.h, self.h, nf, sp, x_t.shape[1], x_t.data_ptr(), target_t.data_ptr(), pa))
+
+    def fit_stats(self, family: int):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib().fs_forest_fit_stats(self.h, family, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+def _params_array(params, n):
+    if params is None:
+        params = GbtParams(50, 3, 0.1, 2)
+    if isinstance(params, GbtParams):
+        params = [params] * n
+    arr = (GbtParams * n)(*params)
+    return arr

@@ -1,0 +1,78 @@
+"""ctypes binding of libfamseer.so (include/famseer.h).
+
+The library is built in-tree (``paper_2201_00194_b200/libfamseer.so``). There is no fallback:
+if the shared object is missing or no B200 is visible, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfamseer.so")
+
+FS_OK, FS_EINVAL, FS_EDOMAIN, FS_ERANGE, FS_ECUDA, FS_ENOMEM, FS_ENCCL = range(7)
+FS_MAX_KNOBS = 16
+
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_u8p = C.POINTER(C.c_uint8)
+_vp = C.c_void_p
+
+
+class GbtParams(C.Structure):
+    """fs_gbt_params == famtune::GbtParams (costmodel.hpp:20-25)."""
+
+    _fields_ = [("trees", C.c_int32), ("depth", C.c_int32), ("learning_rate", C.c_double),
+                ("min_samples_split", C.c_int32)]
+
+
+# (name, restype, argtypes) for every symbol include/famseer.h declares.
+SIGNATURES = [
+    ("fs_last_error", C.c_char_p, []),
+    ("fs_version", C.c_char_p, []),
+    ("fs_device_create", C.c_int, [C.c_int, C.POINTER(_vp)]),
+    ("fs_device_destroy", C.c_int, [_vp]),
+    ("fs_device_set_stream", C.c_int, [_vp, _vp]),
+    ("fs_device_stream", _vp, [_vp]),
+    ("fs_device_check", C.c_int, [_vp]),
+    ("fs_device_launches", C.c_int64, [_vp]),
+    ("fs_feature_dim", C.c_int, [C.c_int32]),
+    ("fs_spaces_create", C.c_int, [_vp, C.c_int32, _i32p, _i32p, _i64p, C.POINTER(_vp)]),
+    ("fs_spaces_destroy", C.c_int, [_vp]),
+    ("fs_spaces_max_feature_dim", C.c_int32, [_vp]),
+    ("fs_featurize", C.c_int, [_vp, _vp, C.c_int64, _i32p, _i32p, C.c_int32, _dp]),
+    ("fs_featurize_d", C.c_int, [_vp, _vp, C.c_int64, _vp, _vp, C.c_int32, _vp]),
+    ("fs_forest_create", C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
+    ("fs_forest_destroy", C.c_int, [_vp]),
+    ("fs_forest_upload", C.c_int, [_vp, C.c_int32, C.c_double, C.c_double, C.c_int32, _i32p, _i32p, _dp, _i32p,
+                                   _i32p, _dp]),
+    ("fs_forest_export", C.c_int, [_vp, C.c_int32, _dp, _i32p, _i32p, _i32p, _i32p, _dp, _i32p, _i32p, _dp, _dp,
+                                   _dp]),
+    ("fs_predict", C.c_int, [_vp, _vp, C.c_int32, _i64p, C.c_int32, _dp, _dp, _u8p]),
+    ("fs_predict_d", C.c_int, [_vp, _vp, C.c_int32, _i64p, C.c_int32, _vp, _vp, _vp]),
+    ("fs_rank", C.c_int, [_vp, C.c_int32, _i64p, _dp, _i32p]),
+    ("fs_rank_d", C.c_int, [_vp, C.c_int32, _i64p, _vp, _vp]),
+    ("fs_fit", C.c_int, [_vp, _vp, C.c_int32, _i64p, C.c_int32, _dp, _dp, C.POINTER(GbtParams)]),
+    ("fs_fit_d", C.c_int, [_vp, _vp, C.c_int32, _i64p, C.c_int32, _vp, _vp, C.POINTER(GbtParams)]),
+    ("fs_forest_fit_stats", C.c_int, [_vp, C.c_int32, _i64p, _i64p]),
+]
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libfamseer.so and attach signatures. Raises if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing - run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

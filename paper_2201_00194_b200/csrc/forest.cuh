@@ -1,0 +1,63 @@
+// Family model store: one ensemble per family (TuningEngine::models_, scheduler.cpp:123-130),
+// kept in two forms.
+//   * pre-order host arrays - the CostModelState layout (costmodel.hpp:27-57), authoritative and
+//     exported unchanged so callers' CostModelState stays the source of truth;
+//   * a compiled device form for predict: every tree expanded to a complete heap of depth
+//     `depth` (early leaves replicated under always-left nodes), node = feature | rank<<16 where
+//     rank is the threshold's index among the sorted unique thresholds the ensemble uses for that
+//     feature. A row's feature value x becomes code(x) = #{unique thresholds < x}, and
+//     x <= t_rank  <=>  code(x) <= rank  exactly (SURVEY.md "Bit-exactness rules" 2), so the
+//     traversal compares small integers instead of FP64 values.
+#pragma once
+
+#include <vector>
+
+#include "fs_common.cuh"
+
+namespace fs {
+
+constexpr int kMaxHeapDepth = 8;  // deeper ensembles take the generic pre-order kernel
+
+struct FamilyModel {
+  // ---- pre-order form (host) ----
+  double base = 0.0;
+  double lr = 0.1;
+  std::vector<int32_t> offsets{0};
+  std::vector<int32_t> feature, left, right;
+  std::vector<double> threshold, value, gain, mse;
+  int64_t screened = 0, exact = 0;  // fit diagnostics
+
+  // ---- compiled form (device) ----
+  bool compiled = false;
+  int n_trees = 0;
+  int depth = 0;       // heap depth (max leaf depth over trees)
+  int d_model = 0;     // 1 + max feature index referenced
+  int code_bytes = 1;  // 1: codes fit uint8, 2: uint16
+  bool generic = false;  // depth > kMaxHeapDepth: pre-order device arrays instead of heaps
+  uint32_t* nodes_d = nullptr;   // [T][2^depth - 1]
+  double* leafv_d = nullptr;     // [T][2^depth]
+  uint8_t* leafid_d = nullptr;   // [T][2^depth]
+  double* uthr_d = nullptr;      // unique thresholds, feature-major
+  int32_t* uoff_d = nullptr;     // [d_model + 1]
+  // generic form
+  int32_t* g_off_d = nullptr;
+  int32_t* g_feat_d = nullptr;
+  double* g_thr_d = nullptr;
+  int32_t* g_left_d = nullptr;
+  int32_t* g_right_d = nullptr;
+  double* g_val_d = nullptr;
+
+  int num_trees() const { return static_cast<int>(offsets.size()) - 1; }
+  void release_device();
+};
+
+// Build the compiled device form from the pre-order arrays (host transformation of the tree
+// table; O(nodes)).
+void compile_model(fs_device* dev, FamilyModel& m);
+
+}  // namespace fs
+
+struct fs_forest {
+  fs_device* dev = nullptr;
+  std::vector<fs::FamilyModel> fams;
+};

@@ -1,0 +1,115 @@
+// Internal plumbing shared by the libfamseer translation units: error mapping, the device
+// context (stream, stream-ordered scratch, deferred-error word, launch counter) and the FP64
+// helpers that keep every reference sum separately rounded (no FMA contraction).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "famseer.h"
+
+namespace fs {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) fail(FS_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(FS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define FS_CUDA(x) ::fs::cuda_check((x), #x)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return FS_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return FS_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return FS_ECUDA;
+  }
+}
+
+// Deferred kernel-side error bits (reported by fs_device_check / the host-pointer entry points).
+enum ErrBits : uint32_t {
+  kErrNonFinitePredict = 1u << 0,  // costmodel.cpp:238-240
+  kErrNonFiniteFit = 1u << 1,      // costmodel.cpp:178-182
+  kErrKnobRange = 1u << 2,         // assignment index outside the knob's value list
+  kErrPadDim = 1u << 3,            // searchspace.cpp:96-100
+  kErrSpaceId = 1u << 4,           // candidate names an unknown space
+  kErrInternal = 1u << 5,          // trainer invariant violated (must never fire)
+};
+
+// Grows-only stream-ordered device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace fs
+
+struct fs_device {
+  int ordinal = 0;
+  int sm_count = 148;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  uint32_t* err_d = nullptr;     // device error word
+  uint32_t* err_h = nullptr;     // pinned mirror
+  int64_t launches = 0;
+  std::vector<fs::DevBuf> slots;  // scratch, indexed by purpose
+
+  void* scratch(int slot, size_t bytes);  // stream-ordered grow; contents undefined
+  void count_launch(int n = 1) { launches += n; }
+  void activate() const;                  // cudaSetDevice(ordinal)
+  uint32_t take_errors();                 // sync + read and clear the error word
+};
+
+namespace fs {
+
+// Scratch slot ids (each purpose owns one growable buffer).
+enum Slot : int {
+  kSlotH2D0 = 0,
+  kSlotH2D1,
+  kSlotH2D2,
+  kSlotD2H0,
+  kSlotD2H1,
+  kSlotRankKeys,
+  kSlotRankKeys2,
+  kSlotRankIdx2,
+  kSlotPredictSeg,
+  kSlotCount
+};
+
+// Throws FS_EINVAL with the reference's message for the deferred bits that are set.
+void raise_deferred(uint32_t bits);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace fs
+
+// FP64 arithmetic in the reference's rounding order. The library is also compiled with
+// -fmad=false, but the hot sums spell the rounding out so no compiler flag can change them.
+__device__ __forceinline__ double fs_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double fs_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double fs_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fs_div(double a, double b) { return __ddiv_rn(a, b); }

@@ -1,0 +1,220 @@
+// Kernel (2): GBDT ensemble predict - predict (costmodel.cpp:237-246) with RegressionTree::eval
+// (:135-143) for a whole candidate population, one launch per family segment.
+//
+// CTA = a tile of 256 candidates, one per thread.
+//   1. Stage: warps stream the tile's FP64 rows from HBM with coalesced loads (lanes over
+//      features), check finiteness (the reference throws on any non-finite feature) and convert
+//      each value the ensemble actually tests into its threshold code (binary search in the
+//      feature's sorted unique thresholds). Codes land in shared memory transposed
+//      [feature][candidate] so a warp reading one feature hits consecutive bytes.
+//   2. Trees are staged through shared memory in chunks; each thread walks its candidate down
+//      every tree of the chunk (fixed-depth heap, no divergence in trip count) and folds
+//      score = score + lr*leaf in tree order with separately rounded __dmul_rn/__dadd_rn - the
+//      reference's `score += learning_rate * tree.eval(x)` without FMA.
+// HBM traffic per candidate = 8*d (row) + 8 (score) [+ T leaf ids]; the model is read once per
+// CTA from L2.
+#include <algorithm>
+
+#include "forest.cuh"
+
+namespace {
+
+constexpr int kTile = 256;
+constexpr int kChunk = 64;
+
+template <typename CodeT, bool kLeaves>
+__global__ void __launch_bounds__(kTile) predict_heap_kernel(
+    const double* __restrict__ x, int64_t rows, int d, int d_model, int depth, int n_trees, double base,
+    double lr, const uint32_t* __restrict__ nodes, const double* __restrict__ leafv,
+    const uint8_t* __restrict__ leafid, const double* __restrict__ uthr, const int32_t* __restrict__ uoff,
+    double* __restrict__ scores, uint8_t* __restrict__ leaf_out, uint32_t* err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nint = (1 << depth) - 1;
+  const int nleaf = 1 << depth;
+  CodeT* codes = reinterpret_cast<CodeT*>(smem);  // [d_model][kTile]
+  size_t off = (static_cast<size_t>(d_model) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
+  double* s_leafv = reinterpret_cast<double*>(smem + off);  // [kChunk][nleaf]
+  off += static_cast<size_t>(kChunk) * nleaf * sizeof(double);
+  uint32_t* s_nodes = reinterpret_cast<uint32_t*>(smem + off);  // [kChunk][nint]
+  off += static_cast<size_t>(kChunk) * nint * sizeof(uint32_t);
+  uint8_t* s_leafid = smem + off;  // [kChunk][nleaf]
+  off += static_cast<size_t>(kChunk) * nleaf;
+  uint8_t* s_lbuf = smem + off;  // [kTile][kChunk]
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kTile;
+  const int tile_rows = static_cast<int>(rows - row0 < kTile ? rows - row0 : kTile);
+
+  bool nonfinite = false;
+  for (int c = warp; c < tile_rows; c += kTile / 32) {
+    const double* xr = x + (row0 + c) * d;
+    for (int f = lane; f < d; f += 32) {
+      const double v = __ldcs(xr + f);  // streamed once
+      nonfinite |= !isfinite(v);
+      if (f < d_model) {
+        int lo = __ldg(uoff + f), hi = __ldg(uoff + f + 1);
+        const int first = lo;
+        while (lo < hi) {  // count of unique thresholds strictly below v
+          const int mid = (lo + hi) >> 1;
+          if (__ldg(uthr + mid) < v) lo = mid + 1;
+          else hi = mid;
+        }
+        codes[f * kTile + c] = static_cast<CodeT>(lo - first);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, fs::kErrNonFinitePredict);
+
+  double score = base;
+  const bool active = tid < tile_rows;
+  for (int t0 = 0; t0 < n_trees; t0 += kChunk) {
+    const int ch = min(kChunk, n_trees - t0);
+    __syncthreads();  // codes ready / previous chunk consumed
+    for (int i = tid; i < ch * nint; i += kTile) s_nodes[i] = __ldg(nodes + static_cast<size_t>(t0) * nint + i);
+    for (int i = tid; i < ch * nleaf; i += kTile) {
+      s_leafv[i] = __ldg(leafv + static_cast<size_t>(t0) * nleaf + i);
+      s_leafid[i] = __ldg(leafid + static_cast<size_t>(t0) * nleaf + i);
+    }
+    __syncthreads();
+    if (active) {
+      for (int t = 0; t < ch; ++t) {
+        const uint32_t* tn = s_nodes + t * nint;
+        int idx = 0;
+        for (int lv = 0; lv < depth; ++lv) {
+          const uint32_t nd = tn[idx];
+          const uint32_t cv = codes[(nd & 0xFFFFu) * kTile + tid];
+          idx = 2 * idx + 1 + (cv > (nd >> 16) ? 1 : 0);
+        }
+        const int slot = idx - nint;
+        score = fs_add(score, fs_mul(lr, s_leafv[t * nleaf + slot]));
+        if (kLeaves) s_lbuf[tid * kChunk + t] = s_leafid[t * nleaf + slot];
+      }
+    }
+    if (kLeaves) {
+      __syncthreads();
+      for (int i = tid; i < tile_rows * ch; i += kTile) {
+        const int c = i / ch, t = i - c * ch;
+        leaf_out[(row0 + c) * n_trees + t0 + t] = s_lbuf[c * kChunk + t];
+      }
+    }
+  }
+  if (active) scores[row0 + tid] = score;
+}
+
+// Trees deeper than kMaxHeapDepth: walk the pre-order arrays directly (rare; hand-built models).
+__global__ void predict_generic_kernel(const double* __restrict__ x, int64_t rows, int d, int n_trees, double base,
+                                       double lr, const int32_t* __restrict__ off, const int32_t* __restrict__ feat,
+                                       const double* __restrict__ thr, const int32_t* __restrict__ left,
+                                       const int32_t* __restrict__ right, const double* __restrict__ val,
+                                       double* __restrict__ scores, uint8_t* __restrict__ leaf_out, uint32_t* err) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const double* xr = x + r * d;
+  bool nonfinite = false;
+  for (int f = 0; f < d; ++f) nonfinite |= !isfinite(xr[f]);
+  if (nonfinite) atomicOr(err, fs::kErrNonFinitePredict);
+  double score = base;
+  for (int t = 0; t < n_trees; ++t) {
+    const int o = off[t];
+    int idx = 0;
+    while (feat[o + idx] >= 0) idx = xr[feat[o + idx]] <= thr[o + idx] ? left[o + idx] : right[o + idx];
+    score = fs_add(score, fs_mul(lr, val[o + idx]));
+    if (leaf_out) leaf_out[r * n_trees + t] = static_cast<uint8_t>(idx);
+  }
+  scores[r] = score;
+}
+
+template <typename CodeT, bool kLeaves>
+void launch_heap(fs_device* dev, const fs::FamilyModel& m, const double* x, int64_t rows, int d, double* scores,
+                 uint8_t* leaf_out) {
+  const int nint = (1 << m.depth) - 1, nleaf = 1 << m.depth;
+  size_t smem = (static_cast<size_t>(m.d_model) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
+  smem += static_cast<size_t>(kChunk) * (nleaf * sizeof(double) + nint * sizeof(uint32_t) + nleaf);
+  if (kLeaves) smem += static_cast<size_t>(kTile) * kChunk;
+  auto* fn = predict_heap_kernel<CodeT, kLeaves>;
+  if (smem > 227 * 1024) fs::fail(FS_EINVAL, "predict: model too wide for the shared-memory tile");
+  FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int grid = static_cast<int>(fs::ceil_div(rows, kTile));
+  fn<<<grid, kTile, smem, dev->stream>>>(x, rows, d, std::min(m.d_model, d), m.depth, m.n_trees, m.base, m.lr,
+                                         m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, scores, leaf_out,
+                                         dev->err_d);
+  dev->count_launch();
+  FS_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+namespace fs {
+
+// Scores rows [seg[f], seg[f+1]) with family f. Leaf ids of segment f start at byte
+// sum_{g<f} rows_g * T_g of leaf_out.
+void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
+                    const double* x, double* scores, uint8_t* leaf_out) {
+  int64_t leaf_off = 0;
+  for (int f = 0; f < nseg; ++f) {
+    const int64_t r0 = seg[f], rows = seg[f + 1] - seg[f];
+    if (f >= static_cast<int32_t>(fo->fams.size())) fail(FS_ERANGE, "predict: segment names an unknown family");
+    const auto& m = fo->fams[static_cast<size_t>(f)];
+    if (!m.compiled) fail(FS_EINVAL, "predict: family " + std::to_string(f) + " has no compiled model");
+    if (m.d_model > d) fail(FS_EINVAL, "predict: model references feature beyond the row width");
+    if (rows <= 0) continue;
+    uint8_t* lo = leaf_out ? leaf_out + leaf_off : nullptr;
+    leaf_off += rows * m.n_trees;
+    if (m.generic) {
+      predict_generic_kernel<<<static_cast<int>(ceil_div(rows, 128)), 128, 0, dev->stream>>>(
+          x + r0 * d, rows, d, m.n_trees, m.base, m.lr, m.g_off_d, m.g_feat_d, m.g_thr_d, m.g_left_d, m.g_right_d,
+          m.g_val_d, scores + r0, lo, dev->err_d);
+      dev->count_launch();
+      FS_CUDA(cudaGetLastError());
+    } else if (m.code_bytes == 1) {
+      if (lo) launch_heap<uint8_t, true>(dev, m, x + r0 * d, rows, d, scores + r0, lo);
+      else launch_heap<uint8_t, false>(dev, m, x + r0 * d, rows, d, scores + r0, nullptr);
+    } else {
+      if (lo) launch_heap<uint16_t, true>(dev, m, x + r0 * d, rows, d, scores + r0, lo);
+      else launch_heap<uint16_t, false>(dev, m, x + r0 * d, rows, d, scores + r0, nullptr);
+    }
+  }
+}
+
+int64_t leaf_bytes(const fs_forest* fo, int32_t nseg, const int64_t* seg) {
+  int64_t b = 0;
+  for (int f = 0; f < nseg && f < static_cast<int32_t>(fo->fams.size()); ++f)
+    b += (seg[f + 1] - seg[f]) * fo->fams[static_cast<size_t>(f)].n_trees;
+  return b;
+}
+
+}  // namespace fs
+
+extern "C" {
+
+int fs_predict_d(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d, const double* x_d,
+                 double* scores_d, uint8_t* leaf_d) {
+  return fs::guard([&] {
+    if (!dev || !fo || nseg < 0 || !seg || d < 0) fs::fail(FS_EINVAL, "fs_predict: bad arguments");
+    dev->activate();
+    fs::launch_predict(dev, fo, nseg, seg, d, x_d, scores_d, leaf_d);
+  });
+}
+
+int fs_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d, const double* x,
+               double* scores, uint8_t* leaf_ids) {
+  return fs::guard([&] {
+    if (!dev || !fo || nseg < 0 || !seg || d < 0) fs::fail(FS_EINVAL, "fs_predict: bad arguments");
+    dev->activate();
+    const int64_t n = seg[nseg] - seg[0];
+    if (n <= 0) return;
+    if (seg[0] != 0) fs::fail(FS_EINVAL, "fs_predict: seg[0] must be 0");
+    auto* xd = static_cast<double*>(dev->scratch(fs::kSlotH2D0, n * d * sizeof(double)));
+    auto* sd = static_cast<double*>(dev->scratch(fs::kSlotD2H0, n * sizeof(double)));
+    const int64_t lb = leaf_ids ? fs::leaf_bytes(fo, nseg, seg) : 0;
+    auto* ld = leaf_ids ? static_cast<uint8_t*>(dev->scratch(fs::kSlotD2H1, std::max<int64_t>(lb, 1))) : nullptr;
+    FS_CUDA(cudaMemcpyAsync(xd, x, n * d * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    fs::launch_predict(dev, fo, nseg, seg, d, xd, sd, ld);
+    FS_CUDA(cudaMemcpyAsync(scores, sd, n * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
+    if (leaf_ids && lb) FS_CUDA(cudaMemcpyAsync(leaf_ids, ld, lb, cudaMemcpyDeviceToHost, dev->stream));
+    fs::raise_deferred(dev->take_errors());
+  });
+}
+
+}  // extern "C"
