@@ -1,16 +1,1633 @@
-// Kernel (3): the boosting trainer (fit, costmodel.cpp:152-222). Under construction.
-#include "forest.cuh"
+// Kernel (3): the boosting trainer - fit (costmodel.cpp:152-222) for F families in one call.
+// Design and bit-exactness argument: fit.cuh. Phases:
+//   prep    distinct values + codes per feature, feature dedup, canonical row order
+//           (costmodel.cpp:161-173), per-feature presorts (:193-201), base (:185-188)
+//   rounds  residual -> fixed point -> per level: histograms (smaller child built, sibling by
+//           exact subtraction), screen, exact reference-order re-evaluation where needed,
+//           stable partition of the order-0 list -> leaves (reference-order totals) ->
+//           prediction update -> commit / early stop (:212) -> MSE (:215-220)
+// The host only launches; no host<->device synchronisation happens inside the boosting loop.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <vector>
+
+#include "fit.cuh"
+
+namespace fs {
+namespace fit {
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// small device helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t value_key(double v) {  // order-preserving, -0.0 == +0.0
+  uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+  if (b == 0x8000000000000000ull) b = 0;
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+__device__ __forceinline__ uint64_t lo_key(double v) {  // order-preserving key for atomicMax
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double lo_from_key(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__device__ __forceinline__ int family_of_pos(const FamDesc* fam, int F, int64_t p) {
+  int lo = 0, hi = F;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (fam[mid].pos0 <= p) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Block-level stable counting sort by an 8-bit digit (blockDim == kSortThreads).
+// out[...] = in indices ordered by (digit, position in `in`). Returns false (and writes nothing)
+// when every element has the same digit, so callers can skip the pass.
+struct SortSmem {
+  int cnt[256];
+  int tot[256];
+  int wc[32 * 256];
+  int uniform;
+};
+
+template <class In, class Digit>
+__device__ bool stable_digit_pass(In in, int32_t* __restrict__ out, int n, Digit digit, SortSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 256; i += blockDim.x) sm.cnt[i] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) atomicAdd(&sm.cnt[digit(in(i))], 1);
+  __syncthreads();
+  if (tid == 0) sm.uniform = n == 0 || sm.cnt[digit(in(0))] == n;
+  __syncthreads();
+  if (sm.uniform) return false;
+  if (warp == 0) {  // exclusive scan of 256 counts
+    int v[8], s = 0;
+    for (int k = 0; k < 8; ++k) {
+      v[k] = sm.cnt[lane * 8 + k];
+      s += v[k];
+    }
+    int incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int run = incl - s;
+    for (int k = 0; k < 8; ++k) {
+      sm.cnt[lane * 8 + k] = run;
+      run += v[k];
+    }
+  }
+  __syncthreads();
+  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+    const int i = t0 + tid;
+    const bool valid = i < n;
+    const int idx = valid ? in(i) : 0;
+    const int dg = valid ? digit(idx) : 256;
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rank == 0) sm.wc[warp * 256 + dg] = __popc(peers);
+    __syncthreads();
+    if (tid < 256) {
+      int run = 0;
+      for (int w = 0; w < 32; ++w) {
+        const int c = sm.wc[w * 256 + tid];
+        sm.wc[w * 256 + tid] = run;
+        run += c;
+      }
+      sm.tot[tid] = run;
+    }
+    __syncthreads();
+    if (valid) out[sm.cnt[dg] + sm.wc[warp * 256 + dg] + rank] = idx;
+    __syncthreads();
+    if (tid < 256) {
+      for (int w = 0; w < 32; ++w) sm.wc[w * 256 + tid] = 0;
+      sm.cnt[tid] += sm.tot[tid];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+__device__ void sort_smem_init(SortSmem& sm) {
+  for (int i = threadIdx.x; i < 32 * 256; i += blockDim.x) sm.wc[i] = 0;
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
+// prep 1: distinct values and codes per (family, feature) - hash path (<= 256 distinct)
+// ------------------------------------------------------------------------------------------
+constexpr int kHashSlots = 512;
+
+__global__ void __launch_bounds__(256) distinct_small_kernel(const double* __restrict__ x, int d,
+                                                             const FamDesc* __restrict__ fam,
+                                                             uint16_t* __restrict__ codes_all,
+                                                             double* __restrict__ vals_all,
+                                                             int32_t* __restrict__ nb_all,
+                                                             uint64_t* __restrict__ hash_all, uint32_t* err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem);                 // [32][512]
+  uint64_t* sorted = tab + 32 * kHashSlots;                          // [32][256]
+  int* cnt = reinterpret_cast<int*>(sorted + 32 * kSmallBins);       // [32]
+  int* ovf = cnt + 32;                                               // [32]
+  unsigned long long* hsh = reinterpret_cast<unsigned long long*>(ovf + 32);  // [32]
+  const FamDesc fd = fam[blockIdx.y];
+  const int j0 = blockIdx.x * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 32 * kHashSlots; i += blockDim.x) tab[i] = 0;
+  if (tid < 32) {
+    cnt[tid] = 0;
+    ovf[tid] = 0;
+    hsh[tid] = 0;
+  }
+  __syncthreads();
+  const int j = j0 + lane;
+  const bool has = j < d;
+  bool nonfinite = false;
+  if (has) {
+    uint64_t* t = tab + lane * kHashSlots;
+    for (int r = warp; r < fd.n; r += 8) {
+      const double v = x[(fd.row0 + r) * d + j];
+      if (!isfinite(v)) {
+        nonfinite = true;
+        continue;
+      }
+      if (ovf[lane]) continue;
+      const uint64_t k = value_key(v);
+      uint32_t h = static_cast<uint32_t>(mix64(k)) & (kHashSlots - 1);
+      for (int probe = 0; probe < kHashSlots; ++probe) {
+        const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(t + h), 0ull,
+                                        static_cast<unsigned long long>(k));
+        if (prev == 0) {
+          if (atomicAdd(&cnt[lane], 1) >= kSmallBins) ovf[lane] = 1;
+          break;
+        }
+        if (prev == k) break;
+        h = (h + 1) & (kHashSlots - 1);
+        if (probe == kHashSlots - 1) ovf[lane] = 1;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, kErrNonFiniteFit);
+  __syncthreads();
+  // rank every present key by counting smaller keys (<= 256 per feature)
+  for (int f = warp; f < 32; f += 8) {
+    if (j0 + f >= d || ovf[f]) continue;
+    const uint64_t* t = tab + f * kHashSlots;
+    for (int s = lane; s < kHashSlots; s += 32) {
+      const uint64_t k = t[s];
+      if (!k) continue;
+      int rank = 0;
+      for (int o = 0; o < kHashSlots; ++o) {
+        const uint64_t q = t[o];
+        rank += (q != 0 && q < k);
+      }
+      sorted[f * kSmallBins + rank] = k;
+    }
+  }
+  __syncthreads();
+  for (int f = warp; f < 32; f += 8) {
+    if (j0 + f >= d) continue;
+    const int64_t fj = static_cast<int64_t>(blockIdx.y) * d + j0 + f;
+    if (lane == 0) nb_all[fj] = ovf[f] ? -1 : cnt[f];
+    if (!ovf[f])
+      for (int i = lane; i < cnt[f]; i += 32) vals_all[fj * kSmallBins + i] = key_value(sorted[f * kSmallBins + i]);
+  }
+  // codes: binary search in the sorted distinct keys
+  if (has && !ovf[lane]) {
+    const uint64_t* sk = sorted + lane * kSmallBins;
+    const int m = cnt[lane];
+    uint64_t hacc = 0;
+    for (int r = warp; r < fd.n; r += 8) {
+      const double v = x[(fd.row0 + r) * d + j];
+      if (!isfinite(v)) continue;
+      const uint64_t k = value_key(v);
+      int lo = 0, hi = m - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sk[mid] < k) lo = mid + 1;
+        else hi = mid;
+      }
+      codes_all[(fd.row0 + r) * d + j] = static_cast<uint16_t>(lo);
+      hacc += mix64((static_cast<uint64_t>(r) << 20) ^ static_cast<uint64_t>(lo) ^ 0x9E3779B97F4A7C15ull);
+    }
+    atomicAdd(&hsh[lane], static_cast<unsigned long long>(hacc));
+  }
+  __syncthreads();
+  if (tid < 32 && j0 + tid < d && !ovf[tid]) hash_all[static_cast<int64_t>(blockIdx.y) * d + j0 + tid] = hsh[tid];
+}
+
+// prep 1b: features with > 256 distinct values - LSD sort of the column by value key, dense rank.
+struct LargeItem {
+  int32_t fam;
+  int32_t feat;
+  int64_t vals0;  // offset into vals_large
+};
+
+__global__ void __launch_bounds__(kSortThreads) distinct_large_kernel(
+    const double* __restrict__ x, int d, const FamDesc* __restrict__ fam, const LargeItem* __restrict__ items,
+    int32_t* __restrict__ bufA, int32_t* __restrict__ bufB, int64_t buf_stride, uint16_t* __restrict__ codes_all,
+    double* __restrict__ vals_large, int32_t* __restrict__ nb_all, uint64_t* __restrict__ hash_all, uint32_t* err) {
+  __shared__ SortSmem sm;
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  __shared__ unsigned long long hsh;
+  const LargeItem it = items[blockIdx.x];
+  const FamDesc fd = fam[it.fam];
+  const int n = fd.n, j = it.feat;
+  int32_t* A = bufA + blockIdx.x * buf_stride;
+  int32_t* B = bufB + blockIdx.x * buf_stride;
+  sort_smem_init(sm);
+  auto key = [&](int r) { return value_key(x[(fd.row0 + r) * d + j]); };
+  bool first = true;
+  for (int byte = 0; byte < 8; ++byte) {
+    auto dig = [&](int r) { return static_cast<int>((key(r) >> (8 * byte)) & 255u); };
+    bool moved;
+    if (first) moved = stable_digit_pass([](int i) { return i; }, B, n, dig, sm);
+    else moved = stable_digit_pass([&](int i) { return A[i]; }, B, n, dig, sm);
+    if (moved) {
+      int32_t* t = A;
+      A = B;
+      B = t;
+      first = false;
+    }
+    __syncthreads();
+  }
+  if (first) {  // already sorted (all digit passes were uniform): identity
+    for (int i = threadIdx.x; i < n; i += blockDim.x) A[i] = i;
+    __syncthreads();
+  }
+  // dense rank: code = (#distinct keys before)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    carry = 0;
+    hsh = 0;
+  }
+  __syncthreads();
+  uint64_t hacc = 0;
+  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+    const int i = t0 + tid;
+    int flag = 0;
+    uint64_t k = 0;
+    if (i < n) {
+      k = key(A[i]);
+      flag = (i == 0) || key(A[i - 1]) != k;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int in_warp = __popc(bal & ((2u << lane) - 1u));  // inclusive
+    if (lane == 31) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      const int v = wsum[lane];
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      wsum[lane] = incl - v;
+    }
+    __syncthreads();
+    if (i < n) {
+      const int code = carry + wsum[warp] + in_warp - 1;
+      if (code > kMaxBins - 1) atomicOr(err, kErrInternal);
+      const int r = A[i];
+      codes_all[(fd.row0 + r) * d + j] = static_cast<uint16_t>(code);
+      if (flag) vals_large[it.vals0 + code] = x[(fd.row0 + r) * d + j] == 0.0 ? 0.0 : x[(fd.row0 + r) * d + j];
+      hacc += mix64((static_cast<uint64_t>(r) << 20) ^ static_cast<uint64_t>(code) ^ 0x9E3779B97F4A7C15ull);
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry += wsum[warp] + in_warp;
+    __syncthreads();
+  }
+  atomicAdd(&hsh, static_cast<unsigned long long>(hacc));
+  __syncthreads();
+  if (tid == 0) {
+    nb_all[static_cast<int64_t>(it.fam) * d + j] = carry;
+    hash_all[static_cast<int64_t>(it.fam) * d + j] = hsh;
+  }
+}
+
+// prep 2: exact verification of hash-equal feature pairs (codes identical on every row?)
+struct PairItem {
+  int32_t fam, a, b, pad;
+};
+
+__global__ void verify_pairs_kernel(const uint16_t* __restrict__ codes_all, int d, const FamDesc* __restrict__ fam,
+                                    const PairItem* __restrict__ pairs, int32_t* __restrict__ mismatch) {
+  const PairItem pr = pairs[blockIdx.x];
+  const FamDesc fd = fam[pr.fam];
+  int bad = 0;
+  for (int r = threadIdx.x; r < fd.n; r += blockDim.x)
+    bad |= codes_all[(fd.row0 + r) * d + pr.a] != codes_all[(fd.row0 + r) * d + pr.b];
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) mismatch[blockIdx.x] = bad;
+}
+
+// prep 3a: per-rep value tables
+__global__ void rep_vals_kernel(const FamDesc* __restrict__ fam, const int32_t* __restrict__ rep_orig,
+                                const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
+                                const int64_t* __restrict__ rep_src, const double* __restrict__ vals_all,
+                                const double* __restrict__ vals_large, int d, double* __restrict__ vals) {
+  const FamDesc fd = fam[blockIdx.y];
+  for (int jj = blockIdx.x; jj < fd.nrep; jj += gridDim.x) {
+    const int r = fd.rep0 + jj;
+    const int64_t src = rep_src[r];
+    const int nb = rep_nb[r];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      const double v = src >= 0 ? vals_large[src + b]
+                                : vals_all[(static_cast<int64_t>(blockIdx.y) * d + rep_orig[r]) * kSmallBins + b];
+      vals[fd.bin0 + rep_boff[r] + b] = v;
+    }
+  }
+}
+
+// prep 3b: canonical row order (costmodel.cpp:161-173) - LSD over (rep codes..., target)
+__global__ void __launch_bounds__(kSortThreads) canonical_kernel(const double* __restrict__ target,
+                                                                 const uint16_t* __restrict__ codes_all, int d,
+                                                                 const FamDesc* __restrict__ fam,
+                                                                 const int32_t* __restrict__ rep_orig,
+                                                                 const int32_t* __restrict__ rep_nb,
+                                                                 int32_t* __restrict__ canon,
+                                                                 int32_t* __restrict__ tmp) {
+  __shared__ SortSmem sm;
+  const FamDesc fd = fam[blockIdx.x];
+  const int n = fd.n;
+  int32_t* A = canon + fd.pos0;
+  int32_t* B = tmp + fd.pos0;
+  sort_smem_init(sm);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) A[i] = i;
+  __syncthreads();
+  auto run = [&](auto dig) {
+    const bool moved = stable_digit_pass([&](int i) { return A[i]; }, B, n, dig, sm);
+    if (moved) {
+      int32_t* t = A;
+      A = B;
+      B = t;
+    }
+    __syncthreads();
+  };
+  for (int byte = 0; byte < 8; ++byte)
+    run([&](int r) { return static_cast<int>((value_key(target[fd.row0 + r]) >> (8 * byte)) & 255u); });
+  for (int jj = fd.nrep - 1; jj >= 0; --jj) {
+    const int f = rep_orig[fd.rep0 + jj];
+    run([&](int r) { return static_cast<int>(codes_all[(fd.row0 + r) * d + f] & 255u); });
+    if (rep_nb[fd.rep0 + jj] > 256) run([&](int r) { return static_cast<int>(codes_all[(fd.row0 + r) * d + f] >> 8); });
+  }
+  if (A != canon + fd.pos0)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) canon[fd.pos0 + i] = A[i];
+}
+
+// prep 3c: rows into canonical order (codes of reps only, targets) + row->family map
+template <typename CodeT>
+__global__ void gather_canonical_kernel(const double* __restrict__ target, const uint16_t* __restrict__ codes_all,
+                                        int d, const FamDesc* __restrict__ fam, int F, int64_t n_tot,
+                                        const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ canon,
+                                        int Dp, CodeT* __restrict__ codes_c, double* __restrict__ target_c,
+                                        int32_t* __restrict__ rowfam) {
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n_tot;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int f = family_of_pos(fam, F, p);
+    const FamDesc fd = fam[f];
+    const int64_t row = fd.row0 + canon[p];
+    rowfam[p] = f;
+    target_c[p] = target[row];
+    CodeT* o = codes_c + p * Dp;
+    for (int jj = 0; jj < Dp; ++jj)
+      o[jj] = jj < fd.nrep ? static_cast<CodeT>(codes_all[row * d + rep_orig[fd.rep0 + jj]]) : CodeT(0);
+  }
+}
+
+// prep 3d: presorted list per rep (costmodel.cpp:193-201): stable by code over canonical positions
+template <typename CodeT>
+__global__ void __launch_bounds__(kSortThreads) presort_kernel(const FamDesc* __restrict__ fam, int Dp,
+                                                               const CodeT* __restrict__ codes_c,
+                                                               const int32_t* __restrict__ rep_nb,
+                                                               int32_t* __restrict__ ord, int32_t* __restrict__ tmp) {
+  __shared__ SortSmem sm;
+  const FamDesc fd = fam[blockIdx.y];
+  const int jj = blockIdx.x;
+  if (jj >= fd.nrep) return;
+  const int n = fd.n;
+  int32_t* out = ord + fd.ord0 + static_cast<int64_t>(jj) * n;
+  int32_t* t = tmp + fd.ord0 + static_cast<int64_t>(jj) * n;
+  sort_smem_init(sm);
+  const CodeT* cc = codes_c + fd.pos0 * Dp + jj;
+  auto lo = [&](int p) { return static_cast<int>(cc[static_cast<int64_t>(p) * Dp] & 255u); };
+  if (rep_nb[fd.rep0 + jj] <= 256) {
+    if (!stable_digit_pass([](int i) { return i; }, out, n, lo, sm))
+      for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = i;
+  } else {
+    auto hi = [&](int p) { return static_cast<int>(static_cast<uint32_t>(cc[static_cast<int64_t>(p) * Dp]) >> 8); };
+    const bool m1 = stable_digit_pass([](int i) { return i; }, t, n, lo, sm);
+    if (!m1)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) t[i] = i;
+    __syncthreads();
+    if (!stable_digit_pass([&](int i) { return t[i]; }, out, n, hi, sm))
+      for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = t[i];
+  }
+}
+
+// cumulative bin counts over the whole family (for the signed-zero threshold lookup)
+template <typename CodeT>
+__global__ void bin_count_kernel(const FamDesc* __restrict__ fam, int F, int64_t n_tot, int Dp,
+                                 const CodeT* __restrict__ codes_c, const int32_t* __restrict__ rowfam,
+                                 const int32_t* __restrict__ rep_boff, int32_t* __restrict__ cle) {
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n_tot;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const FamDesc fd = fam[rowfam[p]];
+    for (int jj = 0; jj < fd.nrep; ++jj)
+      atomicAdd(&cle[fd.bin0 + rep_boff[fd.rep0 + jj] + codes_c[p * Dp + jj]], 1);
+  }
+}
+
+__global__ void bin_prefix_kernel(const FamDesc* __restrict__ fam, const int32_t* __restrict__ rep_boff,
+                                  const int32_t* __restrict__ rep_nb, int32_t* __restrict__ cle) {
+  const FamDesc fd = fam[blockIdx.x];
+  for (int jj = threadIdx.x; jj < fd.nrep; jj += blockDim.x) {
+    int32_t* c = cle + fd.bin0 + rep_boff[fd.rep0 + jj];
+    int run = 0;
+    for (int b = 0; b < rep_nb[fd.rep0 + jj]; ++b) {
+      run += c[b];
+      c[b] = run;
+    }
+  }
+}
+
+// prep 3e: base = sequential mean in canonical order (costmodel.cpp:185-188); pred = base;
+// pristine order-0 list (presorted[0], or canonical order when feature 0 is constant).
+__global__ void base_kernel(const FamDesc* __restrict__ fam, const double* __restrict__ target_c,
+                            double* __restrict__ base, double* __restrict__ pred, const int32_t* __restrict__ ord,
+                            int32_t* __restrict__ ord_root) {
+  const FamDesc fd = fam[blockIdx.x];
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i0 = 0; i0 < fd.n; i0 += 32) {
+      const double v = i0 + lane < fd.n ? target_c[fd.pos0 + i0 + lane] : 0.0;
+      const int m = min(32, fd.n - i0);
+      for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, v, l));
+    }
+    if (lane == 0) base[blockIdx.x] = fd.n ? fs_div(s, static_cast<double>(fd.n)) : 0.0;
+  }
+  __syncthreads();
+  const double b = base[blockIdx.x];
+  for (int i = threadIdx.x; i < fd.n; i += blockDim.x) {
+    pred[fd.pos0 + i] = b;
+    ord_root[fd.pos0 + i] = fd.f0rep >= 0 ? ord[fd.ord0 + static_cast<int64_t>(fd.f0rep) * fd.n + i] : i;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// boosting rounds
+// ------------------------------------------------------------------------------------------
+__global__ void round_init_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st, NodeRec* __restrict__ nodes,
+                                  int slots, TreeRec* __restrict__ trees) {
+  const int f = blockIdx.x;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  NodeRec* nd = nodes + fd.node0;
+  for (int s = threadIdx.x; s < slots; s += blockDim.x) {
+    NodeRec z;
+    memset(&z, 0, sizeof z);
+    if (s == 0) z.n = fd.n;
+    nd[s] = z;
+    TreeRec tz;
+    memset(&tz, 0, sizeof tz);
+    trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = tz;
+  }
+  if (threadIdx.x == 0) st[f].maxabs = 0;
+}
+
+__global__ void residual_kernel(const FamDesc* __restrict__ fam, int F, int64_t n_tot, FamState* __restrict__ st,
+                                const int32_t* __restrict__ rowfam, const double* __restrict__ target_c,
+                                const double* __restrict__ pred, double* __restrict__ resid,
+                                const int32_t* __restrict__ ord_root, int32_t* __restrict__ ord_cur,
+                                int16_t* __restrict__ nodeid) {
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n_tot;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int f = rowfam[p];
+    if (!st[f].active) continue;
+    const double r = fs_sub(target_c[p], pred[p]);  // costmodel.cpp:204-206
+    resid[p] = r;
+    ord_cur[p] = ord_root[p];
+    nodeid[p] = 0;
+    atomicMax(reinterpret_cast<unsigned long long*>(&st[f].maxabs),
+              static_cast<unsigned long long>(__double_as_longlong(fabs(r))));
+  }
+}
+
+__device__ __forceinline__ int fix_shift(uint64_t maxabs_bits, int n) {
+  const double m = __longlong_as_double(static_cast<long long>(maxabs_bits));
+  if (!(m > 0.0)) return 0;
+  int lg = 0;
+  while ((1 << lg) < n) ++lg;
+  const int e = ilogb(m) + 1;  // m < 2^e
+  return 61 - e - lg;          // n * |r| * 2^shift < 2^61
+}
+
+__global__ void fixed_kernel(const FamDesc* __restrict__ fam, int64_t n_tot, FamState* __restrict__ st,
+                             const int32_t* __restrict__ rowfam, const double* __restrict__ resid,
+                             int64_t* __restrict__ rfix) {
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n_tot;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int f = rowfam[p];
+    if (!st[f].active) continue;
+    const int sh = fix_shift(st[f].maxabs, fam[f].n);
+    rfix[p] = __double2ll_rn(ldexp(resid[p], sh));
+    if (p == fam[f].pos0) st[f].shift = sh;
+  }
+}
+
+__device__ __forceinline__ bool node_needs_split(const FamDesc& fd, int level, int n) {
+  return level < fd.depth && n >= max(2, fd.min_split);  // costmodel.cpp:78-80 (+ n>=2 for a boundary)
+}
+
+// Which nodes at `level` are screened, which histograms are built directly / derived.
+__global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                  NodeRec* __restrict__ nodes, int level) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int first = (1 << level) - 1;
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= (1 << level)) return;
+  NodeRec* nd = nodes + fd.node0;
+  const int s = first + local;
+  if (level == 0) {
+    if (node_needs_split(fd, 0, nd[0].n)) nd[0].build = 1;
+    else nd[0].state = kNodeLeaf;
+    return;
+  }
+  const int parent = (s - 1) >> 1;
+  if (nd[parent].state != kNodeSplit) return;
+  const bool need = node_needs_split(fd, level, nd[s].n);
+  if (!need) nd[s].state = kNodeLeaf;
+  if (s & 1) {  // left child decides the pair's build plan
+    const int sib = s + 1;
+    const bool need_sib = node_needs_split(fd, level, nd[sib].n);
+    if (need || need_sib) {
+      const int small = nd[s].n <= nd[sib].n ? s : sib;
+      nd[small].build = 1;
+      nd[small == s ? sib : s].build = 2;
+    }
+  }
+}
+
+__global__ void hist_zero_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st, int level,
+                                 int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active || level >= max(fd.depth, 1)) return;
+  const int64_t base = fd.hist0 + static_cast<int64_t>(level & 1) * fd.level_slots * fd.bins;
+  const int64_t cnt = static_cast<int64_t>(min(1 << level, fd.level_slots)) * fd.bins;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    hsum[base + i] = 0;
+    hcnt[base + i] = 0;
+  }
+}
+
+constexpr int kHistThreads = 256;
+constexpr int kHistTileRows = 64;
+constexpr int kHistChunk = 4096;
+
+// Histogram of one directly-built node over one chunk of its rows. Threads own (feature, row
+// group) pairs, so shared-memory bins are updated without atomics; the CTA then adds its
+// partial histogram to the node's global histogram with integer atomics (exact, order-free).
+template <typename CodeT, bool kGlobal>
+__global__ void __launch_bounds__(kHistThreads) hist_build_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
+    int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
+    const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
+    int64_t* __restrict__ node_abs, int groups) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const NodeRec* nd = nodes + fd.node0;
+  int s;
+  if (level == 0) {
+    if (blockIdx.y) return;
+    s = 0;
+  } else {
+    if (blockIdx.y >= (1u << (level - 1))) return;
+    const int parent = (1 << (level - 1)) - 1 + blockIdx.y;
+    if (nd[parent].state != kNodeSplit) return;
+    s = 2 * parent + 1;
+    if (nd[s].build != 1) s += 1;
+    if (nd[s].build != 1) return;
+  }
+  const int n_v = nd[s].n;
+  const int r0 = blockIdx.x * kHistChunk;
+  if (r0 >= n_v) return;
+  const int rows = min(kHistChunk, n_v - r0);
+  const int seg = nd[s].seg;
+  const int local = s - ((1 << level) - 1);
+  const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
+  const int bins = fd.bins, nrep = fd.nrep;
+
+  int64_t* s_sum = reinterpret_cast<int64_t*>(smem);
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(s_sum + (kGlobal ? 0 : static_cast<int64_t>(groups) * bins));
+  unsigned char* tail = reinterpret_cast<unsigned char*>(s_cnt + (kGlobal ? 0 : static_cast<int64_t>(groups) * bins));
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                          // [kHistTileRows][Dp]
+  int64_t* t_fix = reinterpret_cast<int64_t*>(t_codes + kHistTileRows * Dp);  // [kHistTileRows]
+  __shared__ unsigned long long s_abs;
+  const int tid = threadIdx.x;
+  if (!kGlobal)
+    for (int i = tid; i < groups * bins; i += kHistThreads) {
+      s_sum[i] = 0;
+      s_cnt[i] = 0;
+    }
+  if (tid == 0) s_abs = 0;
+  // thread -> (feature, group)
+  const int per_group = nrep > 0 ? (nrep < kHistThreads ? nrep : kHistThreads) : 1;
+  const int g = tid / per_group;
+  const int fj0 = tid - g * per_group;
+  const bool worker = g < groups && fj0 < nrep;
+  __syncthreads();
+  const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
+  for (int t0 = 0; t0 < rows; t0 += kHistTileRows) {
+    const int tr = min(kHistTileRows, rows - t0);
+    for (int i = tid; i < tr * vec_per_row; i += kHistThreads) {
+      const int r = i / vec_per_row, v = i - r * vec_per_row;
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+      reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+    }
+    unsigned long long a = 0;
+    if (tid < tr) {
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid];
+      const int64_t v = rfix[p];
+      t_fix[tid] = v;
+      a = static_cast<unsigned long long>(v < 0 ? -v : v);
+    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if ((tid & 31) == 0 && a) atomicAdd(&s_abs, a);
+    __syncthreads();
+    if (worker) {
+      for (int fj = fj0; fj < nrep; fj += per_group) {
+        const int boff = rep_boff[fd.rep0 + fj];
+        for (int r = g; r < tr; r += groups) {
+          const int bin = boff + static_cast<int>(t_codes[r * Dp + fj]);
+          if (kGlobal) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(hsum + hbase + bin),
+                      static_cast<unsigned long long>(t_fix[r]));
+            atomicAdd(hcnt + hbase + bin, 1);
+          } else {
+            s_sum[g * bins + bin] += t_fix[r];
+            s_cnt[g * bins + bin] += 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!kGlobal) {
+    for (int b = tid; b < bins; b += kHistThreads) {
+      int64_t sm = 0;
+      int32_t c = 0;
+      for (int gg = 0; gg < groups; ++gg) {
+        sm += s_sum[gg * bins + b];
+        c += s_cnt[gg * bins + b];
+      }
+      if (c) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(hsum + hbase + b), static_cast<unsigned long long>(sm));
+        atomicAdd(hcnt + hbase + b, c);
+      }
+    }
+  }
+  if (tid == 0 && s_abs)
+    atomicAdd(reinterpret_cast<unsigned long long*>(node_abs + fd.node0 + s), s_abs);
+}
+
+// sibling = parent - built child (exact: integer histograms)
+__global__ void hist_derive_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                   const NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
+                                   int32_t* __restrict__ hcnt, int64_t* __restrict__ node_abs) {
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active || level == 0) return;
+  const NodeRec* nd = nodes + fd.node0;
+  const int k = blockIdx.y;
+  if (k >= (1 << (level - 1))) return;
+  const int parent = (1 << (level - 1)) - 1 + k;
+  if (nd[parent].state != kNodeSplit) return;
+  const int c1 = 2 * parent + 1, c2 = c1 + 1;
+  int built, other;
+  if (nd[c1].build == 1 && nd[c2].build == 2) {
+    built = c1;
+    other = c2;
+  } else if (nd[c2].build == 1 && nd[c1].build == 2) {
+    built = c2;
+    other = c1;
+  } else {
+    return;
+  }
+  const int first = (1 << level) - 1, pfirst = (1 << (level - 1)) - 1;
+  const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + (built - first)) * fd.bins;
+  const int64_t ho = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + (other - first)) * fd.bins;
+  const int64_t hp = fd.hist0 + (static_cast<int64_t>((level - 1) & 1) * fd.level_slots + (parent - pfirst)) * fd.bins;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < fd.bins; b += gridDim.x * blockDim.x) {
+    hsum[ho + b] = hsum[hp + b] - hsum[hb + b];
+    hcnt[ho + b] = hcnt[hp + b] - hcnt[hb + b];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    node_abs[fd.node0 + other] = node_abs[fd.node0 + parent] - node_abs[fd.node0 + built];
+}
+
+// Screened gain of one candidate plus a rigorous bound on |reference gain - screened gain|.
+// ls/ts: fixed-point left/total sums; S: sum|r| of the node (real units); scale = 2^-shift.
+// The reference folds sums sequentially (error <= gamma_n * S each), R = T - L rounds once,
+// then ((L*L)/lc + (R*R)/rc) - (T*T)/n rounds ~5 more times; the screen's sums are exact on
+// the quantised residuals (quantisation <= n * scale / 2). Factor 2 covers both sides.
+__device__ __forceinline__ void screen_gain(int64_t ls, int64_t ts, int lc, int n, double scale, double S, double& g,
+                                            double& lo, double& hi) {
+  const double u = 1.1102230246251565e-16;
+  const double L = static_cast<double>(ls) * scale, T = static_cast<double>(ts) * scale;
+  const double R = static_cast<double>(ts - ls) * scale;
+  const int rc = n - lc;
+  const double A = L * L / lc, B = R * R / rc, P = T * T / n;
+  g = (A + B) - P;
+  const double nu = static_cast<double>(n) * u;
+  const double gam = nu / (1.0 - nu);
+  const double q = static_cast<double>(n) * 0.5 * scale;
+  const double EL = gam * S + q, ET = gam * S + q, ER = 2.0 * gam * S + 2.0 * q + u * fabs(R);
+  const double aL = fabs(L) + EL, aR = fabs(R) + ER, aT = fabs(T) + ET;
+  const double dA = (2.0 * fabs(L) + EL) * EL / lc + 4.0 * u * aL * aL / lc;
+  const double dB = (2.0 * fabs(R) + ER) * ER / rc + 4.0 * u * aR * aR / rc;
+  const double dP = (2.0 * fabs(T) + ET) * ET / n + 4.0 * u * aT * aT / n;
+  const double delta = 2.0 * (dA + dB + dP + 4.0 * u * (A + B + P)) + 1e-300;
+  lo = g - delta;
+  hi = g + delta;
+}
+
+// One thread per (family, node at level, rep). pass 0: max lower bound per node. pass 1:
+// window membership (hi >= LO and hi > 0), per-feature best candidate, node window count.
+__global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                              NodeRec* __restrict__ nodes, int level, const int64_t* __restrict__ hsum,
+                              const int32_t* __restrict__ hcnt, const int64_t* __restrict__ node_abs,
+                              const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
+                              WinRec* __restrict__ win, int nrep_max, int level_slots_max, int pass) {
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.y;
+  if (local >= (1 << level)) return;
+  const int jj = blockIdx.x * blockDim.x + threadIdx.x;
+  if (jj >= fd.nrep) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != 0 || nd.build == 0) return;
+  const int n = nd.n;
+  const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins +
+                     rep_boff[fd.rep0 + jj];
+  const int nb = rep_nb[fd.rep0 + jj];
+  const double scale = ldexp(1.0, -st[f].shift);
+  const double S = static_cast<double>(node_abs[fd.node0 + s]) * scale * (1.0 + 1e-12);
+  int64_t ts = 0;
+  for (int b = 0; b < nb; ++b) ts += hsum[hb + b];
+  const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
+  double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
+  int bb = -1, count = 0, cum = 0;
+  int64_t ls = 0;
+  for (int b = 0; b < nb; ++b) {
+    const int c = hcnt[hb + b];
+    if (!c) continue;
+    cum += c;
+    ls += hsum[hb + b];
+    if (cum >= n) break;  // no later non-empty bin: not a boundary
+    double g, lo, hi;
+    screen_gain(ls, ts, cum, n, scale, S, g, lo, hi);
+    if (!pass) {
+      best_lo = fmax(best_lo, lo);
+    } else if (hi >= LO && hi > 0.0) {
+      ++count;
+      if (g > bg) {
+        bg = g;
+        bl = lo;
+        bb = b;
+      }
+    }
+  }
+  if (!pass) {
+    if (best_lo > -INFINITY) atomicMax(reinterpret_cast<unsigned long long*>(&nd.lokey), lo_key(best_lo));
+  } else {
+    WinRec w;
+    w.best_g = bg;
+    w.best_lo = bl;
+    w.best_bin = bb;
+    w.flag = count > 0;
+    win[(static_cast<int64_t>(f) * level_slots_max + local) * nrep_max + jj] = w;
+    if (count) atomicAdd(&nd.wcount, count);
+  }
+}
+
+struct ExactItem {
+  int32_t fam;
+  int16_t slot;
+  int16_t rep;  // -1: node total
+};
+
+// Decide screened nodes; queue the rest for reference-order re-evaluation.
+__global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                              NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
+                              const int32_t* __restrict__ rep_boff, const WinRec* __restrict__ win, int nrep_max,
+                              int level_slots_max, ExactItem* __restrict__ items, int* __restrict__ n_items) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != 0 || nd.build == 0) return;
+  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
+  if (nd.wcount == 0) {  // no candidate can have a positive reference gain
+    nd.state = kNodeLeaf;
+    return;
+  }
+  if (nd.wcount == 1) {
+    for (int jj = 0; jj < fd.nrep; ++jj) {
+      if (!w[jj].flag) continue;
+      if (w[jj].best_lo > 0.0) {
+        nd.state = kNodeSplit;
+        nd.rep = jj;
+        nd.bin = w[jj].best_bin;
+        nd.gain = w[jj].best_g;
+        const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins +
+                           rep_boff[fd.rep0 + jj];
+        int lc = 0;
+        for (int b = 0; b <= nd.bin; ++b) lc += hcnt[hb + b];
+        nd.lc = lc;
+        atomicAdd(&const_cast<FamState*>(st)[f].screened, 1ull);
+        return;
+      }
+      break;
+    }
+  }
+  nd.state = kNodeExact;
+  atomicAdd(&const_cast<FamState*>(st)[f].exact, 1ull);
+  int k = 1;
+  for (int jj = 0; jj < fd.nrep; ++jj) k += w[jj].flag;
+  const int base = atomicAdd(n_items, k);
+  items[base] = {f, static_cast<int16_t>(s), static_cast<int16_t>(-1)};
+  int o = 1;
+  for (int jj = 0; jj < fd.nrep; ++jj)
+    if (w[jj].flag) items[base + o++] = {f, static_cast<int16_t>(s), static_cast<int16_t>(jj)};
+}
+
+// One warp per item: reference-order folds. Item rep < 0: node total over the order-0 list
+// (sum_residuals(order[0]), costmodel.cpp:47). Item rep j: best_split's left sums over feature j's
+// presorted list restricted to the node (:50-55), recorded at every value boundary.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes,
+                                                    const ExactItem* __restrict__ items, const int* __restrict__ n_items,
+                                                    int level, int Dp, const CodeT* __restrict__ codes_c,
+                                                    const double* __restrict__ resid, const int32_t* __restrict__ ord,
+                                                    const int32_t* __restrict__ ord_cur,
+                                                    const int16_t* __restrict__ nodeid,
+                                                    const int32_t* __restrict__ rep_boff, double* __restrict__ lbuf) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int total = *n_items;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += warps) {
+    const ExactItem it = items[w];
+    const FamDesc fd = fam[it.fam];
+    NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int n = nd.n;
+    if (it.rep < 0) {
+      double s = 0.0;
+      const int32_t* L = ord_cur + fd.pos0 + nd.seg;
+      for (int i0 = 0; i0 < n; i0 += 32) {
+        const double v = i0 + lane < n ? resid[fd.pos0 + L[i0 + lane]] : 0.0;
+        const int m = min(32, n - i0);
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, v, l));
+      }
+      if (lane == 0) nd.total = s;
+      continue;
+    }
+    const int jj = it.rep;
+    const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
+    const int local = it.slot - ((1 << level) - 1);
+    double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    double left = 0.0;
+    int prev = -1, seen = 0;
+    for (int i0 = 0; i0 < fd.n && seen < n; i0 += 32) {
+      const int i = i0 + lane;
+      int p = 0, code = 0;
+      double rv = 0.0;
+      bool mem = false;
+      if (i < fd.n) {
+        p = L[i];
+        mem = nodeid[fd.pos0 + p] == it.slot;
+        if (mem) {
+          code = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + jj]);
+          rv = resid[fd.pos0 + p];
+        }
+      }
+      unsigned m = __ballot_sync(0xffffffffu, mem);
+      seen += __popc(m);
+      while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const int c = __shfl_sync(0xffffffffu, code, l);
+        const double v = __shfl_sync(0xffffffffu, rv, l);
+        if (prev >= 0 && c != prev && lane == 0) out[prev] = left;  // boundary after bin `prev`
+        left = fs_add(left, v);
+        prev = c;
+      }
+    }
+  }
+}
+
+// Reference decision over the exactly folded candidates: gain = ((L*L)/lc + (R*R)/rc) - (T*T)/n,
+// R = T - L (costmodel.cpp:58-62), strict > in (feature, threshold) order (:65).
+__global__ void exact_decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                    NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
+                                    const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
+                                    const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
+                                    const double* __restrict__ lbuf) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeExact) return;
+  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
+  const int n = nd.n;
+  const double T = nd.total;
+  const double parent = fs_div(fs_mul(T, T), static_cast<double>(n));
+  double best = 0.0;
+  int bj = -1, bb = -1, blc = 0;
+  for (int jj = 0; jj < fd.nrep; ++jj) {
+    if (!w[jj].flag) continue;
+    const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins +
+                       rep_boff[fd.rep0 + jj];
+    const double* lb = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    int cum = 0;
+    for (int b = 0; b < rep_nb[fd.rep0 + jj]; ++b) {
+      const int c = hcnt[hb + b];
+      if (!c) continue;
+      cum += c;
+      if (cum >= n) break;
+      const double L = lb[b];
+      const double R = fs_sub(T, L);
+      const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+      const double r = fs_div(fs_mul(R, R), static_cast<double>(n - cum));
+      const double g = fs_sub(fs_add(a, r), parent);
+      if (g > best) {
+        best = g;
+        bj = jj;
+        bb = b;
+        blc = cum;
+      }
+    }
+  }
+  if (bj < 0) {
+    nd.state = kNodeLeaf;
+  } else {
+    nd.state = kNodeSplit;
+    nd.rep = bj;
+    nd.bin = bb;
+    nd.gain = best;
+    nd.lc = blc;
+  }
+}
+
+// Split nodes: exact threshold, tree record, stable partition of the order-0 segment in place
+// (costmodel.cpp:94-105 for list 0), row -> child ids, child records.
+template <typename CodeT>
+__global__ void __launch_bounds__(1024) partition_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level, int Dp,
+    const CodeT* __restrict__ codes_c, int32_t* __restrict__ ord_cur, int32_t* __restrict__ scratch,
+    int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_boff,
+    const double* __restrict__ vals, const int32_t* __restrict__ cle, const int32_t* __restrict__ ord,
+    const int32_t* __restrict__ canon, const double* __restrict__ x, int d, TreeRec* __restrict__ trees, int slots) {
+  __shared__ int wsum[32];
+  __shared__ int base_l, base_r;
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x;
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeSplit) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int jj = nd.rep, bin = nd.bin, n = nd.n, seg = nd.seg, lc = nd.lc;
+  TreeRec* tr = trees + fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots;
+  if (tid == 0) {
+    const int orig = rep_orig[fd.rep0 + jj];
+    double thr = vals[fd.bin0 + rep_boff[fd.rep0 + jj] + bin];
+    if (thr == 0.0) {  // +0.0 and -0.0 share a bin: take the last left element's own value
+      const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
+      for (int i = cle[fd.bin0 + rep_boff[fd.rep0 + jj] + bin] - 1; i >= 0; --i) {
+        if (nodeid[fd.pos0 + L[i]] == s) {
+          thr = x[(fd.row0 + canon[fd.pos0 + L[i]]) * d + orig];
+          break;
+        }
+      }
+    }
+    TreeRec r;
+    r.kind = kNodeSplit;
+    r.feature = orig;
+    r.threshold = thr;
+    r.value = 0.0;
+    r.gain = nd.gain;
+    tr[s] = r;
+    base_l = 0;
+    base_r = 0;
+    NodeRec& a = nodes[fd.node0 + 2 * s + 1];
+    NodeRec& b = nodes[fd.node0 + 2 * s + 2];
+    a.n = lc;
+    a.seg = seg;
+    b.n = n - lc;
+    b.seg = seg + lc;
+  }
+  int32_t* src = scratch + fd.pos0 + seg;
+  int32_t* dst = ord_cur + fd.pos0 + seg;
+  for (int i = tid; i < n; i += blockDim.x) src[i] = dst[i];
+  __syncthreads();
+  const int16_t cl = static_cast<int16_t>(2 * s + 1), cr = static_cast<int16_t>(2 * s + 2);
+  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+    const int i = t0 + tid;
+    int p = 0;
+    bool left = false;
+    if (i < n) {
+      p = src[i];
+      left = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + jj]) <= bin;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, left);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      const int v = wsum[lane];
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      wsum[lane] = incl - v;
+    }
+    __syncthreads();
+    const int lrank = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+    if (i < n) {
+      if (left) {
+        dst[base_l + lrank] = p;
+        nodeid[fd.pos0 + p] = cl;
+      } else {
+        dst[lc + base_r + (i - t0) - lrank] = p;
+        nodeid[fd.pos0 + p] = cr;
+      }
+    }
+    __syncthreads();  // every thread has used base_l / base_r for this tile
+    if (warp == 31 && lane == 0) {  // tile total = warp 31's exclusive prefix + its own count
+      const int tile_left = wsum[31] + __popc(bal);
+      const int tile = min(static_cast<int>(blockDim.x), n - t0);
+      base_l += tile_left;
+      base_r += tile - tile_left;
+    }
+    __syncthreads();
+  }
+}
+
+// Leaves: value = (reference-order total) / n (costmodel.cpp:86), prediction += lr * value
+// (:88-90); tree record. One warp per (family, slot).
+__global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamState* __restrict__ st,
+                            NodeRec* __restrict__ nodes, int slots, const int32_t* __restrict__ ord_cur,
+                            const double* __restrict__ resid, double* __restrict__ pred, TreeRec* __restrict__ trees) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int f = static_cast<int>(w / slots), s = static_cast<int>(w % slots);
+  if (f >= F) return;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeLeaf || nd.n == 0) return;
+  // a slot is a leaf of this tree only if its parent split (or it is the root)
+  if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
+  const int n = nd.n;
+  const int32_t* L = ord_cur + fd.pos0 + nd.seg;
+  double sum = 0.0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const double v = i0 + lane < n ? resid[fd.pos0 + L[i0 + lane]] : 0.0;
+    const int m = min(32, n - i0);
+    for (int l = 0; l < m; ++l) sum = fs_add(sum, __shfl_sync(0xffffffffu, v, l));
+  }
+  const double value = fs_div(sum, static_cast<double>(n));
+  const double step = fs_mul(fd.lr, value);
+  for (int i = lane; i < n; i += 32) {
+    const int64_t p = fd.pos0 + L[i];
+    pred[p] = fs_add(pred[p], step);
+  }
+  if (lane == 0) {
+    nd.value = value;
+    TreeRec r;
+    r.kind = kNodeLeaf;
+    r.feature = -1;
+    r.threshold = 0.0;
+    r.value = value;
+    r.gain = 0.0;
+    trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = r;
+  }
+}
+
+// Commit the round's tree or stop (costmodel.cpp:212), then MSE over canonical rows (:215-220).
+// The MSE is a fixed-order tree reduction: deterministic, within 1e-15 relative of the
+// reference's sequential fold (it never feeds back into the model).
+__global__ void commit_mse_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
+                                  const NodeRec* __restrict__ nodes, const double* __restrict__ target_c,
+                                  const double* __restrict__ pred, double* __restrict__ mse, int max_trees) {
+  __shared__ double part[256];
+  __shared__ int commit;
+  const int f = blockIdx.x;
+  const FamDesc fd = fam[f];
+  if (threadIdx.x == 0) {
+    commit = 0;
+    if (st[f].active) {
+      const NodeRec& root = nodes[fd.node0];
+      if (root.state == kNodeLeaf && root.value == 0.0) {
+        st[f].active = 0;
+      } else {
+        commit = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (!commit) return;
+  double a = 0.0;
+  for (int i = threadIdx.x; i < fd.n; i += blockDim.x) {
+    const double e = fs_sub(target_c[fd.pos0 + i], pred[fd.pos0 + i]);
+    a = fs_add(a, fs_mul(e, e));
+  }
+  part[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) part[threadIdx.x] = fs_add(part[threadIdx.x], part[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int t = st[f].ntrees;
+    mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(part[0], static_cast<double>(fd.n));
+    st[f].ntrees = t + 1;
+    if (t + 1 >= fd.trees) st[f].active = 0;
+  }
+}
+
+}  // namespace
+}  // namespace fit
+}  // namespace fs
+
+// ==========================================================================================
+// host orchestration
+// ==========================================================================================
+namespace fs {
+namespace fit {
+namespace {
+
+struct Arena {  // stream-ordered scratch owned by one fit call
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  explicit Arena(cudaStream_t st) : s(st) {}
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    FS_CUDA(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), s));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (!v.empty()) FS_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return p;
+  }
+  ~Arena() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+};
+
+template <class T>
+std::vector<T> download(const T* d, size_t n, cudaStream_t s) {
+  std::vector<T> h(n);
+  if (n) FS_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+inline unsigned grid1(int64_t n, int block, int cap) {
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, block), cap)));
+}
+
+template <typename CodeT>
+void run_rounds(fs_device* dev, Arena& ar, int F, int d, int Dp, int64_t n_tot, int max_trees, int depth_max,
+                int slots, int nrep_max, int max_bins, int n_max, int level_slots_max, const FamDesc* fam_d,
+                FamState* st_d, const double* x_d, const double* target_d, const uint16_t* codes_all,
+                const int32_t* rep_orig_d, const int32_t* rep_nb_d, const int32_t* rep_boff_d, const double* vals_d,
+                int64_t total_ord, int64_t total_bins, int64_t total_hist, int64_t total_lbuf, int64_t total_tree,
+                TreeRec* trees_d, double* mse_d, double* base_d, int min_nrep_hint) {
+  cudaStream_t s = dev->stream;
+  const int sm = dev->sm_count;
+  // ---- prep: canonical order, gather, presorts, bin counts, base -------------------------
+  int32_t* canon = ar.alloc<int32_t>(n_tot);
+  int32_t* tmp = ar.alloc<int32_t>(std::max<int64_t>(n_tot, total_ord));
+  canonical_kernel<<<F, kSortThreads, 0, s>>>(target_d, codes_all, d, fam_d, rep_orig_d, rep_nb_d, canon, tmp);
+  CodeT* codes_c = ar.alloc<CodeT>(static_cast<size_t>(n_tot) * Dp);
+  double* target_c = ar.alloc<double>(n_tot);
+  int32_t* rowfam = ar.alloc<int32_t>(n_tot);
+  gather_canonical_kernel<CodeT><<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(
+      target_d, codes_all, d, fam_d, F, n_tot, rep_orig_d, canon, Dp, codes_c, target_c, rowfam);
+  int32_t* ord = ar.alloc<int32_t>(total_ord);
+  if (nrep_max > 0) presort_kernel<CodeT><<<dim3(nrep_max, F), kSortThreads, 0, s>>>(fam_d, Dp, codes_c, rep_nb_d, ord, tmp);
+  int32_t* cle = ar.alloc<int32_t>(total_bins);
+  FS_CUDA(cudaMemsetAsync(cle, 0, std::max<int64_t>(total_bins, 1) * sizeof(int32_t), s));
+  bin_count_kernel<CodeT><<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, F, n_tot, Dp, codes_c, rowfam, rep_boff_d, cle);
+  bin_prefix_kernel<<<F, 128, 0, s>>>(fam_d, rep_boff_d, rep_nb_d, cle);
+  double* pred = ar.alloc<double>(n_tot);
+  int32_t* ord_root = ar.alloc<int32_t>(n_tot);
+  base_kernel<<<F, 256, 0, s>>>(fam_d, target_c, base_d, pred, ord, ord_root);
+  dev->count_launch(8);
+  FS_CUDA(cudaGetLastError());
+
+  // ---- round state ---------------------------------------------------------------------
+  double* resid = ar.alloc<double>(n_tot);
+  int64_t* rfix = ar.alloc<int64_t>(n_tot);
+  int32_t* ord_cur = ar.alloc<int32_t>(n_tot);
+  int32_t* scratch = ar.alloc<int32_t>(n_tot);
+  int16_t* nodeid = ar.alloc<int16_t>(n_tot);
+  NodeRec* nodes = ar.alloc<NodeRec>(static_cast<size_t>(F) * slots);
+  int64_t* node_abs = ar.alloc<int64_t>(static_cast<size_t>(F) * slots);
+  int64_t* hsum = ar.alloc<int64_t>(total_hist);
+  int32_t* hcnt = ar.alloc<int32_t>(total_hist);
+  double* lbuf = ar.alloc<double>(total_lbuf);
+  WinRec* win = ar.alloc<WinRec>(static_cast<size_t>(F) * level_slots_max * std::max(nrep_max, 1));
+  ExactItem* items = ar.alloc<ExactItem>(static_cast<size_t>(F) * level_slots_max * (nrep_max + 1));
+  int* n_items = ar.alloc<int>(1);
+  (void)total_tree;
+
+  // histogram launch shape
+  const int per_group_min = std::max(1, std::min(min_nrep_hint, kHistThreads));
+  const size_t tile_bytes = ((static_cast<size_t>(kHistTileRows) * Dp * sizeof(CodeT) + 15) & ~size_t(15)) +
+                            kHistTileRows * sizeof(int64_t) + 64;
+  const size_t smem_cap = 200 * 1024;
+  int groups = std::max(1, kHistThreads / std::max(1, std::min(nrep_max, kHistThreads)));
+  (void)per_group_min;
+  while (groups > 1 && static_cast<size_t>(groups) * max_bins * 12 + tile_bytes > smem_cap) --groups;
+  const bool hist_global = static_cast<size_t>(max_bins) * 12 + tile_bytes > smem_cap;
+  const size_t hist_smem = hist_global ? tile_bytes + 16 : ((static_cast<size_t>(groups) * max_bins * 12 + 15) & ~size_t(15)) + tile_bytes;
+  if (hist_global) {
+    FS_CUDA(cudaFuncSetAttribute(hist_build_kernel<CodeT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(hist_smem)));
+  } else {
+    FS_CUDA(cudaFuncSetAttribute(hist_build_kernel<CodeT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(hist_smem)));
+  }
+  const unsigned chunks = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n_max, kHistChunk)));
+
+  for (int round = 0; round < max_trees; ++round) {
+    round_init_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, slots, trees_d);
+    FS_CUDA(cudaMemsetAsync(node_abs, 0, static_cast<size_t>(F) * slots * sizeof(int64_t), s));
+    residual_kernel<<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, F, n_tot, st_d, rowfam, target_c, pred, resid,
+                                                                 ord_root, ord_cur, nodeid);
+    fixed_kernel<<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, n_tot, st_d, rowfam, resid, rfix);
+    dev->count_launch(3);
+    for (int level = 0; level <= depth_max; ++level) {
+      const unsigned lw = 1u << level;
+      level_plan_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level);
+      dev->count_launch();
+      if (level == depth_max || nrep_max == 0) continue;
+      hist_zero_kernel<<<dim3(grid1(static_cast<int64_t>(lw) * max_bins, 256, 64), F), 256, 0, s>>>(fam_d, st_d, level,
+                                                                                                  hsum, hcnt);
+      const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
+      if (hist_global)
+        hist_build_kernel<CodeT, true><<<dim3(chunks, pairs, F), kHistThreads, hist_smem, s>>>(
+            fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, 1);
+      else
+        hist_build_kernel<CodeT, false><<<dim3(chunks, pairs, F), kHistThreads, hist_smem, s>>>(
+            fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, groups);
+      hist_derive_kernel<<<dim3(grid1(max_bins, 256, 16), pairs, F), 256, 0, s>>>(fam_d, st_d, nodes, level, hsum,
+                                                                                  hcnt, node_abs);
+      const dim3 sg(grid1(nrep_max, 128, 1 << 20), lw, F);
+      screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
+                                        std::max(nrep_max, 1), level_slots_max, 0);
+      screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
+                                        std::max(nrep_max, 1), level_slots_max, 1);
+      FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
+      decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
+                                                                     std::max(nrep_max, 1), level_slots_max, items,
+                                                                     n_items);
+      exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord,
+                                                 ord_cur, nodeid, rep_boff_d, lbuf);
+      exact_decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt,
+                                                                           rep_boff_d, rep_nb_d, win,
+                                                                           std::max(nrep_max, 1), level_slots_max, lbuf);
+      partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur, scratch,
+                                                            nodeid, rep_orig_d, rep_boff_d, vals_d, cle, ord, canon,
+                                                            x_d, d, trees_d, slots);
+      dev->count_launch(10);
+    }
+    const int64_t leaf_threads = static_cast<int64_t>(F) * slots * 32;
+    leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
+                                                                                     ord_cur, resid, pred, trees_d);
+    commit_mse_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred, mse_d, max_trees);
+    dev->count_launch(2);
+    FS_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace
+
+// Fit every family segment; results replace fo->fams[f] (pre-order trees + compiled form).
+void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int d, const double* x_d,
+                  const double* target_d, const fs_gbt_params* params) {
+  cudaStream_t s = dev->stream;
+  if (F < 1) return;
+  if (F > static_cast<int>(fo->fams.size())) fail(FS_ERANGE, "fit: more segments than forest families");
+  if (seg[0] != 0) fail(FS_EINVAL, "fit: seg[0] must be 0");
+  int depth_max = 0, max_trees = 0, n_max = 0;
+  for (int f = 0; f < F; ++f) {
+    const int64_t n = seg[f + 1] - seg[f];
+    if (n < 0) fail(FS_EINVAL, "fit: segment offsets must be non-decreasing");
+    if (n > (1 << 30)) fail(FS_EINVAL, "fit: family larger than 2^30 rows");
+    if (params[f].trees < 0) fail(FS_EINVAL, "fit: trees must be >= 0");
+    if (params[f].depth < 0 || params[f].depth > kMaxDepth)
+      fail(FS_EINVAL, "fit: depth must be in [0, " + std::to_string(kMaxDepth) + "]");
+    if (n > 0) {
+      depth_max = std::max(depth_max, params[f].depth);
+      max_trees = std::max(max_trees, params[f].trees);
+      n_max = std::max<int>(n_max, static_cast<int>(n));
+    }
+  }
+  const int64_t n_tot = seg[F];
+  Arena ar(s);
+  // ---- family descriptors (stage 1 needs row0/n only) -----------------------------------
+  std::vector<FamDesc> fam(static_cast<size_t>(F));
+  for (int f = 0; f < F; ++f) {
+    std::memset(&fam[f], 0, sizeof(FamDesc));
+    fam[f].row0 = seg[f];
+    fam[f].pos0 = seg[f];
+    fam[f].n = static_cast<int32_t>(seg[f + 1] - seg[f]);
+    fam[f].trees = fam[f].n > 0 ? params[f].trees : 0;
+    fam[f].depth = params[f].depth;
+    fam[f].min_split = params[f].min_samples_split;
+    fam[f].lr = params[f].learning_rate;
+  }
+  FamDesc* fam_d = ar.upload(fam);
+
+  // ---- stage 1: distinct values / codes ---------------------------------------------------
+  uint16_t* codes_all = ar.alloc<uint16_t>(static_cast<size_t>(std::max<int64_t>(n_tot, 1)) * std::max(d, 1));
+  double* vals_all = ar.alloc<double>(static_cast<size_t>(F) * std::max(d, 1) * kSmallBins);
+  int32_t* nb_all = ar.alloc<int32_t>(static_cast<size_t>(F) * std::max(d, 1));
+  uint64_t* hash_all = ar.alloc<uint64_t>(static_cast<size_t>(F) * std::max(d, 1));
+  FS_CUDA(cudaMemsetAsync(nb_all, 0, static_cast<size_t>(F) * std::max(d, 1) * sizeof(int32_t), s));
+  FS_CUDA(cudaMemsetAsync(hash_all, 0, static_cast<size_t>(F) * std::max(d, 1) * sizeof(uint64_t), s));
+  if (d > 0) {
+    const size_t smem = 32 * kHashSlots * 8 + 32 * kSmallBins * 8 + 32 * 4 * 2 + 32 * 8;
+    FS_CUDA(cudaFuncSetAttribute(distinct_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    distinct_small_kernel<<<dim3(static_cast<unsigned>(ceil_div(d, 32)), F), 256, smem, s>>>(
+        x_d, d, fam_d, codes_all, vals_all, nb_all, hash_all, dev->err_d);
+    dev->count_launch();
+  }
+  raise_deferred(dev->take_errors());
+  std::vector<int32_t> nb = download(nb_all, static_cast<size_t>(F) * d, s);
+  std::vector<LargeItem> large;
+  int64_t vl = 0;
+  for (int f = 0; f < F; ++f)
+    for (int j = 0; j < d; ++j)
+      if (nb[static_cast<size_t>(f) * d + j] < 0) {
+        large.push_back({f, j, vl});
+        vl += fam[f].n;
+      }
+  double* vals_large = ar.alloc<double>(std::max<int64_t>(vl, 1));
+  std::vector<int64_t> large_src(static_cast<size_t>(F) * d, -1);
+  if (!large.empty()) {
+    LargeItem* items_d = ar.upload(large);
+    int32_t* bufA = ar.alloc<int32_t>(large.size() * n_max);
+    int32_t* bufB = ar.alloc<int32_t>(large.size() * n_max);
+    distinct_large_kernel<<<static_cast<unsigned>(large.size()), kSortThreads, 0, s>>>(
+        x_d, d, fam_d, items_d, bufA, bufB, n_max, codes_all, vals_large, nb_all, hash_all, dev->err_d);
+    dev->count_launch();
+    raise_deferred(dev->take_errors());
+    nb = download(nb_all, static_cast<size_t>(F) * d, s);
+    for (const auto& it : large) large_src[static_cast<size_t>(it.fam) * d + it.feat] = it.vals0;
+  }
+  for (int v : nb)
+    if (v > kMaxBins) fail(FS_EINVAL, "fit: more than 65535 distinct values in one feature");
+  std::vector<uint64_t> hh = download(hash_all, static_cast<size_t>(F) * d, s);
+
+  // ---- stage 2: representatives (drop constant and duplicate-column features) -------------
+  std::vector<PairItem> pairs;
+  for (int f = 0; f < F; ++f) {
+    std::map<std::pair<int, uint64_t>, std::vector<int>> seen;
+    for (int j = 0; j < d; ++j) {
+      const int v = nb[static_cast<size_t>(f) * d + j];
+      if (v <= 1) continue;
+      auto& lst = seen[{v, hh[static_cast<size_t>(f) * d + j]}];
+      for (int k : lst) pairs.push_back({f, k, j, 0});
+      lst.push_back(j);
+    }
+  }
+  std::vector<int32_t> mismatch;
+  if (!pairs.empty()) {
+    PairItem* pd = ar.upload(pairs);
+    int32_t* mm = ar.alloc<int32_t>(pairs.size());
+    verify_pairs_kernel<<<static_cast<unsigned>(pairs.size()), 256, 0, s>>>(codes_all, d, fam_d, pd, mm);
+    dev->count_launch();
+    mismatch = download(mm, pairs.size(), s);
+  }
+  std::vector<std::vector<char>> dup(static_cast<size_t>(F), std::vector<char>(static_cast<size_t>(d), 0));
+  for (size_t i = 0; i < pairs.size(); ++i)
+    if (!mismatch[i]) dup[static_cast<size_t>(pairs[i].fam)][static_cast<size_t>(pairs[i].b)] = 1;
+  std::vector<int32_t> rep_orig, rep_nb, rep_boff;
+  std::vector<int64_t> rep_src;
+  int nrep_max = 0, max_bins = 0, max_nb = 0, min_nrep = INT_MAX;
+  int64_t total_ord = 0, total_bins = 0, total_hist = 0, total_lbuf = 0, total_tree = 0;
+  const int slots = (1 << (depth_max + 1)) - 1;
+  const int level_slots_max = std::max(1, 1 << std::max(0, depth_max - 1));
+  for (int f = 0; f < F; ++f) {
+    FamDesc& fd = fam[static_cast<size_t>(f)];
+    fd.rep0 = static_cast<int32_t>(rep_orig.size());
+    int bins = 0;
+    fd.f0rep = -1;
+    if (fd.n > 0)
+      for (int j = 0; j < d; ++j) {
+        const int v = nb[static_cast<size_t>(f) * d + j];
+        if (v <= 1 || dup[static_cast<size_t>(f)][static_cast<size_t>(j)]) continue;
+        if (j == 0) fd.f0rep = static_cast<int32_t>(rep_orig.size()) - fd.rep0;
+        rep_orig.push_back(j);
+        rep_nb.push_back(v);
+        rep_boff.push_back(bins);
+        rep_src.push_back(large_src[static_cast<size_t>(f) * d + j]);
+        bins += v;
+        max_nb = std::max(max_nb, v);
+      }
+    fd.nrep = static_cast<int32_t>(rep_orig.size()) - fd.rep0;
+    fd.bins = bins;
+    fd.level_slots = std::max(1, 1 << std::max(0, fd.depth - 1));
+    fd.ord0 = total_ord;
+    fd.bin0 = total_bins;
+    fd.hist0 = total_hist;
+    fd.lbuf0 = total_lbuf;
+    fd.node0 = static_cast<int64_t>(f) * slots;
+    fd.tree0 = total_tree;
+    total_ord += static_cast<int64_t>(fd.nrep) * fd.n;
+    total_bins += bins;
+    total_hist += 2LL * fd.level_slots * bins;
+    total_lbuf += static_cast<int64_t>(fd.level_slots) * bins;
+    total_tree += static_cast<int64_t>(fd.trees) * slots;
+    nrep_max = std::max(nrep_max, static_cast<int>(fd.nrep));
+    if (fd.n > 0) min_nrep = std::min(min_nrep, static_cast<int>(fd.nrep));
+    max_bins = std::max(max_bins, bins);
+  }
+  if (min_nrep == INT_MAX) min_nrep = 1;
+  const int code_bytes = max_nb <= 256 ? 1 : 2;
+  const int per_vec = 16 / code_bytes;
+  const int Dp = std::max(per_vec, static_cast<int>(ceil_div(std::max(nrep_max, 1), per_vec)) * per_vec);
+  FS_CUDA(cudaMemcpyAsync(fam_d, fam.data(), fam.size() * sizeof(FamDesc), cudaMemcpyHostToDevice, s));
+  int32_t* rep_orig_d = ar.upload(rep_orig);
+  int32_t* rep_nb_d = ar.upload(rep_nb);
+  int32_t* rep_boff_d = ar.upload(rep_boff);
+  int64_t* rep_src_d = ar.upload(rep_src);
+  double* vals_d = ar.alloc<double>(std::max<int64_t>(total_bins, 1));
+  if (nrep_max > 0) {
+    rep_vals_kernel<<<dim3(static_cast<unsigned>(std::min(nrep_max, 1024)), F), 128, 0, s>>>(
+        fam_d, rep_orig_d, rep_boff_d, rep_nb_d, rep_src_d, vals_all, vals_large, d, vals_d);
+    dev->count_launch();
+  }
+  std::vector<FamState> st0(static_cast<size_t>(F));
+  for (int f = 0; f < F; ++f) {
+    std::memset(&st0[f], 0, sizeof(FamState));
+    st0[f].active = fam[f].n > 0 && fam[f].trees > 0;
+  }
+  FamState* st_d = ar.upload(st0);
+  TreeRec* trees_d = ar.alloc<TreeRec>(std::max<int64_t>(total_tree, 1));
+  double* mse_d = ar.alloc<double>(static_cast<size_t>(F) * std::max(max_trees, 1));
+  double* base_d = ar.alloc<double>(F);
+  FS_CUDA(cudaMemsetAsync(base_d, 0, F * sizeof(double), s));
+
+  if (code_bytes == 1)
+    run_rounds<uint8_t>(dev, ar, F, d, Dp, n_tot, max_trees, depth_max, slots, nrep_max, max_bins, n_max,
+                        level_slots_max, fam_d, st_d, x_d, target_d, codes_all, rep_orig_d, rep_nb_d, rep_boff_d,
+                        vals_d, total_ord, total_bins, total_hist, total_lbuf, total_tree, trees_d, mse_d, base_d,
+                        min_nrep);
+  else
+    run_rounds<uint16_t>(dev, ar, F, d, Dp, n_tot, max_trees, depth_max, slots, nrep_max, max_bins, n_max,
+                         level_slots_max, fam_d, st_d, x_d, target_d, codes_all, rep_orig_d, rep_nb_d, rep_boff_d,
+                         vals_d, total_ord, total_bins, total_hist, total_lbuf, total_tree, trees_d, mse_d, base_d,
+                         min_nrep);
+
+  // ---- results: heap-slot records -> pre-order CostModelState layout ------------------------
+  raise_deferred(dev->take_errors());
+  const auto st_h = download(st_d, static_cast<size_t>(F), s);
+  const auto trees_h = download(trees_d, static_cast<size_t>(std::max<int64_t>(total_tree, 1)), s);
+  const auto mse_h = download(mse_d, static_cast<size_t>(F) * std::max(max_trees, 1), s);
+  const auto base_h = download(base_d, static_cast<size_t>(F), s);
+  for (int f = 0; f < F; ++f) {
+    FamilyModel& m = fo->fams[static_cast<size_t>(f)];
+    const FamDesc& fd = fam[static_cast<size_t>(f)];
+    m.lr = fd.lr;
+    m.base = fd.n > 0 ? base_h[static_cast<size_t>(f)] : 0.0;
+    m.offsets.assign(1, 0);
+    m.feature.clear();
+    m.threshold.clear();
+    m.left.clear();
+    m.right.clear();
+    m.value.clear();
+    m.gain.clear();
+    m.mse.clear();
+    const int T = st_h[static_cast<size_t>(f)].ntrees;
+    for (int t = 0; t < T; ++t) {
+      const TreeRec* rec = trees_h.data() + fd.tree0 + static_cast<int64_t>(t) * slots;
+      const int base_idx = static_cast<int>(m.feature.size());
+      std::function<int(int)> emit = [&](int sl) -> int {
+        const int idx = static_cast<int>(m.feature.size()) - base_idx;
+        const TreeRec& r = rec[sl];
+        m.feature.push_back(r.kind == kNodeSplit ? r.feature : -1);
+        m.threshold.push_back(r.kind == kNodeSplit ? r.threshold : 0.0);
+        m.left.push_back(-1);
+        m.right.push_back(-1);
+        m.value.push_back(r.kind == kNodeSplit ? 0.0 : r.value);
+        m.gain.push_back(r.kind == kNodeSplit ? r.gain : 0.0);
+        if (r.kind == kNodeSplit) {
+          const int l = emit(2 * sl + 1);
+          const int rr = emit(2 * sl + 2);
+          m.left[static_cast<size_t>(base_idx + idx)] = l;
+          m.right[static_cast<size_t>(base_idx + idx)] = rr;
+        } else if (r.kind != kNodeLeaf) {
+          fail(FS_ECUDA, "fit: internal error (missing tree node)");
+        }
+        return idx;
+      };
+      emit(0);
+      m.offsets.push_back(static_cast<int32_t>(m.feature.size()));
+      m.mse.push_back(mse_h[static_cast<size_t>(f) * max_trees + t]);
+    }
+    m.screened = static_cast<int64_t>(st_h[static_cast<size_t>(f)].screened);
+    m.exact = static_cast<int64_t>(st_h[static_cast<size_t>(f)].exact);
+    compile_model(dev, m);
+  }
+}
+
+}  // namespace fit
+}  // namespace fs
 
 extern "C" {
 
-int fs_fit(fs_device*, fs_forest*, int32_t, const int64_t*, int32_t, const double*, const double*,
-           const fs_gbt_params*) {
-  return fs::guard([] { fs::fail(FS_ECUDA, "fs_fit: trainer not built yet"); });
+int fs_fit_d(fs_device* dev, fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d, const double* x_d,
+             const double* target_d, const fs_gbt_params* params) {
+  return fs::guard([&] {
+    if (!dev || !fo || nseg < 0 || !seg || d < 0 || !params) fs::fail(FS_EINVAL, "fs_fit: bad arguments");
+    dev->activate();
+    fs::fit::fit_families(dev, fo, nseg, seg, d, x_d, target_d, params);
+  });
 }
 
-int fs_fit_d(fs_device*, fs_forest*, int32_t, const int64_t*, int32_t, const double*, const double*,
-             const fs_gbt_params*) {
-  return fs::guard([] { fs::fail(FS_ECUDA, "fs_fit_d: trainer not built yet"); });
+int fs_fit(fs_device* dev, fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d, const double* x,
+           const double* target, const fs_gbt_params* params) {
+  return fs::guard([&] {
+    if (!dev || !fo || nseg < 0 || !seg || d < 0 || !params) fs::fail(FS_EINVAL, "fs_fit: bad arguments");
+    dev->activate();
+    const int64_t n = seg[nseg];
+    auto* xd = static_cast<double*>(dev->scratch(fs::kSlotH2D0, std::max<int64_t>(n * d, 1) * sizeof(double)));
+    auto* yd = static_cast<double*>(dev->scratch(fs::kSlotH2D1, std::max<int64_t>(n, 1) * sizeof(double)));
+    if (n * d) FS_CUDA(cudaMemcpyAsync(xd, x, n * d * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    if (n) FS_CUDA(cudaMemcpyAsync(yd, target, n * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    fs::fit::fit_families(dev, fo, nseg, seg, d, xd, yd, params);
+  });
+}
+
+int fs_forest_fit_stats(const fs_forest* fo, int32_t family, int64_t* screened, int64_t* exact) {
+  return fs::guard([&] {
+    if (!fo || family < 0 || family >= static_cast<int32_t>(fo->fams.size()))
+      fs::fail(FS_ERANGE, "fs_forest_fit_stats: unknown family id");
+    const auto& m = fo->fams[static_cast<size_t>(family)];
+    if (screened) *screened = m.screened;
+    if (exact) *exact = m.exact;
+  });
 }
 
 }  // extern "C"

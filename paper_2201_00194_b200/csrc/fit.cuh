@@ -1,0 +1,98 @@
+// Kernel (3): the boosting trainer - fit (costmodel.cpp:152-222) for many families at once.
+//
+// Bit-exact design (SURVEY.md 7 "Hard parts" 1-2 and Appendix A P3-P5):
+//   * every value that reaches a tree - base, node totals, leaf values, predictions - is folded
+//     in the reference's order with separately rounded FP64 adds (chains over the canonical /
+//     feature-0-presorted row order);
+//   * split search is a histogram SCREEN in exact 62-bit fixed point (integer sums: associative,
+//     deterministic, exactly subtractable for the sibling trick), with a rigorous per-candidate
+//     bound on how far the reference's own FP64 gain can sit from the screened one;
+//   * when more than one candidate (or one of uncertain sign) survives the bound, the node is
+//     re-evaluated in the reference's order: one warp per (node, surviving feature) folds the
+//     residuals over that feature's presorted list restricted to the node, exactly as
+//     best_split (costmodel.cpp:42-71) does, and the decision applies its strict-> rule.
+// Features that are constant over a family's training set, or whose code column equals an
+// earlier feature's (same order and ties, e.g. log2(v) and v's list position), are dropped up
+// front: the reference can never pick them (strict > keeps the earlier, identical gain).
+#pragma once
+
+#include "forest.cuh"
+
+namespace fs {
+namespace fit {
+
+constexpr int kMaxDepth = 10;                 // 2047 node slots per tree
+constexpr int kSmallBins = 256;               // hash-path distinct-value limit per feature
+constexpr int kMaxBins = 65535;               // per feature (u16 codes)
+constexpr int kSortThreads = 1024;            // stable counting sort CTA
+constexpr int kNodeLeaf = 1, kNodeSplit = 2, kNodeExact = 3;
+
+// Per-family constants (device array).
+struct FamDesc {
+  int64_t row0;   // first caller row (x/target)
+  int64_t pos0;   // first slot in the per-row canonical arrays
+  int64_t ord0;   // first entry of this family's presorted lists (nrep * n)
+  int64_t bin0;   // first bin of this family in per-bin tables
+  int64_t hist0;  // first bin of this family's histogram ring (2 * level_slots * bins)
+  int64_t node0;  // first node slot of this family in per-node tables
+  int64_t lbuf0;  // first entry of this family's exact-fold buffer (level_slots * bins)
+  int64_t tree0;  // first record of this family's tree table (trees * slots)
+  int32_t n;
+  int32_t nrep;
+  int32_t rep0;   // first entry in per-rep tables
+  int32_t bins;   // total bins over reps
+  int32_t trees;
+  int32_t depth;
+  int32_t min_split;
+  int32_t f0rep;  // rep index of original feature 0, -1 if feature 0 is constant
+  int32_t level_slots;  // 2^(depth-1) (max histogrammed nodes per level), >= 1
+  int32_t pad_;
+  double lr;
+};
+
+// Per-family mutable scalars.
+struct FamState {
+  int32_t active;   // still boosting
+  int32_t ntrees;   // committed trees
+  int32_t shift;    // fixed-point exponent of this round
+  int32_t pad_;
+  uint64_t maxabs;  // bits of max |residual| (non-negative doubles order like integers)
+  unsigned long long screened;  // splits decided by the histogram screen alone
+  unsigned long long exact;     // nodes re-evaluated in reference order
+};
+
+// Per node slot (per family, kSlots = 2^(depth_max+1)-1).
+struct NodeRec {
+  int32_t n;        // rows
+  int32_t seg;      // start of its rows in the order-0 list (family-relative)
+  int32_t state;    // 0 absent/undecided, kNodeLeaf, kNodeSplit, kNodeExact
+  int32_t rep;      // split feature (rep index)
+  int32_t bin;      // split bin (left = code <= bin)
+  int32_t lc;       // left count
+  int32_t wcount;   // screen window candidates
+  int32_t build;    // 1 if its histogram is accumulated directly this level
+  double gain;      // split gain (reference's value)
+  double value;     // leaf value
+  double total;     // exact reference-order node total (exact nodes / leaves)
+  uint64_t lokey;   // max lower bound over candidates (order-preserving key)
+};
+
+// Tree table record (per family, per round, per slot).
+struct TreeRec {
+  int32_t kind;     // 0 absent, kNodeLeaf, kNodeSplit
+  int32_t feature;  // original feature index
+  double threshold;
+  double value;
+  double gain;
+};
+
+// Window bookkeeping per (node, rep): screen lower/upper bound of the feature's best candidate.
+struct WinRec {
+  double best_g;    // screened gain of the feature's best candidate
+  double best_lo;
+  int32_t best_bin;
+  int32_t flag;     // feature has >= 1 candidate in the node's window
+};
+
+}  // namespace fit
+}  // namespace fs

@@ -209,14 +209,4 @@ int fs_forest_export(const fs_forest* fo, int32_t family, double* base, int32_t*
   });
 }
 
-int fs_forest_fit_stats(const fs_forest* fo, int32_t family, int64_t* screened, int64_t* exact) {
-  return fs::guard([&] {
-    if (!fo || family < 0 || family >= static_cast<int32_t>(fo->fams.size()))
-      fs::fail(FS_ERANGE, "fs_forest_fit_stats: unknown family id");
-    const auto& m = fo->fams[static_cast<size_t>(family)];
-    if (screened) *screened = m.screened;
-    if (exact) *exact = m.exact;
-  });
-}
-
 }  // extern "C"
