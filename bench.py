@@ -1,0 +1,620 @@
+#!/usr/bin/env python
+"""bench.py - FamilySeer per-family cost model (BASELINE.json metric) on B200.
+
+A step = one tuning round of the hot path over every family of the workload: score each
+family's candidate pool (featurize -> GBDT predict -> rank, scheduler.cpp:187-192) and refit
+each family's model from scratch on its training rows (train_cost_model/fit,
+costmodel.cpp:152-235). Default workload = BASELINE.json configs[1] (ResNet-50-sim, all core-op
+families, 2048 candidates/family, T=100) at pad_dim 164.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl native|reference]
+
+Prints ONE JSON line (rank 0). value = candidates scored per second over whole rounds (score +
+retrain, inputs resident in HBM); e2e = the same through the host-pointer C ABI (fs_score +
+fs_fit + model export, copies inside the timed region). Under torchrun every rank tunes its own
+family set (weak scaling) and the per-family top-g candidates are all-gathered over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidates scored/sec & GBDT train rows/sec at 1/2/4/8 B200; % HBM roofline"
+PAD = 164
+G_TOP = 64  # tune_step batch g (scheduler.cpp:147-148: min(64, B/n))
+
+CONFIGS = {
+    # name: (model, family filter, candidates per family, trees, description)
+    "c1": ("resnet50_sim", ["conv2d"], 512, 100, "single family (conv2d+ReLU, ResNet-50 subgraphs): 512 candidates x 164 "
+           "features, 100-tree GBDT predict + one retrain round"),
+    "c2": ("resnet50_sim", None, 2048, 100, "ResNet-50 full tuning round: all subgraph families, 2048 candidates/family, "
+           "predict + retrain on 1 B200"),
+    "c3": ("mobilenetv2_sim", None, 2048, 100, "MobileNet-V2 family-parallel tuning (depthwise/pointwise families)"),
+    "c4": ("bert_base_sim", ["dense", "batch_matmul", "softmax"], 16384, 500,
+           "BERT-base subgraph families (dense/batch_matmul/softmax) with 16k-candidate populations and 500-tree models"),
+    "c5": ("synthetic64", None, 65536, 1000, "synthetic stress sweep: 64 families x 65k candidates x 164 features, "
+           "1000-tree GBDT"),
+}
+
+
+# ------------------------------------------------------------------------------------------
+# workload (synthetic: random candidates from the model files' knob spaces, quadratic-bowl
+# latencies in the shape of simbackend.cpp:80-102; no datasets or checkpoints exist offline)
+# ------------------------------------------------------------------------------------------
+def load_spaces(name):
+    with open(os.path.join(ROOT, "data", "spaces", name + ".json")) as f:
+        return json.load(f)
+
+
+def synthetic64(seed):
+    rng = np.random.default_rng(seed)
+    subs = []
+    for s in range(64):
+        knobs = [[2 ** j for j in range(int(rng.integers(4, 9)))] for _ in range(16)]
+        subs.append({"id": s, "core_op": f"syn{s:02d}", "knobs": knobs})
+    return {"name": "synthetic64", "subgraphs": subs, "reference_families": {"core-op": list(range(64))}}
+
+
+def sample_space(rng, knobs, n):
+    sizes = [len(v) for v in knobs]
+    total = int(np.prod(sizes, dtype=np.float64))
+    if n >= total:
+        lin = np.arange(total, dtype=np.int64)
+    elif total < 4 * n:
+        lin = rng.choice(total, size=n, replace=False)
+    else:  # large space: draw with replacement then dedup-topup
+        lin = np.unique(rng.integers(0, total, size=int(n * 1.2) + 16, dtype=np.int64))
+        rng.shuffle(lin)
+        lin = lin[:n]
+    a = np.zeros((len(lin), 16), np.int32)
+    for k in range(len(sizes) - 1, -1, -1):
+        a[:, k] = lin % sizes[k]
+        lin = lin // sizes[k]
+    return a
+
+
+def latency(rng, knobs, a):
+    k = len(knobs)
+    z = np.stack([a[:, i] / max(len(knobs[i]) - 1, 1) for i in range(k)], 1)
+    opt = rng.uniform(0, 1, k)
+    curv = rng.uniform(0.5, 2.0)
+    w = rng.uniform(-0.2 / (k * k), 0.2 / (k * k), (k, k))
+    w = (w + w.T) / 2
+    np.fill_diagonal(w, 0)
+    base = math.exp(rng.uniform(math.log(0.1), math.log(10.0)))
+    lat = base * (1 + curv * ((z - opt) ** 2).sum(1) + np.einsum("ni,ij,nj->n", z, w, z))
+    return lat * np.exp(rng.normal(0, 0.02, len(lat)))
+
+
+def build_workload(cfg_name, seed):
+    model, fam_filter, per_family, trees, desc = CONFIGS[cfg_name]
+    doc = synthetic64(seed) if model == "synthetic64" else load_spaces(model)
+    subs = doc["subgraphs"]
+    fam_of = doc["reference_families"]["core-op"]
+    fams = {}
+    for sid, f in enumerate(fam_of):
+        fams.setdefault(f, []).append(sid)
+    rng = np.random.default_rng(seed)
+    spaces = [s["knobs"] for s in subs]
+    pool_so, pool_a, pool_seg = [], [], [0]
+    tr_so, tr_a, tr_lat, tr_seg = [], [], [], [0]
+    fam_names = []
+    for f in sorted(fams):
+        members = fams[f]
+        name = subs[members[0]]["core_op"]
+        if fam_filter and name not in fam_filter:
+            continue
+        fam_names.append(name)
+        space = sum(int(np.prod([len(v) for v in spaces[s]], dtype=np.float64)) for s in members)
+        p = min(per_family, space)
+        for dst_so, dst_a, dst_seg, with_lat in ((pool_so, pool_a, pool_seg, False), (tr_so, tr_a, tr_seg, True)):
+            share = [p // len(members) + (1 if i < p % len(members) else 0) for i in range(len(members))]
+            # respect small subgraph spaces: redistribute leftovers
+            caps = [int(np.prod([len(v) for v in spaces[s]], dtype=np.float64)) for s in members]
+            share = [min(a, c) for a, c in zip(share, caps)]
+            left = p - sum(share)
+            for i in range(len(members)):
+                if left <= 0:
+                    break
+                add = min(left, caps[i] - share[i])
+                share[i] += add
+                left -= add
+            cnt = 0
+            for sid, n in zip(members, share):
+                if n <= 0:
+                    continue
+                a = sample_space(rng, spaces[sid], n)
+                dst_so.append(np.full(len(a), sid, np.int32))
+                dst_a.append(a)
+                if with_lat:
+                    tr_lat.append(latency(rng, spaces[sid], a))
+                cnt += len(a)
+            dst_seg.append(dst_seg[-1] + cnt)
+    W = {
+        "config": cfg_name, "desc": desc, "model": model, "trees": trees, "per_family": per_family, "spaces": spaces,
+        "families": fam_names,
+        "pool_so": np.concatenate(pool_so), "pool_a": np.concatenate(pool_a), "pool_seg": np.array(pool_seg, np.int64),
+        "tr_so": np.concatenate(tr_so), "tr_a": np.concatenate(tr_a), "tr_seg": np.array(tr_seg, np.int64),
+        "tr_y": np.log(np.concatenate(tr_lat)),
+    }
+    return W
+
+
+# ------------------------------------------------------------------------------------------
+# clocks (sampled during the timed region)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        busy = [s for s in sm if s > 0.5 * max(mx or [1])] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------
+# native arm
+# ------------------------------------------------------------------------------------------
+def run_native(args, rank, world, local_rank):
+    import torch
+
+    import paper_2201_00194_b200 as fs
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    W = build_workload(args.config, seed=1000 + rank)
+    dev = fs.Device(local_rank)
+    stream = torch.cuda.ExternalStream(dev.stream)
+    spaces = fs.Spaces(dev, W["spaces"])
+    F = len(W["families"])
+    forest = fs.Forest(dev, F)
+    params = fs.GbtParams(W["trees"], 3, 0.1, 2)
+    P = int(W["pool_seg"][-1])
+    N = int(W["tr_seg"][-1])
+    with torch.cuda.stream(stream):
+        pool_so = torch.from_numpy(W["pool_so"]).cuda()
+        pool_a = torch.from_numpy(W["pool_a"]).cuda()
+        tr_so = torch.from_numpy(W["tr_so"]).cuda()
+        tr_a = torch.from_numpy(W["tr_a"]).cuda()
+        x_tr = torch.empty((N, PAD), dtype=torch.float64, device="cuda")
+        y_tr = torch.from_numpy(W["tr_y"]).cuda()
+        scores = torch.empty(P, dtype=torch.float64, device="cuda")
+        perm = torch.empty(P, dtype=torch.int32, device="cuda")
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+    stream.synchronize()
+    # training rows are MeasurementRecord features (featurized at measurement time, simbackend.cpp:185)
+    spaces.featurize_d(tr_so, tr_a, PAD, x_tr)
+    forest.fit_d(x_tr, y_tr, W["tr_seg"], params)  # model the first round scores with
+    dev.check()
+    pool_seg, tr_seg = W["pool_seg"], W["tr_seg"]
+    fam_base = rank * F
+
+    def topk_allgather():
+        # per-family top-g records {family, pool index, score}; the only collective (NCCL)
+        idx = []
+        for f in range(F):
+            a, b = int(pool_seg[f]), int(pool_seg[f + 1])
+            k = min(G_TOP, b - a)
+            p = perm[a:a + k].long() + a
+            rec = torch.stack([torch.full((k,), fam_base + f, dtype=torch.float64, device="cuda"),
+                               p.double(), scores[p]], 1)
+            if k < G_TOP:
+                rec = torch.cat([rec, torch.full((G_TOP - k, 3), -1.0, dtype=torch.float64, device="cuda")])
+            idx.append(rec)
+        mine = torch.cat(idx)
+        out = torch.empty((world * mine.shape[0], 3), dtype=torch.float64, device="cuda")
+        dist.all_gather_into_tensor(out, mine)
+        return out
+
+    def step():
+        spaces.score_d(forest, pool_so, pool_a, PAD, pool_seg, scores, perm)
+        if dist is not None:
+            topk_allgather()
+        forest.fit_d(x_tr, y_tr, tr_seg, params)
+
+    def timed(fn, k, flush_between=True):
+        times = []
+        for _ in range(k):
+            if flush_between:
+                with torch.cuda.stream(stream):
+                    flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return times
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        dev.check()
+        # ---- timed region: device-resident value ----
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local_rank)
+        clocks.start()
+        l0 = dev.launches
+        dev.counters(reset=True)
+        dev.profile("predict,featurize,rank,fit_hist_build")
+        times = timed(step, args.steps)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        clock_info = clocks.stop()
+        launches = dev.launches - l0
+        prof = dev.profile_read()
+        ctr = dev.counters(reset=True)
+        dev.profile(None)
+        dev.check()
+        total_ms = sum(times)
+        if dist is not None:
+            t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms = float(t.item())
+        # ---- per-phase breakdown (one profiled step, all kernels) ----
+        dev.profile("*")
+        step()
+        breakdown = {k: round(v[1], 4) for k, v in sorted(dev.profile_read().items(), key=lambda kv: -kv[1][1])}
+        dev.profile(None)
+        score_ms = statistics.median(timed(lambda: spaces.score_d(forest, pool_so, pool_a, PAD, pool_seg, scores, perm),
+                                           max(3, args.steps)))
+        fit_ms = statistics.median(timed(lambda: forest.fit_d(x_tr, y_tr, tr_seg, params), max(2, min(args.steps, 5))))
+        fit_stats = [forest.fit_stats(f) for f in range(F)]
+
+    # ---- e2e: host buffers through the C ABI, copies inside the timed region ----
+    e2e = None
+    if not args.no_e2e:
+        h_so = W["pool_so"]
+        h_a = np.ascontiguousarray(W["pool_a"])
+        h_x = x_tr.cpu().numpy()
+        h_y = W["tr_y"]
+        try:  # pinned host staging, as a production caller would hold it
+            h_x_t = torch.from_numpy(h_x).pin_memory()
+            h_x = h_x_t.numpy()
+        except Exception:
+            pass
+        d2h = [0]
+
+        def e2e_step():
+            s_h, p_h = spaces.score(forest, h_so, h_a, PAD, pool_seg)
+            forest.fit(h_x, h_y, seg=tr_seg, params=params)
+            nbytes = s_h.nbytes + p_h.nbytes
+            for f in range(F):
+                e = forest.export(f)
+                nbytes += sum(getattr(e, k).nbytes for k in ("offsets", "feature", "threshold", "left", "right",
+                                                              "value", "gain", "mse"))
+            d2h[0] = nbytes
+
+        with torch.cuda.stream(stream):
+            for _ in range(max(1, args.warmup // 2)):
+                e2e_step()
+            if dist is not None:
+                dist.barrier()
+            e_times = timed(e2e_step, args.steps)
+        e_total = sum(e_times)
+        if dist is not None:
+            t = torch.tensor([e_total], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_total = float(t.item())
+        h2d = h_so.nbytes + h_a.nbytes + h_x.nbytes + h_y.nbytes
+        e2e = {"value": P * world * args.steps / (e_total / 1e3), "unit": "candidates/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
+               "train_rows_per_s": N * world * args.steps / (e_total / 1e3), "ms_per_step": e_total / args.steps,
+               "api": "fs_score + fs_fit + fs_forest_export (host pointers)"}
+
+    # ---- roofline of the dominant HBM kernel ----
+    peak, peak_kind = measured_peak_hbm()
+    roof_candidates = []
+    if "fit_hist_build" in prof and ctr["hist_bytes"]:
+        n_l, ms = prof["fit_hist_build"]
+        roof_candidates.append(("fit_hist_build", ms, ctr["hist_bytes"], n_l,
+                                "rows*(nrep*code_bytes + 8 residual + 4 index), rows counted on device"))
+    if "predict" in prof:
+        n_l, ms = prof["predict"]
+        roof_candidates.append(("predict", ms, args.steps * P * (8 * PAD + 8), n_l, "P*(8*d + 8)"))
+    if "featurize" in prof:
+        n_l, ms = prof["featurize"]
+        roof_candidates.append(("featurize", ms, args.steps * P * (4 * 16 + 4 + 8 * PAD), n_l, "P*(64 + 4 + 8*pad)"))
+    roofline = None
+    if roof_candidates:
+        name, ms, nbytes, n_l, formula = max(roof_candidates, key=lambda r: r[1])
+        ach = nbytes / (ms / 1e3) / 1e9
+        tr = ncu_traffic(name)
+        roofline = {"bound": "hbm", "kernel": name, "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 5), "peak_kind": peak_kind, "traffic": tr,
+                    "algorithmic_bytes_per_launch": nbytes / max(n_l, 1), "launches": n_l,
+                    "avg_launch_ms": ms / max(n_l, 1), "bytes_formula": formula,
+                    "other_kernels": {r[0]: {"ms": round(r[1], 4), "achieved_gbs": round(r[2] / (r[1] / 1e3) / 1e9, 2)}
+                                      for r in roof_candidates if r[0] != name}}
+
+    result = {
+        "metric": METRIC,
+        "value": P * world * args.steps / (total_ms / 1e3),
+        "unit": "candidates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (random candidates from the model's knob spaces, quadratic-bowl latencies)",
+        "config": {"workload": W["desc"], "config": args.config, "model": W["model"], "families": W["families"],
+                   "candidates_per_step": P * world, "train_rows_per_step": N * world, "trees": W["trees"],
+                   "depth": 3, "pad_dim": PAD, "parallelism": f"family-sharded x{world}",
+                   "l2": "flushed between timed steps (256 MB write)"},
+        "train_rows_per_s": N * world * args.steps / (total_ms / 1e3),
+        "train_row_rounds_per_s": N * world * W["trees"] * args.steps / (total_ms / 1e3),
+        "phases_ms": {"score": score_ms, "fit": fit_ms},
+        "scored_per_s_score_only": P * world / (score_ms / 1e3),
+        "fit_rows_per_s_fit_only": N * world / (fit_ms / 1e3),
+        "fit_nodes": {"screened": int(sum(a for a, _ in fit_stats)), "exact": int(sum(b for _, b in fit_stats))},
+        "kernel_ms_one_step": breakdown,
+        "device_counters": ctr,
+        "gpu_launches": int(launches),
+        "clocks": clock_info,
+        "roofline": roofline,
+        "e2e": e2e,
+    }
+    if rank == 0 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(W, forest, x_tr.cpu().numpy(), min_seconds=args.cpu_seconds)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+# ------------------------------------------------------------------------------------------
+# reference CPU arm (oracle/_ref = the unmodified reference core; test/baseline infrastructure)
+# ------------------------------------------------------------------------------------------
+def _ref_round(W, x_tr, models, threads, fams=None):
+    """One round of the reference hot path on host cores: per family featurize+predict+sort of the
+    pool and fit on the training rows, one std::thread-equivalent per family (ctypes drops the GIL)."""
+    import oracle
+
+    r = oracle.ref()
+    F = len(W["families"])
+    fams = list(range(F)) if fams is None else fams
+    pool_so, pool_a, pool_seg = W["pool_so"], W["pool_a"], W["pool_seg"]
+    tr_seg, y = W["tr_seg"], W["tr_y"]
+    out = {}
+
+    def work(f):
+        a, b = int(pool_seg[f]), int(pool_seg[f + 1])
+        x = np.zeros((b - a, PAD))
+        for sid in np.unique(pool_so[a:b]):
+            rows = np.where(pool_so[a:b] == sid)[0]
+            kn = W["spaces"][sid]
+            x[rows] = r.featurize(kn, pool_a[a:b][rows][:, : len(kn)], PAD)
+        s = models[f].predict(x)
+        perm = r.rank(s)
+        ta, tb = int(tr_seg[f]), int(tr_seg[f + 1])
+        m = r.new_model(f, W["trees"])
+        m.add_samples(x_tr[ta:tb], y[ta:tb])
+        m.fit()
+        out[f] = (perm[:G_TOP], m)
+
+    pending = list(fams)
+    lock = threading.Lock()
+
+    def runner():
+        while True:
+            with lock:
+                if not pending:
+                    return
+                f = pending.pop(0)
+            work(f)
+
+    ts = [threading.Thread(target=runner) for _ in range(max(1, min(threads, len(fams))))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return out
+
+
+def _ref_models(W, forest, x_tr, threads):
+    import oracle
+
+    r = oracle.ref()
+    models = []
+    for f in range(len(W["families"])):
+        m = r.new_model(f, W["trees"])
+        if forest is not None:
+            e = forest.export(f)
+            m.load(oracle.Ensemble(e.base, e.lr, e.offsets, e.feature, e.threshold, e.left, e.right, e.value))
+        else:
+            ta, tb = int(W["tr_seg"][f]), int(W["tr_seg"][f + 1])
+            m.add_samples(x_tr[ta:tb], W["tr_y"][ta:tb])
+            m.fit()
+        models.append(m)
+    return models
+
+
+def cpu_baseline(W, forest, x_tr, min_seconds=10.0):
+    threads = os.cpu_count() or 1
+    models = _ref_models(W, forest, x_tr, threads)
+    P = int(W["pool_seg"][-1])
+    rounds, t0 = 0, time.perf_counter()
+    while True:
+        _ref_round(W, x_tr, models, threads)
+        rounds += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or rounds >= 50:
+            break
+    cpu = _cpu_model()
+    return {"value": P * rounds / el, "unit": "candidates/s", "cores": min(threads, len(W["families"])),
+            "kind": "reference", "sample": f"{rounds} full round(s) of the workload ({P} candidates scored + "
+            f"{int(W['tr_seg'][-1])} rows refit, T={W['trees']}), one thread per family, oracle/_ref = unmodified "
+            f"reference core (-O3, no -march)", "seconds": el, "host_cpu": cpu, "nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _featurize_host(W, orc):
+    parts = []
+    for i in range(len(W["tr_seg"]) - 1):
+        a, b = int(W["tr_seg"][i]), int(W["tr_seg"][i + 1])
+        x = np.zeros((b - a, PAD))
+        for sid in np.unique(W["tr_so"][a:b]):
+            rows = np.where(W["tr_so"][a:b] == sid)[0]
+            kn = W["spaces"][sid]
+            x[rows] = orc.featurize(kn, W["tr_a"][a:b][rows][:, : len(kn)], PAD)
+        parts.append(x)
+    return np.concatenate(parts)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import oracle
+
+    try:
+        oracle.ref()
+    except Exception as e:  # pragma: no cover
+        return {"impl": "reference", "unavailable": f"compiled reference missing: {e}"}
+    W = build_workload(args.config, seed=1000)
+    x_tr = _featurize_host(W, oracle.orc())
+    threads = os.cpu_count() or 1
+    models = _ref_models(W, None, x_tr, threads)
+    P, N, F = int(W["pool_seg"][-1]), int(W["tr_seg"][-1]), len(W["families"])
+    for _ in range(args.warmup):
+        _ref_round(W, x_tr, models, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _ref_round(W, x_tr, models, threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    v = P * args.steps / total
+    cores = min(threads, F)
+    return {"metric": METRIC, "impl": "reference", "value": v, "unit": "candidates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same generator and seed as the native arm's rank 0)",
+            "config": {"workload": W["desc"], "config": args.config, "model": W["model"], "families": W["families"],
+                       "candidates_per_step": P, "train_rows_per_step": N, "trees": W["trees"], "pad_dim": PAD},
+            "train_rows_per_s": N * args.steps / total,
+            "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": cores, "kind": "reference",
+                             "sample": "full rounds of the workload, one thread per family (oracle/_ref)",
+                             "host_cpu": _cpu_model(), "nproc": os.cpu_count()},
+            "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_native(args, rank, world, local_rank)
+    if rank == 0 and res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

@@ -70,6 +70,15 @@ void* fs_device_stream(fs_device* dev);
 int fs_device_check(fs_device* dev);
 /* Kernels launched by this device since creation (evidence counter for bench.py). */
 int64_t fs_device_launches(const fs_device* dev);
+/* Device-side work counters since the last reset: [0] histogram algorithmic bytes, [1]
+ * histogram rows, [2] reference-order folds, [3] nodes re-evaluated in reference order. */
+int fs_device_counters(fs_device* dev, int64_t* out, int32_t n, int32_t reset);
+/* Per-kernel CUDA-event timing on the device's stream. `kernels` is a comma-separated list of
+ * kernel names ("*" = all, NULL/"" = off); enabling resets the accumulators. */
+int fs_device_profile(fs_device* dev, const char* kernels);
+int fs_device_profile_read(fs_device* dev, const char* kernel, int64_t* count, double* total_ms);
+/* Comma-separated names seen so far (two-call size query; returns bytes needed incl. NUL). */
+int64_t fs_device_profile_names(fs_device* dev, char* buf, int64_t cap);
 
 /* ---- knob spaces + featurize (searchspace.cpp:90-118, feature_dim :86-88) -------------------
  * n_knobs[s] in [1,16]; n_values[s*16+k] = |values| of knob k; values concatenated space by
@@ -120,6 +129,17 @@ int fs_rank(fs_device* dev, int32_t n_segments, const int64_t* seg, const double
             int32_t* perm);
 int fs_rank_d(fs_device* dev, int32_t n_segments, const int64_t* seg_h, const double* scores_d,
               int32_t* perm_d);
+
+/* ---- score: the batched tune_step scoring block (scheduler.cpp:187-192) ---------------------
+ * featurize -> predict -> rank in one call; the feature matrix never leaves the device.
+ * scores[i] and perm[seg[f] + k] as for fs_predict / fs_rank. Either output may be NULL on the
+ * host-pointer variant. */
+int fs_score(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t n_segments,
+             const int64_t* seg, const int32_t* space_of, const int32_t* assign, int32_t pad_dim,
+             double* scores, int32_t* perm);
+int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t n_segments,
+               const int64_t* seg_h, const int32_t* space_of_d, const int32_t* assign_d,
+               int32_t pad_dim, double* scores_d, int32_t* perm_d);
 
 /* ---- fit (costmodel.cpp:152-222; train_cost_model :224-235 appends log-latency rows first) ---
  * Refit family f's ensemble from scratch on rows [seg[f], seg[f+1]) of x/target with params[f].

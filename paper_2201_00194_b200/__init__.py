@@ -124,6 +124,29 @@ class Device:
     def launches(self) -> int:
         return int(_lib().fs_device_launches(self.h))
 
+    def counters(self, reset: bool = True) -> dict[str, int]:
+        """Device work counters: histogram algorithmic bytes/rows, reference-order folds/nodes."""
+        out = np.zeros(4, np.int64)
+        _check(_lib().fs_device_counters(self.h, _p(out, _capi._i64p), 4, int(reset)))
+        return dict(zip(("hist_bytes", "hist_rows", "exact_chains", "exact_nodes"), (int(v) for v in out)))
+
+    # -- per-kernel CUDA-event timing ------------------------------------------------------------
+    def profile(self, kernels: str | None):
+        """Enable event timing for a comma-separated kernel list ("*" = all, None = off)."""
+        _check(_lib().fs_device_profile(self.h, kernels.encode() if kernels else None))
+
+    def profile_read(self) -> dict[str, tuple[int, float]]:
+        L = _lib()
+        need = L.fs_device_profile_names(self.h, None, 0)
+        buf = C.create_string_buffer(max(int(need), 1))
+        L.fs_device_profile_names(self.h, buf, need)
+        out = {}
+        for name in filter(None, buf.value.decode().split(",")):
+            cnt, ms = C.c_int64(), C.c_double()
+            _check(L.fs_device_profile_read(self.h, name.encode(), C.byref(cnt), C.byref(ms)))
+            out[name] = (cnt.value, ms.value)
+        return out
+
     # -- ranking (scheduler.cpp:187-192) --------------------------------------------------------
     def rank(self, scores, seg=None):
         s = np.ascontiguousarray(scores, np.float64)
@@ -189,6 +212,23 @@ class Spaces:
     def featurize_d(self, space_of_t, assign_t, pad_dim: int, out_t):
         _check(_lib().fs_featurize_d(self.dev.h, self.h, space_of_t.numel(), space_of_t.data_ptr(),
                                      assign_t.data_ptr(), pad_dim, out_t.data_ptr()))
+
+    def score(self, forest: "Forest", space_of, assign, pad_dim: int, seg):
+        """tune_step's scoring block (scheduler.cpp:187-192): featurize -> predict -> rank, host
+        buffers in and out. Returns (scores, perm) with perm segment-local."""
+        so = np.ascontiguousarray(space_of, np.int32)
+        a = np.ascontiguousarray(assign, np.int32)
+        sg, sp = _seg(seg)
+        scores = np.zeros(len(so))
+        perm = np.zeros(len(so), np.int32)
+        _check(_lib().fs_score(self.dev.h, self.h, forest.h, len(sg) - 1, sp, _p(so, _capi._i32p),
+                               _p(a, _capi._i32p), pad_dim, _p(scores, _capi._dp), _p(perm, _capi._i32p)))
+        return scores, perm
+
+    def score_d(self, forest: "Forest", space_of_t, assign_t, pad_dim: int, seg, scores_t, perm_t):
+        sg, sp = _seg(seg)
+        _check(_lib().fs_score_d(self.dev.h, self.h, forest.h, len(sg) - 1, sp, space_of_t.data_ptr(),
+                                 assign_t.data_ptr(), pad_dim, scores_t.data_ptr(), perm_t.data_ptr()))
 
 
 class Forest:

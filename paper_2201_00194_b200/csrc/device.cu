@@ -37,6 +37,53 @@ void* fs_device::scratch(int slot, size_t bytes) {
   return b.p;
 }
 
+bool fs_device::prof_wants(const char* name) const {
+  if (prof_filter.empty()) return false;
+  if (prof_filter == "*") return true;
+  const std::string n(name);
+  size_t pos = 0;
+  while (pos <= prof_filter.size()) {
+    const size_t e = prof_filter.find(',', pos);
+    const std::string tok = prof_filter.substr(pos, e == std::string::npos ? std::string::npos : e - pos);
+    if (tok == n) return true;
+    if (e == std::string::npos) break;
+    pos = e + 1;
+  }
+  return false;
+}
+
+cudaEvent_t fs_device::prof_event() {
+  if (!prof_pool.empty()) {
+    cudaEvent_t e = prof_pool.back();
+    prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  FS_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void fs_device::prof_resolve() {
+  if (prof_pending.empty()) return;
+  FS_CUDA(cudaStreamSynchronize(stream));
+  for (auto& pe : prof_pending) {
+    float ms = 0.f;
+    FS_CUDA(cudaEventElapsedTime(&ms, pe.a, pe.b));
+    bool found = false;
+    for (auto& kv : prof_acc)
+      if (kv.first == pe.name) {
+        kv.second.first += 1;
+        kv.second.second += ms;
+        found = true;
+        break;
+      }
+    if (!found) prof_acc.push_back({pe.name, {1, static_cast<double>(ms)}});
+    prof_pool.push_back(pe.a);
+    prof_pool.push_back(pe.b);
+  }
+  prof_pending.clear();
+}
+
 uint32_t fs_device::take_errors() {
   FS_CUDA(cudaMemcpyAsync(err_h, err_d, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
   FS_CUDA(cudaStreamSynchronize(stream));
@@ -71,6 +118,8 @@ int fs_device_create(int ordinal, fs_device** out) {
       FS_CUDA(cudaStreamCreateWithFlags(&d->own, cudaStreamNonBlocking));
       d->stream = d->own;
       FS_CUDA(cudaMalloc(&d->err_d, sizeof(uint32_t)));
+      FS_CUDA(cudaMalloc(&d->ctr_d, fs::kCtrCount * sizeof(unsigned long long)));
+      FS_CUDA(cudaMemsetAsync(d->ctr_d, 0, fs::kCtrCount * sizeof(unsigned long long), d->stream));
       FS_CUDA(cudaMemsetAsync(d->err_d, 0, sizeof(uint32_t), d->stream));
       FS_CUDA(cudaMallocHost(&d->err_h, sizeof(uint32_t)));
       FS_CUDA(cudaStreamSynchronize(d->stream));
@@ -91,6 +140,7 @@ int fs_device_destroy(fs_device* d) {
       if (b.p) cudaFreeAsync(b.p, d->stream);
     cudaStreamSynchronize(d->stream);
     if (d->err_d) cudaFree(d->err_d);
+    if (d->ctr_d) cudaFree(d->ctr_d);
     if (d->err_h) cudaFreeHost(d->err_h);
     if (d->own) cudaStreamDestroy(d->own);
     delete d;
@@ -119,6 +169,63 @@ int fs_device_check(fs_device* d) {
 }
 
 int64_t fs_device_launches(const fs_device* d) { return d ? d->launches : 0; }
+
+int fs_device_counters(fs_device* d, int64_t* out, int32_t n, int32_t reset) {
+  return fs::guard([&] {
+    if (!d || (n > 0 && !out)) fs::fail(FS_EINVAL, "fs_device_counters: bad arguments");
+    d->activate();
+    unsigned long long h[fs::kCtrCount] = {};
+    FS_CUDA(cudaMemcpyAsync(h, d->ctr_d, sizeof h, cudaMemcpyDeviceToHost, d->stream));
+    FS_CUDA(cudaStreamSynchronize(d->stream));
+    for (int i = 0; i < n && i < fs::kCtrCount; ++i) out[i] = static_cast<int64_t>(h[i]);
+    if (reset) FS_CUDA(cudaMemsetAsync(d->ctr_d, 0, sizeof h, d->stream));
+  });
+}
+
+int fs_device_profile(fs_device* d, const char* kernels) {
+  return fs::guard([&] {
+    if (!d) fs::fail(FS_EINVAL, "fs_device_profile: NULL device");
+    d->activate();
+    d->prof_resolve();
+    d->prof_acc.clear();
+    d->prof_filter = kernels ? kernels : "";
+  });
+}
+
+int fs_device_profile_read(fs_device* d, const char* kernel, int64_t* count, double* total_ms) {
+  return fs::guard([&] {
+    if (!d || !kernel) fs::fail(FS_EINVAL, "fs_device_profile_read: bad arguments");
+    d->activate();
+    d->prof_resolve();
+    if (count) *count = 0;
+    if (total_ms) *total_ms = 0.0;
+    for (const auto& kv : d->prof_acc)
+      if (kv.first == kernel) {
+        if (count) *count = kv.second.first;
+        if (total_ms) *total_ms = kv.second.second;
+      }
+  });
+}
+
+int64_t fs_device_profile_names(fs_device* d, char* buf, int64_t cap) {
+  if (!d) return -1;
+  try {
+    d->prof_resolve();
+  } catch (...) {
+    return -1;
+  }
+  std::string s;
+  for (const auto& kv : d->prof_acc) {
+    if (!s.empty()) s += ',';
+    s += kv.first;
+  }
+  if (buf && cap > 0) {
+    const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(s.size()));
+    std::memcpy(buf, s.data(), static_cast<size_t>(n));
+    buf[n] = '\0';
+  }
+  return static_cast<int64_t>(s.size()) + 1;
+}
 
 int fs_feature_dim(int32_t k) { return 2 * k + k * (k - 1) / 2; }
 

@@ -118,6 +118,7 @@ void launch_featurize(fs_device* dev, const fs_spaces* sp, int64_t n, const int3
   const int block = 256;
   const int64_t want = ceil_div(n, block / 32);
   const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(dev->sm_count) * 8));
+  ProfScope prof(dev, "featurize");
   featurize_kernel<<<grid, block, 0, dev->stream>>>(space_of_d, assign_d, n, pad, sp->n, sp->k_d, sp->nval_d,
                                                      sp->off_d, sp->log_d, sp->pos_d, out_d, dev->err_d);
   dev->count_launch();

@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_build_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
     int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
     const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
-    int64_t* __restrict__ node_abs, int groups) {
+    int64_t* __restrict__ node_abs, int groups, unsigned long long* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
@@ -719,6 +719,11 @@ __global__ void __launch_bounds__(kHistThreads) hist_build_kernel(
   }
   if (tid == 0 && s_abs)
     atomicAdd(reinterpret_cast<unsigned long long*>(node_abs + fd.node0 + s), s_abs);
+  if (tid == 0) {
+    atomicAdd(ctr + kCtrHistBytes,
+              static_cast<unsigned long long>(rows) * (static_cast<unsigned long long>(nrep) * sizeof(CodeT) + 12ull));
+    atomicAdd(ctr + kCtrHistRows, static_cast<unsigned long long>(rows));
+  }
 }
 
 // sibling = parent - built child (exact: integer histograms)
@@ -853,7 +858,8 @@ struct ExactItem {
 __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                               NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
                               const int32_t* __restrict__ rep_boff, const WinRec* __restrict__ win, int nrep_max,
-                              int level_slots_max, ExactItem* __restrict__ items, int* __restrict__ n_items) {
+                              int level_slots_max, ExactItem* __restrict__ items, int* __restrict__ n_items,
+                              unsigned long long* __restrict__ ctr) {
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
@@ -891,6 +897,8 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
   int k = 1;
   for (int jj = 0; jj < fd.nrep; ++jj) k += w[jj].flag;
   const int base = atomicAdd(n_items, k);
+  atomicAdd(ctr + kCtrExactChains, static_cast<unsigned long long>(k));
+  atomicAdd(ctr + kCtrExactNodes, 1ull);
   items[base] = {f, static_cast<int16_t>(s), static_cast<int16_t>(-1)};
   int o = 1;
   for (int jj = 0; jj < fd.nrep; ++jj)
@@ -1254,14 +1262,20 @@ void run_rounds(fs_device* dev, Arena& ar, int F, int d, int Dp, int64_t n_tot, 
   // ---- prep: canonical order, gather, presorts, bin counts, base -------------------------
   int32_t* canon = ar.alloc<int32_t>(n_tot);
   int32_t* tmp = ar.alloc<int32_t>(std::max<int64_t>(n_tot, total_ord));
-  canonical_kernel<<<F, kSortThreads, 0, s>>>(target_d, codes_all, d, fam_d, rep_orig_d, rep_nb_d, canon, tmp);
+  {
+    ProfScope prof(dev, "fit_canonical");
+    canonical_kernel<<<F, kSortThreads, 0, s>>>(target_d, codes_all, d, fam_d, rep_orig_d, rep_nb_d, canon, tmp);
+  }
   CodeT* codes_c = ar.alloc<CodeT>(static_cast<size_t>(n_tot) * Dp);
   double* target_c = ar.alloc<double>(n_tot);
   int32_t* rowfam = ar.alloc<int32_t>(n_tot);
   gather_canonical_kernel<CodeT><<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(
       target_d, codes_all, d, fam_d, F, n_tot, rep_orig_d, canon, Dp, codes_c, target_c, rowfam);
   int32_t* ord = ar.alloc<int32_t>(total_ord);
-  if (nrep_max > 0) presort_kernel<CodeT><<<dim3(nrep_max, F), kSortThreads, 0, s>>>(fam_d, Dp, codes_c, rep_nb_d, ord, tmp);
+  if (nrep_max > 0) {
+    ProfScope prof(dev, "fit_presort");
+    presort_kernel<CodeT><<<dim3(nrep_max, F), kSortThreads, 0, s>>>(fam_d, Dp, codes_c, rep_nb_d, ord, tmp);
+  }
   int32_t* cle = ar.alloc<int32_t>(total_bins);
   FS_CUDA(cudaMemsetAsync(cle, 0, std::max<int64_t>(total_bins, 1) * sizeof(int32_t), s));
   bin_count_kernel<CodeT><<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, F, n_tot, Dp, codes_c, rowfam, rep_boff_d, cle);
@@ -1322,36 +1336,52 @@ void run_rounds(fs_device* dev, Arena& ar, int F, int d, int Dp, int64_t n_tot, 
       hist_zero_kernel<<<dim3(grid1(static_cast<int64_t>(lw) * max_bins, 256, 64), F), 256, 0, s>>>(fam_d, st_d, level,
                                                                                                   hsum, hcnt);
       const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
-      if (hist_global)
-        hist_build_kernel<CodeT, true><<<dim3(chunks, pairs, F), kHistThreads, hist_smem, s>>>(
-            fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, 1);
-      else
-        hist_build_kernel<CodeT, false><<<dim3(chunks, pairs, F), kHistThreads, hist_smem, s>>>(
-            fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, groups);
+      {
+        ProfScope prof(dev, "fit_hist_build");
+        if (hist_global)
+          hist_build_kernel<CodeT, true><<<dim3(chunks, pairs, F), kHistThreads, hist_smem, s>>>(
+              fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, 1, dev->ctr_d);
+        else
+          hist_build_kernel<CodeT, false><<<dim3(chunks, pairs, F), kHistThreads, hist_smem, s>>>(
+              fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, groups,
+              dev->ctr_d);
+      }
       hist_derive_kernel<<<dim3(grid1(max_bins, 256, 16), pairs, F), 256, 0, s>>>(fam_d, st_d, nodes, level, hsum,
                                                                                   hcnt, node_abs);
       const dim3 sg(grid1(nrep_max, 128, 1 << 20), lw, F);
-      screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
-                                        std::max(nrep_max, 1), level_slots_max, 0);
-      screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
-                                        std::max(nrep_max, 1), level_slots_max, 1);
+      {
+        ProfScope prof(dev, "fit_screen");
+        screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
+                                          std::max(nrep_max, 1), level_slots_max, 0);
+        screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
+                                          std::max(nrep_max, 1), level_slots_max, 1);
+      }
       FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
       decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
                                                                      std::max(nrep_max, 1), level_slots_max, items,
-                                                                     n_items);
-      exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord,
-                                                 ord_cur, nodeid, rep_boff_d, lbuf);
+                                                                     n_items, dev->ctr_d);
+      {
+        ProfScope prof(dev, "fit_exact");
+        exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord,
+                                                   ord_cur, nodeid, rep_boff_d, lbuf);
+      }
       exact_decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt,
                                                                            rep_boff_d, rep_nb_d, win,
                                                                            std::max(nrep_max, 1), level_slots_max, lbuf);
-      partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur, scratch,
-                                                            nodeid, rep_orig_d, rep_boff_d, vals_d, cle, ord, canon,
-                                                            x_d, d, trees_d, slots);
+      {
+        ProfScope prof(dev, "fit_partition");
+        partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
+                                                              scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle, ord,
+                                                              canon, x_d, d, trees_d, slots);
+      }
       dev->count_launch(10);
     }
     const int64_t leaf_threads = static_cast<int64_t>(F) * slots * 32;
-    leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
-                                                                                     ord_cur, resid, pred, trees_d);
+    {
+      ProfScope prof(dev, "fit_leaf");
+      leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
+                                                                                       ord_cur, resid, pred, trees_d);
+    }
     commit_mse_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred, mse_d, max_trees);
     dev->count_launch(2);
     FS_CUDA(cudaGetLastError());
@@ -1408,6 +1438,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     const size_t smem = 32 * kHashSlots * 8 + 32 * kSmallBins * 8 + 32 * 4 * 2 + 32 * 8;
     FS_CUDA(cudaFuncSetAttribute(distinct_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
+    ProfScope prof(dev, "fit_distinct");
     distinct_small_kernel<<<dim3(static_cast<unsigned>(ceil_div(d, 32)), F), 256, smem, s>>>(
         x_d, d, fam_d, codes_all, vals_all, nb_all, hash_all, dev->err_d);
     dev->count_launch();
@@ -1529,6 +1560,8 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   double* base_d = ar.alloc<double>(F);
   FS_CUDA(cudaMemsetAsync(base_d, 0, F * sizeof(double), s));
 
+  {
+  ProfScope prof_rounds(dev, "fit_rounds");
   if (code_bytes == 1)
     run_rounds<uint8_t>(dev, ar, F, d, Dp, n_tot, max_trees, depth_max, slots, nrep_max, max_bins, n_max,
                         level_slots_max, fam_d, st_d, x_d, target_d, codes_all, rep_orig_d, rep_nb_d, rep_boff_d,
@@ -1539,6 +1572,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
                          level_slots_max, fam_d, st_d, x_d, target_d, codes_all, rep_orig_d, rep_nb_d, rep_boff_d,
                          vals_d, total_ord, total_bins, total_hist, total_lbuf, total_tree, trees_d, mse_d, base_d,
                          min_nrep);
+  }
 
   // ---- results: heap-slot records -> pre-order CostModelState layout ------------------------
   raise_deferred(dev->take_errors());

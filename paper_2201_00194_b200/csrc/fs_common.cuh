@@ -60,6 +60,15 @@ enum ErrBits : uint32_t {
   kErrInternal = 1u << 5,          // trainer invariant violated (must never fire)
 };
 
+// Device work counters (algorithmic traffic the host cannot know in advance).
+enum Counter : int {
+  kCtrHistBytes = 0,  // histogram build: rows * (nrep * code bytes + 8 residual + 4 list index)
+  kCtrHistRows,       // rows histogrammed
+  kCtrExactChains,    // reference-order folds run (node totals + feature scans)
+  kCtrExactNodes,     // nodes re-evaluated in reference order
+  kCtrCount
+};
+
 // Grows-only stream-ordered device buffer.
 struct DevBuf {
   void* p = nullptr;
@@ -74,15 +83,52 @@ struct fs_device {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   uint32_t* err_d = nullptr;     // device error word
+  unsigned long long* ctr_d = nullptr;  // device work counters (fs_device_counters)
   uint32_t* err_h = nullptr;     // pinned mirror
   int64_t launches = 0;
   std::vector<fs::DevBuf> slots;  // scratch, indexed by purpose
+
+  // Optional per-kernel CUDA-event timing (fs_device_profile): event pairs recorded on the
+  // launching stream around the kernels whose names are enabled, resolved on read.
+  std::string prof_filter;  // comma-separated kernel names, "*" = all, empty = off
+  struct ProfEvent {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfEvent> prof_pending;
+  std::vector<cudaEvent_t> prof_pool;
+  std::vector<std::pair<std::string, std::pair<int64_t, double>>> prof_acc;  // name -> (count, ms)
 
   void* scratch(int slot, size_t bytes);  // stream-ordered grow; contents undefined
   void count_launch(int n = 1) { launches += n; }
   void activate() const;                  // cudaSetDevice(ordinal)
   uint32_t take_errors();                 // sync + read and clear the error word
+  bool prof_wants(const char* name) const;
+  cudaEvent_t prof_event();
+  void prof_resolve();
 };
+
+namespace fs {
+// Scoped timer: `{ ProfScope p(dev, "hist_build"); kernel<<<...>>>(...); }`
+struct ProfScope {
+  fs_device* dev;
+  const char* name;
+  cudaEvent_t a = nullptr;
+  ProfScope(fs_device* d, const char* n) : dev(d), name(n) {
+    if (dev->prof_wants(name)) {
+      a = dev->prof_event();
+      cudaEventRecord(a, dev->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = dev->prof_event();
+      cudaEventRecord(b, dev->stream);
+      dev->prof_pending.push_back({name, a, b});
+    }
+  }
+};
+}  // namespace fs
 
 namespace fs {
 
@@ -97,6 +143,9 @@ enum Slot : int {
   kSlotRankKeys2,
   kSlotRankIdx2,
   kSlotPredictSeg,
+  kSlotScoreX,
+  kSlotScoreS,
+  kSlotScoreP,
   kSlotCount
 };
 

@@ -136,6 +136,7 @@ void launch_heap(fs_device* dev, const fs::FamilyModel& m, const double* x, int6
   if (smem > 227 * 1024) fs::fail(FS_EINVAL, "predict: model too wide for the shared-memory tile");
   FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(fs::ceil_div(rows, kTile));
+  fs::ProfScope prof(dev, "predict");
   fn<<<grid, kTile, smem, dev->stream>>>(x, rows, d, std::min(m.d_model, d), m.depth, m.n_trees, m.base, m.lr,
                                          m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, scores, leaf_out,
                                          dev->err_d);

@@ -169,6 +169,7 @@ void launch_rank(fs_device* dev, int32_t nseg, const int64_t* seg_h, const doubl
   FS_CUDA(cudaMemcpyAsync(seg_d, seg_h, seg_bytes, cudaMemcpyHostToDevice, dev->stream));
   FS_CUDA(cudaMemcpyAsync(ch_d, chunks.data(), ch_bytes, cudaMemcpyHostToDevice, dev->stream));
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), dev->sm_count * 16));
+  ProfScope prof(dev, "rank");
   make_keys_kernel<<<grid, 256, 0, dev->stream>>>(scores_d, seg_d, nseg, n, ka, ia);
   chunk_sort_kernel<<<static_cast<int>(chunks.size()), kSortThreads, 0, dev->stream>>>(ch_d, ka, ia);
   dev->count_launch(2);
