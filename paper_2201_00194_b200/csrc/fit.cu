@@ -1210,6 +1210,606 @@ __global__ void commit_mse_kernel(const FamDesc* __restrict__ fam, FamState* __r
 }  // namespace fs
 
 // ==========================================================================================
+// resident trainer: one CTA per family runs EVERY boosting round of the fit in a single launch,
+// with all per-row state in shared memory. For families of up to a few thousand rows (configs
+// C1-C3) the multi-kernel round above is launch- and L2-latency-bound (~40 launches per round);
+// here a round is ~30 block barriers. Same algorithm, same arithmetic, same tie handling.
+// ==========================================================================================
+namespace fs {
+namespace fit {
+namespace {
+
+constexpr int kResThreads = 1024;
+constexpr int kResMaxDepth = 7;  // node ids fit in uint8
+
+struct ResNode {
+  int32_t n, seg, state, rep, bin, lc, wcount, build;
+  double gain, value, total;
+  unsigned long long lokey;
+  unsigned long long absfix;
+};
+
+struct ResLayout {
+  int ls, slots;
+  size_t codes, resid, pred, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, total;
+};
+
+__host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
+
+__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth) {
+  ResLayout L;
+  L.ls = depth > 0 ? (1 << (depth - 1)) : 1;
+  L.slots = (1 << (depth + 1)) - 1;
+  const size_t nr = nrep > 0 ? static_cast<size_t>(nrep) : 1;
+  size_t o = 0;
+  L.codes = o;
+  o = res_align(o + static_cast<size_t>(n) * nr);
+  L.resid = o;
+  o = res_align(o + static_cast<size_t>(n) * 8);
+  L.pred = o;
+  o = res_align(o + static_cast<size_t>(n) * 8);
+  L.fix = o;
+  o = res_align(o + static_cast<size_t>(n) * 8);
+  L.node = o;
+  o = res_align(o + static_cast<size_t>(n));
+  L.ord0 = o;
+  o = res_align(o + static_cast<size_t>(n) * 2);
+  L.scratch = o;
+  o = res_align(o + static_cast<size_t>(n) * 2);
+  L.hsum = o;
+  o = res_align(o + static_cast<size_t>(2) * L.ls * bins * 8);
+  L.hcnt = o;
+  o = res_align(o + static_cast<size_t>(2) * L.ls * bins * 4);
+  L.lbuf = o;
+  o = res_align(o + static_cast<size_t>(L.ls) * bins * 8);
+  L.nodes = o;
+  o = res_align(o + static_cast<size_t>(L.slots) * sizeof(ResNode));
+  L.win = o;
+  o = res_align(o + static_cast<size_t>(L.ls) * nr * sizeof(WinRec));
+  L.items = o;
+  o = res_align(o + static_cast<size_t>(L.ls) * (nr + 1) * sizeof(int));
+  L.rep = o;
+  o = res_align(o + 2 * nr * sizeof(int));
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ double warp_max_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+  for (int o = 1; o < 32; o <<= 1) {
+    const T t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
+    const FamDesc* __restrict__ fam, FamState* __restrict__ st, const int* __restrict__ fam_list, int Dp,
+    const uint8_t* __restrict__ codes_c, const double* __restrict__ target_c, const double* __restrict__ base,
+    const int32_t* __restrict__ ord, const int32_t* __restrict__ ord_root, const int32_t* __restrict__ rep_orig,
+    const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
+    const int32_t* __restrict__ cle, const int32_t* __restrict__ canon, const double* __restrict__ x, int d,
+    TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
+    unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ unsigned long long s_red[32];
+  __shared__ double s_dred[32];
+  __shared__ int s_wsum[32];
+  __shared__ int s_shift, s_nitems, s_stop, s_base_l, s_base_r;
+  __shared__ unsigned long long s_cnt[3];  // screened splits, exact nodes, exact folds
+  const int f = fam_list[blockIdx.x];
+  const FamDesc fd = fam[f];
+  const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
+  const ResLayout Lo = res_layout(n, nrep, bins, depth);
+  uint8_t* s_codes = sm + Lo.codes;  // [nrep][n]
+  double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
+  double* s_pred = reinterpret_cast<double*>(sm + Lo.pred);
+  long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
+  uint8_t* s_node = sm + Lo.node;
+  uint16_t* s_ord0 = reinterpret_cast<uint16_t*>(sm + Lo.ord0);
+  uint16_t* s_scr = reinterpret_cast<uint16_t*>(sm + Lo.scratch);
+  long long* s_hsum = reinterpret_cast<long long*>(sm + Lo.hsum);
+  int* s_hcnt = reinterpret_cast<int*>(sm + Lo.hcnt);
+  double* s_lbuf = reinterpret_cast<double*>(sm + Lo.lbuf);
+  ResNode* s_nodes = reinterpret_cast<ResNode*>(sm + Lo.nodes);
+  WinRec* s_win = reinterpret_cast<WinRec*>(sm + Lo.win);
+  int* s_items = reinterpret_cast<int*>(sm + Lo.items);
+  int* s_repb = reinterpret_cast<int*>(sm + Lo.rep);
+  int* s_repn = s_repb + (nrep > 0 ? nrep : 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ls = Lo.ls, slots = Lo.slots;
+  unsigned long long c_hist_rows = 0;
+  if (tid < 3) s_cnt[tid] = 0;
+
+  for (int i = tid; i < n * nrep; i += kResThreads) {
+    const int p = i / nrep, j = i - p * nrep;
+    s_codes[j * n + p] = codes_c[(fd.pos0 + p) * Dp + j];
+  }
+  for (int j = tid; j < nrep; j += kResThreads) {
+    s_repb[j] = rep_boff[fd.rep0 + j];
+    s_repn[j] = rep_nb[fd.rep0 + j];
+  }
+  const double b0 = base[f];
+  for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
+  if (tid == 0) s_stop = 0;
+  __syncthreads();
+
+  int ntrees = 0;
+  for (int round = 0; round < fd.trees; ++round) {
+    // ---- residuals (costmodel.cpp:204-206), fixed point, per-round reset ----------------
+    unsigned long long mx = 0;
+    for (int p = tid; p < n; p += kResThreads) {
+      const double r = fs_sub(target_c[fd.pos0 + p], s_pred[p]);
+      s_resid[p] = r;
+      mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(r))));
+      s_node[p] = 0;
+      s_ord0[p] = static_cast<uint16_t>(ord_root[fd.pos0 + p]);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) s_red[warp] = mx;
+    for (int s = tid; s < slots; s += kResThreads) {
+      ResNode z;
+      memset(&z, 0, sizeof z);
+      if (s == 0) z.n = n;
+      s_nodes[s] = z;
+    }
+    TreeRec* tr = trees + fd.tree0 + static_cast<int64_t>(ntrees) * slots_g;
+    for (int s = tid; s < slots_g; s += kResThreads) {
+      TreeRec tz;
+      memset(&tz, 0, sizeof tz);
+      tr[s] = tz;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long m = 0;
+      for (int w = 0; w < kResThreads / 32; ++w) m = max(m, s_red[w]);
+      s_shift = fix_shift(m, n);
+    }
+    __syncthreads();
+    const int shift = s_shift;
+    const double scale = ldexp(1.0, -shift);
+    for (int p = tid; p < n; p += kResThreads) s_fix[p] = __double2ll_rn(ldexp(s_resid[p], shift));
+    __syncthreads();
+
+    for (int level = 0; level <= depth; ++level) {
+      const int first = (1 << level) - 1, nl = 1 << level;
+      // ---- plan (level_plan_kernel) --------------------------------------------------------
+      if (tid < nl) {
+        const int s = first + tid;
+        ResNode& nd = s_nodes[s];
+        if (level == 0) {
+          if (node_needs_split(fd, 0, nd.n)) nd.build = 1;
+          else nd.state = kNodeLeaf;
+        } else if (s_nodes[(s - 1) >> 1].state == kNodeSplit) {
+          const bool need = node_needs_split(fd, level, nd.n);
+          if (!need) nd.state = kNodeLeaf;
+          if (s & 1) {
+            const int sib = s + 1;
+            const bool need_sib = node_needs_split(fd, level, s_nodes[sib].n);
+            if (need || need_sib) {
+              const int small = nd.n <= s_nodes[sib].n ? s : sib;
+              s_nodes[small].build = 1;
+              s_nodes[small == s ? sib : s].build = 2;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (level == depth || nrep == 0) break;
+      const int ring = level & 1;
+      long long* hs = s_hsum + static_cast<size_t>(ring) * ls * bins;
+      int* hc = s_hcnt + static_cast<size_t>(ring) * ls * bins;
+      for (int i = tid; i < nl * bins; i += kResThreads) {
+        hs[i] = 0;
+        hc[i] = 0;
+      }
+      __syncthreads();
+      // ---- histograms of directly built nodes (integer atomics in shared memory) --------------
+      for (int k = 0; k < nl; ++k) {
+        ResNode& nd = s_nodes[first + k];
+        if (nd.build != 1) continue;
+        const int nv = nd.n, seg = nd.seg;
+        long long* h = hs + static_cast<size_t>(k) * bins;
+        int* c = hc + static_cast<size_t>(k) * bins;
+        unsigned long long a = 0;
+        for (int e = tid; e < nv * nrep; e += kResThreads) {
+          const int r = e / nrep, j = e - r * nrep;
+          const int p = s_ord0[seg + r];
+          const int bin = s_repb[j] + s_codes[j * n + p];
+          const long long v = s_fix[p];
+          atomicAdd(reinterpret_cast<unsigned long long*>(h + bin), static_cast<unsigned long long>(v));
+          atomicAdd(c + bin, 1);
+          if (j == 0) a += static_cast<unsigned long long>(v < 0 ? -v : v);
+        }
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0 && a) atomicAdd(&nd.absfix, a);
+        c_hist_rows += tid == 0 ? nv : 0;
+      }
+      __syncthreads();
+      // ---- siblings by exact subtraction --------------------------------------------------------
+      if (level > 0) {
+        const long long* hp = s_hsum + static_cast<size_t>(ring ^ 1) * ls * bins;
+        const int* cp = s_hcnt + static_cast<size_t>(ring ^ 1) * ls * bins;
+        const int pfirst = (1 << (level - 1)) - 1;
+        for (int k2 = 0; k2 < nl / 2; ++k2) {
+          const int parent = pfirst + k2;
+          if (s_nodes[parent].state != kNodeSplit) continue;
+          const int c1 = 2 * parent + 1, c2 = c1 + 1;
+          int built, other;
+          if (s_nodes[c1].build == 1 && s_nodes[c2].build == 2) {
+            built = c1;
+            other = c2;
+          } else if (s_nodes[c2].build == 1 && s_nodes[c1].build == 2) {
+            built = c2;
+            other = c1;
+          } else {
+            continue;
+          }
+          const size_t ob = static_cast<size_t>(other - first) * bins, bb = static_cast<size_t>(built - first) * bins;
+          const size_t pb = static_cast<size_t>(k2) * bins;
+          for (int b = tid; b < bins; b += kResThreads) {
+            hs[ob + b] = hp[pb + b] - hs[bb + b];
+            hc[ob + b] = cp[pb + b] - hc[bb + b];
+          }
+          if (tid == 0) s_nodes[other].absfix = s_nodes[parent].absfix - s_nodes[built].absfix;
+        }
+        __syncthreads();
+      }
+      // ---- screen: warp per (node, feature), lanes over bins --------------------------------
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int it = warp; it < nl * nrep; it += kResThreads / 32) {
+          const int k = it / nrep, j = it - k * nrep;
+          ResNode& nd = s_nodes[first + k];
+          if (nd.state != 0 || nd.build == 0) continue;
+          const int nv = nd.n;
+          const long long* h = hs + static_cast<size_t>(k) * bins + s_repb[j];
+          const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+          const int nb = s_repn[j];
+          const double S = static_cast<double>(nd.absfix) * scale * (1.0 + 1e-12);
+          long long ts = 0;
+          for (int b = lane; b < nb; b += 32) ts += h[b];
+          for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+          const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
+          double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
+          int bb = 0x7fffffff, count = 0, carry_c = 0;
+          long long carry_s = 0;
+          for (int b0 = 0; b0 < nb; b0 += 32) {
+            const int b = b0 + lane;
+            const int cc = b < nb ? c[b] : 0;
+            const long long ss = b < nb ? h[b] : 0;
+            const int ic = warp_incl_scan(cc, lane) + carry_c;
+            const long long is = warp_incl_scan(ss, lane) + carry_s;
+            if (cc > 0 && ic < nv) {
+              double g, lo, hi;
+              screen_gain(is, ts, ic, nv, scale, S, g, lo, hi);
+              if (!pass) {
+                best_lo = fmax(best_lo, lo);
+              } else if (hi >= LO && hi > 0.0) {
+                ++count;
+                if (g > bg || (g == bg && b < bb)) {
+                  bg = g;
+                  bl = lo;
+                  bb = b;
+                }
+              }
+            }
+            carry_c = __shfl_sync(0xffffffffu, ic, 31);
+            carry_s = __shfl_sync(0xffffffffu, is, 31);
+          }
+          if (!pass) {
+            best_lo = warp_max_d(best_lo);
+            if (lane == 0 && best_lo > -INFINITY) atomicMax(&nd.lokey, lo_key(best_lo));
+          } else {
+            for (int o = 16; o > 0; o >>= 1) {
+              count += __shfl_xor_sync(0xffffffffu, count, o);
+              const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+              const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
+              const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+              if (og > bg || (og == bg && ob < bb)) {
+                bg = og;
+                bl = ol;
+                bb = ob;
+              }
+            }
+            if (lane == 0) {
+              WinRec w;
+              w.best_g = bg;
+              w.best_lo = bl;
+              w.best_bin = count ? bb : -1;
+              w.flag = count > 0;
+              s_win[k * nrep + j] = w;
+              if (count) atomicAdd(&nd.wcount, count);
+            }
+          }
+        }
+        __syncthreads();
+      }
+      // ---- decide (decide_kernel) ------------------------------------------------------------
+      if (tid == 0) s_nitems = 0;
+      __syncthreads();
+      if (tid < nl) {
+        const int k = tid;
+        ResNode& nd = s_nodes[first + k];
+        if (nd.state == 0 && nd.build != 0) {
+          const WinRec* w = s_win + k * nrep;
+          bool done = false;
+          if (nd.wcount == 0) {
+            nd.state = kNodeLeaf;
+            done = true;
+          } else if (nd.wcount == 1) {
+            for (int j = 0; j < nrep; ++j) {
+              if (!w[j].flag) continue;
+              if (w[j].best_lo > 0.0) {
+                nd.state = kNodeSplit;
+                nd.rep = j;
+                nd.bin = w[j].best_bin;
+                nd.gain = w[j].best_g;
+                const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+                int lc = 0;
+                for (int b = 0; b <= nd.bin; ++b) lc += c[b];
+                nd.lc = lc;
+                atomicAdd(&s_cnt[0], 1ull);
+                done = true;
+              }
+              break;
+            }
+          }
+          if (!done) {
+            nd.state = kNodeExact;
+            atomicAdd(&s_cnt[1], 1ull);
+            int cnt = 1;
+            for (int j = 0; j < nrep; ++j) cnt += w[j].flag;
+            const int b = atomicAdd(&s_nitems, cnt);
+            s_items[b] = (first + k) << 16 | 0xFFFF;
+            int o = 1;
+            for (int j = 0; j < nrep; ++j)
+              if (w[j].flag) s_items[b + o++] = (first + k) << 16 | j;
+            atomicAdd(&s_cnt[2], static_cast<unsigned long long>(cnt));
+          }
+        }
+      }
+      __syncthreads();
+      // ---- reference-order folds (exact_kernel) ------------------------------------------------
+      for (int it = warp; it < s_nitems; it += kResThreads / 32) {
+        const int s = s_items[it] >> 16, j = s_items[it] & 0xFFFF;
+        ResNode& nd = s_nodes[s];
+        const int nv = nd.n;
+        if (j == 0xFFFF) {
+          double sum = 0.0;
+          for (int i0 = 0; i0 < nv; i0 += 32) {
+            const double v = i0 + lane < nv ? s_resid[s_ord0[nd.seg + i0 + lane]] : 0.0;
+            const int m = min(32, nv - i0);
+            for (int l = 0; l < m; ++l) sum = fs_add(sum, __shfl_sync(0xffffffffu, v, l));
+          }
+          if (lane == 0) nd.total = sum;
+          continue;
+        }
+        const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(j) * n;
+        double* out = s_lbuf + static_cast<size_t>(s - first) * bins + s_repb[j];
+        const uint8_t* cj = s_codes + static_cast<size_t>(j) * n;
+        double left = 0.0;
+        int prev = -1, seen = 0;
+        int p_next = lane < n ? L[lane] : 0;
+        for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
+          const int i = i0 + lane;
+          const int p = p_next;
+          p_next = i + 32 < n ? L[i + 32] : 0;
+          const bool mem = i < n && s_node[p] == s;
+          const int code = mem ? cj[p] : 0;
+          const double rv = mem ? s_resid[p] : 0.0;
+          unsigned m = __ballot_sync(0xffffffffu, mem);
+          seen += __popc(m);
+          while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const int cc = __shfl_sync(0xffffffffu, code, l);
+            const double v = __shfl_sync(0xffffffffu, rv, l);
+            if (prev >= 0 && cc != prev && lane == 0) out[prev] = left;
+            left = fs_add(left, v);
+            prev = cc;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- exact decision (exact_decide_kernel) -------------------------------------------------
+      if (tid < nl) {
+        const int k = tid;
+        ResNode& nd = s_nodes[first + k];
+        if (nd.state == kNodeExact) {
+          const WinRec* w = s_win + k * nrep;
+          const int nv = nd.n;
+          const double T = nd.total;
+          const double parent = fs_div(fs_mul(T, T), static_cast<double>(nv));
+          double best = 0.0;
+          int bj = -1, bbin = -1, blc = 0;
+          for (int j = 0; j < nrep; ++j) {
+            if (!w[j].flag) continue;
+            const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+            const double* lb = s_lbuf + static_cast<size_t>(k) * bins + s_repb[j];
+            int cum = 0;
+            for (int b = 0; b < s_repn[j]; ++b) {
+              const int cb = c[b];
+              if (!cb) continue;
+              cum += cb;
+              if (cum >= nv) break;
+              const double L = lb[b];
+              const double R = fs_sub(T, L);
+              const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+              const double r = fs_div(fs_mul(R, R), static_cast<double>(nv - cum));
+              const double g = fs_sub(fs_add(a, r), parent);
+              if (g > best) {
+                best = g;
+                bj = j;
+                bbin = b;
+                blc = cum;
+              }
+            }
+          }
+          if (bj < 0) {
+            nd.state = kNodeLeaf;
+          } else {
+            nd.state = kNodeSplit;
+            nd.rep = bj;
+            nd.bin = bbin;
+            nd.gain = best;
+            nd.lc = blc;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- split records: threshold, tree record, children -------------------------------------
+      if (tid < nl) {
+        const int s = first + tid;
+        ResNode& nd = s_nodes[s];
+        if (nd.state == kNodeSplit) {
+          const int j = nd.rep;
+          const int orig = rep_orig[fd.rep0 + j];
+          double thr = vals[fd.bin0 + s_repb[j] + nd.bin];
+          if (thr == 0.0) {  // +0.0 / -0.0 share a bin: the last left element's own value
+            const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(j) * n;
+            for (int i = cle[fd.bin0 + s_repb[j] + nd.bin] - 1; i >= 0; --i)
+              if (s_node[L[i]] == s) {
+                thr = x[(fd.row0 + canon[fd.pos0 + L[i]]) * d + orig];
+                break;
+              }
+          }
+          TreeRec r;
+          r.kind = kNodeSplit;
+          r.feature = orig;
+          r.threshold = thr;
+          r.value = 0.0;
+          r.gain = nd.gain;
+          tr[s] = r;
+          ResNode& a = s_nodes[2 * s + 1];
+          ResNode& b = s_nodes[2 * s + 2];
+          a.n = nd.lc;
+          a.seg = nd.seg;
+          b.n = nd.n - nd.lc;
+          b.seg = nd.seg + nd.lc;
+        }
+      }
+      __syncthreads();
+      // ---- stable partition of each split node's order-0 segment -------------------------------
+      for (int k = 0; k < nl; ++k) {
+        const int s = first + k;
+        const ResNode& nd = s_nodes[s];
+        if (nd.state != kNodeSplit) continue;
+        const int nv = nd.n, seg = nd.seg, lc = nd.lc, bin = nd.bin;
+        const uint8_t* cj = s_codes + static_cast<size_t>(nd.rep) * n;
+        for (int i = tid; i < nv; i += kResThreads) s_scr[i] = s_ord0[seg + i];
+        if (tid == 0) {
+          s_base_l = 0;
+          s_base_r = 0;
+        }
+        __syncthreads();
+        const uint8_t cl = static_cast<uint8_t>(2 * s + 1), cr = static_cast<uint8_t>(2 * s + 2);
+        for (int t0 = 0; t0 < nv; t0 += kResThreads) {
+          const int i = t0 + tid;
+          int p = 0;
+          bool left = false;
+          if (i < nv) {
+            p = s_scr[i];
+            left = cj[p] <= bin;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, left);
+          if (lane == 0) s_wsum[warp] = __popc(bal);
+          __syncthreads();
+          if (warp == 0) {
+            const int v = s_wsum[lane];
+            s_wsum[lane] = warp_incl_scan(v, lane) - v;
+          }
+          __syncthreads();
+          const int lrank = s_wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+          if (i < nv) {
+            if (left) {
+              s_ord0[seg + s_base_l + lrank] = static_cast<uint16_t>(p);
+              s_node[p] = cl;
+            } else {
+              s_ord0[seg + lc + s_base_r + (i - t0) - lrank] = static_cast<uint16_t>(p);
+              s_node[p] = cr;
+            }
+          }
+          __syncthreads();
+          if (tid == kResThreads - 1) {
+            const int tile_left = s_wsum[31] + __popc(bal);
+            const int tile = min(kResThreads, nv - t0);
+            s_base_l += tile_left;
+            s_base_r += tile - tile_left;
+          }
+          __syncthreads();
+        }
+      }
+    }
+    // ---- leaves (leaf_kernel): reference-order total / n, prediction update ------------------
+    for (int s = warp; s < slots; s += kResThreads / 32) {
+      ResNode& nd = s_nodes[s];
+      if (nd.state != kNodeLeaf || nd.n == 0) continue;
+      if (s > 0 && s_nodes[(s - 1) >> 1].state != kNodeSplit) continue;
+      const int nv = nd.n;
+      double sum = 0.0;
+      for (int i0 = 0; i0 < nv; i0 += 32) {
+        const double v = i0 + lane < nv ? s_resid[s_ord0[nd.seg + i0 + lane]] : 0.0;
+        const int m = min(32, nv - i0);
+        for (int l = 0; l < m; ++l) sum = fs_add(sum, __shfl_sync(0xffffffffu, v, l));
+      }
+      const double value = fs_div(sum, static_cast<double>(nv));
+      const double step = fs_mul(fd.lr, value);
+      for (int i = lane; i < nv; i += 32) {
+        const int p = s_ord0[nd.seg + i];
+        s_pred[p] = fs_add(s_pred[p], step);
+      }
+      if (lane == 0) {
+        nd.value = value;
+        TreeRec r;
+        r.kind = kNodeLeaf;
+        r.feature = -1;
+        r.threshold = 0.0;
+        r.value = value;
+        r.gain = 0.0;
+        tr[s] = r;
+      }
+    }
+    __syncthreads();
+    // ---- commit / early stop (costmodel.cpp:212) and MSE (:215-220) --------------------------
+    if (s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0) break;  // uniform (smem)
+    double a = 0.0;
+    for (int p = tid; p < n; p += kResThreads) {
+      const double e = fs_sub(target_c[fd.pos0 + p], s_pred[p]);
+      a = fs_add(a, fs_mul(e, e));
+    }
+    for (int o = 16; o > 0; o >>= 1) a = fs_add(a, __shfl_down_sync(0xffffffffu, a, o));
+    if (lane == 0) s_dred[warp] = a;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kResThreads / 32; ++w) t = fs_add(t, s_dred[w]);
+      mse[static_cast<int64_t>(f) * max_trees + ntrees] = fs_div(t, static_cast<double>(n));
+    }
+    ++ntrees;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    st[f].ntrees = ntrees;
+    st[f].active = 0;
+    st[f].screened += s_cnt[0];
+    st[f].exact += s_cnt[1];
+    atomicAdd(ctr + kCtrHistRows, c_hist_rows);
+    atomicAdd(ctr + kCtrHistBytes, c_hist_rows * (static_cast<unsigned long long>(nrep) + 12ull));
+    atomicAdd(ctr + kCtrExactChains, s_cnt[2]);
+    atomicAdd(ctr + kCtrExactNodes, s_cnt[1]);
+  }
+}
+
+}  // namespace
+}  // namespace fit
+}  // namespace fs
+
+// ==========================================================================================
 // host orchestration
 // ==========================================================================================
 namespace fs {
@@ -1250,8 +1850,15 @@ inline unsigned grid1(int64_t n, int block, int cap) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, block), cap)));
 }
 
+struct ResidentPlan {
+  bool enabled = false;
+  std::vector<int> families;
+  size_t smem = 0;
+};
+
 template <typename CodeT>
-void run_rounds(fs_device* dev, Arena& ar, int F, int d, int Dp, int64_t n_tot, int max_trees, int depth_max,
+void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, int d, int Dp, int64_t n_tot,
+                int max_trees, int depth_max,
                 int slots, int nrep_max, int max_bins, int n_max, int level_slots_max, const FamDesc* fam_d,
                 FamState* st_d, const double* x_d, const double* target_d, const uint16_t* codes_all,
                 const int32_t* rep_orig_d, const int32_t* rep_nb_d, const int32_t* rep_boff_d, const double* vals_d,
@@ -1285,6 +1892,22 @@ void run_rounds(fs_device* dev, Arena& ar, int F, int d, int Dp, int64_t n_tot, 
   base_kernel<<<F, 256, 0, s>>>(fam_d, target_c, base_d, pred, ord, ord_root);
   dev->count_launch(8);
   FS_CUDA(cudaGetLastError());
+
+  // ---- resident path: every family fits one CTA's shared memory -> one launch, all rounds ----
+  if (std::is_same<CodeT, uint8_t>::value && resident.enabled) {
+    int* list_d = ar.upload(resident.families);
+    FS_CUDA(cudaFuncSetAttribute(fit_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(resident.smem)));
+    {
+      ProfScope prof(dev, "fit_resident");
+      fit_resident_kernel<<<static_cast<unsigned>(resident.families.size()), kResThreads, resident.smem, s>>>(
+          fam_d, st_d, list_d, Dp, reinterpret_cast<const uint8_t*>(codes_c), target_c, base_d, ord, ord_root,
+          rep_orig_d, rep_nb_d, rep_boff_d, vals_d, cle, canon, x_d, d, trees_d, mse_d, max_trees, slots, dev->ctr_d);
+    }
+    dev->count_launch();
+    FS_CUDA(cudaGetLastError());
+    return;
+  }
 
   // ---- round state ---------------------------------------------------------------------
   double* resid = ar.alloc<double>(n_tot);
@@ -1536,6 +2159,31 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   }
   if (min_nrep == INT_MAX) min_nrep = 1;
   const int code_bytes = max_nb <= 256 ? 1 : 2;
+  // Path choice: FAMSEER_FIT_PATH = auto (default) | resident | multi.
+  ResidentPlan res;
+  {
+    const char* envp = std::getenv("FAMSEER_FIT_PATH");
+    const std::string mode = envp ? envp : "auto";
+    if (mode != "auto" && mode != "resident" && mode != "multi")
+      fail(FS_EINVAL, "FAMSEER_FIT_PATH must be auto, resident or multi");
+    if (mode != "multi" && code_bytes == 1 && depth_max <= kResMaxDepth) {
+      bool ok = true;
+      size_t need = 0;
+      for (int f = 0; f < F; ++f) {
+        const FamDesc& fd = fam[static_cast<size_t>(f)];
+        if (fd.n <= 0 || fd.trees <= 0) continue;
+        if (fd.n > 65535) ok = false;
+        need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth).total);
+        res.families.push_back(f);
+      }
+      if (ok && need <= 225 * 1024 && !res.families.empty()) {
+        res.enabled = true;
+        res.smem = need;
+      }
+    }
+    if (mode == "resident" && !res.enabled && !res.families.empty())
+      fail(FS_EINVAL, "fit: resident path requested but the families do not fit one CTA");
+  }
   const int per_vec = 16 / code_bytes;
   const int Dp = std::max(per_vec, static_cast<int>(ceil_div(std::max(nrep_max, 1), per_vec)) * per_vec);
   FS_CUDA(cudaMemcpyAsync(fam_d, fam.data(), fam.size() * sizeof(FamDesc), cudaMemcpyHostToDevice, s));
@@ -1563,12 +2211,12 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   {
   ProfScope prof_rounds(dev, "fit_rounds");
   if (code_bytes == 1)
-    run_rounds<uint8_t>(dev, ar, F, d, Dp, n_tot, max_trees, depth_max, slots, nrep_max, max_bins, n_max,
+    run_rounds<uint8_t>(res, dev, ar, F, d, Dp, n_tot, max_trees, depth_max, slots, nrep_max, max_bins, n_max,
                         level_slots_max, fam_d, st_d, x_d, target_d, codes_all, rep_orig_d, rep_nb_d, rep_boff_d,
                         vals_d, total_ord, total_bins, total_hist, total_lbuf, total_tree, trees_d, mse_d, base_d,
                         min_nrep);
   else
-    run_rounds<uint16_t>(dev, ar, F, d, Dp, n_tot, max_trees, depth_max, slots, nrep_max, max_bins, n_max,
+    run_rounds<uint16_t>(res, dev, ar, F, d, Dp, n_tot, max_trees, depth_max, slots, nrep_max, max_bins, n_max,
                          level_slots_max, fam_d, st_d, x_d, target_d, codes_all, rep_orig_d, rep_nb_d, rep_boff_d,
                          vals_d, total_ord, total_bins, total_hist, total_lbuf, total_tree, trees_d, mse_d, base_d,
                          min_nrep);

@@ -14,6 +14,14 @@ CASES = [str(t) for t in G["fit_cases"]]
 TREE_FIELDS = ("offsets", "feature", "threshold", "left", "right", "value")
 
 
+@pytest.fixture(autouse=True, params=["auto", "multi"])
+def fit_path(request, monkeypatch):
+    """Every parity test runs on both trainers: the resident one-CTA-per-family kernel (auto picks
+    it when the families fit shared memory) and the multi-kernel round."""
+    monkeypatch.setenv("FAMSEER_FIT_PATH", request.param)
+    return request.param
+
+
 def assert_same_model(got, exp, gains=None, mse_tol=1e-12):
     assert got.base == exp.base
     for k in TREE_FIELDS:
