@@ -575,17 +575,17 @@ __global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamStat
   NodeRec* nd = nodes + fd.node0;
   const int s = first + local;
   if (level == 0) {
-    if (node_needs_split(fd, 0, nd[0].n)) nd[0].build = 1;
+    if (fd.nrep > 0 && node_needs_split(fd, 0, nd[0].n)) nd[0].build = 1;
     else nd[0].state = kNodeLeaf;
     return;
   }
   const int parent = (s - 1) >> 1;
   if (nd[parent].state != kNodeSplit) return;
-  const bool need = node_needs_split(fd, level, nd[s].n);
+  const bool need = fd.nrep > 0 && node_needs_split(fd, level, nd[s].n);
   if (!need) nd[s].state = kNodeLeaf;
   if (s & 1) {  // left child decides the pair's build plan
     const int sib = s + 1;
-    const bool need_sib = node_needs_split(fd, level, nd[sib].n);
+    const bool need_sib = fd.nrep > 0 && node_needs_split(fd, level, nd[sib].n);
     if (need || need_sib) {
       const int small = nd[s].n <= nd[sib].n ? s : sib;
       nd[small].build = 1;
@@ -1231,12 +1231,15 @@ struct ResNode {
 
 struct ResLayout {
   int ls, slots;
-  size_t codes, resid, pred, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, total;
+  size_t codes, resid, pred, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, gsum, gcnt, gabs,
+      total;
 };
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
 
-__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth) {
+// groups: private histogram copies used while accumulating one node (threads own
+// (feature, group) pairs, so no shared-memory atomics are needed).
+__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, int groups) {
   ResLayout L;
   L.ls = depth > 0 ? (1 << (depth - 1)) : 1;
   L.slots = (1 << (depth + 1)) - 1;
@@ -1270,6 +1273,12 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(L.ls) * (nr + 1) * sizeof(int));
   L.rep = o;
   o = res_align(o + 2 * nr * sizeof(int));
+  L.gsum = o;
+  o = res_align(o + static_cast<size_t>(groups) * bins * 8);
+  L.gcnt = o;
+  o = res_align(o + static_cast<size_t>(groups) * bins * 4);
+  L.gabs = o;
+  o = res_align(o + static_cast<size_t>(groups) * 8);
   L.total = o;
   return L;
 }
@@ -1295,7 +1304,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
     const int32_t* __restrict__ cle, const int32_t* __restrict__ canon, const double* __restrict__ x, int d,
     TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
-    unsigned long long* __restrict__ ctr) {
+    unsigned long long* __restrict__ ctr, int groups) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ unsigned long long s_red[32];
   __shared__ double s_dred[32];
@@ -1305,8 +1314,11 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const int f = fam_list[blockIdx.x];
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
-  const ResLayout Lo = res_layout(n, nrep, bins, depth);
+  const ResLayout Lo = res_layout(n, nrep, bins, depth, groups);
   uint8_t* s_codes = sm + Lo.codes;  // [nrep][n]
+  long long* s_gsum = reinterpret_cast<long long*>(sm + Lo.gsum);  // [groups][bins]
+  int* s_gcnt = reinterpret_cast<int*>(sm + Lo.gcnt);
+  unsigned long long* s_gabs = reinterpret_cast<unsigned long long*>(sm + Lo.gabs);
   double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
   double* s_pred = reinterpret_cast<double*>(sm + Lo.pred);
   long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
@@ -1383,14 +1395,14 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         const int s = first + tid;
         ResNode& nd = s_nodes[s];
         if (level == 0) {
-          if (node_needs_split(fd, 0, nd.n)) nd.build = 1;
+          if (nrep > 0 && node_needs_split(fd, 0, nd.n)) nd.build = 1;
           else nd.state = kNodeLeaf;
         } else if (s_nodes[(s - 1) >> 1].state == kNodeSplit) {
-          const bool need = node_needs_split(fd, level, nd.n);
+          const bool need = nrep > 0 && node_needs_split(fd, level, nd.n);
           if (!need) nd.state = kNodeLeaf;
           if (s & 1) {
             const int sib = s + 1;
-            const bool need_sib = node_needs_split(fd, level, s_nodes[sib].n);
+            const bool need_sib = nrep > 0 && node_needs_split(fd, level, s_nodes[sib].n);
             if (need || need_sib) {
               const int small = nd.n <= s_nodes[sib].n ? s : sib;
               s_nodes[small].build = 1;
@@ -1409,28 +1421,63 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         hc[i] = 0;
       }
       __syncthreads();
-      // ---- histograms of directly built nodes (integer atomics in shared memory) --------------
-      for (int k = 0; k < nl; ++k) {
-        ResNode& nd = s_nodes[first + k];
-        if (nd.build != 1) continue;
-        const int nv = nd.n, seg = nd.seg;
-        long long* h = hs + static_cast<size_t>(k) * bins;
-        int* c = hc + static_cast<size_t>(k) * bins;
-        unsigned long long a = 0;
-        for (int e = tid; e < nv * nrep; e += kResThreads) {
-          const int r = e / nrep, j = e - r * nrep;
-          const int p = s_ord0[seg + r];
-          const int bin = s_repb[j] + s_codes[j * n + p];
-          const long long v = s_fix[p];
-          atomicAdd(reinterpret_cast<unsigned long long*>(h + bin), static_cast<unsigned long long>(v));
-          atomicAdd(c + bin, 1);
-          if (j == 0) a += static_cast<unsigned long long>(v < 0 ? -v : v);
+      // ---- histograms of directly built nodes: thread t owns (feature t % nrep, row group
+      // t / nrep) and its group's private bins, so the accumulation needs no atomics; the
+      // group copies are then summed (integers: any order gives the same result).
+      {
+        const int per_group = nrep < kResThreads ? nrep : kResThreads;
+        const int g = tid / per_group, j0 = tid - g * per_group;
+        const bool worker = g < groups;
+        for (int k = 0; k < nl; ++k) {
+          ResNode& nd = s_nodes[first + k];
+          if (nd.build != 1) continue;
+          const int nv = nd.n, seg = nd.seg;
+          for (int i = tid; i < groups * bins; i += kResThreads) {
+            s_gsum[i] = 0;
+            s_gcnt[i] = 0;
+          }
+          if (tid < groups) s_gabs[tid] = 0;
+          __syncthreads();
+          if (worker) {
+            long long* gs = s_gsum + static_cast<size_t>(g) * bins;
+            int* gc = s_gcnt + static_cast<size_t>(g) * bins;
+            unsigned long long a = 0;
+            for (int j = j0; j < nrep; j += per_group) {
+              const int boff = s_repb[j];
+              const uint8_t* cj = s_codes + static_cast<size_t>(j) * n;
+              for (int r = g; r < nv; r += groups) {
+                const int p = s_ord0[seg + r];
+                const long long v = s_fix[p];
+                const int bin = boff + cj[p];
+                gs[bin] += v;
+                gc[bin] += 1;
+                if (j == 0) a += static_cast<unsigned long long>(v < 0 ? -v : v);
+              }
+            }
+            if (j0 == 0) s_gabs[g] = a;
+          }
+          __syncthreads();
+          long long* h = hs + static_cast<size_t>(k) * bins;
+          int* c = hc + static_cast<size_t>(k) * bins;
+          for (int b = tid; b < bins; b += kResThreads) {
+            long long sv = 0;
+            int cv = 0;
+            for (int gg = 0; gg < groups; ++gg) {
+              sv += s_gsum[static_cast<size_t>(gg) * bins + b];
+              cv += s_gcnt[static_cast<size_t>(gg) * bins + b];
+            }
+            h[b] = sv;
+            c[b] = cv;
+          }
+          if (tid == 0) {
+            unsigned long long a = 0;
+            for (int gg = 0; gg < groups; ++gg) a += s_gabs[gg];
+            nd.absfix = a;
+          }
+          c_hist_rows += tid == 0 ? nv : 0;
+          __syncthreads();
         }
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0 && a) atomicAdd(&nd.absfix, a);
-        c_hist_rows += tid == 0 ? nv : 0;
       }
-      __syncthreads();
       // ---- siblings by exact subtraction --------------------------------------------------------
       if (level > 0) {
         const long long* hp = s_hsum + static_cast<size_t>(ring ^ 1) * ls * bins;
@@ -1854,6 +1901,7 @@ struct ResidentPlan {
   bool enabled = false;
   std::vector<int> families;
   size_t smem = 0;
+  int groups = 1;
 };
 
 template <typename CodeT>
@@ -1902,7 +1950,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       ProfScope prof(dev, "fit_resident");
       fit_resident_kernel<<<static_cast<unsigned>(resident.families.size()), kResThreads, resident.smem, s>>>(
           fam_d, st_d, list_d, Dp, reinterpret_cast<const uint8_t*>(codes_c), target_c, base_d, ord, ord_root,
-          rep_orig_d, rep_nb_d, rep_boff_d, vals_d, cle, canon, x_d, d, trees_d, mse_d, max_trees, slots, dev->ctr_d);
+          rep_orig_d, rep_nb_d, rep_boff_d, vals_d, cle, canon, x_d, d, trees_d, mse_d, max_trees, slots, dev->ctr_d,
+          resident.groups);
     }
     dev->count_launch();
     FS_CUDA(cudaGetLastError());
@@ -2168,17 +2217,28 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
       fail(FS_EINVAL, "FAMSEER_FIT_PATH must be auto, resident or multi");
     if (mode != "multi" && code_bytes == 1 && depth_max <= kResMaxDepth) {
       bool ok = true;
-      size_t need = 0;
+      const size_t budget = 225 * 1024;
+      int groups = 32;
       for (int f = 0; f < F; ++f) {
         const FamDesc& fd = fam[static_cast<size_t>(f)];
         if (fd.n <= 0 || fd.trees <= 0) continue;
         if (fd.n > 65535) ok = false;
-        need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth).total);
+        const size_t base_total = res_layout(fd.n, fd.nrep, fd.bins, fd.depth, 0).total;
+        const size_t per = static_cast<size_t>(fd.bins) * 12 + 64;
+        const int fit_g = base_total + per <= budget ? static_cast<int>((budget - base_total) / per) : 0;
+        groups = std::min({groups, fit_g, kResThreads / std::max(1, static_cast<int>(fd.nrep))});
         res.families.push_back(f);
       }
-      if (ok && need <= 225 * 1024 && !res.families.empty()) {
+      size_t need = 0;
+      if (groups >= 1)
+        for (int f : res.families) {
+          const FamDesc& fd = fam[static_cast<size_t>(f)];
+          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups).total);
+        }
+      if (ok && groups >= 1 && need <= budget && !res.families.empty()) {
         res.enabled = true;
         res.smem = need;
+        res.groups = groups;
       }
     }
     if (mode == "resident" && !res.enabled && !res.families.empty())
