@@ -141,6 +141,12 @@ int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t
                const int64_t* seg_h, const int32_t* space_of_d, const int32_t* assign_d,
                int32_t pad_dim, double* scores_d, int32_t* perm_d);
 
+/* ---- pairwise accuracy (costmodel.cpp:248-277) over precomputed scores ---------------------
+ * Pairs with relative latency difference < 1e-6 are excluded, predicted ties score 1/2.
+ * FS_EINVAL for m < 2, FS_EDOMAIN when every pair is excluded. */
+int fs_pairwise_accuracy(fs_device* dev, int64_t m, const double* scores, const double* latency,
+                         double* out);
+
 /* ---- fit (costmodel.cpp:152-222; train_cost_model :224-235 appends log-latency rows first) ---
  * Refit family f's ensemble from scratch on rows [seg[f], seg[f+1]) of x/target with params[f].
  * Trees are bit-identical to the reference's (canonical row order, reference-order sums for every

@@ -157,6 +157,14 @@ class Device:
         _check(_lib().fs_rank(self.h, len(sg) - 1, sp, _p(s, _capi._dp), _p(perm, _capi._i32p)))
         return perm
 
+    def pairwise_accuracy(self, scores, latency) -> float:
+        """costmodel.cpp:248-277 over precomputed scores (pair count on the device)."""
+        s = np.ascontiguousarray(scores, np.float64)
+        lat = np.ascontiguousarray(latency, np.float64)
+        out = C.c_double()
+        _check(_lib().fs_pairwise_accuracy(self.h, len(s), _p(s, _capi._dp), _p(lat, _capi._dp), C.byref(out)))
+        return out.value
+
     def rank_d(self, scores_t, seg, perm_t):
         sg, sp = _seg(seg)
         _check(_lib().fs_rank_d(self.h, len(sg) - 1, sp, scores_t.data_ptr(), perm_t.data_ptr()))

@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(256) distinct_small_kernel(const double* __res
                                                              uint16_t* __restrict__ codes_all,
                                                              double* __restrict__ vals_all,
                                                              int32_t* __restrict__ nb_all,
-                                                             uint64_t* __restrict__ hash_all, uint32_t* err) {
+                                                             uint64_t* __restrict__ hash_all, uint32_t* err,
+                                                             int* __restrict__ negz) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* tab = reinterpret_cast<uint64_t*>(smem);                 // [32][512]
   uint64_t* sorted = tab + 32 * kHashSlots;                          // [32][256]
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256) distinct_small_kernel(const double* __res
   __syncthreads();
   const int j = j0 + lane;
   const bool has = j < d;
-  bool nonfinite = false;
+  bool nonfinite = false, negzero = false;
   if (has) {
     uint64_t* t = tab + lane * kHashSlots;
     for (int r = warp; r < fd.n; r += 8) {
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(256) distinct_small_kernel(const double* __res
         nonfinite = true;
         continue;
       }
+      negzero |= v == 0.0 && signbit(v);
       if (ovf[lane]) continue;
       const uint64_t k = value_key(v);
       uint32_t h = static_cast<uint32_t>(mix64(k)) & (kHashSlots - 1);
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(256) distinct_small_kernel(const double* __res
     }
   }
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, kErrNonFiniteFit);
+  if (__any_sync(0xffffffffu, negzero) && lane == 0) atomicOr(negz + blockIdx.y, 1);
   __syncthreads();
   // rank every present key by counting smaller keys (<= 256 per feature)
   for (int f = warp; f < 32; f += 8) {
@@ -772,17 +775,20 @@ __device__ __forceinline__ void screen_gain(int64_t ls, int64_t ts, int lc, int 
   const double L = static_cast<double>(ls) * scale, T = static_cast<double>(ts) * scale;
   const double R = static_cast<double>(ts - ls) * scale;
   const int rc = n - lc;
-  const double A = L * L / lc, B = R * R / rc, P = T * T / n;
+  // three reciprocals instead of nine divisions; their extra rounding (<= 1 ulp per term) is
+  // covered by the 6u term below
+  const double ilc = 1.0 / lc, irc = 1.0 / rc, in = 1.0 / n;
+  const double A = L * L * ilc, B = R * R * irc, P = T * T * in;
   g = (A + B) - P;
   const double nu = static_cast<double>(n) * u;
   const double gam = nu / (1.0 - nu);
   const double q = static_cast<double>(n) * 0.5 * scale;
   const double EL = gam * S + q, ET = gam * S + q, ER = 2.0 * gam * S + 2.0 * q + u * fabs(R);
   const double aL = fabs(L) + EL, aR = fabs(R) + ER, aT = fabs(T) + ET;
-  const double dA = (2.0 * fabs(L) + EL) * EL / lc + 4.0 * u * aL * aL / lc;
-  const double dB = (2.0 * fabs(R) + ER) * ER / rc + 4.0 * u * aR * aR / rc;
-  const double dP = (2.0 * fabs(T) + ET) * ET / n + 4.0 * u * aT * aT / n;
-  const double delta = 2.0 * (dA + dB + dP + 4.0 * u * (A + B + P)) + 1e-300;
+  const double dA = ((2.0 * fabs(L) + EL) * EL + 4.0 * u * aL * aL) * ilc;
+  const double dB = ((2.0 * fabs(R) + ER) * ER + 4.0 * u * aR * aR) * irc;
+  const double dP = ((2.0 * fabs(T) + ET) * ET + 4.0 * u * aT * aT) * in;
+  const double delta = 2.0 * (dA + dB + dP + 6.0 * u * (A + B + P)) * (1.0 + 8.0 * u) + 1e-300;
   lo = g - delta;
   hi = g + delta;
 }
@@ -814,7 +820,7 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
   for (int b = 0; b < nb; ++b) ts += hsum[hb + b];
   const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
   double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
-  int bb = -1, count = 0, cum = 0;
+  int bb = -1, blc = 0, count = 0, cum = 0;
   int64_t ls = 0;
   for (int b = 0; b < nb; ++b) {
     const int c = hcnt[hb + b];
@@ -832,6 +838,7 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
         bg = g;
         bl = lo;
         bb = b;
+        blc = cum;
       }
     }
   }
@@ -843,6 +850,10 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
     w.best_lo = bl;
     w.best_bin = bb;
     w.flag = count > 0;
+    w.count = count;
+    w.best_lc = blc;
+    w.eq = 0;
+    w.pad_ = 0;
     win[(static_cast<int64_t>(f) * level_slots_max + local) * nrep_max + jj] = w;
     if (count) atomicAdd(&nd.wcount, count);
   }
@@ -1050,7 +1061,7 @@ __global__ void __launch_bounds__(1024) partition_kernel(
   if (tid == 0) {
     const int orig = rep_orig[fd.rep0 + jj];
     double thr = vals[fd.bin0 + rep_boff[fd.rep0 + jj] + bin];
-    if (thr == 0.0) {  // +0.0 and -0.0 share a bin: take the last left element's own value
+    if (thr == 0.0 && fd.negz) {  // +0.0 and -0.0 share a bin: take the last left element's own value
       const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
       for (int i = cle[fd.bin0 + rep_boff[fd.rep0 + jj] + bin] - 1; i >= 0; --i) {
         if (nodeid[fd.pos0 + L[i]] == s) {
@@ -1224,6 +1235,7 @@ constexpr int kResMaxDepth = 7;  // node ids fit in uint8
 
 struct ResNode {
   int32_t n, seg, state, rep, bin, lc, wcount, build;
+  int32_t eqf0, pad_;  // lowest window feature when the window may be one tie class, else -1
   double gain, value, total;
   unsigned long long lokey;
   unsigned long long absfix;
@@ -1232,7 +1244,7 @@ struct ResNode {
 struct ResLayout {
   int ls, slots;
   size_t codes, resid, pred, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, gsum, gcnt, gabs,
-      total;
+      cand, total;
 };
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
@@ -1279,6 +1291,8 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(groups) * bins * 4);
   L.gabs = o;
   o = res_align(o + static_cast<size_t>(groups) * 8);
+  L.cand = o;  // screened (gain, bound) per (node at level, bin)
+  o = res_align(o + static_cast<size_t>(L.ls) * bins * 16);
   L.total = o;
   return L;
 }
@@ -1319,6 +1333,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   long long* s_gsum = reinterpret_cast<long long*>(sm + Lo.gsum);  // [groups][bins]
   int* s_gcnt = reinterpret_cast<int*>(sm + Lo.gcnt);
   unsigned long long* s_gabs = reinterpret_cast<unsigned long long*>(sm + Lo.gabs);
+  double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
+  __shared__ int s_neq;
   double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
   double* s_pred = reinterpret_cast<double*>(sm + Lo.pred);
   long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
@@ -1507,7 +1523,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
         __syncthreads();
       }
-      // ---- screen: warp per (node, feature), lanes over bins --------------------------------
+      // ---- screen: warp per (node, feature), lanes over bins. Pass 0 computes every candidate's
+      // screened gain and bound once (cached) and the node's max lower bound; pass 1 forms the
+      // window {hi >= LO, hi > 0} and records each feature's count / best / left count.
       for (int pass = 0; pass < 2; ++pass) {
         for (int it = warp; it < nl * nrep; it += kResThreads / 32) {
           const int k = it / nrep, j = it - k * nrep;
@@ -1516,37 +1534,51 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           const int nv = nd.n;
           const long long* h = hs + static_cast<size_t>(k) * bins + s_repb[j];
           const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+          double* cand = s_cand + 2 * (static_cast<size_t>(k) * bins + s_repb[j]);
           const int nb = s_repn[j];
-          const double S = static_cast<double>(nd.absfix) * scale * (1.0 + 1e-12);
           long long ts = 0;
-          for (int b = lane; b < nb; b += 32) ts += h[b];
-          for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+          if (!pass) {
+            for (int b = lane; b < nb; b += 32) ts += h[b];
+            for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+          }
+          const double S = static_cast<double>(nd.absfix) * scale * (1.0 + 1e-12);
           const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
           double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
-          int bb = 0x7fffffff, count = 0, carry_c = 0;
+          int bb = 0x7fffffff, blc = 0, count = 0, carry_c = 0;
           long long carry_s = 0;
           for (int b0 = 0; b0 < nb; b0 += 32) {
             const int b = b0 + lane;
             const int cc = b < nb ? c[b] : 0;
-            const long long ss = b < nb ? h[b] : 0;
             const int ic = warp_incl_scan(cc, lane) + carry_c;
-            const long long is = warp_incl_scan(ss, lane) + carry_s;
-            if (cc > 0 && ic < nv) {
-              double g, lo, hi;
-              screen_gain(is, ts, ic, nv, scale, S, g, lo, hi);
-              if (!pass) {
-                best_lo = fmax(best_lo, lo);
-              } else if (hi >= LO && hi > 0.0) {
+            if (!pass) {
+              const long long ss = b < nb ? h[b] : 0;
+              const long long is = warp_incl_scan(ss, lane) + carry_s;
+              if (b < nb) {
+                if (cc > 0 && ic < nv) {
+                  double g, lo, hi;
+                  screen_gain(is, ts, ic, nv, scale, S, g, lo, hi);
+                  cand[2 * b] = g;
+                  cand[2 * b + 1] = hi - g;
+                  best_lo = fmax(best_lo, lo);
+                } else {
+                  cand[2 * b] = NAN;
+                }
+              }
+              carry_s = __shfl_sync(0xffffffffu, is, 31);
+            } else if (b < nb && cc > 0 && ic < nv) {
+              const double g = cand[2 * b], dl = cand[2 * b + 1];
+              const double hi = g + dl;
+              if (hi >= LO && hi > 0.0) {
                 ++count;
                 if (g > bg || (g == bg && b < bb)) {
                   bg = g;
-                  bl = lo;
+                  bl = g - dl;
                   bb = b;
+                  blc = ic;
                 }
               }
             }
             carry_c = __shfl_sync(0xffffffffu, ic, 31);
-            carry_s = __shfl_sync(0xffffffffu, is, 31);
           }
           if (!pass) {
             best_lo = warp_max_d(best_lo);
@@ -1557,10 +1589,12 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               const double og = __shfl_xor_sync(0xffffffffu, bg, o);
               const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
               const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+              const int olc = __shfl_xor_sync(0xffffffffu, blc, o);
               if (og > bg || (og == bg && ob < bb)) {
                 bg = og;
                 bl = ol;
                 bb = ob;
+                blc = olc;
               }
             }
             if (lane == 0) {
@@ -1569,6 +1603,10 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               w.best_lo = bl;
               w.best_bin = count ? bb : -1;
               w.flag = count > 0;
+              w.count = count;
+              w.best_lc = blc;
+              w.eq = 0;
+              w.pad_ = 0;
               s_win[k * nrep + j] = w;
               if (count) atomicAdd(&nd.wcount, count);
             }
@@ -1576,6 +1614,76 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
         __syncthreads();
       }
+      // ---- tie classes: a window whose candidates (one per feature, equal left counts) come
+      // from features whose presorted orders coincide on the node's rows has one reference
+      // gain for all of them (identical folds), so the lowest feature wins by strict > without
+      // any fold. Check order equivalence against the lowest window feature in parallel.
+      if (tid == 0) s_neq = 0;
+      __syncthreads();
+      if (tid < nl) {
+        const int k = tid;
+        ResNode& nd = s_nodes[first + k];
+        nd.eqf0 = -1;
+        if (nd.state == 0 && nd.build != 0 && nd.wcount >= 2) {
+          const WinRec* w = s_win + k * nrep;
+          int f0 = -1, lc0 = -1;
+          bool ok = true;
+          for (int j = 0; j < nrep && ok; ++j) {
+            if (!w[j].flag) continue;
+            if (w[j].count != 1) ok = false;
+            if (f0 < 0) {
+              f0 = j;
+              lc0 = w[j].best_lc;
+            } else if (w[j].best_lc != lc0) {
+              ok = false;
+            }
+          }
+          if (ok && f0 >= 0 && w[f0].best_lo > 0.0) {
+            nd.eqf0 = f0;
+            for (int j = f0 + 1; j < nrep; ++j)
+              if (w[j].flag) s_items[atomicAdd(&s_neq, 1)] = (first + k) << 16 | j;
+          }
+        }
+      }
+      __syncthreads();
+      for (int it = warp; it < s_neq; it += kResThreads / 32) {
+        const int s = s_items[it] >> 16, g = s_items[it] & 0xFFFF;
+        const ResNode& nd = s_nodes[s];
+        const int f0 = nd.eqf0, nv = nd.n;
+        const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(f0) * n;
+        const uint8_t* cf = s_codes + static_cast<size_t>(f0) * n;
+        const uint8_t* cg = s_codes + static_cast<size_t>(g) * n;
+        int pf = -1, pg = -1, seen = 0;
+        bool bad = false;
+        int p_next = lane < n ? L[lane] : 0;
+        for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
+          const int i = i0 + lane;
+          const int p = p_next;
+          p_next = i + 32 < n ? L[i + 32] : 0;
+          const bool mem = i < n && s_node[p] == s;
+          const int a = mem ? cf[p] : 0, b = mem ? cg[p] : 0;
+          const unsigned m = __ballot_sync(0xffffffffu, mem);
+          seen += __popc(m);
+          const unsigned lt = m & ((1u << lane) - 1u);
+          const int src = lt ? 31 - __clz(lt) : lane;
+          int qa = __shfl_sync(0xffffffffu, a, src), qb = __shfl_sync(0xffffffffu, b, src);
+          if (!lt) {
+            qa = pf;
+            qb = pg;
+          }
+          // along feature f0's order (codes non-decreasing) feature g must tie exactly where f0
+          // ties and increase where f0 increases
+          if (mem && qa >= 0 && ((a == qa) != (b == qb) || b < qb)) bad = true;
+          if (m) {
+            const int last = 31 - __clz(m);
+            pf = __shfl_sync(0xffffffffu, a, last);
+            pg = __shfl_sync(0xffffffffu, b, last);
+          }
+        }
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) s_win[(s - first) * nrep + g].eq = !bad;
+      }
+      __syncthreads();
       // ---- decide (decide_kernel) ------------------------------------------------------------
       if (tid == 0) s_nitems = 0;
       __syncthreads();
@@ -1585,26 +1693,30 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         if (nd.state == 0 && nd.build != 0) {
           const WinRec* w = s_win + k * nrep;
           bool done = false;
+          int pick = -1;
           if (nd.wcount == 0) {
             nd.state = kNodeLeaf;
             done = true;
           } else if (nd.wcount == 1) {
-            for (int j = 0; j < nrep; ++j) {
-              if (!w[j].flag) continue;
-              if (w[j].best_lo > 0.0) {
-                nd.state = kNodeSplit;
-                nd.rep = j;
-                nd.bin = w[j].best_bin;
-                nd.gain = w[j].best_g;
-                const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
-                int lc = 0;
-                for (int b = 0; b <= nd.bin; ++b) lc += c[b];
-                nd.lc = lc;
-                atomicAdd(&s_cnt[0], 1ull);
-                done = true;
+            for (int j = 0; j < nrep; ++j)
+              if (w[j].flag) {
+                if (w[j].best_lo > 0.0) pick = j;
+                break;
               }
-              break;
-            }
+          } else if (nd.eqf0 >= 0) {
+            bool all = true;
+            for (int j = nd.eqf0 + 1; j < nrep; ++j)
+              if (w[j].flag && !w[j].eq) all = false;
+            if (all) pick = nd.eqf0;
+          }
+          if (pick >= 0) {
+            nd.state = kNodeSplit;
+            nd.rep = pick;
+            nd.bin = w[pick].best_bin;
+            nd.gain = w[pick].best_g;
+            nd.lc = w[pick].best_lc;
+            atomicAdd(&s_cnt[0], 1ull);
+            done = true;
           }
           if (!done) {
             nd.state = kNodeExact;
@@ -1717,7 +1829,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           const int j = nd.rep;
           const int orig = rep_orig[fd.rep0 + j];
           double thr = vals[fd.bin0 + s_repb[j] + nd.bin];
-          if (thr == 0.0) {  // +0.0 / -0.0 share a bin: the last left element's own value
+          if (thr == 0.0 && fd.negz) {  // +0.0 / -0.0 share a bin: the last left element's own value
             const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(j) * n;
             for (int i = cle[fd.bin0 + s_repb[j] + nd.bin] - 1; i >= 0; --i)
               if (s_node[L[i]] == s) {
@@ -2106,17 +2218,21 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   uint64_t* hash_all = ar.alloc<uint64_t>(static_cast<size_t>(F) * std::max(d, 1));
   FS_CUDA(cudaMemsetAsync(nb_all, 0, static_cast<size_t>(F) * std::max(d, 1) * sizeof(int32_t), s));
   FS_CUDA(cudaMemsetAsync(hash_all, 0, static_cast<size_t>(F) * std::max(d, 1) * sizeof(uint64_t), s));
+  int* negz_d = ar.alloc<int>(F);
+  FS_CUDA(cudaMemsetAsync(negz_d, 0, F * sizeof(int), s));
   if (d > 0) {
     const size_t smem = 32 * kHashSlots * 8 + 32 * kSmallBins * 8 + 32 * 4 * 2 + 32 * 8;
     FS_CUDA(cudaFuncSetAttribute(distinct_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     ProfScope prof(dev, "fit_distinct");
     distinct_small_kernel<<<dim3(static_cast<unsigned>(ceil_div(d, 32)), F), 256, smem, s>>>(
-        x_d, d, fam_d, codes_all, vals_all, nb_all, hash_all, dev->err_d);
+        x_d, d, fam_d, codes_all, vals_all, nb_all, hash_all, dev->err_d, negz_d);
     dev->count_launch();
   }
   raise_deferred(dev->take_errors());
   std::vector<int32_t> nb = download(nb_all, static_cast<size_t>(F) * d, s);
+  const std::vector<int> negz = download(negz_d, static_cast<size_t>(F), s);
+  for (int f = 0; f < F; ++f) fam[static_cast<size_t>(f)].negz = negz[static_cast<size_t>(f)];
   std::vector<LargeItem> large;
   int64_t vl = 0;
   for (int f = 0; f < F; ++f)

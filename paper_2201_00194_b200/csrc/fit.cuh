@@ -46,7 +46,7 @@ struct FamDesc {
   int32_t min_split;
   int32_t f0rep;  // rep index of original feature 0, -1 if feature 0 is constant
   int32_t level_slots;  // 2^(depth-1) (max histogrammed nodes per level), >= 1
-  int32_t pad_;
+  int32_t negz;         // some feature value is -0.0 (thresholds then need the exact row value)
   double lr;
 };
 
@@ -92,6 +92,10 @@ struct WinRec {
   double best_lo;
   int32_t best_bin;
   int32_t flag;     // feature has >= 1 candidate in the node's window
+  int32_t count;    // window candidates of this feature
+  int32_t best_lc;  // left count of the best candidate
+  int32_t eq;       // order-equivalent (within the node) to the node's lowest window feature
+  int32_t pad_;
 };
 
 }  // namespace fit

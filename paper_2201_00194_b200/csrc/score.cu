@@ -25,9 +25,61 @@ static void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* f
   launch_rank(dev, nseg, seg, scores_d, perm_d);
 }
 
+// pairwise_accuracy's pair count (costmodel.cpp:255-276): credit is counted in half units, so
+// the device sum is an exact integer and the result is independent of summation order.
+__global__ void pair_count_kernel(const double* __restrict__ s, const double* __restrict__ lat, int64_t m,
+                                  unsigned long long* __restrict__ acc) {
+  unsigned long long half = 0, counted = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double li = lat[i], si = s[i];
+    for (int64_t j = i + 1; j < m; ++j) {
+      const double lj = lat[j];
+      const double rel = fs_div(fabs(fs_sub(li, lj)), li < lj ? lj : li);
+      if (rel < 1e-6) continue;
+      ++counted;
+      const double sj = s[j];
+      if (si == sj) half += 1;
+      else if ((si < sj) == (li < lj)) half += 2;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    half += __shfl_down_sync(0xffffffffu, half, o);
+    counted += __shfl_down_sync(0xffffffffu, counted, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc, half);
+    atomicAdd(acc + 1, counted);
+  }
+}
+
 }  // namespace fs
 
 extern "C" {
+
+int fs_pairwise_accuracy(fs_device* dev, int64_t m, const double* scores, const double* latency, double* out) {
+  return fs::guard([&] {
+    if (!dev || !out || m < 0) fs::fail(FS_EINVAL, "fs_pairwise_accuracy: bad arguments");
+    if (m < 2) fs::fail(FS_EINVAL, "pairwise_accuracy: need at least two validation records");
+    dev->activate();
+    auto* buf = static_cast<unsigned char*>(dev->scratch(fs::kSlotH2D0, static_cast<size_t>(m) * 16 + 64));
+    auto* sd = reinterpret_cast<double*>(buf);
+    auto* ld = sd + m;
+    auto* acc = reinterpret_cast<unsigned long long*>(ld + m);
+    FS_CUDA(cudaMemcpyAsync(sd, scores, m * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    FS_CUDA(cudaMemcpyAsync(ld, latency, m * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    FS_CUDA(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), dev->stream));
+    const int grid = static_cast<int>(std::min<int64_t>(fs::ceil_div(m, 256), dev->sm_count * 8));
+    fs::pair_count_kernel<<<grid, 256, 0, dev->stream>>>(sd, ld, m, acc);
+    dev->count_launch();
+    FS_CUDA(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    FS_CUDA(cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, dev->stream));
+    FS_CUDA(cudaStreamSynchronize(dev->stream));
+    if (h[1] == 0) fs::fail(FS_EDOMAIN, "pairwise_accuracy: all validation pairs excluded as ties");
+    *out = (static_cast<double>(h[0]) * 0.5) / static_cast<double>(h[1]);
+  });
+}
 
 int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg_h,
                const int32_t* space_of_d, const int32_t* assign_d, int32_t pad_dim, double* scores_d,
