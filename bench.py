@@ -449,35 +449,37 @@ def run_native(args, rank, world, local_rank):
 # ------------------------------------------------------------------------------------------
 # reference CPU arm (oracle/_ref = the unmodified reference core; test/baseline infrastructure)
 # ------------------------------------------------------------------------------------------
-def _ref_round(W, x_tr, models, threads, fams=None):
-    """One round of the reference hot path on host cores: per family featurize+predict+sort of the
-    pool and fit on the training rows, one std::thread-equivalent per family (ctypes drops the GIL)."""
+def _ref_family(W, x_tr, models, f, trees=None):
+    """The reference hot path for one family: featurize + predict + std::sort of its pool
+    (scheduler.cpp:187-192) and a from-scratch fit on its rows (costmodel.cpp:152-222), on the
+    compiled reference (oracle/_ref). Returns (score seconds, fit seconds, trees fitted)."""
     import oracle
 
     r = oracle.ref()
-    F = len(W["families"])
-    fams = list(range(F)) if fams is None else fams
     pool_so, pool_a, pool_seg = W["pool_so"], W["pool_a"], W["pool_seg"]
-    tr_seg, y = W["tr_seg"], W["tr_y"]
-    out = {}
+    a, b = int(pool_seg[f]), int(pool_seg[f + 1])
+    t0 = time.perf_counter()
+    x = np.zeros((b - a, PAD))
+    for sid in np.unique(pool_so[a:b]):
+        rows = np.where(pool_so[a:b] == sid)[0]
+        kn = W["spaces"][sid]
+        x[rows] = r.featurize(kn, pool_a[a:b][rows][:, : len(kn)], PAD)
+    s = models[f].predict(x)
+    r.rank(s)
+    t1 = time.perf_counter()
+    t = trees or W["trees"]
+    ta, tb = int(W["tr_seg"][f]), int(W["tr_seg"][f + 1])
+    m = r.new_model(f, t)
+    m.add_samples(x_tr[ta:tb], W["tr_y"][ta:tb])
+    m.fit()
+    m.free()
+    return t1 - t0, time.perf_counter() - t1, t
 
-    def work(f):
-        a, b = int(pool_seg[f]), int(pool_seg[f + 1])
-        x = np.zeros((b - a, PAD))
-        for sid in np.unique(pool_so[a:b]):
-            rows = np.where(pool_so[a:b] == sid)[0]
-            kn = W["spaces"][sid]
-            x[rows] = r.featurize(kn, pool_a[a:b][rows][:, : len(kn)], PAD)
-        s = models[f].predict(x)
-        perm = r.rank(s)
-        ta, tb = int(tr_seg[f]), int(tr_seg[f + 1])
-        m = r.new_model(f, W["trees"])
-        m.add_samples(x_tr[ta:tb], y[ta:tb])
-        m.fit()
-        out[f] = (perm[:G_TOP], m)
 
-    pending = list(fams)
-    lock = threading.Lock()
+def _parallel(fams, threads, fn):
+    """Run fn(f) for every family on up to `threads` host threads (ctypes releases the GIL),
+    like one std::thread per family. Returns {f: fn(f)}."""
+    pending, out, lock = list(fams), {}, threading.Lock()
 
     def runner():
         while True:
@@ -485,7 +487,7 @@ def _ref_round(W, x_tr, models, threads, fams=None):
                 if not pending:
                     return
                 f = pending.pop(0)
-            work(f)
+            out[f] = fn(f)
 
     ts = [threading.Thread(target=runner) for _ in range(max(1, min(threads, len(fams))))]
     for t in ts:
@@ -493,6 +495,37 @@ def _ref_round(W, x_tr, models, threads, fams=None):
     for t in ts:
         t.join()
     return out
+
+
+def _ref_round(W, x_tr, models, threads, plan):
+    """One (possibly sampled) round on the host cores. plan = (families, tree sample). Full
+    rounds time every family with all trees. Sampled rounds (configs too large to run, e.g. C5
+    at ~0.3 core-hours per family) time the families in `families` with `tree sample` trees and
+    extrapolate linearly in trees and in the family count: per-family time = score + fit * T/t,
+    round = ceil(F / threads) waves of the mean family time. Returns (seconds, extrapolated?)."""
+    fams, t_s = plan
+    F = len(W["families"])
+    t0 = time.perf_counter()
+    res = _parallel(fams, threads, lambda f: _ref_family(W, x_tr, models, f, t_s))
+    wall = time.perf_counter() - t0
+    if len(fams) == F and (t_s is None or t_s >= W["trees"]):
+        return wall, False
+    per = [sc + fi * W["trees"] / t for sc, fi, t in res.values()]
+    waves = math.ceil(F / max(1, min(threads, F)))
+    return waves * (sum(per) / len(per)), True
+
+
+def _ref_plan(W, threads):
+    """Full rounds when a round is cheap enough; else a bounded sample (~10-20 s of CPU work)."""
+    F = len(W["families"])
+    rows = [int(W["tr_seg"][f + 1] - W["tr_seg"][f]) for f in range(F)]
+    # survey probe P1: ~3.8 us per (row x tree) at d=164 on one core (fit dominates)
+    est = max(rows) * W["trees"] * 3.8e-6 * math.ceil(F / max(1, min(threads, F)))
+    if est <= 20.0:
+        return list(range(F)), None
+    big = sorted(range(F), key=lambda f: (-rows[f], f))[: max(1, min(threads, F, 2))]
+    t_s = max(1, min(W["trees"], int(10.0 / (max(rows) * 3.8e-6))))
+    return big, t_s
 
 
 def _ref_models(W, forest, x_tr, threads):
@@ -507,8 +540,12 @@ def _ref_models(W, forest, x_tr, threads):
             m.load(oracle.Ensemble(e.base, e.lr, e.offsets, e.feature, e.threshold, e.left, e.right, e.value))
         else:
             ta, tb = int(W["tr_seg"][f]), int(W["tr_seg"][f + 1])
-            m.add_samples(x_tr[ta:tb], W["tr_y"][ta:tb])
-            m.fit()
+            _, t_s = _ref_plan(W, threads)
+            m2 = r.new_model(f, min(W["trees"], t_s or W["trees"]))
+            m2.add_samples(x_tr[ta:tb], W["tr_y"][ta:tb])
+            m2.fit()
+            m.load(m2.export())
+            m2.free()
         models.append(m)
     return models
 
@@ -516,19 +553,24 @@ def _ref_models(W, forest, x_tr, threads):
 def cpu_baseline(W, forest, x_tr, min_seconds=10.0):
     threads = os.cpu_count() or 1
     models = _ref_models(W, forest, x_tr, threads)
+    plan = _ref_plan(W, threads)
     P = int(W["pool_seg"][-1])
-    rounds, t0 = 0, time.perf_counter()
+    rounds, t_sum, extrap, t0 = 0, 0.0, False, time.perf_counter()
     while True:
-        _ref_round(W, x_tr, models, threads)
+        sec, extrap = _ref_round(W, x_tr, models, threads, plan)
+        t_sum += sec
         rounds += 1
-        el = time.perf_counter() - t0
-        if el >= min_seconds or rounds >= 50:
+        if time.perf_counter() - t0 >= min_seconds or rounds >= 50:
             break
-    cpu = _cpu_model()
-    return {"value": P * rounds / el, "unit": "candidates/s", "cores": min(threads, len(W["families"])),
-            "kind": "reference", "sample": f"{rounds} full round(s) of the workload ({P} candidates scored + "
-            f"{int(W['tr_seg'][-1])} rows refit, T={W['trees']}), one thread per family, oracle/_ref = unmodified "
-            f"reference core (-O3, no -march)", "seconds": el, "host_cpu": cpu, "nproc": os.cpu_count()}
+    fams, t_s = plan
+    sample = (f"{rounds} full round(s) of the workload ({P} candidates scored + {int(W['tr_seg'][-1])} rows refit, "
+              f"T={W['trees']})" if not extrap else
+              f"{rounds} sampled round(s): families {fams} scored in full and fit with {t_s} of {W['trees']} trees, "
+              f"EXTRAPOLATED linearly in trees and family count")
+    return {"value": P * rounds / t_sum, "unit": "candidates/s", "cores": min(threads, len(W["families"])),
+            "kind": "reference", "sample": sample + "; one thread per family; oracle/_ref = unmodified reference "
+            "core (-O3, no -march)", "extrapolated": extrap, "seconds": time.perf_counter() - t0,
+            "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
 
 
 def _cpu_model():
@@ -568,14 +610,14 @@ def run_reference(args, rank, world):
     x_tr = _featurize_host(W, oracle.orc())
     threads = os.cpu_count() or 1
     models = _ref_models(W, None, x_tr, threads)
+    plan = _ref_plan(W, threads)
     P, N, F = int(W["pool_seg"][-1]), int(W["tr_seg"][-1]), len(W["families"])
     for _ in range(args.warmup):
-        _ref_round(W, x_tr, models, threads)
-    times = []
+        _ref_round(W, x_tr, models, threads, plan)
+    times, extrap = [], False
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        _ref_round(W, x_tr, models, threads)
-        times.append(time.perf_counter() - t0)
+        sec, extrap = _ref_round(W, x_tr, models, threads, plan)
+        times.append(sec)
     total = sum(times)
     v = P * args.steps / total
     cores = min(threads, F)
@@ -587,7 +629,8 @@ def run_reference(args, rank, world):
                        "candidates_per_step": P, "train_rows_per_step": N, "trees": W["trees"], "pad_dim": PAD},
             "train_rows_per_s": N * args.steps / total,
             "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": cores, "kind": "reference",
-                             "sample": "full rounds of the workload, one thread per family (oracle/_ref)",
+                             "sample": ("full rounds" if not extrap else f"sampled rounds {plan}, extrapolated")
+                             + " of the workload, one thread per family (oracle/_ref)", "extrapolated": extrap,
                              "host_cpu": _cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 

@@ -126,9 +126,14 @@ class Device:
 
     def counters(self, reset: bool = True) -> dict[str, int]:
         """Device work counters: histogram algorithmic bytes/rows, reference-order folds/nodes."""
-        out = np.zeros(4, np.int64)
-        _check(_lib().fs_device_counters(self.h, _p(out, _capi._i64p), 4, int(reset)))
-        return dict(zip(("hist_bytes", "hist_rows", "exact_chains", "exact_nodes"), (int(v) for v in out)))
+        out = np.zeros(20, np.int64)
+        _check(_lib().fs_device_counters(self.h, _p(out, _capi._i64p), 20, int(reset)))
+        d = dict(zip(("hist_bytes", "hist_rows", "exact_chains", "exact_nodes"), (int(v) for v in out[:4])))
+        names = ("residual", "plan", "hist", "derive", "screen", "tie_class", "decide", "exact_fold", "split",
+                 "partition", "leaves", "mse")
+        if out[4:16].any():
+            d["resident_phase_cycles_cta0"] = {k: int(v) for k, v in zip(names, out[4:16])}
+        return d
 
     # -- per-kernel CUDA-event timing ------------------------------------------------------------
     def profile(self, kernels: str | None):

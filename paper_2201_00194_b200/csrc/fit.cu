@@ -1335,6 +1335,18 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   unsigned long long* s_gabs = reinterpret_cast<unsigned long long*>(sm + Lo.gabs);
   double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
   __shared__ int s_neq;
+  // phase timers (CTA 0, thread 0): where a round's cycles go (fs_device_counters [4..15])
+  __shared__ long long s_ph[12];
+  long long t_prev = clock64();
+  if (threadIdx.x < 12) s_ph[threadIdx.x] = 0;
+#define RES_PHASE(i)                        \
+  do {                                      \
+    if (tid == 0) {                         \
+      const long long t_ = clock64();       \
+      s_ph[i] += t_ - t_prev;               \
+      t_prev = t_;                          \
+    }                                       \
+  } while (0)
   double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
   double* s_pred = reinterpret_cast<double*>(sm + Lo.pred);
   long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
@@ -1403,6 +1415,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const double scale = ldexp(1.0, -shift);
     for (int p = tid; p < n; p += kResThreads) s_fix[p] = __double2ll_rn(ldexp(s_resid[p], shift));
     __syncthreads();
+      RES_PHASE(0);
 
     for (int level = 0; level <= depth; ++level) {
       const int first = (1 << level) - 1, nl = 1 << level;
@@ -1428,6 +1441,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
       }
       __syncthreads();
+      RES_PHASE(1);
       if (level == depth || nrep == 0) break;
       const int ring = level & 1;
       long long* hs = s_hsum + static_cast<size_t>(ring) * ls * bins;
@@ -1494,6 +1508,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           __syncthreads();
         }
       }
+      RES_PHASE(2);
       // ---- siblings by exact subtraction --------------------------------------------------------
       if (level > 0) {
         const long long* hp = s_hsum + static_cast<size_t>(ring ^ 1) * ls * bins;
@@ -1522,6 +1537,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           if (tid == 0) s_nodes[other].absfix = s_nodes[parent].absfix - s_nodes[built].absfix;
         }
         __syncthreads();
+      RES_PHASE(3);
       }
       // ---- screen: warp per (node, feature), lanes over bins. Pass 0 computes every candidate's
       // screened gain and bound once (cached) and the node's max lower bound; pass 1 forms the
@@ -1614,6 +1630,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
         __syncthreads();
       }
+      RES_PHASE(4);
       // ---- tie classes: a window whose candidates (one per feature, equal left counts) come
       // from features whose presorted orders coincide on the node's rows has one reference
       // gain for all of them (identical folds), so the lowest feature wins by strict > without
@@ -1684,6 +1701,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         if (lane == 0) s_win[(s - first) * nrep + g].eq = !bad;
       }
       __syncthreads();
+      RES_PHASE(5);
       // ---- decide (decide_kernel) ------------------------------------------------------------
       if (tid == 0) s_nitems = 0;
       __syncthreads();
@@ -1733,6 +1751,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
       }
       __syncthreads();
+      RES_PHASE(6);
       // ---- reference-order folds (exact_kernel) ------------------------------------------------
       for (int it = warp; it < s_nitems; it += kResThreads / 32) {
         const int s = s_items[it] >> 16, j = s_items[it] & 0xFFFF;
@@ -1775,6 +1794,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
       }
       __syncthreads();
+      RES_PHASE(7);
       // ---- exact decision (exact_decide_kernel) -------------------------------------------------
       if (tid < nl) {
         const int k = tid;
@@ -1853,6 +1873,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
       }
       __syncthreads();
+      RES_PHASE(8);
       // ---- stable partition of each split node's order-0 segment -------------------------------
       for (int k = 0; k < nl; ++k) {
         const int s = first + k;
@@ -1904,6 +1925,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
       }
     }
+      RES_PHASE(9);
     // ---- leaves (leaf_kernel): reference-order total / n, prediction update ------------------
     for (int s = warp; s < slots; s += kResThreads / 32) {
       ResNode& nd = s_nodes[s];
@@ -1934,6 +1956,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       }
     }
     __syncthreads();
+      RES_PHASE(10);
     // ---- commit / early stop (costmodel.cpp:212) and MSE (:215-220) --------------------------
     if (s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0) break;  // uniform (smem)
     double a = 0.0;
@@ -1951,6 +1974,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     }
     ++ntrees;
     __syncthreads();
+      RES_PHASE(11);
   }
   if (tid == 0) {
     st[f].ntrees = ntrees;
@@ -1961,6 +1985,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     atomicAdd(ctr + kCtrHistBytes, c_hist_rows * (static_cast<unsigned long long>(nrep) + 12ull));
     atomicAdd(ctr + kCtrExactChains, s_cnt[2]);
     atomicAdd(ctr + kCtrExactNodes, s_cnt[1]);
+    if (blockIdx.x == 0)
+      for (int i = 0; i < 12; ++i) atomicAdd(ctr + kCtrPhase0 + i, static_cast<unsigned long long>(s_ph[i]));
   }
 }
 

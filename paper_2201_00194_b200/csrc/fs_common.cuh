@@ -66,7 +66,8 @@ enum Counter : int {
   kCtrHistRows,       // rows histogrammed
   kCtrExactChains,    // reference-order folds run (node totals + feature scans)
   kCtrExactNodes,     // nodes re-evaluated in reference order
-  kCtrCount
+  kCtrPhase0,         // resident trainer: SM cycles per phase (kResPhases entries, CTA 0's view)
+  kCtrCount = kCtrPhase0 + 16
 };
 
 // Grows-only stream-ordered device buffer.

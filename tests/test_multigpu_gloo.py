@@ -1,0 +1,88 @@
+"""Host logic of the family-sharded multi-GPU path, on CPU with the gloo backend, world size 2:
+deterministic LPT family assignment, top-g record packing, the all-gather (the one collective)
+and the merge must reproduce the single-process result exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2201_00194_b200 import sharding
+
+G = 8
+
+
+def _workload(seed=0, families=7):
+    rng = np.random.default_rng(seed)
+    sizes = rng.integers(3, 40, families)
+    seg = np.concatenate([[0], np.cumsum(sizes)])
+    scores = np.round(rng.normal(0, 1, seg[-1]), 2)  # ties on purpose
+    perms = []
+    for f in range(families):
+        s = scores[seg[f]:seg[f + 1]]
+        perms.append(np.lexsort((np.arange(len(s)), s)))  # (score, index) order
+    return sizes, seg, scores, np.concatenate(perms)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sizes, seg, scores, perm = _workload()
+    owner = sharding.assign_families([sharding.family_cost(n, n, 100) for n in sizes], world)
+    mine = [f for f in range(len(sizes)) if owner[f] == rank]
+    # this rank's segments, as its device would hold them
+    sub_seg = np.concatenate([[0], np.cumsum([sizes[f] for f in mine])]) if mine else np.zeros(1, np.int64)
+    sub_scores = np.concatenate([scores[seg[f]:seg[f + 1]] for f in mine]) if mine else np.zeros(0)
+    sub_perm = np.concatenate([perm[seg[f]:seg[f + 1]] for f in mine]) if mine else np.zeros(0, np.int64)
+    # fixed-size contribution: every rank sends max_families_per_rank blocks
+    per_rank = max(sum(1 for f in range(len(sizes)) if owner[f] == r) for r in range(world))
+    rec = sharding.pack_topk(mine, sub_seg, sub_perm, sub_scores, G)
+    pad = np.full(((per_rank - len(mine)) * G, sharding.RECORD_FIELDS), -1.0)
+    mine_t = torch.from_numpy(np.concatenate([rec, pad]))
+    out = [torch.empty_like(mine_t) for _ in range(world)]
+    dist.all_gather(out, mine_t)
+    merged = sharding.merge_topk(torch.cat(out).numpy(), G)
+    q.put((rank, {k: v.tolist() for k, v in merged.items()}, owner))
+    dist.destroy_process_group()
+
+
+def test_assignment_is_deterministic_and_balanced():
+    costs = [sharding.family_cost(n, n, 100) for n in (2048, 2048, 108, 96, 24, 2048, 500)]
+    a = sharding.assign_families(costs, 2)
+    assert a == sharding.assign_families(costs, 2)
+    loads = [sum(c for c, r in zip(costs, a) if r == k) for k in range(2)]
+    assert max(loads) - min(loads) <= max(costs)
+    assert sharding.assign_families(costs, 1) == [0] * len(costs)
+
+
+@pytest.mark.timeout(120)
+def test_gloo_world2_topk_allgather_matches_single_process():
+    sizes, seg, scores, perm = _workload()
+    single = sharding.merge_topk(sharding.pack_topk(list(range(len(sizes))), seg, perm, scores, G), G)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=90) for _ in procs]
+    for p in procs:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    for rank, merged, owner in results:
+        assert sorted(set(owner)) == [0, 1]
+        assert list(merged) == list(single)
+        for f, recs in merged.items():
+            assert np.array_equal(np.array(recs), single[f]), (rank, f)
