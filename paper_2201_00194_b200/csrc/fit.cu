@@ -865,6 +865,90 @@ struct ExactItem {
   int16_t rep;  // -1: node total
 };
 
+// Tie classes: a node whose window holds exactly one candidate per feature, all with the same
+// left count, is one tie class if every window feature orders the node's rows exactly like the
+// lowest one (identical folds, identical reference gains; strict > keeps the lowest feature).
+// Prep queues one order-equivalence check per (node, other window feature).
+__global__ void tieclass_prep_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                     NodeRec* __restrict__ nodes, int level, const WinRec* __restrict__ win,
+                                     int nrep_max, int level_slots_max, ExactItem* __restrict__ items,
+                                     int* __restrict__ n_items) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  nd.eqf0 = -1;
+  if (nd.state != 0 || nd.build == 0 || nd.wcount < 2) return;
+  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
+  int f0 = -1, lc0 = -1;
+  for (int jj = 0; jj < fd.nrep; ++jj) {
+    if (!w[jj].flag) continue;
+    if (w[jj].count != 1) return;
+    if (f0 < 0) {
+      f0 = jj;
+      lc0 = w[jj].best_lc;
+    } else if (w[jj].best_lc != lc0) {
+      return;
+    }
+  }
+  if (f0 < 0 || !(w[f0].best_lo > 0.0)) return;
+  nd.eqf0 = f0;
+  for (int jj = f0 + 1; jj < fd.nrep; ++jj)
+    if (w[jj].flag) items[atomicAdd(n_items, 1)] = {f, static_cast<int16_t>(s), static_cast<int16_t>(jj)};
+}
+
+// One warp per check: walk the lowest window feature's presorted list restricted to the node;
+// the other feature must tie exactly where it ties and increase where it increases.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) tieclass_check_kernel(
+    const FamDesc* __restrict__ fam, const NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const int32_t* __restrict__ ord, const int16_t* __restrict__ nodeid, WinRec* __restrict__ win, int nrep_max,
+    int level_slots_max) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int total = *n_items;
+  for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < total; wi += warps) {
+    const ExactItem it = items[wi];
+    const FamDesc fd = fam[it.fam];
+    const NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int f0 = nd.eqf0, g = it.rep, nv = nd.n, n = fd.n;
+    const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(f0) * n;
+    int pf = -1, pg = -1, seen = 0;
+    bool bad = false;
+    int p_next = lane < n ? L[lane] : 0;
+    for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
+      const int i = i0 + lane;
+      const int p = p_next;
+      p_next = i + 32 < n ? L[i + 32] : 0;
+      const bool mem = i < n && nodeid[fd.pos0 + p] == it.slot;
+      const int a = mem ? static_cast<int>(codes_c[(fd.pos0 + p) * Dp + f0]) : 0;
+      const int b = mem ? static_cast<int>(codes_c[(fd.pos0 + p) * Dp + g]) : 0;
+      const unsigned m = __ballot_sync(0xffffffffu, mem);
+      seen += __popc(m);
+      const unsigned lt = m & ((1u << lane) - 1u);
+      const int src = lt ? 31 - __clz(lt) : lane;
+      int qa = __shfl_sync(0xffffffffu, a, src), qb = __shfl_sync(0xffffffffu, b, src);
+      if (!lt) {
+        qa = pf;
+        qb = pg;
+      }
+      if (mem && qa >= 0 && ((a == qa) != (b == qb) || b < qb)) bad = true;
+      if (m) {
+        const int last = 31 - __clz(m);
+        pf = __shfl_sync(0xffffffffu, a, last);
+        pg = __shfl_sync(0xffffffffu, b, last);
+      }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    const int local = it.slot - ((1 << level) - 1);
+    if (lane == 0) win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + g].eq = !bad;
+  }
+}
+
 // Decide screened nodes; queue the rest for reference-order re-evaluation.
 __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                               NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
@@ -884,25 +968,30 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
     nd.state = kNodeLeaf;
     return;
   }
+  int pick = -1;
   if (nd.wcount == 1) {
-    for (int jj = 0; jj < fd.nrep; ++jj) {
-      if (!w[jj].flag) continue;
-      if (w[jj].best_lo > 0.0) {
-        nd.state = kNodeSplit;
-        nd.rep = jj;
-        nd.bin = w[jj].best_bin;
-        nd.gain = w[jj].best_g;
-        const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins +
-                           rep_boff[fd.rep0 + jj];
-        int lc = 0;
-        for (int b = 0; b <= nd.bin; ++b) lc += hcnt[hb + b];
-        nd.lc = lc;
-        atomicAdd(&const_cast<FamState*>(st)[f].screened, 1ull);
-        return;
+    for (int jj = 0; jj < fd.nrep; ++jj)
+      if (w[jj].flag) {
+        if (w[jj].best_lo > 0.0) pick = jj;
+        break;
       }
-      break;
-    }
+  } else if (nd.eqf0 >= 0) {  // one tie class: the lowest feature wins by strict >
+    bool all = true;
+    for (int jj = nd.eqf0 + 1; jj < fd.nrep; ++jj)
+      if (w[jj].flag && !w[jj].eq) all = false;
+    if (all) pick = nd.eqf0;
   }
+  if (pick >= 0) {
+    nd.state = kNodeSplit;
+    nd.rep = pick;
+    nd.bin = w[pick].best_bin;
+    nd.gain = w[pick].best_g;
+    nd.lc = w[pick].best_lc;
+    atomicAdd(&const_cast<FamState*>(st)[f].screened, 1ull);
+    return;
+  }
+  (void)hcnt;
+  (void)rep_boff;
   nd.state = kNodeExact;
   atomicAdd(&const_cast<FamState*>(st)[f].exact, 1ull);
   int k = 1;
@@ -914,6 +1003,42 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
   int o = 1;
   for (int jj = 0; jj < fd.nrep; ++jj)
     if (w[jj].flag) items[base + o++] = {f, static_cast<int16_t>(s), static_cast<int16_t>(jj)};
+}
+
+// sum_residuals (costmodel.cpp:36-40) of v[idx[0..n)) in list order by one warp: four chunks of
+// 32 gathers are in flight at once, then each chunk's values are added in lane order (shuffles
+// hoisted ahead of the dependent add chain). Every lane returns the sum.
+__device__ __forceinline__ double warp_fold_gather(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                   int n) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    double x[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 32 * c + lane;
+      x[c] = i < n ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int base = i0 + 32 * c;
+      if (base >= n) break;
+      const int m = min(32, n - base);
+      if (m == 32) {
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          double t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
+        }
+      } else {
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
+      }
+    }
+  }
+  return s;
 }
 
 // One warp per item: reference-order folds. Item rep < 0: node total over the order-0 list
@@ -936,13 +1061,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
     NodeRec& nd = nodes[fd.node0 + it.slot];
     const int n = nd.n;
     if (it.rep < 0) {
-      double s = 0.0;
-      const int32_t* L = ord_cur + fd.pos0 + nd.seg;
-      for (int i0 = 0; i0 < n; i0 += 32) {
-        const double v = i0 + lane < n ? resid[fd.pos0 + L[i0 + lane]] : 0.0;
-        const int m = min(32, n - i0);
-        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, v, l));
-      }
+      const double s = warp_fold_gather(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, n);
       if (lane == 0) nd.total = s;
       continue;
     }
@@ -952,29 +1071,42 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
     double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
     double left = 0.0;
     int prev = -1, seen = 0;
-    for (int i0 = 0; i0 < fd.n && seen < n; i0 += 32) {
-      const int i = i0 + lane;
-      int p = 0, code = 0;
-      double rv = 0.0;
-      bool mem = false;
-      if (i < fd.n) {
-        p = L[i];
-        mem = nodeid[fd.pos0 + p] == it.slot;
-        if (mem) {
-          code = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + jj]);
-          rv = resid[fd.pos0 + p];
-        }
+    // 4 chunks of 32 list entries in flight: index loads, then the dependent gathers
+    for (int i0 = 0; i0 < fd.n && seen < n; i0 += 128) {
+      int p[4], code[4];
+      double rv[4];
+      bool mem[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) p[c] = i0 + 32 * c + lane < fd.n ? L[i0 + 32 * c + lane] : -1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mem[c] = p[c] >= 0 && nodeid[fd.pos0 + p[c]] == it.slot;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        code[c] = mem[c] ? static_cast<int>(codes_c[(fd.pos0 + p[c]) * Dp + jj]) : 0;
+        rv[c] = mem[c] ? resid[fd.pos0 + p[c]] : 0.0;
       }
-      unsigned m = __ballot_sync(0xffffffffu, mem);
-      seen += __popc(m);
-      while (m) {
-        const int l = __ffs(m) - 1;
-        m &= m - 1;
-        const int c = __shfl_sync(0xffffffffu, code, l);
-        const double v = __shfl_sync(0xffffffffu, rv, l);
-        if (prev >= 0 && c != prev && lane == 0) out[prev] = left;  // boundary after bin `prev`
-        left = fs_add(left, v);
-        prev = c;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, mem[c]);
+        seen += __popc(m);
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          if (!((m >> l0) & 0xFFu)) continue;
+          int cc[8];
+          double vv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            cc[k] = __shfl_sync(0xffffffffu, code[c], l0 + k);
+            vv[k] = __shfl_sync(0xffffffffu, rv[c], l0 + k);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if ((m >> (l0 + k)) & 1u) {
+              if (prev >= 0 && cc[k] != prev && lane == 0) out[prev] = left;  // boundary after bin `prev`
+              left = fs_add(left, vv[k]);
+              prev = cc[k];
+            }
+          }
+        }
       }
     }
   }
@@ -1150,12 +1282,7 @@ __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamSta
   if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
   const int n = nd.n;
   const int32_t* L = ord_cur + fd.pos0 + nd.seg;
-  double sum = 0.0;
-  for (int i0 = 0; i0 < n; i0 += 32) {
-    const double v = i0 + lane < n ? resid[fd.pos0 + L[i0 + lane]] : 0.0;
-    const int m = min(32, n - i0);
-    for (int l = 0; l < m; ++l) sum = fs_add(sum, __shfl_sync(0xffffffffu, v, l));
-  }
+  const double sum = warp_fold_gather(resid + fd.pos0, L, n);
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
   for (int i = lane; i < n; i += 32) {
@@ -1295,6 +1422,33 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(L.ls) * bins * 16);
   L.total = o;
   return L;
+}
+
+// sum_residuals (costmodel.cpp:36-40) over a shared-memory index list, by ONE thread: the fold
+// order is the list order and every add is rounded separately. Loads of the next 8 elements are
+// issued before the current 8 adds, so the loop runs at the FP64 add latency instead of the
+// load latency.
+__device__ __forceinline__ double fold_seq(const double* __restrict__ v, const uint16_t* __restrict__ idx, int n) {
+  double s = 0.0;
+  int i = 0;
+  if (n >= 8) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = v[idx[k]];
+    for (i = 8; i + 8 <= n; i += 8) {
+      double b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[k] = v[idx[i + k]];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = b[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+  }
+  for (; i < n; ++i) s = fs_add(s, v[idx[i]]);
+  return s;
 }
 
 __device__ __forceinline__ double warp_max_d(double v) {
@@ -1758,13 +1912,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         ResNode& nd = s_nodes[s];
         const int nv = nd.n;
         if (j == 0xFFFF) {
-          double sum = 0.0;
-          for (int i0 = 0; i0 < nv; i0 += 32) {
-            const double v = i0 + lane < nv ? s_resid[s_ord0[nd.seg + i0 + lane]] : 0.0;
-            const int m = min(32, nv - i0);
-            for (int l = 0; l < m; ++l) sum = fs_add(sum, __shfl_sync(0xffffffffu, v, l));
-          }
-          if (lane == 0) nd.total = sum;
+          if (lane == 0) nd.total = fold_seq(s_resid, s_ord0 + nd.seg, nv);
           continue;
         }
         const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(j) * n;
@@ -1780,16 +1928,26 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           const bool mem = i < n && s_node[p] == s;
           const int code = mem ? cj[p] : 0;
           const double rv = mem ? s_resid[p] : 0.0;
-          unsigned m = __ballot_sync(0xffffffffu, mem);
+          const unsigned m = __ballot_sync(0xffffffffu, mem);
           seen += __popc(m);
-          while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            const int cc = __shfl_sync(0xffffffffu, code, l);
-            const double v = __shfl_sync(0xffffffffu, rv, l);
-            if (prev >= 0 && cc != prev && lane == 0) out[prev] = left;
-            left = fs_add(left, v);
-            prev = cc;
+          // members in lane order; shuffles hoisted ahead of the dependent add chain
+          for (int l0 = 0; l0 < 32; l0 += 8) {
+            if (!((m >> l0) & 0xFFu)) continue;
+            int cc[8];
+            double vv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              cc[k] = __shfl_sync(0xffffffffu, code, l0 + k);
+              vv[k] = __shfl_sync(0xffffffffu, rv, l0 + k);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if ((m >> (l0 + k)) & 1u) {
+                if (prev >= 0 && cc[k] != prev && lane == 0) out[prev] = left;
+                left = fs_add(left, vv[k]);
+                prev = cc[k];
+              }
+            }
           }
         }
       }
@@ -1874,54 +2032,54 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       }
       __syncthreads();
       RES_PHASE(8);
-      // ---- stable partition of each split node's order-0 segment -------------------------------
-      for (int k = 0; k < nl; ++k) {
-        const int s = first + k;
-        const ResNode& nd = s_nodes[s];
-        if (nd.state != kNodeSplit) continue;
-        const int nv = nd.n, seg = nd.seg, lc = nd.lc, bin = nd.bin;
-        const uint8_t* cj = s_codes + static_cast<size_t>(nd.rep) * n;
-        for (int i = tid; i < nv; i += kResThreads) s_scr[i] = s_ord0[seg + i];
-        if (tid == 0) {
-          s_base_l = 0;
-          s_base_r = 0;
-        }
-        __syncthreads();
-        const uint8_t cl = static_cast<uint8_t>(2 * s + 1), cr = static_cast<uint8_t>(2 * s + 2);
-        for (int t0 = 0; t0 < nv; t0 += kResThreads) {
-          const int i = t0 + tid;
-          int p = 0;
-          bool left = false;
-          if (i < nv) {
-            p = s_scr[i];
-            left = cj[p] <= bin;
-          }
-          const unsigned bal = __ballot_sync(0xffffffffu, left);
-          if (lane == 0) s_wsum[warp] = __popc(bal);
+      // ---- stable partition of every split node's order-0 segment (costmodel.cpp:94-105 for
+      // list 0) in one sweep over the whole list: a block-wide exclusive scan of "goes left"
+      // flags; its value at the node's segment start turns it into the rank inside the node
+      // (segments are contiguous). Pass 0 records the per-node scan bases, pass 1 scatters.
+      {
+        int nsplit = 0;
+        for (int k = 0; k < nl; ++k) nsplit += s_nodes[first + k].state == kNodeSplit;
+        if (nsplit) {
+          for (int i = tid; i < n; i += kResThreads) s_scr[i] = s_ord0[i];
           __syncthreads();
-          if (warp == 0) {
-            const int v = s_wsum[lane];
-            s_wsum[lane] = warp_incl_scan(v, lane) - v;
-          }
-          __syncthreads();
-          const int lrank = s_wsum[warp] + __popc(bal & ((1u << lane) - 1u));
-          if (i < nv) {
-            if (left) {
-              s_ord0[seg + s_base_l + lrank] = static_cast<uint16_t>(p);
-              s_node[p] = cl;
-            } else {
-              s_ord0[seg + lc + s_base_r + (i - t0) - lrank] = static_cast<uint16_t>(p);
-              s_node[p] = cr;
+          for (int pass = 0; pass < 2; ++pass) {
+            if (tid == 0) s_base_l = 0;
+            __syncthreads();
+            for (int t0 = 0; t0 < n; t0 += kResThreads) {
+              const int i = t0 + tid;
+              int p = 0, v = -1;
+              bool left = false;
+              if (i < n) {
+                p = s_scr[i];
+                v = s_node[p];
+                if (s_nodes[v].state != kNodeSplit) v = -1;
+                else left = s_codes[static_cast<size_t>(s_nodes[v].rep) * n + p] <= s_nodes[v].bin;
+              }
+              const unsigned bal = __ballot_sync(0xffffffffu, left);
+              if (lane == 0) s_wsum[warp] = __popc(bal);
+              __syncthreads();
+              if (warp == 0) {
+                const int wv = s_wsum[lane];
+                s_wsum[lane] = warp_incl_scan(wv, lane) - wv;
+              }
+              __syncthreads();
+              const int P = s_base_l + s_wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+              if (v >= 0) {
+                ResNode& nd = s_nodes[v];
+                if (pass == 0) {
+                  if (i == nd.seg) nd.pad_ = P;
+                } else {
+                  const int lrank = P - nd.pad_;
+                  const int dst = left ? nd.seg + lrank : nd.seg + nd.lc + (i - nd.seg) - lrank;
+                  s_ord0[dst] = static_cast<uint16_t>(p);
+                  s_node[p] = static_cast<uint8_t>(left ? 2 * v + 1 : 2 * v + 2);
+                }
+              }
+              __syncthreads();
+              if (tid == kResThreads - 1) s_base_l += s_wsum[31] + __popc(bal);
+              __syncthreads();
             }
           }
-          __syncthreads();
-          if (tid == kResThreads - 1) {
-            const int tile_left = s_wsum[31] + __popc(bal);
-            const int tile = min(kResThreads, nv - t0);
-            s_base_l += tile_left;
-            s_base_r += tile - tile_left;
-          }
-          __syncthreads();
         }
       }
     }
@@ -1933,11 +2091,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       if (s > 0 && s_nodes[(s - 1) >> 1].state != kNodeSplit) continue;
       const int nv = nd.n;
       double sum = 0.0;
-      for (int i0 = 0; i0 < nv; i0 += 32) {
-        const double v = i0 + lane < nv ? s_resid[s_ord0[nd.seg + i0 + lane]] : 0.0;
-        const int m = min(32, nv - i0);
-        for (int l = 0; l < m; ++l) sum = fs_add(sum, __shfl_sync(0xffffffffu, v, l));
-      }
+      if (lane == 0) sum = fold_seq(s_resid, s_ord0 + nd.seg, nv);
+      sum = __shfl_sync(0xffffffffu, sum, 0);
       const double value = fs_div(sum, static_cast<double>(nv));
       const double step = fs_mul(fd.lr, value);
       for (int i = lane; i < nv; i += 32) {
@@ -2131,7 +2286,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   }
   const unsigned chunks = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n_max, kHistChunk)));
 
-  for (int round = 0; round < max_trees; ++round) {
+  // One boosting round = a fixed launch sequence whose arguments never change (the round index
+  // lives on the device in FamState::ntrees), so it is captured once as a CUDA graph and replayed
+  // max_trees times; families that stopped early skip their work inside the kernels.
+  const int64_t l0 = dev->launches;
+  auto round_body = [&]() {
     round_init_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, slots, trees_d);
     FS_CUDA(cudaMemsetAsync(node_abs, 0, static_cast<size_t>(F) * slots * sizeof(int64_t), s));
     residual_kernel<<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, F, n_tot, st_d, rowfam, target_c, pred, resid,
@@ -2167,6 +2326,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                           std::max(nrep_max, 1), level_slots_max, 1);
       }
       FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
+      tieclass_prep_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(
+          fam_d, st_d, nodes, level, win, std::max(nrep_max, 1), level_slots_max, items, n_items);
+      tieclass_check_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, ord,
+                                                           nodeid, win, std::max(nrep_max, 1), level_slots_max);
+      dev->count_launch(2);
+      FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
       decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
                                                                      std::max(nrep_max, 1), level_slots_max, items,
                                                                      n_items, dev->ctr_d);
@@ -2195,7 +2360,32 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
     commit_mse_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred, mse_d, max_trees);
     dev->count_launch(2);
     FS_CUDA(cudaGetLastError());
+  };
+  if (max_trees <= 0) return;
+  if (std::getenv("FAMSEER_NO_GRAPH") != nullptr) {
+    for (int round = 0; round < max_trees; ++round) round_body();
+    return;
   }
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  dev->capturing = true;
+  FS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    round_body();
+  } catch (...) {
+    cudaStreamEndCapture(s, &graph);
+    dev->capturing = false;
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  FS_CUDA(cudaStreamEndCapture(s, &graph));
+  dev->capturing = false;
+  const int64_t per_round = dev->launches - l0;
+  FS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  for (int round = 0; round < max_trees; ++round) FS_CUDA(cudaGraphLaunch(exec, s));
+  dev->launches = l0 + per_round * max_trees;
+  FS_CUDA(cudaGraphExecDestroy(exec));
+  FS_CUDA(cudaGraphDestroy(graph));
 }
 
 }  // namespace

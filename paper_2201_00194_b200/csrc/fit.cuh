@@ -71,6 +71,8 @@ struct NodeRec {
   int32_t lc;       // left count
   int32_t wcount;   // screen window candidates
   int32_t build;    // 1 if its histogram is accumulated directly this level
+  int32_t eqf0;     // lowest window feature when the window may be one tie class, else -1
+  int32_t pad_;
   double gain;      // split gain (reference's value)
   double value;     // leaf value
   double total;     // exact reference-order node total (exact nodes / leaves)

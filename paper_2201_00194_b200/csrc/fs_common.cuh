@@ -87,6 +87,7 @@ struct fs_device {
   unsigned long long* ctr_d = nullptr;  // device work counters (fs_device_counters)
   uint32_t* err_h = nullptr;     // pinned mirror
   int64_t launches = 0;
+  bool capturing = false;  // inside CUDA-graph capture: no event timing
   std::vector<fs::DevBuf> slots;  // scratch, indexed by purpose
 
   // Optional per-kernel CUDA-event timing (fs_device_profile): event pairs recorded on the
@@ -116,7 +117,7 @@ struct ProfScope {
   const char* name;
   cudaEvent_t a = nullptr;
   ProfScope(fs_device* d, const char* n) : dev(d), name(n) {
-    if (dev->prof_wants(name)) {
+    if (!dev->capturing && dev->prof_wants(name)) {
       a = dev->prof_event();
       cudaEventRecord(a, dev->stream);
     }
