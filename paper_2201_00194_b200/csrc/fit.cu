@@ -729,6 +729,123 @@ __global__ void __launch_bounds__(kHistThreads) hist_build_kernel(
   }
 }
 
+// Column-layout histogram build (the default shape). Warp w owns feature group fg = w % NFG
+// (features 32fg .. 32fg+31, lane = feature) and row group w / NFG. A group's bins live in
+// shared memory as [bin][32 lanes], so the 32 updates a warp issues for one row always hit 32
+// different banks (no conflicts, no atomics); row groups own private copies that are summed at
+// the flush. grp_off[f][fg] = entry offset of feature group fg (entries = bins x 32).
+constexpr int kColWarps = 6;
+
+template <typename CodeT>
+__global__ void __launch_bounds__(kColWarps * 32) hist_build_col_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
+    int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
+    const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ grp_off,
+    const int32_t* __restrict__ grp_rg, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
+    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const NodeRec* nd = nodes + fd.node0;
+  int s;
+  if (level == 0) {
+    if (blockIdx.y) return;
+    s = 0;
+  } else {
+    if (blockIdx.y >= (1u << (level - 1))) return;
+    const int parent = (1 << (level - 1)) - 1 + blockIdx.y;
+    if (nd[parent].state != kNodeSplit) return;
+    s = 2 * parent + 1;
+    if (nd[s].build != 1) s += 1;
+    if (nd[s].build != 1) return;
+  }
+  const int n_v = nd[s].n;
+  const int r0 = blockIdx.x * kHistChunk;
+  if (r0 >= n_v) return;
+  const int rows = min(kHistChunk, n_v - r0);
+  const int seg = nd[s].seg;
+  const int local = s - ((1 << level) - 1);
+  const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
+  const int nrep = fd.nrep;
+  const int nfg = (nrep + 31) >> 5;
+  const int32_t* go = grp_off + static_cast<int64_t>(f) * (kColWarps + 1);
+  const int gsz = go[nfg];            // entries per copy
+  const int rg = grp_rg[f];           // row groups (copies)
+  int64_t* s_sum = reinterpret_cast<int64_t*>(smem);                        // [rg][gsz]
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(s_sum + static_cast<int64_t>(rg) * gsz);
+  unsigned char* tail = reinterpret_cast<unsigned char*>(s_cnt + static_cast<int64_t>(rg) * gsz);
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                            // [kHistTileRows][Dp]
+  int64_t* t_fix = reinterpret_cast<int64_t*>(t_codes + kHistTileRows * Dp);  // [kHistTileRows]
+  __shared__ unsigned long long s_abs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < rg * gsz; i += kColWarps * 32) {
+    s_sum[i] = 0;
+    s_cnt[i] = 0;
+  }
+  if (tid == 0) s_abs = 0;
+  const int fg = warp % nfg, rgi = warp / nfg;
+  const bool worker = rgi < rg;
+  const int j = 32 * fg + lane;
+  const bool jv = worker && j < nrep;
+  int64_t* my_sum = s_sum + static_cast<int64_t>(rgi) * gsz + go[fg] + lane;
+  int32_t* my_cnt = s_cnt + static_cast<int64_t>(rgi) * gsz + go[fg] + lane;
+  __syncthreads();
+  const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
+  for (int t0 = 0; t0 < rows; t0 += kHistTileRows) {
+    const int tr = min(kHistTileRows, rows - t0);
+    for (int i = tid; i < tr * vec_per_row; i += kColWarps * 32) {
+      const int r = i / vec_per_row, v = i - r * vec_per_row;
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+      reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+    }
+    unsigned long long a = 0;
+    for (int r = tid; r < tr; r += kColWarps * 32) {
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+      const int64_t v = rfix[p];
+      t_fix[r] = v;
+      a += static_cast<unsigned long long>(v < 0 ? -v : v);
+    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (lane == 0 && a) atomicAdd(&s_abs, a);
+    __syncthreads();
+    if (jv) {
+      for (int r = rgi; r < tr; r += rg) {
+        const int b = static_cast<int>(t_codes[r * Dp + j]);
+        my_sum[b * 32] += t_fix[r];
+        my_cnt[b * 32] += 1;
+      }
+    }
+    __syncthreads();
+  }
+  // flush: entry e = (fg, b, lane) -> global bin boff_j + b
+  for (int e = tid; e < gsz; e += kColWarps * 32) {
+    int g = 0;
+    while (g + 1 < nfg && go[g + 1] <= e) ++g;
+    const int within = e - go[g];
+    const int b = within >> 5, jj = 32 * g + (within & 31);
+    if (jj >= nrep || b >= rep_nb[fd.rep0 + jj]) continue;
+    int64_t sm = 0;
+    int32_t c = 0;
+    for (int k = 0; k < rg; ++k) {
+      sm += s_sum[static_cast<int64_t>(k) * gsz + e];
+      c += s_cnt[static_cast<int64_t>(k) * gsz + e];
+    }
+    if (c) {
+      const int64_t gb = hbase + rep_boff[fd.rep0 + jj] + b;
+      atomicAdd(reinterpret_cast<unsigned long long*>(hsum + gb), static_cast<unsigned long long>(sm));
+      atomicAdd(hcnt + gb, c);
+    }
+  }
+  if (tid == 0) {
+    if (s_abs) atomicAdd(reinterpret_cast<unsigned long long*>(node_abs + fd.node0 + s), s_abs);
+    atomicAdd(ctr + kCtrHistBytes,
+              static_cast<unsigned long long>(rows) * (static_cast<unsigned long long>(nrep) * sizeof(CodeT) + 12ull));
+    atomicAdd(ctr + kCtrHistRows, static_cast<unsigned long long>(rows));
+  }
+}
+
 // sibling = parent - built child (exact: integer histograms)
 __global__ void hist_derive_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                                    const NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
@@ -1378,7 +1495,7 @@ __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_
 
 // groups: private histogram copies used while accumulating one node (threads own
 // (feature, group) pairs, so no shared-memory atomics are needed).
-__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, int groups) {
+__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, int groups, bool pre_smem) {
   ResLayout L;
   L.ls = depth > 0 ? (1 << (depth - 1)) : 1;
   L.slots = (1 << (depth + 1)) - 1;
@@ -1388,8 +1505,8 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(n) * nr);
   L.resid = o;
   o = res_align(o + static_cast<size_t>(n) * 8);
-  L.pred = o;
-  o = res_align(o + static_cast<size_t>(n) * 8);
+  L.pred = o;  // presorted lists [nrep][n] as u16 (when pre_smem), else empty
+  o = res_align(o + (pre_smem ? static_cast<size_t>(n) * nr * 2 : 0));
   L.fix = o;
   o = res_align(o + static_cast<size_t>(n) * 8);
   L.node = o;
@@ -1472,7 +1589,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
     const int32_t* __restrict__ cle, const int32_t* __restrict__ canon, const double* __restrict__ x, int d,
     TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
-    unsigned long long* __restrict__ ctr, int groups) {
+    unsigned long long* __restrict__ ctr, int groups, double* __restrict__ pred_g, int pre_smem) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ unsigned long long s_red[32];
   __shared__ double s_dred[32];
@@ -1482,7 +1599,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const int f = fam_list[blockIdx.x];
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
-  const ResLayout Lo = res_layout(n, nrep, bins, depth, groups);
+  const ResLayout Lo = res_layout(n, nrep, bins, depth, groups, pre_smem != 0);
   uint8_t* s_codes = sm + Lo.codes;  // [nrep][n]
   long long* s_gsum = reinterpret_cast<long long*>(sm + Lo.gsum);  // [groups][bins]
   int* s_gcnt = reinterpret_cast<int*>(sm + Lo.gcnt);
@@ -1502,7 +1619,12 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     }                                       \
   } while (0)
   double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
-  double* s_pred = reinterpret_cast<double*>(sm + Lo.pred);
+  double* s_pred = pred_g + fd.pos0;  // predictions stay in global memory (L2-resident)
+  uint16_t* s_pre = reinterpret_cast<uint16_t*>(sm + Lo.pred);  // presorted lists, if staged
+  const int32_t* g_pre = ord + fd.ord0;
+  auto pre_at = [&](int j, int i) -> int {
+    return pre_smem ? static_cast<int>(s_pre[static_cast<size_t>(j) * n + i]) : g_pre[static_cast<size_t>(j) * n + i];
+  };
   long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
   uint8_t* s_node = sm + Lo.node;
   uint16_t* s_ord0 = reinterpret_cast<uint16_t*>(sm + Lo.ord0);
@@ -1530,6 +1652,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   }
   const double b0 = base[f];
   for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
+  if (pre_smem)
+    for (int i = tid; i < n * nrep; i += kResThreads) s_pre[i] = static_cast<uint16_t>(g_pre[i]);
   if (tid == 0) s_stop = 0;
   __syncthreads();
 
@@ -1821,16 +1945,15 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         const int s = s_items[it] >> 16, g = s_items[it] & 0xFFFF;
         const ResNode& nd = s_nodes[s];
         const int f0 = nd.eqf0, nv = nd.n;
-        const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(f0) * n;
         const uint8_t* cf = s_codes + static_cast<size_t>(f0) * n;
         const uint8_t* cg = s_codes + static_cast<size_t>(g) * n;
         int pf = -1, pg = -1, seen = 0;
         bool bad = false;
-        int p_next = lane < n ? L[lane] : 0;
+        int p_next = lane < n ? pre_at(f0, lane) : 0;
         for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
           const int i = i0 + lane;
           const int p = p_next;
-          p_next = i + 32 < n ? L[i + 32] : 0;
+          p_next = i + 32 < n ? pre_at(f0, i + 32) : 0;
           const bool mem = i < n && s_node[p] == s;
           const int a = mem ? cf[p] : 0, b = mem ? cg[p] : 0;
           const unsigned m = __ballot_sync(0xffffffffu, mem);
@@ -1915,16 +2038,15 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           if (lane == 0) nd.total = fold_seq(s_resid, s_ord0 + nd.seg, nv);
           continue;
         }
-        const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(j) * n;
         double* out = s_lbuf + static_cast<size_t>(s - first) * bins + s_repb[j];
         const uint8_t* cj = s_codes + static_cast<size_t>(j) * n;
         double left = 0.0;
         int prev = -1, seen = 0;
-        int p_next = lane < n ? L[lane] : 0;
+        int p_next = lane < n ? pre_at(j, lane) : 0;
         for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
           const int i = i0 + lane;
           const int p = p_next;
-          p_next = i + 32 < n ? L[i + 32] : 0;
+          p_next = i + 32 < n ? pre_at(j, i + 32) : 0;
           const bool mem = i < n && s_node[p] == s;
           const int code = mem ? cj[p] : 0;
           const double rv = mem ? s_resid[p] : 0.0;
@@ -2082,8 +2204,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           }
         }
       }
-    }
       RES_PHASE(9);
+    }
+      RES_PHASE(1);
     // ---- leaves (leaf_kernel): reference-order total / n, prediction update ------------------
     for (int s = warp; s < slots; s += kResThreads / 32) {
       ResNode& nd = s_nodes[s];
@@ -2195,6 +2318,12 @@ struct ResidentPlan {
   std::vector<int> families;
   size_t smem = 0;
   int groups = 1;
+  bool pre_smem = false;
+  // column-layout histogram plan for the multi-kernel path (hist_build_col_kernel)
+  bool col = false;
+  std::vector<int32_t> col_off;  // [F][kColWarps + 1] entry offsets per feature group
+  std::vector<int32_t> col_rg;   // [F] row groups (private copies)
+  size_t col_smem = 0;
 };
 
 template <typename CodeT>
@@ -2244,7 +2373,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       fit_resident_kernel<<<static_cast<unsigned>(resident.families.size()), kResThreads, resident.smem, s>>>(
           fam_d, st_d, list_d, Dp, reinterpret_cast<const uint8_t*>(codes_c), target_c, base_d, ord, ord_root,
           rep_orig_d, rep_nb_d, rep_boff_d, vals_d, cle, canon, x_d, d, trees_d, mse_d, max_trees, slots, dev->ctr_d,
-          resident.groups);
+          resident.groups, pred, resident.pre_smem ? 1 : 0);
     }
     dev->count_launch();
     FS_CUDA(cudaGetLastError());
@@ -2285,6 +2414,14 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                  static_cast<int>(hist_smem)));
   }
   const unsigned chunks = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n_max, kHistChunk)));
+  int32_t* col_off_d = nullptr;
+  int32_t* col_rg_d = nullptr;
+  if (resident.col) {
+    col_off_d = ar.upload(resident.col_off);
+    col_rg_d = ar.upload(resident.col_rg);
+    FS_CUDA(cudaFuncSetAttribute(hist_build_col_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(resident.col_smem)));
+  }
 
   // One boosting round = a fixed launch sequence whose arguments never change (the round index
   // lives on the device in FamState::ntrees), so it is captured once as a CUDA graph and replayed
@@ -2307,7 +2444,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
       {
         ProfScope prof(dev, "fit_hist_build");
-        if (hist_global)
+        if (resident.col)
+          hist_build_col_kernel<CodeT><<<dim3(chunks, pairs, F), kColWarps * 32, resident.col_smem, s>>>(
+              fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, rep_nb_d, col_off_d, col_rg_d, hsum,
+              hcnt, node_abs, dev->ctr_d);
+        else if (hist_global)
           hist_build_kernel<CodeT, true><<<dim3(chunks, pairs, F), kHistThreads, hist_smem, s>>>(
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, 1, dev->ctr_d);
         else
@@ -2548,33 +2689,81 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     if (mode != "auto" && mode != "resident" && mode != "multi")
       fail(FS_EINVAL, "FAMSEER_FIT_PATH must be auto, resident or multi");
     if (mode != "multi" && code_bytes == 1 && depth_max <= kResMaxDepth) {
-      bool ok = true;
-      const size_t budget = 225 * 1024;
-      int groups = 32;
-      for (int f = 0; f < F; ++f) {
-        const FamDesc& fd = fam[static_cast<size_t>(f)];
-        if (fd.n <= 0 || fd.trees <= 0) continue;
-        if (fd.n > 65535) ok = false;
-        const size_t base_total = res_layout(fd.n, fd.nrep, fd.bins, fd.depth, 0).total;
-        const size_t per = static_cast<size_t>(fd.bins) * 12 + 64;
-        const int fit_g = base_total + per <= budget ? static_cast<int>((budget - base_total) / per) : 0;
-        groups = std::min({groups, fit_g, kResThreads / std::max(1, static_cast<int>(fd.nrep))});
-        res.families.push_back(f);
-      }
-      size_t need = 0;
-      if (groups >= 1)
-        for (int f : res.families) {
+      // Prefer staging the presorted lists in shared memory (reference-order folds and tie-class
+      // scans then never touch HBM/L2); drop them to global memory if that is what it takes to fit.
+      for (const bool pre_smem : {true, false}) {
+        bool ok = true;
+        const size_t budget = 225 * 1024;
+        int groups = 32;
+        std::vector<int> fams_ok;
+        for (int f = 0; f < F; ++f) {
           const FamDesc& fd = fam[static_cast<size_t>(f)];
-          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups).total);
+          if (fd.n <= 0 || fd.trees <= 0) continue;
+          if (fd.n > 65535) ok = false;
+          const size_t base_total = res_layout(fd.n, fd.nrep, fd.bins, fd.depth, 0, pre_smem).total;
+          const size_t per = static_cast<size_t>(fd.bins) * 12 + 64;
+          const int fit_g = base_total + per <= budget ? static_cast<int>((budget - base_total) / per) : 0;
+          groups = std::min({groups, fit_g, kResThreads / std::max(1, static_cast<int>(fd.nrep))});
+          fams_ok.push_back(f);
         }
-      if (ok && groups >= 1 && need <= budget && !res.families.empty()) {
-        res.enabled = true;
-        res.smem = need;
-        res.groups = groups;
+        size_t need = 0;
+        if (groups >= 1)
+          for (int f : fams_ok) {
+            const FamDesc& fd = fam[static_cast<size_t>(f)];
+            need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups, pre_smem).total);
+          }
+        res.families = fams_ok;
+        if (ok && groups >= 1 && need <= budget && !fams_ok.empty()) {
+          res.enabled = true;
+          res.smem = need;
+          res.groups = groups;
+          res.pre_smem = pre_smem;
+          break;
+        }
       }
     }
     if (mode == "resident" && !res.enabled && !res.families.empty())
       fail(FS_EINVAL, "fit: resident path requested but the families do not fit one CTA");
+  }
+  // Column-layout histogram plan (multi-kernel path): per feature group of 32 the largest bin
+  // count; row-group copies while they fit the shared-memory budget.
+  if (!res.enabled && !std::getenv("FAMSEER_HIST_ROWMAJOR")) {
+    const size_t cap = 200 * 1024;
+    const int pv = 16 / code_bytes;
+    const int dp = std::max(pv, static_cast<int>(ceil_div(std::max(nrep_max, 1), pv)) * pv);
+    const size_t tile = ((static_cast<size_t>(kHistTileRows) * dp * code_bytes + 15) & ~size_t(15)) +
+                        kHistTileRows * sizeof(int64_t) + 64;
+    bool ok = true;
+    res.col_off.assign(static_cast<size_t>(F) * (kColWarps + 1), 0);
+    res.col_rg.assign(static_cast<size_t>(F), 1);
+    size_t need = 0;
+    for (int f = 0; f < F && ok; ++f) {
+      const FamDesc& fd = fam[static_cast<size_t>(f)];
+      const int nfg = (fd.nrep + 31) / 32;
+      if (nfg > kColWarps) {
+        ok = false;
+        break;
+      }
+      int32_t off = 0;
+      for (int g = 0; g < nfg; ++g) {
+        int mx = 0;
+        for (int j = 32 * g; j < std::min(fd.nrep, 32 * g + 32); ++j)
+          mx = std::max(mx, rep_nb[static_cast<size_t>(fd.rep0 + j)]);
+        res.col_off[static_cast<size_t>(f) * (kColWarps + 1) + g] = off;
+        off += mx * 32;
+      }
+      for (int g = nfg; g <= kColWarps; ++g) res.col_off[static_cast<size_t>(f) * (kColWarps + 1) + g] = off;
+      const size_t per_copy = static_cast<size_t>(off) * 12;
+      int rg = std::max(1, kColWarps / std::max(1, nfg));
+      while (rg > 1 && rg * per_copy + tile > cap) --rg;
+      if (per_copy + tile > cap) ok = false;
+      res.col_rg[static_cast<size_t>(f)] = rg;
+      need = std::max(need, rg * per_copy + tile);
+    }
+    if (ok) {
+      res.col = true;
+      res.col_smem = need;
+    }
   }
   const int per_vec = 16 / code_bytes;
   const int Dp = std::max(per_vec, static_cast<int>(ceil_div(std::max(nrep_max, 1), per_vec)) * per_vec);

@@ -130,6 +130,7 @@ void compile_model(fs_device* dev, FamilyModel& m) {
   m.leafv_d = upload(leafv, dev->stream);
   m.leafid_d = upload(leafid, dev->stream);
   m.uthr_d = upload(uthr, dev->stream);
+  m.n_uthr = static_cast<int>(uthr.size());
   m.uoff_d = upload(uoff, dev->stream);
   FS_CUDA(cudaStreamSynchronize(dev->stream));
   m.compiled = true;

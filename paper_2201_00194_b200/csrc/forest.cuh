@@ -38,6 +38,7 @@ struct FamilyModel {
   double* leafv_d = nullptr;     // [T][2^depth]
   uint8_t* leafid_d = nullptr;   // [T][2^depth]
   double* uthr_d = nullptr;      // unique thresholds, feature-major
+  int n_uthr = 0;
   int32_t* uoff_d = nullptr;     // [d_model + 1]
   // generic form
   int32_t* g_off_d = nullptr;

@@ -22,12 +22,12 @@ namespace {
 constexpr int kTile = 256;
 constexpr int kChunk = 64;
 
-template <typename CodeT, bool kLeaves>
+template <typename CodeT, bool kLeaves, bool kSmemThr>
 __global__ void __launch_bounds__(kTile) predict_heap_kernel(
     const double* __restrict__ x, int64_t rows, int d, int d_model, int depth, int n_trees, double base,
     double lr, const uint32_t* __restrict__ nodes, const double* __restrict__ leafv,
-    const uint8_t* __restrict__ leafid, const double* __restrict__ uthr, const int32_t* __restrict__ uoff,
-    double* __restrict__ scores, uint8_t* __restrict__ leaf_out, uint32_t* err) {
+    const uint8_t* __restrict__ leafid, const double* __restrict__ uthr_g, const int32_t* __restrict__ uoff_g,
+    int n_uthr, double* __restrict__ scores, uint8_t* __restrict__ leaf_out, uint32_t* err) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int nint = (1 << depth) - 1;
   const int nleaf = 1 << depth;
@@ -40,9 +40,24 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
   uint8_t* s_leafid = smem + off;  // [kChunk][nleaf]
   off += static_cast<size_t>(kChunk) * nleaf;
   uint8_t* s_lbuf = smem + off;  // [kTile][kChunk]
+  off += kLeaves ? static_cast<size_t>(kTile) * kChunk : 0;
+  off = (off + 15) & ~size_t(15);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  // The threshold tables the codes are searched in: staged in shared memory when they fit
+  // (binary-search steps then cost a shared load instead of an L2 round trip).
+  const double* uthr = uthr_g;
+  const int32_t* uoff = uoff_g;
+  if (kSmemThr) {
+    double* su = reinterpret_cast<double*>(smem + off);
+    int32_t* so = reinterpret_cast<int32_t*>(su + n_uthr);
+    for (int i = tid; i < n_uthr; i += kTile) su[i] = __ldg(uthr_g + i);
+    for (int i = tid; i <= d_model; i += kTile) so[i] = __ldg(uoff_g + i);
+    __syncthreads();
+    uthr = su;
+    uoff = so;
+  }
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kTile;
   const int tile_rows = static_cast<int>(rows - row0 < kTile ? rows - row0 : kTile);
 
@@ -53,11 +68,11 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
       const double v = __ldcs(xr + f);  // streamed once
       nonfinite |= !isfinite(v);
       if (f < d_model) {
-        int lo = __ldg(uoff + f), hi = __ldg(uoff + f + 1);
+        int lo = uoff[f], hi = uoff[f + 1];
         const int first = lo;
         while (lo < hi) {  // count of unique thresholds strictly below v
           const int mid = (lo + hi) >> 1;
-          if (__ldg(uthr + mid) < v) lo = mid + 1;
+          if (uthr[mid] < v) lo = mid + 1;
           else hi = mid;
         }
         codes[f * kTile + c] = static_cast<CodeT>(lo - first);
@@ -125,23 +140,35 @@ __global__ void predict_generic_kernel(const double* __restrict__ x, int64_t row
   scores[r] = score;
 }
 
-template <typename CodeT, bool kLeaves>
-void launch_heap(fs_device* dev, const fs::FamilyModel& m, const double* x, int64_t rows, int d, double* scores,
-                 uint8_t* leaf_out) {
+template <typename CodeT, bool kLeaves, bool kSmemThr>
+void launch_heap_impl(fs_device* dev, const fs::FamilyModel& m, const double* x, int64_t rows, int d, double* scores,
+                      uint8_t* leaf_out) {
   const int nint = (1 << m.depth) - 1, nleaf = 1 << m.depth;
   size_t smem = (static_cast<size_t>(m.d_model) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
   smem += static_cast<size_t>(kChunk) * (nleaf * sizeof(double) + nint * sizeof(uint32_t) + nleaf);
   if (kLeaves) smem += static_cast<size_t>(kTile) * kChunk;
-  auto* fn = predict_heap_kernel<CodeT, kLeaves>;
+  smem = (smem + 15) & ~size_t(15);
+  if (kSmemThr) smem += static_cast<size_t>(m.n_uthr) * sizeof(double) + (m.d_model + 1) * sizeof(int32_t);
+  auto* fn = predict_heap_kernel<CodeT, kLeaves, kSmemThr>;
   if (smem > 227 * 1024) fs::fail(FS_EINVAL, "predict: model too wide for the shared-memory tile");
   FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(fs::ceil_div(rows, kTile));
   fs::ProfScope prof(dev, "predict");
   fn<<<grid, kTile, smem, dev->stream>>>(x, rows, d, std::min(m.d_model, d), m.depth, m.n_trees, m.base, m.lr,
-                                         m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, scores, leaf_out,
-                                         dev->err_d);
+                                         m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, m.n_uthr, scores,
+                                         leaf_out, dev->err_d);
   dev->count_launch();
   FS_CUDA(cudaGetLastError());
+}
+
+template <typename CodeT, bool kLeaves>
+void launch_heap(fs_device* dev, const fs::FamilyModel& m, const double* x, int64_t rows, int d, double* scores,
+                 uint8_t* leaf_out) {
+  // thresholds in shared memory when they take <= 48 KB (T <~ 850 at depth 3)
+  if (static_cast<size_t>(m.n_uthr) * sizeof(double) <= 48 * 1024)
+    launch_heap_impl<CodeT, kLeaves, true>(dev, m, x, rows, d, scores, leaf_out);
+  else
+    launch_heap_impl<CodeT, kLeaves, false>(dev, m, x, rows, d, scores, leaf_out);
 }
 
 }  // namespace

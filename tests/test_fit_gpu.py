@@ -14,11 +14,14 @@ CASES = [str(t) for t in G["fit_cases"]]
 TREE_FIELDS = ("offsets", "feature", "threshold", "left", "right", "value")
 
 
-@pytest.fixture(autouse=True, params=["auto", "multi"])
+@pytest.fixture(autouse=True, params=["auto", "multi", "multi_rowmajor"])
 def fit_path(request, monkeypatch):
-    """Every parity test runs on both trainers: the resident one-CTA-per-family kernel (auto picks
-    it when the families fit shared memory) and the multi-kernel round."""
-    monkeypatch.setenv("FAMSEER_FIT_PATH", request.param)
+    """Every parity test runs on every trainer shape: the resident one-CTA-per-family kernel (auto
+    picks it when the families fit shared memory), the multi-kernel round with the column-layout
+    histogram, and the multi-kernel round with the row-major histogram."""
+    monkeypatch.setenv("FAMSEER_FIT_PATH", "auto" if request.param == "auto" else "multi")
+    if request.param == "multi_rowmajor":
+        monkeypatch.setenv("FAMSEER_HIST_ROWMAJOR", "1")
     return request.param
 
 

@@ -76,10 +76,11 @@ def random_forest(rng, d, trees, depth, n_thr=6, ragged=True):
 
 
 @pytest.mark.parametrize("depth,trees,n_thr,d", [(3, 200, 6, 40), (1, 10, 3, 40), (5, 50, 8, 40),
-                                                 (3, 300, 2000, 2), (10, 5, 4, 40)])
+                                                 (3, 300, 2000, 2), (10, 5, 4, 40), (3, 1200, 40000, 2)])
 def test_random_forests_multi_segment(dev, orc, depth, trees, n_thr, d):
     # (3, 300, 2000, 2): >254 distinct thresholds per feature -> 16-bit codes
     # (10, 5, 4, 40): deeper than the heap limit -> generic pre-order kernel
+    # (3, 1200, 40000, 2): > 6144 unique thresholds -> threshold tables searched in global memory
     rng = np.random.default_rng(depth * 100 + trees)
     ens = [random_forest(rng, d, trees, depth, n_thr) for _ in range(3)]
     fo = fs.Forest(dev, 3)
