@@ -133,6 +133,9 @@ class Device:
                  "partition", "leaves", "mse")
         if out[4:16].any():
             d["resident_phase_cycles_cta0"] = {k: int(v) for k, v in zip(names, out[4:16])}
+        if out[16:20].any():
+            d["exact_reasons"] = {k: int(v) for k, v in zip(("multi_candidate_feature", "different_partitions",
+                                                               "orders_differ", "uncertain_sign"), out[16:20])}
         return d
 
     # -- per-kernel CUDA-event timing ------------------------------------------------------------

@@ -1596,6 +1596,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   __shared__ int s_wsum[32];
   __shared__ int s_shift, s_nitems, s_stop, s_base_l, s_base_r;
   __shared__ unsigned long long s_cnt[3];  // screened splits, exact nodes, exact folds
+  __shared__ unsigned long long s_why[4];  // exact-node reasons
   const int f = fam_list[blockIdx.x];
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
@@ -1641,6 +1642,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const int ls = Lo.ls, slots = Lo.slots;
   unsigned long long c_hist_rows = 0;
   if (tid < 3) s_cnt[tid] = 0;
+  if (tid < 4) s_why[tid] = 0;
 
   for (int i = tid; i < n * nrep; i += kResThreads) {
     const int p = i / nrep, j = i - p * nrep;
@@ -2016,6 +2018,23 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           if (!done) {
             nd.state = kNodeExact;
             atomicAdd(&s_cnt[1], 1ull);
+            {  // why the screen could not decide (diagnostics, fs_device_counters [16..19])
+              int why = 3;  // sign of the only candidate uncertain
+              if (nd.wcount >= 2) {
+                why = 2;  // orders not equivalent
+                int lc0 = -1;
+                for (int j = 0; j < nrep; ++j) {
+                  if (!w[j].flag) continue;
+                  if (w[j].count > 1) {
+                    why = 0;  // several window candidates on one feature
+                    break;
+                  }
+                  if (lc0 < 0) lc0 = w[j].best_lc;
+                  else if (w[j].best_lc != lc0) why = 1;  // different partitions
+                }
+              }
+              atomicAdd(&s_why[why], 1ull);
+            }
             int cnt = 1;
             for (int j = 0; j < nrep; ++j) cnt += w[j].flag;
             const int b = atomicAdd(&s_nitems, cnt);
@@ -2265,6 +2284,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     atomicAdd(ctr + kCtrExactNodes, s_cnt[1]);
     if (blockIdx.x == 0)
       for (int i = 0; i < 12; ++i) atomicAdd(ctr + kCtrPhase0 + i, static_cast<unsigned long long>(s_ph[i]));
+    for (int i = 0; i < 4; ++i) atomicAdd(ctr + kCtrPhase0 + 12 + i, s_why[i]);
   }
 }
 

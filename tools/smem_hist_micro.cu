@@ -84,7 +84,35 @@ void run(const char* name, int threads) {
   cudaFree(s);
 }
 
+// dependent FP64 add chain (the reference-order fold's latency floor)
+__global__ void dadd_chain(const double* v, double* out, unsigned long long* cycles) {
+  double s = 0.0, a = v[threadIdx.x], b = v[threadIdx.x + 1];
+  const long long t0 = clock64();
+#pragma unroll 16
+  for (int i = 0; i < 65536; ++i) {
+    s = __dadd_rn(s, a);
+    a = __dadd_rn(a, b) * 0.0 + a;  // keep a live without lengthening the chain
+  }
+  const long long t1 = clock64();
+  out[threadIdx.x] = s;
+  if (threadIdx.x == 0) cycles[0] = t1 - t0;
+}
+
 int main() {
+  {
+    double *v, *o;
+    unsigned long long* c;
+    cudaMalloc(&v, 64 * 8);
+    cudaMalloc(&o, 64 * 8);
+    cudaMalloc(&c, 8);
+    cudaMemset(v, 0, 64 * 8);
+    dadd_chain<<<1, 32>>>(v, o, c);
+    dadd_chain<<<1, 32>>>(v, o, c);
+    unsigned long long h = 0;
+    cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+    std::printf("dependent DADD chain: %.2f cycles per add (upper bound, includes the side chain)\n",
+                double(h) / 65536.0);
+  }
   run<0, 32>("atomic32 x1", 1024);
   run<1, 32>("atomic32 x3 limbs", 1024);
   run<2, 32>("private rmw64 chain", 1024);
