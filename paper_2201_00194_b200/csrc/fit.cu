@@ -846,6 +846,139 @@ __global__ void __launch_bounds__(kColWarps * 32) hist_build_col_kernel(
   }
 }
 
+// Limb-atomic histogram build (the default shape). Only 32-bit shared-memory atomics are native
+// on sm_100a (64-bit ones compile to CAS spin loops), so each 62-bit fixed-point residual v is
+// offset to u = v + 2^62 (in [0, 2^63)) and split into three 21-bit limbs accumulated with
+// native 32-bit atomics by ALL 1024 threads (any thread may update any bin). Limb sums over at
+// most kAtomSub = 2048 rows stay below 2^32; they are then folded exactly into 64-bit per-bin
+// accumulators: U = S0 + S1*2^21 + S2*2^42, count = (U + 2^61) >> 62 (|sum v| < 2^61 by the
+// choice of the fixed-point shift), sum = U - count*2^62. No count atomic is needed.
+constexpr int kAtomThreads = 1024;
+constexpr int kAtomSub = 2048;
+constexpr int kAtomChunk = 8192;
+constexpr int kAtomTile = 128;
+constexpr uint32_t kLimbMask = (1u << 21) - 1u;
+
+template <typename CodeT>
+__global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
+    int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
+    const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
+    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const NodeRec* nd = nodes + fd.node0;
+  int s;
+  if (level == 0) {
+    if (blockIdx.y) return;
+    s = 0;
+  } else {
+    if (blockIdx.y >= (1u << (level - 1))) return;
+    const int parent = (1 << (level - 1)) - 1 + blockIdx.y;
+    if (nd[parent].state != kNodeSplit) return;
+    s = 2 * parent + 1;
+    if (nd[s].build != 1) s += 1;
+    if (nd[s].build != 1) return;
+  }
+  const int n_v = nd[s].n;
+  const int r0 = blockIdx.x * kAtomChunk;
+  if (r0 >= n_v) return;
+  const int rows = min(kAtomChunk, n_v - r0);
+  const int seg = nd[s].seg;
+  const int local = s - ((1 << level) - 1);
+  const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
+  const int nrep = fd.nrep, bins = fd.bins;
+  // layout: limbs[3][bins] u32 | acc_sum[bins] i64 | acc_cnt[bins] i32 | boff[nrep] | tile codes | tile limbs
+  uint32_t* limb = reinterpret_cast<uint32_t*>(smem);
+  int64_t* acc_sum = reinterpret_cast<int64_t*>(smem + ((static_cast<size_t>(3) * bins * 4 + 15) & ~size_t(15)));
+  int32_t* acc_cnt = reinterpret_cast<int32_t*>(acc_sum + bins);
+  int32_t* s_boff = acc_cnt + bins;
+  unsigned char* tail = reinterpret_cast<unsigned char*>(s_boff + nrep);
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                              // [kAtomTile][Dp]
+  uint32_t* t_limb = reinterpret_cast<uint32_t*>(t_codes + kAtomTile * Dp);     // [kAtomTile][3]
+  __shared__ unsigned long long s_abs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < bins; b += kAtomThreads) {
+    acc_sum[b] = 0;
+    acc_cnt[b] = 0;
+  }
+  for (int j = tid; j < nrep; j += kAtomThreads) s_boff[j] = rep_boff[fd.rep0 + j];
+  if (tid == 0) s_abs = 0;
+  const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
+  for (int sub0 = 0; sub0 < rows; sub0 += kAtomSub) {
+    for (int i = tid; i < 3 * bins; i += kAtomThreads) limb[i] = 0;
+    __syncthreads();
+    const int sub_end = min(rows, sub0 + kAtomSub);
+    for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
+      const int tr = min(kAtomTile, sub_end - t0);
+      for (int i = tid; i < tr * vec_per_row; i += kAtomThreads) {
+        const int r = i / vec_per_row, v = i - r * vec_per_row;
+        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+        reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+      }
+      unsigned long long a = 0;
+      if (tid < tr) {
+        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid];
+        const int64_t v = rfix[p];
+        const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+        t_limb[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;
+        t_limb[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;
+        t_limb[3 * tid + 2] = static_cast<uint32_t>(u >> 42);
+        a = static_cast<unsigned long long>(v < 0 ? -v : v);
+      }
+      if (warp * 32 < tr) {
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0 && a) atomicAdd(&s_abs, a);
+      }
+      __syncthreads();
+      for (int r = warp; r < tr; r += kAtomThreads / 32) {
+        const uint32_t l0 = t_limb[3 * r], l1 = t_limb[3 * r + 1], l2 = t_limb[3 * r + 2];
+        const CodeT* cr = t_codes + r * Dp;
+        for (int j = lane; j < nrep; j += 32) {
+          const int bin = s_boff[j] + static_cast<int>(cr[j]);
+          atomicAdd(limb + bin, l0);
+          atomicAdd(limb + bins + bin, l1);
+          atomicAdd(limb + 2 * bins + bin, l2);
+        }
+      }
+      __syncthreads();
+    }
+    for (int b = tid; b < bins; b += kAtomThreads) {
+      const unsigned __int128 U = static_cast<unsigned __int128>(limb[b]) +
+                                  (static_cast<unsigned __int128>(limb[bins + b]) << 21) +
+                                  (static_cast<unsigned __int128>(limb[2 * bins + b]) << 42);
+      const uint64_t c = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
+      const unsigned __int128 sv = U - (static_cast<unsigned __int128>(c) << 62);
+      acc_sum[b] += static_cast<int64_t>(static_cast<uint64_t>(sv));
+      acc_cnt[b] += static_cast<int32_t>(c);
+    }
+    __syncthreads();
+  }
+  for (int b = tid; b < bins; b += kAtomThreads) {
+    if (acc_cnt[b]) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(hsum + hbase + b), static_cast<unsigned long long>(acc_sum[b]));
+      atomicAdd(hcnt + hbase + b, acc_cnt[b]);
+    }
+  }
+  if (tid == 0) {
+    if (s_abs) atomicAdd(reinterpret_cast<unsigned long long*>(node_abs + fd.node0 + s), s_abs);
+    atomicAdd(ctr + kCtrHistBytes,
+              static_cast<unsigned long long>(rows) * (static_cast<unsigned long long>(nrep) * sizeof(CodeT) + 12ull));
+    atomicAdd(ctr + kCtrHistRows, static_cast<unsigned long long>(rows));
+  }
+}
+
+inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes) {
+  size_t o = (static_cast<size_t>(3) * bins * 4 + 15) & ~size_t(15);
+  o += static_cast<size_t>(bins) * 12 + static_cast<size_t>(nrep) * 4;
+  o = (o + 15) & ~size_t(15);
+  o += static_cast<size_t>(kAtomTile) * Dp * code_bytes + static_cast<size_t>(kAtomTile) * 12 + 16;
+  return o;
+}
+
 // sibling = parent - built child (exact: integer histograms)
 __global__ void hist_derive_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                                    const NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
@@ -1731,58 +1864,67 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         hc[i] = 0;
       }
       __syncthreads();
-      // ---- histograms of directly built nodes: thread t owns (feature t % nrep, row group
-      // t / nrep) and its group's private bins, so the accumulation needs no atomics; the
-      // group copies are then summed (integers: any order gives the same result).
+      // ---- histograms of directly built nodes: every thread takes (row, feature) elements and
+      // adds the row's three 21-bit limbs of u = v + 2^62 with native 32-bit shared atomics; every
+      // 2048 rows the limb sums are folded exactly into the node's 64-bit histogram (see
+      // hist_build_atomic_kernel for the arithmetic).
       {
-        const int per_group = nrep < kResThreads ? nrep : kResThreads;
-        const int g = tid / per_group, j0 = tid - g * per_group;
-        const bool worker = g < groups;
+        uint32_t* limb = reinterpret_cast<uint32_t*>(s_gsum);  // [3][bins] (groups >= 2 -> fits)
+        const int rpw = nrep <= 32 ? 32 / nrep : 1;            // rows per warp iteration
+        const int lr = nrep <= 32 ? lane / nrep : 0;           // row within the iteration
+        const int lj = nrep <= 32 ? lane - lr * nrep : lane;   // first feature of this lane
+        const bool lane_ok = nrep <= 32 ? lr < rpw : true;
         for (int k = 0; k < nl; ++k) {
           ResNode& nd = s_nodes[first + k];
           if (nd.build != 1) continue;
           const int nv = nd.n, seg = nd.seg;
-          for (int i = tid; i < groups * bins; i += kResThreads) {
-            s_gsum[i] = 0;
-            s_gcnt[i] = 0;
-          }
-          if (tid < groups) s_gabs[tid] = 0;
-          __syncthreads();
-          if (worker) {
-            long long* gs = s_gsum + static_cast<size_t>(g) * bins;
-            int* gc = s_gcnt + static_cast<size_t>(g) * bins;
-            unsigned long long a = 0;
-            for (int j = j0; j < nrep; j += per_group) {
-              const int boff = s_repb[j];
-              const uint8_t* cj = s_codes + static_cast<size_t>(j) * n;
-              for (int r = g; r < nv; r += groups) {
-                const int p = s_ord0[seg + r];
-                const long long v = s_fix[p];
-                const int bin = boff + cj[p];
-                gs[bin] += v;
-                gc[bin] += 1;
-                if (j == 0) a += static_cast<unsigned long long>(v < 0 ? -v : v);
-              }
-            }
-            if (j0 == 0) s_gabs[g] = a;
-          }
-          __syncthreads();
           long long* h = hs + static_cast<size_t>(k) * bins;
           int* c = hc + static_cast<size_t>(k) * bins;
           for (int b = tid; b < bins; b += kResThreads) {
-            long long sv = 0;
-            int cv = 0;
-            for (int gg = 0; gg < groups; ++gg) {
-              sv += s_gsum[static_cast<size_t>(gg) * bins + b];
-              cv += s_gcnt[static_cast<size_t>(gg) * bins + b];
-            }
-            h[b] = sv;
-            c[b] = cv;
+            h[b] = 0;
+            c[b] = 0;
           }
+          unsigned long long a = 0;
+          for (int sub0 = 0; sub0 < nv; sub0 += kAtomSub) {
+            for (int i = tid; i < 3 * bins; i += kResThreads) limb[i] = 0;
+            __syncthreads();
+            const int sub_end = min(nv, sub0 + kAtomSub);
+            for (int r0 = sub0 + warp * rpw; r0 < sub_end; r0 += (kResThreads / 32) * rpw) {
+              const int r = r0 + lr;
+              if (!lane_ok || r >= sub_end) continue;
+              const int p = s_ord0[seg + r];
+              const long long v = s_fix[p];
+              const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+              const uint32_t l0 = static_cast<uint32_t>(u) & kLimbMask;
+              const uint32_t l1 = static_cast<uint32_t>(u >> 21) & kLimbMask;
+              const uint32_t l2 = static_cast<uint32_t>(u >> 42);
+              if (lj == 0) a += static_cast<unsigned long long>(v < 0 ? -v : v);
+              for (int j = lj; j < nrep; j += (nrep <= 32 ? nrep : 32)) {
+                const int bin = s_repb[j] + s_codes[static_cast<size_t>(j) * n + p];
+                atomicAdd(limb + bin, l0);
+                atomicAdd(limb + bins + bin, l1);
+                atomicAdd(limb + 2 * bins + bin, l2);
+                if (nrep <= 32) break;
+              }
+            }
+            __syncthreads();
+            for (int b = tid; b < bins; b += kResThreads) {
+              const unsigned __int128 U = static_cast<unsigned __int128>(limb[b]) +
+                                          (static_cast<unsigned __int128>(limb[bins + b]) << 21) +
+                                          (static_cast<unsigned __int128>(limb[2 * bins + b]) << 42);
+              const uint64_t cnt = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
+              h[b] += static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
+              c[b] += static_cast<int>(cnt);
+            }
+            __syncthreads();
+          }
+          for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          if (lane == 0) s_red[warp] = a;
+          __syncthreads();
           if (tid == 0) {
-            unsigned long long a = 0;
-            for (int gg = 0; gg < groups; ++gg) a += s_gabs[gg];
-            nd.absfix = a;
+            unsigned long long t = 0;
+            for (int w = 0; w < kResThreads / 32; ++w) t += s_red[w];
+            nd.absfix = t;
           }
           c_hist_rows += tid == 0 ? nv : 0;
           __syncthreads();
@@ -2340,6 +2482,8 @@ struct ResidentPlan {
   int groups = 1;
   bool pre_smem = false;
   // column-layout histogram plan for the multi-kernel path (hist_build_col_kernel)
+  bool atomic = false;  // limb-atomic histogram (default)
+  size_t atomic_smem = 0;
   bool col = false;
   std::vector<int32_t> col_off;  // [F][kColWarps + 1] entry offsets per feature group
   std::vector<int32_t> col_rg;   // [F] row groups (private copies)
@@ -2436,6 +2580,9 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   const unsigned chunks = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n_max, kHistChunk)));
   int32_t* col_off_d = nullptr;
   int32_t* col_rg_d = nullptr;
+  if (resident.atomic)
+    FS_CUDA(cudaFuncSetAttribute(hist_build_atomic_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(resident.atomic_smem)));
   if (resident.col) {
     col_off_d = ar.upload(resident.col_off);
     col_rg_d = ar.upload(resident.col_rg);
@@ -2464,7 +2611,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
       {
         ProfScope prof(dev, "fit_hist_build");
-        if (resident.col)
+        if (resident.atomic)
+          hist_build_atomic_kernel<CodeT><<<dim3(static_cast<unsigned>(ceil_div(n_max, kAtomChunk)), pairs, F),
+                                             kAtomThreads, resident.atomic_smem, s>>>(
+              fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d);
+        else if (resident.col)
           hist_build_col_kernel<CodeT><<<dim3(chunks, pairs, F), kColWarps * 32, resident.col_smem, s>>>(
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, rep_nb_d, col_off_d, col_rg_d, hsum,
               hcnt, node_abs, dev->ctr_d);
@@ -2714,26 +2865,18 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
       for (const bool pre_smem : {true, false}) {
         bool ok = true;
         const size_t budget = 225 * 1024;
-        int groups = 32;
+        const int groups = 2;  // the histogram's limb scratch (3 x 32-bit per bin) lives in 2 "group" slots
         std::vector<int> fams_ok;
+        size_t need = 0;
         for (int f = 0; f < F; ++f) {
           const FamDesc& fd = fam[static_cast<size_t>(f)];
           if (fd.n <= 0 || fd.trees <= 0) continue;
           if (fd.n > 65535) ok = false;
-          const size_t base_total = res_layout(fd.n, fd.nrep, fd.bins, fd.depth, 0, pre_smem).total;
-          const size_t per = static_cast<size_t>(fd.bins) * 12 + 64;
-          const int fit_g = base_total + per <= budget ? static_cast<int>((budget - base_total) / per) : 0;
-          groups = std::min({groups, fit_g, kResThreads / std::max(1, static_cast<int>(fd.nrep))});
+          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups, pre_smem).total);
           fams_ok.push_back(f);
         }
-        size_t need = 0;
-        if (groups >= 1)
-          for (int f : fams_ok) {
-            const FamDesc& fd = fam[static_cast<size_t>(f)];
-            need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups, pre_smem).total);
-          }
         res.families = fams_ok;
-        if (ok && groups >= 1 && need <= budget && !fams_ok.empty()) {
+        if (ok && need <= budget && !fams_ok.empty()) {
           res.enabled = true;
           res.smem = need;
           res.groups = groups;
@@ -2747,7 +2890,21 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   }
   // Column-layout histogram plan (multi-kernel path): per feature group of 32 the largest bin
   // count; row-group copies while they fit the shared-memory budget.
-  if (!res.enabled && !std::getenv("FAMSEER_HIST_ROWMAJOR")) {
+  // Histogram shape for the multi-kernel path: FAMSEER_HIST = atomic (default) | col | rowmajor.
+  const char* hist_env = std::getenv("FAMSEER_HIST");
+  const std::string hist_mode = hist_env ? hist_env : (std::getenv("FAMSEER_HIST_ROWMAJOR") ? "rowmajor" : "atomic");
+  if (hist_mode != "atomic" && hist_mode != "col" && hist_mode != "rowmajor")
+    fail(FS_EINVAL, "FAMSEER_HIST must be atomic, col or rowmajor");
+  if (!res.enabled && hist_mode == "atomic") {
+    const int pv = 16 / code_bytes;
+    const int dp = std::max(pv, static_cast<int>(ceil_div(std::max(nrep_max, 1), pv)) * pv);
+    const size_t need = hist_atomic_smem(max_bins, nrep_max, dp, code_bytes);
+    if (need <= 200 * 1024) {
+      res.atomic = true;
+      res.atomic_smem = need;
+    }
+  }
+  if (!res.enabled && !res.atomic && hist_mode != "rowmajor") {
     const size_t cap = 200 * 1024;
     const int pv = 16 / code_bytes;
     const int dp = std::max(pv, static_cast<int>(ceil_div(std::max(nrep_max, 1), pv)) * pv);

@@ -22,23 +22,47 @@ namespace {
 constexpr int kTile = 256;
 constexpr int kChunk = 64;
 
+// One family's compiled ensemble, as the batched kernel sees it.
+struct PredModel {
+  const uint32_t* nodes;
+  const double* leafv;
+  const uint8_t* leafid;
+  const double* uthr;
+  const int32_t* uoff;
+  double base, lr;
+  int depth, n_trees, d_model, n_uthr;
+};
+
+// One CTA's work: a tile of up to kTile rows of one family segment.
+struct PredJob {
+  int32_t model, rows;
+  int64_t row0;   // first row (into x / scores)
+  int64_t leaf0;  // byte offset of row0's leaf ids
+};
+
+// Every family segment of a predict call is scored by ONE launch (a family is typically a few
+// hundred tiles; one launch per family left most of the 148 SMs idle). Shared memory is laid out
+// for the largest model of the launch; each CTA uses its own model's shape.
 template <typename CodeT, bool kLeaves, bool kSmemThr>
 __global__ void __launch_bounds__(kTile) predict_heap_kernel(
-    const double* __restrict__ x, int64_t rows, int d, int d_model, int depth, int n_trees, double base,
-    double lr, const uint32_t* __restrict__ nodes, const double* __restrict__ leafv,
-    const uint8_t* __restrict__ leafid, const double* __restrict__ uthr_g, const int32_t* __restrict__ uoff_g,
-    int n_uthr, double* __restrict__ scores, uint8_t* __restrict__ leaf_out, uint32_t* err) {
+    const double* __restrict__ x, int d, const PredModel* __restrict__ models, const PredJob* __restrict__ jobs,
+    int max_dmodel, int max_depth, int max_uthr, double* __restrict__ scores, uint8_t* __restrict__ leaf_out,
+    uint32_t* err) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const PredJob job = jobs[blockIdx.x];
+  const PredModel M = models[job.model];
+  const int depth = M.depth, d_model = M.d_model, n_trees = M.n_trees;
   const int nint = (1 << depth) - 1;
   const int nleaf = 1 << depth;
+  const int mnint = (1 << max_depth) - 1, mnleaf = 1 << max_depth;
   CodeT* codes = reinterpret_cast<CodeT*>(smem);  // [d_model][kTile]
-  size_t off = (static_cast<size_t>(d_model) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
+  size_t off = (static_cast<size_t>(max_dmodel) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
   double* s_leafv = reinterpret_cast<double*>(smem + off);  // [kChunk][nleaf]
-  off += static_cast<size_t>(kChunk) * nleaf * sizeof(double);
+  off += static_cast<size_t>(kChunk) * mnleaf * sizeof(double);
   uint32_t* s_nodes = reinterpret_cast<uint32_t*>(smem + off);  // [kChunk][nint]
-  off += static_cast<size_t>(kChunk) * nint * sizeof(uint32_t);
+  off += static_cast<size_t>(kChunk) * mnint * sizeof(uint32_t);
   uint8_t* s_leafid = smem + off;  // [kChunk][nleaf]
-  off += static_cast<size_t>(kChunk) * nleaf;
+  off += static_cast<size_t>(kChunk) * mnleaf;
   uint8_t* s_lbuf = smem + off;  // [kTile][kChunk]
   off += kLeaves ? static_cast<size_t>(kTile) * kChunk : 0;
   off = (off + 15) & ~size_t(15);
@@ -47,19 +71,19 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
   const int warp = tid >> 5, lane = tid & 31;
   // The threshold tables the codes are searched in: staged in shared memory when they fit
   // (binary-search steps then cost a shared load instead of an L2 round trip).
-  const double* uthr = uthr_g;
-  const int32_t* uoff = uoff_g;
+  const double* uthr = M.uthr;
+  const int32_t* uoff = M.uoff;
   if (kSmemThr) {
     double* su = reinterpret_cast<double*>(smem + off);
-    int32_t* so = reinterpret_cast<int32_t*>(su + n_uthr);
-    for (int i = tid; i < n_uthr; i += kTile) su[i] = __ldg(uthr_g + i);
-    for (int i = tid; i <= d_model; i += kTile) so[i] = __ldg(uoff_g + i);
+    int32_t* so = reinterpret_cast<int32_t*>(su + max_uthr);
+    for (int i = tid; i < M.n_uthr; i += kTile) su[i] = __ldg(M.uthr + i);
+    for (int i = tid; i <= d_model; i += kTile) so[i] = __ldg(M.uoff + i);
     __syncthreads();
     uthr = su;
     uoff = so;
   }
-  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kTile;
-  const int tile_rows = static_cast<int>(rows - row0 < kTile ? rows - row0 : kTile);
+  const int64_t row0 = job.row0;
+  const int tile_rows = job.rows;
 
   bool nonfinite = false;
   for (int c = warp; c < tile_rows; c += kTile / 32) {
@@ -81,15 +105,16 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
   }
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, fs::kErrNonFinitePredict);
 
-  double score = base;
+  double score = M.base;
+  const double lr = M.lr;
   const bool active = tid < tile_rows;
   for (int t0 = 0; t0 < n_trees; t0 += kChunk) {
     const int ch = min(kChunk, n_trees - t0);
     __syncthreads();  // codes ready / previous chunk consumed
-    for (int i = tid; i < ch * nint; i += kTile) s_nodes[i] = __ldg(nodes + static_cast<size_t>(t0) * nint + i);
+    for (int i = tid; i < ch * nint; i += kTile) s_nodes[i] = __ldg(M.nodes + static_cast<size_t>(t0) * nint + i);
     for (int i = tid; i < ch * nleaf; i += kTile) {
-      s_leafv[i] = __ldg(leafv + static_cast<size_t>(t0) * nleaf + i);
-      s_leafid[i] = __ldg(leafid + static_cast<size_t>(t0) * nleaf + i);
+      s_leafv[i] = __ldg(M.leafv + static_cast<size_t>(t0) * nleaf + i);
+      s_leafid[i] = __ldg(M.leafid + static_cast<size_t>(t0) * nleaf + i);
     }
     __syncthreads();
     if (active) {
@@ -110,7 +135,7 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
       __syncthreads();
       for (int i = tid; i < tile_rows * ch; i += kTile) {
         const int c = i / ch, t = i - c * ch;
-        leaf_out[(row0 + c) * n_trees + t0 + t] = s_lbuf[c * kChunk + t];
+        leaf_out[job.leaf0 + static_cast<int64_t>(c) * n_trees + t0 + t] = s_lbuf[c * kChunk + t];
       }
     }
   }
@@ -140,35 +165,35 @@ __global__ void predict_generic_kernel(const double* __restrict__ x, int64_t row
   scores[r] = score;
 }
 
+struct HeapGroup {
+  std::vector<PredModel> models;
+  std::vector<PredJob> jobs;
+  int max_dmodel = 0, max_depth = 0, max_uthr = 0;
+};
+
 template <typename CodeT, bool kLeaves, bool kSmemThr>
-void launch_heap_impl(fs_device* dev, const fs::FamilyModel& m, const double* x, int64_t rows, int d, double* scores,
-                      uint8_t* leaf_out) {
-  const int nint = (1 << m.depth) - 1, nleaf = 1 << m.depth;
-  size_t smem = (static_cast<size_t>(m.d_model) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
-  smem += static_cast<size_t>(kChunk) * (nleaf * sizeof(double) + nint * sizeof(uint32_t) + nleaf);
+void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, double* scores, uint8_t* leaf_out) {
+  if (g.jobs.empty()) return;
+  const int mnint = (1 << g.max_depth) - 1, mnleaf = 1 << g.max_depth;
+  size_t smem = (static_cast<size_t>(g.max_dmodel) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
+  smem += static_cast<size_t>(kChunk) * (mnleaf * sizeof(double) + mnint * sizeof(uint32_t) + mnleaf);
   if (kLeaves) smem += static_cast<size_t>(kTile) * kChunk;
   smem = (smem + 15) & ~size_t(15);
-  if (kSmemThr) smem += static_cast<size_t>(m.n_uthr) * sizeof(double) + (m.d_model + 1) * sizeof(int32_t);
+  if (kSmemThr) smem += static_cast<size_t>(g.max_uthr) * sizeof(double) + (g.max_dmodel + 1) * sizeof(int32_t);
   auto* fn = predict_heap_kernel<CodeT, kLeaves, kSmemThr>;
   if (smem > 227 * 1024) fs::fail(FS_EINVAL, "predict: model too wide for the shared-memory tile");
   FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const int grid = static_cast<int>(fs::ceil_div(rows, kTile));
+  const size_t mb = g.models.size() * sizeof(PredModel), jb = g.jobs.size() * sizeof(PredJob);
+  auto* buf = static_cast<unsigned char*>(dev->scratch(fs::kSlotPredictSeg, mb + jb + 16));
+  auto* md = reinterpret_cast<PredModel*>(buf);
+  auto* jd = reinterpret_cast<PredJob*>(buf + ((mb + 15) & ~size_t(15)));
+  FS_CUDA(cudaMemcpyAsync(md, g.models.data(), mb, cudaMemcpyHostToDevice, dev->stream));
+  FS_CUDA(cudaMemcpyAsync(jd, g.jobs.data(), jb, cudaMemcpyHostToDevice, dev->stream));
   fs::ProfScope prof(dev, "predict");
-  fn<<<grid, kTile, smem, dev->stream>>>(x, rows, d, std::min(m.d_model, d), m.depth, m.n_trees, m.base, m.lr,
-                                         m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, m.n_uthr, scores,
-                                         leaf_out, dev->err_d);
+  fn<<<static_cast<unsigned>(g.jobs.size()), kTile, smem, dev->stream>>>(x, d, md, jd, g.max_dmodel, g.max_depth,
+                                                                         g.max_uthr, scores, leaf_out, dev->err_d);
   dev->count_launch();
   FS_CUDA(cudaGetLastError());
-}
-
-template <typename CodeT, bool kLeaves>
-void launch_heap(fs_device* dev, const fs::FamilyModel& m, const double* x, int64_t rows, int d, double* scores,
-                 uint8_t* leaf_out) {
-  // thresholds in shared memory when they take <= 48 KB (T <~ 850 at depth 3)
-  if (static_cast<size_t>(m.n_uthr) * sizeof(double) <= 48 * 1024)
-    launch_heap_impl<CodeT, kLeaves, true>(dev, m, x, rows, d, scores, leaf_out);
-  else
-    launch_heap_impl<CodeT, kLeaves, false>(dev, m, x, rows, d, scores, leaf_out);
 }
 
 }  // namespace
@@ -176,10 +201,12 @@ void launch_heap(fs_device* dev, const fs::FamilyModel& m, const double* x, int6
 namespace fs {
 
 // Scores rows [seg[f], seg[f+1]) with family f. Leaf ids of segment f start at byte
-// sum_{g<f} rows_g * T_g of leaf_out.
+// sum_{g<f} rows_g * T_g of leaf_out. All heap-form families go out in one launch (per code width
+// / threshold-table placement, normally one); deeper-than-heap models use the generic kernel.
 void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
                     const double* x, double* scores, uint8_t* leaf_out) {
   int64_t leaf_off = 0;
+  HeapGroup groups[2][2];  // [code_bytes == 2][thresholds in smem]
   for (int f = 0; f < nseg; ++f) {
     const int64_t r0 = seg[f], rows = seg[f + 1] - seg[f];
     if (f >= static_cast<int32_t>(fo->fams.size())) fail(FS_ERANGE, "predict: segment names an unknown family");
@@ -187,22 +214,43 @@ void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int
     if (!m.compiled) fail(FS_EINVAL, "predict: family " + std::to_string(f) + " has no compiled model");
     if (m.d_model > d) fail(FS_EINVAL, "predict: model references feature beyond the row width");
     if (rows <= 0) continue;
-    uint8_t* lo = leaf_out ? leaf_out + leaf_off : nullptr;
+    const int64_t lo = leaf_off;
     leaf_off += rows * m.n_trees;
     if (m.generic) {
       predict_generic_kernel<<<static_cast<int>(ceil_div(rows, 128)), 128, 0, dev->stream>>>(
           x + r0 * d, rows, d, m.n_trees, m.base, m.lr, m.g_off_d, m.g_feat_d, m.g_thr_d, m.g_left_d, m.g_right_d,
-          m.g_val_d, scores + r0, lo, dev->err_d);
+          m.g_val_d, scores + r0, leaf_out ? leaf_out + lo : nullptr, dev->err_d);
       dev->count_launch();
       FS_CUDA(cudaGetLastError());
-    } else if (m.code_bytes == 1) {
-      if (lo) launch_heap<uint8_t, true>(dev, m, x + r0 * d, rows, d, scores + r0, lo);
-      else launch_heap<uint8_t, false>(dev, m, x + r0 * d, rows, d, scores + r0, nullptr);
-    } else {
-      if (lo) launch_heap<uint16_t, true>(dev, m, x + r0 * d, rows, d, scores + r0, lo);
-      else launch_heap<uint16_t, false>(dev, m, x + r0 * d, rows, d, scores + r0, nullptr);
+      continue;
     }
+    const bool smem_thr = static_cast<size_t>(m.n_uthr) * sizeof(double) <= 48 * 1024;
+    HeapGroup& g = groups[m.code_bytes == 2][smem_thr];
+    const int mi = static_cast<int>(g.models.size());
+    g.models.push_back({m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, m.base, m.lr, m.depth, m.n_trees,
+                        std::min(m.d_model, d), m.n_uthr});
+    g.max_dmodel = std::max(g.max_dmodel, std::min(m.d_model, d));
+    g.max_depth = std::max(g.max_depth, m.depth);
+    g.max_uthr = std::max(g.max_uthr, m.n_uthr);
+    for (int64_t t = 0; t < rows; t += kTile)
+      g.jobs.push_back({mi, static_cast<int32_t>(std::min<int64_t>(kTile, rows - t)), r0 + t, lo + t * m.n_trees});
   }
+  for (int cb = 0; cb < 2; ++cb)
+    for (int st = 0; st < 2; ++st) {
+      const HeapGroup& g = groups[cb][st];
+      if (g.jobs.empty()) continue;
+      if (cb == 0) {
+        if (leaf_out) st ? launch_group<uint8_t, true, true>(dev, g, x, d, scores, leaf_out)
+                         : launch_group<uint8_t, true, false>(dev, g, x, d, scores, leaf_out);
+        else st ? launch_group<uint8_t, false, true>(dev, g, x, d, scores, nullptr)
+                : launch_group<uint8_t, false, false>(dev, g, x, d, scores, nullptr);
+      } else {
+        if (leaf_out) st ? launch_group<uint16_t, true, true>(dev, g, x, d, scores, leaf_out)
+                         : launch_group<uint16_t, true, false>(dev, g, x, d, scores, leaf_out);
+        else st ? launch_group<uint16_t, false, true>(dev, g, x, d, scores, nullptr)
+                : launch_group<uint16_t, false, false>(dev, g, x, d, scores, nullptr);
+      }
+    }
 }
 
 int64_t leaf_bytes(const fs_forest* fo, int32_t nseg, const int64_t* seg) {

@@ -14,14 +14,16 @@ CASES = [str(t) for t in G["fit_cases"]]
 TREE_FIELDS = ("offsets", "feature", "threshold", "left", "right", "value")
 
 
-@pytest.fixture(autouse=True, params=["auto", "multi", "multi_rowmajor"])
+@pytest.fixture(autouse=True, params=["auto", "multi", "multi_col", "multi_rowmajor"])
 def fit_path(request, monkeypatch):
     """Every parity test runs on every trainer shape: the resident one-CTA-per-family kernel (auto
-    picks it when the families fit shared memory), the multi-kernel round with the column-layout
-    histogram, and the multi-kernel round with the row-major histogram."""
+    picks it when the families fit shared memory) and the multi-kernel round with each histogram
+    build (limb-atomic default, column layout, row-major)."""
     monkeypatch.setenv("FAMSEER_FIT_PATH", "auto" if request.param == "auto" else "multi")
-    if request.param == "multi_rowmajor":
-        monkeypatch.setenv("FAMSEER_HIST_ROWMAJOR", "1")
+    if request.param == "multi_col":
+        monkeypatch.setenv("FAMSEER_HIST", "col")
+    elif request.param == "multi_rowmajor":
+        monkeypatch.setenv("FAMSEER_HIST", "rowmajor")
     return request.param
 
 
