@@ -1103,7 +1103,7 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
     w.count = count;
     w.best_lc = blc;
     w.eq = 0;
-    w.pad_ = 0;
+    w.maxlc = 0;
     win[(static_cast<int64_t>(f) * level_slots_max + local) * nrep_max + jj] = w;
     if (count) atomicAdd(&nd.wcount, count);
   }
@@ -1608,6 +1608,7 @@ namespace fit {
 namespace {
 
 constexpr int kResThreads = 1024;
+constexpr int kResWarps = kResThreads / 32;
 constexpr int kResMaxDepth = 7;  // node ids fit in uint8
 
 struct ResNode {
@@ -1619,9 +1620,9 @@ struct ResNode {
 };
 
 struct ResLayout {
-  int ls, slots;
-  size_t codes, resid, pred, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, gsum, gcnt, gabs,
-      cand, total;
+  int ls, slots, cs;
+  size_t codes, resid, pred, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, cand,
+      total;
 };
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
@@ -1634,8 +1635,11 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   L.slots = (1 << (depth + 1)) - 1;
   const size_t nr = nrep > 0 ? static_cast<size_t>(nrep) : 1;
   size_t o = 0;
+  // codes [nrep][cs]: cs = 4 (mod 128) so the lanes reading one row's codes of consecutive
+  // features fall in consecutive banks
+  L.cs = ((n + 127) & ~127) + 4;
   L.codes = o;
-  o = res_align(o + static_cast<size_t>(n) * nr);
+  o = res_align(o + static_cast<size_t>(L.cs) * nr);
   L.resid = o;
   o = res_align(o + static_cast<size_t>(n) * 8);
   L.pred = o;  // presorted lists [nrep][n] as u16 (when pre_smem), else empty
@@ -1662,12 +1666,11 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(L.ls) * (nr + 1) * sizeof(int));
   L.rep = o;
   o = res_align(o + 2 * nr * sizeof(int));
-  L.gsum = o;
-  o = res_align(o + static_cast<size_t>(groups) * bins * 8);
-  L.gcnt = o;
-  o = res_align(o + static_cast<size_t>(groups) * bins * 4);
-  L.gabs = o;
-  o = res_align(o + static_cast<size_t>(groups) * 8);
+  L.limb = o;  // per level node: 3 x 32-bit limb sums per bin + 3 limbs of sum |v| (histogram sweep)
+  o = res_align(o + std::max<size_t>(static_cast<size_t>(L.ls) * (3 * static_cast<size_t>(bins) + 3) * 4, 8 * 512));
+  (void)groups;
+  L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
+  o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
   L.cand = o;  // screened (gain, bound) per (node at level, bin)
   o = res_align(o + static_cast<size_t>(L.ls) * bins * 16);
   L.total = o;
@@ -1734,10 +1737,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
   const ResLayout Lo = res_layout(n, nrep, bins, depth, groups, pre_smem != 0);
-  uint8_t* s_codes = sm + Lo.codes;  // [nrep][n]
-  long long* s_gsum = reinterpret_cast<long long*>(sm + Lo.gsum);  // [groups][bins]
-  int* s_gcnt = reinterpret_cast<int*>(sm + Lo.gcnt);
-  unsigned long long* s_gabs = reinterpret_cast<unsigned long long*>(sm + Lo.gabs);
+  uint8_t* s_codes = sm + Lo.codes;  // [nrep][cs]
+  const int cs = Lo.cs;
+  uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [level node][3 * bins + 3]
   double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
   __shared__ int s_neq;
   // phase timers (CTA 0, thread 0): where a round's cycles go (fs_device_counters [4..15])
@@ -1773,13 +1775,16 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   int* s_repn = s_repb + (nrep > 0 ? nrep : 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ls = Lo.ls, slots = Lo.slots;
+  // ceil(2^32 / nrep): e / nrep == umulhi(e, magic) for e < 2^32 / nrep (nrep >= 2; the host
+  // keeps nrep <= 1024 on this path, so every e < kAtomSub * nrep qualifies)
+  const unsigned nrep_magic = nrep > 1 ? static_cast<unsigned>((0x100000000ull + nrep - 1) / nrep) : 0u;
   unsigned long long c_hist_rows = 0;
   if (tid < 3) s_cnt[tid] = 0;
   if (tid < 4) s_why[tid] = 0;
 
   for (int i = tid; i < n * nrep; i += kResThreads) {
     const int p = i / nrep, j = i - p * nrep;
-    s_codes[j * n + p] = codes_c[(fd.pos0 + p) * Dp + j];
+    s_codes[j * cs + p] = codes_c[(fd.pos0 + p) * Dp + j];
   }
   for (int j = tid; j < nrep; j += kResThreads) {
     s_repb[j] = rep_boff[fd.rep0 + j];
@@ -1864,70 +1869,67 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         hc[i] = 0;
       }
       __syncthreads();
-      // ---- histograms of directly built nodes: every thread takes (row, feature) elements and
-      // adds the row's three 21-bit limbs of u = v + 2^62 with native 32-bit shared atomics; every
-      // 2048 rows the limb sums are folded exactly into the node's 64-bit histogram (see
-      // hist_build_atomic_kernel for the arithmetic).
+      // ---- histograms of every directly built node of the level in ONE sweep over the rows:
+      // a warp takes 32 consecutive rows of one feature (conflict-free code loads; rows are read
+      // in canonical position order, no index chasing) and adds each row's three 21-bit limbs of
+      // u = v + 2^62 into its node's limb histogram with native 32-bit shared atomics (plus the
+      // limbs of |v| for the screen bound, on the feature-0 items). Every kAtomSub rows the limb
+      // sums are folded exactly into the nodes' 64-bit histograms (see hist_build_atomic_kernel
+      // for the arithmetic).
       {
-        uint32_t* limb = reinterpret_cast<uint32_t*>(s_gsum);  // [3][bins] (groups >= 2 -> fits)
-        const int rpw = nrep <= 32 ? 32 / nrep : 1;            // rows per warp iteration
-        const int lr = nrep <= 32 ? lane / nrep : 0;           // row within the iteration
-        const int lj = nrep <= 32 ? lane - lr * nrep : lane;   // first feature of this lane
-        const bool lane_ok = nrep <= 32 ? lr < rpw : true;
-        for (int k = 0; k < nl; ++k) {
-          ResNode& nd = s_nodes[first + k];
-          if (nd.build != 1) continue;
-          const int nv = nd.n, seg = nd.seg;
-          long long* h = hs + static_cast<size_t>(k) * bins;
-          int* c = hc + static_cast<size_t>(k) * bins;
-          for (int b = tid; b < bins; b += kResThreads) {
-            h[b] = 0;
-            c[b] = 0;
-          }
-          unsigned long long a = 0;
-          for (int sub0 = 0; sub0 < nv; sub0 += kAtomSub) {
-            for (int i = tid; i < 3 * bins; i += kResThreads) limb[i] = 0;
+        const int lstride = 3 * bins + 3;
+        int nbuilt = 0;
+        for (int k = 0; k < nl; ++k) nbuilt += s_nodes[first + k].build == 1;
+        if (nbuilt) {
+          for (int sub0 = 0; sub0 < n; sub0 += kAtomSub) {
+            for (int i = tid; i < nl * lstride; i += kResThreads) s_limb[i] = 0;
             __syncthreads();
-            const int sub_end = min(nv, sub0 + kAtomSub);
-            for (int r0 = sub0 + warp * rpw; r0 < sub_end; r0 += (kResThreads / 32) * rpw) {
-              const int r = r0 + lr;
-              if (!lane_ok || r >= sub_end) continue;
-              const int p = s_ord0[seg + r];
+            const int rows = min(kAtomSub, n - sub0);
+            const unsigned total = static_cast<unsigned>(rows) * static_cast<unsigned>(nrep);
+            for (unsigned e = tid; e < total; e += kResThreads) {
+              const int r = nrep == 1 ? static_cast<int>(e) : static_cast<int>(__umulhi(e, nrep_magic));  // e / nrep
+              const int j = static_cast<int>(e) - r * nrep;
+              const int p = sub0 + r;
+              const int k = static_cast<int>(s_node[p]) - first;
+              if (k < 0 || k >= nl || s_nodes[first + k].build != 1) continue;
               const long long v = s_fix[p];
               const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
-              const uint32_t l0 = static_cast<uint32_t>(u) & kLimbMask;
-              const uint32_t l1 = static_cast<uint32_t>(u >> 21) & kLimbMask;
-              const uint32_t l2 = static_cast<uint32_t>(u >> 42);
-              if (lj == 0) a += static_cast<unsigned long long>(v < 0 ? -v : v);
-              for (int j = lj; j < nrep; j += (nrep <= 32 ? nrep : 32)) {
-                const int bin = s_repb[j] + s_codes[static_cast<size_t>(j) * n + p];
-                atomicAdd(limb + bin, l0);
-                atomicAdd(limb + bins + bin, l1);
-                atomicAdd(limb + 2 * bins + bin, l2);
-                if (nrep <= 32) break;
+              uint32_t* lb = s_limb + k * lstride;
+              const int bin = s_repb[j] + s_codes[static_cast<size_t>(j) * cs + p];
+              atomicAdd(lb + bin, static_cast<uint32_t>(u) & kLimbMask);
+              atomicAdd(lb + bins + bin, static_cast<uint32_t>(u >> 21) & kLimbMask);
+              atomicAdd(lb + 2 * bins + bin, static_cast<uint32_t>(u >> 42));
+              if (j == 0) {
+                const uint64_t av = static_cast<uint64_t>(v < 0 ? -v : v);
+                atomicAdd(lb + 3 * bins, static_cast<uint32_t>(av) & kLimbMask);
+                atomicAdd(lb + 3 * bins + 1, static_cast<uint32_t>(av >> 21) & kLimbMask);
+                atomicAdd(lb + 3 * bins + 2, static_cast<uint32_t>(av >> 42));
               }
             }
             __syncthreads();
-            for (int b = tid; b < bins; b += kResThreads) {
-              const unsigned __int128 U = static_cast<unsigned __int128>(limb[b]) +
-                                          (static_cast<unsigned __int128>(limb[bins + b]) << 21) +
-                                          (static_cast<unsigned __int128>(limb[2 * bins + b]) << 42);
+            for (int i = tid; i < nl * bins; i += kResThreads) {
+              const int k = i / bins, b = i - k * bins;
+              if (s_nodes[first + k].build != 1) continue;
+              const uint32_t* lb = s_limb + k * lstride;
+              const unsigned __int128 U = static_cast<unsigned __int128>(lb[b]) +
+                                          (static_cast<unsigned __int128>(lb[bins + b]) << 21) +
+                                          (static_cast<unsigned __int128>(lb[2 * bins + b]) << 42);
               const uint64_t cnt = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
-              h[b] += static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
-              c[b] += static_cast<int>(cnt);
+              hs[i] += static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
+              hc[i] += static_cast<int>(cnt);
             }
+            if (tid < nl && s_nodes[first + tid].build == 1) {
+              const uint32_t* lb = s_limb + tid * lstride + 3 * bins;
+              const unsigned long long add = static_cast<unsigned long long>(lb[0]) +
+                                             (static_cast<unsigned long long>(lb[1]) << 21) +
+                                             (static_cast<unsigned long long>(lb[2]) << 42);
+              ResNode& nd = s_nodes[first + tid];
+              nd.absfix = (sub0 == 0 ? 0ull : nd.absfix) + add;
+            }
+            if (tid == 0 && sub0 == 0)
+              for (int k = 0; k < nl; ++k) c_hist_rows += s_nodes[first + k].build == 1 ? s_nodes[first + k].n : 0;
             __syncthreads();
           }
-          for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-          if (lane == 0) s_red[warp] = a;
-          __syncthreads();
-          if (tid == 0) {
-            unsigned long long t = 0;
-            for (int w = 0; w < kResThreads / 32; ++w) t += s_red[w];
-            nd.absfix = t;
-          }
-          c_hist_rows += tid == 0 ? nv : 0;
-          __syncthreads();
         }
       }
       RES_PHASE(2);
@@ -1982,7 +1984,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           const double S = static_cast<double>(nd.absfix) * scale * (1.0 + 1e-12);
           const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
           double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
-          int bb = 0x7fffffff, blc = 0, count = 0, carry_c = 0;
+          int bb = 0x7fffffff, blc = 0, count = 0, carry_c = 0, mlc = 0;
           long long carry_s = 0;
           for (int b0 = 0; b0 < nb; b0 += 32) {
             const int b = b0 + lane;
@@ -2008,6 +2010,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               const double hi = g + dl;
               if (hi >= LO && hi > 0.0) {
                 ++count;
+                mlc = max(mlc, ic);
                 if (g > bg || (g == bg && b < bb)) {
                   bg = g;
                   bl = g - dl;
@@ -2024,6 +2027,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           } else {
             for (int o = 16; o > 0; o >>= 1) {
               count += __shfl_xor_sync(0xffffffffu, count, o);
+              mlc = max(mlc, __shfl_xor_sync(0xffffffffu, mlc, o));
               const double og = __shfl_xor_sync(0xffffffffu, bg, o);
               const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
               const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
@@ -2044,7 +2048,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               w.count = count;
               w.best_lc = blc;
               w.eq = 0;
-              w.pad_ = 0;
+              w.maxlc = mlc;
               s_win[k * nrep + j] = w;
               if (count) atomicAdd(&nd.wcount, count);
             }
@@ -2085,43 +2089,64 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
       }
       __syncthreads();
-      for (int it = warp; it < s_neq; it += kResThreads / 32) {
-        const int s = s_items[it] >> 16, g = s_items[it] & 0xFFFF;
-        const ResNode& nd = s_nodes[s];
-        const int f0 = nd.eqf0, nv = nd.n;
-        const uint8_t* cf = s_codes + static_cast<size_t>(f0) * n;
-        const uint8_t* cg = s_codes + static_cast<size_t>(g) * n;
-        int pf = -1, pg = -1, seen = 0;
-        bool bad = false;
-        int p_next = lane < n ? pre_at(f0, lane) : 0;
-        for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
-          const int i = i0 + lane;
-          const int p = p_next;
-          p_next = i + 32 < n ? pre_at(f0, i + 32) : 0;
-          const bool mem = i < n && s_node[p] == s;
-          const int a = mem ? cf[p] : 0, b = mem ? cg[p] : 0;
-          const unsigned m = __ballot_sync(0xffffffffu, mem);
-          seen += __popc(m);
-          const unsigned lt = m & ((1u << lane) - 1u);
-          const int src = lt ? 31 - __clz(lt) : lane;
-          int qa = __shfl_sync(0xffffffffu, a, src), qb = __shfl_sync(0xffffffffu, b, src);
-          if (!lt) {
-            qa = pf;
-            qb = pg;
+      // Order equivalence of g with f0 on the node's rows <=> the map code_f0 -> code_g over
+      // those rows is a function that is strictly increasing (ties align and the stable sorts
+      // by (code, canonical position) then coincide). Checked without any ordered scan: phi[a] =
+      // the g code of some row with f0 code a (racy plain stores), then every row must agree
+      // with phi and phi must increase over the present a. Rows come from the node's order-0
+      // segment in any order; items are batched through the (free) limb scratch.
+      {
+        uint16_t* phi = reinterpret_cast<uint16_t*>(s_limb);
+        const int cap = static_cast<int>((Lo.stage - Lo.limb) / 512);  // items of 256 u16 (>= 8)
+        const int neq = s_neq;
+        for (int b0 = 0; b0 < neq; b0 += cap) {
+          const int nb_items = min(cap, neq - b0);
+          for (int i = tid; i < nb_items * 256; i += kResThreads) phi[i] = 0xFFFFu;
+          if (tid < nb_items) {
+            const int s = s_items[b0 + tid] >> 16, g = s_items[b0 + tid] & 0xFFFF;
+            s_win[(s - first) * nrep + g].eq = 1;
           }
-          // along feature f0's order (codes non-decreasing) feature g must tie exactly where f0
-          // ties and increase where f0 increases
-          if (mem && qa >= 0 && ((a == qa) != (b == qb) || b < qb)) bad = true;
-          if (m) {
-            const int last = 31 - __clz(m);
-            pf = __shfl_sync(0xffffffffu, a, last);
-            pg = __shfl_sync(0xffffffffu, b, last);
+          __syncthreads();
+          for (int pass = 0; pass < 2; ++pass) {
+            for (int q = 0; q < nb_items; ++q) {
+              const int s = s_items[b0 + q] >> 16, g = s_items[b0 + q] & 0xFFFF;
+              const ResNode& nd = s_nodes[s];
+              const uint8_t* cf = s_codes + static_cast<size_t>(nd.eqf0) * cs;
+              const uint8_t* cg = s_codes + static_cast<size_t>(g) * cs;
+              uint16_t* ph = phi + q * 256;
+              bool bad = false;
+              for (int i = tid; i < nd.n; i += kResThreads) {
+                const int pr = s_ord0[nd.seg + i];
+                if (pass == 0) ph[cf[pr]] = cg[pr];
+                else bad |= ph[cf[pr]] != cg[pr];
+              }
+              if (pass == 1 && bad) s_win[(s - first) * nrep + g].eq = 0;
+            }
+            __syncthreads();
           }
+          // phi strictly increasing over the present f0 codes (warp per item)
+          for (int q = warp; q < nb_items; q += kResThreads / 32) {
+            const int s = s_items[b0 + q] >> 16, g = s_items[b0 + q] & 0xFFFF;
+            const int nb = s_repn[s_nodes[s].eqf0];
+            const uint16_t* ph = phi + q * 256;
+            int carry = -1;
+            bool bad = false;
+            for (int a0 = 0; a0 < nb; a0 += 32) {
+              const int a = a0 + lane;
+              const int v = a < nb ? ph[a] : 0xFFFF;
+              const bool present = v != 0xFFFF;
+              const unsigned m = __ballot_sync(0xffffffffu, present);
+              const unsigned lt = m & ((1u << lane) - 1u);
+              int pv = __shfl_sync(0xffffffffu, v, lt ? 31 - __clz(lt) : 0);
+              if (!lt) pv = carry;
+              if (present && pv >= 0 && v <= pv) bad = true;
+              if (m) carry = __shfl_sync(0xffffffffu, v, 31 - __clz(m));
+            }
+            if (__any_sync(0xffffffffu, bad) && lane == 0) s_win[(s - first) * nrep + g].eq = 0;
+          }
+          __syncthreads();
         }
-        bad = __any_sync(0xffffffffu, bad);
-        if (lane == 0) s_win[(s - first) * nrep + g].eq = !bad;
       }
-      __syncthreads();
       RES_PHASE(5);
       // ---- decide (decide_kernel) ------------------------------------------------------------
       if (tid == 0) s_nitems = 0;
@@ -2191,85 +2216,111 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       __syncthreads();
       RES_PHASE(6);
       // ---- reference-order folds (exact_kernel) ------------------------------------------------
-      for (int it = warp; it < s_nitems; it += kResThreads / 32) {
-        const int s = s_items[it] >> 16, j = s_items[it] & 0xFFFF;
-        ResNode& nd = s_nodes[s];
-        const int nv = nd.n;
-        if (j == 0xFFFF) {
-          if (lane == 0) nd.total = fold_seq(s_resid, s_ord0 + nd.seg, nv);
-          continue;
-        }
-        double* out = s_lbuf + static_cast<size_t>(s - first) * bins + s_repb[j];
-        const uint8_t* cj = s_codes + static_cast<size_t>(j) * n;
-        double left = 0.0;
-        int prev = -1, seen = 0;
-        int p_next = lane < n ? pre_at(j, lane) : 0;
-        for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
-          const int i = i0 + lane;
-          const int p = p_next;
-          p_next = i + 32 < n ? pre_at(j, i + 32) : 0;
-          const bool mem = i < n && s_node[p] == s;
-          const int code = mem ? cj[p] : 0;
-          const double rv = mem ? s_resid[p] : 0.0;
-          const unsigned m = __ballot_sync(0xffffffffu, mem);
-          seen += __popc(m);
-          // members in lane order; shuffles hoisted ahead of the dependent add chain
-          for (int l0 = 0; l0 < 32; l0 += 8) {
-            if (!((m >> l0) & 0xFFu)) continue;
-            int cc[8];
-            double vv[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              cc[k] = __shfl_sync(0xffffffffu, code, l0 + k);
-              vv[k] = __shfl_sync(0xffffffffu, rv, l0 + k);
+      // Warp per item. The node total is one fold over its order-0 segment. A window feature's
+      // fold walks the feature's presorted list: lanes test 32 entries for node membership, the
+      // members are compacted (ballot rank) into the warp's staging slots, and lane 0 folds them
+      // in list order, recording the left sum at every value boundary - but only up to the
+      // largest window left count (candidates beyond it cannot win, costmodel.cpp:65 strict >).
+      {
+        double* st_v = reinterpret_cast<double*>(sm + Lo.stage) + warp * 32;
+        uint8_t* st_c = sm + Lo.stage + static_cast<size_t>(kResThreads / 32) * 32 * 8 + warp * 32;
+        for (int it = warp; it < s_nitems; it += kResThreads / 32) {
+          const int s = s_items[it] >> 16, j = s_items[it] & 0xFFFF;
+          ResNode& nd = s_nodes[s];
+          const int nv = nd.n;
+          if (j == 0xFFFF) {
+            if (lane == 0) nd.total = fold_seq(s_resid, s_ord0 + nd.seg, nv);
+            continue;
+          }
+          const int need = s_win[(s - first) * nrep + j].maxlc;
+          double* out = s_lbuf + static_cast<size_t>(s - first) * bins + s_repb[j];
+          const uint8_t* cj = s_codes + static_cast<size_t>(j) * cs;
+          double left = 0.0;
+          int prev = -1, seen = 0;
+          int p_next = lane < n ? pre_at(j, lane) : 0;
+          for (int i0 = 0; i0 < n && seen < need; i0 += 32) {
+            const int i = i0 + lane;
+            const int p = p_next;
+            p_next = i + 32 < n ? pre_at(j, i + 32) : 0;
+            const bool mem = i < n && s_node[p] == s;
+            const unsigned m = __ballot_sync(0xffffffffu, mem);
+            if (mem) {
+              const int dst = __popc(m & ((1u << lane) - 1u));
+              st_v[dst] = s_resid[p];
+              st_c[dst] = cj[p];
             }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              if ((m >> (l0 + k)) & 1u) {
-                if (prev >= 0 && cc[k] != prev && lane == 0) out[prev] = left;
-                left = fs_add(left, vv[k]);
-                prev = cc[k];
+            __syncwarp();
+            const int cnt = min(__popc(m), need - seen);
+            if (lane == 0) {
+#pragma unroll 8
+              for (int t = 0; t < cnt; ++t) {
+                const int c = st_c[t];
+                if (c != prev && prev >= 0) out[prev] = left;
+                left = fs_add(left, st_v[t]);
+                prev = c;
               }
             }
+            seen += cnt;
+            __syncwarp();
           }
+          if (lane == 0 && prev >= 0) out[prev] = left;
         }
       }
       __syncthreads();
       RES_PHASE(7);
-      // ---- exact decision (exact_decide_kernel) -------------------------------------------------
-      if (tid < nl) {
-        const int k = tid;
+      // ---- exact decision (exact_decide_kernel): warp per node, lanes over a window feature's
+      // bins; the reference's strict > over (feature asc, threshold asc) = first occurrence of
+      // the maximum, so the warp reduction keeps the largest gain and, on equal gains, the
+      // earliest (feature, bin).
+      for (int k = warp; k < nl; k += kResWarps) {
         ResNode& nd = s_nodes[first + k];
-        if (nd.state == kNodeExact) {
-          const WinRec* w = s_win + k * nrep;
-          const int nv = nd.n;
-          const double T = nd.total;
-          const double parent = fs_div(fs_mul(T, T), static_cast<double>(nv));
-          double best = 0.0;
-          int bj = -1, bbin = -1, blc = 0;
-          for (int j = 0; j < nrep; ++j) {
-            if (!w[j].flag) continue;
-            const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
-            const double* lb = s_lbuf + static_cast<size_t>(k) * bins + s_repb[j];
-            int cum = 0;
-            for (int b = 0; b < s_repn[j]; ++b) {
-              const int cb = c[b];
-              if (!cb) continue;
-              cum += cb;
-              if (cum >= nv) break;
+        if (nd.state != kNodeExact) continue;
+        const WinRec* w = s_win + k * nrep;
+        const int nv = nd.n;
+        const double T = nd.total;
+        const double parent = fs_div(fs_mul(T, T), static_cast<double>(nv));
+        double best = 0.0;
+        int bj = -1, bbin = -1, blc = 0;
+        for (int j = 0; j < nrep; ++j) {
+          if (!w[j].flag) continue;
+          const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+          const double* lb = s_lbuf + static_cast<size_t>(k) * bins + s_repb[j];
+          const int nb = s_repn[j], lim = w[j].maxlc;
+          int carry = 0;
+          for (int b0 = 0; b0 < nb && carry < lim; b0 += 32) {
+            const int b = b0 + lane;
+            const int cb = b < nb ? c[b] : 0;
+            const int cum = warp_incl_scan(cb, lane) + carry;
+            if (cb > 0 && cum < nv && cum <= lim) {  // folds stop at the last window candidate
               const double L = lb[b];
               const double R = fs_sub(T, L);
               const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
               const double r = fs_div(fs_mul(R, R), static_cast<double>(nv - cum));
               const double g = fs_sub(fs_add(a, r), parent);
-              if (g > best) {
+              if (g > best) {  // lanes ascend in b, so a lane keeps its first maximum
                 best = g;
                 bj = j;
                 bbin = b;
                 blc = cum;
               }
             }
+            carry = __shfl_sync(0xffffffffu, cum, 31);
           }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          const int obin = __shfl_xor_sync(0xffffffffu, bbin, o);
+          const int olc = __shfl_xor_sync(0xffffffffu, blc, o);
+          const bool take = oj >= 0 && (bj < 0 || ob > best || (ob == best && (oj < bj || (oj == bj && obin < bbin))));
+          if (take) {
+            best = ob;
+            bj = oj;
+            bbin = obin;
+            blc = olc;
+          }
+        }
+        if (lane == 0) {
           if (bj < 0) {
             nd.state = kNodeLeaf;
           } else {
@@ -2336,7 +2387,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                 p = s_scr[i];
                 v = s_node[p];
                 if (s_nodes[v].state != kNodeSplit) v = -1;
-                else left = s_codes[static_cast<size_t>(s_nodes[v].rep) * n + p] <= s_nodes[v].bin;
+                else left = s_codes[static_cast<size_t>(s_nodes[v].rep) * cs + p] <= s_nodes[v].bin;
               }
               const unsigned bal = __ballot_sync(0xffffffffu, left);
               if (lane == 0) s_wsum[warp] = __popc(bal);
@@ -2871,7 +2922,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
         for (int f = 0; f < F; ++f) {
           const FamDesc& fd = fam[static_cast<size_t>(f)];
           if (fd.n <= 0 || fd.trees <= 0) continue;
-          if (fd.n > 65535) ok = false;
+          if (fd.n > 65535 || fd.nrep > 1024) ok = false;
           need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups, pre_smem).total);
           fams_ok.push_back(f);
         }

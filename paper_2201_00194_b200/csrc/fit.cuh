@@ -97,7 +97,7 @@ struct WinRec {
   int32_t count;    // window candidates of this feature
   int32_t best_lc;  // left count of the best candidate
   int32_t eq;       // order-equivalent (within the node) to the node's lowest window feature
-  int32_t pad_;
+  int32_t maxlc;    // largest left count among the feature's window candidates
 };
 
 }  // namespace fit

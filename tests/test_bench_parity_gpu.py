@@ -1,0 +1,54 @@
+"""Parity at the benchmark's own workloads (bench.py configs): every family of the round is fitted
+on the GPU in one batched call and must reproduce the oracle's trees bit for bit, and the scored
+pool's scores and (score, index) ranking must match. C1-C3 exercise the resident trainer (one CTA
+per family), C4 (fewer trees, so the oracle finishes in seconds) the multi-kernel round."""
+import numpy as np
+import pytest
+
+import bench
+import oracle
+import paper_2201_00194_b200 as fs
+
+pytestmark = pytest.mark.gpu
+FIELDS = ("offsets", "feature", "threshold", "left", "right", "value")
+
+
+@pytest.mark.parametrize("cfg,trees,path", [("c1", 100, "auto"), ("c2", 100, "auto"), ("c3", 60, "auto"),
+                                            ("c2", 30, "multi"), ("c4", 12, "auto")])
+def test_bench_round_bit_exact(dev, orc, monkeypatch, cfg, trees, path):
+    monkeypatch.setenv("FAMSEER_FIT_PATH", path)
+    W = bench.build_workload(cfg, 1000)
+    x = bench._featurize_host(W, orc)
+    seg, y = W["tr_seg"], W["tr_y"]
+    F = len(W["families"])
+    fo = fs.Forest(dev, F)
+    fo.fit(x, y, seg=list(seg), params=fs.GbtParams(trees, 3, 0.1, 2))
+    sp = fs.Spaces(dev, W["spaces"])
+    scores, perm = sp.score(fo, W["pool_so"], W["pool_a"], bench.PAD, W["pool_seg"])
+    xp = None
+    for f in range(F):
+        a, b = int(seg[f]), int(seg[f + 1])
+        exp = orc.fit(x[a:b], y[a:b], trees=trees)
+        got = fo.export(f)
+        assert got.base == exp.base, (cfg, f)
+        for k in FIELDS:
+            assert np.array_equal(getattr(got, k), getattr(exp, k)), (cfg, f, k)
+        internal = exp.feature >= 0
+        np.testing.assert_allclose(got.gain[internal], exp.gain[internal], rtol=1e-5, atol=0)
+        # scoring: featurize + predict + rank of this family's pool
+        pa, pb = int(W["pool_seg"][f]), int(W["pool_seg"][f + 1])
+        if xp is None:
+            xp = _featurize_pool(W, orc)
+        s_exp = orc.predict(exp, xp[pa:pb])
+        assert np.array_equal(scores[pa:pb], s_exp), (cfg, f)
+        assert np.array_equal(perm[pa:pb], orc.rank(s_exp)), (cfg, f)
+
+
+def _featurize_pool(W, orc):
+    P = int(W["pool_seg"][-1])
+    x = np.zeros((P, bench.PAD))
+    for sid in np.unique(W["pool_so"]):
+        rows = np.where(W["pool_so"] == sid)[0]
+        kn = W["spaces"][sid]
+        x[rows] = orc.featurize(kn, W["pool_a"][rows][:, : len(kn)], bench.PAD)
+    return x
