@@ -1603,12 +1603,16 @@ __global__ void commit_mse_kernel(const FamDesc* __restrict__ fam, FamState* __r
 // C1-C3) the multi-kernel round above is launch- and L2-latency-bound (~40 launches per round);
 // here a round is ~30 block barriers. Same algorithm, same arithmetic, same tie handling.
 // ==========================================================================================
+#ifndef FS_RES_THREADS
+#define FS_RES_THREADS 512
+#endif
 namespace fs {
 namespace fit {
 namespace {
 
-constexpr int kResThreads = 1024;
+constexpr int kResThreads = FS_RES_THREADS;
 constexpr int kResWarps = kResThreads / 32;
+constexpr int kPartE = 4;  // partition: consecutive order-0 entries per thread per chunk
 constexpr int kResMaxDepth = 7;  // node ids fit in uint8
 
 struct ResNode {
@@ -1621,7 +1625,7 @@ struct ResNode {
 
 struct ResLayout {
   int ls, slots, cs;
-  size_t codes, resid, pred, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, cand,
+  size_t codes, resid, pred, fix, node, rowk, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, cand,
       total;
 };
 
@@ -1647,6 +1651,8 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   L.fix = o;
   o = res_align(o + static_cast<size_t>(n) * 8);
   L.node = o;
+  o = res_align(o + static_cast<size_t>(n));
+  L.rowk = o;  // per row: its level node's index when that node's histogram is built, else 0xFF
   o = res_align(o + static_cast<size_t>(n));
   L.ord0 = o;
   o = res_align(o + static_cast<size_t>(n) * 2);
@@ -1730,7 +1736,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   __shared__ unsigned long long s_red[32];
   __shared__ double s_dred[32];
   __shared__ int s_wsum[32];
-  __shared__ int s_shift, s_nitems, s_stop, s_base_l, s_base_r;
+  __shared__ int s_shift, s_nitems, s_ctot;
   __shared__ unsigned long long s_cnt[3];  // screened splits, exact nodes, exact folds
   __shared__ unsigned long long s_why[4];  // exact-node reasons
   const int f = fam_list[blockIdx.x];
@@ -1763,6 +1769,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   };
   long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
   uint8_t* s_node = sm + Lo.node;
+  uint8_t* s_rowk = sm + Lo.rowk;
   uint16_t* s_ord0 = reinterpret_cast<uint16_t*>(sm + Lo.ord0);
   uint16_t* s_scr = reinterpret_cast<uint16_t*>(sm + Lo.scratch);
   long long* s_hsum = reinterpret_cast<long long*>(sm + Lo.hsum);
@@ -1775,9 +1782,6 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   int* s_repn = s_repb + (nrep > 0 ? nrep : 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ls = Lo.ls, slots = Lo.slots;
-  // ceil(2^32 / nrep): e / nrep == umulhi(e, magic) for e < 2^32 / nrep (nrep >= 2; the host
-  // keeps nrep <= 1024 on this path, so every e < kAtomSub * nrep qualifies)
-  const unsigned nrep_magic = nrep > 1 ? static_cast<unsigned>((0x100000000ull + nrep - 1) / nrep) : 0u;
   unsigned long long c_hist_rows = 0;
   if (tid < 3) s_cnt[tid] = 0;
   if (tid < 4) s_why[tid] = 0;
@@ -1794,7 +1798,6 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
   if (pre_smem)
     for (int i = tid; i < n * nrep; i += kResThreads) s_pre[i] = static_cast<uint16_t>(g_pre[i]);
-  if (tid == 0) s_stop = 0;
   __syncthreads();
 
   int ntrees = 0;
@@ -1870,40 +1873,50 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       }
       __syncthreads();
       // ---- histograms of every directly built node of the level in ONE sweep over the rows:
-      // a warp takes 32 consecutive rows of one feature (conflict-free code loads; rows are read
-      // in canonical position order, no index chasing) and adds each row's three 21-bit limbs of
-      // u = v + 2^62 into its node's limb histogram with native 32-bit shared atomics (plus the
-      // limbs of |v| for the screen bound, on the feature-0 items). Every kAtomSub rows the limb
-      // sums are folded exactly into the nodes' 64-bit histograms (see hist_build_atomic_kernel
-      // for the arithmetic).
+      // thread t owns feature j = t % nrep (nrep <= kResThreads here) and walks rows r = t / nrep,
+      // + G, ... (G = kResThreads / nrep), so a warp's lanes hit different features (bins apart, no
+      // same-address atomics) and the code loads fall in different banks (cs = 4 mod 128). Rows
+      // of built nodes carry their level-node index in s_rowk. Each row adds the three 21-bit
+      // limbs of u = v + 2^62 to its node's limb histogram with native 32-bit shared atomics
+      // (plus the limbs of |v| for the screen bound, by the feature-0 threads). Every kAtomSub
+      // rows the limb sums are folded exactly into the nodes' 64-bit histograms (see
+      // hist_build_atomic_kernel for the arithmetic).
       {
         const int lstride = 3 * bins + 3;
         int nbuilt = 0;
         for (int k = 0; k < nl; ++k) nbuilt += s_nodes[first + k].build == 1;
         if (nbuilt) {
+          for (int p = tid; p < n; p += kResThreads) {
+            const int k = static_cast<int>(s_node[p]) - first;
+            s_rowk[p] = (k >= 0 && k < nl && s_nodes[first + k].build == 1) ? static_cast<uint8_t>(k) : 0xFF;
+          }
+          const int G = kResThreads / nrep;
+          const int hj = tid - (tid / nrep) * nrep, hr = tid / nrep;
+          const bool hact = hr < G;
+          const uint8_t* hcode = s_codes + static_cast<size_t>(hj) * cs;
+          const int hbin0 = s_repb[hj];
           for (int sub0 = 0; sub0 < n; sub0 += kAtomSub) {
             for (int i = tid; i < nl * lstride; i += kResThreads) s_limb[i] = 0;
             __syncthreads();
-            const int rows = min(kAtomSub, n - sub0);
-            const unsigned total = static_cast<unsigned>(rows) * static_cast<unsigned>(nrep);
-            for (unsigned e = tid; e < total; e += kResThreads) {
-              const int r = nrep == 1 ? static_cast<int>(e) : static_cast<int>(__umulhi(e, nrep_magic));  // e / nrep
-              const int j = static_cast<int>(e) - r * nrep;
-              const int p = sub0 + r;
-              const int k = static_cast<int>(s_node[p]) - first;
-              if (k < 0 || k >= nl || s_nodes[first + k].build != 1) continue;
-              const long long v = s_fix[p];
-              const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
-              uint32_t* lb = s_limb + k * lstride;
-              const int bin = s_repb[j] + s_codes[static_cast<size_t>(j) * cs + p];
-              atomicAdd(lb + bin, static_cast<uint32_t>(u) & kLimbMask);
-              atomicAdd(lb + bins + bin, static_cast<uint32_t>(u >> 21) & kLimbMask);
-              atomicAdd(lb + 2 * bins + bin, static_cast<uint32_t>(u >> 42));
-              if (j == 0) {
-                const uint64_t av = static_cast<uint64_t>(v < 0 ? -v : v);
-                atomicAdd(lb + 3 * bins, static_cast<uint32_t>(av) & kLimbMask);
-                atomicAdd(lb + 3 * bins + 1, static_cast<uint32_t>(av >> 21) & kLimbMask);
-                atomicAdd(lb + 3 * bins + 2, static_cast<uint32_t>(av >> 42));
+            const int sub_end = min(n, sub0 + kAtomSub);
+            if (hact) {
+#pragma unroll 4
+              for (int p = sub0 + hr; p < sub_end; p += G) {
+                const int k = s_rowk[p];
+                if (k == 0xFF) continue;
+                const long long v = s_fix[p];
+                const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+                uint32_t* lb = s_limb + k * lstride + hbin0 + hcode[p];
+                atomicAdd(lb, static_cast<uint32_t>(u) & kLimbMask);
+                atomicAdd(lb + bins, static_cast<uint32_t>(u >> 21) & kLimbMask);
+                atomicAdd(lb + 2 * bins, static_cast<uint32_t>(u >> 42));
+                if (hj == 0) {
+                  const uint64_t av = static_cast<uint64_t>(v < 0 ? -v : v);
+                  uint32_t* la = s_limb + k * lstride + 3 * bins;
+                  atomicAdd(la, static_cast<uint32_t>(av) & kLimbMask);
+                  atomicAdd(la + 1, static_cast<uint32_t>(av >> 21) & kLimbMask);
+                  atomicAdd(la + 2, static_cast<uint32_t>(av >> 42));
+                }
               }
             }
             __syncthreads();
@@ -2281,8 +2294,28 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         const double parent = fs_div(fs_mul(T, T), static_cast<double>(nv));
         double best = 0.0;
         int bj = -1, bbin = -1, blc = 0;
+        // features with one window candidate (the common case): lane per feature, the only
+        // candidate that can win on that feature is its window candidate (best_bin / best_lc:
+        // every other candidate's gain is provably below LO, costmodel.cpp:65 strict >)
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          if (j < nrep && w[j].flag && w[j].count == 1) {
+            const int cum = w[j].best_lc;
+            const double L = s_lbuf[static_cast<size_t>(k) * bins + s_repb[j] + w[j].best_bin];
+            const double R = fs_sub(T, L);
+            const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+            const double r = fs_div(fs_mul(R, R), static_cast<double>(nv - cum));
+            const double g = fs_sub(fs_add(a, r), parent);
+            if (g > best) {  // first candidate of this lane: no earlier (feature, bin) to beat
+              best = g;
+              bj = j;
+              bbin = w[j].best_bin;
+              blc = cum;
+            }
+          }
+        }
         for (int j = 0; j < nrep; ++j) {
-          if (!w[j].flag) continue;
+          if (!w[j].flag || w[j].count == 1) continue;
           const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
           const double* lb = s_lbuf + static_cast<size_t>(k) * bins + s_repb[j];
           const int nb = s_repn[j], lim = w[j].maxlc;
@@ -2297,7 +2330,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
               const double r = fs_div(fs_mul(R, R), static_cast<double>(nv - cum));
               const double g = fs_sub(fs_add(a, r), parent);
-              if (g > best) {  // lanes ascend in b, so a lane keeps its first maximum
+              // a lane's candidates do not arrive in (feature, bin) order: full tie-break
+              if (g > best || (g == best && bj >= 0 && (j < bj || (j == bj && b < bbin)))) {
                 best = g;
                 bj = j;
                 bbin = b;
@@ -2369,51 +2403,74 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       // ---- stable partition of every split node's order-0 segment (costmodel.cpp:94-105 for
       // list 0) in one sweep over the whole list: a block-wide exclusive scan of "goes left"
       // flags; its value at the node's segment start turns it into the rank inside the node
-      // (segments are contiguous). Pass 0 records the per-node scan bases, pass 1 scatters.
+      // (segments are contiguous). Elements are read once into registers (kPartE consecutive per
+      // thread per chunk), scattered into the other order buffer, and the buffers swap.
       {
         int nsplit = 0;
         for (int k = 0; k < nl; ++k) nsplit += s_nodes[first + k].state == kNodeSplit;
         if (nsplit) {
-          for (int i = tid; i < n; i += kResThreads) s_scr[i] = s_ord0[i];
-          __syncthreads();
-          for (int pass = 0; pass < 2; ++pass) {
-            if (tid == 0) s_base_l = 0;
-            __syncthreads();
-            for (int t0 = 0; t0 < n; t0 += kResThreads) {
-              const int i = t0 + tid;
-              int p = 0, v = -1;
-              bool left = false;
+          int base = 0;  // exclusive scan carried across chunks (uniform)
+          for (int c0 = 0; c0 < n; c0 += kResThreads * kPartE) {
+            int pe[kPartE], ve[kPartE];
+            bool le[kPartE];
+            int cnt = 0;
+#pragma unroll
+            for (int e = 0; e < kPartE; ++e) {
+              const int i = c0 + tid * kPartE + e;
+              pe[e] = 0;
+              ve[e] = -1;
+              le[e] = false;
               if (i < n) {
-                p = s_scr[i];
-                v = s_node[p];
-                if (s_nodes[v].state != kNodeSplit) v = -1;
-                else left = s_codes[static_cast<size_t>(s_nodes[v].rep) * cs + p] <= s_nodes[v].bin;
-              }
-              const unsigned bal = __ballot_sync(0xffffffffu, left);
-              if (lane == 0) s_wsum[warp] = __popc(bal);
-              __syncthreads();
-              if (warp == 0) {
-                const int wv = s_wsum[lane];
-                s_wsum[lane] = warp_incl_scan(wv, lane) - wv;
-              }
-              __syncthreads();
-              const int P = s_base_l + s_wsum[warp] + __popc(bal & ((1u << lane) - 1u));
-              if (v >= 0) {
-                ResNode& nd = s_nodes[v];
-                if (pass == 0) {
-                  if (i == nd.seg) nd.pad_ = P;
-                } else {
-                  const int lrank = P - nd.pad_;
-                  const int dst = left ? nd.seg + lrank : nd.seg + nd.lc + (i - nd.seg) - lrank;
-                  s_ord0[dst] = static_cast<uint16_t>(p);
-                  s_node[p] = static_cast<uint8_t>(left ? 2 * v + 1 : 2 * v + 2);
+                pe[e] = s_ord0[i];
+                const int v = s_node[pe[e]];
+                if (s_nodes[v].state == kNodeSplit) {
+                  ve[e] = v;
+                  le[e] = s_codes[static_cast<size_t>(s_nodes[v].rep) * cs + pe[e]] <= s_nodes[v].bin;
                 }
               }
-              __syncthreads();
-              if (tid == kResThreads - 1) s_base_l += s_wsum[31] + __popc(bal);
-              __syncthreads();
+              cnt += le[e];
             }
+            const int incl = warp_incl_scan(cnt, lane);
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+              const int wv = lane < kResWarps ? s_wsum[lane] : 0;
+              const int inc = warp_incl_scan(wv, lane);
+              s_wsum[lane] = inc - wv;
+              if (lane == 31) s_ctot = inc;
+            }
+            __syncthreads();
+            int P = base + s_wsum[warp] + incl - cnt;  // exclusive scan at this thread's first element
+            const int chunk_total = s_ctot;
+            int Pe[kPartE];
+#pragma unroll
+            for (int e = 0; e < kPartE; ++e) {
+              Pe[e] = P;
+              P += le[e];
+              const int i = c0 + tid * kPartE + e;
+              if (ve[e] >= 0 && i == s_nodes[ve[e]].seg) s_nodes[ve[e]].pad_ = Pe[e];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < kPartE; ++e) {
+              const int i = c0 + tid * kPartE + e;
+              if (i >= n) continue;
+              if (ve[e] < 0) {
+                s_scr[i] = static_cast<uint16_t>(pe[e]);
+                continue;
+              }
+              const ResNode& nd = s_nodes[ve[e]];
+              const int lrank = Pe[e] - nd.pad_;
+              const int dst = le[e] ? nd.seg + lrank : nd.seg + nd.lc + (i - nd.seg) - lrank;
+              s_scr[dst] = static_cast<uint16_t>(pe[e]);
+              s_node[pe[e]] = static_cast<uint8_t>(le[e] ? 2 * ve[e] + 1 : 2 * ve[e] + 2);
+            }
+            base += chunk_total;
+            __syncthreads();
           }
+          uint16_t* t = s_ord0;
+          s_ord0 = s_scr;
+          s_scr = t;
         }
       }
       RES_PHASE(9);
@@ -2922,7 +2979,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
         for (int f = 0; f < F; ++f) {
           const FamDesc& fd = fam[static_cast<size_t>(f)];
           if (fd.n <= 0 || fd.trees <= 0) continue;
-          if (fd.n > 65535 || fd.nrep > 1024) ok = false;
+          if (fd.n > 65535 || fd.nrep > kResThreads) ok = false;
           need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups, pre_smem).total);
           fams_ok.push_back(f);
         }
