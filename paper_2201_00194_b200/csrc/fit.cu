@@ -1625,8 +1625,8 @@ struct ResNode {
 
 struct ResLayout {
   int ls, slots, cs;
-  size_t codes, resid, pred, fix, node, rowk, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, cand,
-      total;
+  size_t codes, resid, pred, fix, node, rowk, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, clc, binrep,
+      cand, total;
 };
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
@@ -1677,6 +1677,10 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   (void)groups;
   L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
   o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
+  L.clc = o;  // left count per (node at level, bin)
+  o = res_align(o + static_cast<size_t>(L.ls) * bins * 4);
+  L.binrep = o;  // feature (rep) of every bin
+  o = res_align(o + static_cast<size_t>(bins) * 2);
   L.cand = o;  // screened (gain, bound) per (node at level, bin)
   o = res_align(o + static_cast<size_t>(L.ls) * bins * 16);
   L.total = o;
@@ -1747,6 +1751,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const int cs = Lo.cs;
   uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [level node][3 * bins + 3]
   double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
+  int* s_clc = reinterpret_cast<int*>(sm + Lo.clc);           // [level node][bin] left count
+  uint16_t* s_binrep = reinterpret_cast<uint16_t*>(sm + Lo.binrep);
   __shared__ int s_neq;
   // phase timers (CTA 0, thread 0): where a round's cycles go (fs_device_counters [4..15])
   __shared__ long long s_ph[12];
@@ -1793,6 +1799,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   for (int j = tid; j < nrep; j += kResThreads) {
     s_repb[j] = rep_boff[fd.rep0 + j];
     s_repn[j] = rep_nb[fd.rep0 + j];
+    for (int b = 0; b < rep_nb[fd.rep0 + j]; ++b) s_binrep[rep_boff[fd.rep0 + j] + b] = static_cast<uint16_t>(j);
   }
   const double b0 = base[f];
   for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
@@ -1976,98 +1983,93 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         __syncthreads();
       RES_PHASE(3);
       }
-      // ---- screen: warp per (node, feature), lanes over bins. Pass 0 computes every candidate's
-      // screened gain and bound once (cached) and the node's max lower bound; pass 1 forms the
-      // window {hi >= LO, hi > 0} and records each feature's count / best / left count.
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int it = warp; it < nl * nrep; it += kResThreads / 32) {
-          const int k = it / nrep, j = it - k * nrep;
-          ResNode& nd = s_nodes[first + k];
-          if (nd.state != 0 || nd.build == 0) continue;
-          const int nv = nd.n;
-          const long long* h = hs + static_cast<size_t>(k) * bins + s_repb[j];
-          const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
-          double* cand = s_cand + 2 * (static_cast<size_t>(k) * bins + s_repb[j]);
-          const int nb = s_repn[j];
-          long long ts = 0;
-          if (!pass) {
-            for (int b = lane; b < nb; b += 32) ts += h[b];
-            for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
-          }
-          const double S = static_cast<double>(nd.absfix) * scale * (1.0 + 1e-12);
-          const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
-          double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
-          int bb = 0x7fffffff, blc = 0, count = 0, carry_c = 0, mlc = 0;
-          long long carry_s = 0;
-          for (int b0 = 0; b0 < nb; b0 += 32) {
-            const int b = b0 + lane;
-            const int cc = b < nb ? c[b] : 0;
-            const int ic = warp_incl_scan(cc, lane) + carry_c;
-            if (!pass) {
-              const long long ss = b < nb ? h[b] : 0;
-              const long long is = warp_incl_scan(ss, lane) + carry_s;
-              if (b < nb) {
-                if (cc > 0 && ic < nv) {
-                  double g, lo, hi;
+      // ---- screen: thread per candidate (level node k, bin). Pass 0: the feature's prefix
+      // count / sum up to the bin by a short loop over its bins, the screened gain and its bound
+      // (cached), the node's max lower bound (segmented warp max, then one 64-bit atomicMax per
+      // node segment of the warp). Pass 1: window membership {hi >= LO, hi > 0} with 32-bit
+      // atomics: per (node, feature) window count and largest left count; the candidate's data
+      // is written racily, which is exact whenever the feature has ONE window candidate - the
+      // only case that reads it.
+      {
+        const int ncand = nl * bins;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int c0 = 0; c0 < ncand; c0 += kResThreads) {
+            const int ci = c0 + tid;
+            int k = ci < ncand ? ci / bins : nl;
+            const int bi = ci - k * bins;
+            bool live = k < nl;
+            ResNode* ndp = live ? &s_nodes[first + k] : nullptr;
+            if (live && (ndp->state != 0 || ndp->build == 0)) live = false;
+            int j = 0, b = 0, ic = 0;
+            double lo = -INFINITY;
+            if (live) {
+              j = s_binrep[bi];
+              b = bi - s_repb[j];
+            }
+            if (pass == 0) {
+              if (live) {
+                const int nb = s_repn[j];
+                const long long* h = hs + static_cast<size_t>(k) * bins + s_repb[j];
+                const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+                if (b == 0) {
+                  WinRec z;
+                  memset(&z, 0, sizeof z);
+                  z.best_bin = -1;
+                  s_win[k * nrep + j] = z;
+                }
+                long long is = 0, ts = 0;
+                for (int t = 0; t < nb; ++t) {
+                  const long long hv = h[t];
+                  ts += hv;
+                  if (t <= b) {
+                    is += hv;
+                    ic += c[t];
+                  }
+                }
+                s_clc[ci] = ic;
+                const int nv = ndp->n;
+                if (c[b] > 0 && ic < nv) {
+                  const double S = static_cast<double>(ndp->absfix) * scale * (1.0 + 1e-12);
+                  double g, hi;
                   screen_gain(is, ts, ic, nv, scale, S, g, lo, hi);
-                  cand[2 * b] = g;
-                  cand[2 * b + 1] = hi - g;
-                  best_lo = fmax(best_lo, lo);
+                  s_cand[2 * ci] = g;
+                  s_cand[2 * ci + 1] = hi - g;
                 } else {
-                  cand[2 * b] = NAN;
+                  s_cand[2 * ci] = NAN;
                 }
               }
-              carry_s = __shfl_sync(0xffffffffu, is, 31);
-            } else if (b < nb && cc > 0 && ic < nv) {
-              const double g = cand[2 * b], dl = cand[2 * b + 1];
-              const double hi = g + dl;
-              if (hi >= LO && hi > 0.0) {
-                ++count;
-                mlc = max(mlc, ic);
-                if (g > bg || (g == bg && b < bb)) {
-                  bg = g;
-                  bl = g - dl;
-                  bb = b;
-                  blc = ic;
+              // segmented (by node) warp max of the lower bounds; lanes' nodes are non-decreasing
+              const int kk = live ? k : -1;
+              double m = lo;
+              for (int o = 1; o < 32; o <<= 1) {
+                const double om = __shfl_up_sync(0xffffffffu, m, o);
+                const int ok_ = __shfl_up_sync(0xffffffffu, kk, o);
+                if (lane >= o && ok_ == kk) m = fmax(m, om);
+              }
+              const int knext = __shfl_down_sync(0xffffffffu, kk, 1);
+              if (kk >= 0 && (lane == 31 || knext != kk) && m > -INFINITY) atomicMax(&ndp->lokey, lo_key(m));
+            } else if (live) {
+              const double g = s_cand[2 * ci];
+              if (!isnan(g)) {
+                const double dl = s_cand[2 * ci + 1];
+                const double hi = g + dl;
+                if (hi >= lo_from_key(ndp->lokey) && hi > 0.0) {
+                  WinRec& w = s_win[k * nrep + j];
+                  ic = s_clc[ci];
+                  atomicAdd(&w.count, 1);
+                  atomicMax(&w.maxlc, ic);
+                  atomicAdd(&ndp->wcount, 1);
+                  w.flag = 1;
+                  w.best_g = g;
+                  w.best_lo = g - dl;
+                  w.best_bin = b;
+                  w.best_lc = ic;
                 }
               }
             }
-            carry_c = __shfl_sync(0xffffffffu, ic, 31);
           }
-          if (!pass) {
-            best_lo = warp_max_d(best_lo);
-            if (lane == 0 && best_lo > -INFINITY) atomicMax(&nd.lokey, lo_key(best_lo));
-          } else {
-            for (int o = 16; o > 0; o >>= 1) {
-              count += __shfl_xor_sync(0xffffffffu, count, o);
-              mlc = max(mlc, __shfl_xor_sync(0xffffffffu, mlc, o));
-              const double og = __shfl_xor_sync(0xffffffffu, bg, o);
-              const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
-              const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
-              const int olc = __shfl_xor_sync(0xffffffffu, blc, o);
-              if (og > bg || (og == bg && ob < bb)) {
-                bg = og;
-                bl = ol;
-                bb = ob;
-                blc = olc;
-              }
-            }
-            if (lane == 0) {
-              WinRec w;
-              w.best_g = bg;
-              w.best_lo = bl;
-              w.best_bin = count ? bb : -1;
-              w.flag = count > 0;
-              w.count = count;
-              w.best_lc = blc;
-              w.eq = 0;
-              w.maxlc = mlc;
-              s_win[k * nrep + j] = w;
-              if (count) atomicAdd(&nd.wcount, count);
-            }
-          }
+          __syncthreads();
         }
-        __syncthreads();
       }
       RES_PHASE(4);
       // ---- tie classes: a window whose candidates (one per feature, equal left counts) come
