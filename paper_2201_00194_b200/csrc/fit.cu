@@ -1625,15 +1625,15 @@ struct ResNode {
 
 struct ResLayout {
   int ls, slots, cs;
-  size_t codes, resid, pred, fix, node, rowk, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, clc, binrep,
-      cand, total;
+  size_t codes, resid, pred, predv, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, clc, binrep,
+      vals, cand, total;
 };
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
 
 // groups: private histogram copies used while accumulating one node (threads own
 // (feature, group) pairs, so no shared-memory atomics are needed).
-__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, int groups, bool pre_smem) {
+__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, bool pred_smem, bool pre_smem) {
   ResLayout L;
   L.ls = depth > 0 ? (1 << (depth - 1)) : 1;
   L.slots = (1 << (depth + 1)) - 1;
@@ -1648,11 +1648,11 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(n) * 8);
   L.pred = o;  // presorted lists [nrep][n] as u16 (when pre_smem), else empty
   o = res_align(o + (pre_smem ? static_cast<size_t>(n) * nr * 2 : 0));
+  L.predv = o;  // running predictions (when pred_smem), else they live in global memory
+  o = res_align(o + (pred_smem ? static_cast<size_t>(n) * 8 : 0));
   L.fix = o;
   o = res_align(o + static_cast<size_t>(n) * 8);
   L.node = o;
-  o = res_align(o + static_cast<size_t>(n));
-  L.rowk = o;  // per row: its level node's index when that node's histogram is built, else 0xFF
   o = res_align(o + static_cast<size_t>(n));
   L.ord0 = o;
   o = res_align(o + static_cast<size_t>(n) * 2);
@@ -1672,15 +1672,16 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(L.ls) * (nr + 1) * sizeof(int));
   L.rep = o;
   o = res_align(o + 2 * nr * sizeof(int));
-  L.limb = o;  // per level node: 3 x 32-bit limb sums per bin + 3 limbs of sum |v| (histogram sweep)
-  o = res_align(o + std::max<size_t>(static_cast<size_t>(L.ls) * (3 * static_cast<size_t>(bins) + 3) * 4, 8 * 512));
-  (void)groups;
+  L.limb = o;  // per level node: 3 x 32-bit limb sums per bin, then 4 x 16-bit limbs of sum |v| per node
+  o = res_align(o + std::max<size_t>(static_cast<size_t>(L.ls) * (3 * static_cast<size_t>(bins) + 4) * 4, 8 * 512));
   L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
   o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
   L.clc = o;  // left count per (node at level, bin)
   o = res_align(o + static_cast<size_t>(L.ls) * bins * 4);
   L.binrep = o;  // feature (rep) of every bin
   o = res_align(o + static_cast<size_t>(bins) * 2);
+  L.vals = o;  // threshold value of every bin + original feature of every rep (split records)
+  o = res_align(o + static_cast<size_t>(bins) * 8 + nr * 4);
   L.cand = o;  // screened (gain, bound) per (node at level, bin)
   o = res_align(o + static_cast<size_t>(L.ls) * bins * 16);
   L.total = o;
@@ -1735,7 +1736,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
     const int32_t* __restrict__ cle, const int32_t* __restrict__ canon, const double* __restrict__ x, int d,
     TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
-    unsigned long long* __restrict__ ctr, int groups, double* __restrict__ pred_g, int pre_smem) {
+    unsigned long long* __restrict__ ctr, int pred_smem, double* __restrict__ pred_g, int pre_smem) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ unsigned long long s_red[32];
   __shared__ double s_dred[32];
@@ -1746,13 +1747,15 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const int f = fam_list[blockIdx.x];
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
-  const ResLayout Lo = res_layout(n, nrep, bins, depth, groups, pre_smem != 0);
+  const ResLayout Lo = res_layout(n, nrep, bins, depth, pred_smem != 0, pre_smem != 0);
   uint8_t* s_codes = sm + Lo.codes;  // [nrep][cs]
   const int cs = Lo.cs;
-  uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [level node][3 * bins + 3]
+  uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [level node][3 * bins], [level node][4]
   double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
   int* s_clc = reinterpret_cast<int*>(sm + Lo.clc);           // [level node][bin] left count
   uint16_t* s_binrep = reinterpret_cast<uint16_t*>(sm + Lo.binrep);
+  double* s_vals = reinterpret_cast<double*>(sm + Lo.vals);
+  int* s_rorig = reinterpret_cast<int*>(s_vals + bins);
   __shared__ int s_neq;
   // phase timers (CTA 0, thread 0): where a round's cycles go (fs_device_counters [4..15])
   __shared__ long long s_ph[12];
@@ -1767,7 +1770,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     }                                       \
   } while (0)
   double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
-  double* s_pred = pred_g + fd.pos0;  // predictions stay in global memory (L2-resident)
+  // running predictions: shared memory when they fit, else global (L2-resident)
+  double* s_pred = pred_smem ? reinterpret_cast<double*>(sm + Lo.predv) : pred_g + fd.pos0;
   uint16_t* s_pre = reinterpret_cast<uint16_t*>(sm + Lo.pred);  // presorted lists, if staged
   const int32_t* g_pre = ord + fd.ord0;
   auto pre_at = [&](int j, int i) -> int {
@@ -1775,7 +1779,6 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   };
   long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
   uint8_t* s_node = sm + Lo.node;
-  uint8_t* s_rowk = sm + Lo.rowk;
   uint16_t* s_ord0 = reinterpret_cast<uint16_t*>(sm + Lo.ord0);
   uint16_t* s_scr = reinterpret_cast<uint16_t*>(sm + Lo.scratch);
   long long* s_hsum = reinterpret_cast<long long*>(sm + Lo.hsum);
@@ -1800,7 +1803,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     s_repb[j] = rep_boff[fd.rep0 + j];
     s_repn[j] = rep_nb[fd.rep0 + j];
     for (int b = 0; b < rep_nb[fd.rep0 + j]; ++b) s_binrep[rep_boff[fd.rep0 + j] + b] = static_cast<uint16_t>(j);
+    s_rorig[j] = rep_orig[fd.rep0 + j];
   }
+  for (int b = tid; b < bins; b += kResThreads) s_vals[b] = vals[fd.bin0 + b];
   const double b0 = base[f];
   for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
   if (pre_smem)
@@ -1874,82 +1879,77 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       const int ring = level & 1;
       long long* hs = s_hsum + static_cast<size_t>(ring) * ls * bins;
       int* hc = s_hcnt + static_cast<size_t>(ring) * ls * bins;
-      for (int i = tid; i < nl * bins; i += kResThreads) {
-        hs[i] = 0;
-        hc[i] = 0;
-      }
-      __syncthreads();
-      // ---- histograms of every directly built node of the level in ONE sweep over the rows:
-      // thread t owns feature j = t % nrep (nrep <= kResThreads here) and walks rows r = t / nrep,
-      // + G, ... (G = kResThreads / nrep), so a warp's lanes hit different features (bins apart, no
-      // same-address atomics) and the code loads fall in different banks (cs = 4 mod 128). Rows
-      // of built nodes carry their level-node index in s_rowk. Each row adds the three 21-bit
-      // limbs of u = v + 2^62 to its node's limb histogram with native 32-bit shared atomics
-      // (plus the limbs of |v| for the screen bound, by the feature-0 threads). Every kAtomSub
-      // rows the limb sums are folded exactly into the nodes' 64-bit histograms (see
-      // hist_build_atomic_kernel for the arithmetic).
+      // ---- histograms of every directly built node of the level. Thread t owns feature
+      // j = t % nrep (nrep <= kResThreads here) and walks the node's order-0 segment at rows
+      // r = t / nrep, + G, ... (G = kResThreads / nrep): a warp's lanes hit different features
+      // (bins apart, no same-address atomics) and their code loads fall in different banks
+      // (cs = 4 mod 128). Each row adds the three 21-bit limbs of u = v + 2^62 to the node's
+      // limb histogram with native 32-bit shared atomics; sum |v| (the screen bound) goes in
+      // four 16-bit limbs, one thread per row. Every kAtomSub rows the limb sums are folded
+      // exactly into the nodes' 64-bit histograms (see hist_build_atomic_kernel for the
+      // arithmetic); the first fold overwrites, so nothing is zeroed up front.
       {
-        const int lstride = 3 * bins + 3;
-        int nbuilt = 0;
-        for (int k = 0; k < nl; ++k) nbuilt += s_nodes[first + k].build == 1;
-        if (nbuilt) {
-          for (int p = tid; p < n; p += kResThreads) {
-            const int k = static_cast<int>(s_node[p]) - first;
-            s_rowk[p] = (k >= 0 && k < nl && s_nodes[first + k].build == 1) ? static_cast<uint8_t>(k) : 0xFF;
-          }
-          const int G = kResThreads / nrep;
-          const int hj = tid - (tid / nrep) * nrep, hr = tid / nrep;
-          const bool hact = hr < G;
-          const uint8_t* hcode = s_codes + static_cast<size_t>(hj) * cs;
-          const int hbin0 = s_repb[hj];
-          for (int sub0 = 0; sub0 < n; sub0 += kAtomSub) {
-            for (int i = tid; i < nl * lstride; i += kResThreads) s_limb[i] = 0;
-            __syncthreads();
-            const int sub_end = min(n, sub0 + kAtomSub);
+        const int lstride = 3 * bins;
+        uint32_t* s_absl = s_limb + static_cast<size_t>(nl) * lstride;  // [nl][4]
+        int maxnv = 0;
+        for (int k = 0; k < nl; ++k)
+          if (s_nodes[first + k].build == 1) maxnv = max(maxnv, s_nodes[first + k].n);
+        const int G = kResThreads / nrep;
+        const int hj = tid - (tid / nrep) * nrep, hr = tid / nrep;
+        const bool hact = hr < G;
+        const uint8_t* hcode = s_codes + static_cast<size_t>(hj) * cs;
+        const int hbin0 = s_repb[hj];
+        for (int sub0 = 0; sub0 < maxnv; sub0 += kAtomSub) {
+          for (int i = tid; i < nl * (lstride + 4); i += kResThreads) s_limb[i] = 0;
+          __syncthreads();
+          for (int k = 0; k < nl; ++k) {
+            const ResNode& nd = s_nodes[first + k];
+            if (nd.build != 1) continue;
+            const int q_end = min(nd.n, sub0 + kAtomSub);
+            const uint16_t* rows = s_ord0 + nd.seg;
+            uint32_t* lk = s_limb + k * lstride + hbin0;
             if (hact) {
 #pragma unroll 4
-              for (int p = sub0 + hr; p < sub_end; p += G) {
-                const int k = s_rowk[p];
-                if (k == 0xFF) continue;
-                const long long v = s_fix[p];
-                const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
-                uint32_t* lb = s_limb + k * lstride + hbin0 + hcode[p];
+              for (int q = sub0 + hr; q < q_end; q += G) {
+                const int p = rows[q];
+                const uint64_t u = static_cast<uint64_t>(s_fix[p]) + (1ull << 62);
+                uint32_t* lb = lk + hcode[p];
                 atomicAdd(lb, static_cast<uint32_t>(u) & kLimbMask);
                 atomicAdd(lb + bins, static_cast<uint32_t>(u >> 21) & kLimbMask);
                 atomicAdd(lb + 2 * bins, static_cast<uint32_t>(u >> 42));
-                if (hj == 0) {
-                  const uint64_t av = static_cast<uint64_t>(v < 0 ? -v : v);
-                  uint32_t* la = s_limb + k * lstride + 3 * bins;
-                  atomicAdd(la, static_cast<uint32_t>(av) & kLimbMask);
-                  atomicAdd(la + 1, static_cast<uint32_t>(av >> 21) & kLimbMask);
-                  atomicAdd(la + 2, static_cast<uint32_t>(av >> 42));
-                }
               }
             }
-            __syncthreads();
-            for (int i = tid; i < nl * bins; i += kResThreads) {
-              const int k = i / bins, b = i - k * bins;
-              if (s_nodes[first + k].build != 1) continue;
-              const uint32_t* lb = s_limb + k * lstride;
-              const unsigned __int128 U = static_cast<unsigned __int128>(lb[b]) +
-                                          (static_cast<unsigned __int128>(lb[bins + b]) << 21) +
-                                          (static_cast<unsigned __int128>(lb[2 * bins + b]) << 42);
-              const uint64_t cnt = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
-              hs[i] += static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
-              hc[i] += static_cast<int>(cnt);
+            for (int q = sub0 + tid; q < q_end; q += kResThreads) {
+              const long long v = s_fix[rows[q]];
+              const uint64_t av = static_cast<uint64_t>(v < 0 ? -v : v);
+#pragma unroll
+              for (int t = 0; t < 4; ++t) atomicAdd(s_absl + 4 * k + t, static_cast<uint32_t>(av >> (16 * t)) & 0xFFFFu);
             }
-            if (tid < nl && s_nodes[first + tid].build == 1) {
-              const uint32_t* lb = s_limb + tid * lstride + 3 * bins;
-              const unsigned long long add = static_cast<unsigned long long>(lb[0]) +
-                                             (static_cast<unsigned long long>(lb[1]) << 21) +
-                                             (static_cast<unsigned long long>(lb[2]) << 42);
-              ResNode& nd = s_nodes[first + tid];
-              nd.absfix = (sub0 == 0 ? 0ull : nd.absfix) + add;
-            }
-            if (tid == 0 && sub0 == 0)
-              for (int k = 0; k < nl; ++k) c_hist_rows += s_nodes[first + k].build == 1 ? s_nodes[first + k].n : 0;
-            __syncthreads();
           }
+          __syncthreads();
+          for (int i = tid; i < nl * bins; i += kResThreads) {
+            const int k = i / bins, b = i - k * bins;
+            if (s_nodes[first + k].build != 1) continue;
+            const uint32_t* lb = s_limb + k * lstride;
+            const unsigned __int128 U = static_cast<unsigned __int128>(lb[b]) +
+                                        (static_cast<unsigned __int128>(lb[bins + b]) << 21) +
+                                        (static_cast<unsigned __int128>(lb[2 * bins + b]) << 42);
+            const uint64_t cnt = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
+            const long long hv = static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
+            hs[i] = (sub0 == 0 ? 0ll : hs[i]) + hv;
+            hc[i] = (sub0 == 0 ? 0 : hc[i]) + static_cast<int>(cnt);
+          }
+          if (tid < nl && s_nodes[first + tid].build == 1) {
+            const uint32_t* la = s_absl + 4 * tid;
+            unsigned long long add = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) add += static_cast<unsigned long long>(la[t]) << (16 * t);
+            ResNode& nd = s_nodes[first + tid];
+            nd.absfix = (sub0 == 0 ? 0ull : nd.absfix) + add;
+          }
+          if (tid == 0 && sub0 == 0)
+            for (int k = 0; k < nl; ++k) c_hist_rows += s_nodes[first + k].build == 1 ? s_nodes[first + k].n : 0;
+          __syncthreads();
         }
       }
       RES_PHASE(2);
@@ -2243,8 +2243,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           const int s = s_items[it] >> 16, j = s_items[it] & 0xFFFF;
           ResNode& nd = s_nodes[s];
           const int nv = nd.n;
-          if (j == 0xFFFF) {
-            if (lane == 0) nd.total = fold_seq(s_resid, s_ord0 + nd.seg, nv);
+          if (j == 0xFFFF) {  // every lane runs the same chain (broadcast loads): no divergence
+            const double t = fold_seq(s_resid, s_ord0 + nd.seg, nv);
+            if (lane == 0) nd.total = t;
             continue;
           }
           const int need = s_win[(s - first) * nrep + j].maxlc;
@@ -2266,14 +2267,12 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
             }
             __syncwarp();
             const int cnt = min(__popc(m), need - seen);
-            if (lane == 0) {
 #pragma unroll 8
-              for (int t = 0; t < cnt; ++t) {
-                const int c = st_c[t];
-                if (c != prev && prev >= 0) out[prev] = left;
-                left = fs_add(left, st_v[t]);
-                prev = c;
-              }
+            for (int t = 0; t < cnt; ++t) {  // all lanes fold identically (broadcast loads)
+              const int c = st_c[t];
+              if (c != prev && prev >= 0 && lane == 0) out[prev] = left;
+              left = fs_add(left, st_v[t]);
+              prev = c;
             }
             seen += cnt;
             __syncwarp();
@@ -2375,8 +2374,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         ResNode& nd = s_nodes[s];
         if (nd.state == kNodeSplit) {
           const int j = nd.rep;
-          const int orig = rep_orig[fd.rep0 + j];
-          double thr = vals[fd.bin0 + s_repb[j] + nd.bin];
+          const int orig = s_rorig[j];
+          double thr = s_vals[s_repb[j] + nd.bin];
           if (thr == 0.0 && fd.negz) {  // +0.0 / -0.0 share a bin: the last left element's own value
             const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(j) * n;
             for (int i = cle[fd.bin0 + s_repb[j] + nd.bin] - 1; i >= 0; --i)
@@ -2589,7 +2588,7 @@ struct ResidentPlan {
   bool enabled = false;
   std::vector<int> families;
   size_t smem = 0;
-  int groups = 1;
+  bool pred_smem = false;
   bool pre_smem = false;
   // column-layout histogram plan for the multi-kernel path (hist_build_col_kernel)
   bool atomic = false;  // limb-atomic histogram (default)
@@ -2647,7 +2646,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       fit_resident_kernel<<<static_cast<unsigned>(resident.families.size()), kResThreads, resident.smem, s>>>(
           fam_d, st_d, list_d, Dp, reinterpret_cast<const uint8_t*>(codes_c), target_c, base_d, ord, ord_root,
           rep_orig_d, rep_nb_d, rep_boff_d, vals_d, cle, canon, x_d, d, trees_d, mse_d, max_trees, slots, dev->ctr_d,
-          resident.groups, pred, resident.pre_smem ? 1 : 0);
+          resident.pred_smem ? 1 : 0, pred, resident.pre_smem ? 1 : 0);
     }
     dev->count_launch();
     FS_CUDA(cudaGetLastError());
@@ -2970,26 +2969,28 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     if (mode != "auto" && mode != "resident" && mode != "multi")
       fail(FS_EINVAL, "FAMSEER_FIT_PATH must be auto, resident or multi");
     if (mode != "multi" && code_bytes == 1 && depth_max <= kResMaxDepth) {
-      // Prefer staging the presorted lists in shared memory (reference-order folds and tie-class
-      // scans then never touch HBM/L2); drop them to global memory if that is what it takes to fit.
-      for (const bool pre_smem : {true, false}) {
+      // Shared-memory staging options, most valuable first: the running predictions (read and
+      // updated every round) and the presorted lists (reference-order folds); whatever does not
+      // fit stays in global memory (L2-resident).
+      const bool opts[4][2] = {{true, true}, {true, false}, {false, true}, {false, false}};
+      for (const auto& op : opts) {
+        const bool pred_smem = op[0], pre_smem = op[1];
         bool ok = true;
         const size_t budget = 225 * 1024;
-        const int groups = 2;  // the histogram's limb scratch (3 x 32-bit per bin) lives in 2 "group" slots
         std::vector<int> fams_ok;
         size_t need = 0;
         for (int f = 0; f < F; ++f) {
           const FamDesc& fd = fam[static_cast<size_t>(f)];
           if (fd.n <= 0 || fd.trees <= 0) continue;
           if (fd.n > 65535 || fd.nrep > kResThreads) ok = false;
-          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, groups, pre_smem).total);
+          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, pred_smem, pre_smem).total);
           fams_ok.push_back(f);
         }
         res.families = fams_ok;
         if (ok && need <= budget && !fams_ok.empty()) {
           res.enabled = true;
           res.smem = need;
-          res.groups = groups;
+          res.pred_smem = pred_smem;
           res.pre_smem = pre_smem;
           break;
         }
