@@ -1631,9 +1631,34 @@ struct ResLayout {
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
 
+// Lane-column histogram shape (conflict-free shared atomics): lane l of every warp owns bank
+// column l. nrep <= 32: lanes l < (32 / nrep) * nrep take feature l % nrep (copy l / nrep of
+// it), so the column height is the largest bin count. nrep > 32: lane l takes features l, l+32,
+// ... stacked in its column (cofs = offset of a feature's bins in its lane's column).
+__host__ __device__ inline int col_height(int nrep, const int32_t* nb, int32_t* cofs) {
+  int H = 1;
+  if (nrep <= 32) {
+    for (int j = 0; j < nrep; ++j) {
+      if (cofs) cofs[j] = 0;
+      H = nb[j] > H ? nb[j] : H;
+    }
+    return H;
+  }
+  for (int l = 0; l < 32; ++l) {
+    int h = 0;
+    for (int j = l; j < nrep; j += 32) {
+      if (cofs) cofs[j] = h;
+      h += nb[j];
+    }
+    H = h > H ? h : H;
+  }
+  return H;
+}
+
 // groups: private histogram copies used while accumulating one node (threads own
 // (feature, group) pairs, so no shared-memory atomics are needed).
-__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, bool pred_smem, bool pre_smem) {
+__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, int colh, bool pred_smem,
+                                                bool pre_smem) {
   ResLayout L;
   L.ls = depth > 0 ? (1 << (depth - 1)) : 1;
   L.slots = (1 << (depth + 1)) - 1;
@@ -1672,8 +1697,10 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(L.ls) * (nr + 1) * sizeof(int));
   L.rep = o;
   o = res_align(o + 2 * nr * sizeof(int));
-  L.limb = o;  // per level node: 3 x 32-bit limb sums per bin, then 4 x 16-bit limbs of sum |v| per node
-  o = res_align(o + std::max<size_t>(static_cast<size_t>(L.ls) * (3 * static_cast<size_t>(bins) + 4) * 4, 8 * 512));
+  L.limb = o;  // lane-column limb histogram [3][colh][32] u32, 4 x 16-bit limbs of sum |v| per level node,
+               // column offset per rep
+  o = res_align(o + std::max<size_t>(static_cast<size_t>(3) * colh * 32 * 4 + static_cast<size_t>(L.ls) * 4 * 4 + nr * 4,
+                                      8 * 512));
   L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
   o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
   L.clc = o;  // left count per (node at level, bin)
@@ -1747,10 +1774,13 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const int f = fam_list[blockIdx.x];
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
-  const ResLayout Lo = res_layout(n, nrep, bins, depth, pred_smem != 0, pre_smem != 0);
+  const int colh = nrep > 0 ? col_height(nrep, rep_nb + fd.rep0, nullptr) : 1;
+  const ResLayout Lo = res_layout(n, nrep, bins, depth, colh, pred_smem != 0, pre_smem != 0);
   uint8_t* s_codes = sm + Lo.codes;  // [nrep][cs]
   const int cs = Lo.cs;
-  uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [level node][3 * bins], [level node][4]
+  uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [3][colh][32]
+  uint32_t* s_absl = s_limb + 3 * colh * 32;                      // [level node][4]
+  int* s_cofs = reinterpret_cast<int*>(s_absl + Lo.ls * 4);        // [nrep]
   double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
   int* s_clc = reinterpret_cast<int*>(sm + Lo.clc);           // [level node][bin] left count
   uint16_t* s_binrep = reinterpret_cast<uint16_t*>(sm + Lo.binrep);
@@ -1806,6 +1836,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     s_rorig[j] = rep_orig[fd.rep0 + j];
   }
   for (int b = tid; b < bins; b += kResThreads) s_vals[b] = vals[fd.bin0 + b];
+  if (tid == 0 && nrep > 0) col_height(nrep, rep_nb + fd.rep0, s_cofs);
   const double b0 = base[f];
   for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
   if (pre_smem)
@@ -1879,77 +1910,99 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       const int ring = level & 1;
       long long* hs = s_hsum + static_cast<size_t>(ring) * ls * bins;
       int* hc = s_hcnt + static_cast<size_t>(ring) * ls * bins;
-      // ---- histograms of every directly built node of the level. Thread t owns feature
-      // j = t % nrep (nrep <= kResThreads here) and walks the node's order-0 segment at rows
-      // r = t / nrep, + G, ... (G = kResThreads / nrep): a warp's lanes hit different features
-      // (bins apart, no same-address atomics) and their code loads fall in different banks
-      // (cs = 4 mod 128). Each row adds the three 21-bit limbs of u = v + 2^62 to the node's
-      // limb histogram with native 32-bit shared atomics; sum |v| (the screen bound) goes in
-      // four 16-bit limbs, one thread per row. Every kAtomSub rows the limb sums are folded
-      // exactly into the nodes' 64-bit histograms (see hist_build_atomic_kernel for the
-      // arithmetic); the first fold overwrites, so nothing is zeroed up front.
+      // ---- histograms of every directly built node of the level, one node at a time, in lane
+      // columns (col_height): every lane of a warp adds into its own bank column, so a 32-lane
+      // shared atomic is one wavefront. A row adds the three 21-bit limbs of u = v + 2^62 per
+      // feature with native 32-bit shared atomics; every kAtomSub rows the copies' limb sums are
+      // folded exactly into the node's 64-bit histogram (see hist_build_atomic_kernel for the
+      // arithmetic; the first fold overwrites). sum |v| (the screen bound) is a per-thread
+      // 64-bit sum (< 2^61 by the fixed-point shift), warp-reduced, added as 16-bit limbs.
       {
-        const int lstride = 3 * bins;
-        uint32_t* s_absl = s_limb + static_cast<size_t>(nl) * lstride;  // [nl][4]
-        int maxnv = 0;
-        for (int k = 0; k < nl; ++k)
-          if (s_nodes[first + k].build == 1) maxnv = max(maxnv, s_nodes[first + k].n);
-        const int G = kResThreads / nrep;
-        const int hj = tid - (tid / nrep) * nrep, hr = tid / nrep;
-        const bool hact = hr < G;
-        const uint8_t* hcode = s_codes + static_cast<size_t>(hj) * cs;
-        const int hbin0 = s_repb[hj];
-        for (int sub0 = 0; sub0 < maxnv; sub0 += kAtomSub) {
-          for (int i = tid; i < nl * (lstride + 4); i += kResThreads) s_limb[i] = 0;
-          __syncthreads();
-          for (int k = 0; k < nl; ++k) {
-            const ResNode& nd = s_nodes[first + k];
-            if (nd.build != 1) continue;
-            const int q_end = min(nd.n, sub0 + kAtomSub);
-            const uint16_t* rows = s_ord0 + nd.seg;
-            uint32_t* lk = s_limb + k * lstride + hbin0;
+        const int rpw = nrep <= 32 ? 32 / nrep : 1;  // rows per warp step
+        const int hj = nrep <= 32 ? lane % nrep : lane;
+        const int hm = nrep <= 32 ? lane / nrep : 0;
+        const bool hact = nrep <= 32 ? hm < rpw : true;
+        const int cpad = 3 * colh * 32;
+        for (int k = 0; k < nl; ++k) {
+          ResNode& nd = s_nodes[first + k];
+          if (nd.build != 1) continue;
+          const int nv = nd.n;
+          const uint16_t* rows = s_ord0 + nd.seg;
+          for (int sub0 = 0; sub0 < nv; sub0 += kAtomSub) {
+            for (int i = tid; i < cpad; i += kResThreads) s_limb[i] = 0;
+            if (tid < 4) s_absl[4 * k + tid] = 0;
+            __syncthreads();
+            const int q_end = min(nv, sub0 + kAtomSub);
+            unsigned long long asum = 0;
             if (hact) {
+              if (nrep <= 32) {
+                const uint8_t* hcode = s_codes + static_cast<size_t>(hj) * cs;
+                uint32_t* colp = s_limb + lane;
 #pragma unroll 4
-              for (int q = sub0 + hr; q < q_end; q += G) {
-                const int p = rows[q];
-                const uint64_t u = static_cast<uint64_t>(s_fix[p]) + (1ull << 62);
-                uint32_t* lb = lk + hcode[p];
-                atomicAdd(lb, static_cast<uint32_t>(u) & kLimbMask);
-                atomicAdd(lb + bins, static_cast<uint32_t>(u >> 21) & kLimbMask);
-                atomicAdd(lb + 2 * bins, static_cast<uint32_t>(u >> 42));
+                for (int q = sub0 + warp * rpw + hm; q < q_end; q += kResWarps * rpw) {
+                  const int p = rows[q];
+                  const long long v = s_fix[p];
+                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+                  uint32_t* c = colp + hcode[p] * 32;
+                  atomicAdd(c, static_cast<uint32_t>(u) & kLimbMask);
+                  atomicAdd(c + colh * 32, static_cast<uint32_t>(u >> 21) & kLimbMask);
+                  atomicAdd(c + 2 * colh * 32, static_cast<uint32_t>(u >> 42));
+                  if (hj == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
+                }
+              } else {
+                for (int q = sub0 + warp; q < q_end; q += kResWarps) {
+                  const int p = rows[q];
+                  const long long v = s_fix[p];
+                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+                  const uint32_t l0 = static_cast<uint32_t>(u) & kLimbMask;
+                  const uint32_t l1 = static_cast<uint32_t>(u >> 21) & kLimbMask;
+                  const uint32_t l2 = static_cast<uint32_t>(u >> 42);
+                  for (int j = lane; j < nrep; j += 32) {
+                    uint32_t* c = s_limb + lane + (s_cofs[j] + s_codes[static_cast<size_t>(j) * cs + p]) * 32;
+                    atomicAdd(c, l0);
+                    atomicAdd(c + colh * 32, l1);
+                    atomicAdd(c + 2 * colh * 32, l2);
+                  }
+                  if (lane == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
+                }
               }
             }
-            for (int q = sub0 + tid; q < q_end; q += kResThreads) {
-              const long long v = s_fix[rows[q]];
-              const uint64_t av = static_cast<uint64_t>(v < 0 ? -v : v);
+            for (int o = 16; o > 0; o >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, o);
+            if (lane == 0 && asum) {
 #pragma unroll
-              for (int t = 0; t < 4; ++t) atomicAdd(s_absl + 4 * k + t, static_cast<uint32_t>(av >> (16 * t)) & 0xFFFFu);
+              for (int t = 0; t < 4; ++t) atomicAdd(s_absl + 4 * k + t, static_cast<uint32_t>(asum >> (16 * t)) & 0xFFFFu);
             }
-          }
-          __syncthreads();
-          for (int i = tid; i < nl * bins; i += kResThreads) {
-            const int k = i / bins, b = i - k * bins;
-            if (s_nodes[first + k].build != 1) continue;
-            const uint32_t* lb = s_limb + k * lstride;
-            const unsigned __int128 U = static_cast<unsigned __int128>(lb[b]) +
-                                        (static_cast<unsigned __int128>(lb[bins + b]) << 21) +
-                                        (static_cast<unsigned __int128>(lb[2 * bins + b]) << 42);
-            const uint64_t cnt = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
-            const long long hv = static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
-            hs[i] = (sub0 == 0 ? 0ll : hs[i]) + hv;
-            hc[i] = (sub0 == 0 ? 0 : hc[i]) + static_cast<int>(cnt);
-          }
-          if (tid < nl && s_nodes[first + tid].build == 1) {
-            const uint32_t* la = s_absl + 4 * tid;
-            unsigned long long add = 0;
+            __syncthreads();
+            long long* hk = hs + static_cast<size_t>(k) * bins;
+            int* ck = hc + static_cast<size_t>(k) * bins;
+            for (int i = tid; i < bins; i += kResThreads) {
+              const int j = s_binrep[i], b = i - s_repb[j];
+              unsigned __int128 U = 0;
+              if (nrep <= 32) {
+                for (int m = 0; m < rpw; ++m) {
+                  const uint32_t* c = s_limb + b * 32 + j + m * nrep;
+                  U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+                       (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+                }
+              } else {
+                const uint32_t* c = s_limb + (s_cofs[j] + b) * 32 + (j & 31);
+                U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+                    (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+              }
+              const uint64_t cnt = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
+              const long long hv = static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
+              hk[i] = (sub0 == 0 ? 0ll : hk[i]) + hv;
+              ck[i] = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
+            }
+            if (tid == 0) {
+              unsigned long long add = 0;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) add += static_cast<unsigned long long>(la[t]) << (16 * t);
-            ResNode& nd = s_nodes[first + tid];
-            nd.absfix = (sub0 == 0 ? 0ull : nd.absfix) + add;
+              for (int t = 0; t < 4; ++t) add += static_cast<unsigned long long>(s_absl[4 * k + t]) << (16 * t);
+              nd.absfix = (sub0 == 0 ? 0ull : nd.absfix) + add;
+              if (sub0 == 0) c_hist_rows += nv;
+            }
+            __syncthreads();
           }
-          if (tid == 0 && sub0 == 0)
-            for (int k = 0; k < nl; ++k) c_hist_rows += s_nodes[first + k].build == 1 ? s_nodes[first + k].n : 0;
-          __syncthreads();
         }
       }
       RES_PHASE(2);
@@ -2983,7 +3036,8 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
           const FamDesc& fd = fam[static_cast<size_t>(f)];
           if (fd.n <= 0 || fd.trees <= 0) continue;
           if (fd.n > 65535 || fd.nrep > kResThreads) ok = false;
-          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, pred_smem, pre_smem).total);
+          const int colh = fd.nrep > 0 ? col_height(fd.nrep, rep_nb.data() + fd.rep0, nullptr) : 1;
+          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, colh, pred_smem, pre_smem).total);
           fams_ok.push_back(f);
         }
         res.families = fams_ok;
