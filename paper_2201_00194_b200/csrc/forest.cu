@@ -2,6 +2,7 @@
 // form. See forest.cuh for the layout.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <functional>
 #include <memory>
 
@@ -10,11 +11,9 @@
 namespace fs {
 
 void FamilyModel::release_device() {
-  for (void* p : {static_cast<void*>(nodes_d), static_cast<void*>(leafv_d), static_cast<void*>(leafid_d),
-                  static_cast<void*>(uthr_d), static_cast<void*>(uoff_d), static_cast<void*>(g_off_d),
-                  static_cast<void*>(g_feat_d), static_cast<void*>(g_thr_d), static_cast<void*>(g_left_d),
-                  static_cast<void*>(g_right_d), static_cast<void*>(g_val_d)})
-    if (p) cudaFree(p);
+  if (blob_d) cudaFree(blob_d);
+  blob_d = nullptr;
+  blob_cap = 0;
   nodes_d = nullptr;
   leafv_d = nullptr;
   leafid_d = nullptr;
@@ -27,18 +26,39 @@ void FamilyModel::release_device() {
 
 namespace {
 
-template <class T>
-T* upload(const std::vector<T>& v, cudaStream_t s) {
-  T* p = nullptr;
-  FS_CUDA(cudaMalloc(&p, std::max<size_t>(1, v.size()) * sizeof(T)));
-  if (!v.empty()) FS_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
-  return p;
-}
+// Packs host arrays into one staging buffer (16-byte aligned parts) and copies it into the
+// model's grow-only device blob with a single async copy. Pageable-source cudaMemcpyAsync
+// returns once the bytes are staged, so the host vectors may die right after.
+struct BlobPacker {
+  std::vector<unsigned char> host;
+  std::vector<size_t> offs;
+  template <class T>
+  void add(const std::vector<T>& v) {
+    const size_t o = (host.size() + 15) & ~size_t(15);
+    offs.push_back(o);
+    host.resize(o + std::max<size_t>(1, v.size()) * sizeof(T), 0);
+    if (!v.empty()) std::memcpy(host.data() + o, v.data(), v.size() * sizeof(T));
+  }
+  void commit(FamilyModel& m, cudaStream_t s) {
+    if (host.size() > m.blob_cap) {
+      if (m.blob_d) FS_CUDA(cudaFree(m.blob_d));
+      m.blob_d = nullptr;
+      const size_t cap = std::max<size_t>(host.size() + host.size() / 2, 4096);
+      FS_CUDA(cudaMalloc(&m.blob_d, cap));
+      m.blob_cap = cap;
+    }
+    FS_CUDA(cudaMemcpyAsync(m.blob_d, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+  }
+  template <class T>
+  T* at(const FamilyModel& m, int i) const {
+    return reinterpret_cast<T*>(m.blob_d + offs[static_cast<size_t>(i)]);
+  }
+};
 
 }  // namespace
 
 void compile_model(fs_device* dev, FamilyModel& m) {
-  m.release_device();
+  m.compiled = false;
   const int T = m.num_trees();
   m.n_trees = T;
   // Validate structure and find depth / feature range.
@@ -62,13 +82,21 @@ void compile_model(fs_device* dev, FamilyModel& m) {
   m.generic = depth > kMaxHeapDepth;
 
   if (m.generic) {
-    m.g_off_d = upload(m.offsets, dev->stream);
-    m.g_feat_d = upload(m.feature, dev->stream);
-    m.g_thr_d = upload(m.threshold, dev->stream);
-    m.g_left_d = upload(m.left, dev->stream);
-    m.g_right_d = upload(m.right, dev->stream);
-    m.g_val_d = upload(m.value, dev->stream);
-    FS_CUDA(cudaStreamSynchronize(dev->stream));
+    BlobPacker pk;
+    pk.add(m.offsets);
+    pk.add(m.feature);
+    pk.add(m.threshold);
+    pk.add(m.left);
+    pk.add(m.right);
+    pk.add(m.value);
+    pk.commit(m, dev->stream);
+    m.g_off_d = pk.at<int32_t>(m, 0);
+    m.g_feat_d = pk.at<int32_t>(m, 1);
+    m.g_thr_d = pk.at<double>(m, 2);
+    m.g_left_d = pk.at<int32_t>(m, 3);
+    m.g_right_d = pk.at<int32_t>(m, 4);
+    m.g_val_d = pk.at<double>(m, 5);
+    m.nodes_d = nullptr;
     m.compiled = true;
     return;
   }
@@ -126,13 +154,21 @@ void compile_model(fs_device* dev, FamilyModel& m) {
     };
     place(0, 0, 0);
   }
-  m.nodes_d = upload(nodes, dev->stream);
-  m.leafv_d = upload(leafv, dev->stream);
-  m.leafid_d = upload(leafid, dev->stream);
-  m.uthr_d = upload(uthr, dev->stream);
+  BlobPacker pk;
+  pk.add(nodes);
+  pk.add(leafv);
+  pk.add(leafid);
+  pk.add(uthr);
+  pk.add(uoff);
+  pk.commit(m, dev->stream);
+  m.nodes_d = pk.at<uint32_t>(m, 0);
+  m.leafv_d = pk.at<double>(m, 1);
+  m.leafid_d = pk.at<uint8_t>(m, 2);
+  m.uthr_d = pk.at<double>(m, 3);
   m.n_uthr = static_cast<int>(uthr.size());
-  m.uoff_d = upload(uoff, dev->stream);
-  FS_CUDA(cudaStreamSynchronize(dev->stream));
+  m.uoff_d = pk.at<int32_t>(m, 4);
+  m.g_off_d = m.g_feat_d = m.g_left_d = m.g_right_d = nullptr;
+  m.g_thr_d = m.g_val_d = nullptr;
   m.compiled = true;
 }
 

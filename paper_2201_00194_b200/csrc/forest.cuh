@@ -48,6 +48,11 @@ struct FamilyModel {
   int32_t* g_right_d = nullptr;
   double* g_val_d = nullptr;
 
+  // all compiled arrays live in one grow-only device blob (refits reuse it: no cudaMalloc /
+  // cudaFree per fit, one copy per compile)
+  unsigned char* blob_d = nullptr;
+  size_t blob_cap = 0;
+
   int num_trees() const { return static_cast<int>(offsets.size()) - 1; }
   void release_device();
 };
