@@ -1,4 +1,5 @@
 // fs_device: one context per GPU (stream, scratch arena, deferred-error word, launch counter).
+#include <algorithm>
 #include <cstdio>
 #include <string>
 
@@ -84,6 +85,18 @@ void fs_device::prof_resolve() {
   prof_pending.clear();
 }
 
+void* fs_device::pinned(size_t bytes) {
+  if (bytes > pinned_cap) {
+    FS_CUDA(cudaStreamSynchronize(stream));
+    if (pinned_h) FS_CUDA(cudaFreeHost(pinned_h));
+    pinned_h = nullptr;
+    const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
+    FS_CUDA(cudaHostAlloc(&pinned_h, cap, cudaHostAllocDefault));
+    pinned_cap = cap;
+  }
+  return pinned_h;
+}
+
 uint32_t fs_device::take_errors() {
   FS_CUDA(cudaMemcpyAsync(err_h, err_d, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
   FS_CUDA(cudaStreamSynchronize(stream));
@@ -142,6 +155,7 @@ int fs_device_destroy(fs_device* d) {
     if (d->err_d) cudaFree(d->err_d);
     if (d->ctr_d) cudaFree(d->ctr_d);
     if (d->err_h) cudaFreeHost(d->err_h);
+    if (d->pinned_h) cudaFreeHost(d->pinned_h);
     if (d->own) cudaStreamDestroy(d->own);
     delete d;
   });

@@ -2728,6 +2728,44 @@ std::vector<T> download(const T* d, size_t n, cudaStream_t s) {
   return h;
 }
 
+// Several device->host reads with ONE stream synchronization: async copies into the device's
+// pinned staging buffer (plus the deferred-error word), one sync, then unpack. Returns the
+// error bits (see fs_device::take_errors).
+struct BatchRead {
+  struct Item {
+    const void* src;
+    void* dst;
+    size_t bytes;
+  };
+  std::vector<Item> items;
+  template <class T>
+  void add(const T* d, std::vector<T>& h, size_t n) {
+    h.resize(n);
+    if (n) items.push_back({d, h.data(), n * sizeof(T)});
+  }
+  uint32_t run(fs_device* dev) {
+    size_t total = 16;
+    for (const auto& it : items) total += (it.bytes + 15) & ~size_t(15);
+    auto* st = static_cast<unsigned char*>(dev->pinned(total));
+    size_t o = 16;
+    FS_CUDA(cudaMemcpyAsync(st, dev->err_d, sizeof(uint32_t), cudaMemcpyDeviceToHost, dev->stream));
+    for (const auto& it : items) {
+      FS_CUDA(cudaMemcpyAsync(st + o, it.src, it.bytes, cudaMemcpyDeviceToHost, dev->stream));
+      o += (it.bytes + 15) & ~size_t(15);
+    }
+    FS_CUDA(cudaStreamSynchronize(dev->stream));
+    o = 16;
+    for (const auto& it : items) {
+      std::memcpy(it.dst, st + o, it.bytes);
+      o += (it.bytes + 15) & ~size_t(15);
+    }
+    uint32_t bits;
+    std::memcpy(&bits, st, sizeof bits);
+    if (bits) FS_CUDA(cudaMemsetAsync(dev->err_d, 0, sizeof(uint32_t), dev->stream));
+    return bits;
+  }
+};
+
 inline unsigned grid1(int64_t n, int block, int cap) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, block), cap)));
 }
@@ -3019,9 +3057,16 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     }
     dev->count_launch();
   }
-  raise_deferred(dev->take_errors());
-  std::vector<int32_t> nb = download(nb_all, static_cast<size_t>(F) * d, s);
-  const std::vector<int> negz = download(negz_d, static_cast<size_t>(F), s);
+  std::vector<int32_t> nb;
+  std::vector<int> negz;
+  std::vector<uint64_t> hh;
+  {
+    BatchRead br;
+    br.add(nb_all, nb, static_cast<size_t>(F) * d);
+    br.add(negz_d, negz, static_cast<size_t>(F));
+    br.add(hash_all, hh, static_cast<size_t>(F) * d);
+    raise_deferred(br.run(dev));
+  }
   for (int f = 0; f < F; ++f) fam[static_cast<size_t>(f)].negz = negz[static_cast<size_t>(f)];
   std::vector<LargeItem> large;
   int64_t vl = 0;
@@ -3040,13 +3085,14 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     distinct_large_kernel<<<static_cast<unsigned>(large.size()), kSortThreads, 0, s>>>(
         x_d, d, fam_d, items_d, bufA, bufB, n_max, codes_all, vals_large, nb_all, hash_all, dev->err_d);
     dev->count_launch();
-    raise_deferred(dev->take_errors());
-    nb = download(nb_all, static_cast<size_t>(F) * d, s);
+    BatchRead br;
+    br.add(nb_all, nb, static_cast<size_t>(F) * d);
+    br.add(hash_all, hh, static_cast<size_t>(F) * d);
+    raise_deferred(br.run(dev));
     for (const auto& it : large) large_src[static_cast<size_t>(it.fam) * d + it.feat] = it.vals0;
   }
   for (int v : nb)
     if (v > kMaxBins) fail(FS_EINVAL, "fit: more than 65535 distinct values in one feature");
-  std::vector<uint64_t> hh = download(hash_all, static_cast<size_t>(F) * d, s);
 
   // ---- stage 2: representatives (drop constant and duplicate-column features) -------------
   std::vector<PairItem> pairs;
@@ -3246,11 +3292,17 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   }
 
   // ---- results: heap-slot records -> pre-order CostModelState layout ------------------------
-  raise_deferred(dev->take_errors());
-  const auto st_h = download(st_d, static_cast<size_t>(F), s);
-  const auto trees_h = download(trees_d, static_cast<size_t>(std::max<int64_t>(total_tree, 1)), s);
-  const auto mse_h = download(mse_d, static_cast<size_t>(F) * std::max(max_trees, 1), s);
-  const auto base_h = download(base_d, static_cast<size_t>(F), s);
+  std::vector<FamState> st_h;
+  std::vector<TreeRec> trees_h;
+  std::vector<double> mse_h, base_h;
+  {
+    BatchRead br;
+    br.add(st_d, st_h, static_cast<size_t>(F));
+    br.add(trees_d, trees_h, static_cast<size_t>(std::max<int64_t>(total_tree, 1)));
+    br.add(mse_d, mse_h, static_cast<size_t>(F) * std::max(max_trees, 1));
+    br.add(base_d, base_h, static_cast<size_t>(F));
+    raise_deferred(br.run(dev));
+  }
   for (int f = 0; f < F; ++f) {
     FamilyModel& m = fo->fams[static_cast<size_t>(f)];
     const FamDesc& fd = fam[static_cast<size_t>(f)];

@@ -101,6 +101,9 @@ struct fs_device {
   std::vector<cudaEvent_t> prof_pool;
   std::vector<std::pair<std::string, std::pair<int64_t, double>>> prof_acc;  // name -> (count, ms)
 
+  void* pinned_h = nullptr;     // pinned host staging for batched device->host reads (grow-only)
+  size_t pinned_cap = 0;
+  void* pinned(size_t bytes);      // grow-only; synchronizes the stream when it has to grow
   void* scratch(int slot, size_t bytes);  // stream-ordered grow; contents undefined
   void count_launch(int n = 1) { launches += n; }
   void activate() const;                  // cudaSetDevice(ordinal)
