@@ -97,6 +97,23 @@ void* fs_device::pinned(size_t bytes) {
   return pinned_h;
 }
 
+void* fs_device::pinned_upload(size_t bytes) {
+  if (up_evt) FS_CUDA(cudaEventSynchronize(up_evt));
+  if (bytes > up_cap) {
+    if (up_h) FS_CUDA(cudaFreeHost(up_h));
+    up_h = nullptr;
+    const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
+    FS_CUDA(cudaHostAlloc(&up_h, cap, cudaHostAllocDefault));
+    up_cap = cap;
+  }
+  return up_h;
+}
+
+void fs_device::upload_done() {
+  if (!up_evt) FS_CUDA(cudaEventCreateWithFlags(&up_evt, cudaEventDisableTiming));
+  FS_CUDA(cudaEventRecord(up_evt, stream));
+}
+
 uint32_t fs_device::take_errors() {
   FS_CUDA(cudaMemcpyAsync(err_h, err_d, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
   FS_CUDA(cudaStreamSynchronize(stream));
@@ -156,6 +173,11 @@ int fs_device_destroy(fs_device* d) {
     if (d->ctr_d) cudaFree(d->ctr_d);
     if (d->err_h) cudaFreeHost(d->err_h);
     if (d->pinned_h) cudaFreeHost(d->pinned_h);
+    if (d->up_evt) {
+      cudaEventSynchronize(d->up_evt);
+      cudaEventDestroy(d->up_evt);
+    }
+    if (d->up_h) cudaFreeHost(d->up_h);
     if (d->own) cudaStreamDestroy(d->own);
     delete d;
   });

@@ -8,6 +8,8 @@
 //           prediction update -> commit / early stop (:212) -> MSE (:215-220)
 // The host only launches; no host<->device synchronisation happens inside the boosting loop.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -3019,6 +3021,14 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     }
   }
   const int64_t n_tot = seg[F];
+  // FAMSEER_HOST_TIMING=1: host wall-clock per stage of this call on stderr (diagnostics)
+  const bool ht = std::getenv("FAMSEER_HOST_TIMING") != nullptr;
+  const auto ht0 = std::chrono::steady_clock::now();
+  auto htick = [&](const char* what) {
+    if (ht)
+      std::fprintf(stderr, "[fit host] %-22s %8.1f us\n", what,
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ht0).count());
+  };
   Arena ar(s);
   // ---- family descriptors (stage 1 needs row0/n only) -----------------------------------
   std::vector<FamDesc> fam(static_cast<size_t>(F));
@@ -3091,6 +3101,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     raise_deferred(br.run(dev));
     for (const auto& it : large) large_src[static_cast<size_t>(it.fam) * d + it.feat] = it.vals0;
   }
+  htick("distinct read");
   for (int v : nb)
     if (v > kMaxBins) fail(FS_EINVAL, "fit: more than 65535 distinct values in one feature");
 
@@ -3114,6 +3125,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     dev->count_launch();
     mismatch = download(mm, pairs.size(), s);
   }
+  htick("pairs verified");
   std::vector<std::vector<char>> dup(static_cast<size_t>(F), std::vector<char>(static_cast<size_t>(d), 0));
   for (size_t i = 0; i < pairs.size(); ++i)
     if (!mismatch[i]) dup[static_cast<size_t>(pairs[i].fam)][static_cast<size_t>(pairs[i].b)] = 1;
@@ -3277,6 +3289,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   double* base_d = ar.alloc<double>(F);
   FS_CUDA(cudaMemsetAsync(base_d, 0, F * sizeof(double), s));
 
+  htick("plan uploaded");
   {
   ProfScope prof_rounds(dev, "fit_rounds");
   if (code_bytes == 1)
@@ -3292,6 +3305,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   }
 
   // ---- results: heap-slot records -> pre-order CostModelState layout ------------------------
+  htick("rounds launched");
   std::vector<FamState> st_h;
   std::vector<TreeRec> trees_h;
   std::vector<double> mse_h, base_h;
@@ -3303,6 +3317,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     br.add(base_d, base_h, static_cast<size_t>(F));
     raise_deferred(br.run(dev));
   }
+  htick("results read");
   for (int f = 0; f < F; ++f) {
     FamilyModel& m = fo->fams[static_cast<size_t>(f)];
     const FamDesc& fd = fam[static_cast<size_t>(f)];
@@ -3317,36 +3332,45 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     m.gain.clear();
     m.mse.clear();
     const int T = st_h[static_cast<size_t>(f)].ntrees;
+    m.offsets.reserve(static_cast<size_t>(T) + 1);
+    for (auto* v : {&m.feature, &m.left, &m.right}) v->reserve(static_cast<size_t>(T) * slots);
+    for (auto* v : {&m.threshold, &m.value, &m.gain}) v->reserve(static_cast<size_t>(T) * slots);
+    struct Emit {
+      int slot, parent, side;  // parent: global index of the parent node (-1 root), side 0 left / 1 right
+    };
+    std::vector<Emit> es;
     for (int t = 0; t < T; ++t) {
       const TreeRec* rec = trees_h.data() + fd.tree0 + static_cast<int64_t>(t) * slots;
       const int base_idx = static_cast<int>(m.feature.size());
-      std::function<int(int)> emit = [&](int sl) -> int {
-        const int idx = static_cast<int>(m.feature.size()) - base_idx;
-        const TreeRec& r = rec[sl];
+      es.assign(1, {0, -1, 0});
+      while (!es.empty()) {  // pre-order: left subtree before right (costmodel.cpp:108-111)
+        const Emit e = es.back();
+        es.pop_back();
+        const int gidx = static_cast<int>(m.feature.size());
+        const TreeRec& r = rec[e.slot];
+        if (r.kind != kNodeSplit && r.kind != kNodeLeaf) fail(FS_ECUDA, "fit: internal error (missing tree node)");
         m.feature.push_back(r.kind == kNodeSplit ? r.feature : -1);
         m.threshold.push_back(r.kind == kNodeSplit ? r.threshold : 0.0);
         m.left.push_back(-1);
         m.right.push_back(-1);
         m.value.push_back(r.kind == kNodeSplit ? 0.0 : r.value);
         m.gain.push_back(r.kind == kNodeSplit ? r.gain : 0.0);
+        if (e.parent >= 0) (e.side ? m.right : m.left)[static_cast<size_t>(e.parent)] = gidx - base_idx;
         if (r.kind == kNodeSplit) {
-          const int l = emit(2 * sl + 1);
-          const int rr = emit(2 * sl + 2);
-          m.left[static_cast<size_t>(base_idx + idx)] = l;
-          m.right[static_cast<size_t>(base_idx + idx)] = rr;
-        } else if (r.kind != kNodeLeaf) {
-          fail(FS_ECUDA, "fit: internal error (missing tree node)");
+          es.push_back({2 * e.slot + 2, gidx, 1});
+          es.push_back({2 * e.slot + 1, gidx, 0});
         }
-        return idx;
-      };
-      emit(0);
+      }
       m.offsets.push_back(static_cast<int32_t>(m.feature.size()));
       m.mse.push_back(mse_h[static_cast<size_t>(f) * max_trees + t]);
     }
     m.screened = static_cast<int64_t>(st_h[static_cast<size_t>(f)].screened);
     m.exact = static_cast<int64_t>(st_h[static_cast<size_t>(f)].exact);
+    htick("  family converted");
     compile_model(dev, m);
+    htick("  family compiled");
   }
+  htick("models compiled");
 }
 
 }  // namespace fit

@@ -39,7 +39,7 @@ struct BlobPacker {
     host.resize(o + std::max<size_t>(1, v.size()) * sizeof(T), 0);
     if (!v.empty()) std::memcpy(host.data() + o, v.data(), v.size() * sizeof(T));
   }
-  void commit(FamilyModel& m, cudaStream_t s) {
+  void commit(FamilyModel& m, fs_device* dev) {
     if (host.size() > m.blob_cap) {
       if (m.blob_d) FS_CUDA(cudaFree(m.blob_d));
       m.blob_d = nullptr;
@@ -47,7 +47,11 @@ struct BlobPacker {
       FS_CUDA(cudaMalloc(&m.blob_d, cap));
       m.blob_cap = cap;
     }
-    FS_CUDA(cudaMemcpyAsync(m.blob_d, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+    // through pinned staging: a truly asynchronous copy (no pageable-staging stream sync)
+    void* st = dev->pinned_upload(host.size());
+    std::memcpy(st, host.data(), host.size());
+    FS_CUDA(cudaMemcpyAsync(m.blob_d, st, host.size(), cudaMemcpyHostToDevice, dev->stream));
+    dev->upload_done();
   }
   template <class T>
   T* at(const FamilyModel& m, int i) const {
@@ -63,18 +67,25 @@ void compile_model(fs_device* dev, FamilyModel& m) {
   m.n_trees = T;
   // Validate structure and find depth / feature range.
   int depth = 0, dmodel = 0;
-  std::function<int(int, int, int)> walk = [&](int o, int idx, int lvl) -> int {
-    const int n = m.offsets[static_cast<size_t>(o) + 1] - m.offsets[static_cast<size_t>(o)];
-    if (idx < 0 || idx >= n || lvl > 64) fail(FS_EINVAL, "forest: malformed tree (child index out of range)");
-    const size_t g = static_cast<size_t>(m.offsets[static_cast<size_t>(o)] + idx);
-    if (m.feature[g] < 0) return lvl;
-    dmodel = std::max(dmodel, m.feature[g] + 1);
-    return std::max(walk(o, m.left[g], lvl + 1), walk(o, m.right[g], lvl + 1));
-  };
+  std::vector<std::pair<int, int>> stk;  // (node index in tree, level)
   for (int t = 0; t < T; ++t) {
-    if (m.offsets[static_cast<size_t>(t) + 1] <= m.offsets[static_cast<size_t>(t)])
-      fail(FS_EINVAL, "forest: empty tree");
-    depth = std::max(depth, walk(t, 0, 0));
+    const int o = m.offsets[static_cast<size_t>(t)];
+    const int n = m.offsets[static_cast<size_t>(t) + 1] - o;
+    if (n <= 0) fail(FS_EINVAL, "forest: empty tree");
+    stk.assign(1, {0, 0});
+    while (!stk.empty()) {
+      const auto [idx, lvl] = stk.back();
+      stk.pop_back();
+      if (idx < 0 || idx >= n || lvl > 64) fail(FS_EINVAL, "forest: malformed tree (child index out of range)");
+      const size_t g = static_cast<size_t>(o + idx);
+      if (m.feature[g] < 0) {
+        depth = std::max(depth, lvl);
+        continue;
+      }
+      dmodel = std::max(dmodel, m.feature[g] + 1);
+      stk.push_back({m.left[g], lvl + 1});
+      stk.push_back({m.right[g], lvl + 1});
+    }
   }
   if (dmodel > 65535) fail(FS_EINVAL, "forest: feature index exceeds 65535");
   m.depth = depth;
@@ -89,7 +100,7 @@ void compile_model(fs_device* dev, FamilyModel& m) {
     pk.add(m.left);
     pk.add(m.right);
     pk.add(m.value);
-    pk.commit(m, dev->stream);
+    pk.commit(m, dev);
     m.g_off_d = pk.at<int32_t>(m, 0);
     m.g_feat_d = pk.at<int32_t>(m, 1);
     m.g_thr_d = pk.at<double>(m, 2);
@@ -126,20 +137,27 @@ void compile_model(fs_device* dev, FamilyModel& m) {
   std::vector<uint32_t> nodes(static_cast<size_t>(T) * nint, 0);
   std::vector<double> leafv(static_cast<size_t>(T) * nleaf, 0.0);
   std::vector<uint8_t> leafid(static_cast<size_t>(T) * nleaf, 0);
+  struct Place {
+    int idx, heap, lvl;
+  };
+  std::vector<Place> ps;
   for (int t = 0; t < T; ++t) {
     const int o = m.offsets[static_cast<size_t>(t)];
-    std::function<void(int, int, int)> place = [&](int idx, int heap, int lvl) {
-      const size_t g = static_cast<size_t>(o + idx);
-      if (lvl == depth) {
-        leafv[static_cast<size_t>(t) * nleaf + (heap - nint)] = m.value[g];
-        leafid[static_cast<size_t>(t) * nleaf + (heap - nint)] = static_cast<uint8_t>(idx);
-        return;
+    ps.assign(1, {0, 0, 0});
+    while (!ps.empty()) {
+      const Place c = ps.back();
+      ps.pop_back();
+      const size_t g = static_cast<size_t>(o + c.idx);
+      if (c.lvl == depth) {
+        leafv[static_cast<size_t>(t) * nleaf + (c.heap - nint)] = m.value[g];
+        leafid[static_cast<size_t>(t) * nleaf + (c.heap - nint)] = static_cast<uint8_t>(c.idx);
+        continue;
       }
       uint32_t node;
       int li, ri;
       if (m.feature[g] < 0) {  // early leaf: replicate down an always-left path
         node = always_left_rank << 16;
-        li = ri = idx;
+        li = ri = c.idx;
       } else {
         const int f = m.feature[g];
         const auto& u = uq[static_cast<size_t>(f)];
@@ -148,11 +166,10 @@ void compile_model(fs_device* dev, FamilyModel& m) {
         li = m.left[g];
         ri = m.right[g];
       }
-      nodes[static_cast<size_t>(t) * nint + heap] = node;
-      place(li, 2 * heap + 1, lvl + 1);
-      place(ri, 2 * heap + 2, lvl + 1);
-    };
-    place(0, 0, 0);
+      nodes[static_cast<size_t>(t) * nint + c.heap] = node;
+      ps.push_back({li, 2 * c.heap + 1, c.lvl + 1});
+      ps.push_back({ri, 2 * c.heap + 2, c.lvl + 1});
+    }
   }
   BlobPacker pk;
   pk.add(nodes);
@@ -160,7 +177,7 @@ void compile_model(fs_device* dev, FamilyModel& m) {
   pk.add(leafid);
   pk.add(uthr);
   pk.add(uoff);
-  pk.commit(m, dev->stream);
+  pk.commit(m, dev);
   m.nodes_d = pk.at<uint32_t>(m, 0);
   m.leafv_d = pk.at<double>(m, 1);
   m.leafid_d = pk.at<uint8_t>(m, 2);

@@ -104,6 +104,11 @@ struct fs_device {
   void* pinned_h = nullptr;     // pinned host staging for batched device->host reads (grow-only)
   size_t pinned_cap = 0;
   void* pinned(size_t bytes);      // grow-only; synchronizes the stream when it has to grow
+  void* up_h = nullptr;            // pinned host staging for async host->device model uploads
+  size_t up_cap = 0;
+  cudaEvent_t up_evt = nullptr;    // recorded after the last upload from up_h
+  void* pinned_upload(size_t bytes);  // waits until the previous upload from it has been read
+  void upload_done();                 // record up_evt on the stream after issuing the copies
   void* scratch(int slot, size_t bytes);  // stream-ordered grow; contents undefined
   void count_launch(int n = 1) { launches += n; }
   void activate() const;                  // cudaSetDevice(ordinal)
