@@ -943,6 +943,30 @@ __global__ void __launch_bounds__(kColWarps * 32) hist_build_col_kernel(
   }
 }
 
+// Lane-column histogram shape (conflict-free shared atomics): lane l of every warp owns bank
+// column l. nrep <= 32: lanes l < (32 / nrep) * nrep take feature l % nrep (copy l / nrep of
+// it), so the column height is the largest bin count. nrep > 32: lane l takes features l, l+32,
+// ... stacked in its column (cofs = offset of a feature's bins in its lane's column).
+__host__ __device__ inline int col_height(int nrep, const int32_t* nb, int32_t* cofs) {
+  int H = 1;
+  if (nrep <= 32) {
+    for (int j = 0; j < nrep; ++j) {
+      if (cofs) cofs[j] = 0;
+      H = nb[j] > H ? nb[j] : H;
+    }
+    return H;
+  }
+  for (int l = 0; l < 32; ++l) {
+    int h = 0;
+    for (int j = l; j < nrep; j += 32) {
+      if (cofs) cofs[j] = h;
+      h += nb[j];
+    }
+    H = h > H ? h : H;
+  }
+  return H;
+}
+
 // Limb-atomic histogram build (the default shape). Only 32-bit shared-memory atomics are native
 // on sm_100a (64-bit ones compile to CAS spin loops), so each 62-bit fixed-point residual v is
 // offset to u = v + 2^62 (in [0, 2^63)) and split into three 21-bit limbs accumulated with
@@ -961,7 +985,7 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
     int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
     const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
-    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr) {
+    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr, int colh_max) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
@@ -987,26 +1011,46 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
   const int local = s - ((1 << level) - 1);
   const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
   const int nrep = fd.nrep, bins = fd.bins;
-  // layout: limbs[3][bins] u32 | acc_sum[bins] i64 | acc_cnt[bins] i32 | boff[nrep] | tile codes | tile limbs
+  // layout: limbs[3][colh_max][32] u32 (lane columns, see col_height) | acc_sum[bins] i64 |
+  // acc_cnt[bins] i32 | binrep[bins] u16 | boff[nrep] | cofs[nrep] | tile codes | tile limbs
   uint32_t* limb = reinterpret_cast<uint32_t*>(smem);
-  int64_t* acc_sum = reinterpret_cast<int64_t*>(smem + ((static_cast<size_t>(3) * bins * 4 + 15) & ~size_t(15)));
+  int64_t* acc_sum =
+      reinterpret_cast<int64_t*>(smem + ((static_cast<size_t>(3) * colh_max * 32 * 4 + 15) & ~size_t(15)));
   int32_t* acc_cnt = reinterpret_cast<int32_t*>(acc_sum + bins);
-  int32_t* s_boff = acc_cnt + bins;
-  unsigned char* tail = reinterpret_cast<unsigned char*>(s_boff + nrep);
+  uint16_t* s_binrep = reinterpret_cast<uint16_t*>(acc_cnt + bins);
+  int32_t* s_boff = reinterpret_cast<int32_t*>(s_binrep + ((bins + 1) & ~1));
+  int32_t* s_cofs = s_boff + nrep;
+  int32_t* s_nbv = s_cofs + nrep;
+  unsigned char* tail = reinterpret_cast<unsigned char*>(s_nbv + nrep);
   tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
   CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                              // [kAtomTile][Dp]
   uint32_t* t_limb = reinterpret_cast<uint32_t*>(t_codes + kAtomTile * Dp);     // [kAtomTile][3]
   __shared__ unsigned long long s_abs;
+  __shared__ int s_colh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int b = tid; b < bins; b += kAtomThreads) {
     acc_sum[b] = 0;
     acc_cnt[b] = 0;
   }
-  for (int j = tid; j < nrep; j += kAtomThreads) s_boff[j] = rep_boff[fd.rep0 + j];
+  for (int j = tid; j < nrep; j += kAtomThreads) {
+    const int b0 = rep_boff[fd.rep0 + j];
+    const int b1 = j + 1 < nrep ? rep_boff[fd.rep0 + j + 1] : bins;
+    s_boff[j] = b0;
+    s_nbv[j] = b1 - b0;
+    for (int b = b0; b < b1; ++b) s_binrep[b] = static_cast<uint16_t>(j);
+  }
   if (tid == 0) s_abs = 0;
+  __syncthreads();
+  if (tid == 0) s_colh = col_height(nrep, s_nbv, s_cofs);
+  __syncthreads();
+  const int colh = s_colh;
+  const int rpw = nrep <= 32 ? 32 / nrep : 1;  // rows per warp step (lane copies, nrep <= 32)
+  const int hj = nrep <= 32 ? lane % nrep : lane;
+  const int hm = nrep <= 32 ? lane / nrep : 0;
+  const bool hact = nrep <= 32 ? hm < rpw : true;
   const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
   for (int sub0 = 0; sub0 < rows; sub0 += kAtomSub) {
-    for (int i = tid; i < 3 * bins; i += kAtomThreads) limb[i] = 0;
+    for (int i = tid; i < 3 * colh * 32; i += kAtomThreads) limb[i] = 0;
     __syncthreads();
     const int sub_end = min(rows, sub0 + kAtomSub);
     for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
@@ -1031,22 +1075,46 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
         if (lane == 0 && a) atomicAdd(&s_abs, a);
       }
       __syncthreads();
-      for (int r = warp; r < tr; r += kAtomThreads / 32) {
-        const uint32_t l0 = t_limb[3 * r], l1 = t_limb[3 * r + 1], l2 = t_limb[3 * r + 2];
-        const CodeT* cr = t_codes + r * Dp;
-        for (int j = lane; j < nrep; j += 32) {
-          const int bin = s_boff[j] + static_cast<int>(cr[j]);
-          atomicAdd(limb + bin, l0);
-          atomicAdd(limb + bins + bin, l1);
-          atomicAdd(limb + 2 * bins + bin, l2);
+      // lane columns: every lane adds into its own bank column -> one wavefront per atomic
+      if (hact) {
+        uint32_t* colp = limb + lane;
+        if (nrep <= 32) {
+          for (int r = warp * rpw + hm; r < tr; r += (kAtomThreads / 32) * rpw) {
+            const uint32_t* tl = t_limb + 3 * r;
+            uint32_t* c = colp + static_cast<int>(t_codes[r * Dp + hj]) * 32;
+            atomicAdd(c, tl[0]);
+            atomicAdd(c + colh * 32, tl[1]);
+            atomicAdd(c + 2 * colh * 32, tl[2]);
+          }
+        } else {
+          for (int r = warp; r < tr; r += kAtomThreads / 32) {
+            const uint32_t l0 = t_limb[3 * r], l1 = t_limb[3 * r + 1], l2 = t_limb[3 * r + 2];
+            const CodeT* cr = t_codes + r * Dp;
+            for (int j = lane; j < nrep; j += 32) {
+              uint32_t* c = colp + (s_cofs[j] + static_cast<int>(cr[j])) * 32;
+              atomicAdd(c, l0);
+              atomicAdd(c + colh * 32, l1);
+              atomicAdd(c + 2 * colh * 32, l2);
+            }
+          }
         }
       }
       __syncthreads();
     }
     for (int b = tid; b < bins; b += kAtomThreads) {
-      const unsigned __int128 U = static_cast<unsigned __int128>(limb[b]) +
-                                  (static_cast<unsigned __int128>(limb[bins + b]) << 21) +
-                                  (static_cast<unsigned __int128>(limb[2 * bins + b]) << 42);
+      const int j = s_binrep[b], bb = b - s_boff[j];
+      unsigned __int128 U = 0;
+      if (nrep <= 32) {
+        for (int m = 0; m < rpw; ++m) {
+          const uint32_t* c = limb + bb * 32 + j + m * nrep;
+          U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+               (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+        }
+      } else {
+        const uint32_t* c = limb + (s_cofs[j] + bb) * 32 + (j & 31);
+        U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+            (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+      }
       const uint64_t c = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
       const unsigned __int128 sv = U - (static_cast<unsigned __int128>(c) << 62);
       acc_sum[b] += static_cast<int64_t>(static_cast<uint64_t>(sv));
@@ -1068,9 +1136,9 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
   }
 }
 
-inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes) {
-  size_t o = (static_cast<size_t>(3) * bins * 4 + 15) & ~size_t(15);
-  o += static_cast<size_t>(bins) * 12 + static_cast<size_t>(nrep) * 4;
+inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes, int colh) {
+  size_t o = (static_cast<size_t>(3) * colh * 32 * 4 + 15) & ~size_t(15);
+  o += static_cast<size_t>(bins) * 14 + static_cast<size_t>(nrep) * 12 + 16;
   o = (o + 15) & ~size_t(15);
   o += static_cast<size_t>(kAtomTile) * Dp * code_bytes + static_cast<size_t>(kAtomTile) * 12 + 16;
   return o;
@@ -1727,30 +1795,6 @@ struct ResLayout {
 };
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
-
-// Lane-column histogram shape (conflict-free shared atomics): lane l of every warp owns bank
-// column l. nrep <= 32: lanes l < (32 / nrep) * nrep take feature l % nrep (copy l / nrep of
-// it), so the column height is the largest bin count. nrep > 32: lane l takes features l, l+32,
-// ... stacked in its column (cofs = offset of a feature's bins in its lane's column).
-__host__ __device__ inline int col_height(int nrep, const int32_t* nb, int32_t* cofs) {
-  int H = 1;
-  if (nrep <= 32) {
-    for (int j = 0; j < nrep; ++j) {
-      if (cofs) cofs[j] = 0;
-      H = nb[j] > H ? nb[j] : H;
-    }
-    return H;
-  }
-  for (int l = 0; l < 32; ++l) {
-    int h = 0;
-    for (int j = l; j < nrep; j += 32) {
-      if (cofs) cofs[j] = h;
-      h += nb[j];
-    }
-    H = h > H ? h : H;
-  }
-  return H;
-}
 
 // groups: private histogram copies used while accumulating one node (threads own
 // (feature, group) pairs, so no shared-memory atomics are needed).
@@ -2780,6 +2824,7 @@ struct ResidentPlan {
   bool pre_smem = false;
   // column-layout histogram plan for the multi-kernel path (hist_build_col_kernel)
   bool atomic = false;  // limb-atomic histogram (default)
+  int colh_max = 1;     // its lane-column height (col_height), max over families
   size_t atomic_smem = 0;
   bool col = false;
   std::vector<int32_t> col_off;  // [F][kColWarps + 1] entry offsets per feature group
@@ -2911,7 +2956,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         if (resident.atomic)
           hist_build_atomic_kernel<CodeT><<<dim3(static_cast<unsigned>(ceil_div(n_max, kAtomChunk)), pairs, F),
                                              kAtomThreads, resident.atomic_smem, s>>>(
-              fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d);
+              fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
+              resident.colh_max);
         else if (resident.col)
           hist_build_col_kernel<CodeT><<<dim3(chunks, pairs, F), kColWarps * 32, resident.col_smem, s>>>(
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, rep_nb_d, col_off_d, col_rg_d, hsum,
@@ -3221,10 +3267,16 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   if (!res.enabled && hist_mode == "atomic") {
     const int pv = 16 / code_bytes;
     const int dp = std::max(pv, static_cast<int>(ceil_div(std::max(nrep_max, 1), pv)) * pv);
-    const size_t need = hist_atomic_smem(max_bins, nrep_max, dp, code_bytes);
+    int colh_max = 1;
+    for (int f = 0; f < F; ++f) {
+      const FamDesc& fd = fam[static_cast<size_t>(f)];
+      if (fd.nrep > 0) colh_max = std::max(colh_max, col_height(fd.nrep, rep_nb.data() + fd.rep0, nullptr));
+    }
+    const size_t need = hist_atomic_smem(max_bins, nrep_max, dp, code_bytes, colh_max);
     if (need <= 200 * 1024) {
       res.atomic = true;
       res.atomic_smem = need;
+      res.colh_max = colh_max;
     }
   }
   if (!res.enabled && !res.atomic && hist_mode != "rowmajor") {
