@@ -1425,14 +1425,22 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
 // hoisted ahead of the dependent add chain). Every lane returns the sum.
 __device__ __forceinline__ double warp_fold_gather(const double* __restrict__ v, const int32_t* __restrict__ idx,
                                                    int n) {
+  // Software-pipelined: the next 128 gathers (L2 latency) are in flight while the current 128
+  // values are folded in order (the dependent FP64 add chain).
   const int lane = threadIdx.x & 31;
   double s = 0.0;
+  double x[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = 32 * c + lane;
+    x[c] = i < n ? v[idx[i]] : 0.0;
+  }
   for (int i0 = 0; i0 < n; i0 += 128) {
-    double x[4];
+    double y[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int i = i0 + 32 * c + lane;
-      x[c] = i < n ? v[idx[i]] : 0.0;
+      const int i = i0 + 128 + 32 * c + lane;
+      y[c] = i < n ? v[idx[i]] : 0.0;
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -1452,6 +1460,8 @@ __device__ __forceinline__ double warp_fold_gather(const double* __restrict__ v,
         for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
       }
     }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = y[c];
   }
   return s;
 }
@@ -1700,9 +1710,21 @@ __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamSta
   const double sum = warp_fold_gather(resid + fd.pos0, L, n);
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
-  for (int i = lane; i < n; i += 32) {
-    const int64_t p = fd.pos0 + L[i];
-    pred[p] = fs_add(pred[p], step);
+  // prediction update, 8 rows per lane in flight (a plain loop serialises on L2 latency:
+  // the compiler cannot prove the index and prediction arrays do not alias)
+  for (int i0 = 0; i0 < n; i0 += 256) {
+    int64_t pp[8];
+    double pv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + 32 * k + lane;
+      pp[k] = i < n ? fd.pos0 + L[i] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pv[k] = pp[k] >= 0 ? pred[pp[k]] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (pp[k] >= 0) pred[pp[k]] = fs_add(pv[k], step);
   }
   if (lane == 0) {
     nd.value = value;
