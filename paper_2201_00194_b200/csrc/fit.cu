@@ -1208,6 +1208,15 @@ __device__ __forceinline__ void screen_gain(int64_t ls, int64_t ts, int lc, int 
   hi = g + delta;
 }
 
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+  for (int o = 1; o < 32; o <<= 1) {
+    const T t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
 // One thread per (family, node at level, rep). pass 0: max lower bound per node. pass 1:
 // window membership (hi >= LO and hi > 0), per-feature best candidate, node window count.
 __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
@@ -1215,12 +1224,15 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
                               const int32_t* __restrict__ hcnt, const int64_t* __restrict__ node_abs,
                               const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
                               WinRec* __restrict__ win, int nrep_max, int level_slots_max, int pass) {
+  // warp per (node, rep), lanes over the rep's bins: coalesced histogram reads, warp prefix
+  // scans for the left count / sum, every candidate's screen in parallel
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
   const int local = blockIdx.y;
   if (local >= (1 << level)) return;
-  const int jj = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int jj = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (jj >= fd.nrep) return;
   const int s = (1 << level) - 1 + local;
   NodeRec& nd = nodes[fd.node0 + s];
@@ -1232,45 +1244,69 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
   const double scale = ldexp(1.0, -st[f].shift);
   const double S = static_cast<double>(node_abs[fd.node0 + s]) * scale * (1.0 + 1e-12);
   int64_t ts = 0;
-  for (int b = 0; b < nb; ++b) ts += hsum[hb + b];
+  for (int b = lane; b < nb; b += 32) ts += hsum[hb + b];
+  for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
   const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
   double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
-  int bb = -1, blc = 0, count = 0, cum = 0;
-  int64_t ls = 0;
-  for (int b = 0; b < nb; ++b) {
-    const int c = hcnt[hb + b];
-    if (!c) continue;
-    cum += c;
-    ls += hsum[hb + b];
-    if (cum >= n) break;  // no later non-empty bin: not a boundary
-    double g, lo, hi;
-    screen_gain(ls, ts, cum, n, scale, S, g, lo, hi);
-    if (!pass) {
-      best_lo = fmax(best_lo, lo);
-    } else if (hi >= LO && hi > 0.0) {
-      ++count;
-      if (g > bg) {
-        bg = g;
-        bl = lo;
-        bb = b;
-        blc = cum;
+  int bb = 0x7fffffff, blc = 0, count = 0, mlc = 0, carry_c = 0;
+  int64_t carry_s = 0;
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    const int cc = b < nb ? hcnt[hb + b] : 0;
+    const int64_t sv = b < nb ? hsum[hb + b] : 0;
+    const int ic = warp_incl_scan(cc, lane) + carry_c;
+    const int64_t is = warp_incl_scan(sv, lane) + carry_s;
+    if (b < nb && cc > 0 && ic < n) {  // a boundary after bin b (a later bin is non-empty)
+      double g, lo, hi;
+      screen_gain(is, ts, ic, n, scale, S, g, lo, hi);
+      if (!pass) {
+        best_lo = fmax(best_lo, lo);
+      } else if (hi >= LO && hi > 0.0) {
+        ++count;
+        mlc = max(mlc, ic);
+        if (g > bg || (g == bg && b < bb)) {
+          bg = g;
+          bl = lo;
+          bb = b;
+          blc = ic;
+        }
       }
     }
+    carry_c = __shfl_sync(0xffffffffu, ic, 31);
+    carry_s = __shfl_sync(0xffffffffu, is, 31);
   }
   if (!pass) {
-    if (best_lo > -INFINITY) atomicMax(reinterpret_cast<unsigned long long*>(&nd.lokey), lo_key(best_lo));
+    for (int o = 16; o > 0; o >>= 1) best_lo = fmax(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
+    if (lane == 0 && best_lo > -INFINITY)
+      atomicMax(reinterpret_cast<unsigned long long*>(&nd.lokey), lo_key(best_lo));
   } else {
-    WinRec w;
-    w.best_g = bg;
-    w.best_lo = bl;
-    w.best_bin = bb;
-    w.flag = count > 0;
-    w.count = count;
-    w.best_lc = blc;
-    w.eq = 0;
-    w.maxlc = 0;
-    win[(static_cast<int64_t>(f) * level_slots_max + local) * nrep_max + jj] = w;
-    if (count) atomicAdd(&nd.wcount, count);
+    for (int o = 16; o > 0; o >>= 1) {
+      count += __shfl_xor_sync(0xffffffffu, count, o);
+      mlc = max(mlc, __shfl_xor_sync(0xffffffffu, mlc, o));
+      const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+      const int olc = __shfl_xor_sync(0xffffffffu, blc, o);
+      if (og > bg || (og == bg && ob < bb)) {
+        bg = og;
+        bl = ol;
+        bb = ob;
+        blc = olc;
+      }
+    }
+    if (lane == 0) {
+      WinRec w;
+      w.best_g = bg;
+      w.best_lo = bl;
+      w.best_bin = count ? bb : -1;
+      w.flag = count > 0;
+      w.count = count;
+      w.best_lc = blc;
+      w.eq = 0;
+      w.maxlc = mlc;
+      win[(static_cast<int64_t>(f) * level_slots_max + local) * nrep_max + jj] = w;
+      if (count) atomicAdd(&nd.wcount, count);
+    }
   }
 }
 
@@ -1910,14 +1946,6 @@ __device__ __forceinline__ double warp_max_d(double v) {
   return v;
 }
 
-template <class T>
-__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
-  for (int o = 1; o < 32; o <<= 1) {
-    const T t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  return v;
-}
 
 __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const FamDesc* __restrict__ fam, FamState* __restrict__ st, const int* __restrict__ fam_list, int Dp,
@@ -2994,7 +3022,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       }
       hist_derive_kernel<<<dim3(grid1(max_bins, 256, 16), pairs, F), 256, 0, s>>>(fam_d, st_d, nodes, level, hsum,
                                                                                   hcnt, node_abs);
-      const dim3 sg(grid1(nrep_max, 128, 1 << 20), lw, F);
+      const dim3 sg(grid1(nrep_max, 4, 1 << 20), lw, F);  // 4 warps (reps) per 128-thread block
       {
         ProfScope prof(dev, "fit_screen");
         screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
