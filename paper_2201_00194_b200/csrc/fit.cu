@@ -1353,6 +1353,62 @@ __global__ void tieclass_prep_kernel(const FamDesc* __restrict__ fam, const FamS
 
 // One warp per check: walk the lowest window feature's presorted list restricted to the node;
 // the other feature must tie exactly where it ties and increase where it increases.
+// Order equivalence of g with f0 on the node's rows <=> the map code_f0 -> code_g over those rows
+// is a function that strictly increases (ties align, and the stable sorts by (code, canonical
+// position) then coincide). CTA per item: phi[a] = the g code of some row with f0 code a (racy
+// plain stores), every row must agree with phi, phi must increase over the present a. Rows come
+// from the node's order-0 segment, in any order - no scan of the presorted lists.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) tieclass_phi_kernel(
+    const FamDesc* __restrict__ fam, const NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const int32_t* __restrict__ ord_cur, const int32_t* __restrict__ rep_nb, WinRec* __restrict__ win,
+    int nrep_max, int level_slots_max) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* phi = reinterpret_cast<uint16_t*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int total = *n_items;
+  for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+    const ExactItem it = items[wi];
+    const FamDesc fd = fam[it.fam];
+    const NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int f0 = nd.eqf0, g = it.rep, nv = nd.n;
+    const int nb = rep_nb[fd.rep0 + f0];
+    const int32_t* rows = ord_cur + fd.pos0 + nd.seg;
+    const CodeT* cb = codes_c + fd.pos0 * Dp;
+    __syncthreads();  // previous item done with phi
+    for (int a = tid; a < nb; a += blockDim.x) phi[a] = 0xFFFFu;
+    __syncthreads();
+    for (int i = tid; i < nv; i += blockDim.x) {
+      const int64_t p = rows[i];
+      phi[cb[p * Dp + f0]] = static_cast<uint16_t>(cb[p * Dp + g]);
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int i = tid; i < nv; i += blockDim.x) {
+      const int64_t p = rows[i];
+      bad |= phi[cb[p * Dp + f0]] != static_cast<uint16_t>(cb[p * Dp + g]);
+    }
+    if (tid < 32) {  // phi strictly increasing over the present f0 codes
+      int carry = -1;
+      for (int a0 = 0; a0 < nb; a0 += 32) {
+        const int a = a0 + lane;
+        const int v = a < nb ? phi[a] : 0xFFFF;
+        const bool present = v != 0xFFFF;
+        const unsigned m = __ballot_sync(0xffffffffu, present);
+        const unsigned lt = m & ((1u << lane) - 1u);
+        int pv = __shfl_sync(0xffffffffu, v, lt ? 31 - __clz(lt) : 0);
+        if (!lt) pv = carry;
+        if (present && pv >= 0 && v <= pv) bad = true;
+        if (m) carry = __shfl_sync(0xffffffffu, v, 31 - __clz(m));
+      }
+    }
+    bad = __syncthreads_or(bad);
+    const int local = it.slot - ((1 << level) - 1);
+    if (tid == 0) win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + g].eq = !bad;
+  }
+}
+
 template <typename CodeT>
 __global__ void __launch_bounds__(256) tieclass_check_kernel(
     const FamDesc* __restrict__ fam, const NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
@@ -2875,6 +2931,7 @@ struct ResidentPlan {
   // column-layout histogram plan for the multi-kernel path (hist_build_col_kernel)
   bool atomic = false;  // limb-atomic histogram (default)
   int colh_max = 1;     // its lane-column height (col_height), max over families
+  size_t phi_smem = 0;  // tie-class phi table bytes (largest per-feature bin count x 2); 0 = ordered scan
   size_t atomic_smem = 0;
   bool col = false;
   std::vector<int32_t> col_off;  // [F][kColWarps + 1] entry offsets per feature group
@@ -2972,6 +3029,9 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   const unsigned chunks = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n_max, kHistChunk)));
   int32_t* col_off_d = nullptr;
   int32_t* col_rg_d = nullptr;
+  if (resident.phi_smem > 0)
+    FS_CUDA(cudaFuncSetAttribute(tieclass_phi_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(resident.phi_smem)));
   if (resident.atomic)
     FS_CUDA(cudaFuncSetAttribute(hist_build_atomic_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(resident.atomic_smem)));
@@ -3033,8 +3093,13 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
       tieclass_prep_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(
           fam_d, st_d, nodes, level, win, std::max(nrep_max, 1), level_slots_max, items, n_items);
-      tieclass_check_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, ord,
-                                                           nodeid, win, std::max(nrep_max, 1), level_slots_max);
+      if (resident.phi_smem > 0)
+        tieclass_phi_kernel<CodeT><<<sm * 4, 256, resident.phi_smem, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c,
+                                                                 ord_cur, rep_nb_d, win, std::max(nrep_max, 1),
+                                                                 level_slots_max);
+      else
+        tieclass_check_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, ord,
+                                                             nodeid, win, std::max(nrep_max, 1), level_slots_max);
       dev->count_launch(2);
       FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
       decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
@@ -3268,6 +3333,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   }
   if (min_nrep == INT_MAX) min_nrep = 1;
   const int code_bytes = max_nb <= 256 ? 1 : 2;
+  const size_t phi_bytes = (static_cast<size_t>(std::max(max_nb, 1)) * 2 + 15) & ~size_t(15);
   // Path choice: FAMSEER_FIT_PATH = auto (default) | resident | multi.
   ResidentPlan res;
   {
@@ -3307,6 +3373,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     if (mode == "resident" && !res.enabled && !res.families.empty())
       fail(FS_EINVAL, "fit: resident path requested but the families do not fit one CTA");
   }
+  if (phi_bytes <= 96 * 1024 && !std::getenv("FAMSEER_TIE_SCAN")) res.phi_smem = phi_bytes;
   // Column-layout histogram plan (multi-kernel path): per feature group of 32 the largest bin
   // count; row-group copies while they fit the shared-memory budget.
   // Histogram shape for the multi-kernel path: FAMSEER_HIST = atomic (default) | col | rowmajor.
