@@ -316,7 +316,7 @@ def run_native(args, rank, world, local_rank):
         clocks.start()
         l0 = dev.launches
         dev.counters(reset=True)
-        dev.profile("predict,featurize,rank,fit_resident")
+        dev.profile("predict,featurize,score_fused,rank,fit_resident")
         times = timed(step, args.steps)
         torch.cuda.synchronize()
         if dist is not None:
@@ -404,7 +404,8 @@ def run_native(args, rank, world, local_rank):
                       "latency-bound: all per-row state lives in shared memory for the whole fit; HBM carries "
                       "only the inputs once, so the HBM fraction is structurally small"))
     for k, formula, per in (("predict", "P*(8*d + 8)", 8 * PAD + 8), ("featurize", "P*(64 + 4 + 8*pad)",
-                                                                       4 * 16 + 4 + 8 * PAD)):
+                                                                       4 * 16 + 4 + 8 * PAD),
+                            ("score_fused", "P*(64 + 4 + 8): descriptor in, score out", 4 * 16 + 4 + 8)):
         if k in prof_all:
             n_l, ms = prof_all[k]
             cands.append((k, ms, P * per, n_l, formula, None))

@@ -18,31 +18,8 @@
 
 #include "fs_common.cuh"
 
-struct fs_spaces {
-  fs_device* dev = nullptr;
-  int32_t n = 0;
-  int32_t max_fd = 0;
-  std::vector<int32_t> k_h;  // knobs per space
-  int32_t* k_d = nullptr;    // [n]
-  int32_t* nval_d = nullptr; // [n*16]
-  int32_t* off_d = nullptr;  // [n*16] offset into log/pos tables
-  double* log_d = nullptr;
-  double* pos_d = nullptr;
-};
 
 namespace {
-
-// Pair table: for K knobs, pair q (row-major i<j order, searchspace.cpp:111-116) -> i | j<<4.
-__device__ __forceinline__ void pair_of(int k, int q, int& i, int& j) {
-  int row = 0;
-  int remaining = q;
-  while (remaining >= k - 1 - row) {
-    remaining -= k - 1 - row;
-    ++row;
-  }
-  i = row;
-  j = row + 1 + remaining;
-}
 
 __global__ void __launch_bounds__(256) featurize_kernel(const int32_t* __restrict__ space_of,
                                                         const int32_t* __restrict__ assign, int64_t n,
@@ -94,7 +71,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const int32_t* __restric
         src_a = j - k;
       } else if (j < dim) {
         kind = 3;
-        pair_of(k, j - 2 * k, src_a, src_b);
+        fs::pair_of(k, j - 2 * k, src_a, src_b);
       }
       const double la = __shfl_sync(0xffffffffu, lg, src_a);
       const double lb = __shfl_sync(0xffffffffu, lg, src_b);

@@ -976,7 +976,7 @@ __host__ __device__ inline int col_height(int nrep, const int32_t* nb, int32_t* 
 // choice of the fixed-point shift), sum = U - count*2^62. No count atomic is needed.
 constexpr int kAtomThreads = 1024;
 constexpr int kAtomSub = 2048;
-constexpr int kAtomChunk = 8192;
+constexpr int kAtomChunk = 8192;  // max rows per CTA (fewer when the batch is small: >= 2 CTAs per SM)
 constexpr int kAtomTile = 128;
 constexpr uint32_t kLimbMask = (1u << 21) - 1u;
 
@@ -985,7 +985,7 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
     int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
     const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
-    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr, int colh_max) {
+    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr, int colh_max, int chunk) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
@@ -1004,9 +1004,9 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
     if (nd[s].build != 1) return;
   }
   const int n_v = nd[s].n;
-  const int r0 = blockIdx.x * kAtomChunk;
+  const int r0 = blockIdx.x * chunk;
   if (r0 >= n_v) return;
-  const int rows = min(kAtomChunk, n_v - r0);
+  const int rows = min(chunk, n_v - r0);
   const int seg = nd[s].seg;
   const int local = s - ((1 << level) - 1);
   const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
@@ -2949,6 +2949,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                 TreeRec* trees_d, double* mse_d, double* base_d, int min_nrep_hint) {
   cudaStream_t s = dev->stream;
   const int sm = dev->sm_count;
+  // rows per histogram CTA: kAtomChunk, shrunk (multiples of kAtomTile) until the root level
+  // alone launches >= 2 CTAs per SM - a few large families otherwise leave most SMs idle
+  int atom_chunk = kAtomChunk;
+  while (atom_chunk > 2 * kAtomTile && static_cast<int64_t>(ceil_div(n_max, atom_chunk)) * F < 2LL * sm)
+    atom_chunk /= 2;
   // ---- prep: canonical order, gather, presorts, bin counts, base -------------------------
   int32_t* canon = ar.alloc<int32_t>(n_tot);
   int32_t* tmp = ar.alloc<int32_t>(std::max<int64_t>(n_tot, total_ord));
@@ -3064,10 +3069,10 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       {
         ProfScope prof(dev, "fit_hist_build");
         if (resident.atomic)
-          hist_build_atomic_kernel<CodeT><<<dim3(static_cast<unsigned>(ceil_div(n_max, kAtomChunk)), pairs, F),
+          hist_build_atomic_kernel<CodeT><<<dim3(static_cast<unsigned>(ceil_div(n_max, atom_chunk)), pairs, F),
                                              kAtomThreads, resident.atomic_smem, s>>>(
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
-              resident.colh_max);
+              resident.colh_max, atom_chunk);
         else if (resident.col)
           hist_build_col_kernel<CodeT><<<dim3(chunks, pairs, F), kColWarps * 32, resident.col_smem, s>>>(
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, rep_nb_d, col_off_d, col_rg_d, hsum,

@@ -172,3 +172,31 @@ __device__ __forceinline__ double fs_add(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ double fs_sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double fs_mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double fs_div(double a, double b) { return __ddiv_rn(a, b); }
+
+// Device-resident knob-space tables (fs_spaces_create): per (space, knob, value index) the
+// reference's log2(value) and list position, both computed on the host (searchspace.cpp:103-109).
+struct fs_spaces {
+  fs_device* dev = nullptr;
+  int32_t n = 0;
+  int32_t max_fd = 0;
+  std::vector<int32_t> k_h;  // knobs per space
+  int32_t* k_d = nullptr;    // [n]
+  int32_t* nval_d = nullptr; // [n*16]
+  int32_t* off_d = nullptr;  // [n*16] offset into log/pos tables
+  double* log_d = nullptr;
+  double* pos_d = nullptr;
+};
+
+namespace fs {
+// Pair q of K knobs in the reference's row-major i<j order (searchspace.cpp:111-116).
+__device__ __forceinline__ void pair_of(int k, int q, int& i, int& j) {
+  int row = 0;
+  int remaining = q;
+  while (remaining >= k - 1 - row) {
+    remaining -= k - 1 - row;
+    ++row;
+  }
+  i = row;
+  j = row + 1 + remaining;
+}
+}  // namespace fs

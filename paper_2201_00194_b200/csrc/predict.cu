@@ -33,6 +33,21 @@ struct PredModel {
   int depth, n_trees, d_model, n_uthr;
 };
 
+// Candidate descriptors for the fused score path (kFused): the kernel computes each tested
+// feature from the assignment exactly as featurize does (searchspace.cpp:90-118; log2/position
+// tables built on the host, pair products one __dmul_rn) instead of reading a feature row.
+struct SpaceTabs {
+  const int32_t* space_of;  // [P]
+  const int32_t* assign;    // [P][16] value indices
+  const int32_t* k;         // [n_spaces] knobs
+  const int32_t* nval;      // [n_spaces][16]
+  const int32_t* off;       // [n_spaces][16] offset into log/pos
+  const double* log;
+  const double* pos;
+  int n_spaces;
+  int pad;
+};
+
 // One CTA's work: a tile of up to kTile rows of one family segment.
 struct PredJob {
   int32_t model, rows;
@@ -43,11 +58,11 @@ struct PredJob {
 // Every family segment of a predict call is scored by ONE launch (a family is typically a few
 // hundred tiles; one launch per family left most of the 148 SMs idle). Shared memory is laid out
 // for the largest model of the launch; each CTA uses its own model's shape.
-template <typename CodeT, bool kLeaves, bool kSmemThr>
+template <typename CodeT, bool kLeaves, bool kSmemThr, bool kFused>
 __global__ void __launch_bounds__(kTile) predict_heap_kernel(
     const double* __restrict__ x, int d, const PredModel* __restrict__ models, const PredJob* __restrict__ jobs,
     int max_dmodel, int max_depth, int max_uthr, double* __restrict__ scores, uint8_t* __restrict__ leaf_out,
-    uint32_t* err) {
+    uint32_t* err, SpaceTabs sp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const PredJob job = jobs[blockIdx.x];
   const PredModel M = models[job.model];
@@ -85,25 +100,79 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
   const int64_t row0 = job.row0;
   const int tile_rows = job.rows;
 
-  bool nonfinite = false;
-  for (int c = warp; c < tile_rows; c += kTile / 32) {
-    const double* xr = x + (row0 + c) * d;
-    for (int f = lane; f < d; f += 32) {
-      const double v = __ldcs(xr + f);  // streamed once
-      nonfinite |= !isfinite(v);
-      if (f < d_model) {
-        int lo = uoff[f], hi = uoff[f + 1];
-        const int first = lo;
-        while (lo < hi) {  // count of unique thresholds strictly below v
-          const int mid = (lo + hi) >> 1;
-          if (uthr[mid] < v) lo = mid + 1;
-          else hi = mid;
+  auto code_of = [&](int f, double v) {
+    int lo = uoff[f], hi = uoff[f + 1];
+    const int first = lo;
+    while (lo < hi) {  // count of unique thresholds strictly below v
+      const int mid = (lo + hi) >> 1;
+      if (uthr[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    return static_cast<CodeT>(lo - first);
+  };
+  if constexpr (kFused) {
+    // warp per candidate: lane k < K fetches knob k's log2 / position; every tested feature is
+    // formed from shuffles (featurize_kernel's arithmetic) and coded - no feature row in HBM
+    for (int c = warp; c < tile_rows; c += kTile / 32) {
+      const int64_t cand = row0 + c;
+      const int s = __ldg(sp.space_of + cand);
+      const bool bad_space = s < 0 || s >= sp.n_spaces;
+      const int k = bad_space ? 0 : __ldg(sp.k + s);
+      const int dim = 2 * k + k * (k - 1) / 2;
+      double lg = 0.0, ps = 0.0;
+      bool bad = false;
+      if (lane < k) {
+        const int a = __ldg(sp.assign + cand * FS_MAX_KNOBS + lane);
+        const int m = __ldg(sp.nval + s * FS_MAX_KNOBS + lane);
+        if (a < 0 || a >= m) {
+          bad = true;
+        } else {
+          const int off = __ldg(sp.off + s * FS_MAX_KNOBS + lane);
+          lg = __ldg(sp.log + off + a);
+          ps = __ldg(sp.pos + off + a);
         }
-        codes[f * kTile + c] = static_cast<CodeT>(lo - first);
+      }
+      const unsigned any_bad = __ballot_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        if (bad_space) atomicOr(err, fs::kErrSpaceId);
+        if (any_bad) atomicOr(err, fs::kErrKnobRange);
+        if (sp.pad < dim) atomicOr(err, fs::kErrPadDim);
+      }
+      for (int base = 0; base < d_model; base += 32) {
+        const int f = base + lane;
+        int src_a = 0, src_b = 0, kind = 0;  // 0 zero (padding), 1 log, 2 pos, 3 product
+        if (f < k) {
+          kind = 1;
+          src_a = f;
+        } else if (f < 2 * k) {
+          kind = 2;
+          src_a = f - k;
+        } else if (f < dim) {
+          kind = 3;
+          fs::pair_of(k, f - 2 * k, src_a, src_b);
+        }
+        const double la = __shfl_sync(0xffffffffu, lg, src_a);
+        const double lb = __shfl_sync(0xffffffffu, lg, src_b);
+        const double pa = __shfl_sync(0xffffffffu, ps, src_a);
+        double v = 0.0;
+        if (kind == 1) v = la;
+        else if (kind == 2) v = pa;
+        else if (kind == 3) v = fs_mul(la, lb);
+        if (f < d_model) codes[f * kTile + c] = code_of(f, v);
       }
     }
+  } else {
+    bool nonfinite = false;
+    for (int c = warp; c < tile_rows; c += kTile / 32) {
+      const double* xr = x + (row0 + c) * d;
+      for (int f = lane; f < d; f += 32) {
+        const double v = __ldcs(xr + f);  // streamed once
+        nonfinite |= !isfinite(v);
+        if (f < d_model) codes[f * kTile + c] = code_of(f, v);
+      }
+    }
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, fs::kErrNonFinitePredict);
   }
-  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, fs::kErrNonFinitePredict);
 
   double score = M.base;
   const double lr = M.lr;
@@ -171,8 +240,9 @@ struct HeapGroup {
   int max_dmodel = 0, max_depth = 0, max_uthr = 0;
 };
 
-template <typename CodeT, bool kLeaves, bool kSmemThr>
-void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, double* scores, uint8_t* leaf_out) {
+template <typename CodeT, bool kLeaves, bool kSmemThr, bool kFused>
+void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, double* scores, uint8_t* leaf_out,
+                  const SpaceTabs& sp) {
   if (g.jobs.empty()) return;
   const int mnint = (1 << g.max_depth) - 1, mnleaf = 1 << g.max_depth;
   size_t smem = (static_cast<size_t>(g.max_dmodel) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
@@ -180,7 +250,7 @@ void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, do
   if (kLeaves) smem += static_cast<size_t>(kTile) * kChunk;
   smem = (smem + 15) & ~size_t(15);
   if (kSmemThr) smem += static_cast<size_t>(g.max_uthr) * sizeof(double) + (g.max_dmodel + 1) * sizeof(int32_t);
-  auto* fn = predict_heap_kernel<CodeT, kLeaves, kSmemThr>;
+  auto* fn = predict_heap_kernel<CodeT, kLeaves, kSmemThr, kFused>;
   if (smem > 227 * 1024) fs::fail(FS_EINVAL, "predict: model too wide for the shared-memory tile");
   FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const size_t mb = g.models.size() * sizeof(PredModel), jb = g.jobs.size() * sizeof(PredJob);
@@ -189,9 +259,9 @@ void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, do
   auto* jd = reinterpret_cast<PredJob*>(buf + ((mb + 15) & ~size_t(15)));
   FS_CUDA(cudaMemcpyAsync(md, g.models.data(), mb, cudaMemcpyHostToDevice, dev->stream));
   FS_CUDA(cudaMemcpyAsync(jd, g.jobs.data(), jb, cudaMemcpyHostToDevice, dev->stream));
-  fs::ProfScope prof(dev, "predict");
-  fn<<<static_cast<unsigned>(g.jobs.size()), kTile, smem, dev->stream>>>(x, d, md, jd, g.max_dmodel, g.max_depth,
-                                                                         g.max_uthr, scores, leaf_out, dev->err_d);
+  fs::ProfScope prof(dev, kFused ? "score_fused" : "predict");
+  fn<<<static_cast<unsigned>(g.jobs.size()), kTile, smem, dev->stream>>>(
+      x, d, md, jd, g.max_dmodel, g.max_depth, g.max_uthr, scores, leaf_out, dev->err_d, sp);
   dev->count_launch();
   FS_CUDA(cudaGetLastError());
 }
@@ -203,8 +273,9 @@ namespace fs {
 // Scores rows [seg[f], seg[f+1]) with family f. Leaf ids of segment f start at byte
 // sum_{g<f} rows_g * T_g of leaf_out. All heap-form families go out in one launch (per code width
 // / threshold-table placement, normally one); deeper-than-heap models use the generic kernel.
-void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
-                    const double* x, double* scores, uint8_t* leaf_out) {
+template <bool kFused>
+void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
+                         const double* x, double* scores, uint8_t* leaf_out, const SpaceTabs& sp) {
   int64_t leaf_off = 0;
   HeapGroup groups[2][2];  // [code_bytes == 2][thresholds in smem]
   for (int f = 0; f < nseg; ++f) {
@@ -217,6 +288,7 @@ void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int
     const int64_t lo = leaf_off;
     leaf_off += rows * m.n_trees;
     if (m.generic) {
+      if (kFused) fail(FS_EINVAL, "score: fused path needs heap-form models");
       predict_generic_kernel<<<static_cast<int>(ceil_div(rows, 128)), 128, 0, dev->stream>>>(
           x + r0 * d, rows, d, m.n_trees, m.base, m.lr, m.g_off_d, m.g_feat_d, m.g_thr_d, m.g_left_d, m.g_right_d,
           m.g_val_d, scores + r0, leaf_out ? leaf_out + lo : nullptr, dev->err_d);
@@ -240,17 +312,30 @@ void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int
       const HeapGroup& g = groups[cb][st];
       if (g.jobs.empty()) continue;
       if (cb == 0) {
-        if (leaf_out) st ? launch_group<uint8_t, true, true>(dev, g, x, d, scores, leaf_out)
-                         : launch_group<uint8_t, true, false>(dev, g, x, d, scores, leaf_out);
-        else st ? launch_group<uint8_t, false, true>(dev, g, x, d, scores, nullptr)
-                : launch_group<uint8_t, false, false>(dev, g, x, d, scores, nullptr);
+        if (leaf_out) st ? launch_group<uint8_t, true, true, kFused>(dev, g, x, d, scores, leaf_out, sp)
+                         : launch_group<uint8_t, true, false, kFused>(dev, g, x, d, scores, leaf_out, sp);
+        else st ? launch_group<uint8_t, false, true, kFused>(dev, g, x, d, scores, nullptr, sp)
+                : launch_group<uint8_t, false, false, kFused>(dev, g, x, d, scores, nullptr, sp);
       } else {
-        if (leaf_out) st ? launch_group<uint16_t, true, true>(dev, g, x, d, scores, leaf_out)
-                         : launch_group<uint16_t, true, false>(dev, g, x, d, scores, leaf_out);
-        else st ? launch_group<uint16_t, false, true>(dev, g, x, d, scores, nullptr)
-                : launch_group<uint16_t, false, false>(dev, g, x, d, scores, nullptr);
+        if (leaf_out) st ? launch_group<uint16_t, true, true, kFused>(dev, g, x, d, scores, leaf_out, sp)
+                         : launch_group<uint16_t, true, false, kFused>(dev, g, x, d, scores, leaf_out, sp);
+        else st ? launch_group<uint16_t, false, true, kFused>(dev, g, x, d, scores, nullptr, sp)
+                : launch_group<uint16_t, false, false, kFused>(dev, g, x, d, scores, nullptr, sp);
       }
     }
+}
+
+void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
+                    const double* x, double* scores, uint8_t* leaf_out) {
+  launch_predict_impl<false>(dev, fo, nseg, seg, d, x, scores, leaf_out, SpaceTabs{});
+}
+
+// Fused featurize -> predict: candidates come as (space id, value indices)
+// descriptors; no feature matrix is written or read. pad plays the row width d.
+void launch_score_fused(fs_device* dev, const fs_spaces* spc, const fs_forest* fo, int32_t nseg, const int64_t* seg,
+                        const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores) {
+  const SpaceTabs sp{space_of_d, assign_d, spc->k_d, spc->nval_d, spc->off_d, spc->log_d, spc->pos_d, spc->n, pad};
+  launch_predict_impl<true>(dev, fo, nseg, seg, pad, nullptr, scores, nullptr, sp);
 }
 
 int64_t leaf_bytes(const fs_forest* fo, int32_t nseg, const int64_t* seg) {

@@ -3,6 +3,7 @@
 // (costmodel.cpp:237-246), then rank each family's pool by (score, index). The feature matrix
 // lives only in device scratch.
 #include <algorithm>
+#include <cstdlib>
 
 #include "forest.cuh"
 
@@ -12,6 +13,8 @@ void launch_featurize(fs_device* dev, const fs_spaces* sp, int64_t n, const int3
 void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
                     const double* x, double* scores, uint8_t* leaf_out);
 void launch_rank(fs_device* dev, int32_t nseg, const int64_t* seg_h, const double* scores_d, int32_t* perm_d);
+void launch_score_fused(fs_device* dev, const fs_spaces* spc, const fs_forest* fo, int32_t nseg, const int64_t* seg,
+                        const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores);
 
 static void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg,
                          const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores_d,
@@ -19,9 +22,19 @@ static void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* f
   const int64_t n = seg[nseg];
   if (n <= 0) return;
   if (seg[0] != 0) fail(FS_EINVAL, "score: seg[0] must be 0");
-  auto* x = static_cast<double*>(dev->scratch(kSlotScoreX, static_cast<size_t>(n) * pad * sizeof(double)));
-  launch_featurize(dev, sp, n, space_of_d, assign_d, pad, x);
-  launch_predict(dev, fo, nseg, seg, pad, x, scores_d, nullptr);
+  // Fused by default: every tested feature is computed from the descriptor inside the predict
+  // tile (no pad*8-byte feature row per candidate in HBM). FAMSEER_SCORE_UNFUSED=1 (or a
+  // deeper-than-heap model) takes featurize -> predict through a device feature matrix.
+  bool fused = std::getenv("FAMSEER_SCORE_UNFUSED") == nullptr;
+  for (int f = 0; f < nseg && fused; ++f)
+    if (f < static_cast<int32_t>(fo->fams.size()) && fo->fams[static_cast<size_t>(f)].generic) fused = false;
+  if (fused) {
+    launch_score_fused(dev, sp, fo, nseg, seg, space_of_d, assign_d, pad, scores_d);
+  } else {
+    auto* x = static_cast<double*>(dev->scratch(kSlotScoreX, static_cast<size_t>(n) * pad * sizeof(double)));
+    launch_featurize(dev, sp, n, space_of_d, assign_d, pad, x);
+    launch_predict(dev, fo, nseg, seg, pad, x, scores_d, nullptr);
+  }
   launch_rank(dev, nseg, seg, scores_d, perm_d);
 }
 

@@ -52,3 +52,21 @@ def _featurize_pool(W, orc):
         kn = W["spaces"][sid]
         x[rows] = orc.featurize(kn, W["pool_a"][rows][:, : len(kn)], bench.PAD)
     return x
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_score_fused_equals_featurize_then_predict(dev, orc, monkeypatch, cfg):
+    """fs_score's fused descriptor path (no feature matrix) == featurize -> predict -> rank."""
+    W = bench.build_workload(cfg, 7)
+    x = bench._featurize_host(W, orc)
+    F = len(W["families"])
+    fo = fs.Forest(dev, F)
+    fo.fit(x, W["tr_y"], seg=list(W["tr_seg"]), params=fs.GbtParams(40, 3, 0.1, 2))
+    sp = fs.Spaces(dev, W["spaces"])
+    s1, p1 = sp.score(fo, W["pool_so"], W["pool_a"], bench.PAD, W["pool_seg"])
+    monkeypatch.setenv("FAMSEER_SCORE_UNFUSED", "1")
+    s2, p2 = sp.score(fo, W["pool_so"], W["pool_a"], bench.PAD, W["pool_seg"])
+    assert np.array_equal(s1, s2) and np.array_equal(p1, p2)
+    xp = _featurize_pool(W, orc)
+    s3 = fo.predict(xp, seg=list(W["pool_seg"]))
+    assert np.array_equal(s1, s3)
