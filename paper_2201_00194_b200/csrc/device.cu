@@ -109,6 +109,15 @@ void* fs_device::pinned_upload(size_t bytes) {
   return up_h;
 }
 
+cudaStream_t fs_device::aux_stream() {
+  if (!aux) {
+    FS_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    FS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    FS_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  return aux;
+}
+
 void fs_device::upload_done() {
   if (!up_evt) FS_CUDA(cudaEventCreateWithFlags(&up_evt, cudaEventDisableTiming));
   FS_CUDA(cudaEventRecord(up_evt, stream));
@@ -178,6 +187,12 @@ int fs_device_destroy(fs_device* d) {
       cudaEventDestroy(d->up_evt);
     }
     if (d->up_h) cudaFreeHost(d->up_h);
+    if (d->aux) {
+      cudaStreamSynchronize(d->aux);
+      cudaStreamDestroy(d->aux);
+      cudaEventDestroy(d->ev_fork);
+      cudaEventDestroy(d->ev_join);
+    }
     if (d->own) cudaStreamDestroy(d->own);
     delete d;
   });

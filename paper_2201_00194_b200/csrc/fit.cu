@@ -1457,6 +1457,70 @@ __global__ void __launch_bounds__(256) tieclass_check_kernel(
 }
 
 // Decide screened nodes; queue the rest for reference-order re-evaluation.
+__device__ __forceinline__ double warp_fold_gather(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                   int n) {
+  // Software-pipelined: the next 128 gathers (L2 latency) are in flight while the current 128
+  // values are folded in order (the dependent FP64 add chain).
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  double x[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = 32 * c + lane;
+    x[c] = i < n ? v[idx[i]] : 0.0;
+  }
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    double y[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 128 + 32 * c + lane;
+      y[c] = i < n ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int base = i0 + 32 * c;
+      if (base >= n) break;
+      const int m = min(32, n - base);
+      if (m == 32) {
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          double t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
+        }
+      } else {
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = y[c];
+  }
+  return s;
+}
+
+// Node totals (costmodel.cpp:47, sum_residuals over the feature-0 list) for every node of the
+// level that will be screened, on a forked stream: the reference-order chains run while the
+// histogram / screen / tie-class kernels of the same level do. nd.pad_ = 1 marks the total valid
+// (exact decisions and leaf values then reuse it - the same fold over the same segment).
+__global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                              NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ ord_cur,
+                              const double* __restrict__ resid) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (local >= (1 << level)) return;
+  NodeRec& nd = nodes[fd.node0 + (1 << level) - 1 + local];
+  if (nd.state != 0 || nd.build == 0 || nd.n <= 0) return;
+  const double t = warp_fold_gather(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, nd.n);
+  if ((threadIdx.x & 31) == 0) {
+    nd.total = t;
+    nd.pad_ = 1;
+  }
+}
+
 __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                               NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
                               const int32_t* __restrict__ rep_boff, const WinRec* __restrict__ win, int nrep_max,
@@ -1501,13 +1565,14 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
   (void)rep_boff;
   nd.state = kNodeExact;
   atomicAdd(&const_cast<FamState*>(st)[f].exact, 1ull);
-  int k = 1;
+  const int tot = nd.pad_ ? 0 : 1;  // node total still to fold (not precomputed by totals_kernel)
+  int k = tot;
   for (int jj = 0; jj < fd.nrep; ++jj) k += w[jj].flag;
   const int base = atomicAdd(n_items, k);
   atomicAdd(ctr + kCtrExactChains, static_cast<unsigned long long>(k));
   atomicAdd(ctr + kCtrExactNodes, 1ull);
-  items[base] = {f, static_cast<int16_t>(s), static_cast<int16_t>(-1)};
-  int o = 1;
+  if (tot) items[base] = {f, static_cast<int16_t>(s), static_cast<int16_t>(-1)};
+  int o = tot;
   for (int jj = 0; jj < fd.nrep; ++jj)
     if (w[jj].flag) items[base + o++] = {f, static_cast<int16_t>(s), static_cast<int16_t>(jj)};
 }
@@ -1515,48 +1580,6 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
 // sum_residuals (costmodel.cpp:36-40) of v[idx[0..n)) in list order by one warp: four chunks of
 // 32 gathers are in flight at once, then each chunk's values are added in lane order (shuffles
 // hoisted ahead of the dependent add chain). Every lane returns the sum.
-__device__ __forceinline__ double warp_fold_gather(const double* __restrict__ v, const int32_t* __restrict__ idx,
-                                                   int n) {
-  // Software-pipelined: the next 128 gathers (L2 latency) are in flight while the current 128
-  // values are folded in order (the dependent FP64 add chain).
-  const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  double x[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int i = 32 * c + lane;
-    x[c] = i < n ? v[idx[i]] : 0.0;
-  }
-  for (int i0 = 0; i0 < n; i0 += 128) {
-    double y[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = i0 + 128 + 32 * c + lane;
-      y[c] = i < n ? v[idx[i]] : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int base = i0 + 32 * c;
-      if (base >= n) break;
-      const int m = min(32, n - base);
-      if (m == 32) {
-#pragma unroll
-        for (int l0 = 0; l0 < 32; l0 += 8) {
-          double t[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
-        }
-      } else {
-        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) x[c] = y[c];
-  }
-  return s;
-}
 
 // One warp per item: reference-order folds. Item rep < 0: node total over the order-0 list
 // (sum_residuals(order[0]), costmodel.cpp:47). Item rep j: best_split's left sums over feature j's
@@ -1568,7 +1591,9 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
                                                     const double* __restrict__ resid, const int32_t* __restrict__ ord,
                                                     const int32_t* __restrict__ ord_cur,
                                                     const int16_t* __restrict__ nodeid,
-                                                    const int32_t* __restrict__ rep_boff, double* __restrict__ lbuf) {
+                                                    const int32_t* __restrict__ rep_boff, double* __restrict__ lbuf,
+                                                    const WinRec* __restrict__ win, int nrep_max,
+                                                    int level_slots_max) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int total = *n_items;
@@ -1587,9 +1612,12 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
     const int local = it.slot - ((1 << level) - 1);
     double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
     double left = 0.0;
-    int prev = -1, seen = 0;
+    int prev = -1, seen = 0, used = 0;
+    // candidates past the feature's largest window left count cannot win (costmodel.cpp:65
+    // strict >): the fold stops there
+    const int need = win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + jj].maxlc;
     // 4 chunks of 32 list entries in flight: index loads, then the dependent gathers
-    for (int i0 = 0; i0 < fd.n && seen < n; i0 += 128) {
+    for (int i0 = 0; i0 < fd.n && seen < need; i0 += 128) {
       int p[4], code[4];
       double rv[4];
       bool mem[4];
@@ -1617,15 +1645,17 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
           }
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            if ((m >> (l0 + k)) & 1u) {
+            if (((m >> (l0 + k)) & 1u) && used < need) {
               if (prev >= 0 && cc[k] != prev && lane == 0) out[prev] = left;  // boundary after bin `prev`
               left = fs_add(left, vv[k]);
               prev = cc[k];
+              ++used;
             }
           }
         }
       }
     }
+    if (lane == 0 && prev >= 0 && used == need) out[prev] = left;  // the last window boundary
   }
 }
 
@@ -1655,12 +1685,27 @@ __global__ void exact_decide_kernel(const FamDesc* __restrict__ fam, const FamSt
     const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins +
                        rep_boff[fd.rep0 + jj];
     const double* lb = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    if (w[jj].count == 1) {  // its window candidate is the only one of this feature that can win
+      const int cum = w[jj].best_lc, b = w[jj].best_bin;
+      const double L = lb[b];
+      const double R = fs_sub(T, L);
+      const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+      const double r = fs_div(fs_mul(R, R), static_cast<double>(n - cum));
+      const double g = fs_sub(fs_add(a, r), parent);
+      if (g > best) {
+        best = g;
+        bj = jj;
+        bb = b;
+        blc = cum;
+      }
+      continue;
+    }
     int cum = 0;
     for (int b = 0; b < rep_nb[fd.rep0 + jj]; ++b) {
       const int c = hcnt[hb + b];
       if (!c) continue;
       cum += c;
-      if (cum >= n) break;
+      if (cum >= n || cum > w[jj].maxlc) break;  // folds stop at the last window candidate
       const double L = lb[b];
       const double R = fs_sub(T, L);
       const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
@@ -1799,7 +1844,8 @@ __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamSta
   if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
   const int n = nd.n;
   const int32_t* L = ord_cur + fd.pos0 + nd.seg;
-  const double sum = warp_fold_gather(resid + fd.pos0, L, n);
+  // the same fold as the node total when totals_kernel already produced it (costmodel.cpp:86)
+  const double sum = nd.pad_ ? nd.total : warp_fold_gather(resid + fd.pos0, L, n);
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
   // prediction update, 8 rows per lane in flight (a plain loop serialises on L2 latency:
@@ -3051,6 +3097,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   // lives on the device in FamState::ntrees), so it is captured once as a CUDA graph and replayed
   // max_trees times; families that stopped early skip their work inside the kernels.
   const int64_t l0 = dev->launches;
+  const bool fork_totals = std::getenv("FAMSEER_FORK_TOTALS") != nullptr;
+  cudaStream_t aux = fork_totals ? dev->aux_stream() : nullptr;
   auto round_body = [&]() {
     round_init_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, slots, trees_d);
     FS_CUDA(cudaMemsetAsync(node_abs, 0, static_cast<size_t>(F) * slots * sizeof(int64_t), s));
@@ -3063,6 +3111,17 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       level_plan_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level);
       dev->count_launch();
       if (level == depth_max || nrep_max == 0) continue;
+      // Optional fork (FAMSEER_FORK_TOTALS=1): every screened node's total on a side stream while
+      // this level's histogram..decide kernels run; joined before the exact folds. Measured
+      // slower at C4 (the root chain outlasts the level's other kernels and the join then
+      // stalls every level, exact or not), so the totals are folded only for exact nodes.
+      if (fork_totals) {
+        FS_CUDA(cudaEventRecord(dev->ev_fork, s));
+        FS_CUDA(cudaStreamWaitEvent(aux, dev->ev_fork, 0));
+        totals_kernel<<<dim3(grid1(lw, 4, 1 << 20), F), 128, 0, aux>>>(fam_d, st_d, nodes, level, ord_cur, resid);
+        FS_CUDA(cudaEventRecord(dev->ev_join, aux));
+        dev->count_launch();
+      }
       hist_zero_kernel<<<dim3(grid1(static_cast<int64_t>(lw) * max_bins, 256, 64), F), 256, 0, s>>>(fam_d, st_d, level,
                                                                                                   hsum, hcnt);
       const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
@@ -3110,10 +3169,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
                                                                      std::max(nrep_max, 1), level_slots_max, items,
                                                                      n_items, dev->ctr_d);
+      if (fork_totals) FS_CUDA(cudaStreamWaitEvent(s, dev->ev_join, 0));  // join: totals ready
       {
         ProfScope prof(dev, "fit_exact");
         exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord,
-                                                   ord_cur, nodeid, rep_boff_d, lbuf);
+                                                   ord_cur, nodeid, rep_boff_d, lbuf, win, std::max(nrep_max, 1),
+                                                   level_slots_max);
       }
       exact_decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt,
                                                                            rep_boff_d, rep_nb_d, win,
