@@ -632,8 +632,17 @@ __global__ void residual_kernel(const FamDesc* __restrict__ fam, int F, int64_t 
     resid[p] = r;
     ord_cur[p] = ord_root[p];
     nodeid[p] = 0;
-    atomicMax(reinterpret_cast<unsigned long long*>(&st[f].maxabs),
-              static_cast<unsigned long long>(__double_as_longlong(fabs(r))));
+    // max |r| bits (non-negative doubles order like integers): warp-reduced when the warp's
+    // rows share a family (the common case - families are contiguous), else per lane
+    unsigned long long m = static_cast<unsigned long long>(__double_as_longlong(fabs(r)));
+    const unsigned act = __activemask();
+    const int f0 = __shfl_sync(act, f, __ffs(act) - 1);
+    if (__all_sync(act, f == f0) && act == 0xffffffffu) {
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(&st[f].maxabs), m);
+    } else {
+      atomicMax(reinterpret_cast<unsigned long long*>(&st[f].maxabs), m);
+    }
   }
 }
 
@@ -1879,43 +1888,55 @@ __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamSta
 // Commit the round's tree or stop (costmodel.cpp:212), then MSE over canonical rows (:215-220).
 // The MSE is a fixed-order tree reduction: deterministic, within 1e-15 relative of the
 // reference's sequential fold (it never feeds back into the model).
-__global__ void commit_mse_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
-                                  const NodeRec* __restrict__ nodes, const double* __restrict__ target_c,
-                                  const double* __restrict__ pred, double* __restrict__ mse, int max_trees) {
-  __shared__ double part[256];
-  __shared__ int commit;
-  const int f = blockIdx.x;
+// MSE per round (costmodel.cpp:215-220; a fixed-order reduction - it never feeds back):
+// blocks of kMseRows rows per family produce partials (block tree reduction), mse_final_kernel
+// adds them in block order; it also commits the tree or applies the early stop (:212).
+constexpr int kMseRows = 2048;
+__device__ __forceinline__ bool round_commits(const FamDesc& fd, const FamState& st, const NodeRec* nodes) {
+  if (!st.active) return false;
+  const NodeRec& root = nodes[fd.node0];
+  return !(root.state == kNodeLeaf && root.value == 0.0);
+}
+__global__ void mse_partial_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                   const NodeRec* __restrict__ nodes, const double* __restrict__ target_c,
+                                   const double* __restrict__ pred, double* __restrict__ part, int max_blocks) {
+  __shared__ double red[256];
+  const int f = blockIdx.y;
   const FamDesc fd = fam[f];
-  if (threadIdx.x == 0) {
-    commit = 0;
-    if (st[f].active) {
-      const NodeRec& root = nodes[fd.node0];
-      if (root.state == kNodeLeaf && root.value == 0.0) {
-        st[f].active = 0;
-      } else {
-        commit = 1;
-      }
-    }
-  }
-  __syncthreads();
-  if (!commit) return;
+  const int r0 = blockIdx.x * kMseRows;
+  if (r0 >= fd.n || !round_commits(fd, st[f], nodes)) return;
+  const int r1 = min(fd.n, r0 + kMseRows);
   double a = 0.0;
-  for (int i = threadIdx.x; i < fd.n; i += blockDim.x) {
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
     const double e = fs_sub(target_c[fd.pos0 + i], pred[fd.pos0 + i]);
     a = fs_add(a, fs_mul(e, e));
   }
-  part[threadIdx.x] = a;
+  red[threadIdx.x] = a;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) part[threadIdx.x] = fs_add(part[threadIdx.x], part[threadIdx.x + o]);
+    if (threadIdx.x < o) red[threadIdx.x] = fs_add(red[threadIdx.x], red[threadIdx.x + o]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    const int t = st[f].ntrees;
-    mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(part[0], static_cast<double>(fd.n));
-    st[f].ntrees = t + 1;
-    if (t + 1 >= fd.trees) st[f].active = 0;
+  if (threadIdx.x == 0) part[static_cast<int64_t>(f) * max_blocks + blockIdx.x] = red[0];
+}
+__global__ void mse_final_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
+                                 const NodeRec* __restrict__ nodes, const double* __restrict__ part, int max_blocks,
+                                 double* __restrict__ mse, int max_trees) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= gridDim.x * blockDim.x) return;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  if (!round_commits(fd, st[f], nodes)) {
+    st[f].active = 0;  // single leaf of value exactly 0: the reference stops boosting
+    return;
   }
+  double a = 0.0;
+  const int nb = (fd.n + kMseRows - 1) / kMseRows;
+  for (int b = 0; b < nb; ++b) a = fs_add(a, part[static_cast<int64_t>(f) * max_blocks + b]);
+  const int t = st[f].ntrees;
+  mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(a, static_cast<double>(fd.n));
+  st[f].ntrees = t + 1;
+  if (t + 1 >= fd.trees) st[f].active = 0;
 }
 
 }  // namespace
@@ -3097,6 +3118,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   // lives on the device in FamState::ntrees), so it is captured once as a CUDA graph and replayed
   // max_trees times; families that stopped early skip their work inside the kernels.
   const int64_t l0 = dev->launches;
+  const int mse_blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(n_max, kMseRows)));
+  double* mse_part = ar.alloc<double>(static_cast<size_t>(F) * mse_blocks);
   const bool fork_totals = std::getenv("FAMSEER_FORK_TOTALS") != nullptr;
   cudaStream_t aux = fork_totals ? dev->aux_stream() : nullptr;
   auto round_body = [&]() {
@@ -3193,7 +3216,10 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
                                                                                        ord_cur, resid, pred, trees_d);
     }
-    commit_mse_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred, mse_d, max_trees);
+    mse_partial_kernel<<<dim3(static_cast<unsigned>(mse_blocks), F), 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred,
+                                                                              mse_part, mse_blocks);
+    mse_final_kernel<<<F, 1, 0, s>>>(fam_d, st_d, nodes, mse_part, mse_blocks, mse_d, max_trees);
+    dev->count_launch();
     dev->count_launch(2);
     FS_CUDA(cudaGetLastError());
   };
