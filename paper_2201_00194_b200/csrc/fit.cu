@@ -1329,6 +1329,24 @@ struct ExactItem {
 // left count, is one tie class if every window feature orders the node's rows exactly like the
 // lowest one (identical folds, identical reference gains; strict > keeps the lowest feature).
 // Prep queues one order-equivalence check per (node, other window feature).
+// The per-node decision kernels below run a warp per (family, node) with lanes over the
+// node's features (window records read in parallel; ballots replace the serial scans).
+__device__ __forceinline__ int first_flag_feature(const WinRec* w, int nrep, int from, bool need_count1,
+                                                  bool& multi) {
+  // lowest flagged feature >= from; multi = some flagged feature has count != 1 (when asked)
+  const int lane = threadIdx.x & 31;
+  int first = -1;
+  multi = false;
+  for (int j0 = from; j0 < nrep; j0 += 32) {
+    const int j = j0 + lane;
+    const bool fl = j < nrep && w[j].flag;
+    const unsigned m = __ballot_sync(0xffffffffu, fl);
+    if (need_count1 && __any_sync(0xffffffffu, fl && w[j].count != 1)) multi = true;
+    if (m && first < 0) first = j0 + __ffs(m) - 1;
+  }
+  return first;
+}
+
 __global__ void tieclass_prep_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                                      NodeRec* __restrict__ nodes, int level, const WinRec* __restrict__ win,
                                      int nrep_max, int level_slots_max, ExactItem* __restrict__ items,
@@ -1336,28 +1354,104 @@ __global__ void tieclass_prep_kernel(const FamDesc* __restrict__ fam, const FamS
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
-  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int local = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (local >= (1 << level)) return;
   const int s = (1 << level) - 1 + local;
   NodeRec& nd = nodes[fd.node0 + s];
-  nd.eqf0 = -1;
+  if (lane == 0) nd.eqf0 = -1;
   if (nd.state != 0 || nd.build == 0 || nd.wcount < 2) return;
   const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
-  int f0 = -1, lc0 = -1;
-  for (int jj = 0; jj < fd.nrep; ++jj) {
-    if (!w[jj].flag) continue;
-    if (w[jj].count != 1) return;
-    if (f0 < 0) {
-      f0 = jj;
-      lc0 = w[jj].best_lc;
-    } else if (w[jj].best_lc != lc0) {
-      return;
-    }
+  bool multi;
+  const int f0 = first_flag_feature(w, fd.nrep, 0, true, multi);
+  if (multi || f0 < 0 || !(w[f0].best_lo > 0.0)) return;
+  const int lc0 = w[f0].best_lc;
+  bool diff = false;
+  for (int j0 = f0 + 1; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    if (__any_sync(0xffffffffu, j < fd.nrep && w[j].flag && w[j].best_lc != lc0)) diff = true;
   }
-  if (f0 < 0 || !(w[f0].best_lo > 0.0)) return;
-  nd.eqf0 = f0;
-  for (int jj = f0 + 1; jj < fd.nrep; ++jj)
-    if (w[jj].flag) items[atomicAdd(n_items, 1)] = {f, static_cast<int16_t>(s), static_cast<int16_t>(jj)};
+  if (diff) return;
+  if (lane == 0) nd.eqf0 = f0;
+  for (int j0 = f0 + 1; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    const bool fl = j < fd.nrep && w[j].flag;
+    const unsigned m = __ballot_sync(0xffffffffu, fl);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(n_items, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (fl) items[base + __popc(m & ((1u << lane) - 1u))] = {f, static_cast<int16_t>(s), static_cast<int16_t>(j)};
+  }
+}
+
+__global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                              NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
+                              const int32_t* __restrict__ rep_boff, const WinRec* __restrict__ win, int nrep_max,
+                              int level_slots_max, ExactItem* __restrict__ items, int* __restrict__ n_items,
+                              unsigned long long* __restrict__ ctr) {
+  (void)hcnt;
+  (void)rep_boff;
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int lane = threadIdx.x & 31;
+  const int local = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != 0 || nd.build == 0) return;
+  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
+  if (nd.wcount == 0) {  // no candidate can have a positive reference gain
+    if (lane == 0) nd.state = kNodeLeaf;
+    return;
+  }
+  int pick = -1;
+  if (nd.wcount == 1) {
+    bool multi;
+    const int j = first_flag_feature(w, fd.nrep, 0, false, multi);
+    if (j >= 0 && w[j].best_lo > 0.0) pick = j;
+  } else if (nd.eqf0 >= 0) {  // one tie class: the lowest feature wins by strict >
+    bool all = true;
+    for (int j0 = nd.eqf0 + 1; j0 < fd.nrep; j0 += 32) {
+      const int j = j0 + lane;
+      if (__any_sync(0xffffffffu, j < fd.nrep && w[j].flag && !w[j].eq)) all = false;
+    }
+    if (all) pick = nd.eqf0;
+  }
+  if (pick >= 0) {
+    if (lane == 0) {
+      nd.state = kNodeSplit;
+      nd.rep = pick;
+      nd.bin = w[pick].best_bin;
+      nd.gain = w[pick].best_g;
+      nd.lc = w[pick].best_lc;
+      atomicAdd(&const_cast<FamState*>(st)[f].screened, 1ull);
+    }
+    return;
+  }
+  const int tot = nd.pad_ ? 0 : 1;  // node total still to fold (not precomputed by totals_kernel)
+  int k = tot;
+  for (int j0 = 0; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    k += __popc(__ballot_sync(0xffffffffu, j < fd.nrep && w[j].flag));
+  }
+  int base = 0;
+  if (lane == 0) {
+    nd.state = kNodeExact;
+    atomicAdd(&const_cast<FamState*>(st)[f].exact, 1ull);
+    base = atomicAdd(n_items, k);
+    atomicAdd(ctr + kCtrExactChains, static_cast<unsigned long long>(k));
+    atomicAdd(ctr + kCtrExactNodes, 1ull);
+    if (tot) items[base] = {f, static_cast<int16_t>(s), static_cast<int16_t>(-1)};
+  }
+  base = __shfl_sync(0xffffffffu, base, 0) + tot;
+  for (int j0 = 0; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    const bool fl = j < fd.nrep && w[j].flag;
+    const unsigned m = __ballot_sync(0xffffffffu, fl);
+    if (fl) items[base + __popc(m & ((1u << lane) - 1u))] = {f, static_cast<int16_t>(s), static_cast<int16_t>(j)};
+    base += __popc(m);
+  }
 }
 
 // One warp per check: walk the lowest window feature's presorted list restricted to the node;
@@ -1530,61 +1624,6 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
   }
 }
 
-__global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
-                              NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
-                              const int32_t* __restrict__ rep_boff, const WinRec* __restrict__ win, int nrep_max,
-                              int level_slots_max, ExactItem* __restrict__ items, int* __restrict__ n_items,
-                              unsigned long long* __restrict__ ctr) {
-  const int f = blockIdx.y;
-  const FamDesc fd = fam[f];
-  if (!st[f].active) return;
-  const int local = blockIdx.x * blockDim.x + threadIdx.x;
-  if (local >= (1 << level)) return;
-  const int s = (1 << level) - 1 + local;
-  NodeRec& nd = nodes[fd.node0 + s];
-  if (nd.state != 0 || nd.build == 0) return;
-  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
-  if (nd.wcount == 0) {  // no candidate can have a positive reference gain
-    nd.state = kNodeLeaf;
-    return;
-  }
-  int pick = -1;
-  if (nd.wcount == 1) {
-    for (int jj = 0; jj < fd.nrep; ++jj)
-      if (w[jj].flag) {
-        if (w[jj].best_lo > 0.0) pick = jj;
-        break;
-      }
-  } else if (nd.eqf0 >= 0) {  // one tie class: the lowest feature wins by strict >
-    bool all = true;
-    for (int jj = nd.eqf0 + 1; jj < fd.nrep; ++jj)
-      if (w[jj].flag && !w[jj].eq) all = false;
-    if (all) pick = nd.eqf0;
-  }
-  if (pick >= 0) {
-    nd.state = kNodeSplit;
-    nd.rep = pick;
-    nd.bin = w[pick].best_bin;
-    nd.gain = w[pick].best_g;
-    nd.lc = w[pick].best_lc;
-    atomicAdd(&const_cast<FamState*>(st)[f].screened, 1ull);
-    return;
-  }
-  (void)hcnt;
-  (void)rep_boff;
-  nd.state = kNodeExact;
-  atomicAdd(&const_cast<FamState*>(st)[f].exact, 1ull);
-  const int tot = nd.pad_ ? 0 : 1;  // node total still to fold (not precomputed by totals_kernel)
-  int k = tot;
-  for (int jj = 0; jj < fd.nrep; ++jj) k += w[jj].flag;
-  const int base = atomicAdd(n_items, k);
-  atomicAdd(ctr + kCtrExactChains, static_cast<unsigned long long>(k));
-  atomicAdd(ctr + kCtrExactNodes, 1ull);
-  if (tot) items[base] = {f, static_cast<int16_t>(s), static_cast<int16_t>(-1)};
-  int o = tot;
-  for (int jj = 0; jj < fd.nrep; ++jj)
-    if (w[jj].flag) items[base + o++] = {f, static_cast<int16_t>(s), static_cast<int16_t>(jj)};
-}
 
 // sum_residuals (costmodel.cpp:36-40) of v[idx[0..n)) in list order by one warp: four chunks of
 // 32 gathers are in flight at once, then each chunk's values are added in lane order (shuffles
@@ -3178,7 +3217,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                           std::max(nrep_max, 1), level_slots_max, 1);
       }
       FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
-      tieclass_prep_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(
+      tieclass_prep_kernel<<<dim3(grid1(lw, 4, 1 << 20), F), 128, 0, s>>>(  // warp per node
           fam_d, st_d, nodes, level, win, std::max(nrep_max, 1), level_slots_max, items, n_items);
       if (resident.phi_smem > 0)
         tieclass_phi_kernel<CodeT><<<sm * 4, 256, resident.phi_smem, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c,
@@ -3189,7 +3228,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                                              nodeid, win, std::max(nrep_max, 1), level_slots_max);
       dev->count_launch(2);
       FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
-      decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
+      decide_kernel<<<dim3(grid1(lw, 4, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
                                                                      std::max(nrep_max, 1), level_slots_max, items,
                                                                      n_items, dev->ctr_d);
       if (fork_totals) FS_CUDA(cudaStreamWaitEvent(s, dev->ev_join, 0));  // join: totals ready
