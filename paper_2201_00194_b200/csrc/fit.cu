@@ -3334,7 +3334,9 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     fam[f].min_split = params[f].min_samples_split;
     fam[f].lr = params[f].learning_rate;
   }
+  htick("entry");
   FamDesc* fam_d = ar.upload(fam);
+  htick("fam uploaded");
 
   // ---- stage 1: distinct values / codes ---------------------------------------------------
   uint16_t* codes_all = ar.alloc<uint16_t>(static_cast<size_t>(std::max<int64_t>(n_tot, 1)) * std::max(d, 1));
@@ -3345,6 +3347,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   FS_CUDA(cudaMemsetAsync(hash_all, 0, static_cast<size_t>(F) * std::max(d, 1) * sizeof(uint64_t), s));
   int* negz_d = ar.alloc<int>(F);
   FS_CUDA(cudaMemsetAsync(negz_d, 0, F * sizeof(int), s));
+  htick("stage-1 buffers");
   if (d > 0) {
     const size_t smem = 32 * kHashSlots * 8 + 32 * kSmallBins * 8 + 32 * 4 * 2 + 32 * 8;
     ProfScope prof(dev, "fit_distinct");
