@@ -3621,6 +3621,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     raise_deferred(br.run(dev));
   }
   htick("results read");
+  UploadBatch batch;
   for (int f = 0; f < F; ++f) {
     FamilyModel& m = fo->fams[static_cast<size_t>(f)];
     const FamDesc& fd = fam[static_cast<size_t>(f)];
@@ -3669,10 +3670,9 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     }
     m.screened = static_cast<int64_t>(st_h[static_cast<size_t>(f)].screened);
     m.exact = static_cast<int64_t>(st_h[static_cast<size_t>(f)].exact);
-    htick("  family converted");
-    compile_model(dev, m);
-    htick("  family compiled");
+    compile_model(dev, m, &batch);
   }
+  batch.flush(dev);
   htick("models compiled");
 }
 

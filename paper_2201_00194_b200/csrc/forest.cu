@@ -39,13 +39,17 @@ struct BlobPacker {
     host.resize(o + std::max<size_t>(1, v.size()) * sizeof(T), 0);
     if (!v.empty()) std::memcpy(host.data() + o, v.data(), v.size() * sizeof(T));
   }
-  void commit(FamilyModel& m, fs_device* dev) {
+  void commit(FamilyModel& m, fs_device* dev, UploadBatch* batch) {
     if (host.size() > m.blob_cap) {
       if (m.blob_d) FS_CUDA(cudaFree(m.blob_d));
       m.blob_d = nullptr;
       const size_t cap = std::max<size_t>(host.size() + host.size() / 2, 4096);
       FS_CUDA(cudaMalloc(&m.blob_d, cap));
       m.blob_cap = cap;
+    }
+    if (batch) {
+      batch->add(m.blob_d, host.data(), host.size());
+      return;
     }
     // through pinned staging: a truly asynchronous copy (no pageable-staging stream sync)
     void* st = dev->pinned_upload(host.size());
@@ -61,7 +65,25 @@ struct BlobPacker {
 
 }  // namespace
 
-void compile_model(fs_device* dev, FamilyModel& m) {
+void UploadBatch::add(unsigned char* dst, const unsigned char* src, size_t bytes) {
+  const size_t o = (host.size() + 15) & ~size_t(15);
+  host.resize(o + bytes);
+  std::memcpy(host.data() + o, src, bytes);
+  items.push_back({dst, {o, bytes}});
+}
+
+void UploadBatch::flush(fs_device* dev) {
+  if (items.empty()) return;
+  auto* st = static_cast<unsigned char*>(dev->pinned_upload(host.size()));
+  std::memcpy(st, host.data(), host.size());
+  for (const auto& it : items)
+    FS_CUDA(cudaMemcpyAsync(it.first, st + it.second.first, it.second.second, cudaMemcpyHostToDevice, dev->stream));
+  dev->upload_done();
+  items.clear();
+  host.clear();
+}
+
+void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch) {
   m.compiled = false;
   const int T = m.num_trees();
   m.n_trees = T;
@@ -100,7 +122,7 @@ void compile_model(fs_device* dev, FamilyModel& m) {
     pk.add(m.left);
     pk.add(m.right);
     pk.add(m.value);
-    pk.commit(m, dev);
+    pk.commit(m, dev, batch);
     m.g_off_d = pk.at<int32_t>(m, 0);
     m.g_feat_d = pk.at<int32_t>(m, 1);
     m.g_thr_d = pk.at<double>(m, 2);
@@ -112,20 +134,28 @@ void compile_model(fs_device* dev, FamilyModel& m) {
     return;
   }
 
-  // Unique thresholds per feature (== equality, so -0.0 and +0.0 share a rank).
-  std::vector<std::vector<double>> uq(static_cast<size_t>(dmodel));
+  // Unique thresholds per feature (== equality, so -0.0 and +0.0 share a rank): one sort of all
+  // (feature, threshold) pairs, then per-feature slices.
+  std::vector<std::pair<int, double>> ft;
+  ft.reserve(m.feature.size());
   for (size_t g = 0; g < m.feature.size(); ++g)
-    if (m.feature[g] >= 0) uq[static_cast<size_t>(m.feature[g])].push_back(m.threshold[g]);
-  size_t max_u = 0;
+    if (m.feature[g] >= 0) ft.push_back({m.feature[g], m.threshold[g]});
+  std::sort(ft.begin(), ft.end(), [](const std::pair<int, double>& a, const std::pair<int, double>& b) {
+    return a.first != b.first ? a.first < b.first : a.second < b.second;
+  });
   std::vector<int32_t> uoff(static_cast<size_t>(dmodel) + 1, 0);
   std::vector<double> uthr;
-  for (int f = 0; f < dmodel; ++f) {
-    auto& u = uq[static_cast<size_t>(f)];
-    std::sort(u.begin(), u.end());
-    u.erase(std::unique(u.begin(), u.end(), [](double a, double b) { return a == b; }), u.end());
-    uoff[static_cast<size_t>(f)] = static_cast<int32_t>(uthr.size());
-    uthr.insert(uthr.end(), u.begin(), u.end());
-    max_u = std::max(max_u, u.size());
+  uthr.reserve(ft.size());
+  size_t max_u = 0;
+  {
+    size_t i = 0;
+    for (int f = 0; f < dmodel; ++f) {
+      uoff[static_cast<size_t>(f)] = static_cast<int32_t>(uthr.size());
+      const size_t start = uthr.size();
+      for (; i < ft.size() && ft[i].first == f; ++i)
+        if (uthr.size() == start || !(uthr.back() == ft[i].second)) uthr.push_back(ft[i].second);
+      max_u = std::max(max_u, uthr.size() - start);
+    }
   }
   uoff[static_cast<size_t>(dmodel)] = static_cast<int32_t>(uthr.size());
   if (max_u > 65534) fail(FS_EINVAL, "forest: more than 65534 distinct thresholds on one feature");
@@ -160,8 +190,9 @@ void compile_model(fs_device* dev, FamilyModel& m) {
         li = ri = c.idx;
       } else {
         const int f = m.feature[g];
-        const auto& u = uq[static_cast<size_t>(f)];
-        const auto rank = static_cast<uint32_t>(std::lower_bound(u.begin(), u.end(), m.threshold[g]) - u.begin());
+        const double* u0 = uthr.data() + uoff[static_cast<size_t>(f)];
+        const double* u1 = uthr.data() + uoff[static_cast<size_t>(f) + 1];
+        const auto rank = static_cast<uint32_t>(std::lower_bound(u0, u1, m.threshold[g]) - u0);
         node = static_cast<uint32_t>(f) | (rank << 16);
         li = m.left[g];
         ri = m.right[g];
@@ -177,7 +208,7 @@ void compile_model(fs_device* dev, FamilyModel& m) {
   pk.add(leafid);
   pk.add(uthr);
   pk.add(uoff);
-  pk.commit(m, dev);
+  pk.commit(m, dev, batch);
   m.nodes_d = pk.at<uint32_t>(m, 0);
   m.leafv_d = pk.at<double>(m, 1);
   m.leafid_d = pk.at<uint8_t>(m, 2);

@@ -57,9 +57,17 @@ struct FamilyModel {
   void release_device();
 };
 
+// Host->device copies of several compiled models gathered into one pinned staging pass.
+struct UploadBatch {
+  std::vector<unsigned char> host;
+  std::vector<std::pair<unsigned char*, std::pair<size_t, size_t>>> items;  // dst, (offset, bytes)
+  void add(unsigned char* dst, const unsigned char* src, size_t bytes);
+  void flush(fs_device* dev);  // one pinned staging fill, async copies, no host wait
+};
+
 // Build the compiled device form from the pre-order arrays (host transformation of the tree
-// table; O(nodes)).
-void compile_model(fs_device* dev, FamilyModel& m);
+// table; O(nodes)). With a batch, the device copy is deferred to batch->flush().
+void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch = nullptr);
 
 }  // namespace fs
 
