@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfamseer.so")
+# FAMSEER_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("FAMSEER_LIB") or os.path.join(HERE, "libfamseer.so")
 
 FS_OK, FS_EINVAL, FS_EDOMAIN, FS_ERANGE, FS_ECUDA, FS_ENOMEM, FS_ENCCL = range(7)
 FS_MAX_KNOBS = 16

@@ -2142,12 +2142,25 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   __shared__ int s_neq;
   // phase timers (CTA 0, thread 0): where a round's cycles go (fs_device_counters [4..15])
   __shared__ long long s_ph[12];
+  // Phase clock: __syncthreads() is BAR.SYNC.DEFER_BLOCKING - a warp only blocks at the first
+  // dependent instruction after it - so a bare clock read right after a barrier would bill the
+  // barrier wait to the NEXT phase. The read takes a register input loaded from shared memory
+  // after the barrier (the load cannot complete before the barrier does); memory clobber keeps
+  // the compiler from moving work across it.
+  __shared__ int s_clkdep;
+  auto clk = [&]() {
+    long long t;
+    const int dep = *reinterpret_cast<volatile int*>(&s_clkdep);
+    asm volatile("add.s32 %1, %1, 0;\n\tmov.u64 %0, %%clock64;" : "=l"(t) : "r"(dep) : "memory");
+    return t;
+  };
+  if (threadIdx.x == 0) s_clkdep = 0;
   long long t_prev = clock64();
   if (threadIdx.x < 12) s_ph[threadIdx.x] = 0;
 #define RES_PHASE(i)                        \
   do {                                      \
     if (tid == 0) {                         \
-      const long long t_ = clock64();       \
+      const long long t_ = clk();           \
       s_ph[i] += t_ - t_prev;               \
       t_prev = t_;                          \
     }                                       \
