@@ -1998,6 +1998,15 @@ namespace {
 constexpr int kResThreads = FS_RES_THREADS;
 constexpr int kResWarps = kResThreads / 32;
 constexpr int kPartE = 4;  // partition: consecutive order-0 entries per thread per chunk
+// Resident histogram precision: FS_RES_LIMBS 3 = the multi-kernel's 62-bit fixed point (three
+// 21-bit limbs per update); 2 = 39-bit fixed point (n * max|v| < 2^39, two limbs per update -
+// a third fewer shared atomics; the screen bound widens with the quantum, so near-ties are
+// re-evaluated exactly as before).
+#ifndef FS_RES_LIMBS
+#define FS_RES_LIMBS 3
+#endif
+constexpr int kResLimbs = FS_RES_LIMBS;
+constexpr int kResBias = kResLimbs == 3 ? 62 : 40;  // u = v + 2^bias, count = round(U / 2^bias)
 constexpr int kResMaxDepth = 7;  // node ids fit in uint8
 
 struct ResNode {
@@ -2238,7 +2247,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     if (tid == 0) {
       unsigned long long m = 0;
       for (int w = 0; w < kResThreads / 32; ++w) m = max(m, s_red[w]);
-      s_shift = fix_shift(m, n);
+      s_shift = kResLimbs == 3 ? fix_shift(m, n) : fix_shift(m, n) - 22;  // n*|v| < 2^61 resp. 2^39
     }
     __syncthreads();
     const int shift = s_shift;
@@ -2308,18 +2317,18 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                 for (int q = sub0 + warp * rpw + hm; q < q_end; q += kResWarps * rpw) {
                   const int p = rows[q];
                   const long long v = s_fix[p];
-                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << kResBias);
                   uint32_t* c = colp + hcode[p] * 32;
                   atomicAdd(c, static_cast<uint32_t>(u) & kLimbMask);
                   atomicAdd(c + colh * 32, static_cast<uint32_t>(u >> 21) & kLimbMask);
-                  atomicAdd(c + 2 * colh * 32, static_cast<uint32_t>(u >> 42));
+                  if (kResLimbs == 3) atomicAdd(c + 2 * colh * 32, static_cast<uint32_t>(u >> 42));
                   if (hj == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
                 }
               } else {
                 for (int q = sub0 + warp; q < q_end; q += kResWarps) {
                   const int p = rows[q];
                   const long long v = s_fix[p];
-                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << kResBias);
                   const uint32_t l0 = static_cast<uint32_t>(u) & kLimbMask;
                   const uint32_t l1 = static_cast<uint32_t>(u >> 21) & kLimbMask;
                   const uint32_t l2 = static_cast<uint32_t>(u >> 42);
@@ -2327,7 +2336,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                     uint32_t* c = s_limb + lane + (s_cofs[j] + s_codes[static_cast<size_t>(j) * cs + p]) * 32;
                     atomicAdd(c, l0);
                     atomicAdd(c + colh * 32, l1);
-                    atomicAdd(c + 2 * colh * 32, l2);
+                    if (kResLimbs == 3) atomicAdd(c + 2 * colh * 32, l2);
                   }
                   if (lane == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
                 }
@@ -2355,8 +2364,10 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                 U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
                     (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
               }
-              const uint64_t cnt = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
-              const long long hv = static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << 62)));
+              const uint64_t cnt =
+                  static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << (kResBias - 1))) >> kResBias);
+              const long long hv =
+                  static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << kResBias)));
               hk[i] = (sub0 == 0 ? 0ll : hk[i]) + hv;
               ck[i] = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
             }
