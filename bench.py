@@ -152,6 +152,30 @@ def build_workload(cfg_name, seed):
     return W
 
 
+def shard_workload(W, rank, world):
+    """This rank's families of a global workload (deterministic LPT on rows*T + pool*T,
+    paper_2201_00194_b200/sharding.py); records the global unit counts for whole-job rates."""
+    from paper_2201_00194_b200 import sharding
+
+    F = len(W["families"])
+    ps, ts = W["pool_seg"], W["tr_seg"]
+    costs = [sharding.family_cost(int(ts[f + 1] - ts[f]), int(ps[f + 1] - ps[f]), W["trees"]) for f in range(F)]
+    owner = sharding.assign_families(costs, world)
+    mine = [f for f in range(F) if owner[f] == rank]
+    out = dict(W)
+    for key_so, key_a, key_seg in (("pool_so", "pool_a", "pool_seg"), ("tr_so", "tr_a", "tr_seg")):
+        seg = W[key_seg]
+        idx = np.concatenate([np.arange(seg[f], seg[f + 1]) for f in mine]) if mine else np.zeros(0, np.int64)
+        out[key_so], out[key_a] = W[key_so][idx], W[key_a][idx]
+        out[key_seg] = np.concatenate([[0], np.cumsum([seg[f + 1] - seg[f] for f in mine])]).astype(np.int64)
+        if key_seg == "tr_seg":
+            out["tr_y"] = W["tr_y"][idx]
+    out["families"] = [W["families"][f] for f in mine]
+    out["family_ids"] = mine
+    out["P_global"], out["N_global"] = int(ps[-1]), int(ts[-1])
+    return out
+
+
 # ------------------------------------------------------------------------------------------
 # clocks (sampled during the timed region)
 # ------------------------------------------------------------------------------------------
@@ -239,7 +263,12 @@ def run_native(args, rank, world, local_rank):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    W = build_workload(args.config, seed=1000 + rank)
+    if args.shard == "families":
+        # strong scaling: ONE global workload, families LPT-partitioned over ranks
+        W = shard_workload(build_workload(args.config, seed=1000), rank, world)
+    else:
+        # weak scaling: every rank tunes its own copy of the workload (own seed)
+        W = build_workload(args.config, seed=1000 + rank)
     dev = fs.Device(local_rank)
     stream = torch.cuda.ExternalStream(dev.stream)
     spaces = fs.Spaces(dev, W["spaces"])
@@ -248,6 +277,9 @@ def run_native(args, rank, world, local_rank):
     params = fs.GbtParams(W["trees"], 3, 0.1, 2)
     P = int(W["pool_seg"][-1])
     N = int(W["tr_seg"][-1])
+    # whole-job units per step: all ranks' work (the global workload when families are sharded)
+    P_job = W.get("P_global", P * world)
+    N_job = W.get("N_global", N * world)
     with torch.cuda.stream(stream):
         pool_so = torch.from_numpy(W["pool_so"]).cuda()
         pool_a = torch.from_numpy(W["pool_a"]).cuda()
@@ -264,7 +296,8 @@ def run_native(args, rank, world, local_rank):
     forest.fit_d(x_tr, y_tr, W["tr_seg"], params)  # model the first round scores with
     dev.check()
     pool_seg, tr_seg = W["pool_seg"], W["tr_seg"]
-    fam_base = rank * F
+    fam_base = rank * F if args.shard != "families" else 0
+    fam_ids = W.get("family_ids", list(range(F)))
 
     def topk_allgather():
         # per-family top-g records {family, pool index, score}; the only collective (NCCL)
@@ -273,7 +306,7 @@ def run_native(args, rank, world, local_rank):
             a, b = int(pool_seg[f]), int(pool_seg[f + 1])
             k = min(G_TOP, b - a)
             p = perm[a:a + k].long() + a
-            rec = torch.stack([torch.full((k,), fam_base + f, dtype=torch.float64, device="cuda"),
+            rec = torch.stack([torch.full((k,), fam_base + fam_ids[f], dtype=torch.float64, device="cuda"),
                                p.double(), scores[p]], 1)
             if k < G_TOP:
                 rec = torch.cat([rec, torch.full((G_TOP - k, 3), -1.0, dtype=torch.float64, device="cuda")])
@@ -385,9 +418,9 @@ def run_native(args, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_total = float(t.item())
         h2d = h_so.nbytes + h_a.nbytes + h_x.nbytes + h_y.nbytes
-        e2e = {"value": P * world * args.steps / (e_total / 1e3), "unit": "candidates/s",
+        e2e = {"value": P_job * args.steps / (e_total / 1e3), "unit": "candidates/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
-               "train_rows_per_s": N * world * args.steps / (e_total / 1e3), "ms_per_step": e_total / args.steps,
+               "train_rows_per_s": N_job * args.steps / (e_total / 1e3), "ms_per_step": e_total / args.steps,
                "api": "fs_score + fs_fit + fs_forest_export (host pointers)"}
 
     # ---- roofline of the dominant kernel (from the per-kernel replica step) ----
@@ -426,26 +459,27 @@ def run_native(args, rank, world, local_rank):
 
     result = {
         "metric": METRIC,
-        "value": P * world * args.steps / (total_ms / 1e3),
+        "value": P_job * args.steps / (total_ms / 1e3),
         "unit": "candidates/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.shard == "families" else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (random candidates from the model's knob spaces, quadratic-bowl latencies)",
         "config": {"workload": W["desc"], "config": args.config, "model": W["model"], "families": W["families"],
-                   "candidates_per_step": P * world, "train_rows_per_step": N * world, "trees": W["trees"],
-                   "depth": 3, "pad_dim": PAD, "parallelism": f"family-sharded x{world}",
+                   "candidates_per_step": P_job, "train_rows_per_step": N_job, "trees": W["trees"],
+                   "depth": 3, "pad_dim": PAD, "parallelism": (f"families LPT-sharded over {world} GPU(s)" if args.shard == "families" else
+                                   f"family-parallel replicas x{world}"),
                    "l2": "flushed between timed steps (256 MB write)"},
-        "train_rows_per_s": N * world * args.steps / (total_ms / 1e3),
-        "train_row_rounds_per_s": N * world * W["trees"] * args.steps / (total_ms / 1e3),
+        "train_rows_per_s": N_job * args.steps / (total_ms / 1e3),
+        "train_row_rounds_per_s": N_job * W["trees"] * args.steps / (total_ms / 1e3),
         "phases_ms": {"score": score_ms, "fit": fit_ms},
         "scored_per_s_score_only": P * world / (score_ms / 1e3),
-        "fit_rows_per_s_fit_only": N * world / (fit_ms / 1e3),
+        "fit_rows_per_s_fit_only": N_job / (fit_ms / 1e3),
         "fit_nodes": {"screened": int(sum(a for a, _ in fit_stats)), "exact": int(sum(b for _, b in fit_stats))},
         "kernel_ms_one_step": breakdown,
         "kernel_ms_timed_region": timed_kernel_ms,
@@ -662,6 +696,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--shard", default="replicate", choices=["replicate", "families"],
+                    help="replicate: every rank tunes its own workload copy (weak scaling); families: one "
+                         "global workload, families LPT-partitioned over ranks (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -86,3 +86,25 @@ def test_gloo_world2_topk_allgather_matches_single_process():
         assert list(merged) == list(single)
         for f, recs in merged.items():
             assert np.array_equal(np.array(recs), single[f]), (rank, f)
+
+
+def test_bench_family_sharding_covers_global_workload():
+    """bench.py --shard families: every family lands on exactly one rank, rows/pools intact."""
+    import bench
+
+    W = bench.build_workload("c2", 1000)
+    for world in (1, 2, 4, 8):
+        seen, rows, pool = [], 0, 0
+        for r in range(world):
+            S = bench.shard_workload(W, r, world)
+            seen += S["family_ids"]
+            rows += int(S["tr_seg"][-1])
+            pool += int(S["pool_seg"][-1])
+            assert S["P_global"] == int(W["pool_seg"][-1]) and S["N_global"] == int(W["tr_seg"][-1])
+            for i, f in enumerate(S["family_ids"]):
+                a, b = int(W["tr_seg"][f]), int(W["tr_seg"][f + 1])
+                sa, sb = int(S["tr_seg"][i]), int(S["tr_seg"][i + 1])
+                assert np.array_equal(S["tr_a"][sa:sb], W["tr_a"][a:b])
+                assert np.array_equal(S["tr_y"][sa:sb], W["tr_y"][a:b])
+        assert sorted(seen) == list(range(len(W["families"])))
+        assert rows == int(W["tr_seg"][-1]) and pool == int(W["pool_seg"][-1])
