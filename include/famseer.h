@@ -146,6 +146,12 @@ int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t
  * FS_EINVAL for m < 2, FS_EDOMAIN when every pair is excluded. */
 int fs_pairwise_accuracy(fs_device* dev, int64_t m, const double* scores, const double* latency,
                          double* out);
+/* Batched form (the heatmap's n x n model/validation-set grid,
+ * experiment.cpp:135-167): out[k] = pairwise accuracy of segment k = [seg[k], seg[k+1]) of
+ * scores/latency, one launch for all segments. FS_EINVAL if a segment holds < 2 records,
+ * FS_EDOMAIN if a segment excludes every pair (fs_last_error names the first such segment). */
+int fs_pairwise_accuracy_batch(fs_device* dev, int32_t n_segments, const int64_t* seg, const double* scores,
+                               const double* latency, double* out);
 
 /* ---- fit (costmodel.cpp:152-222; train_cost_model :224-235 appends log-latency rows first) ---
  * Refit family f's ensemble from scratch on rows [seg[f], seg[f+1]) of x/target with params[f].

@@ -173,6 +173,17 @@ class Device:
         _check(_lib().fs_pairwise_accuracy(self.h, len(s), _p(s, _capi._dp), _p(lat, _capi._dp), C.byref(out)))
         return out.value
 
+    def pairwise_accuracy_batch(self, scores, latency, seg) -> np.ndarray:
+        """Per-segment pairwise accuracy in one launch (the accuracy heatmap's model x
+        validation-set grid, experiment.cpp:135-167)."""
+        s = np.ascontiguousarray(scores, np.float64)
+        lat = np.ascontiguousarray(latency, np.float64)
+        sg, sp = _seg(seg)
+        out = np.zeros(len(sg) - 1)
+        _check(_lib().fs_pairwise_accuracy_batch(self.h, len(sg) - 1, sp, _p(s, _capi._dp), _p(lat, _capi._dp),
+                                                  _p(out, _capi._dp)))
+        return out
+
     def rank_d(self, scores_t, seg, perm_t):
         sg, sp = _seg(seg)
         _check(_lib().fs_rank_d(self.h, len(sg) - 1, sp, scores_t.data_ptr(), perm_t.data_ptr()))

@@ -3,6 +3,8 @@
 // (costmodel.cpp:237-246), then rank each family's pool by (score, index). The feature matrix
 // lives only in device scratch.
 #include <algorithm>
+#include <string>
+#include <vector>
 #include <cstdlib>
 
 #include "forest.cuh"
@@ -66,9 +68,81 @@ __global__ void pair_count_kernel(const double* __restrict__ s, const double* __
   }
 }
 
+// Batched pair counts: blockIdx.y = segment, counts in half units per segment (exact integers,
+// order-independent).
+__global__ void pair_count_seg_kernel(const double* __restrict__ s, const double* __restrict__ lat,
+                                      const int64_t* __restrict__ seg, unsigned long long* __restrict__ acc) {
+  const int k = blockIdx.y;
+  const int64_t a = seg[k], m = seg[k + 1] - seg[k];
+  unsigned long long half = 0, counted = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double li = lat[a + i], si = s[a + i];
+    for (int64_t j = i + 1; j < m; ++j) {
+      const double lj = lat[a + j];
+      const double rel = fs_div(fabs(fs_sub(li, lj)), li < lj ? lj : li);
+      if (rel < 1e-6) continue;
+      ++counted;
+      const double sj = s[a + j];
+      if (si == sj) half += 1;
+      else if ((si < sj) == (li < lj)) half += 2;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    half += __shfl_down_sync(0xffffffffu, half, o);
+    counted += __shfl_down_sync(0xffffffffu, counted, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc + 2 * k, half);
+    atomicAdd(acc + 2 * k + 1, counted);
+  }
+}
+
 }  // namespace fs
 
 extern "C" {
+
+int fs_pairwise_accuracy_batch(fs_device* dev, int32_t nseg, const int64_t* seg, const double* scores,
+                               const double* latency, double* out) {
+  return fs::guard([&] {
+    if (!dev || !out || nseg < 0 || (nseg > 0 && (!seg || !scores || !latency)))
+      fs::fail(FS_EINVAL, "fs_pairwise_accuracy_batch: bad arguments");
+    if (nseg == 0) return;
+    if (seg[0] != 0) fs::fail(FS_EINVAL, "fs_pairwise_accuracy_batch: seg[0] must be 0");
+    int64_t mmax = 0;
+    for (int k = 0; k < nseg; ++k) {
+      const int64_t m = seg[k + 1] - seg[k];
+      if (m < 2)
+        fs::fail(FS_EINVAL, "pairwise_accuracy: segment " + std::to_string(k) + " has fewer than two records");
+      mmax = std::max(mmax, m);
+    }
+    dev->activate();
+    const int64_t n = seg[nseg];
+    auto* buf = static_cast<unsigned char*>(
+        dev->scratch(fs::kSlotH2D0, static_cast<size_t>(n) * 16 + static_cast<size_t>(nseg + 1) * 8 + nseg * 16 + 64));
+    auto* sd = reinterpret_cast<double*>(buf);
+    auto* ld = sd + n;
+    auto* segd = reinterpret_cast<int64_t*>(ld + n);
+    auto* acc = reinterpret_cast<unsigned long long*>(segd + nseg + 1);
+    FS_CUDA(cudaMemcpyAsync(sd, scores, n * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    FS_CUDA(cudaMemcpyAsync(ld, latency, n * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    FS_CUDA(cudaMemcpyAsync(segd, seg, (nseg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, dev->stream));
+    FS_CUDA(cudaMemsetAsync(acc, 0, 2 * nseg * sizeof(unsigned long long), dev->stream));
+    const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(fs::ceil_div(mmax, 256), 64)));
+    fs::pair_count_seg_kernel<<<dim3(gx, static_cast<unsigned>(nseg)), 256, 0, dev->stream>>>(sd, ld, segd, acc);
+    dev->count_launch();
+    FS_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> h(2 * static_cast<size_t>(nseg));
+    FS_CUDA(cudaMemcpyAsync(h.data(), acc, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, dev->stream));
+    FS_CUDA(cudaStreamSynchronize(dev->stream));
+    for (int k = 0; k < nseg; ++k) {
+      if (h[2 * k + 1] == 0)
+        fs::fail(FS_EDOMAIN, "pairwise_accuracy: segment " + std::to_string(k) + ": all validation pairs excluded as ties");
+      out[k] = (static_cast<double>(h[2 * k]) * 0.5) / static_cast<double>(h[2 * k + 1]);
+    }
+  });
+}
+
 
 int fs_pairwise_accuracy(fs_device* dev, int64_t m, const double* scores, const double* latency, double* out) {
   return fs::guard([&] {
