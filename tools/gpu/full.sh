@@ -10,5 +10,7 @@ timeout 900 python bench.py --config c4 --steps 3 --warmup 3 > gpurun_out/bench_
 timeout 1800 python bench.py --config c5 --steps 3 --warmup 3 --no-e2e > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo c5=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
 bash tools/gpu/prof_resident.sh
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:hist_build_atomic -c 1 -f -o gpurun_out/prof_hist_c4 python tools/fit_once.py c4 5 > gpurun_out/ncu_hist.log 2>&1; echo ncu3=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:hist_build_atomic -c 1 -f -o gpurun_out/prof_hist_c5 python tools/fit_once.py c5 2 > gpurun_out/ncu_hist.log 2>&1; echo ncu3=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:predict_heap -c 1 -f -o gpurun_out/prof_score_c2 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_score.log 2>&1; echo ncu4=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4_fit.csv python tools/fit_once.py c4 20 > /dev/null 2>&1; echo ncu5=$?
 timeout 600 python tools/roofline_probe.py --families 8 --rows 65536 --trees 1000 > gpurun_out/roofline_probe.json 2> gpurun_out/roofline_probe.err; echo probe=$?
