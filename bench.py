@@ -385,20 +385,21 @@ def run_native(args, rank, world, local_rank):
     # ---- e2e: host buffers through the C ABI, copies inside the timed region ----
     e2e = None
     if not args.no_e2e:
-        h_so = W["pool_so"]
-        h_a = np.ascontiguousarray(W["pool_a"])
-        h_x = x_tr.cpu().numpy()
-        h_y = W["tr_y"]
-        try:  # pinned host staging, as a production caller would hold it
-            h_x_t = torch.from_numpy(h_x).pin_memory()
-            h_x = h_x_t.numpy()
-        except Exception:
-            pass
+        def pinned(a):  # pinned host staging, as a production caller would hold it
+            try:
+                return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+            except Exception:
+                return np.ascontiguousarray(a)
+
+        h_so, h_a = pinned(W["pool_so"]), pinned(W["pool_a"])
+        # training rows travel as measurement records (candidate descriptor + log latency); their
+        # features are computed on the device (fs_fit_records, simbackend.cpp:185)
+        h_tso, h_ta, h_y = pinned(W["tr_so"]), pinned(W["tr_a"]), pinned(W["tr_y"])
         d2h = [0]
 
         def e2e_step():
             s_h, p_h = spaces.score(forest, h_so, h_a, PAD, pool_seg)
-            forest.fit(h_x, h_y, seg=tr_seg, params=params)
+            forest.fit_records(spaces, h_tso, h_ta, PAD, h_y, seg=tr_seg, params=params)
             nbytes = s_h.nbytes + p_h.nbytes
             for f in range(F):
                 e = forest.export(f)
@@ -417,11 +418,11 @@ def run_native(args, rank, world, local_rank):
             t = torch.tensor([e_total], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_total = float(t.item())
-        h2d = h_so.nbytes + h_a.nbytes + h_x.nbytes + h_y.nbytes
+        h2d = h_so.nbytes + h_a.nbytes + h_tso.nbytes + h_ta.nbytes + h_y.nbytes
         e2e = {"value": P_job * args.steps / (e_total / 1e3), "unit": "candidates/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
                "train_rows_per_s": N_job * args.steps / (e_total / 1e3), "ms_per_step": e_total / args.steps,
-               "api": "fs_score + fs_fit + fs_forest_export (host pointers)"}
+               "api": "fs_score + fs_fit_records + fs_forest_export (host pointers)"}
 
     # ---- roofline of the dominant kernel (from the per-kernel replica step) ----
     peak, peak_kind = measured_peak_hbm()

@@ -163,6 +163,18 @@ int fs_fit(fs_device* dev, fs_forest* fo, int32_t n_segments, const int64_t* seg
 int fs_fit_d(fs_device* dev, fs_forest* fo, int32_t n_segments, const int64_t* seg_h, int32_t d,
              const double* x_d, const double* target_d, const fs_gbt_params* params);
 
+/* fit from measurement records (MeasurementRecord: candidate + log latency, searchspace.hpp:52-57):
+ * each record's features are featurize(space_of[i], assign[i], pad_dim) computed on the device
+ * (the reference featurizes them at measurement time, simbackend.cpp:185) - the host sends 68
+ * bytes per record instead of pad_dim*8. target[i] = log(latency_ms) as the caller computes it
+ * (costmodel.cpp:228-233). Otherwise identical to fs_fit. */
+int fs_fit_records(fs_device* dev, fs_forest* fo, const fs_spaces* sp, int32_t n_segments, const int64_t* seg,
+                   const int32_t* space_of, const int32_t* assign, int32_t pad_dim, const double* target,
+                   const fs_gbt_params* params);
+int fs_fit_records_d(fs_device* dev, fs_forest* fo, const fs_spaces* sp, int32_t n_segments,
+                     const int64_t* seg_h, const int32_t* space_of_d, const int32_t* assign_d, int32_t pad_dim,
+                     const double* target_d, const fs_gbt_params* params);
+
 /* Fit diagnostics of the last fs_fit on this forest family: internal nodes resolved by the
  * histogram screen alone / by exact reference-order re-evaluation of the tie window. */
 int fs_forest_fit_stats(const fs_forest* fo, int32_t family, int64_t* screened,

@@ -355,6 +355,29 @@ class Forest:
         pa = _params_array(params, nf)
         _check(_lib().fs_fit_d(self.dev.h, self.h, nf, sp, x_t.shape[1], x_t.data_ptr(), target_t.data_ptr(), pa))
 
+    def fit_records(self, spaces: "Spaces", space_of, assign, pad_dim: int, target, seg=None, params=None):
+        """Refit from measurement records (candidate descriptors + log latency): features are
+        computed on the device (simbackend.cpp:185), the host sends 68 B per record."""
+        so = np.ascontiguousarray(space_of, np.int32)
+        a = np.ascontiguousarray(assign, np.int32)
+        if a.ndim != 2 or a.shape[1] != 16:
+            raise InvalidArgument("assign must be [n][16] value indices")
+        y = np.ascontiguousarray(target, np.float64)
+        if seg is None:
+            seg = [0, len(so)]
+        sg, sp = _seg(seg)
+        nf = len(sg) - 1
+        pa = _params_array(params, nf)
+        _check(_lib().fs_fit_records(self.dev.h, self.h, spaces.h, nf, sp, _p(so, _capi._i32p), _p(a, _capi._i32p),
+                                     pad_dim, _p(y, _capi._dp), pa))
+
+    def fit_records_d(self, spaces: "Spaces", space_of_t, assign_t, pad_dim: int, target_t, seg, params=None):
+        sg, sp = _seg(seg)
+        nf = len(sg) - 1
+        pa = _params_array(params, nf)
+        _check(_lib().fs_fit_records_d(self.dev.h, self.h, spaces.h, nf, sp, space_of_t.data_ptr(),
+                                       assign_t.data_ptr(), pad_dim, target_t.data_ptr(), pa))
+
     def fit_stats(self, family: int):
         a, b = C.c_int64(), C.c_int64()
         _check(_lib().fs_forest_fit_stats(self.h, family, C.byref(a), C.byref(b)))

@@ -45,6 +45,10 @@ SIGNATURES = [
     ("fs_device_profile_names", C.c_int64, [_vp, C.c_char_p, C.c_int64]),
     ("fs_pairwise_accuracy", C.c_int, [_vp, C.c_int64, _dp, _dp, _dp]),
     ("fs_pairwise_accuracy_batch", C.c_int, [_vp, C.c_int32, _i64p, _dp, _dp, _dp]),
+    ("fs_fit_records", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _i32p, C.c_int32, _dp,
+                                 C.POINTER(GbtParams)]),
+    ("fs_fit_records_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp,
+                                   C.POINTER(GbtParams)]),
     ("fs_score", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _i32p, C.c_int32, _dp, _i32p]),
     ("fs_score_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp]),
     ("fs_feature_dim", C.c_int, [C.c_int32]),

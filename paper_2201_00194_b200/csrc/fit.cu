@@ -22,6 +22,11 @@
 #include "fit.cuh"
 
 namespace fs {
+void launch_featurize(fs_device* dev, const fs_spaces* sp, int64_t n, const int32_t* space_of_d,
+                      const int32_t* assign_d, int32_t pad, double* out_d);
+}  // namespace fs
+
+namespace fs {
 namespace fit {
 namespace {
 
@@ -3725,6 +3730,52 @@ int fs_fit(fs_device* dev, fs_forest* fo, int32_t nseg, const int64_t* seg, int3
     if (n * d) FS_CUDA(cudaMemcpyAsync(xd, x, n * d * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
     if (n) FS_CUDA(cudaMemcpyAsync(yd, target, n * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
     fs::fit::fit_families(dev, fo, nseg, seg, d, xd, yd, params);
+  });
+}
+
+int fs_fit_records_d(fs_device* dev, fs_forest* fo, const fs_spaces* sp, int32_t nseg, const int64_t* seg,
+                     const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, const double* target_d,
+                     const fs_gbt_params* params) {
+  return fs::guard([&] {
+    if (!dev || !fo || !sp || nseg < 0 || !seg || pad < 0 || !params)
+      fs::fail(FS_EINVAL, "fs_fit_records: bad arguments");
+    dev->activate();
+    const int64_t n = seg[nseg];
+    auto* xd = static_cast<double*>(dev->scratch(fs::kSlotFitX, std::max<int64_t>(n * pad, 1) * sizeof(double)));
+    fs::launch_featurize(dev, sp, n, space_of_d, assign_d, pad, xd);
+    fs::fit::fit_families(dev, fo, nseg, seg, pad, xd, target_d, params);
+  });
+}
+
+int fs_fit_records(fs_device* dev, fs_forest* fo, const fs_spaces* sp, int32_t nseg, const int64_t* seg,
+                   const int32_t* space_of, const int32_t* assign, int32_t pad, const double* target,
+                   const fs_gbt_params* params) {
+  return fs::guard([&] {
+    if (!dev || !fo || !sp || nseg < 0 || !seg || pad < 0 || !params)
+      fs::fail(FS_EINVAL, "fs_fit_records: bad arguments");
+    dev->activate();
+    const int64_t n = seg[nseg];
+    // the reference validates every record's dimension on the host (searchspace.cpp:94-101)
+    for (int64_t i = 0; i < n; ++i) {
+      const int s = space_of[i];
+      if (s < 0 || s >= sp->n) fs::fail(FS_EINVAL, "fit_records: unknown space id");
+      if (pad < fs_feature_dim(sp->k_h[static_cast<size_t>(s)])) fs::fail(FS_EINVAL, "fit_records: pad_dim too small");
+    }
+    const size_t b_so = static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(int32_t);
+    const size_t b_a = static_cast<size_t>(std::max<int64_t>(n, 1)) * FS_MAX_KNOBS * sizeof(int32_t);
+    const size_t b_t = static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(double);
+    auto* in = static_cast<unsigned char*>(dev->scratch(fs::kSlotFitIn, b_t + b_so + b_a + 32));
+    auto* td = reinterpret_cast<double*>(in);
+    auto* sd = reinterpret_cast<int32_t*>(in + b_t);
+    auto* ad = reinterpret_cast<int32_t*>(in + b_t + b_so);
+    if (n) {
+      FS_CUDA(cudaMemcpyAsync(td, target, n * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+      FS_CUDA(cudaMemcpyAsync(sd, space_of, n * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
+      FS_CUDA(cudaMemcpyAsync(ad, assign, n * FS_MAX_KNOBS * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
+    }
+    auto* xd = static_cast<double*>(dev->scratch(fs::kSlotFitX, std::max<int64_t>(n * pad, 1) * sizeof(double)));
+    fs::launch_featurize(dev, sp, n, sd, ad, pad, xd);
+    fs::fit::fit_families(dev, fo, nseg, seg, pad, xd, td, params);
   });
 }
 

@@ -159,6 +159,8 @@ enum Slot : int {
   kSlotScoreX,
   kSlotScoreS,
   kSlotScoreP,
+  kSlotFitX,    // featurized training records (fs_fit_records)
+  kSlotFitIn,   // their descriptors / targets (host-pointer form)
   kSlotCount
 };
 

@@ -70,3 +70,20 @@ def test_score_fused_equals_featurize_then_predict(dev, orc, monkeypatch, cfg):
     xp = _featurize_pool(W, orc)
     s3 = fo.predict(xp, seg=list(W["pool_seg"]))
     assert np.array_equal(s1, s3)
+
+
+def test_fit_records_equals_fit_on_featurized_rows(dev, orc):
+    """fs_fit_records (descriptors, device featurize) == fs_fit on the host-featurized rows."""
+    W = bench.build_workload("c3", 11)
+    sp = fs.Spaces(dev, W["spaces"])
+    F = len(W["families"])
+    a = fs.Forest(dev, F)
+    a.fit_records(sp, W["tr_so"], W["tr_a"], bench.PAD, W["tr_y"], seg=list(W["tr_seg"]),
+                  params=fs.GbtParams(30, 3, 0.1, 2))
+    b = fs.Forest(dev, F)
+    b.fit(bench._featurize_host(W, orc), W["tr_y"], seg=list(W["tr_seg"]), params=fs.GbtParams(30, 3, 0.1, 2))
+    for f in range(F):
+        ea, eb = a.export(f), b.export(f)
+        assert ea.base == eb.base
+        for k in FIELDS:
+            assert np.array_equal(getattr(ea, k), getattr(eb, k)), (f, k)
