@@ -2117,6 +2117,77 @@ __device__ __forceinline__ double fold_seq(const double* __restrict__ v, const u
   return s;
 }
 
+// Warp-collective exact sequential fold (sum_residuals, costmodel.cpp:36-40) of a long chain in
+// about half the dependent-add latency, by speculation on the midpoint value:
+//   1. every lane accumulates a strided part of x_0..x_{m-1} in double-double (TwoSum); the warp
+//      reduction gives P ~= the EXACT prefix sum (the sequential result differs from it only by
+//      the chain's accumulated roundings, typically a few ulps);
+//   2. lane 0 folds x_0..x_{m-1} from 0.0 - the true S_m - while lanes 1..31 fold x_m..x_{n-1}
+//      from the 31 doubles P-15ulp .. P+15ulp, all in the same loop;
+//   3. the lane whose start is bit-identical to S_m holds the exact S_n (the fold is a function
+//      of its start); if none is, the warp continues sequentially from S_m (same result, no
+//      saving). Every add is still the reference's separately rounded sequential one.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = fs_add(a, b);
+  const double bb = fs_sub(s, a);
+  e = fs_add(fs_sub(a, fs_sub(s, bb)), fs_sub(b, bb));
+}
+__device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles -> consecutive ints
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : static_cast<long long>(0x8000000000000000ull) - b;
+}
+__device__ __forceinline__ double ord_dbl(long long o) {
+  return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
+}
+__device__ __forceinline__ double fold_spec(const double* __restrict__ v, const uint16_t* __restrict__ idx, int n) {
+  const int lane = threadIdx.x & 31;
+  if (n < 192) return fold_seq(v, idx, n);
+  const int m = n >> 1;
+  double hi = 0.0, lo = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    double s, e;
+    two_sum(hi, v[idx[i]], s, e);
+    hi = s;
+    lo = fs_add(lo, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, e;
+    two_sum(hi, oh, s, e);
+    hi = s;
+    lo = fs_add(fs_add(lo, ol), e);
+  }
+  const double P = fs_add(hi, lo);
+  const double start = lane == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (lane - 16));
+  const uint16_t* seq = idx + (lane == 0 ? 0 : m);
+  const int len = lane == 0 ? m : n - m;  // n - m is m or m + 1
+  double s = start;
+  {
+    int i = 0;
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = v[seq[k]];
+    for (i = 8; i + 8 <= m; i += 8) {
+      double b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[k] = v[seq[i + k]];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = b[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+    for (; i < len; ++i) s = fs_add(s, v[seq[i]]);
+  }
+  const double Sm = __shfl_sync(0xffffffffu, s, 0);
+  const unsigned hit = __ballot_sync(0xffffffffu, lane != 0 && __double_as_longlong(start) == __double_as_longlong(Sm));
+  if (hit) return __shfl_sync(0xffffffffu, s, __ffs(hit) - 1);
+  double t = Sm;  // speculation missed: finish the chain from the true midpoint
+  for (int i = m; i < n; ++i) t = fs_add(t, v[idx[i]]);
+  return t;
+}
+
 __device__ __forceinline__ double warp_max_d(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
@@ -2679,7 +2750,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           ResNode& nd = s_nodes[s];
           const int nv = nd.n;
           if (j == 0xFFFF) {  // every lane runs the same chain (broadcast loads): no divergence
-            const double t = fold_seq(s_resid, s_ord0 + nd.seg, nv);
+            const double t = fold_spec(s_resid, s_ord0 + nd.seg, nv);
             if (lane == 0) nd.total = t;
             continue;
           }
@@ -2918,9 +2989,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       if (nd.state != kNodeLeaf || nd.n == 0) continue;
       if (s > 0 && s_nodes[(s - 1) >> 1].state != kNodeSplit) continue;
       const int nv = nd.n;
-      double sum = 0.0;
-      if (lane == 0) sum = fold_seq(s_resid, s_ord0 + nd.seg, nv);
-      sum = __shfl_sync(0xffffffffu, sum, 0);
+      const double sum = fold_spec(s_resid, s_ord0 + nd.seg, nv);  // warp-collective
       const double value = fs_div(sum, static_cast<double>(nv));
       const double step = fs_mul(fd.lr, value);
       for (int i = lane; i < nv; i += 32) {
