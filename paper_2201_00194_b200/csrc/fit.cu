@@ -1823,6 +1823,8 @@ __global__ void __launch_bounds__(1024) partition_kernel(
     r.threshold = thr;
     r.value = 0.0;
     r.gain = nd.gain;
+    r.rep = jj;
+    r.bin = bin;
     tr[s] = r;
     base_l = 0;
     base_r = 0;
@@ -1925,6 +1927,8 @@ __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamSta
     r.threshold = 0.0;
     r.value = value;
     r.gain = 0.0;
+    r.rep = -1;
+    r.bin = 0;
     trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = r;
   }
 }
@@ -2896,6 +2900,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           r.threshold = thr;
           r.value = 0.0;
           r.gain = nd.gain;
+          r.rep = j;
+          r.bin = nd.bin;
           tr[s] = r;
           ResNode& a = s_nodes[2 * s + 1];
           ResNode& b = s_nodes[2 * s + 2];
@@ -3004,6 +3010,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         r.threshold = 0.0;
         r.value = value;
         r.gain = 0.0;
+        r.rep = -1;
+        r.bin = 0;
         tr[s] = r;
       }
     }
@@ -3040,6 +3048,119 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     if (blockIdx.x == 0)
       for (int i = 0; i < 12; ++i) atomicAdd(ctr + kCtrPhase0 + i, static_cast<unsigned long long>(s_ph[i]));
     for (int i = 0; i < 4; ++i) atomicAdd(ctr + kCtrPhase0 + 12 + i, s_why[i]);
+  }
+}
+
+}  // namespace
+}  // namespace fit
+}  // namespace fs
+
+namespace fs {
+namespace fit {
+namespace {
+
+constexpr int kCompileSlots = 255;  // heap slots of a depth-7 tree (device compile limit)
+
+// ==========================================================================================
+// fit epilogue on the device: per family, the reference pre-order export of every tree
+// (costmodel.cpp:82-83 node numbering, :108-111 left before right) and the compiled predict form
+// (forest.cuh: complete heap of the family's depth, node = rep | bin << 16 where bin is the
+// threshold's rank among the rep's distinct values, early leaves replicated under always-left
+// nodes), written straight into the family's model blob - no host round trip after a fit.
+// Compiled features are representatives; fmap maps them back to original feature ids.
+// ==========================================================================================
+struct ExportJob {
+  unsigned char* blob;
+  DevLayout lay;
+  int depth;      // heap depth of the compiled form (the family's tree depth)
+  int code_wide;  // codes are u16 (always-left rank 0xFFFF instead of 0xFF)
+};
+
+__global__ void __launch_bounds__(128) export_compile_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const TreeRec* __restrict__ trees,
+    int slots, const double* __restrict__ mse, int max_trees, const double* __restrict__ base,
+    const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
+    const ExportJob* __restrict__ jobs) {
+  const int f = blockIdx.x;
+  const FamDesc fd = fam[f];
+  const ExportJob jb = jobs[f];
+  const DevLayout& L = jb.lay;
+  unsigned char* B = jb.blob;
+  const int T = fd.n > 0 ? st[f].ntrees : 0;
+  if (threadIdx.x == 0) {
+    ModelMeta mt;
+    mt.base = fd.n > 0 ? base[f] : 0.0;
+    mt.n_trees = T;
+    mt.pad_ = 0;
+    mt.screened = static_cast<int64_t>(st[f].screened);
+    mt.exact = static_cast<int64_t>(st[f].exact);
+    *reinterpret_cast<ModelMeta*>(B + L.meta) = mt;
+  }
+  double* uthr = reinterpret_cast<double*>(B + L.uthr);
+  int32_t* uoff = reinterpret_cast<int32_t*>(B + L.uoff);
+  int32_t* fmap = reinterpret_cast<int32_t*>(B + L.fmap);
+  for (int b = threadIdx.x; b < fd.bins; b += blockDim.x) uthr[b] = vals[fd.bin0 + b];
+  for (int j = threadIdx.x; j <= fd.nrep; j += blockDim.x) {
+    uoff[j] = j < fd.nrep ? rep_boff[fd.rep0 + j] : fd.bins;
+    if (j < fd.nrep) fmap[j] = rep_orig[fd.rep0 + j];
+  }
+  const int D = jb.depth, nint = (1 << D) - 1, nleaf = 1 << D, S = L.slots;
+  const uint32_t always_left = jb.code_wide ? 0xFFFFu : 0xFFu;
+  uint32_t* nodes = reinterpret_cast<uint32_t*>(B + L.nodes);
+  double* leafv = reinterpret_cast<double*>(B + L.leafv);
+  uint8_t* leafid = B + L.leafid;
+  int32_t* cnt = reinterpret_cast<int32_t*>(B + L.cnt);
+  int32_t* feat = reinterpret_cast<int32_t*>(B + L.feat);
+  double* thr = reinterpret_cast<double*>(B + L.thr);
+  int32_t* lft = reinterpret_cast<int32_t*>(B + L.left);
+  int32_t* rgt = reinterpret_cast<int32_t*>(B + L.right);
+  double* val = reinterpret_cast<double*>(B + L.val);
+  double* gain = reinterpret_cast<double*>(B + L.gain);
+  double* mo = reinterpret_cast<double*>(B + L.mse);
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    mo[t] = mse[static_cast<int64_t>(f) * max_trees + t];
+    const TreeRec* rec = trees + fd.tree0 + static_cast<int64_t>(t) * slots;
+    // subtree sizes bottom-up over the heap slots, then pre-order indices top-down
+    int size[kCompileSlots], pidx[kCompileSlots];
+    for (int h = S - 1; h >= 0; --h) {
+      size[h] = 0;
+      if (rec[h].kind == kNodeLeaf) size[h] = 1;
+      else if (rec[h].kind == kNodeSplit) size[h] = 1 + size[2 * h + 1] + size[2 * h + 2];
+    }
+    for (int h = 0; h < S; ++h) pidx[h] = -1;
+    pidx[0] = 0;
+    const size_t o = static_cast<size_t>(t) * S;
+    for (int h = 0; h < S; ++h) {  // parents precede children in heap order
+      const int i = pidx[h];
+      if (i < 0) continue;
+      const TreeRec& r = rec[h];
+      const bool sp = r.kind == kNodeSplit;
+      feat[o + i] = sp ? r.feature : -1;
+      thr[o + i] = sp ? r.threshold : 0.0;
+      val[o + i] = sp ? 0.0 : r.value;
+      gain[o + i] = sp ? r.gain : 0.0;
+      lft[o + i] = -1;
+      rgt[o + i] = -1;
+      if (sp) {
+        pidx[2 * h + 1] = i + 1;
+        pidx[2 * h + 2] = i + 1 + size[2 * h + 1];
+        lft[o + i] = i + 1;
+        rgt[o + i] = i + 1 + size[2 * h + 1];
+      }
+    }
+    cnt[t] = size[0];
+    // compiled heap
+    for (int h = 0; h < nint; ++h) {
+      const TreeRec& r = rec[h];
+      nodes[static_cast<size_t>(t) * nint + h] =
+          r.kind == kNodeSplit ? static_cast<uint32_t>(r.rep) | (static_cast<uint32_t>(r.bin) << 16) : always_left << 16;
+    }
+    for (int q = 0; q < nleaf; ++q) {
+      int h = nint + q;  // deepest existing ancestor-or-self is the leaf covering this heap leaf
+      while (h > 0 && rec[h].kind == 0) h = (h - 1) >> 1;
+      leafv[static_cast<size_t>(t) * nleaf + q] = rec[h].value;
+      leafid[static_cast<size_t>(t) * nleaf + q] = static_cast<uint8_t>(pidx[h]);
+    }
   }
 }
 
@@ -3707,6 +3828,87 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
 
   // ---- results: heap-slot records -> pre-order CostModelState layout ------------------------
   htick("rounds launched");
+  // Epilogue. Default: export + compile on the device straight into each family's model blob
+  // (no host round trip; the host pre-order arrays are materialised when first asked for).
+  // FAMSEER_HOST_COMPILE=1 (or trees deeper than the device compile handles): read the tree
+  // tables back and compile on the host.
+  const bool dev_compile = depth_max <= kResMaxDepth && slots <= kCompileSlots && !std::getenv("FAMSEER_HOST_COMPILE");
+  if (dev_compile) {
+    std::vector<ExportJob> jobs(static_cast<size_t>(F));
+    for (int f = 0; f < F; ++f) {
+      FamilyModel& m = fo->fams[static_cast<size_t>(f)];
+      const FamDesc& fd = fam[static_cast<size_t>(f)];
+      const int T = std::max(fd.n > 0 ? fd.trees : 0, 0), D = std::max(fd.depth, 0);
+      const int S = (1 << (D + 1)) - 1, nint = (1 << D) - 1, nleaf = 1 << D;
+      const int nrep = std::max(static_cast<int>(fd.nrep), 0), bins = std::max(static_cast<int>(fd.bins), 0);
+      int max_nb = 0, d_orig = 0;
+      for (int j = 0; j < nrep; ++j) {
+        max_nb = std::max(max_nb, static_cast<int>(rep_nb[static_cast<size_t>(fd.rep0 + j)]));
+        d_orig = std::max(d_orig, static_cast<int>(rep_orig[static_cast<size_t>(fd.rep0 + j)]) + 1);
+      }
+      DevLayout L;
+      size_t o = 0;
+      auto put = [&](size_t bytes) {
+        const size_t at = o;
+        o = (o + bytes + 15) & ~size_t(15);
+        return at;
+      };
+      L.meta = put(sizeof(ModelMeta));
+      L.nodes = put(static_cast<size_t>(T) * nint * 4);
+      L.leafv = put(static_cast<size_t>(T) * nleaf * 8);
+      L.leafid = put(static_cast<size_t>(T) * nleaf);
+      L.uthr = put(static_cast<size_t>(bins) * 8);
+      L.uoff = put(static_cast<size_t>(nrep + 1) * 4);
+      L.fmap = put(static_cast<size_t>(nrep) * 4);
+      L.cnt = put(static_cast<size_t>(T) * 4);
+      L.feat = put(static_cast<size_t>(T) * S * 4);
+      L.thr = put(static_cast<size_t>(T) * S * 8);
+      L.left = put(static_cast<size_t>(T) * S * 4);
+      L.right = put(static_cast<size_t>(T) * S * 4);
+      L.val = put(static_cast<size_t>(T) * S * 8);
+      L.gain = put(static_cast<size_t>(T) * S * 8);
+      L.mse = put(static_cast<size_t>(T) * 8);
+      L.total = o;
+      L.max_trees = T;
+      L.slots = S;
+      if (L.total > m.blob_cap) {
+        if (m.blob_d) FS_CUDA(cudaFree(m.blob_d));
+        m.blob_d = nullptr;
+        const size_t cap = std::max<size_t>(L.total + L.total / 2, 4096);
+        FS_CUDA(cudaMalloc(&m.blob_d, cap));
+        m.blob_cap = cap;
+      }
+      const bool wide = max_nb > 255;
+      jobs[static_cast<size_t>(f)] = {m.blob_d, L, D, wide ? 1 : 0};
+      m.lr = fd.lr;
+      m.compiled = true;
+      m.generic = false;
+      m.pending = true;
+      m.lay = L;
+      m.depth = D;
+      m.d_model = nrep;
+      m.d_orig = d_orig;
+      m.code_bytes = wide ? 2 : 1;
+      m.n_uthr = bins;
+      m.n_trees = T;  // upper bound until materialised (the device meta holds the count)
+      m.nodes_d = reinterpret_cast<uint32_t*>(m.blob_d + L.nodes);
+      m.leafv_d = reinterpret_cast<double*>(m.blob_d + L.leafv);
+      m.leafid_d = m.blob_d + L.leafid;
+      m.uthr_d = reinterpret_cast<double*>(m.blob_d + L.uthr);
+      m.uoff_d = reinterpret_cast<int32_t*>(m.blob_d + L.uoff);
+      m.fmap_d = reinterpret_cast<const int32_t*>(m.blob_d + L.fmap);
+      m.meta_d = reinterpret_cast<const ModelMeta*>(m.blob_d + L.meta);
+      m.g_off_d = m.g_feat_d = m.g_left_d = m.g_right_d = nullptr;
+      m.g_thr_d = m.g_val_d = nullptr;
+    }
+    ExportJob* jobs_d = ar.upload(jobs);
+    export_compile_kernel<<<F, 128, 0, s>>>(fam_d, st_d, trees_d, slots, mse_d, std::max(max_trees, 1), base_d,
+                                            rep_orig_d, rep_boff_d, vals_d, jobs_d);
+    dev->count_launch();
+    FS_CUDA(cudaGetLastError());
+    htick("device export launched");
+    return;
+  }
   std::vector<FamState> st_h;
   std::vector<TreeRec> trees_h;
   std::vector<double> mse_h, base_h;
@@ -3853,6 +4055,7 @@ int fs_forest_fit_stats(const fs_forest* fo, int32_t family, int64_t* screened, 
     if (!fo || family < 0 || family >= static_cast<int32_t>(fo->fams.size()))
       fs::fail(FS_ERANGE, "fs_forest_fit_stats: unknown family id");
     const auto& m = fo->fams[static_cast<size_t>(family)];
+    fs::materialize(fo->dev, m);
     if (screened) *screened = m.screened;
     if (exact) *exact = m.exact;
   });

@@ -86,6 +86,8 @@ struct TreeRec {
   double threshold;
   double value;
   double gain;
+  int32_t rep;      // split: representative feature index (compiled model feature)
+  int32_t bin;      // split: bin of the threshold among the rep's distinct values (its rank)
 };
 
 // Window bookkeeping per (node, rep): screen lower/upper bound of the feature's best candidate.

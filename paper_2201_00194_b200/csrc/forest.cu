@@ -14,6 +14,9 @@ void FamilyModel::release_device() {
   if (blob_d) cudaFree(blob_d);
   blob_d = nullptr;
   blob_cap = 0;
+  pending = false;
+  fmap_d = nullptr;
+  meta_d = nullptr;
   nodes_d = nullptr;
   leafv_d = nullptr;
   leafid_d = nullptr;
@@ -83,8 +86,58 @@ void UploadBatch::flush(fs_device* dev) {
   host.clear();
 }
 
+void materialize(fs_device* dev, const FamilyModel& m) { materialize(dev, const_cast<FamilyModel&>(m)); }
+
+void materialize(fs_device* dev, FamilyModel& m) {
+  if (!m.pending) return;
+  const DevLayout& L = m.lay;
+  const size_t bytes = L.total - L.meta;
+  std::vector<unsigned char> h(bytes);
+  FS_CUDA(cudaMemcpyAsync(h.data(), m.blob_d + L.meta, bytes, cudaMemcpyDeviceToHost, dev->stream));
+  FS_CUDA(cudaStreamSynchronize(dev->stream));
+  auto at = [&](size_t off) { return h.data() + (off - L.meta); };
+  ModelMeta meta;
+  std::memcpy(&meta, at(L.meta), sizeof meta);
+  const int T = meta.n_trees, S = L.slots;
+  const auto* cnt = reinterpret_cast<const int32_t*>(at(L.cnt));
+  const auto* feat = reinterpret_cast<const int32_t*>(at(L.feat));
+  const auto* thr = reinterpret_cast<const double*>(at(L.thr));
+  const auto* lft = reinterpret_cast<const int32_t*>(at(L.left));
+  const auto* rgt = reinterpret_cast<const int32_t*>(at(L.right));
+  const auto* val = reinterpret_cast<const double*>(at(L.val));
+  const auto* gn = reinterpret_cast<const double*>(at(L.gain));
+  const auto* mse = reinterpret_cast<const double*>(at(L.mse));
+  m.base = meta.base;
+  m.screened = meta.screened;
+  m.exact = meta.exact;
+  m.offsets.assign(1, 0);
+  m.feature.clear();
+  m.threshold.clear();
+  m.left.clear();
+  m.right.clear();
+  m.value.clear();
+  m.gain.clear();
+  for (int t = 0; t < T; ++t) {
+    const size_t o = static_cast<size_t>(t) * S;
+    const int c = cnt[t];
+    m.feature.insert(m.feature.end(), feat + o, feat + o + c);
+    m.threshold.insert(m.threshold.end(), thr + o, thr + o + c);
+    m.left.insert(m.left.end(), lft + o, lft + o + c);
+    m.right.insert(m.right.end(), rgt + o, rgt + o + c);
+    m.value.insert(m.value.end(), val + o, val + o + c);
+    m.gain.insert(m.gain.end(), gn + o, gn + o + c);
+    m.offsets.push_back(static_cast<int32_t>(m.feature.size()));
+  }
+  m.mse.assign(mse, mse + T);
+  m.n_trees = T;
+  m.pending = false;
+}
+
 void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch) {
   m.compiled = false;
+  m.pending = false;
+  m.fmap_d = nullptr;
+  m.meta_d = nullptr;
   const int T = m.num_trees();
   m.n_trees = T;
   // Validate structure and find depth / feature range.
@@ -275,6 +328,7 @@ int fs_forest_export(const fs_forest* fo, int32_t family, double* base, int32_t*
     if (!fo || family < 0 || family >= static_cast<int32_t>(fo->fams.size()))
       fs::fail(FS_ERANGE, "fs_forest_export: unknown family id " + std::to_string(family));
     const auto& m = fo->fams[static_cast<size_t>(family)];
+    fs::materialize(fo->dev, m);
     const int T = m.num_trees();
     const int N = m.offsets.back();
     if (base) *base = m.base;

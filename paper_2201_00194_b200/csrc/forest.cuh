@@ -18,6 +18,24 @@ namespace fs {
 
 constexpr int kMaxHeapDepth = 8;  // deeper ensembles take the generic pre-order kernel
 
+// Device-side header of a compiled model (first bytes of the blob when the fit compiled it on
+// the device): predict reads n_trees / base from here, so fs_fit needs no host round trip.
+struct ModelMeta {
+  double base;
+  int32_t n_trees;
+  int32_t pad_;
+  int64_t screened, exact;  // fit diagnostics
+};
+
+// Offsets (bytes into blob_d) of a device-compiled fit result: the compiled predict form and the
+// reference pre-order export, both written by the fit's export kernel.
+struct DevLayout {
+  size_t meta, nodes, leafv, leafid, uthr, uoff, fmap;  // compiled
+  size_t cnt, feat, thr, left, right, val, gain, mse;   // pre-order export (per tree: S slots)
+  size_t total;
+  int max_trees = 0, slots = 0;  // S = nodes per tree slot block
+};
+
 struct FamilyModel {
   // ---- pre-order form (host) ----
   double base = 0.0;
@@ -52,6 +70,12 @@ struct FamilyModel {
   // cudaFree per fit, one copy per compile)
   unsigned char* blob_d = nullptr;
   size_t blob_cap = 0;
+  // fit compiled on the device: host pre-order arrays are materialised on first use
+  bool pending = false;
+  DevLayout lay;
+  const int32_t* fmap_d = nullptr;    // compiled feature -> original feature (nullptr = identity)
+  int d_orig = 0;                     // 1 + largest original feature referenced (row-width check)
+  const ModelMeta* meta_d = nullptr;  // device n_trees / base (nullptr = host fields)
 
   int num_trees() const { return static_cast<int>(offsets.size()) - 1; }
   void release_device();
@@ -64,6 +88,10 @@ struct UploadBatch {
   void add(unsigned char* dst, const unsigned char* src, size_t bytes);
   void flush(fs_device* dev);  // one pinned staging fill, async copies, no host wait
 };
+
+// Download a device-compiled fit's pre-order export into the host arrays (no-op otherwise).
+void materialize(fs_device* dev, FamilyModel& m);
+void materialize(fs_device* dev, const FamilyModel& m);
 
 // Build the compiled device form from the pre-order arrays (host transformation of the tree
 // table; O(nodes)). With a batch, the device copy is deferred to batch->flush().

@@ -31,6 +31,8 @@ struct PredModel {
   const int32_t* uoff;
   double base, lr;
   int depth, n_trees, d_model, n_uthr;
+  const int32_t* fmap;       // compiled feature -> original feature (nullptr: identity)
+  const fs::ModelMeta* meta;  // device-compiled fit: n_trees / base live on the device
 };
 
 // Candidate descriptors for the fused score path (kFused): the kernel computes each tested
@@ -66,7 +68,9 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
   extern __shared__ __align__(16) unsigned char smem[];
   const PredJob job = jobs[blockIdx.x];
   const PredModel M = models[job.model];
-  const int depth = M.depth, d_model = M.d_model, n_trees = M.n_trees;
+  const int depth = M.depth, d_model = M.d_model;
+  const int n_trees = M.meta ? M.meta->n_trees : M.n_trees;
+  const int32_t* fmap = M.fmap;
   const int nint = (1 << depth) - 1;
   const int nleaf = 1 << depth;
   const int mnint = (1 << max_depth) - 1, mnleaf = 1 << max_depth;
@@ -140,16 +144,17 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
       }
       for (int base = 0; base < d_model; base += 32) {
         const int f = base + lane;
+        const int g = f < d_model && fmap ? __ldg(fmap + f) : f;  // the original feature index
         int src_a = 0, src_b = 0, kind = 0;  // 0 zero (padding), 1 log, 2 pos, 3 product
-        if (f < k) {
+        if (g < k) {
           kind = 1;
-          src_a = f;
-        } else if (f < 2 * k) {
+          src_a = g;
+        } else if (g < 2 * k) {
           kind = 2;
-          src_a = f - k;
-        } else if (f < dim) {
+          src_a = g - k;
+        } else if (g < dim) {
           kind = 3;
-          fs::pair_of(k, f - 2 * k, src_a, src_b);
+          fs::pair_of(k, g - 2 * k, src_a, src_b);
         }
         const double la = __shfl_sync(0xffffffffu, lg, src_a);
         const double lb = __shfl_sync(0xffffffffu, lg, src_b);
@@ -168,13 +173,15 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
       for (int f = lane; f < d; f += 32) {
         const double v = __ldcs(xr + f);  // streamed once
         nonfinite |= !isfinite(v);
-        if (f < d_model) codes[f * kTile + c] = code_of(f, v);
+        if (!fmap && f < d_model) codes[f * kTile + c] = code_of(f, v);
       }
+      if (fmap)  // compiled features are representatives: gather their original columns (L1 hits)
+        for (int f = lane; f < d_model; f += 32) codes[f * kTile + c] = code_of(f, xr[__ldg(fmap + f)]);
     }
     if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, fs::kErrNonFinitePredict);
   }
 
-  double score = M.base;
+  double score = M.meta ? M.meta->base : M.base;
   const double lr = M.lr;
   const bool active = tid < tile_rows;
   for (int t0 = 0; t0 < n_trees; t0 += kChunk) {
@@ -283,7 +290,8 @@ void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, cons
     if (f >= static_cast<int32_t>(fo->fams.size())) fail(FS_ERANGE, "predict: segment names an unknown family");
     const auto& m = fo->fams[static_cast<size_t>(f)];
     if (!m.compiled) fail(FS_EINVAL, "predict: family " + std::to_string(f) + " has no compiled model");
-    if (m.d_model > d) fail(FS_EINVAL, "predict: model references feature beyond the row width");
+    if ((m.fmap_d ? m.d_orig : m.d_model) > d) fail(FS_EINVAL, "predict: model references feature beyond the row width");
+    if (leaf_out && m.pending) materialize(dev, m);  // leaf-id layout needs the true tree count
     if (rows <= 0) continue;
     const int64_t lo = leaf_off;
     leaf_off += rows * m.n_trees;
@@ -300,8 +308,8 @@ void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, cons
     HeapGroup& g = groups[m.code_bytes == 2][smem_thr];
     const int mi = static_cast<int>(g.models.size());
     g.models.push_back({m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, m.base, m.lr, m.depth, m.n_trees,
-                        std::min(m.d_model, d), m.n_uthr});
-    g.max_dmodel = std::max(g.max_dmodel, std::min(m.d_model, d));
+                        m.fmap_d ? m.d_model : std::min(m.d_model, d), m.n_uthr, m.fmap_d, m.meta_d});
+    g.max_dmodel = std::max(g.max_dmodel, m.fmap_d ? m.d_model : std::min(m.d_model, d));
     g.max_depth = std::max(g.max_depth, m.depth);
     g.max_uthr = std::max(g.max_uthr, m.n_uthr);
     for (int64_t t = 0; t < rows; t += kTile)
@@ -340,8 +348,10 @@ void launch_score_fused(fs_device* dev, const fs_spaces* spc, const fs_forest* f
 
 int64_t leaf_bytes(const fs_forest* fo, int32_t nseg, const int64_t* seg) {
   int64_t b = 0;
-  for (int f = 0; f < nseg && f < static_cast<int32_t>(fo->fams.size()); ++f)
+  for (int f = 0; f < nseg && f < static_cast<int32_t>(fo->fams.size()); ++f) {
+    materialize(fo->dev, fo->fams[static_cast<size_t>(f)]);
     b += (seg[f + 1] - seg[f]) * fo->fams[static_cast<size_t>(f)].n_trees;
+  }
   return b;
 }
 
