@@ -37,7 +37,10 @@ def build(with_ref: bool | None = None) -> None:
     if with_ref is None:
         with_ref = os.path.isdir("/root/reference/proj/core/src")
     if with_ref:
-        targets.append("ref")
+        # the compiled reference core, and the reference's unchanged tuning engine linked both
+        # against it (engine_ref) and against the B200 drop-in (engine_b200) for
+        # tests/test_engine_e2e.py - built here, they travel to the GPU box as binaries
+        targets += ["ref", "engines"]
     subprocess.run(["make", "-s", "-C", HERE, "-j8", *targets], check=True)
 
 
