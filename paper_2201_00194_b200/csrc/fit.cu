@@ -2028,7 +2028,7 @@ struct ResNode {
 
 struct ResLayout {
   int ls, slots, cs;
-  size_t codes, resid, pred, predv, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, clc, binrep,
+  size_t codes, resid, pred, predv, targ, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, clc, binrep,
       vals, cand, total;
 };
 
@@ -2054,6 +2054,8 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + (pre_smem ? static_cast<size_t>(n) * nr * 2 : 0));
   L.predv = o;  // running predictions (when pred_smem), else they live in global memory
   o = res_align(o + (pred_smem ? static_cast<size_t>(n) * 8 : 0));
+  L.targ = o;  // canonical targets and the root order-0 list, staged with the predictions
+  o = res_align(o + (pred_smem ? static_cast<size_t>(n) * 10 : 0));
   L.fix = o;
   o = res_align(o + static_cast<size_t>(n) * 8);
   L.node = o;
@@ -2255,8 +2257,21 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     }                                       \
   } while (0)
   double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
-  // running predictions: shared memory when they fit, else global (L2-resident)
+  // running predictions: shared memory when they fit, else global (L2-resident); the targets
+  // and the root order-0 list are staged with them (read every round)
   double* s_pred = pred_smem ? reinterpret_cast<double*>(sm + Lo.predv) : pred_g + fd.pos0;
+  const double* s_targ = target_c + fd.pos0;
+  const int32_t* g_ordr = ord_root + fd.pos0;
+  uint16_t* s_ordr = nullptr;
+  if (pred_smem) {
+    double* t = reinterpret_cast<double*>(sm + Lo.targ);
+    s_ordr = reinterpret_cast<uint16_t*>(t + n);
+    for (int p = threadIdx.x; p < n; p += kResThreads) {
+      t[p] = target_c[fd.pos0 + p];
+      s_ordr[p] = static_cast<uint16_t>(ord_root[fd.pos0 + p]);
+    }
+    s_targ = t;
+  }
   uint16_t* s_pre = reinterpret_cast<uint16_t*>(sm + Lo.pred);  // presorted lists, if staged
   const int32_t* g_pre = ord + fd.ord0;
   auto pre_at = [&](int j, int i) -> int {
@@ -2303,11 +2318,11 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     // ---- residuals (costmodel.cpp:204-206), fixed point, per-round reset ----------------
     unsigned long long mx = 0;
     for (int p = tid; p < n; p += kResThreads) {
-      const double r = fs_sub(target_c[fd.pos0 + p], s_pred[p]);
+      const double r = fs_sub(s_targ[p], s_pred[p]);
       s_resid[p] = r;
       mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(r))));
       s_node[p] = 0;
-      s_ord0[p] = static_cast<uint16_t>(ord_root[fd.pos0 + p]);
+      s_ord0[p] = s_ordr ? s_ordr[p] : static_cast<uint16_t>(g_ordr[p]);
     }
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) s_red[warp] = mx;
@@ -2676,66 +2691,69 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       // ---- decide (decide_kernel) ------------------------------------------------------------
       if (tid == 0) s_nitems = 0;
       __syncthreads();
-      if (tid < nl) {
-        const int k = tid;
+      // warp per node, lanes over the node's features (window records read in parallel)
+      for (int k = warp; k < nl; k += kResWarps) {
         ResNode& nd = s_nodes[first + k];
-        if (nd.state == 0 && nd.build != 0) {
-          const WinRec* w = s_win + k * nrep;
-          bool done = false;
-          int pick = -1;
-          if (nd.wcount == 0) {
-            nd.state = kNodeLeaf;
-            done = true;
-          } else if (nd.wcount == 1) {
-            for (int j = 0; j < nrep; ++j)
-              if (w[j].flag) {
-                if (w[j].best_lo > 0.0) pick = j;
-                break;
-              }
-          } else if (nd.eqf0 >= 0) {
-            bool all = true;
-            for (int j = nd.eqf0 + 1; j < nrep; ++j)
-              if (w[j].flag && !w[j].eq) all = false;
-            if (all) pick = nd.eqf0;
-          }
-          if (pick >= 0) {
+        if (nd.state != 0 || nd.build == 0) continue;
+        const WinRec* w = s_win + k * nrep;
+        if (nd.wcount == 0) {
+          if (lane == 0) nd.state = kNodeLeaf;
+          continue;
+        }
+        int pick = -1, nflag = 0, f0 = -1;
+        bool multi = false, notall = false;
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          const bool fl = j < nrep && w[j].flag;
+          const unsigned m = __ballot_sync(0xffffffffu, fl);
+          nflag += __popc(m);
+          if (m && f0 < 0) f0 = j0 + __ffs(m) - 1;
+          multi |= __any_sync(0xffffffffu, fl && w[j].count > 1);
+          notall |= __any_sync(0xffffffffu, fl && j > nd.eqf0 && !w[j].eq);
+        }
+        if (nd.wcount == 1) {
+          if (f0 >= 0 && w[f0].best_lo > 0.0) pick = f0;
+        } else if (nd.eqf0 >= 0 && !notall) {
+          pick = nd.eqf0;
+        }
+        if (pick >= 0) {
+          if (lane == 0) {
             nd.state = kNodeSplit;
             nd.rep = pick;
             nd.bin = w[pick].best_bin;
             nd.gain = w[pick].best_g;
             nd.lc = w[pick].best_lc;
             atomicAdd(&s_cnt[0], 1ull);
-            done = true;
           }
-          if (!done) {
-            nd.state = kNodeExact;
-            atomicAdd(&s_cnt[1], 1ull);
-            {  // why the screen could not decide (diagnostics, fs_device_counters [16..19])
-              int why = 3;  // sign of the only candidate uncertain
-              if (nd.wcount >= 2) {
-                why = 2;  // orders not equivalent
-                int lc0 = -1;
-                for (int j = 0; j < nrep; ++j) {
-                  if (!w[j].flag) continue;
-                  if (w[j].count > 1) {
-                    why = 0;  // several window candidates on one feature
-                    break;
-                  }
-                  if (lc0 < 0) lc0 = w[j].best_lc;
-                  else if (w[j].best_lc != lc0) why = 1;  // different partitions
-                }
-              }
-              atomicAdd(&s_why[why], 1ull);
-            }
-            int cnt = 1;
-            for (int j = 0; j < nrep; ++j) cnt += w[j].flag;
-            const int b = atomicAdd(&s_nitems, cnt);
-            s_items[b] = (first + k) << 16 | 0xFFFF;
-            int o = 1;
-            for (int j = 0; j < nrep; ++j)
-              if (w[j].flag) s_items[b + o++] = (first + k) << 16 | j;
-            atomicAdd(&s_cnt[2], static_cast<unsigned long long>(cnt));
+          continue;
+        }
+        // exact re-evaluation: why the screen could not decide (diagnostics, device counters)
+        int why = 3;  // sign of the only candidate uncertain
+        if (nd.wcount >= 2) {
+          const int lc0 = w[f0].best_lc;
+          bool diff = false;
+          for (int j0 = 0; j0 < nrep; j0 += 32) {
+            const int j = j0 + lane;
+            diff |= __any_sync(0xffffffffu, j < nrep && w[j].flag && w[j].best_lc != lc0);
           }
+          why = multi ? 0 : diff ? 1 : 2;  // several candidates on a feature / partitions / orders
+        }
+        int base = 0;
+        if (lane == 0) {
+          nd.state = kNodeExact;
+          atomicAdd(&s_cnt[1], 1ull);
+          atomicAdd(&s_why[why], 1ull);
+          base = atomicAdd(&s_nitems, nflag + 1);
+          s_items[base] = (first + k) << 16 | 0xFFFF;
+          atomicAdd(&s_cnt[2], static_cast<unsigned long long>(nflag + 1));
+        }
+        base = __shfl_sync(0xffffffffu, base, 0) + 1;
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          const bool fl = j < nrep && w[j].flag;
+          const unsigned m = __ballot_sync(0xffffffffu, fl);
+          if (fl) s_items[base + __popc(m & ((1u << lane) - 1u))] = (first + k) << 16 | j;
+          base += __popc(m);
         }
       }
       __syncthreads();
@@ -3021,7 +3039,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     if (s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0) break;  // uniform (smem)
     double a = 0.0;
     for (int p = tid; p < n; p += kResThreads) {
-      const double e = fs_sub(target_c[fd.pos0 + p], s_pred[p]);
+      const double e = fs_sub(s_targ[p], s_pred[p]);
       a = fs_add(a, fs_mul(e, e));
     }
     for (int o = 16; o > 0; o >>= 1) a = fs_add(a, __shfl_down_sync(0xffffffffu, a, o));
