@@ -171,6 +171,7 @@ def shard_workload(W, rank, world):
         if key_seg == "tr_seg":
             out["tr_y"] = W["tr_y"][idx]
     out["families"] = [W["families"][f] for f in mine]
+    out["fam_cap"] = max(owner.count(r) for r in range(world))  # all-gather record slots per rank
     out["family_ids"] = mine
     out["P_global"], out["N_global"] = int(ps[-1]), int(ts[-1])
     return out
@@ -257,12 +258,20 @@ def run_native(args, rank, world, local_rank):
 
     import paper_2201_00194_b200 as fs
 
+    # one process per GPU; FAMSEER_BENCH_SHARE_GPU=1 maps several ranks onto the visible GPUs
+    # (multi-rank code-path check on a 1-GPU box; collectives then go through gloo)
+    share = os.environ.get("FAMSEER_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.shard == "families":
         # strong scaling: ONE global workload, families LPT-partitioned over ranks
         W = shard_workload(build_workload(args.config, seed=1000), rank, world)
@@ -273,7 +282,7 @@ def run_native(args, rank, world, local_rank):
     stream = torch.cuda.ExternalStream(dev.stream)
     spaces = fs.Spaces(dev, W["spaces"])
     F = len(W["families"])
-    forest = fs.Forest(dev, F)
+    forest = fs.Forest(dev, max(F, 1))  # a rank may own no family (--shard families, N > F)
     params = fs.GbtParams(W["trees"], 3, 0.1, 2)
     P = int(W["pool_seg"][-1])
     N = int(W["tr_seg"][-1])
@@ -292,8 +301,9 @@ def run_native(args, rank, world, local_rank):
         flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
     stream.synchronize()
     # training rows are MeasurementRecord features (featurized at measurement time, simbackend.cpp:185)
-    spaces.featurize_d(tr_so, tr_a, PAD, x_tr)
-    forest.fit_d(x_tr, y_tr, W["tr_seg"], params)  # model the first round scores with
+    if F:
+        spaces.featurize_d(tr_so, tr_a, PAD, x_tr)
+        forest.fit_d(x_tr, y_tr, W["tr_seg"], params)  # model the first round scores with
     dev.check()
     pool_seg, tr_seg = W["pool_seg"], W["tr_seg"]
     fam_base = rank * F if args.shard != "families" else 0
@@ -311,16 +321,25 @@ def run_native(args, rank, world, local_rank):
             if k < G_TOP:
                 rec = torch.cat([rec, torch.full((G_TOP - k, 3), -1.0, dtype=torch.float64, device="cuda")])
             idx.append(rec)
-        mine = torch.cat(idx)
+        mine = torch.cat(idx) if idx else torch.empty((0, 3), dtype=torch.float64, device="cuda")
+        cap = W.get("fam_cap", F) * G_TOP  # every rank contributes the same record count
+        if mine.shape[0] < cap:
+            mine = torch.cat([mine, torch.full((cap - mine.shape[0], 3), -1.0, dtype=torch.float64, device="cuda")])
+        if share:  # gloo path of the shared-GPU check: host tensors
+            parts = [torch.empty_like(mine, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, mine.cpu())
+            return torch.cat(parts)
         out = torch.empty((world * mine.shape[0], 3), dtype=torch.float64, device="cuda")
         dist.all_gather_into_tensor(out, mine)
         return out
 
     def step():
-        spaces.score_d(forest, pool_so, pool_a, PAD, pool_seg, scores, perm)
+        if F:
+            spaces.score_d(forest, pool_so, pool_a, PAD, pool_seg, scores, perm)
         if dist is not None:
             topk_allgather()
-        forest.fit_d(x_tr, y_tr, tr_seg, params)
+        if F:
+            forest.fit_d(x_tr, y_tr, tr_seg, params)
 
     def timed(fn, k, flush_between=True):
         times = []
@@ -362,7 +381,7 @@ def run_native(args, rank, world, local_rank):
         dev.check()
         total_ms = sum(times)
         if dist is not None:
-            t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+            t = torch.tensor([total_ms], dtype=torch.float64, device="cpu" if share else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             total_ms = float(t.item())
         # ---- per-kernel breakdown: one extra, untimed step with every kernel event-timed. The
@@ -377,9 +396,9 @@ def run_native(args, rank, world, local_rank):
         dev.profile(None)
         del os.environ["FAMSEER_NO_GRAPH"]
         breakdown = {k: round(v[1], 4) for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1][1])}
-        score_ms = statistics.median(timed(lambda: spaces.score_d(forest, pool_so, pool_a, PAD, pool_seg, scores, perm),
+        score_ms = statistics.median(timed(lambda: F and spaces.score_d(forest, pool_so, pool_a, PAD, pool_seg, scores, perm),
                                            max(3, args.steps)))
-        fit_ms = statistics.median(timed(lambda: forest.fit_d(x_tr, y_tr, tr_seg, params), max(2, min(args.steps, 5))))
+        fit_ms = statistics.median(timed(lambda: F and forest.fit_d(x_tr, y_tr, tr_seg, params), max(2, min(args.steps, 5))))
         fit_stats = [forest.fit_stats(f) for f in range(F)]
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region ----
@@ -398,6 +417,9 @@ def run_native(args, rank, world, local_rank):
         d2h = [0]
 
         def e2e_step():
+            if not F:
+                d2h[0] = 0
+                return
             s_h, p_h = spaces.score(forest, h_so, h_a, PAD, pool_seg)
             forest.fit_records(spaces, h_tso, h_ta, PAD, h_y, seg=tr_seg, params=params)
             nbytes = s_h.nbytes + p_h.nbytes
@@ -415,7 +437,7 @@ def run_native(args, rank, world, local_rank):
             e_times = timed(e2e_step, args.steps)
         e_total = sum(e_times)
         if dist is not None:
-            t = torch.tensor([e_total], dtype=torch.float64, device="cuda")
+            t = torch.tensor([e_total], dtype=torch.float64, device="cpu" if share else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_total = float(t.item())
         h2d = h_so.nbytes + h_a.nbytes + h_tso.nbytes + h_ta.nbytes + h_y.nbytes
