@@ -474,8 +474,10 @@ __global__ void __launch_bounds__(kSortThreads) canonical_kernel(const double* _
                                                                  const int32_t* __restrict__ rep_orig,
                                                                  const int32_t* __restrict__ rep_nb,
                                                                  int32_t* __restrict__ canon,
-                                                                 int32_t* __restrict__ tmp) {
+                                                                 int32_t* __restrict__ tmp,
+                                                                 const int* __restrict__ eligible) {
   __shared__ SortSmem sm;
+  if (eligible && eligible[blockIdx.x]) return;  // canonical_bitonic_kernel sorts this family
   const FamDesc fd = fam[blockIdx.x];
   const int n = fd.n;
   int32_t* A = canon + fd.pos0;
@@ -581,19 +583,107 @@ __global__ void bin_prefix_kernel(const FamDesc* __restrict__ fam, const int32_t
 
 // prep 3e: base = sequential mean in canonical order (costmodel.cpp:185-188); pred = base;
 // pristine order-0 list (presorted[0], or canonical order when feature 0 is constant).
+// Canonical row order (costmodel.cpp:161-173) for families whose key rows fit one CTA's shared
+// memory and hold no -0.0: rows are ranked by (representative codes in feature order, target) -
+// a lexicographic key packed big-endian into 32-bit words (codes preserve each feature's value
+// order; constant and duplicate columns cannot change it) - with one bitonic sort. Equal keys are
+// bitwise-identical rows (no -0.0), so their relative order is unobservable. Other families
+// keep the stable LSD passes of canonical_kernel (which leaves them untouched here: eligible
+// families are skipped there).
+__device__ __forceinline__ bool key_less(const uint32_t* a, const uint32_t* b, int W) {
+  for (int w = 0; w < W; ++w)
+    if (a[w] != b[w]) return a[w] < b[w];
+  return false;
+}
+
+__global__ void __launch_bounds__(kSortThreads) canonical_bitonic_kernel(
+    const double* __restrict__ target, const uint16_t* __restrict__ codes_all, int d,
+    const FamDesc* __restrict__ fam, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_nb,
+    const int* __restrict__ eligible, int32_t* __restrict__ canon) {
+  extern __shared__ __align__(16) uint32_t ks[];  // [P][W] keys, then [P] row ids
+  const int f = blockIdx.x;
+  if (!eligible[f]) return;
+  const FamDesc fd = fam[f];
+  const int n = fd.n, nrep = fd.nrep;
+  int wide = 0;
+  for (int j = 0; j < nrep; ++j) wide |= rep_nb[fd.rep0 + j] > 256;
+  const int cb = wide ? 2 : 1;                 // bytes per code
+  const int W = (nrep * cb + 3) / 4 + 2;       // code words + 64-bit target key
+  int P = 1;
+  while (P < n) P <<= 1;
+  uint32_t* ids = ks + static_cast<size_t>(P) * W;
+  for (int r = threadIdx.x; r < P; r += blockDim.x) {
+    uint32_t* k = ks + static_cast<size_t>(r) * W;
+    ids[r] = r;
+    if (r >= n) {
+      for (int w = 0; w < W; ++w) k[w] = 0xFFFFFFFFu;
+      continue;
+    }
+    for (int w = 0; w < W - 2; ++w) k[w] = 0;
+    for (int j = 0; j < nrep; ++j) {
+      const uint32_t c = codes_all[(fd.row0 + r) * d + rep_orig[fd.rep0 + j]];
+      for (int b = cb - 1; b >= 0; --b) {  // big-endian bytes: word compare == lexicographic
+        const int byte = j * cb + (cb - 1 - b);
+        k[byte >> 2] |= ((c >> (8 * b)) & 255u) << (8 * (3 - (byte & 3)));
+      }
+    }
+    const uint64_t tk = value_key(target[fd.row0 + r]);
+    k[W - 2] = static_cast<uint32_t>(tk >> 32);
+    k[W - 1] = static_cast<uint32_t>(tk);
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        uint32_t* a = ks + static_cast<size_t>(lo) * W;
+        uint32_t* b = ks + static_cast<size_t>(hi) * W;
+        if (key_less(b, a, W) == up) {
+          for (int w = 0; w < W; ++w) {
+            const uint32_t t = a[w];
+            a[w] = b[w];
+            b[w] = t;
+          }
+          const uint32_t t = ids[lo];
+          ids[lo] = ids[hi];
+          ids[hi] = t;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) canon[fd.pos0 + i] = static_cast<int32_t>(ids[i]);
+}
+
 __global__ void base_kernel(const FamDesc* __restrict__ fam, const double* __restrict__ target_c,
                             double* __restrict__ base, double* __restrict__ pred, const int32_t* __restrict__ ord,
                             int32_t* __restrict__ ord_root) {
   const FamDesc fd = fam[blockIdx.x];
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {
+  if (threadIdx.x == 0) {  // sequential mean in canonical order (costmodel.cpp:185-188)
+    const double* t = target_c + fd.pos0;
     double s = 0.0;
-    for (int i0 = 0; i0 < fd.n; i0 += 32) {
-      const double v = i0 + lane < fd.n ? target_c[fd.pos0 + i0 + lane] : 0.0;
-      const int m = min(32, fd.n - i0);
-      for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, v, l));
+    int i = 0;
+    if (fd.n >= 8) {  // the next 8 loads are in flight while 8 dependent adds run
+      double a[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = t[k];
+      for (i = 8; i + 8 <= fd.n; i += 8) {
+        double b[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) b[k] = t[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = b[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
     }
-    if (lane == 0) base[blockIdx.x] = fd.n ? fs_div(s, static_cast<double>(fd.n)) : 0.0;
+    for (; i < fd.n; ++i) s = fs_add(s, t[i]);
+    base[blockIdx.x] = fd.n ? fs_div(s, static_cast<double>(fd.n)) : 0.0;
   }
   __syncthreads();
   const double b = base[blockIdx.x];
@@ -3275,6 +3365,8 @@ struct ResidentPlan {
   bool atomic = false;  // limb-atomic histogram (default)
   int colh_max = 1;     // its lane-column height (col_height), max over families
   size_t phi_smem = 0;  // tie-class phi table bytes (largest per-feature bin count x 2); 0 = ordered scan
+  std::vector<int> bitonic_ok;  // per family: canonical order by one bitonic sort (else LSD passes)
+  size_t bitonic_smem = 0;
   size_t atomic_smem = 0;
   bool col = false;
   std::vector<int32_t> col_off;  // [F][kColWarps + 1] entry offsets per feature group
@@ -3292,6 +3384,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                 TreeRec* trees_d, double* mse_d, double* base_d, int min_nrep_hint) {
   cudaStream_t s = dev->stream;
   const int sm = dev->sm_count;
+  const size_t bitonic_smem = resident.bitonic_smem;
+  const int* bitonic_ok = bitonic_smem > 0 ? ar.upload(resident.bitonic_ok) : nullptr;
+  if (bitonic_smem > 0)
+    FS_CUDA(cudaFuncSetAttribute(canonical_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bitonic_smem)));
   // rows per histogram CTA: kAtomChunk, shrunk (multiples of kAtomTile) until the root level
   // alone launches >= 2 CTAs per SM - a few large families otherwise leave most SMs idle
   int atom_chunk = kAtomChunk;
@@ -3302,7 +3399,13 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   int32_t* tmp = ar.alloc<int32_t>(std::max<int64_t>(n_tot, total_ord));
   {
     ProfScope prof(dev, "fit_canonical");
-    canonical_kernel<<<F, kSortThreads, 0, s>>>(target_d, codes_all, d, fam_d, rep_orig_d, rep_nb_d, canon, tmp);
+    if (bitonic_smem > 0) {
+      canonical_bitonic_kernel<<<F, kSortThreads, bitonic_smem, s>>>(target_d, codes_all, d, fam_d, rep_orig_d,
+                                                                     rep_nb_d, bitonic_ok, canon);
+      dev->count_launch();
+    }
+    canonical_kernel<<<F, kSortThreads, 0, s>>>(target_d, codes_all, d, fam_d, rep_orig_d, rep_nb_d, canon, tmp,
+                                                bitonic_ok);
   }
   CodeT* codes_c = ar.alloc<CodeT>(static_cast<size_t>(n_tot) * Dp);
   double* target_c = ar.alloc<double>(n_tot);
@@ -3745,6 +3848,23 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
       fail(FS_EINVAL, "fit: resident path requested but the families do not fit one CTA");
   }
   if (phi_bytes <= 96 * 1024 && !std::getenv("FAMSEER_TIE_SCAN")) res.phi_smem = phi_bytes;
+  // canonical order by bitonic sort: families without -0.0 whose packed keys fit shared memory
+  if (!std::getenv("FAMSEER_CANON_LSD")) {
+    res.bitonic_ok.assign(static_cast<size_t>(F), 0);
+    for (int f = 0; f < F; ++f) {
+      const FamDesc& fd = fam[static_cast<size_t>(f)];
+      if (fd.n <= 1 || fd.negz) continue;
+      int wide = 0;
+      for (int j = 0; j < fd.nrep; ++j) wide |= rep_nb[static_cast<size_t>(fd.rep0 + j)] > 256;
+      const int W = (fd.nrep * (wide ? 2 : 1) + 3) / 4 + 2;
+      int P = 1;
+      while (P < fd.n) P <<= 1;
+      const size_t need = static_cast<size_t>(P) * (W + 1) * 4;
+      if (need > 160 * 1024) continue;
+      res.bitonic_ok[static_cast<size_t>(f)] = 1;
+      res.bitonic_smem = std::max(res.bitonic_smem, need);
+    }
+  }
   // Column-layout histogram plan (multi-kernel path): per feature group of 32 the largest bin
   // count; row-group copies while they fit the shared-memory budget.
   // Histogram shape for the multi-kernel path: FAMSEER_HIST = atomic (default) | col | rowmajor.
