@@ -661,7 +661,6 @@ __global__ void base_kernel(const FamDesc* __restrict__ fam, const double* __res
                             double* __restrict__ base, double* __restrict__ pred, const int32_t* __restrict__ ord,
                             int32_t* __restrict__ ord_root) {
   const FamDesc fd = fam[blockIdx.x];
-  const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {  // sequential mean in canonical order (costmodel.cpp:185-188)
     const double* t = target_c + fd.pos0;
     double s = 0.0;
@@ -2284,10 +2283,6 @@ __device__ __forceinline__ double fold_spec(const double* __restrict__ v, const 
   return t;
 }
 
-__device__ __forceinline__ double warp_max_d(double v) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 
 
 __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
@@ -4136,7 +4131,7 @@ int fs_fit(fs_device* dev, fs_forest* fo, int32_t nseg, const int64_t* seg, int3
     const int64_t n = seg[nseg];
     auto* xd = static_cast<double*>(dev->scratch(fs::kSlotH2D0, std::max<int64_t>(n * d, 1) * sizeof(double)));
     auto* yd = static_cast<double*>(dev->scratch(fs::kSlotH2D1, std::max<int64_t>(n, 1) * sizeof(double)));
-    if (n * d) FS_CUDA(cudaMemcpyAsync(xd, x, n * d * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    if (n * d > 0) FS_CUDA(cudaMemcpyAsync(xd, x, n * d * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
     if (n) FS_CUDA(cudaMemcpyAsync(yd, target, n * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
     fs::fit::fit_families(dev, fo, nseg, seg, d, xd, yd, params);
   });
