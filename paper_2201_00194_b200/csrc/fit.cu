@@ -1973,6 +1973,187 @@ __global__ void __launch_bounds__(1024) partition_kernel(
 
 // Leaves: value = (reference-order total) / n (costmodel.cpp:86), prediction += lr * value
 // (:88-90); tree record. One warp per (family, slot).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = fs_add(a, b);
+  const double bb = fs_sub(s, a);
+  e = fs_add(fs_sub(a, fs_sub(s, bb)), fs_sub(b, bb));
+}
+__device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles -> consecutive ints
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : static_cast<long long>(0x8000000000000000ull) - b;
+}
+__device__ __forceinline__ double ord_dbl(long long o) {
+  return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
+}
+// CTA-wide exact sequential fold of a long gathered chain (sum_residuals, costmodel.cpp:36-40) by
+// midpoint speculation (the warp version is fold_spec): the block's double-double sum of
+// x_0..x_{m-1} estimates the exact prefix P; thread 0 folds x_0..x_{m-1} from 0.0 (the true S_m)
+// while threads t = 1..255 fold x_m..x_{n-1} from the doubles P + (t-128) ulp; the thread whose
+// start is bit-identical to S_m holds S_n. A miss finishes the chain from S_m (same result).
+// All 256 threads must call it; the result is returned to every thread.
+__device__ __forceinline__ double warp_fold_gather_from(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                        int n, double s) {
+  // warp_fold_gather with a per-lane start value: every lane folds the same sequence (loaded
+  // cooperatively, 128 gathers in flight ahead of the adds) from its own start
+  const int lane = threadIdx.x & 31;
+  double x[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = 32 * c + lane;
+    x[c] = i < n ? v[idx[i]] : 0.0;
+  }
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    double y[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 128 + 32 * c + lane;
+      y[c] = i < n ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int base = i0 + 32 * c;
+      if (base >= n) break;
+      const int m = min(32, n - base);
+      if (m == 32) {
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          double t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
+        }
+      } else {
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = y[c];
+  }
+  return s;
+}
+
+__device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
+                                                double* red /* smem [2*8+2] */) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = static_cast<int>(blockDim.x >> 5);
+  if (n < 4096 || nw < 2) {  // short chain: warp 0 folds it
+    if (warp == 0) {
+      const double r = warp_fold_gather_from(v, idx, n, 0.0);
+      if (lane == 0) red[16] = r;
+    }
+    __syncthreads();
+    const double r = red[16];
+    __syncthreads();
+    return r;
+  }
+  const int m = n >> 1;
+  // exact-prefix estimate of x_0..x_{m-1}: double-double partial sums (8 gathers in flight)
+  double hi = 0.0, lo = 0.0;
+  for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * blockDim.x;
+      a[k] = i < m ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double s, e;
+      two_sum(hi, a[k], s, e);
+      hi = s;
+      lo = fs_add(lo, e);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, e;
+    two_sum(hi, oh, s, e);
+    hi = s;
+    lo = fs_add(fs_add(lo, ol), e);
+  }
+  if (lane == 0) {
+    red[warp] = hi;
+    red[8 + warp] = lo;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double h = 0.0, l = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      double s, e;
+      two_sum(h, red[w], s, e);
+      h = s;
+      l = fs_add(fs_add(l, red[8 + w]), e);
+    }
+    red[17] = fs_add(h, l);
+  }
+  __syncthreads();
+  const double P = red[17];
+  // warp 0 folds the first half from 0.0 (the true S_m); warps 1.. fold the second half from
+  // the candidate starts P + k ulp, k centred on 0 (32 * (nw - 1) candidates)
+  const int cand = tid - 32;  // 0 .. 32*(nw-1)-1
+  const double start = warp == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (cand - 16 * (nw - 1)));
+  const double r = warp == 0 ? warp_fold_gather_from(v, idx, m, 0.0)
+                             : warp_fold_gather_from(v, idx + m, n - m, start);
+  __shared__ int hit;
+  if (tid == 0) {
+    red[16] = r;  // S_m
+    hit = 0;
+  }
+  __syncthreads();
+  if (warp > 0 && __double_as_longlong(start) == __double_as_longlong(red[16])) {
+    red[17] = r;
+    hit = 1;
+  }
+  __syncthreads();
+  if (!hit && warp == 0) {  // speculation missed: finish from the true midpoint
+    const double t = warp_fold_gather_from(v, idx + m, n - m, red[16]);
+    if (lane == 0) red[17] = t;
+  }
+  __syncthreads();
+  const double out = red[17];
+  __syncthreads();
+  return out;
+}
+
+// Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
+// the leaf's order-0 segment / n (cta_fold_spec), then pred += lr*value over its rows.
+__global__ void __launch_bounds__(256) leaf_cta_kernel(const FamDesc* __restrict__ fam, int F,
+                                                       const FamState* __restrict__ st, NodeRec* __restrict__ nodes,
+                                                       int slots, const int32_t* __restrict__ ord_cur,
+                                                       const double* __restrict__ resid, double* __restrict__ pred,
+                                                       TreeRec* __restrict__ trees) {
+  __shared__ double red[18];
+  const int f = blockIdx.y, s = blockIdx.x;
+  if (f >= F) return;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeLeaf || nd.n == 0) return;
+  if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
+  const int n = nd.n;
+  const int32_t* L = ord_cur + fd.pos0 + nd.seg;
+  const double sum = nd.pad_ ? nd.total : cta_fold_spec(resid + fd.pos0, L, n, red);
+  const double value = fs_div(sum, static_cast<double>(n));
+  const double step = fs_mul(fd.lr, value);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t p = fd.pos0 + L[i];
+    pred[p] = fs_add(pred[p], step);
+  }
+  if (threadIdx.x == 0) {
+    nd.value = value;
+    TreeRec r;
+    r.kind = kNodeLeaf;
+    r.feature = -1;
+    r.threshold = 0.0;
+    r.value = value;
+    r.gain = 0.0;
+    r.rep = -1;
+    r.bin = 0;
+    trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = r;
+  }
+}
+
 __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamState* __restrict__ st,
                             NodeRec* __restrict__ nodes, int slots, const int32_t* __restrict__ ord_cur,
                             const double* __restrict__ resid, double* __restrict__ pred, TreeRec* __restrict__ trees) {
@@ -2222,18 +2403,6 @@ __device__ __forceinline__ double fold_seq(const double* __restrict__ v, const u
 //   3. the lane whose start is bit-identical to S_m holds the exact S_n (the fold is a function
 //      of its start); if none is, the warp continues sequentially from S_m (same result, no
 //      saving). Every add is still the reference's separately rounded sequential one.
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-  s = fs_add(a, b);
-  const double bb = fs_sub(s, a);
-  e = fs_add(fs_sub(a, fs_sub(s, bb)), fs_sub(b, bb));
-}
-__device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles -> consecutive ints
-  const long long b = __double_as_longlong(x);
-  return b >= 0 ? b : static_cast<long long>(0x8000000000000000ull) - b;
-}
-__device__ __forceinline__ double ord_dbl(long long o) {
-  return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
-}
 __device__ __forceinline__ double fold_spec(const double* __restrict__ v, const uint16_t* __restrict__ idx, int n) {
   const int lane = threadIdx.x & 31;
   if (n < 192) return fold_seq(v, idx, n);
@@ -3587,8 +3756,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
     const int64_t leaf_threads = static_cast<int64_t>(F) * slots * 32;
     {
       ProfScope prof(dev, "fit_leaf");
-      leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
-                                                                                       ord_cur, resid, pred, trees_d);
+      if (std::getenv("FAMSEER_LEAF_WARP"))
+        leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
+                                                                                         ord_cur, resid, pred, trees_d);
+      else
+        leaf_cta_kernel<<<dim3(static_cast<unsigned>(slots), F), 256, 0, s>>>(fam_d, F, st_d, nodes, slots, ord_cur,
+                                                                               resid, pred, trees_d);
     }
     mse_partial_kernel<<<dim3(static_cast<unsigned>(mse_blocks), F), 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred,
                                                                               mse_part, mse_blocks);
