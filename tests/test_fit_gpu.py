@@ -142,7 +142,7 @@ def test_signed_zero_features(dev, orc):
                               getattr(exp, k).view(np.int64) if getattr(exp, k).dtype == np.float64 else getattr(exp, k)), k
 
 
-@pytest.mark.parametrize("depth,min_split", [(1, 2), (5, 2), (6, 30), (0, 2)])
+@pytest.mark.parametrize("depth,min_split", [(1, 2), (5, 2), (6, 30), (0, 2), (9, 2)])
 def test_depth_and_min_split(dev, orc, depth, min_split):
     doc = load_spaces("bert_large_sim")
     members = families(doc)[1]
@@ -160,3 +160,16 @@ def test_fit_stats_reported(dev, orc):
     fo.fit(x, y)
     screened, exact = fo.fit_stats(0)
     assert screened + exact > 0
+
+
+@pytest.mark.parametrize("tag", CASES[:4])
+def test_host_compile_epilogue(dev, orc, monkeypatch, tag):
+    """FAMSEER_HOST_COMPILE=1: tree tables read back and compiled on the host (the fallback the
+    device epilogue replaces; also what deeper-than-7 trees use) - same trees, same scores."""
+    monkeypatch.setenv("FAMSEER_HOST_COMPILE", "1")
+    x, y = G[f"fit_{tag}_x"], G[f"fit_{tag}_y"]
+    trees = int(G[f"fit_{tag}_trees"][0])
+    fo = fs.Forest(dev, 1)
+    fo.fit(x, y, params=fs.GbtParams(trees, 3, 0.1, 2))
+    assert np.array_equal(fo.export(0).feature, G[f"fit_{tag}_feature"])
+    assert np.array_equal(fo.predict(x), G[f"fit_{tag}_pred"])
