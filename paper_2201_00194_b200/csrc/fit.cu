@@ -1726,6 +1726,117 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 // One warp per item: reference-order folds. Item rep < 0: node total over the order-0 list
 // (sum_residuals(order[0]), costmodel.cpp:47). Item rep j: best_split's left sums over feature j's
 // presorted list restricted to the node (:50-55), recorded at every value boundary.
+// exact folds of nodes below a quarter of the family go through exact_small_kernel
+__device__ __forceinline__ bool exact_is_small(int nv, int n) { return static_cast<int64_t>(nv) * 4 < n; }
+
+// Exact reference-order folds for SMALL nodes (nv * 4 < n): instead of scanning the feature's
+// full presorted list for the node's members (exact_kernel; costs O(n) gathers per item however
+// small the node), a CTA compacts the node's rows in canonical order (a coalesced scan of the
+// node ids), stable-sorts them by the feature's code (the presorted order restricted to the
+// node is exactly (code, canonical position) order), and warp 0 folds them - the same adds in
+// the same order as best_split (costmodel.cpp:50-69), stopping at the last window candidate.
+template <typename CodeT>
+__global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
+    const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const double* __restrict__ resid, const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_boff,
+    double* __restrict__ lbuf, const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
+    int32_t* __restrict__ scratch, int n_max) {
+  __shared__ SortSmem sm;
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total = *n_items;
+  sort_smem_init(sm);
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const ExactItem it = items[w];
+    if (it.rep < 0) continue;
+    const FamDesc fd = fam[it.fam];
+    const NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int nv = nd.n, n = fd.n;
+    if (!exact_is_small(nv, n)) continue;
+    const int jj = it.rep;
+    const int local = it.slot - ((1 << level) - 1);
+    const int need = win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + jj].maxlc;
+    double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    int32_t* A = scratch + static_cast<int64_t>(blockIdx.x) * 2 * n_max;
+    int32_t* B = A + n_max;
+    // 1. the node's rows in canonical order
+    int base = 0;
+    for (int p0 = 0; p0 < n; p0 += blockDim.x) {
+      const int p = p0 + tid;
+      const bool mem = p < n && nodeid[fd.pos0 + p] == it.slot;
+      const unsigned m = __ballot_sync(0xffffffffu, mem);
+      if (lane == 0) wsum[warp] = __popc(m);
+      __syncthreads();
+      if (warp == 0) {
+        const int v = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+        int incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        wsum[lane] = incl - v;
+        if (lane == 31) sm.uniform = incl;  // chunk total (borrowed field)
+      }
+      __syncthreads();
+      if (mem) A[base + wsum[warp] + __popc(m & ((1u << lane) - 1u))] = p;
+      base += sm.uniform;
+      __syncthreads();
+    }
+    // 2. stable sort by the feature's code: (code, canonical position) = presorted order
+    const CodeT* cj = codes_c + static_cast<int64_t>(fd.pos0) * Dp + jj;
+    int32_t* src = A;
+    int32_t* dst = B;
+    if (stable_digit_pass([&](int i) { return src[i]; }, dst, nv,
+                          [&](int p) { return static_cast<int>(cj[static_cast<int64_t>(p) * Dp] & 255u); }, sm)) {
+      int32_t* t = src;
+      src = dst;
+      dst = t;
+    }
+    __syncthreads();
+    if (sizeof(CodeT) == 2) {
+      if (stable_digit_pass([&](int i) { return src[i]; }, dst, nv,
+                            [&](int p) { return static_cast<int>(cj[static_cast<int64_t>(p) * Dp] >> 8); }, sm)) {
+        int32_t* t = src;
+        src = dst;
+        dst = t;
+      }
+      __syncthreads();
+    }
+    // 3. the fold (warp 0; members in list order, boundaries at code changes)
+    if (warp == 0) {
+      double left = 0.0;
+      int prev = -1;
+      for (int i0 = 0; i0 < need; i0 += 32) {
+        const int i = i0 + lane;
+        const int p = i < need ? src[i] : 0;
+        const int code = i < need ? static_cast<int>(cj[static_cast<int64_t>(p) * Dp]) : 0;
+        const double rv = i < need ? resid[fd.pos0 + p] : 0.0;
+        const int cnt = min(32, need - i0);
+        for (int l0 = 0; l0 < cnt; l0 += 8) {
+          int cc[8];
+          double vv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            cc[k] = __shfl_sync(0xffffffffu, code, l0 + k);
+            vv[k] = __shfl_sync(0xffffffffu, rv, l0 + k);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (l0 + k < cnt) {
+              if (prev >= 0 && cc[k] != prev && lane == 0) out[prev] = left;
+              left = fs_add(left, vv[k]);
+              prev = cc[k];
+            }
+          }
+        }
+      }
+      if (lane == 0 && prev >= 0) out[prev] = left;  // the last window boundary
+    }
+    __syncthreads();
+  }
+}
+
 template <typename CodeT>
 __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes,
                                                     const ExactItem* __restrict__ items, const int* __restrict__ n_items,
@@ -1735,7 +1846,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
                                                     const int16_t* __restrict__ nodeid,
                                                     const int32_t* __restrict__ rep_boff, double* __restrict__ lbuf,
                                                     const WinRec* __restrict__ win, int nrep_max,
-                                                    int level_slots_max) {
+                                                    int level_slots_max, int small_path) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int total = *n_items;
@@ -1749,6 +1860,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
       if (lane == 0) nd.total = s;
       continue;
     }
+    if (exact_is_small(n, fd.n) && small_path) continue;  // exact_small_kernel folds it
     const int jj = it.rep;
     const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
     const int local = it.slot - ((1 << level) - 1);
@@ -2210,6 +2322,7 @@ __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamSta
 // blocks of kMseRows rows per family produce partials (block tree reduction), mse_final_kernel
 // adds them in block order; it also commits the tree or applies the early stop (:212).
 constexpr int kMseRows = 2048;
+constexpr int kExactSmallCtas = 64;  // CTAs of exact_small_kernel (items loop over them)
 __device__ __forceinline__ bool round_commits(const FamDesc& fd, const FamState& st, const NodeRec* nodes) {
   if (!st.active) return false;
   const NodeRec& root = nodes[fd.node0];
@@ -3664,6 +3777,10 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   const int mse_blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(n_max, kMseRows)));
   double* mse_part = ar.alloc<double>(static_cast<size_t>(F) * mse_blocks);
   const bool fork_totals = std::getenv("FAMSEER_FORK_TOTALS") != nullptr;
+  // small-node exact folds (exact_small_kernel): per-CTA scratch of two n_max index buffers
+  int32_t* small_scratch = std::getenv("FAMSEER_EXACT_SCAN")
+                               ? nullptr
+                               : ar.alloc<int32_t>(static_cast<size_t>(kExactSmallCtas) * 2 * std::max(n_max, 1));
   cudaStream_t aux = fork_totals ? dev->aux_stream() : nullptr;
   auto round_body = [&]() {
     round_init_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, slots, trees_d);
@@ -3740,7 +3857,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         ProfScope prof(dev, "fit_exact");
         exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord,
                                                    ord_cur, nodeid, rep_boff_d, lbuf, win, std::max(nrep_max, 1),
-                                                   level_slots_max);
+                                                   level_slots_max, small_scratch ? 1 : 0);
+        if (small_scratch)
+          exact_small_kernel<CodeT><<<kExactSmallCtas, kSortThreads, 0, s>>>(
+              fam_d, nodes, items, n_items, level, Dp, codes_c, resid, nodeid, rep_boff_d, lbuf, win,
+              std::max(nrep_max, 1), level_slots_max, small_scratch, n_max);
       }
       exact_decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt,
                                                                            rep_boff_d, rep_nb_d, win,
