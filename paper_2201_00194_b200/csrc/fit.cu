@@ -1727,7 +1727,7 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 // (sum_residuals(order[0]), costmodel.cpp:47). Item rep j: best_split's left sums over feature j's
 // presorted list restricted to the node (:50-55), recorded at every value boundary.
 // exact folds of nodes below a quarter of the family go through exact_small_kernel
-__device__ __forceinline__ bool exact_is_small(int nv, int n) { return static_cast<int64_t>(nv) * 4 < static_cast<int64_t>(n) * 3; }
+__device__ __forceinline__ bool exact_is_small(int nv, int n) { return nv < n; }
 
 // Exact reference-order folds for SMALL nodes (nv * 4 < n): instead of scanning the feature's
 // full presorted list for the node's members (exact_kernel; costs O(n) gathers per item however
