@@ -2041,13 +2041,16 @@ __global__ void __launch_bounds__(1024) partition_kernel(
   for (int i = tid; i < n; i += blockDim.x) src[i] = dst[i];
   __syncthreads();
   const int16_t cl = static_cast<int16_t>(2 * s + 1), cr = static_cast<int16_t>(2 * s + 2);
+  // the next chunk's index and code gathers are issued before this chunk's scan and scatter
+  int p_nx = tid < n ? src[tid] : 0;
+  int c_nx = tid < n ? static_cast<int>(codes_c[(fd.pos0 + p_nx) * Dp + jj]) : 0;
   for (int t0 = 0; t0 < n; t0 += blockDim.x) {
     const int i = t0 + tid;
-    int p = 0;
-    bool left = false;
-    if (i < n) {
-      p = src[i];
-      left = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + jj]) <= bin;
+    const int p = p_nx;
+    const bool left = i < n && c_nx <= bin;
+    if (i + static_cast<int>(blockDim.x) < n) {
+      p_nx = src[i + blockDim.x];
+      c_nx = static_cast<int>(codes_c[(fd.pos0 + p_nx) * Dp + jj]);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, left);
     if (lane == 0) wsum[warp] = __popc(bal);
