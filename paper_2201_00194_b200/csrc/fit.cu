@@ -2251,9 +2251,21 @@ __global__ void __launch_bounds__(256) leaf_cta_kernel(const FamDesc* __restrict
   const double sum = nd.pad_ ? nd.total : cta_fold_spec(resid + fd.pos0, L, n, red);
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int64_t p = fd.pos0 + L[i];
-    pred[p] = fs_add(pred[p], step);
+  // prediction update, 8 rows per thread in flight (index and prediction gathers issued before
+  // the stores: the compiler cannot prove the arrays do not alias)
+  for (int i0 = 0; i0 < n; i0 += 8 * static_cast<int>(blockDim.x)) {
+    int64_t pp[8];
+    double pv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * blockDim.x + threadIdx.x;
+      pp[k] = i < n ? fd.pos0 + L[i] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pv[k] = pp[k] >= 0 ? pred[pp[k]] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (pp[k] >= 0) pred[pp[k]] = fs_add(pv[k], step);
   }
   if (threadIdx.x == 0) {
     nd.value = value;
