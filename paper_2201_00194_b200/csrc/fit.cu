@@ -2405,6 +2405,7 @@ namespace {
 constexpr int kResThreads = FS_RES_THREADS;
 constexpr int kResWarps = kResThreads / 32;
 constexpr int kPartE = 4;  // partition: consecutive order-0 entries per thread per chunk
+constexpr int kSpecBufs = 4;  // warps whose single-candidate exact folds use the speculative split
 // Resident histogram precision: FS_RES_LIMBS 3 = the multi-kernel's 62-bit fixed point (three
 // 21-bit limbs per update); 2 = 39-bit fixed point (n * max|v| < 2^39, two limbs per update -
 // a third fewer shared atomics; the screen bound widens with the quantum, so near-ties are
@@ -2426,7 +2427,7 @@ struct ResNode {
 
 struct ResLayout {
   int ls, slots, cs;
-  size_t codes, resid, pred, predv, targ, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, stage, clc, binrep,
+  size_t codes, resid, pred, predv, targ, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, sbuf, stage, clc, binrep,
       vals, cand, total;
 };
 
@@ -2435,7 +2436,7 @@ __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_
 // groups: private histogram copies used while accumulating one node (threads own
 // (feature, group) pairs, so no shared-memory atomics are needed).
 __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, int colh, bool pred_smem,
-                                                bool pre_smem) {
+                                                bool pre_smem, int spec_bufs = 0) {
   ResLayout L;
   L.ls = depth > 0 ? (1 << (depth - 1)) : 1;
   L.slots = (1 << (depth + 1)) - 1;
@@ -2480,6 +2481,8 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
                // column offset per rep
   o = res_align(o + std::max<size_t>(static_cast<size_t>(3) * colh * 32 * 4 + static_cast<size_t>(L.ls) * 4 * 4 + nr * 4,
                                       8 * 512));
+  L.sbuf = o;  // speculative exact folds: spec_bufs member lists of up to n rows (u16)
+  o = res_align(o + static_cast<size_t>(spec_bufs) * n * 2);
   L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
   o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
   L.clc = o;  // left count per (node at level, bin)
@@ -2589,7 +2592,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
     const int32_t* __restrict__ cle, const int32_t* __restrict__ canon, const double* __restrict__ x, int d,
     TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
-    unsigned long long* __restrict__ ctr, int pred_smem, double* __restrict__ pred_g, int pre_smem) {
+    unsigned long long* __restrict__ ctr, int pred_smem, double* __restrict__ pred_g, int pre_smem, int spec_bufs) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ unsigned long long s_red[32];
   __shared__ double s_dred[32];
@@ -2601,7 +2604,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
   const int colh = nrep > 0 ? col_height(nrep, rep_nb + fd.rep0, nullptr) : 1;
-  const ResLayout Lo = res_layout(n, nrep, bins, depth, colh, pred_smem != 0, pre_smem != 0);
+  const ResLayout Lo = res_layout(n, nrep, bins, depth, colh, pred_smem != 0, pre_smem != 0, spec_bufs);
+  uint16_t* s_sbuf = reinterpret_cast<uint16_t*>(sm + Lo.sbuf);
   uint8_t* s_codes = sm + Lo.codes;  // [nrep][cs]
   const int cs = Lo.cs;
   uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [3][colh][32]
@@ -3161,6 +3165,28 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           const int need = s_win[(s - first) * nrep + j].maxlc;
           double* out = s_lbuf + static_cast<size_t>(s - first) * bins + s_repb[j];
           const uint8_t* cj = s_codes + static_cast<size_t>(j) * cs;
+          if (warp < spec_bufs && s_win[(s - first) * nrep + j].count == 1) {
+            // one window candidate: only L at its left count is needed. Compact the node's
+            // members of the feature's presorted list (in list order) into this warp's buffer,
+            // then fold them with the speculative midpoint split (fold_spec).
+            uint16_t* buf = s_sbuf + static_cast<size_t>(warp) * n;
+            int got = 0;
+            int p_nx = lane < n ? pre_at(j, lane) : 0;
+            for (int i0 = 0; i0 < n && got < need; i0 += 32) {
+              const int i = i0 + lane;
+              const int p = p_nx;
+              p_nx = i + 32 < n ? pre_at(j, i + 32) : 0;
+              const bool mem = i < n && s_node[p] == s;
+              const unsigned m = __ballot_sync(0xffffffffu, mem);
+              const int dst = got + __popc(m & ((1u << lane) - 1u));
+              if (mem && dst < need) buf[dst] = static_cast<uint16_t>(p);
+              got += __popc(m);
+            }
+            __syncwarp();
+            const double L = fold_spec(s_resid, buf, need);
+            if (lane == 0) out[s_win[(s - first) * nrep + j].best_bin] = L;
+            continue;
+          }
           double left = 0.0;
           int prev = -1, seen = 0;
           int p_next = lane < n ? pre_at(j, lane) : 0;
@@ -3653,6 +3679,7 @@ struct ResidentPlan {
   size_t smem = 0;
   bool pred_smem = false;
   bool pre_smem = false;
+  int spec_bufs = 0;  // warps with a speculative exact-fold member buffer
   // column-layout histogram plan for the multi-kernel path (hist_build_col_kernel)
   bool atomic = false;  // limb-atomic histogram (default)
   int colh_max = 1;     // its lane-column height (col_height), max over families
@@ -3729,7 +3756,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       fit_resident_kernel<<<static_cast<unsigned>(resident.families.size()), kResThreads, resident.smem, s>>>(
           fam_d, st_d, list_d, Dp, reinterpret_cast<const uint8_t*>(codes_c), target_c, base_d, ord, ord_root,
           rep_orig_d, rep_nb_d, rep_boff_d, vals_d, cle, canon, x_d, d, trees_d, mse_d, max_trees, slots, dev->ctr_d,
-          resident.pred_smem ? 1 : 0, pred, resident.pre_smem ? 1 : 0);
+          resident.pred_smem ? 1 : 0, pred, resident.pre_smem ? 1 : 0, resident.spec_bufs);
     }
     dev->count_launch();
     FS_CUDA(cudaGetLastError());
@@ -4123,9 +4150,11 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
       // Shared-memory staging options, most valuable first: the running predictions (read and
       // updated every round) and the presorted lists (reference-order folds); whatever does not
       // fit stays in global memory (L2-resident).
-      const bool opts[4][2] = {{true, true}, {true, false}, {false, true}, {false, false}};
+      const int opts[8][3] = {{1, 1, kSpecBufs}, {1, 1, 0}, {1, 0, kSpecBufs}, {1, 0, 0},
+                              {0, 1, kSpecBufs}, {0, 1, 0},  {0, 0, kSpecBufs}, {0, 0, 0}};
       for (const auto& op : opts) {
-        const bool pred_smem = op[0], pre_smem = op[1];
+        const bool pred_smem = op[0] != 0, pre_smem = op[1] != 0;
+        const int spec = std::getenv("FAMSEER_NO_SPEC") ? 0 : op[2];
         bool ok = true;
         const size_t budget = 225 * 1024;
         std::vector<int> fams_ok;
@@ -4135,7 +4164,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
           if (fd.n <= 0 || fd.trees <= 0) continue;
           if (fd.n > 65535 || fd.nrep > kResThreads) ok = false;
           const int colh = fd.nrep > 0 ? col_height(fd.nrep, rep_nb.data() + fd.rep0, nullptr) : 1;
-          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, colh, pred_smem, pre_smem).total);
+          need = std::max(need, res_layout(fd.n, fd.nrep, fd.bins, fd.depth, colh, pred_smem, pre_smem, spec).total);
           fams_ok.push_back(f);
         }
         res.families = fams_ok;
@@ -4144,6 +4173,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
           res.smem = need;
           res.pred_smem = pred_smem;
           res.pre_smem = pre_smem;
+          res.spec_bufs = spec;
           break;
         }
       }
