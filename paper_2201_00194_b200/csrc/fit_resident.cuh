@@ -1,0 +1,1097 @@
+// fit_resident.cuh - the resident trainer: one CTA per family runs every boosting round (C1-C3)
+// Part of the trainer translation unit: included once, by fit.cu only (shares its
+// anonymous namespace, constants and helpers).
+#pragma once
+
+
+// ==========================================================================================
+// resident trainer: one CTA per family runs EVERY boosting round of the fit in a single launch,
+// with all per-row state in shared memory. For families of up to a few thousand rows (configs
+// C1-C3) the multi-kernel round above is launch- and L2-latency-bound (~40 launches per round);
+// here a round is ~30 block barriers. Same algorithm, same arithmetic, same tie handling.
+// ==========================================================================================
+#ifndef FS_RES_THREADS
+#define FS_RES_THREADS 512
+#endif
+namespace fs {
+namespace fit {
+namespace {
+
+constexpr int kResThreads = FS_RES_THREADS;
+constexpr int kResWarps = kResThreads / 32;
+constexpr int kPartE = 4;  // partition: consecutive order-0 entries per thread per chunk
+constexpr int kSpecBufs = 4;  // warps whose single-candidate exact folds use the speculative split
+// Resident histogram precision: FS_RES_LIMBS 3 = the multi-kernel's 62-bit fixed point (three
+// 21-bit limbs per update); 2 = 39-bit fixed point (n * max|v| < 2^39, two limbs per update -
+// a third fewer shared atomics; the screen bound widens with the quantum, so near-ties are
+// re-evaluated exactly as before).
+#ifndef FS_RES_LIMBS
+#define FS_RES_LIMBS 3
+#endif
+constexpr int kResLimbs = FS_RES_LIMBS;
+constexpr int kResBias = kResLimbs == 3 ? 62 : 40;  // u = v + 2^bias, count = round(U / 2^bias)
+constexpr int kResMaxDepth = 7;  // node ids fit in uint8
+
+struct ResNode {
+  int32_t n, seg, state, rep, bin, lc, wcount, build;
+  int32_t eqf0, pad_;  // lowest window feature when the window may be one tie class, else -1
+  double gain, value, total;
+  unsigned long long lokey;
+  unsigned long long absfix;
+};
+
+struct ResLayout {
+  int ls, slots, cs;
+  size_t codes, resid, pred, predv, targ, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, sbuf, stage, clc, binrep,
+      vals, cand, total;
+};
+
+__host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
+
+// groups: private histogram copies used while accumulating one node (threads own
+// (feature, group) pairs, so no shared-memory atomics are needed).
+__host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int depth, int colh, bool pred_smem,
+                                                bool pre_smem, int spec_bufs = 0) {
+  ResLayout L;
+  L.ls = depth > 0 ? (1 << (depth - 1)) : 1;
+  L.slots = (1 << (depth + 1)) - 1;
+  const size_t nr = nrep > 0 ? static_cast<size_t>(nrep) : 1;
+  size_t o = 0;
+  // codes [nrep][cs]: cs = 4 (mod 128) so the lanes reading one row's codes of consecutive
+  // features fall in consecutive banks
+  L.cs = ((n + 127) & ~127) + 4;
+  L.codes = o;
+  o = res_align(o + static_cast<size_t>(L.cs) * nr);
+  L.resid = o;
+  o = res_align(o + static_cast<size_t>(n) * 8);
+  L.pred = o;  // presorted lists [nrep][n] as u16 (when pre_smem), else empty
+  o = res_align(o + (pre_smem ? static_cast<size_t>(n) * nr * 2 : 0));
+  L.predv = o;  // running predictions (when pred_smem), else they live in global memory
+  o = res_align(o + (pred_smem ? static_cast<size_t>(n) * 8 : 0));
+  L.targ = o;  // canonical targets and the root order-0 list, staged with the predictions
+  o = res_align(o + (pred_smem ? static_cast<size_t>(n) * 10 : 0));
+  L.fix = o;
+  o = res_align(o + static_cast<size_t>(n) * 8);
+  L.node = o;
+  o = res_align(o + static_cast<size_t>(n));
+  L.ord0 = o;
+  o = res_align(o + static_cast<size_t>(n) * 2);
+  L.scratch = o;
+  o = res_align(o + static_cast<size_t>(n) * 2);
+  L.hsum = o;
+  o = res_align(o + static_cast<size_t>(2) * L.ls * bins * 8);
+  L.hcnt = o;
+  o = res_align(o + static_cast<size_t>(2) * L.ls * bins * 4);
+  L.lbuf = o;
+  o = res_align(o + static_cast<size_t>(L.ls) * bins * 8);
+  L.nodes = o;
+  o = res_align(o + static_cast<size_t>(L.slots) * sizeof(ResNode));
+  L.win = o;
+  o = res_align(o + static_cast<size_t>(L.ls) * nr * sizeof(WinRec));
+  L.items = o;
+  o = res_align(o + static_cast<size_t>(L.ls) * (nr + 1) * sizeof(int));
+  L.rep = o;
+  o = res_align(o + 2 * nr * sizeof(int));
+  L.limb = o;  // lane-column limb histogram [3][colh][32] u32, 4 x 16-bit limbs of sum |v| per level node,
+               // column offset per rep
+  o = res_align(o + std::max<size_t>(static_cast<size_t>(3) * colh * 32 * 4 + static_cast<size_t>(L.ls) * 4 * 4 + nr * 4,
+                                      8 * 512));
+  L.sbuf = o;  // speculative exact folds: spec_bufs member lists of up to n rows (u16)
+  o = res_align(o + static_cast<size_t>(spec_bufs) * n * 2);
+  L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
+  o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
+  L.clc = o;  // left count per (node at level, bin)
+  o = res_align(o + static_cast<size_t>(L.ls) * bins * 4);
+  L.binrep = o;  // feature (rep) of every bin
+  o = res_align(o + static_cast<size_t>(bins) * 2);
+  L.vals = o;  // threshold value of every bin + original feature of every rep (split records)
+  o = res_align(o + static_cast<size_t>(bins) * 8 + nr * 4);
+  L.cand = o;  // screened (gain, bound) per (node at level, bin)
+  o = res_align(o + static_cast<size_t>(L.ls) * bins * 16);
+  L.total = o;
+  return L;
+}
+
+// sum_residuals (costmodel.cpp:36-40) over a shared-memory index list, by ONE thread: the fold
+// order is the list order and every add is rounded separately. Loads of the next 8 elements are
+// issued before the current 8 adds, so the loop runs at the FP64 add latency instead of the
+// load latency.
+__device__ __forceinline__ double fold_seq(const double* __restrict__ v, const uint16_t* __restrict__ idx, int n) {
+  double s = 0.0;
+  int i = 0;
+  if (n >= 8) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = v[idx[k]];
+    for (i = 8; i + 8 <= n; i += 8) {
+      double b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[k] = v[idx[i + k]];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = b[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+  }
+  for (; i < n; ++i) s = fs_add(s, v[idx[i]]);
+  return s;
+}
+
+// Warp-collective exact sequential fold (sum_residuals, costmodel.cpp:36-40) of a long chain in
+// about half the dependent-add latency, by speculation on the midpoint value:
+//   1. every lane accumulates a strided part of x_0..x_{m-1} in double-double (TwoSum); the warp
+//      reduction gives P ~= the EXACT prefix sum (the sequential result differs from it only by
+//      the chain's accumulated roundings, typically a few ulps);
+//   2. lane 0 folds x_0..x_{m-1} from 0.0 - the true S_m - while lanes 1..31 fold x_m..x_{n-1}
+//      from the 31 doubles P-15ulp .. P+15ulp, all in the same loop;
+//   3. the lane whose start is bit-identical to S_m holds the exact S_n (the fold is a function
+//      of its start); if none is, the warp continues sequentially from S_m (same result, no
+//      saving). Every add is still the reference's separately rounded sequential one.
+__device__ __forceinline__ double fold_spec(const double* __restrict__ v, const uint16_t* __restrict__ idx, int n) {
+  const int lane = threadIdx.x & 31;
+  if (n < 192) return fold_seq(v, idx, n);
+  const int m = n >> 1;
+  double hi = 0.0, lo = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    double s, e;
+    two_sum(hi, v[idx[i]], s, e);
+    hi = s;
+    lo = fs_add(lo, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, e;
+    two_sum(hi, oh, s, e);
+    hi = s;
+    lo = fs_add(fs_add(lo, ol), e);
+  }
+  const double P = fs_add(hi, lo);
+  const double start = lane == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (lane - 16));
+  const uint16_t* seq = idx + (lane == 0 ? 0 : m);
+  const int len = lane == 0 ? m : n - m;  // n - m is m or m + 1
+  double s = start;
+  {
+    int i = 0;
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = v[seq[k]];
+    for (i = 8; i + 8 <= m; i += 8) {
+      double b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[k] = v[seq[i + k]];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = b[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+    for (; i < len; ++i) s = fs_add(s, v[seq[i]]);
+  }
+  const double Sm = __shfl_sync(0xffffffffu, s, 0);
+  const unsigned hit = __ballot_sync(0xffffffffu, lane != 0 && __double_as_longlong(start) == __double_as_longlong(Sm));
+  if (hit) return __shfl_sync(0xffffffffu, s, __ffs(hit) - 1);
+  double t = Sm;  // speculation missed: finish the chain from the true midpoint
+  for (int i = m; i < n; ++i) t = fs_add(t, v[idx[i]]);
+  return t;
+}
+
+
+
+__global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
+    const FamDesc* __restrict__ fam, FamState* __restrict__ st, const int* __restrict__ fam_list, int Dp,
+    const uint8_t* __restrict__ codes_c, const double* __restrict__ target_c, const double* __restrict__ base,
+    const int32_t* __restrict__ ord, const int32_t* __restrict__ ord_root, const int32_t* __restrict__ rep_orig,
+    const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
+    const int32_t* __restrict__ cle, const int32_t* __restrict__ canon, const double* __restrict__ x, int d,
+    TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
+    unsigned long long* __restrict__ ctr, int pred_smem, double* __restrict__ pred_g, int pre_smem, int spec_bufs) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ unsigned long long s_red[32];
+  __shared__ double s_dred[32];
+  __shared__ int s_wsum[32];
+  __shared__ int s_shift, s_nitems, s_ctot;
+  __shared__ unsigned long long s_cnt[3];  // screened splits, exact nodes, exact folds
+  __shared__ unsigned long long s_why[4];  // exact-node reasons
+  const int f = fam_list[blockIdx.x];
+  const FamDesc fd = fam[f];
+  const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
+  const int colh = nrep > 0 ? col_height(nrep, rep_nb + fd.rep0, nullptr) : 1;
+  const ResLayout Lo = res_layout(n, nrep, bins, depth, colh, pred_smem != 0, pre_smem != 0, spec_bufs);
+  uint16_t* s_sbuf = reinterpret_cast<uint16_t*>(sm + Lo.sbuf);
+  uint8_t* s_codes = sm + Lo.codes;  // [nrep][cs]
+  const int cs = Lo.cs;
+  uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [3][colh][32]
+  uint32_t* s_absl = s_limb + 3 * colh * 32;                      // [level node][4]
+  int* s_cofs = reinterpret_cast<int*>(s_absl + Lo.ls * 4);        // [nrep]
+  double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
+  int* s_clc = reinterpret_cast<int*>(sm + Lo.clc);           // [level node][bin] left count
+  uint16_t* s_binrep = reinterpret_cast<uint16_t*>(sm + Lo.binrep);
+  double* s_vals = reinterpret_cast<double*>(sm + Lo.vals);
+  int* s_rorig = reinterpret_cast<int*>(s_vals + bins);
+  __shared__ int s_neq;
+  // phase timers (CTA 0, thread 0): where a round's cycles go (fs_device_counters [4..15])
+  __shared__ long long s_ph[12];
+  // Phase clock: __syncthreads() is BAR.SYNC.DEFER_BLOCKING - a warp only blocks at the first
+  // dependent instruction after it - so a bare clock read right after a barrier would bill the
+  // barrier wait to the NEXT phase. The read takes a register input loaded from shared memory
+  // after the barrier (the load cannot complete before the barrier does); memory clobber keeps
+  // the compiler from moving work across it.
+  __shared__ int s_clkdep;
+  auto clk = [&]() {
+    long long t;
+    const int dep = *reinterpret_cast<volatile int*>(&s_clkdep);
+    asm volatile("add.s32 %1, %1, 0;\n\tmov.u64 %0, %%clock64;" : "=l"(t) : "r"(dep) : "memory");
+    return t;
+  };
+  if (threadIdx.x == 0) s_clkdep = 0;
+  long long t_prev = clock64();
+  if (threadIdx.x < 12) s_ph[threadIdx.x] = 0;
+#define RES_PHASE(i)                        \
+  do {                                      \
+    if (tid == 0) {                         \
+      const long long t_ = clk();           \
+      s_ph[i] += t_ - t_prev;               \
+      t_prev = t_;                          \
+    }                                       \
+  } while (0)
+  double* s_resid = reinterpret_cast<double*>(sm + Lo.resid);
+  // running predictions: shared memory when they fit, else global (L2-resident); the targets
+  // and the root order-0 list are staged with them (read every round)
+  double* s_pred = pred_smem ? reinterpret_cast<double*>(sm + Lo.predv) : pred_g + fd.pos0;
+  const double* s_targ = target_c + fd.pos0;
+  const int32_t* g_ordr = ord_root + fd.pos0;
+  uint16_t* s_ordr = nullptr;
+  if (pred_smem) {
+    double* t = reinterpret_cast<double*>(sm + Lo.targ);
+    s_ordr = reinterpret_cast<uint16_t*>(t + n);
+    for (int p = threadIdx.x; p < n; p += kResThreads) {
+      t[p] = target_c[fd.pos0 + p];
+      s_ordr[p] = static_cast<uint16_t>(ord_root[fd.pos0 + p]);
+    }
+    s_targ = t;
+  }
+  uint16_t* s_pre = reinterpret_cast<uint16_t*>(sm + Lo.pred);  // presorted lists, if staged
+  const int32_t* g_pre = ord + fd.ord0;
+  auto pre_at = [&](int j, int i) -> int {
+    return pre_smem ? static_cast<int>(s_pre[static_cast<size_t>(j) * n + i]) : g_pre[static_cast<size_t>(j) * n + i];
+  };
+  long long* s_fix = reinterpret_cast<long long*>(sm + Lo.fix);
+  uint8_t* s_node = sm + Lo.node;
+  uint16_t* s_ord0 = reinterpret_cast<uint16_t*>(sm + Lo.ord0);
+  uint16_t* s_scr = reinterpret_cast<uint16_t*>(sm + Lo.scratch);
+  long long* s_hsum = reinterpret_cast<long long*>(sm + Lo.hsum);
+  int* s_hcnt = reinterpret_cast<int*>(sm + Lo.hcnt);
+  double* s_lbuf = reinterpret_cast<double*>(sm + Lo.lbuf);
+  ResNode* s_nodes = reinterpret_cast<ResNode*>(sm + Lo.nodes);
+  WinRec* s_win = reinterpret_cast<WinRec*>(sm + Lo.win);
+  int* s_items = reinterpret_cast<int*>(sm + Lo.items);
+  int* s_repb = reinterpret_cast<int*>(sm + Lo.rep);
+  int* s_repn = s_repb + (nrep > 0 ? nrep : 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ls = Lo.ls, slots = Lo.slots;
+  unsigned long long c_hist_rows = 0;
+  if (tid < 3) s_cnt[tid] = 0;
+  if (tid < 4) s_why[tid] = 0;
+
+  for (int i = tid; i < n * nrep; i += kResThreads) {
+    const int p = i / nrep, j = i - p * nrep;
+    s_codes[j * cs + p] = codes_c[(fd.pos0 + p) * Dp + j];
+  }
+  for (int j = tid; j < nrep; j += kResThreads) {
+    s_repb[j] = rep_boff[fd.rep0 + j];
+    s_repn[j] = rep_nb[fd.rep0 + j];
+    for (int b = 0; b < rep_nb[fd.rep0 + j]; ++b) s_binrep[rep_boff[fd.rep0 + j] + b] = static_cast<uint16_t>(j);
+    s_rorig[j] = rep_orig[fd.rep0 + j];
+  }
+  for (int b = tid; b < bins; b += kResThreads) s_vals[b] = vals[fd.bin0 + b];
+  if (tid == 0 && nrep > 0) col_height(nrep, rep_nb + fd.rep0, s_cofs);
+  const double b0 = base[f];
+  for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
+  if (pre_smem)
+    for (int i = tid; i < n * nrep; i += kResThreads) s_pre[i] = static_cast<uint16_t>(g_pre[i]);
+  __syncthreads();
+
+  int ntrees = 0;
+  for (int round = 0; round < fd.trees; ++round) {
+    // ---- residuals (costmodel.cpp:204-206), fixed point, per-round reset ----------------
+    unsigned long long mx = 0;
+    for (int p = tid; p < n; p += kResThreads) {
+      const double r = fs_sub(s_targ[p], s_pred[p]);
+      s_resid[p] = r;
+      mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(r))));
+      s_node[p] = 0;
+      s_ord0[p] = s_ordr ? s_ordr[p] : static_cast<uint16_t>(g_ordr[p]);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) s_red[warp] = mx;
+    for (int s = tid; s < slots; s += kResThreads) {
+      ResNode z;
+      memset(&z, 0, sizeof z);
+      if (s == 0) z.n = n;
+      s_nodes[s] = z;
+    }
+    TreeRec* tr = trees + fd.tree0 + static_cast<int64_t>(ntrees) * slots_g;
+    for (int s = tid; s < slots_g; s += kResThreads) {
+      TreeRec tz;
+      memset(&tz, 0, sizeof tz);
+      tr[s] = tz;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long m = 0;
+      for (int w = 0; w < kResThreads / 32; ++w) m = max(m, s_red[w]);
+      s_shift = kResLimbs == 3 ? fix_shift(m, n) : fix_shift(m, n) - 22;  // n*|v| < 2^61 resp. 2^39
+    }
+    __syncthreads();
+    const int shift = s_shift;
+    const double scale = ldexp(1.0, -shift);
+    for (int p = tid; p < n; p += kResThreads) s_fix[p] = __double2ll_rn(ldexp(s_resid[p], shift));
+    __syncthreads();
+      RES_PHASE(0);
+
+    for (int level = 0; level <= depth; ++level) {
+      const int first = (1 << level) - 1, nl = 1 << level;
+      // ---- plan (level_plan_kernel) --------------------------------------------------------
+      if (tid < nl) {
+        const int s = first + tid;
+        ResNode& nd = s_nodes[s];
+        if (level == 0) {
+          if (nrep > 0 && node_needs_split(fd, 0, nd.n)) nd.build = 1;
+          else nd.state = kNodeLeaf;
+        } else if (s_nodes[(s - 1) >> 1].state == kNodeSplit) {
+          const bool need = nrep > 0 && node_needs_split(fd, level, nd.n);
+          if (!need) nd.state = kNodeLeaf;
+          if (s & 1) {
+            const int sib = s + 1;
+            const bool need_sib = nrep > 0 && node_needs_split(fd, level, s_nodes[sib].n);
+            if (need || need_sib) {
+              const int small = nd.n <= s_nodes[sib].n ? s : sib;
+              s_nodes[small].build = 1;
+              s_nodes[small == s ? sib : s].build = 2;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      RES_PHASE(1);
+      if (level == depth || nrep == 0) break;
+      const int ring = level & 1;
+      long long* hs = s_hsum + static_cast<size_t>(ring) * ls * bins;
+      int* hc = s_hcnt + static_cast<size_t>(ring) * ls * bins;
+      // ---- histograms of every directly built node of the level, one node at a time, in lane
+      // columns (col_height): every lane of a warp adds into its own bank column, so a 32-lane
+      // shared atomic is one wavefront. A row adds the three 21-bit limbs of u = v + 2^62 per
+      // feature with native 32-bit shared atomics; every kAtomSub rows the copies' limb sums are
+      // folded exactly into the node's 64-bit histogram (see hist_build_atomic_kernel for the
+      // arithmetic; the first fold overwrites). sum |v| (the screen bound) is a per-thread
+      // 64-bit sum (< 2^61 by the fixed-point shift), warp-reduced, added as 16-bit limbs.
+      {
+        const int rpw = nrep <= 32 ? 32 / nrep : 1;  // rows per warp step
+        const int hj = nrep <= 32 ? lane % nrep : lane;
+        const int hm = nrep <= 32 ? lane / nrep : 0;
+        const bool hact = nrep <= 32 ? hm < rpw : true;
+        const int cpad = 3 * colh * 32;
+        for (int k = 0; k < nl; ++k) {
+          ResNode& nd = s_nodes[first + k];
+          if (nd.build != 1) continue;
+          const int nv = nd.n;
+          const uint16_t* rows = s_ord0 + nd.seg;
+          for (int sub0 = 0; sub0 < nv; sub0 += kAtomSub) {
+            for (int i = tid; i < cpad; i += kResThreads) s_limb[i] = 0;
+            if (tid < 4) s_absl[4 * k + tid] = 0;
+            __syncthreads();
+            const int q_end = min(nv, sub0 + kAtomSub);
+            unsigned long long asum = 0;
+            if (hact) {
+              if (nrep <= 32) {
+                const uint8_t* hcode = s_codes + static_cast<size_t>(hj) * cs;
+                uint32_t* colp = s_limb + lane;
+#pragma unroll 4
+                for (int q = sub0 + warp * rpw + hm; q < q_end; q += kResWarps * rpw) {
+                  const int p = rows[q];
+                  const long long v = s_fix[p];
+                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << kResBias);
+                  uint32_t* c = colp + hcode[p] * 32;
+                  atomicAdd(c, static_cast<uint32_t>(u) & kLimbMask);
+                  atomicAdd(c + colh * 32, static_cast<uint32_t>(u >> 21) & kLimbMask);
+                  if (kResLimbs == 3) atomicAdd(c + 2 * colh * 32, static_cast<uint32_t>(u >> 42));
+                  if (hj == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
+                }
+              } else {
+                for (int q = sub0 + warp; q < q_end; q += kResWarps) {
+                  const int p = rows[q];
+                  const long long v = s_fix[p];
+                  const uint64_t u = static_cast<uint64_t>(v) + (1ull << kResBias);
+                  const uint32_t l0 = static_cast<uint32_t>(u) & kLimbMask;
+                  const uint32_t l1 = static_cast<uint32_t>(u >> 21) & kLimbMask;
+                  const uint32_t l2 = static_cast<uint32_t>(u >> 42);
+                  for (int j = lane; j < nrep; j += 32) {
+                    uint32_t* c = s_limb + lane + (s_cofs[j] + s_codes[static_cast<size_t>(j) * cs + p]) * 32;
+                    atomicAdd(c, l0);
+                    atomicAdd(c + colh * 32, l1);
+                    if (kResLimbs == 3) atomicAdd(c + 2 * colh * 32, l2);
+                  }
+                  if (lane == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
+                }
+              }
+            }
+            for (int o = 16; o > 0; o >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, o);
+            if (lane == 0 && asum) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t) atomicAdd(s_absl + 4 * k + t, static_cast<uint32_t>(asum >> (16 * t)) & 0xFFFFu);
+            }
+            __syncthreads();
+            long long* hk = hs + static_cast<size_t>(k) * bins;
+            int* ck = hc + static_cast<size_t>(k) * bins;
+            for (int i = tid; i < bins; i += kResThreads) {
+              const int j = s_binrep[i], b = i - s_repb[j];
+              unsigned __int128 U = 0;
+              if (nrep <= 32) {
+                for (int m = 0; m < rpw; ++m) {
+                  const uint32_t* c = s_limb + b * 32 + j + m * nrep;
+                  U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+                       (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+                }
+              } else {
+                const uint32_t* c = s_limb + (s_cofs[j] + b) * 32 + (j & 31);
+                U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+                    (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+              }
+              const uint64_t cnt =
+                  static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << (kResBias - 1))) >> kResBias);
+              const long long hv =
+                  static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << kResBias)));
+              hk[i] = (sub0 == 0 ? 0ll : hk[i]) + hv;
+              ck[i] = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
+            }
+            if (tid == 0) {
+              unsigned long long add = 0;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) add += static_cast<unsigned long long>(s_absl[4 * k + t]) << (16 * t);
+              nd.absfix = (sub0 == 0 ? 0ull : nd.absfix) + add;
+              if (sub0 == 0) c_hist_rows += nv;
+            }
+            __syncthreads();
+          }
+        }
+      }
+      RES_PHASE(2);
+      // ---- siblings by exact subtraction --------------------------------------------------------
+      if (level > 0) {
+        const long long* hp = s_hsum + static_cast<size_t>(ring ^ 1) * ls * bins;
+        const int* cp = s_hcnt + static_cast<size_t>(ring ^ 1) * ls * bins;
+        const int pfirst = (1 << (level - 1)) - 1;
+        for (int k2 = 0; k2 < nl / 2; ++k2) {
+          const int parent = pfirst + k2;
+          if (s_nodes[parent].state != kNodeSplit) continue;
+          const int c1 = 2 * parent + 1, c2 = c1 + 1;
+          int built, other;
+          if (s_nodes[c1].build == 1 && s_nodes[c2].build == 2) {
+            built = c1;
+            other = c2;
+          } else if (s_nodes[c2].build == 1 && s_nodes[c1].build == 2) {
+            built = c2;
+            other = c1;
+          } else {
+            continue;
+          }
+          const size_t ob = static_cast<size_t>(other - first) * bins, bb = static_cast<size_t>(built - first) * bins;
+          const size_t pb = static_cast<size_t>(k2) * bins;
+          for (int b = tid; b < bins; b += kResThreads) {
+            hs[ob + b] = hp[pb + b] - hs[bb + b];
+            hc[ob + b] = cp[pb + b] - hc[bb + b];
+          }
+          if (tid == 0) s_nodes[other].absfix = s_nodes[parent].absfix - s_nodes[built].absfix;
+        }
+        __syncthreads();
+      RES_PHASE(3);
+      }
+      // ---- screen: thread per candidate (level node k, bin). Pass 0: the feature's prefix
+      // count / sum up to the bin by a short loop over its bins, the screened gain and its bound
+      // (cached), the node's max lower bound (segmented warp max, then one 64-bit atomicMax per
+      // node segment of the warp). Pass 1: window membership {hi >= LO, hi > 0} with 32-bit
+      // atomics: per (node, feature) window count and largest left count; the candidate's data
+      // is written racily, which is exact whenever the feature has ONE window candidate - the
+      // only case that reads it.
+      {
+        const int ncand = nl * bins;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int c0 = 0; c0 < ncand; c0 += kResThreads) {
+            const int ci = c0 + tid;
+            int k = ci < ncand ? ci / bins : nl;
+            const int bi = ci - k * bins;
+            bool live = k < nl;
+            ResNode* ndp = live ? &s_nodes[first + k] : nullptr;
+            if (live && (ndp->state != 0 || ndp->build == 0)) live = false;
+            int j = 0, b = 0, ic = 0;
+            double lo = -INFINITY;
+            if (live) {
+              j = s_binrep[bi];
+              b = bi - s_repb[j];
+            }
+            if (pass == 0) {
+              if (live) {
+                const int nb = s_repn[j];
+                const long long* h = hs + static_cast<size_t>(k) * bins + s_repb[j];
+                const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+                if (b == 0) {
+                  WinRec z;
+                  memset(&z, 0, sizeof z);
+                  z.best_bin = -1;
+                  s_win[k * nrep + j] = z;
+                }
+                long long is = 0, ts = 0;
+                for (int t = 0; t < nb; ++t) {
+                  const long long hv = h[t];
+                  ts += hv;
+                  if (t <= b) {
+                    is += hv;
+                    ic += c[t];
+                  }
+                }
+                s_clc[ci] = ic;
+                const int nv = ndp->n;
+                if (c[b] > 0 && ic < nv) {
+                  const double S = static_cast<double>(ndp->absfix) * scale * (1.0 + 1e-12);
+                  double g, hi;
+                  screen_gain(is, ts, ic, nv, scale, S, g, lo, hi);
+                  s_cand[2 * ci] = g;
+                  s_cand[2 * ci + 1] = hi - g;
+                } else {
+                  s_cand[2 * ci] = NAN;
+                }
+              }
+              // segmented (by node) warp max of the lower bounds; lanes' nodes are non-decreasing
+              const int kk = live ? k : -1;
+              double m = lo;
+              for (int o = 1; o < 32; o <<= 1) {
+                const double om = __shfl_up_sync(0xffffffffu, m, o);
+                const int ok_ = __shfl_up_sync(0xffffffffu, kk, o);
+                if (lane >= o && ok_ == kk) m = fmax(m, om);
+              }
+              const int knext = __shfl_down_sync(0xffffffffu, kk, 1);
+              if (kk >= 0 && (lane == 31 || knext != kk) && m > -INFINITY) atomicMax(&ndp->lokey, lo_key(m));
+            } else if (live) {
+              const double g = s_cand[2 * ci];
+              if (!isnan(g)) {
+                const double dl = s_cand[2 * ci + 1];
+                const double hi = g + dl;
+                if (hi >= lo_from_key(ndp->lokey) && hi > 0.0) {
+                  WinRec& w = s_win[k * nrep + j];
+                  ic = s_clc[ci];
+                  atomicAdd(&w.count, 1);
+                  atomicMax(&w.maxlc, ic);
+                  atomicAdd(&ndp->wcount, 1);
+                  w.flag = 1;
+                  w.best_g = g;
+                  w.best_lo = g - dl;
+                  w.best_bin = b;
+                  w.best_lc = ic;
+                }
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      RES_PHASE(4);
+      // ---- tie classes: a window whose candidates (one per feature, equal left counts) come
+      // from features whose presorted orders coincide on the node's rows has one reference
+      // gain for all of them (identical folds), so the lowest feature wins by strict > without
+      // any fold. Check order equivalence against the lowest window feature in parallel.
+      if (tid == 0) s_neq = 0;
+      __syncthreads();
+      if (tid < nl) {
+        const int k = tid;
+        ResNode& nd = s_nodes[first + k];
+        nd.eqf0 = -1;
+        if (nd.state == 0 && nd.build != 0 && nd.wcount >= 2) {
+          const WinRec* w = s_win + k * nrep;
+          int f0 = -1, lc0 = -1;
+          bool ok = true;
+          for (int j = 0; j < nrep && ok; ++j) {
+            if (!w[j].flag) continue;
+            if (w[j].count != 1) ok = false;
+            if (f0 < 0) {
+              f0 = j;
+              lc0 = w[j].best_lc;
+            } else if (w[j].best_lc != lc0) {
+              ok = false;
+            }
+          }
+          if (ok && f0 >= 0 && w[f0].best_lo > 0.0) {
+            nd.eqf0 = f0;
+            for (int j = f0 + 1; j < nrep; ++j)
+              if (w[j].flag) s_items[atomicAdd(&s_neq, 1)] = (first + k) << 16 | j;
+          }
+        }
+      }
+      __syncthreads();
+      // Order equivalence of g with f0 on the node's rows <=> the map code_f0 -> code_g over
+      // those rows is a function that is strictly increasing (ties align and the stable sorts
+      // by (code, canonical position) then coincide). Checked without any ordered scan: phi[a] =
+      // the g code of some row with f0 code a (racy plain stores), then every row must agree
+      // with phi and phi must increase over the present a. Rows come from the node's order-0
+      // segment in any order; items are batched through the (free) limb scratch.
+      {
+        uint16_t* phi = reinterpret_cast<uint16_t*>(s_limb);
+        const int cap = static_cast<int>((Lo.stage - Lo.limb) / 512);  // items of 256 u16 (>= 8)
+        const int neq = s_neq;
+        for (int b0 = 0; b0 < neq; b0 += cap) {
+          const int nb_items = min(cap, neq - b0);
+          for (int i = tid; i < nb_items * 256; i += kResThreads) phi[i] = 0xFFFFu;
+          if (tid < nb_items) {
+            const int s = s_items[b0 + tid] >> 16, g = s_items[b0 + tid] & 0xFFFF;
+            s_win[(s - first) * nrep + g].eq = 1;
+          }
+          __syncthreads();
+          for (int pass = 0; pass < 2; ++pass) {
+            for (int q = 0; q < nb_items; ++q) {
+              const int s = s_items[b0 + q] >> 16, g = s_items[b0 + q] & 0xFFFF;
+              const ResNode& nd = s_nodes[s];
+              const uint8_t* cf = s_codes + static_cast<size_t>(nd.eqf0) * cs;
+              const uint8_t* cg = s_codes + static_cast<size_t>(g) * cs;
+              uint16_t* ph = phi + q * 256;
+              bool bad = false;
+              for (int i = tid; i < nd.n; i += kResThreads) {
+                const int pr = s_ord0[nd.seg + i];
+                if (pass == 0) ph[cf[pr]] = cg[pr];
+                else bad |= ph[cf[pr]] != cg[pr];
+              }
+              if (pass == 1 && bad) s_win[(s - first) * nrep + g].eq = 0;
+            }
+            __syncthreads();
+          }
+          // phi strictly increasing over the present f0 codes (warp per item)
+          for (int q = warp; q < nb_items; q += kResThreads / 32) {
+            const int s = s_items[b0 + q] >> 16, g = s_items[b0 + q] & 0xFFFF;
+            const int nb = s_repn[s_nodes[s].eqf0];
+            const uint16_t* ph = phi + q * 256;
+            int carry = -1;
+            bool bad = false;
+            for (int a0 = 0; a0 < nb; a0 += 32) {
+              const int a = a0 + lane;
+              const int v = a < nb ? ph[a] : 0xFFFF;
+              const bool present = v != 0xFFFF;
+              const unsigned m = __ballot_sync(0xffffffffu, present);
+              const unsigned lt = m & ((1u << lane) - 1u);
+              int pv = __shfl_sync(0xffffffffu, v, lt ? 31 - __clz(lt) : 0);
+              if (!lt) pv = carry;
+              if (present && pv >= 0 && v <= pv) bad = true;
+              if (m) carry = __shfl_sync(0xffffffffu, v, 31 - __clz(m));
+            }
+            if (__any_sync(0xffffffffu, bad) && lane == 0) s_win[(s - first) * nrep + g].eq = 0;
+          }
+          __syncthreads();
+        }
+      }
+      RES_PHASE(5);
+      // ---- decide (decide_kernel) ------------------------------------------------------------
+      if (tid == 0) s_nitems = 0;
+      __syncthreads();
+      // warp per node, lanes over the node's features (window records read in parallel)
+      for (int k = warp; k < nl; k += kResWarps) {
+        ResNode& nd = s_nodes[first + k];
+        if (nd.state != 0 || nd.build == 0) continue;
+        const WinRec* w = s_win + k * nrep;
+        if (nd.wcount == 0) {
+          if (lane == 0) nd.state = kNodeLeaf;
+          continue;
+        }
+        int pick = -1, nflag = 0, f0 = -1;
+        bool multi = false, notall = false;
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          const bool fl = j < nrep && w[j].flag;
+          const unsigned m = __ballot_sync(0xffffffffu, fl);
+          nflag += __popc(m);
+          if (m && f0 < 0) f0 = j0 + __ffs(m) - 1;
+          multi |= __any_sync(0xffffffffu, fl && w[j].count > 1);
+          notall |= __any_sync(0xffffffffu, fl && j > nd.eqf0 && !w[j].eq);
+        }
+        if (nd.wcount == 1) {
+          if (f0 >= 0 && w[f0].best_lo > 0.0) pick = f0;
+        } else if (nd.eqf0 >= 0 && !notall) {
+          pick = nd.eqf0;
+        }
+        if (pick >= 0) {
+          if (lane == 0) {
+            nd.state = kNodeSplit;
+            nd.rep = pick;
+            nd.bin = w[pick].best_bin;
+            nd.gain = w[pick].best_g;
+            nd.lc = w[pick].best_lc;
+            atomicAdd(&s_cnt[0], 1ull);
+          }
+          continue;
+        }
+        // exact re-evaluation: why the screen could not decide (diagnostics, device counters)
+        int why = 3;  // sign of the only candidate uncertain
+        if (nd.wcount >= 2) {
+          const int lc0 = w[f0].best_lc;
+          bool diff = false;
+          for (int j0 = 0; j0 < nrep; j0 += 32) {
+            const int j = j0 + lane;
+            diff |= __any_sync(0xffffffffu, j < nrep && w[j].flag && w[j].best_lc != lc0);
+          }
+          why = multi ? 0 : diff ? 1 : 2;  // several candidates on a feature / partitions / orders
+        }
+        int base = 0;
+        if (lane == 0) {
+          nd.state = kNodeExact;
+          atomicAdd(&s_cnt[1], 1ull);
+          atomicAdd(&s_why[why], 1ull);
+          base = atomicAdd(&s_nitems, nflag + 1);
+          s_items[base] = (first + k) << 16 | 0xFFFF;
+          atomicAdd(&s_cnt[2], static_cast<unsigned long long>(nflag + 1));
+        }
+        base = __shfl_sync(0xffffffffu, base, 0) + 1;
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          const bool fl = j < nrep && w[j].flag;
+          const unsigned m = __ballot_sync(0xffffffffu, fl);
+          if (fl) s_items[base + __popc(m & ((1u << lane) - 1u))] = (first + k) << 16 | j;
+          base += __popc(m);
+        }
+      }
+      __syncthreads();
+      RES_PHASE(6);
+      // ---- reference-order folds (exact_kernel) ------------------------------------------------
+      // Warp per item. The node total is one fold over its order-0 segment. A window feature's
+      // fold walks the feature's presorted list: lanes test 32 entries for node membership, the
+      // members are compacted (ballot rank) into the warp's staging slots, and lane 0 folds them
+      // in list order, recording the left sum at every value boundary - but only up to the
+      // largest window left count (candidates beyond it cannot win, costmodel.cpp:65 strict >).
+      {
+        double* st_v = reinterpret_cast<double*>(sm + Lo.stage) + warp * 32;
+        uint8_t* st_c = sm + Lo.stage + static_cast<size_t>(kResThreads / 32) * 32 * 8 + warp * 32;
+        for (int it = warp; it < s_nitems; it += kResThreads / 32) {
+          const int s = s_items[it] >> 16, j = s_items[it] & 0xFFFF;
+          ResNode& nd = s_nodes[s];
+          const int nv = nd.n;
+          if (j == 0xFFFF) {  // every lane runs the same chain (broadcast loads): no divergence
+            const double t = fold_spec(s_resid, s_ord0 + nd.seg, nv);
+            if (lane == 0) nd.total = t;
+            continue;
+          }
+          const int need = s_win[(s - first) * nrep + j].maxlc;
+          double* out = s_lbuf + static_cast<size_t>(s - first) * bins + s_repb[j];
+          const uint8_t* cj = s_codes + static_cast<size_t>(j) * cs;
+          if (warp < spec_bufs && s_win[(s - first) * nrep + j].count == 1) {
+            // one window candidate: only L at its left count is needed. Compact the node's
+            // members of the feature's presorted list (in list order) into this warp's buffer,
+            // then fold them with the speculative midpoint split (fold_spec).
+            uint16_t* buf = s_sbuf + static_cast<size_t>(warp) * n;
+            int got = 0;
+            int p_nx = lane < n ? pre_at(j, lane) : 0;
+            for (int i0 = 0; i0 < n && got < need; i0 += 32) {
+              const int i = i0 + lane;
+              const int p = p_nx;
+              p_nx = i + 32 < n ? pre_at(j, i + 32) : 0;
+              const bool mem = i < n && s_node[p] == s;
+              const unsigned m = __ballot_sync(0xffffffffu, mem);
+              const int dst = got + __popc(m & ((1u << lane) - 1u));
+              if (mem && dst < need) buf[dst] = static_cast<uint16_t>(p);
+              got += __popc(m);
+            }
+            __syncwarp();
+            const double L = fold_spec(s_resid, buf, need);
+            if (lane == 0) out[s_win[(s - first) * nrep + j].best_bin] = L;
+            continue;
+          }
+          double left = 0.0;
+          int prev = -1, seen = 0;
+          int p_next = lane < n ? pre_at(j, lane) : 0;
+          for (int i0 = 0; i0 < n && seen < need; i0 += 32) {
+            const int i = i0 + lane;
+            const int p = p_next;
+            p_next = i + 32 < n ? pre_at(j, i + 32) : 0;
+            const bool mem = i < n && s_node[p] == s;
+            const unsigned m = __ballot_sync(0xffffffffu, mem);
+            if (mem) {
+              const int dst = __popc(m & ((1u << lane) - 1u));
+              st_v[dst] = s_resid[p];
+              st_c[dst] = cj[p];
+            }
+            __syncwarp();
+            const int cnt = min(__popc(m), need - seen);
+#pragma unroll 8
+            for (int t = 0; t < cnt; ++t) {  // all lanes fold identically (broadcast loads)
+              const int c = st_c[t];
+              if (c != prev && prev >= 0 && lane == 0) out[prev] = left;
+              left = fs_add(left, st_v[t]);
+              prev = c;
+            }
+            seen += cnt;
+            __syncwarp();
+          }
+          if (lane == 0 && prev >= 0) out[prev] = left;
+        }
+      }
+      __syncthreads();
+      RES_PHASE(7);
+      // ---- exact decision (exact_decide_kernel): warp per node, lanes over a window feature's
+      // bins; the reference's strict > over (feature asc, threshold asc) = first occurrence of
+      // the maximum, so the warp reduction keeps the largest gain and, on equal gains, the
+      // earliest (feature, bin).
+      for (int k = warp; k < nl; k += kResWarps) {
+        ResNode& nd = s_nodes[first + k];
+        if (nd.state != kNodeExact) continue;
+        const WinRec* w = s_win + k * nrep;
+        const int nv = nd.n;
+        const double T = nd.total;
+        const double parent = fs_div(fs_mul(T, T), static_cast<double>(nv));
+        double best = 0.0;
+        int bj = -1, bbin = -1, blc = 0;
+        // features with one window candidate (the common case): lane per feature, the only
+        // candidate that can win on that feature is its window candidate (best_bin / best_lc:
+        // every other candidate's gain is provably below LO, costmodel.cpp:65 strict >)
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          if (j < nrep && w[j].flag && w[j].count == 1) {
+            const int cum = w[j].best_lc;
+            const double L = s_lbuf[static_cast<size_t>(k) * bins + s_repb[j] + w[j].best_bin];
+            const double R = fs_sub(T, L);
+            const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+            const double r = fs_div(fs_mul(R, R), static_cast<double>(nv - cum));
+            const double g = fs_sub(fs_add(a, r), parent);
+            if (g > best) {  // first candidate of this lane: no earlier (feature, bin) to beat
+              best = g;
+              bj = j;
+              bbin = w[j].best_bin;
+              blc = cum;
+            }
+          }
+        }
+        for (int j = 0; j < nrep; ++j) {
+          if (!w[j].flag || w[j].count == 1) continue;
+          const int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+          const double* lb = s_lbuf + static_cast<size_t>(k) * bins + s_repb[j];
+          const int nb = s_repn[j], lim = w[j].maxlc;
+          int carry = 0;
+          for (int b0 = 0; b0 < nb && carry < lim; b0 += 32) {
+            const int b = b0 + lane;
+            const int cb = b < nb ? c[b] : 0;
+            const int cum = warp_incl_scan(cb, lane) + carry;
+            if (cb > 0 && cum < nv && cum <= lim) {  // folds stop at the last window candidate
+              const double L = lb[b];
+              const double R = fs_sub(T, L);
+              const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+              const double r = fs_div(fs_mul(R, R), static_cast<double>(nv - cum));
+              const double g = fs_sub(fs_add(a, r), parent);
+              // a lane's candidates do not arrive in (feature, bin) order: full tie-break
+              if (g > best || (g == best && bj >= 0 && (j < bj || (j == bj && b < bbin)))) {
+                best = g;
+                bj = j;
+                bbin = b;
+                blc = cum;
+              }
+            }
+            carry = __shfl_sync(0xffffffffu, cum, 31);
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          const int obin = __shfl_xor_sync(0xffffffffu, bbin, o);
+          const int olc = __shfl_xor_sync(0xffffffffu, blc, o);
+          const bool take = oj >= 0 && (bj < 0 || ob > best || (ob == best && (oj < bj || (oj == bj && obin < bbin))));
+          if (take) {
+            best = ob;
+            bj = oj;
+            bbin = obin;
+            blc = olc;
+          }
+        }
+        if (lane == 0) {
+          if (bj < 0) {
+            nd.state = kNodeLeaf;
+          } else {
+            nd.state = kNodeSplit;
+            nd.rep = bj;
+            nd.bin = bbin;
+            nd.gain = best;
+            nd.lc = blc;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- split records: threshold, tree record, children -------------------------------------
+      if (tid < nl) {
+        const int s = first + tid;
+        ResNode& nd = s_nodes[s];
+        if (nd.state == kNodeSplit) {
+          const int j = nd.rep;
+          const int orig = s_rorig[j];
+          double thr = s_vals[s_repb[j] + nd.bin];
+          if (thr == 0.0 && fd.negz) {  // +0.0 / -0.0 share a bin: the last left element's own value
+            const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(j) * n;
+            for (int i = cle[fd.bin0 + s_repb[j] + nd.bin] - 1; i >= 0; --i)
+              if (s_node[L[i]] == s) {
+                thr = x[(fd.row0 + canon[fd.pos0 + L[i]]) * d + orig];
+                break;
+              }
+          }
+          TreeRec r;
+          r.kind = kNodeSplit;
+          r.feature = orig;
+          r.threshold = thr;
+          r.value = 0.0;
+          r.gain = nd.gain;
+          r.rep = j;
+          r.bin = nd.bin;
+          tr[s] = r;
+          ResNode& a = s_nodes[2 * s + 1];
+          ResNode& b = s_nodes[2 * s + 2];
+          a.n = nd.lc;
+          a.seg = nd.seg;
+          b.n = nd.n - nd.lc;
+          b.seg = nd.seg + nd.lc;
+        }
+      }
+      __syncthreads();
+      RES_PHASE(8);
+      // ---- stable partition of every split node's order-0 segment (costmodel.cpp:94-105 for
+      // list 0) in one sweep over the whole list: a block-wide exclusive scan of "goes left"
+      // flags; its value at the node's segment start turns it into the rank inside the node
+      // (segments are contiguous). Elements are read once into registers (kPartE consecutive per
+      // thread per chunk), scattered into the other order buffer, and the buffers swap.
+      {
+        int nsplit = 0;
+        for (int k = 0; k < nl; ++k) nsplit += s_nodes[first + k].state == kNodeSplit;
+        if (nsplit) {
+          int base = 0;  // exclusive scan carried across chunks (uniform)
+          for (int c0 = 0; c0 < n; c0 += kResThreads * kPartE) {
+            int pe[kPartE], ve[kPartE];
+            bool le[kPartE];
+            int cnt = 0;
+#pragma unroll
+            for (int e = 0; e < kPartE; ++e) {
+              const int i = c0 + tid * kPartE + e;
+              pe[e] = 0;
+              ve[e] = -1;
+              le[e] = false;
+              if (i < n) {
+                pe[e] = s_ord0[i];
+                const int v = s_node[pe[e]];
+                if (s_nodes[v].state == kNodeSplit) {
+                  ve[e] = v;
+                  le[e] = s_codes[static_cast<size_t>(s_nodes[v].rep) * cs + pe[e]] <= s_nodes[v].bin;
+                }
+              }
+              cnt += le[e];
+            }
+            const int incl = warp_incl_scan(cnt, lane);
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+              const int wv = lane < kResWarps ? s_wsum[lane] : 0;
+              const int inc = warp_incl_scan(wv, lane);
+              s_wsum[lane] = inc - wv;
+              if (lane == 31) s_ctot = inc;
+            }
+            __syncthreads();
+            int P = base + s_wsum[warp] + incl - cnt;  // exclusive scan at this thread's first element
+            const int chunk_total = s_ctot;
+            int Pe[kPartE];
+#pragma unroll
+            for (int e = 0; e < kPartE; ++e) {
+              Pe[e] = P;
+              P += le[e];
+              const int i = c0 + tid * kPartE + e;
+              if (ve[e] >= 0 && i == s_nodes[ve[e]].seg) s_nodes[ve[e]].pad_ = Pe[e];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < kPartE; ++e) {
+              const int i = c0 + tid * kPartE + e;
+              if (i >= n) continue;
+              if (ve[e] < 0) {
+                s_scr[i] = static_cast<uint16_t>(pe[e]);
+                continue;
+              }
+              const ResNode& nd = s_nodes[ve[e]];
+              const int lrank = Pe[e] - nd.pad_;
+              const int dst = le[e] ? nd.seg + lrank : nd.seg + nd.lc + (i - nd.seg) - lrank;
+              s_scr[dst] = static_cast<uint16_t>(pe[e]);
+              s_node[pe[e]] = static_cast<uint8_t>(le[e] ? 2 * ve[e] + 1 : 2 * ve[e] + 2);
+            }
+            base += chunk_total;
+            __syncthreads();
+          }
+          uint16_t* t = s_ord0;
+          s_ord0 = s_scr;
+          s_scr = t;
+        }
+      }
+      RES_PHASE(9);
+    }
+      RES_PHASE(1);
+    // ---- leaves (leaf_kernel): reference-order total / n, prediction update ------------------
+    for (int s = warp; s < slots; s += kResThreads / 32) {
+      ResNode& nd = s_nodes[s];
+      if (nd.state != kNodeLeaf || nd.n == 0) continue;
+      if (s > 0 && s_nodes[(s - 1) >> 1].state != kNodeSplit) continue;
+      const int nv = nd.n;
+      const double sum = fold_spec(s_resid, s_ord0 + nd.seg, nv);  // warp-collective
+      const double value = fs_div(sum, static_cast<double>(nv));
+      const double step = fs_mul(fd.lr, value);
+      for (int i = lane; i < nv; i += 32) {
+        const int p = s_ord0[nd.seg + i];
+        s_pred[p] = fs_add(s_pred[p], step);
+      }
+      if (lane == 0) {
+        nd.value = value;
+        TreeRec r;
+        r.kind = kNodeLeaf;
+        r.feature = -1;
+        r.threshold = 0.0;
+        r.value = value;
+        r.gain = 0.0;
+        r.rep = -1;
+        r.bin = 0;
+        tr[s] = r;
+      }
+    }
+    __syncthreads();
+      RES_PHASE(10);
+    // ---- commit / early stop (costmodel.cpp:212) and MSE (:215-220) --------------------------
+    if (s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0) break;  // uniform (smem)
+    double a = 0.0;
+    for (int p = tid; p < n; p += kResThreads) {
+      const double e = fs_sub(s_targ[p], s_pred[p]);
+      a = fs_add(a, fs_mul(e, e));
+    }
+    for (int o = 16; o > 0; o >>= 1) a = fs_add(a, __shfl_down_sync(0xffffffffu, a, o));
+    if (lane == 0) s_dred[warp] = a;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kResThreads / 32; ++w) t = fs_add(t, s_dred[w]);
+      mse[static_cast<int64_t>(f) * max_trees + ntrees] = fs_div(t, static_cast<double>(n));
+    }
+    ++ntrees;
+    __syncthreads();
+      RES_PHASE(11);
+  }
+  if (tid == 0) {
+    st[f].ntrees = ntrees;
+    st[f].active = 0;
+    st[f].screened += s_cnt[0];
+    st[f].exact += s_cnt[1];
+    atomicAdd(ctr + kCtrHistRows, c_hist_rows);
+    atomicAdd(ctr + kCtrHistBytes, c_hist_rows * (static_cast<unsigned long long>(nrep) + 12ull));
+    atomicAdd(ctr + kCtrExactChains, s_cnt[2]);
+    atomicAdd(ctr + kCtrExactNodes, s_cnt[1]);
+    if (blockIdx.x == 0)
+      for (int i = 0; i < 12; ++i) atomicAdd(ctr + kCtrPhase0 + i, static_cast<unsigned long long>(s_ph[i]));
+    for (int i = 0; i < 4; ++i) atomicAdd(ctr + kCtrPhase0 + 12 + i, s_why[i]);
+  }
+}
+
+}  // namespace
+}  // namespace fit
+}  // namespace fs

@@ -1,0 +1,1631 @@
+// fit_round.cuh - the multi-kernel boosting round (families too large for one CTA: C4/C5)
+// Part of the trainer translation unit: included once, by fit.cu only (shares its
+// anonymous namespace, constants and helpers).
+#pragma once
+
+namespace fs {
+namespace fit {
+namespace {
+
+// Which nodes at `level` are screened, which histograms are built directly / derived.
+__global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                  NodeRec* __restrict__ nodes, int level) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int first = (1 << level) - 1;
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= (1 << level)) return;
+  NodeRec* nd = nodes + fd.node0;
+  const int s = first + local;
+  if (level == 0) {
+    if (fd.nrep > 0 && node_needs_split(fd, 0, nd[0].n)) nd[0].build = 1;
+    else nd[0].state = kNodeLeaf;
+    return;
+  }
+  const int parent = (s - 1) >> 1;
+  if (nd[parent].state != kNodeSplit) return;
+  const bool need = fd.nrep > 0 && node_needs_split(fd, level, nd[s].n);
+  if (!need) nd[s].state = kNodeLeaf;
+  if (s & 1) {  // left child decides the pair's build plan
+    const int sib = s + 1;
+    const bool need_sib = fd.nrep > 0 && node_needs_split(fd, level, nd[sib].n);
+    if (need || need_sib) {
+      const int small = nd[s].n <= nd[sib].n ? s : sib;
+      nd[small].build = 1;
+      nd[small == s ? sib : s].build = 2;
+    }
+  }
+}
+
+__global__ void hist_zero_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st, int level,
+                                 int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active || level >= max(fd.depth, 1)) return;
+  const int64_t base = fd.hist0 + static_cast<int64_t>(level & 1) * fd.level_slots * fd.bins;
+  const int64_t cnt = static_cast<int64_t>(min(1 << level, fd.level_slots)) * fd.bins;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    hsum[base + i] = 0;
+    hcnt[base + i] = 0;
+  }
+}
+
+constexpr int kHistThreads = 256;
+constexpr int kHistTileRows = 64;
+constexpr int kHistChunk = 4096;
+
+// Histogram of one directly-built node over one chunk of its rows. Threads own (feature, row
+// group) pairs, so shared-memory bins are updated without atomics; the CTA then adds its
+// partial histogram to the node's global histogram with integer atomics (exact, order-free).
+template <typename CodeT, bool kGlobal>
+__global__ void __launch_bounds__(kHistThreads) hist_build_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
+    int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
+    const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
+    int64_t* __restrict__ node_abs, int groups, unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const NodeRec* nd = nodes + fd.node0;
+  int s;
+  if (level == 0) {
+    if (blockIdx.y) return;
+    s = 0;
+  } else {
+    if (blockIdx.y >= (1u << (level - 1))) return;
+    const int parent = (1 << (level - 1)) - 1 + blockIdx.y;
+    if (nd[parent].state != kNodeSplit) return;
+    s = 2 * parent + 1;
+    if (nd[s].build != 1) s += 1;
+    if (nd[s].build != 1) return;
+  }
+  const int n_v = nd[s].n;
+  const int r0 = blockIdx.x * kHistChunk;
+  if (r0 >= n_v) return;
+  const int rows = min(kHistChunk, n_v - r0);
+  const int seg = nd[s].seg;
+  const int local = s - ((1 << level) - 1);
+  const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
+  const int bins = fd.bins, nrep = fd.nrep;
+
+  int64_t* s_sum = reinterpret_cast<int64_t*>(smem);
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(s_sum + (kGlobal ? 0 : static_cast<int64_t>(groups) * bins));
+  unsigned char* tail = reinterpret_cast<unsigned char*>(s_cnt + (kGlobal ? 0 : static_cast<int64_t>(groups) * bins));
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                          // [kHistTileRows][Dp]
+  int64_t* t_fix = reinterpret_cast<int64_t*>(t_codes + kHistTileRows * Dp);  // [kHistTileRows]
+  __shared__ unsigned long long s_abs;
+  const int tid = threadIdx.x;
+  if (!kGlobal)
+    for (int i = tid; i < groups * bins; i += kHistThreads) {
+      s_sum[i] = 0;
+      s_cnt[i] = 0;
+    }
+  if (tid == 0) s_abs = 0;
+  // thread -> (feature, group)
+  const int per_group = nrep > 0 ? (nrep < kHistThreads ? nrep : kHistThreads) : 1;
+  const int g = tid / per_group;
+  const int fj0 = tid - g * per_group;
+  const bool worker = g < groups && fj0 < nrep;
+  __syncthreads();
+  const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
+  for (int t0 = 0; t0 < rows; t0 += kHistTileRows) {
+    const int tr = min(kHistTileRows, rows - t0);
+    for (int i = tid; i < tr * vec_per_row; i += kHistThreads) {
+      const int r = i / vec_per_row, v = i - r * vec_per_row;
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+      reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+    }
+    unsigned long long a = 0;
+    if (tid < tr) {
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid];
+      const int64_t v = rfix[p];
+      t_fix[tid] = v;
+      a = static_cast<unsigned long long>(v < 0 ? -v : v);
+    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if ((tid & 31) == 0 && a) atomicAdd(&s_abs, a);
+    __syncthreads();
+    if (worker) {
+      for (int fj = fj0; fj < nrep; fj += per_group) {
+        const int boff = rep_boff[fd.rep0 + fj];
+        for (int r = g; r < tr; r += groups) {
+          const int bin = boff + static_cast<int>(t_codes[r * Dp + fj]);
+          if (kGlobal) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(hsum + hbase + bin),
+                      static_cast<unsigned long long>(t_fix[r]));
+            atomicAdd(hcnt + hbase + bin, 1);
+          } else {
+            s_sum[g * bins + bin] += t_fix[r];
+            s_cnt[g * bins + bin] += 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!kGlobal) {
+    for (int b = tid; b < bins; b += kHistThreads) {
+      int64_t sm = 0;
+      int32_t c = 0;
+      for (int gg = 0; gg < groups; ++gg) {
+        sm += s_sum[gg * bins + b];
+        c += s_cnt[gg * bins + b];
+      }
+      if (c) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(hsum + hbase + b), static_cast<unsigned long long>(sm));
+        atomicAdd(hcnt + hbase + b, c);
+      }
+    }
+  }
+  if (tid == 0 && s_abs)
+    atomicAdd(reinterpret_cast<unsigned long long*>(node_abs + fd.node0 + s), s_abs);
+  if (tid == 0) {
+    atomicAdd(ctr + kCtrHistBytes,
+              static_cast<unsigned long long>(rows) * (static_cast<unsigned long long>(nrep) * sizeof(CodeT) + 12ull));
+    atomicAdd(ctr + kCtrHistRows, static_cast<unsigned long long>(rows));
+  }
+}
+
+// Column-layout histogram build (the default shape). Warp w owns feature group fg = w % NFG
+// (features 32fg .. 32fg+31, lane = feature) and row group w / NFG. A group's bins live in
+// shared memory as [bin][32 lanes], so the 32 updates a warp issues for one row always hit 32
+// different banks (no conflicts, no atomics); row groups own private copies that are summed at
+// the flush. grp_off[f][fg] = entry offset of feature group fg (entries = bins x 32).
+constexpr int kColWarps = 6;
+
+template <typename CodeT>
+__global__ void __launch_bounds__(kColWarps * 32) hist_build_col_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
+    int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
+    const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ grp_off,
+    const int32_t* __restrict__ grp_rg, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
+    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const NodeRec* nd = nodes + fd.node0;
+  int s;
+  if (level == 0) {
+    if (blockIdx.y) return;
+    s = 0;
+  } else {
+    if (blockIdx.y >= (1u << (level - 1))) return;
+    const int parent = (1 << (level - 1)) - 1 + blockIdx.y;
+    if (nd[parent].state != kNodeSplit) return;
+    s = 2 * parent + 1;
+    if (nd[s].build != 1) s += 1;
+    if (nd[s].build != 1) return;
+  }
+  const int n_v = nd[s].n;
+  const int r0 = blockIdx.x * kHistChunk;
+  if (r0 >= n_v) return;
+  const int rows = min(kHistChunk, n_v - r0);
+  const int seg = nd[s].seg;
+  const int local = s - ((1 << level) - 1);
+  const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
+  const int nrep = fd.nrep;
+  const int nfg = (nrep + 31) >> 5;
+  const int32_t* go = grp_off + static_cast<int64_t>(f) * (kColWarps + 1);
+  const int gsz = go[nfg];            // entries per copy
+  const int rg = grp_rg[f];           // row groups (copies)
+  int64_t* s_sum = reinterpret_cast<int64_t*>(smem);                        // [rg][gsz]
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(s_sum + static_cast<int64_t>(rg) * gsz);
+  unsigned char* tail = reinterpret_cast<unsigned char*>(s_cnt + static_cast<int64_t>(rg) * gsz);
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                            // [kHistTileRows][Dp]
+  int64_t* t_fix = reinterpret_cast<int64_t*>(t_codes + kHistTileRows * Dp);  // [kHistTileRows]
+  __shared__ unsigned long long s_abs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < rg * gsz; i += kColWarps * 32) {
+    s_sum[i] = 0;
+    s_cnt[i] = 0;
+  }
+  if (tid == 0) s_abs = 0;
+  const int fg = warp % nfg, rgi = warp / nfg;
+  const bool worker = rgi < rg;
+  const int j = 32 * fg + lane;
+  const bool jv = worker && j < nrep;
+  int64_t* my_sum = s_sum + static_cast<int64_t>(rgi) * gsz + go[fg] + lane;
+  int32_t* my_cnt = s_cnt + static_cast<int64_t>(rgi) * gsz + go[fg] + lane;
+  __syncthreads();
+  const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
+  for (int t0 = 0; t0 < rows; t0 += kHistTileRows) {
+    const int tr = min(kHistTileRows, rows - t0);
+    for (int i = tid; i < tr * vec_per_row; i += kColWarps * 32) {
+      const int r = i / vec_per_row, v = i - r * vec_per_row;
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+      reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+    }
+    unsigned long long a = 0;
+    for (int r = tid; r < tr; r += kColWarps * 32) {
+      const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+      const int64_t v = rfix[p];
+      t_fix[r] = v;
+      a += static_cast<unsigned long long>(v < 0 ? -v : v);
+    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (lane == 0 && a) atomicAdd(&s_abs, a);
+    __syncthreads();
+    if (jv) {
+      for (int r = rgi; r < tr; r += rg) {
+        const int b = static_cast<int>(t_codes[r * Dp + j]);
+        my_sum[b * 32] += t_fix[r];
+        my_cnt[b * 32] += 1;
+      }
+    }
+    __syncthreads();
+  }
+  // flush: entry e = (fg, b, lane) -> global bin boff_j + b
+  for (int e = tid; e < gsz; e += kColWarps * 32) {
+    int g = 0;
+    while (g + 1 < nfg && go[g + 1] <= e) ++g;
+    const int within = e - go[g];
+    const int b = within >> 5, jj = 32 * g + (within & 31);
+    if (jj >= nrep || b >= rep_nb[fd.rep0 + jj]) continue;
+    int64_t sm = 0;
+    int32_t c = 0;
+    for (int k = 0; k < rg; ++k) {
+      sm += s_sum[static_cast<int64_t>(k) * gsz + e];
+      c += s_cnt[static_cast<int64_t>(k) * gsz + e];
+    }
+    if (c) {
+      const int64_t gb = hbase + rep_boff[fd.rep0 + jj] + b;
+      atomicAdd(reinterpret_cast<unsigned long long*>(hsum + gb), static_cast<unsigned long long>(sm));
+      atomicAdd(hcnt + gb, c);
+    }
+  }
+  if (tid == 0) {
+    if (s_abs) atomicAdd(reinterpret_cast<unsigned long long*>(node_abs + fd.node0 + s), s_abs);
+    atomicAdd(ctr + kCtrHistBytes,
+              static_cast<unsigned long long>(rows) * (static_cast<unsigned long long>(nrep) * sizeof(CodeT) + 12ull));
+    atomicAdd(ctr + kCtrHistRows, static_cast<unsigned long long>(rows));
+  }
+}
+
+// Lane-column histogram shape (conflict-free shared atomics): lane l of every warp owns bank
+// column l. nrep <= 32: lanes l < (32 / nrep) * nrep take feature l % nrep (copy l / nrep of
+// it), so the column height is the largest bin count. nrep > 32: lane l takes features l, l+32,
+// ... stacked in its column (cofs = offset of a feature's bins in its lane's column).
+__host__ __device__ inline int col_height(int nrep, const int32_t* nb, int32_t* cofs) {
+  int H = 1;
+  if (nrep <= 32) {
+    for (int j = 0; j < nrep; ++j) {
+      if (cofs) cofs[j] = 0;
+      H = nb[j] > H ? nb[j] : H;
+    }
+    return H;
+  }
+  for (int l = 0; l < 32; ++l) {
+    int h = 0;
+    for (int j = l; j < nrep; j += 32) {
+      if (cofs) cofs[j] = h;
+      h += nb[j];
+    }
+    H = h > H ? h : H;
+  }
+  return H;
+}
+
+// Limb-atomic histogram build (the default shape). Only 32-bit shared-memory atomics are native
+// on sm_100a (64-bit ones compile to CAS spin loops), so each 62-bit fixed-point residual v is
+// offset to u = v + 2^62 (in [0, 2^63)) and split into three 21-bit limbs accumulated with
+// native 32-bit atomics by ALL 1024 threads (any thread may update any bin). Limb sums over at
+// most kAtomSub = 2048 rows stay below 2^32; they are then folded exactly into 64-bit per-bin
+// accumulators: U = S0 + S1*2^21 + S2*2^42, count = (U + 2^61) >> 62 (|sum v| < 2^61 by the
+// choice of the fixed-point shift), sum = U - count*2^62. No count atomic is needed.
+constexpr int kAtomThreads = 1024;
+constexpr int kAtomSub = 2048;
+constexpr int kAtomChunk = 8192;  // max rows per CTA (fewer when the batch is small: >= 2 CTAs per SM)
+constexpr int kAtomTile = 128;
+constexpr uint32_t kLimbMask = (1u << 21) - 1u;
+
+template <typename CodeT>
+__global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
+    int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
+    const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
+    int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr, int colh_max, int chunk) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const NodeRec* nd = nodes + fd.node0;
+  int s;
+  if (level == 0) {
+    if (blockIdx.y) return;
+    s = 0;
+  } else {
+    if (blockIdx.y >= (1u << (level - 1))) return;
+    const int parent = (1 << (level - 1)) - 1 + blockIdx.y;
+    if (nd[parent].state != kNodeSplit) return;
+    s = 2 * parent + 1;
+    if (nd[s].build != 1) s += 1;
+    if (nd[s].build != 1) return;
+  }
+  const int n_v = nd[s].n;
+  const int r0 = blockIdx.x * chunk;
+  if (r0 >= n_v) return;
+  const int rows = min(chunk, n_v - r0);
+  const int seg = nd[s].seg;
+  const int local = s - ((1 << level) - 1);
+  const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
+  const int nrep = fd.nrep, bins = fd.bins;
+  // layout: limbs[3][colh_max][32] u32 (lane columns, see col_height) | acc_sum[bins] i64 |
+  // acc_cnt[bins] i32 | binrep[bins] u16 | boff[nrep] | cofs[nrep] | tile codes | tile limbs
+  uint32_t* limb = reinterpret_cast<uint32_t*>(smem);
+  int64_t* acc_sum =
+      reinterpret_cast<int64_t*>(smem + ((static_cast<size_t>(3) * colh_max * 32 * 4 + 15) & ~size_t(15)));
+  int32_t* acc_cnt = reinterpret_cast<int32_t*>(acc_sum + bins);
+  uint16_t* s_binrep = reinterpret_cast<uint16_t*>(acc_cnt + bins);
+  int32_t* s_boff = reinterpret_cast<int32_t*>(s_binrep + ((bins + 1) & ~1));
+  int32_t* s_cofs = s_boff + nrep;
+  int32_t* s_nbv = s_cofs + nrep;
+  unsigned char* tail = reinterpret_cast<unsigned char*>(s_nbv + nrep);
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                              // [kAtomTile][Dp]
+  uint32_t* t_limb = reinterpret_cast<uint32_t*>(t_codes + kAtomTile * Dp);     // [kAtomTile][3]
+  __shared__ unsigned long long s_abs;
+  __shared__ int s_colh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < bins; b += kAtomThreads) {
+    acc_sum[b] = 0;
+    acc_cnt[b] = 0;
+  }
+  for (int j = tid; j < nrep; j += kAtomThreads) {
+    const int b0 = rep_boff[fd.rep0 + j];
+    const int b1 = j + 1 < nrep ? rep_boff[fd.rep0 + j + 1] : bins;
+    s_boff[j] = b0;
+    s_nbv[j] = b1 - b0;
+    for (int b = b0; b < b1; ++b) s_binrep[b] = static_cast<uint16_t>(j);
+  }
+  if (tid == 0) s_abs = 0;
+  __syncthreads();
+  if (tid == 0) s_colh = col_height(nrep, s_nbv, s_cofs);
+  __syncthreads();
+  const int colh = s_colh;
+  const int rpw = nrep <= 32 ? 32 / nrep : 1;  // rows per warp step (lane copies, nrep <= 32)
+  const int hj = nrep <= 32 ? lane % nrep : lane;
+  const int hm = nrep <= 32 ? lane / nrep : 0;
+  const bool hact = nrep <= 32 ? hm < rpw : true;
+  const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
+  for (int sub0 = 0; sub0 < rows; sub0 += kAtomSub) {
+    for (int i = tid; i < 3 * colh * 32; i += kAtomThreads) limb[i] = 0;
+    __syncthreads();
+    const int sub_end = min(rows, sub0 + kAtomSub);
+    for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
+      const int tr = min(kAtomTile, sub_end - t0);
+      for (int i = tid; i < tr * vec_per_row; i += kAtomThreads) {
+        const int r = i / vec_per_row, v = i - r * vec_per_row;
+        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+        reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+      }
+      unsigned long long a = 0;
+      if (tid < tr) {
+        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid];
+        const int64_t v = rfix[p];
+        const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+        t_limb[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;
+        t_limb[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;
+        t_limb[3 * tid + 2] = static_cast<uint32_t>(u >> 42);
+        a = static_cast<unsigned long long>(v < 0 ? -v : v);
+      }
+      if (warp * 32 < tr) {
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0 && a) atomicAdd(&s_abs, a);
+      }
+      __syncthreads();
+      // lane columns: every lane adds into its own bank column -> one wavefront per atomic
+      if (hact) {
+        uint32_t* colp = limb + lane;
+        if (nrep <= 32) {
+          for (int r = warp * rpw + hm; r < tr; r += (kAtomThreads / 32) * rpw) {
+            const uint32_t* tl = t_limb + 3 * r;
+            uint32_t* c = colp + static_cast<int>(t_codes[r * Dp + hj]) * 32;
+            atomicAdd(c, tl[0]);
+            atomicAdd(c + colh * 32, tl[1]);
+            atomicAdd(c + 2 * colh * 32, tl[2]);
+          }
+        } else {
+          for (int r = warp; r < tr; r += kAtomThreads / 32) {
+            const uint32_t l0 = t_limb[3 * r], l1 = t_limb[3 * r + 1], l2 = t_limb[3 * r + 2];
+            const CodeT* cr = t_codes + r * Dp;
+            for (int j = lane; j < nrep; j += 32) {
+              uint32_t* c = colp + (s_cofs[j] + static_cast<int>(cr[j])) * 32;
+              atomicAdd(c, l0);
+              atomicAdd(c + colh * 32, l1);
+              atomicAdd(c + 2 * colh * 32, l2);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    for (int b = tid; b < bins; b += kAtomThreads) {
+      const int j = s_binrep[b], bb = b - s_boff[j];
+      unsigned __int128 U = 0;
+      if (nrep <= 32) {
+        for (int m = 0; m < rpw; ++m) {
+          const uint32_t* c = limb + bb * 32 + j + m * nrep;
+          U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+               (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+        }
+      } else {
+        const uint32_t* c = limb + (s_cofs[j] + bb) * 32 + (j & 31);
+        U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+            (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+      }
+      const uint64_t c = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
+      const unsigned __int128 sv = U - (static_cast<unsigned __int128>(c) << 62);
+      acc_sum[b] += static_cast<int64_t>(static_cast<uint64_t>(sv));
+      acc_cnt[b] += static_cast<int32_t>(c);
+    }
+    __syncthreads();
+  }
+  for (int b = tid; b < bins; b += kAtomThreads) {
+    if (acc_cnt[b]) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(hsum + hbase + b), static_cast<unsigned long long>(acc_sum[b]));
+      atomicAdd(hcnt + hbase + b, acc_cnt[b]);
+    }
+  }
+  if (tid == 0) {
+    if (s_abs) atomicAdd(reinterpret_cast<unsigned long long*>(node_abs + fd.node0 + s), s_abs);
+    atomicAdd(ctr + kCtrHistBytes,
+              static_cast<unsigned long long>(rows) * (static_cast<unsigned long long>(nrep) * sizeof(CodeT) + 12ull));
+    atomicAdd(ctr + kCtrHistRows, static_cast<unsigned long long>(rows));
+  }
+}
+
+inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes, int colh) {
+  size_t o = (static_cast<size_t>(3) * colh * 32 * 4 + 15) & ~size_t(15);
+  o += static_cast<size_t>(bins) * 14 + static_cast<size_t>(nrep) * 12 + 16;
+  o = (o + 15) & ~size_t(15);
+  o += static_cast<size_t>(kAtomTile) * Dp * code_bytes + static_cast<size_t>(kAtomTile) * 12 + 16;
+  return o;
+}
+
+// sibling = parent - built child (exact: integer histograms)
+__global__ void hist_derive_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                   const NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
+                                   int32_t* __restrict__ hcnt, int64_t* __restrict__ node_abs) {
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active || level == 0) return;
+  const NodeRec* nd = nodes + fd.node0;
+  const int k = blockIdx.y;
+  if (k >= (1 << (level - 1))) return;
+  const int parent = (1 << (level - 1)) - 1 + k;
+  if (nd[parent].state != kNodeSplit) return;
+  const int c1 = 2 * parent + 1, c2 = c1 + 1;
+  int built, other;
+  if (nd[c1].build == 1 && nd[c2].build == 2) {
+    built = c1;
+    other = c2;
+  } else if (nd[c2].build == 1 && nd[c1].build == 2) {
+    built = c2;
+    other = c1;
+  } else {
+    return;
+  }
+  const int first = (1 << level) - 1, pfirst = (1 << (level - 1)) - 1;
+  const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + (built - first)) * fd.bins;
+  const int64_t ho = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + (other - first)) * fd.bins;
+  const int64_t hp = fd.hist0 + (static_cast<int64_t>((level - 1) & 1) * fd.level_slots + (parent - pfirst)) * fd.bins;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < fd.bins; b += gridDim.x * blockDim.x) {
+    hsum[ho + b] = hsum[hp + b] - hsum[hb + b];
+    hcnt[ho + b] = hcnt[hp + b] - hcnt[hb + b];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    node_abs[fd.node0 + other] = node_abs[fd.node0 + parent] - node_abs[fd.node0 + built];
+}
+
+// Screened gain of one candidate plus a rigorous bound on |reference gain - screened gain|.
+// ls/ts: fixed-point left/total sums; S: sum|r| of the node (real units); scale = 2^-shift.
+// The reference folds sums sequentially (error <= gamma_n * S each), R = T - L rounds once,
+// then ((L*L)/lc + (R*R)/rc) - (T*T)/n rounds ~5 more times; the screen's sums are exact on
+// the quantised residuals (quantisation <= n * scale / 2). Factor 2 covers both sides.
+__device__ __forceinline__ void screen_gain(int64_t ls, int64_t ts, int lc, int n, double scale, double S, double& g,
+                                            double& lo, double& hi) {
+  const double u = 1.1102230246251565e-16;
+  const double L = static_cast<double>(ls) * scale, T = static_cast<double>(ts) * scale;
+  const double R = static_cast<double>(ts - ls) * scale;
+  const int rc = n - lc;
+  // three reciprocals instead of nine divisions; their extra rounding (<= 1 ulp per term) is
+  // covered by the 6u term below
+  const double ilc = 1.0 / lc, irc = 1.0 / rc, in = 1.0 / n;
+  const double A = L * L * ilc, B = R * R * irc, P = T * T * in;
+  g = (A + B) - P;
+  const double nu = static_cast<double>(n) * u;
+  const double gam = nu / (1.0 - nu);
+  const double q = static_cast<double>(n) * 0.5 * scale;
+  const double EL = gam * S + q, ET = gam * S + q, ER = 2.0 * gam * S + 2.0 * q + u * fabs(R);
+  const double aL = fabs(L) + EL, aR = fabs(R) + ER, aT = fabs(T) + ET;
+  const double dA = ((2.0 * fabs(L) + EL) * EL + 4.0 * u * aL * aL) * ilc;
+  const double dB = ((2.0 * fabs(R) + ER) * ER + 4.0 * u * aR * aR) * irc;
+  const double dP = ((2.0 * fabs(T) + ET) * ET + 4.0 * u * aT * aT) * in;
+  const double delta = 2.0 * (dA + dB + dP + 6.0 * u * (A + B + P)) * (1.0 + 8.0 * u) + 1e-300;
+  lo = g - delta;
+  hi = g + delta;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+  for (int o = 1; o < 32; o <<= 1) {
+    const T t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// One thread per (family, node at level, rep). pass 0: max lower bound per node. pass 1:
+// window membership (hi >= LO and hi > 0), per-feature best candidate, node window count.
+__global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                              NodeRec* __restrict__ nodes, int level, const int64_t* __restrict__ hsum,
+                              const int32_t* __restrict__ hcnt, const int64_t* __restrict__ node_abs,
+                              const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
+                              WinRec* __restrict__ win, int nrep_max, int level_slots_max, int pass) {
+  // warp per (node, rep), lanes over the rep's bins: coalesced histogram reads, warp prefix
+  // scans for the left count / sum, every candidate's screen in parallel
+  const int f = blockIdx.z;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.y;
+  if (local >= (1 << level)) return;
+  const int lane = threadIdx.x & 31;
+  const int jj = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (jj >= fd.nrep) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != 0 || nd.build == 0) return;
+  const int n = nd.n;
+  const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins +
+                     rep_boff[fd.rep0 + jj];
+  const int nb = rep_nb[fd.rep0 + jj];
+  const double scale = ldexp(1.0, -st[f].shift);
+  const double S = static_cast<double>(node_abs[fd.node0 + s]) * scale * (1.0 + 1e-12);
+  int64_t ts = 0;
+  for (int b = lane; b < nb; b += 32) ts += hsum[hb + b];
+  for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+  const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
+  double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
+  int bb = 0x7fffffff, blc = 0, count = 0, mlc = 0, carry_c = 0;
+  int64_t carry_s = 0;
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    const int cc = b < nb ? hcnt[hb + b] : 0;
+    const int64_t sv = b < nb ? hsum[hb + b] : 0;
+    const int ic = warp_incl_scan(cc, lane) + carry_c;
+    const int64_t is = warp_incl_scan(sv, lane) + carry_s;
+    if (b < nb && cc > 0 && ic < n) {  // a boundary after bin b (a later bin is non-empty)
+      double g, lo, hi;
+      screen_gain(is, ts, ic, n, scale, S, g, lo, hi);
+      if (!pass) {
+        best_lo = fmax(best_lo, lo);
+      } else if (hi >= LO && hi > 0.0) {
+        ++count;
+        mlc = max(mlc, ic);
+        if (g > bg || (g == bg && b < bb)) {
+          bg = g;
+          bl = lo;
+          bb = b;
+          blc = ic;
+        }
+      }
+    }
+    carry_c = __shfl_sync(0xffffffffu, ic, 31);
+    carry_s = __shfl_sync(0xffffffffu, is, 31);
+  }
+  if (!pass) {
+    for (int o = 16; o > 0; o >>= 1) best_lo = fmax(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
+    if (lane == 0 && best_lo > -INFINITY)
+      atomicMax(reinterpret_cast<unsigned long long*>(&nd.lokey), lo_key(best_lo));
+  } else {
+    for (int o = 16; o > 0; o >>= 1) {
+      count += __shfl_xor_sync(0xffffffffu, count, o);
+      mlc = max(mlc, __shfl_xor_sync(0xffffffffu, mlc, o));
+      const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+      const int olc = __shfl_xor_sync(0xffffffffu, blc, o);
+      if (og > bg || (og == bg && ob < bb)) {
+        bg = og;
+        bl = ol;
+        bb = ob;
+        blc = olc;
+      }
+    }
+    if (lane == 0) {
+      WinRec w;
+      w.best_g = bg;
+      w.best_lo = bl;
+      w.best_bin = count ? bb : -1;
+      w.flag = count > 0;
+      w.count = count;
+      w.best_lc = blc;
+      w.eq = 0;
+      w.maxlc = mlc;
+      win[(static_cast<int64_t>(f) * level_slots_max + local) * nrep_max + jj] = w;
+      if (count) atomicAdd(&nd.wcount, count);
+    }
+  }
+}
+
+struct ExactItem {
+  int32_t fam;
+  int16_t slot;
+  int16_t rep;  // -1: node total
+};
+
+// Tie classes: a node whose window holds exactly one candidate per feature, all with the same
+// left count, is one tie class if every window feature orders the node's rows exactly like the
+// lowest one (identical folds, identical reference gains; strict > keeps the lowest feature).
+// Prep queues one order-equivalence check per (node, other window feature).
+// The per-node decision kernels below run a warp per (family, node) with lanes over the
+// node's features (window records read in parallel; ballots replace the serial scans).
+__device__ __forceinline__ int first_flag_feature(const WinRec* w, int nrep, int from, bool need_count1,
+                                                  bool& multi) {
+  // lowest flagged feature >= from; multi = some flagged feature has count != 1 (when asked)
+  const int lane = threadIdx.x & 31;
+  int first = -1;
+  multi = false;
+  for (int j0 = from; j0 < nrep; j0 += 32) {
+    const int j = j0 + lane;
+    const bool fl = j < nrep && w[j].flag;
+    const unsigned m = __ballot_sync(0xffffffffu, fl);
+    if (need_count1 && __any_sync(0xffffffffu, fl && w[j].count != 1)) multi = true;
+    if (m && first < 0) first = j0 + __ffs(m) - 1;
+  }
+  return first;
+}
+
+__global__ void tieclass_prep_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                     NodeRec* __restrict__ nodes, int level, const WinRec* __restrict__ win,
+                                     int nrep_max, int level_slots_max, ExactItem* __restrict__ items,
+                                     int* __restrict__ n_items) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int lane = threadIdx.x & 31;
+  const int local = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (lane == 0) nd.eqf0 = -1;
+  if (nd.state != 0 || nd.build == 0 || nd.wcount < 2) return;
+  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
+  bool multi;
+  const int f0 = first_flag_feature(w, fd.nrep, 0, true, multi);
+  if (multi || f0 < 0 || !(w[f0].best_lo > 0.0)) return;
+  const int lc0 = w[f0].best_lc;
+  bool diff = false;
+  for (int j0 = f0 + 1; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    if (__any_sync(0xffffffffu, j < fd.nrep && w[j].flag && w[j].best_lc != lc0)) diff = true;
+  }
+  if (diff) return;
+  if (lane == 0) nd.eqf0 = f0;
+  for (int j0 = f0 + 1; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    const bool fl = j < fd.nrep && w[j].flag;
+    const unsigned m = __ballot_sync(0xffffffffu, fl);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(n_items, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (fl) items[base + __popc(m & ((1u << lane) - 1u))] = {f, static_cast<int16_t>(s), static_cast<int16_t>(j)};
+  }
+}
+
+__global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                              NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
+                              const int32_t* __restrict__ rep_boff, const WinRec* __restrict__ win, int nrep_max,
+                              int level_slots_max, ExactItem* __restrict__ items, int* __restrict__ n_items,
+                              unsigned long long* __restrict__ ctr) {
+  (void)hcnt;
+  (void)rep_boff;
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int lane = threadIdx.x & 31;
+  const int local = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != 0 || nd.build == 0) return;
+  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
+  if (nd.wcount == 0) {  // no candidate can have a positive reference gain
+    if (lane == 0) nd.state = kNodeLeaf;
+    return;
+  }
+  int pick = -1;
+  if (nd.wcount == 1) {
+    bool multi;
+    const int j = first_flag_feature(w, fd.nrep, 0, false, multi);
+    if (j >= 0 && w[j].best_lo > 0.0) pick = j;
+  } else if (nd.eqf0 >= 0) {  // one tie class: the lowest feature wins by strict >
+    bool all = true;
+    for (int j0 = nd.eqf0 + 1; j0 < fd.nrep; j0 += 32) {
+      const int j = j0 + lane;
+      if (__any_sync(0xffffffffu, j < fd.nrep && w[j].flag && !w[j].eq)) all = false;
+    }
+    if (all) pick = nd.eqf0;
+  }
+  if (pick >= 0) {
+    if (lane == 0) {
+      nd.state = kNodeSplit;
+      nd.rep = pick;
+      nd.bin = w[pick].best_bin;
+      nd.gain = w[pick].best_g;
+      nd.lc = w[pick].best_lc;
+      atomicAdd(&const_cast<FamState*>(st)[f].screened, 1ull);
+    }
+    return;
+  }
+  const int tot = nd.pad_ ? 0 : 1;  // node total still to fold (not precomputed by totals_kernel)
+  int k = tot;
+  for (int j0 = 0; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    k += __popc(__ballot_sync(0xffffffffu, j < fd.nrep && w[j].flag));
+  }
+  int base = 0;
+  if (lane == 0) {
+    nd.state = kNodeExact;
+    atomicAdd(&const_cast<FamState*>(st)[f].exact, 1ull);
+    base = atomicAdd(n_items, k);
+    atomicAdd(ctr + kCtrExactChains, static_cast<unsigned long long>(k));
+    atomicAdd(ctr + kCtrExactNodes, 1ull);
+    if (tot) items[base] = {f, static_cast<int16_t>(s), static_cast<int16_t>(-1)};
+  }
+  base = __shfl_sync(0xffffffffu, base, 0) + tot;
+  for (int j0 = 0; j0 < fd.nrep; j0 += 32) {
+    const int j = j0 + lane;
+    const bool fl = j < fd.nrep && w[j].flag;
+    const unsigned m = __ballot_sync(0xffffffffu, fl);
+    if (fl) items[base + __popc(m & ((1u << lane) - 1u))] = {f, static_cast<int16_t>(s), static_cast<int16_t>(j)};
+    base += __popc(m);
+  }
+}
+
+// One warp per check: walk the lowest window feature's presorted list restricted to the node;
+// the other feature must tie exactly where it ties and increase where it increases.
+// Order equivalence of g with f0 on the node's rows <=> the map code_f0 -> code_g over those rows
+// is a function that strictly increases (ties align, and the stable sorts by (code, canonical
+// position) then coincide). CTA per item: phi[a] = the g code of some row with f0 code a (racy
+// plain stores), every row must agree with phi, phi must increase over the present a. Rows come
+// from the node's order-0 segment, in any order - no scan of the presorted lists.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) tieclass_phi_kernel(
+    const FamDesc* __restrict__ fam, const NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const int32_t* __restrict__ ord_cur, const int32_t* __restrict__ rep_nb, WinRec* __restrict__ win,
+    int nrep_max, int level_slots_max) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* phi = reinterpret_cast<uint16_t*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int total = *n_items;
+  for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+    const ExactItem it = items[wi];
+    const FamDesc fd = fam[it.fam];
+    const NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int f0 = nd.eqf0, g = it.rep, nv = nd.n;
+    const int nb = rep_nb[fd.rep0 + f0];
+    const int32_t* rows = ord_cur + fd.pos0 + nd.seg;
+    const CodeT* cb = codes_c + fd.pos0 * Dp;
+    __syncthreads();  // previous item done with phi
+    for (int a = tid; a < nb; a += blockDim.x) phi[a] = 0xFFFFu;
+    __syncthreads();
+    for (int i = tid; i < nv; i += blockDim.x) {
+      const int64_t p = rows[i];
+      phi[cb[p * Dp + f0]] = static_cast<uint16_t>(cb[p * Dp + g]);
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int i = tid; i < nv; i += blockDim.x) {
+      const int64_t p = rows[i];
+      bad |= phi[cb[p * Dp + f0]] != static_cast<uint16_t>(cb[p * Dp + g]);
+    }
+    if (tid < 32) {  // phi strictly increasing over the present f0 codes
+      int carry = -1;
+      for (int a0 = 0; a0 < nb; a0 += 32) {
+        const int a = a0 + lane;
+        const int v = a < nb ? phi[a] : 0xFFFF;
+        const bool present = v != 0xFFFF;
+        const unsigned m = __ballot_sync(0xffffffffu, present);
+        const unsigned lt = m & ((1u << lane) - 1u);
+        int pv = __shfl_sync(0xffffffffu, v, lt ? 31 - __clz(lt) : 0);
+        if (!lt) pv = carry;
+        if (present && pv >= 0 && v <= pv) bad = true;
+        if (m) carry = __shfl_sync(0xffffffffu, v, 31 - __clz(m));
+      }
+    }
+    bad = __syncthreads_or(bad);
+    const int local = it.slot - ((1 << level) - 1);
+    if (tid == 0) win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + g].eq = !bad;
+  }
+}
+
+template <typename CodeT>
+__global__ void __launch_bounds__(256) tieclass_check_kernel(
+    const FamDesc* __restrict__ fam, const NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const int32_t* __restrict__ ord, const int16_t* __restrict__ nodeid, WinRec* __restrict__ win, int nrep_max,
+    int level_slots_max) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int total = *n_items;
+  for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < total; wi += warps) {
+    const ExactItem it = items[wi];
+    const FamDesc fd = fam[it.fam];
+    const NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int f0 = nd.eqf0, g = it.rep, nv = nd.n, n = fd.n;
+    const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(f0) * n;
+    int pf = -1, pg = -1, seen = 0;
+    bool bad = false;
+    int p_next = lane < n ? L[lane] : 0;
+    for (int i0 = 0; i0 < n && seen < nv; i0 += 32) {
+      const int i = i0 + lane;
+      const int p = p_next;
+      p_next = i + 32 < n ? L[i + 32] : 0;
+      const bool mem = i < n && nodeid[fd.pos0 + p] == it.slot;
+      const int a = mem ? static_cast<int>(codes_c[(fd.pos0 + p) * Dp + f0]) : 0;
+      const int b = mem ? static_cast<int>(codes_c[(fd.pos0 + p) * Dp + g]) : 0;
+      const unsigned m = __ballot_sync(0xffffffffu, mem);
+      seen += __popc(m);
+      const unsigned lt = m & ((1u << lane) - 1u);
+      const int src = lt ? 31 - __clz(lt) : lane;
+      int qa = __shfl_sync(0xffffffffu, a, src), qb = __shfl_sync(0xffffffffu, b, src);
+      if (!lt) {
+        qa = pf;
+        qb = pg;
+      }
+      if (mem && qa >= 0 && ((a == qa) != (b == qb) || b < qb)) bad = true;
+      if (m) {
+        const int last = 31 - __clz(m);
+        pf = __shfl_sync(0xffffffffu, a, last);
+        pg = __shfl_sync(0xffffffffu, b, last);
+      }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    const int local = it.slot - ((1 << level) - 1);
+    if (lane == 0) win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + g].eq = !bad;
+  }
+}
+
+// Decide screened nodes; queue the rest for reference-order re-evaluation.
+__device__ __forceinline__ double warp_fold_gather(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                   int n) {
+  // Software-pipelined: the next 128 gathers (L2 latency) are in flight while the current 128
+  // values are folded in order (the dependent FP64 add chain).
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  double x[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = 32 * c + lane;
+    x[c] = i < n ? v[idx[i]] : 0.0;
+  }
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    double y[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 128 + 32 * c + lane;
+      y[c] = i < n ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int base = i0 + 32 * c;
+      if (base >= n) break;
+      const int m = min(32, n - base);
+      if (m == 32) {
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          double t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
+        }
+      } else {
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = y[c];
+  }
+  return s;
+}
+
+// Node totals (costmodel.cpp:47, sum_residuals over the feature-0 list) for every node of the
+// level that will be screened, on a forked stream: the reference-order chains run while the
+// histogram / screen / tie-class kernels of the same level do. nd.pad_ = 1 marks the total valid
+// (exact decisions and leaf values then reuse it - the same fold over the same segment).
+__global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                              NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ ord_cur,
+                              const double* __restrict__ resid) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (local >= (1 << level)) return;
+  NodeRec& nd = nodes[fd.node0 + (1 << level) - 1 + local];
+  if (nd.state != 0 || nd.build == 0 || nd.n <= 0) return;
+  const double t = warp_fold_gather(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, nd.n);
+  if ((threadIdx.x & 31) == 0) {
+    nd.total = t;
+    nd.pad_ = 1;
+  }
+}
+
+
+// sum_residuals (costmodel.cpp:36-40) of v[idx[0..n)) in list order by one warp: four chunks of
+// 32 gathers are in flight at once, then each chunk's values are added in lane order (shuffles
+// hoisted ahead of the dependent add chain). Every lane returns the sum.
+
+// One warp per item: reference-order folds. Item rep < 0: node total over the order-0 list
+// (sum_residuals(order[0]), costmodel.cpp:47). Item rep j: best_split's left sums over feature j's
+// presorted list restricted to the node (:50-55), recorded at every value boundary.
+// exact folds of nodes below a quarter of the family go through exact_small_kernel
+__device__ __forceinline__ bool exact_is_small(int nv, int n) { return nv < n; }
+
+// Exact reference-order folds for SMALL nodes (nv * 4 < n): instead of scanning the feature's
+// full presorted list for the node's members (exact_kernel; costs O(n) gathers per item however
+// small the node), a CTA compacts the node's rows in canonical order (a coalesced scan of the
+// node ids), stable-sorts them by the feature's code (the presorted order restricted to the
+// node is exactly (code, canonical position) order), and warp 0 folds them - the same adds in
+// the same order as best_split (costmodel.cpp:50-69), stopping at the last window candidate.
+template <typename CodeT>
+__global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
+    const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const double* __restrict__ resid, const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_boff,
+    double* __restrict__ lbuf, const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
+    int32_t* __restrict__ scratch, int n_max) {
+  __shared__ SortSmem sm;
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total = *n_items;
+  sort_smem_init(sm);
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const ExactItem it = items[w];
+    if (it.rep < 0) continue;
+    const FamDesc fd = fam[it.fam];
+    const NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int nv = nd.n, n = fd.n;
+    if (!exact_is_small(nv, n)) continue;
+    const int jj = it.rep;
+    const int local = it.slot - ((1 << level) - 1);
+    const int need = win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + jj].maxlc;
+    double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    int32_t* A = scratch + static_cast<int64_t>(blockIdx.x) * 2 * n_max;
+    int32_t* B = A + n_max;
+    // 1. the node's rows in canonical order
+    int base = 0;
+    for (int p0 = 0; p0 < n; p0 += blockDim.x) {
+      const int p = p0 + tid;
+      const bool mem = p < n && nodeid[fd.pos0 + p] == it.slot;
+      const unsigned m = __ballot_sync(0xffffffffu, mem);
+      if (lane == 0) wsum[warp] = __popc(m);
+      __syncthreads();
+      if (warp == 0) {
+        const int v = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+        int incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        wsum[lane] = incl - v;
+        if (lane == 31) sm.uniform = incl;  // chunk total (borrowed field)
+      }
+      __syncthreads();
+      if (mem) A[base + wsum[warp] + __popc(m & ((1u << lane) - 1u))] = p;
+      base += sm.uniform;
+      __syncthreads();
+    }
+    // 2. stable sort by the feature's code: (code, canonical position) = presorted order
+    const CodeT* cj = codes_c + static_cast<int64_t>(fd.pos0) * Dp + jj;
+    int32_t* src = A;
+    int32_t* dst = B;
+    if (stable_digit_pass([&](int i) { return src[i]; }, dst, nv,
+                          [&](int p) { return static_cast<int>(cj[static_cast<int64_t>(p) * Dp] & 255u); }, sm)) {
+      int32_t* t = src;
+      src = dst;
+      dst = t;
+    }
+    __syncthreads();
+    if (sizeof(CodeT) == 2) {
+      if (stable_digit_pass([&](int i) { return src[i]; }, dst, nv,
+                            [&](int p) { return static_cast<int>(cj[static_cast<int64_t>(p) * Dp] >> 8); }, sm)) {
+        int32_t* t = src;
+        src = dst;
+        dst = t;
+      }
+      __syncthreads();
+    }
+    // 3. the fold (warp 0; members in list order, boundaries at code changes)
+    if (warp == 0) {
+      double left = 0.0;
+      int prev = -1;
+      for (int i0 = 0; i0 < need; i0 += 32) {
+        const int i = i0 + lane;
+        const int p = i < need ? src[i] : 0;
+        const int code = i < need ? static_cast<int>(cj[static_cast<int64_t>(p) * Dp]) : 0;
+        const double rv = i < need ? resid[fd.pos0 + p] : 0.0;
+        const int cnt = min(32, need - i0);
+        for (int l0 = 0; l0 < cnt; l0 += 8) {
+          int cc[8];
+          double vv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            cc[k] = __shfl_sync(0xffffffffu, code, l0 + k);
+            vv[k] = __shfl_sync(0xffffffffu, rv, l0 + k);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (l0 + k < cnt) {
+              if (prev >= 0 && cc[k] != prev && lane == 0) out[prev] = left;
+              left = fs_add(left, vv[k]);
+              prev = cc[k];
+            }
+          }
+        }
+      }
+      if (lane == 0 && prev >= 0) out[prev] = left;  // the last window boundary
+    }
+    __syncthreads();
+  }
+}
+
+template <typename CodeT>
+__global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes,
+                                                    const ExactItem* __restrict__ items, const int* __restrict__ n_items,
+                                                    int level, int Dp, const CodeT* __restrict__ codes_c,
+                                                    const double* __restrict__ resid, const int32_t* __restrict__ ord,
+                                                    const int32_t* __restrict__ ord_cur,
+                                                    const int16_t* __restrict__ nodeid,
+                                                    const int32_t* __restrict__ rep_boff, double* __restrict__ lbuf,
+                                                    const WinRec* __restrict__ win, int nrep_max,
+                                                    int level_slots_max, int small_path) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int total = *n_items;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += warps) {
+    const ExactItem it = items[w];
+    const FamDesc fd = fam[it.fam];
+    NodeRec& nd = nodes[fd.node0 + it.slot];
+    const int n = nd.n;
+    if (it.rep < 0) {
+      const double s = warp_fold_gather(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, n);
+      if (lane == 0) nd.total = s;
+      continue;
+    }
+    if (exact_is_small(n, fd.n) && small_path) continue;  // exact_small_kernel folds it
+    const int jj = it.rep;
+    const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
+    const int local = it.slot - ((1 << level) - 1);
+    double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    double left = 0.0;
+    int prev = -1, seen = 0, used = 0;
+    // candidates past the feature's largest window left count cannot win (costmodel.cpp:65
+    // strict >): the fold stops there
+    const int need = win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + jj].maxlc;
+    // 4 chunks of 32 list entries in flight: index loads, then the dependent gathers
+    for (int i0 = 0; i0 < fd.n && seen < need; i0 += 128) {
+      int p[4], code[4];
+      double rv[4];
+      bool mem[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) p[c] = i0 + 32 * c + lane < fd.n ? L[i0 + 32 * c + lane] : -1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mem[c] = p[c] >= 0 && nodeid[fd.pos0 + p[c]] == it.slot;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        code[c] = mem[c] ? static_cast<int>(codes_c[(fd.pos0 + p[c]) * Dp + jj]) : 0;
+        rv[c] = mem[c] ? resid[fd.pos0 + p[c]] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, mem[c]);
+        seen += __popc(m);
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          if (!((m >> l0) & 0xFFu)) continue;
+          int cc[8];
+          double vv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            cc[k] = __shfl_sync(0xffffffffu, code[c], l0 + k);
+            vv[k] = __shfl_sync(0xffffffffu, rv[c], l0 + k);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (((m >> (l0 + k)) & 1u) && used < need) {
+              if (prev >= 0 && cc[k] != prev && lane == 0) out[prev] = left;  // boundary after bin `prev`
+              left = fs_add(left, vv[k]);
+              prev = cc[k];
+              ++used;
+            }
+          }
+        }
+      }
+    }
+    if (lane == 0 && prev >= 0 && used == need) out[prev] = left;  // the last window boundary
+  }
+}
+
+// Reference decision over the exactly folded candidates: gain = ((L*L)/lc + (R*R)/rc) - (T*T)/n,
+// R = T - L (costmodel.cpp:58-62), strict > in (feature, threshold) order (:65).
+__global__ void exact_decide_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                    NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ hcnt,
+                                    const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
+                                    const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
+                                    const double* __restrict__ lbuf) {
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeExact) return;
+  const WinRec* w = win + (static_cast<int64_t>(f) * level_slots_max + local) * nrep_max;
+  const int n = nd.n;
+  const double T = nd.total;
+  const double parent = fs_div(fs_mul(T, T), static_cast<double>(n));
+  double best = 0.0;
+  int bj = -1, bb = -1, blc = 0;
+  for (int jj = 0; jj < fd.nrep; ++jj) {
+    if (!w[jj].flag) continue;
+    const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins +
+                       rep_boff[fd.rep0 + jj];
+    const double* lb = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    if (w[jj].count == 1) {  // its window candidate is the only one of this feature that can win
+      const int cum = w[jj].best_lc, b = w[jj].best_bin;
+      const double L = lb[b];
+      const double R = fs_sub(T, L);
+      const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+      const double r = fs_div(fs_mul(R, R), static_cast<double>(n - cum));
+      const double g = fs_sub(fs_add(a, r), parent);
+      if (g > best) {
+        best = g;
+        bj = jj;
+        bb = b;
+        blc = cum;
+      }
+      continue;
+    }
+    int cum = 0;
+    for (int b = 0; b < rep_nb[fd.rep0 + jj]; ++b) {
+      const int c = hcnt[hb + b];
+      if (!c) continue;
+      cum += c;
+      if (cum >= n || cum > w[jj].maxlc) break;  // folds stop at the last window candidate
+      const double L = lb[b];
+      const double R = fs_sub(T, L);
+      const double a = fs_div(fs_mul(L, L), static_cast<double>(cum));
+      const double r = fs_div(fs_mul(R, R), static_cast<double>(n - cum));
+      const double g = fs_sub(fs_add(a, r), parent);
+      if (g > best) {
+        best = g;
+        bj = jj;
+        bb = b;
+        blc = cum;
+      }
+    }
+  }
+  if (bj < 0) {
+    nd.state = kNodeLeaf;
+  } else {
+    nd.state = kNodeSplit;
+    nd.rep = bj;
+    nd.bin = bb;
+    nd.gain = best;
+    nd.lc = blc;
+  }
+}
+
+// Split nodes: exact threshold, tree record, stable partition of the order-0 segment in place
+// (costmodel.cpp:94-105 for list 0), row -> child ids, child records.
+template <typename CodeT>
+__global__ void __launch_bounds__(1024) partition_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level, int Dp,
+    const CodeT* __restrict__ codes_c, int32_t* __restrict__ ord_cur, int32_t* __restrict__ scratch,
+    int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_boff,
+    const double* __restrict__ vals, const int32_t* __restrict__ cle, const int32_t* __restrict__ ord,
+    const int32_t* __restrict__ canon, const double* __restrict__ x, int d, TreeRec* __restrict__ trees, int slots) {
+  __shared__ int wsum[32];
+  __shared__ int base_l, base_r;
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x;
+  if (local >= (1 << level)) return;
+  const int s = (1 << level) - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeSplit) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int jj = nd.rep, bin = nd.bin, n = nd.n, seg = nd.seg, lc = nd.lc;
+  TreeRec* tr = trees + fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots;
+  if (tid == 0) {
+    const int orig = rep_orig[fd.rep0 + jj];
+    double thr = vals[fd.bin0 + rep_boff[fd.rep0 + jj] + bin];
+    if (thr == 0.0 && fd.negz) {  // +0.0 and -0.0 share a bin: take the last left element's own value
+      const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
+      for (int i = cle[fd.bin0 + rep_boff[fd.rep0 + jj] + bin] - 1; i >= 0; --i) {
+        if (nodeid[fd.pos0 + L[i]] == s) {
+          thr = x[(fd.row0 + canon[fd.pos0 + L[i]]) * d + orig];
+          break;
+        }
+      }
+    }
+    TreeRec r;
+    r.kind = kNodeSplit;
+    r.feature = orig;
+    r.threshold = thr;
+    r.value = 0.0;
+    r.gain = nd.gain;
+    r.rep = jj;
+    r.bin = bin;
+    tr[s] = r;
+    base_l = 0;
+    base_r = 0;
+    NodeRec& a = nodes[fd.node0 + 2 * s + 1];
+    NodeRec& b = nodes[fd.node0 + 2 * s + 2];
+    a.n = lc;
+    a.seg = seg;
+    b.n = n - lc;
+    b.seg = seg + lc;
+  }
+  int32_t* src = scratch + fd.pos0 + seg;
+  int32_t* dst = ord_cur + fd.pos0 + seg;
+  for (int i = tid; i < n; i += blockDim.x) src[i] = dst[i];
+  __syncthreads();
+  const int16_t cl = static_cast<int16_t>(2 * s + 1), cr = static_cast<int16_t>(2 * s + 2);
+  // the next chunk's index and code gathers are issued before this chunk's scan and scatter
+  int p_nx = tid < n ? src[tid] : 0;
+  int c_nx = tid < n ? static_cast<int>(codes_c[(fd.pos0 + p_nx) * Dp + jj]) : 0;
+  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+    const int i = t0 + tid;
+    const int p = p_nx;
+    const bool left = i < n && c_nx <= bin;
+    if (i + static_cast<int>(blockDim.x) < n) {
+      p_nx = src[i + blockDim.x];
+      c_nx = static_cast<int>(codes_c[(fd.pos0 + p_nx) * Dp + jj]);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, left);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      const int v = wsum[lane];
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      wsum[lane] = incl - v;
+    }
+    __syncthreads();
+    const int lrank = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+    if (i < n) {
+      if (left) {
+        dst[base_l + lrank] = p;
+        nodeid[fd.pos0 + p] = cl;
+      } else {
+        dst[lc + base_r + (i - t0) - lrank] = p;
+        nodeid[fd.pos0 + p] = cr;
+      }
+    }
+    __syncthreads();  // every thread has used base_l / base_r for this tile
+    if (warp == 31 && lane == 0) {  // tile total = warp 31's exclusive prefix + its own count
+      const int tile_left = wsum[31] + __popc(bal);
+      const int tile = min(static_cast<int>(blockDim.x), n - t0);
+      base_l += tile_left;
+      base_r += tile - tile_left;
+    }
+    __syncthreads();
+  }
+}
+
+// Leaves: value = (reference-order total) / n (costmodel.cpp:86), prediction += lr * value
+// (:88-90); tree record. One warp per (family, slot).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = fs_add(a, b);
+  const double bb = fs_sub(s, a);
+  e = fs_add(fs_sub(a, fs_sub(s, bb)), fs_sub(b, bb));
+}
+__device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles -> consecutive ints
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : static_cast<long long>(0x8000000000000000ull) - b;
+}
+__device__ __forceinline__ double ord_dbl(long long o) {
+  return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
+}
+// CTA-wide exact sequential fold of a long gathered chain (sum_residuals, costmodel.cpp:36-40) by
+// midpoint speculation (the warp version is fold_spec): the block's double-double sum of
+// x_0..x_{m-1} estimates the exact prefix P; thread 0 folds x_0..x_{m-1} from 0.0 (the true S_m)
+// while threads t = 1..255 fold x_m..x_{n-1} from the doubles P + (t-128) ulp; the thread whose
+// start is bit-identical to S_m holds S_n. A miss finishes the chain from S_m (same result).
+// All 256 threads must call it; the result is returned to every thread.
+__device__ __forceinline__ double warp_fold_gather_from(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                        int n, double s) {
+  // warp_fold_gather with a per-lane start value: every lane folds the same sequence (loaded
+  // cooperatively, 128 gathers in flight ahead of the adds) from its own start
+  const int lane = threadIdx.x & 31;
+  double x[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = 32 * c + lane;
+    x[c] = i < n ? v[idx[i]] : 0.0;
+  }
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    double y[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 128 + 32 * c + lane;
+      y[c] = i < n ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int base = i0 + 32 * c;
+      if (base >= n) break;
+      const int m = min(32, n - base);
+      if (m == 32) {
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          double t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
+        }
+      } else {
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = y[c];
+  }
+  return s;
+}
+
+__device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
+                                                double* red /* smem [2*8+2] */) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = static_cast<int>(blockDim.x >> 5);
+  if (n < 4096 || nw < 2) {  // short chain: warp 0 folds it
+    if (warp == 0) {
+      const double r = warp_fold_gather_from(v, idx, n, 0.0);
+      if (lane == 0) red[16] = r;
+    }
+    __syncthreads();
+    const double r = red[16];
+    __syncthreads();
+    return r;
+  }
+  const int m = n >> 1;
+  // exact-prefix estimate of x_0..x_{m-1}: double-double partial sums (8 gathers in flight)
+  double hi = 0.0, lo = 0.0;
+  for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * blockDim.x;
+      a[k] = i < m ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double s, e;
+      two_sum(hi, a[k], s, e);
+      hi = s;
+      lo = fs_add(lo, e);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, e;
+    two_sum(hi, oh, s, e);
+    hi = s;
+    lo = fs_add(fs_add(lo, ol), e);
+  }
+  if (lane == 0) {
+    red[warp] = hi;
+    red[8 + warp] = lo;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double h = 0.0, l = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      double s, e;
+      two_sum(h, red[w], s, e);
+      h = s;
+      l = fs_add(fs_add(l, red[8 + w]), e);
+    }
+    red[17] = fs_add(h, l);
+  }
+  __syncthreads();
+  const double P = red[17];
+  // warp 0 folds the first half from 0.0 (the true S_m); warps 1.. fold the second half from
+  // the candidate starts P + k ulp, k centred on 0 (32 * (nw - 1) candidates)
+  const int cand = tid - 32;  // 0 .. 32*(nw-1)-1
+  const double start = warp == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (cand - 16 * (nw - 1)));
+  const double r = warp == 0 ? warp_fold_gather_from(v, idx, m, 0.0)
+                             : warp_fold_gather_from(v, idx + m, n - m, start);
+  __shared__ int hit;
+  if (tid == 0) {
+    red[16] = r;  // S_m
+    hit = 0;
+  }
+  __syncthreads();
+  if (warp > 0 && __double_as_longlong(start) == __double_as_longlong(red[16])) {
+    red[17] = r;
+    hit = 1;
+  }
+  __syncthreads();
+  if (!hit && warp == 0) {  // speculation missed: finish from the true midpoint
+    const double t = warp_fold_gather_from(v, idx + m, n - m, red[16]);
+    if (lane == 0) red[17] = t;
+  }
+  __syncthreads();
+  const double out = red[17];
+  __syncthreads();
+  return out;
+}
+
+// Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
+// the leaf's order-0 segment / n (cta_fold_spec), then pred += lr*value over its rows.
+__global__ void __launch_bounds__(256) leaf_cta_kernel(const FamDesc* __restrict__ fam, int F,
+                                                       const FamState* __restrict__ st, NodeRec* __restrict__ nodes,
+                                                       int slots, const int32_t* __restrict__ ord_cur,
+                                                       const double* __restrict__ resid, double* __restrict__ pred,
+                                                       TreeRec* __restrict__ trees) {
+  __shared__ double red[18];
+  const int f = blockIdx.y, s = blockIdx.x;
+  if (f >= F) return;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeLeaf || nd.n == 0) return;
+  if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
+  const int n = nd.n;
+  const int32_t* L = ord_cur + fd.pos0 + nd.seg;
+  const double sum = nd.pad_ ? nd.total : cta_fold_spec(resid + fd.pos0, L, n, red);
+  const double value = fs_div(sum, static_cast<double>(n));
+  const double step = fs_mul(fd.lr, value);
+  // prediction update, 8 rows per thread in flight (index and prediction gathers issued before
+  // the stores: the compiler cannot prove the arrays do not alias)
+  for (int i0 = 0; i0 < n; i0 += 8 * static_cast<int>(blockDim.x)) {
+    int64_t pp[8];
+    double pv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * blockDim.x + threadIdx.x;
+      pp[k] = i < n ? fd.pos0 + L[i] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pv[k] = pp[k] >= 0 ? pred[pp[k]] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (pp[k] >= 0) pred[pp[k]] = fs_add(pv[k], step);
+  }
+  if (threadIdx.x == 0) {
+    nd.value = value;
+    TreeRec r;
+    r.kind = kNodeLeaf;
+    r.feature = -1;
+    r.threshold = 0.0;
+    r.value = value;
+    r.gain = 0.0;
+    r.rep = -1;
+    r.bin = 0;
+    trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = r;
+  }
+}
+
+__global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamState* __restrict__ st,
+                            NodeRec* __restrict__ nodes, int slots, const int32_t* __restrict__ ord_cur,
+                            const double* __restrict__ resid, double* __restrict__ pred, TreeRec* __restrict__ trees) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int f = static_cast<int>(w / slots), s = static_cast<int>(w % slots);
+  if (f >= F) return;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeLeaf || nd.n == 0) return;
+  // a slot is a leaf of this tree only if its parent split (or it is the root)
+  if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
+  const int n = nd.n;
+  const int32_t* L = ord_cur + fd.pos0 + nd.seg;
+  // the same fold as the node total when totals_kernel already produced it (costmodel.cpp:86)
+  const double sum = nd.pad_ ? nd.total : warp_fold_gather(resid + fd.pos0, L, n);
+  const double value = fs_div(sum, static_cast<double>(n));
+  const double step = fs_mul(fd.lr, value);
+  // prediction update, 8 rows per lane in flight (a plain loop serialises on L2 latency:
+  // the compiler cannot prove the index and prediction arrays do not alias)
+  for (int i0 = 0; i0 < n; i0 += 256) {
+    int64_t pp[8];
+    double pv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + 32 * k + lane;
+      pp[k] = i < n ? fd.pos0 + L[i] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pv[k] = pp[k] >= 0 ? pred[pp[k]] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (pp[k] >= 0) pred[pp[k]] = fs_add(pv[k], step);
+  }
+  if (lane == 0) {
+    nd.value = value;
+    TreeRec r;
+    r.kind = kNodeLeaf;
+    r.feature = -1;
+    r.threshold = 0.0;
+    r.value = value;
+    r.gain = 0.0;
+    r.rep = -1;
+    r.bin = 0;
+    trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = r;
+  }
+}
+
+// Commit the round's tree or stop (costmodel.cpp:212), then MSE over canonical rows (:215-220).
+// The MSE is a fixed-order tree reduction: deterministic, within 1e-15 relative of the
+// reference's sequential fold (it never feeds back into the model).
+// MSE per round (costmodel.cpp:215-220; a fixed-order reduction - it never feeds back):
+// blocks of kMseRows rows per family produce partials (block tree reduction), mse_final_kernel
+// adds them in block order; it also commits the tree or applies the early stop (:212).
+constexpr int kMseRows = 2048;
+constexpr int kExactSmallCtas = 64;  // CTAs of exact_small_kernel (items loop over them)
+__device__ __forceinline__ bool round_commits(const FamDesc& fd, const FamState& st, const NodeRec* nodes) {
+  if (!st.active) return false;
+  const NodeRec& root = nodes[fd.node0];
+  return !(root.state == kNodeLeaf && root.value == 0.0);
+}
+__global__ void mse_partial_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                   const NodeRec* __restrict__ nodes, const double* __restrict__ target_c,
+                                   const double* __restrict__ pred, double* __restrict__ part, int max_blocks) {
+  __shared__ double red[256];
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  const int r0 = blockIdx.x * kMseRows;
+  if (r0 >= fd.n || !round_commits(fd, st[f], nodes)) return;
+  const int r1 = min(fd.n, r0 + kMseRows);
+  double a = 0.0;
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double e = fs_sub(target_c[fd.pos0 + i], pred[fd.pos0 + i]);
+    a = fs_add(a, fs_mul(e, e));
+  }
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fs_add(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[static_cast<int64_t>(f) * max_blocks + blockIdx.x] = red[0];
+}
+__global__ void mse_final_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
+                                 const NodeRec* __restrict__ nodes, const double* __restrict__ part, int max_blocks,
+                                 double* __restrict__ mse, int max_trees) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= gridDim.x * blockDim.x) return;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  if (!round_commits(fd, st[f], nodes)) {
+    st[f].active = 0;  // single leaf of value exactly 0: the reference stops boosting
+    return;
+  }
+  double a = 0.0;
+  const int nb = (fd.n + kMseRows - 1) / kMseRows;
+  for (int b = 0; b < nb; ++b) a = fs_add(a, part[static_cast<int64_t>(f) * max_blocks + b]);
+  const int t = st[f].ntrees;
+  mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(a, static_cast<double>(fd.n));
+  st[f].ntrees = t + 1;
+  if (t + 1 >= fd.trees) st[f].active = 0;
+}
+
+}  // namespace
+}  // namespace fit
+}  // namespace fs
