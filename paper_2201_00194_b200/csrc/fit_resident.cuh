@@ -1038,11 +1038,6 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       const int nv = nd.n;
       const double sum = fold_spec(s_resid, s_ord0 + nd.seg, nv);  // warp-collective
       const double value = fs_div(sum, static_cast<double>(nv));
-      const double step = fs_mul(fd.lr, value);
-      for (int i = lane; i < nv; i += 32) {
-        const int p = s_ord0[nd.seg + i];
-        s_pred[p] = fs_add(s_pred[p], step);
-      }
       if (lane == 0) {
         nd.value = value;
         TreeRec r;
@@ -1058,13 +1053,18 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     }
     __syncthreads();
       RES_PHASE(10);
-    // ---- commit / early stop (costmodel.cpp:212) and MSE (:215-220) --------------------------
-    if (s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0) break;  // uniform (smem)
+    // ---- prediction update (costmodel.cpp:88-90: pred += lr * leaf value, every row through
+    // its final leaf slot, all threads) fused with the MSE (:215-220); commit or early stop
+    // (:212 - the update happens before the reference's stop test too)
+    const bool stop = s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0;  // uniform (smem)
     double a = 0.0;
     for (int p = tid; p < n; p += kResThreads) {
-      const double e = fs_sub(s_targ[p], s_pred[p]);
+      const double pr = fs_add(s_pred[p], fs_mul(fd.lr, s_nodes[s_node[p]].value));
+      s_pred[p] = pr;
+      const double e = fs_sub(s_targ[p], pr);
       a = fs_add(a, fs_mul(e, e));
     }
+    if (stop) break;
     for (int o = 16; o > 0; o >>= 1) a = fs_add(a, __shfl_down_sync(0xffffffffu, a, o));
     if (lane == 0) s_dred[warp] = a;
     __syncthreads();
