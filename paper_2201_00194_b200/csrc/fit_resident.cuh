@@ -315,18 +315,23 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   __syncthreads();
 
   int ntrees = 0;
+  bool have_resid = false;
   for (int round = 0; round < fd.trees; ++round) {
     // ---- residuals (costmodel.cpp:204-206), fixed point, per-round reset ----------------
-    unsigned long long mx = 0;
-    for (int p = tid; p < n; p += kResThreads) {
-      const double r = fs_sub(s_targ[p], s_pred[p]);
-      s_resid[p] = r;
-      mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(r))));
-      s_node[p] = 0;
-      s_ord0[p] = s_ordr ? s_ordr[p] : static_cast<uint16_t>(g_ordr[p]);
+    // (from round 1 on, the previous round's prediction/MSE pass already wrote the residuals,
+    // their max |r| per warp and the row resets)
+    if (!have_resid) {
+      unsigned long long mx = 0;
+      for (int p = tid; p < n; p += kResThreads) {
+        const double r = fs_sub(s_targ[p], s_pred[p]);
+        s_resid[p] = r;
+        mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(r))));
+        s_node[p] = 0;
+        s_ord0[p] = s_ordr ? s_ordr[p] : static_cast<uint16_t>(g_ordr[p]);
+      }
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) s_red[warp] = mx;
     }
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) s_red[warp] = mx;
     for (int s = tid; s < slots; s += kResThreads) {
       ResNode z;
       memset(&z, 0, sizeof z);
@@ -1058,13 +1063,21 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     // (:212 - the update happens before the reference's stop test too)
     const bool stop = s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0;  // uniform (smem)
     double a = 0.0;
+    unsigned long long mx = 0;
     for (int p = tid; p < n; p += kResThreads) {
       const double pr = fs_add(s_pred[p], fs_mul(fd.lr, s_nodes[s_node[p]].value));
       s_pred[p] = pr;
-      const double e = fs_sub(s_targ[p], pr);
+      const double e = fs_sub(s_targ[p], pr);  // = the next round's residual (costmodel.cpp:204-206)
       a = fs_add(a, fs_mul(e, e));
+      s_resid[p] = e;
+      mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(e))));
+      s_node[p] = 0;
+      s_ord0[p] = s_ordr ? s_ordr[p] : static_cast<uint16_t>(g_ordr[p]);
     }
     if (stop) break;
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) s_red[warp] = mx;
+    have_resid = true;
     for (int o = 16; o > 0; o >>= 1) a = fs_add(a, __shfl_down_sync(0xffffffffu, a, o));
     if (lane == 0) s_dred[warp] = a;
     __syncthreads();
