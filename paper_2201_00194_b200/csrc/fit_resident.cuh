@@ -408,6 +408,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
             for (int i = tid; i < cpad; i += kResThreads) s_limb[i] = 0;
             if (tid < 4) s_absl[4 * k + tid] = 0;
             __syncthreads();
+#ifdef FS_RES_HIST_SPLIT
+            RES_PHASE(1);  // A/B probe: zeroing billed to "plan"
+#endif
             const int q_end = min(nv, sub0 + kAtomSub);
             unsigned long long asum = 0;
             if (hact) {
@@ -449,6 +452,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               for (int t = 0; t < 4; ++t) atomicAdd(s_absl + 4 * k + t, static_cast<uint32_t>(asum >> (16 * t)) & 0xFFFFu);
             }
             __syncthreads();
+#ifdef FS_RES_HIST_SPLIT
+            RES_PHASE(2);  // accumulate
+#endif
             long long* hk = hs + static_cast<size_t>(k) * bins;
             int* ck = hc + static_cast<size_t>(k) * bins;
             for (int i = tid; i < bins; i += kResThreads) {
@@ -480,6 +486,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               if (sub0 == 0) c_hist_rows += nv;
             }
             __syncthreads();
+#ifdef FS_RES_HIST_SPLIT
+            RES_PHASE(3);  // limb fold billed to "derive"
+#endif
           }
         }
       }
@@ -600,6 +609,9 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
             }
           }
           __syncthreads();
+#ifdef FS_RES_SCREEN_SPLIT
+          RES_PHASE(pass == 0 ? 4 : 3);  // A/B probe: pass 1 billed to "derive"
+#endif
         }
       }
       RES_PHASE(4);
