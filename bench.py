@@ -147,7 +147,7 @@ def build_workload(cfg_name, seed):
         "families": fam_names,
         "pool_so": np.concatenate(pool_so), "pool_a": np.concatenate(pool_a), "pool_seg": np.array(pool_seg, np.int64),
         "tr_so": np.concatenate(tr_so), "tr_a": np.concatenate(tr_a), "tr_seg": np.array(tr_seg, np.int64),
-        "tr_y": np.log(np.concatenate(tr_lat)),
+        "tr_y": np.log(np.concatenate(tr_lat)), "tr_lat": np.concatenate(tr_lat),
     }
     return W
 

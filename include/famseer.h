@@ -175,6 +175,33 @@ int fs_fit_records_d(fs_device* dev, fs_forest* fo, const fs_spaces* sp, int32_t
                      const int64_t* seg_h, const int32_t* space_of_d, const int32_t* assign_d, int32_t pad_dim,
                      const double* target_d, const fs_gbt_params* params);
 
+/* ---- device-resident training store -----------------------------------
+ * CostModelState::training_set (costmodel.hpp:48-57) of F families kept on the device across
+ * retrains: train_cost_model's append (costmodel.cpp:224-233) sends only the new batch, and each
+ * family's canonical row order (:161-173) is maintained by merge-insert instead of a full re-sort
+ * per fit. A refit from the store is bit-identical to fs_fit on the family's rows in append order.
+ * Rows [seg[k], seg[k+1]) of an append go to family[k]; target = log(latency_ms) (:232), computed
+ * on the host like the reference. Empty batch or latency <= 0 -> FS_EINVAL (:225-231, nothing is
+ * appended); unknown family -> FS_ERANGE. */
+typedef struct fs_store fs_store;
+int fs_store_create(fs_device* dev, int32_t n_families, int32_t d, fs_store** out);
+int fs_store_destroy(fs_store* st);
+int fs_store_append(fs_store* st, int32_t n_segments, const int32_t* family, const int64_t* seg,
+                    const double* x, const double* latency_ms);
+/* the same from measurement records (candidate descriptors, featurized on the device at d) */
+int fs_store_append_records(fs_store* st, const fs_spaces* sp, int32_t n_segments,
+                            const int32_t* family, const int64_t* seg, const int32_t* space_of,
+                            const int32_t* assign, const double* latency_ms);
+int fs_store_rows(const fs_store* st, int32_t family, int64_t* rows);
+/* rows / targets in append order; canonical = family-relative row ids in canonical order when
+ * *canonical_valid (a bulk append leaves it to the next fit). Any pointer may be NULL. */
+int fs_store_read(const fs_store* st, int32_t family, double* x, double* target, int32_t* canonical,
+                  int32_t* canonical_valid);
+/* fit(model) (costmodel.cpp:152-222) of the listed store families on everything they hold;
+ * results replace forest family families[k] with params[k]. */
+int fs_store_fit(fs_store* st, fs_forest* fo, int32_t n_families, const int32_t* families,
+                 const fs_gbt_params* params);
+
 /* Fit diagnostics of the last fs_fit on this forest family: internal nodes resolved by the
  * histogram screen alone / by exact reference-order re-evaluation of the tie window. */
 int fs_forest_fit_stats(const fs_forest* fo, int32_t family, int64_t* screened,

@@ -23,7 +23,7 @@ import numpy as np
 from . import _capi
 from ._capi import FS_MAX_KNOBS, GbtParams
 
-__all__ = ["Device", "Spaces", "Forest", "Ensemble", "GbtParams", "FamseerError", "InvalidArgument",
+__all__ = ["Device", "Spaces", "Forest", "Store", "Ensemble", "GbtParams", "FamseerError", "InvalidArgument",
            "DomainError", "OutOfRange", "feature_dim", "FS_MAX_KNOBS"]
 
 
@@ -382,6 +382,82 @@ class Forest:
         a, b = C.c_int64(), C.c_int64()
         _check(_lib().fs_forest_fit_stats(self.h, family, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+
+class Store:
+    """fs_store: every family's training set kept on the device across retrains (SURVEY.md 8f
+    row 2; CostModelState::training_set, costmodel.hpp:48-57). append() is train_cost_model's
+    push_back (costmodel.cpp:224-233: target = log(latency)), fit() its refit (:152-222); the
+    canonical row order is maintained by merge-insert instead of re-sorted per fit."""
+
+    def __init__(self, dev: Device, n_families: int, d: int):
+        self.dev = dev
+        self.n = n_families
+        self.d = d
+        h = _capi._vp()
+        _check(_lib().fs_store_create(dev.h, n_families, d, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().fs_store_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _segs(family, seg, n):
+        fam = np.ascontiguousarray(np.atleast_1d(family), np.int32)
+        if seg is None:
+            seg = [0, n]
+        sg = np.ascontiguousarray(seg, np.int64)
+        if len(sg) != len(fam) + 1:
+            raise InvalidArgument("seg must have one more entry than family")
+        return fam, sg
+
+    def append(self, family, x, latency_ms, seg=None):
+        """Rows [seg[k], seg[k+1]) of x / latency_ms go to family[k]."""
+        xa = np.ascontiguousarray(x, np.float64).reshape(-1, self.d) if self.d else np.zeros((len(latency_ms), 0))
+        lat = np.ascontiguousarray(latency_ms, np.float64)
+        fam, sg = self._segs(family, seg, len(lat))
+        _check(_lib().fs_store_append(self.h, len(fam), _p(fam, _capi._i32p), _p(sg, _capi._i64p),
+                                      _p(xa, _capi._dp), _p(lat, _capi._dp)))
+
+    def append_records(self, spaces: "Spaces", family, space_of, assign, latency_ms, seg=None):
+        so = np.ascontiguousarray(space_of, np.int32)
+        a = np.ascontiguousarray(assign, np.int32)
+        if a.ndim != 2 or a.shape[1] != 16:
+            raise InvalidArgument("assign must be [n][16] value indices")
+        lat = np.ascontiguousarray(latency_ms, np.float64)
+        fam, sg = self._segs(family, seg, len(lat))
+        _check(_lib().fs_store_append_records(self.h, spaces.h, len(fam), _p(fam, _capi._i32p),
+                                              _p(sg, _capi._i64p), _p(so, _capi._i32p), _p(a, _capi._i32p),
+                                              _p(lat, _capi._dp)))
+
+    def rows(self, family: int) -> int:
+        r = C.c_int64()
+        _check(_lib().fs_store_rows(self.h, family, C.byref(r)))
+        return r.value
+
+    def read(self, family: int):
+        """(x, target, canonical order or None) of one family, rows in append order."""
+        n = self.rows(family)
+        x = np.zeros((n, self.d))
+        y = np.zeros(n)
+        c = np.zeros(n, np.int32)
+        ok = C.c_int32()
+        _check(_lib().fs_store_read(self.h, family, _p(x, _capi._dp), _p(y, _capi._dp), _p(c, _capi._i32p),
+                                    C.byref(ok)))
+        return x, y, (c if ok.value else None)
+
+    def fit(self, forest: "Forest", families=None, params=None):
+        fam = np.ascontiguousarray(range(self.n) if families is None else families, np.int32)
+        pa = _params_array(params, len(fam))
+        _check(_lib().fs_store_fit(self.h, forest.h, len(fam), _p(fam, _capi._i32p), pa))
 
 
 def _params_array(params, n):

@@ -49,6 +49,13 @@ SIGNATURES = [
                                  C.POINTER(GbtParams)]),
     ("fs_fit_records_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp,
                                    C.POINTER(GbtParams)]),
+    ("fs_store_create", C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    ("fs_store_destroy", C.c_int, [_vp]),
+    ("fs_store_append", C.c_int, [_vp, C.c_int32, _i32p, _i64p, _dp, _dp]),
+    ("fs_store_append_records", C.c_int, [_vp, _vp, C.c_int32, _i32p, _i64p, _i32p, _i32p, _dp]),
+    ("fs_store_rows", C.c_int, [_vp, C.c_int32, _i64p]),
+    ("fs_store_read", C.c_int, [_vp, C.c_int32, _dp, _dp, _i32p, _i32p]),
+    ("fs_store_fit", C.c_int, [_vp, _vp, C.c_int32, _i32p, C.POINTER(GbtParams)]),
     ("fs_score", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _i32p, C.c_int32, _dp, _i32p]),
     ("fs_score_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp]),
     ("fs_feature_dim", C.c_int, [C.c_int32]),

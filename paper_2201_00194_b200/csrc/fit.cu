@@ -122,8 +122,10 @@ struct ResidentPlan {
   bool atomic = false;  // limb-atomic histogram (default)
   int colh_max = 1;     // its lane-column height (col_height), max over families
   size_t phi_smem = 0;  // tie-class phi table bytes (largest per-feature bin count x 2); 0 = ordered scan
-  std::vector<int> bitonic_ok;  // per family: canonical order by one bitonic sort (else LSD passes)
+  std::vector<int> bitonic_ok;  // per family: 1 = canonical order by one bitonic sort, 2 = given (fs_store), 0 = LSD passes
   size_t bitonic_smem = 0;
+  std::vector<int> canon_io;    // per family: FitRows::io (empty: none)
+  int32_t* store_canon = nullptr;
   size_t atomic_smem = 0;
   bool col = false;
   std::vector<int32_t> col_off;  // [F][kColWarps + 1] entry offsets per feature group
@@ -142,7 +144,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   cudaStream_t s = dev->stream;
   const int sm = dev->sm_count;
   const size_t bitonic_smem = resident.bitonic_smem;
-  const int* bitonic_ok = bitonic_smem > 0 ? ar.upload(resident.bitonic_ok) : nullptr;
+  const bool have_io = !resident.canon_io.empty();
+  const int* bitonic_ok = bitonic_smem > 0 || have_io ? ar.upload(resident.bitonic_ok) : nullptr;
   if (bitonic_smem > 0)
     FS_CUDA(cudaFuncSetAttribute(canonical_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bitonic_smem)));
@@ -163,6 +166,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
     }
     canonical_kernel<<<F, kSortThreads, 0, s>>>(target_d, codes_all, d, fam_d, rep_orig_d, rep_nb_d, canon, tmp,
                                                 bitonic_ok);
+    if (have_io) {
+      const int* io_d = ar.upload(resident.canon_io);
+      canon_io_kernel<<<grid1(n_tot, 256, sm * 8), 256, 0, s>>>(fam_d, F, n_tot, io_d, resident.store_canon, canon);
+      dev->count_launch();
+    }
   }
   CodeT* codes_c = ar.alloc<CodeT>(static_cast<size_t>(n_tot) * Dp);
   double* target_c = ar.alloc<double>(n_tot);
@@ -402,10 +410,13 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
 
 // Fit every family segment; results replace fo->fams[f] (pre-order trees + compiled form).
 void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int d, const double* x_d,
-                  const double* target_d, const fs_gbt_params* params) {
+                  const double* target_d, const fs_gbt_params* params, const FitRows* rows) {
   cudaStream_t s = dev->stream;
   if (F < 1) return;
-  if (F > static_cast<int>(fo->fams.size())) fail(FS_ERANGE, "fit: more segments than forest families");
+  auto fam_id = [&](int f) { return rows && rows->fam_id ? rows->fam_id[f] : f; };
+  for (int f = 0; f < F; ++f)
+    if (fam_id(f) < 0 || fam_id(f) >= static_cast<int>(fo->fams.size()))
+      fail(FS_ERANGE, "fit: more segments than forest families");
   if (seg[0] != 0) fail(FS_EINVAL, "fit: seg[0] must be 0");
   int depth_max = 0, max_trees = 0, n_max = 0;
   for (int f = 0; f < F; ++f) {
@@ -435,7 +446,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   std::vector<FamDesc> fam(static_cast<size_t>(F));
   for (int f = 0; f < F; ++f) {
     std::memset(&fam[f], 0, sizeof(FamDesc));
-    fam[f].row0 = seg[f];
+    fam[f].row0 = rows && rows->row0 ? rows->row0[f] : seg[f];
     fam[f].pos0 = seg[f];
     fam[f].n = static_cast<int32_t>(seg[f + 1] - seg[f]);
     fam[f].trees = fam[f].n > 0 ? params[f].trees : 0;
@@ -448,7 +459,8 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   htick("fam uploaded");
 
   // ---- stage 1: distinct values / codes ---------------------------------------------------
-  uint16_t* codes_all = ar.alloc<uint16_t>(static_cast<size_t>(std::max<int64_t>(n_tot, 1)) * std::max(d, 1));
+  const int64_t span = rows && rows->row0 ? rows->span : n_tot;  // rows addressable in x
+  uint16_t* codes_all = ar.alloc<uint16_t>(static_cast<size_t>(std::max<int64_t>(span, 1)) * std::max(d, 1));
   double* vals_all = ar.alloc<double>(static_cast<size_t>(F) * std::max(d, 1) * kSmallBins);
   int32_t* nb_all = ar.alloc<int32_t>(static_cast<size_t>(F) * std::max(d, 1));
   uint64_t* hash_all = ar.alloc<uint64_t>(static_cast<size_t>(F) * std::max(d, 1));
@@ -482,6 +494,8 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     raise_deferred(br.run(dev));
   }
   for (int f = 0; f < F; ++f) fam[static_cast<size_t>(f)].negz = negz[static_cast<size_t>(f)];
+  if (rows && rows->negz_out)
+    for (int f = 0; f < F; ++f) rows->negz_out[f] = negz[static_cast<size_t>(f)];
   std::vector<LargeItem> large;
   int64_t vl = 0;
   for (int f = 0; f < F; ++f)
@@ -637,6 +651,18 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
       res.bitonic_smem = std::max(res.bitonic_smem, need);
     }
   }
+  // canonical order supplied by / returned to the caller's store (FitRows::io); a family holding
+  // a -0.0 always sorts (its ties are not bitwise-identical rows) and returns nothing
+  if (rows && rows->io && rows->canon) {
+    res.canon_io.assign(static_cast<size_t>(F), 0);
+    res.bitonic_ok.resize(static_cast<size_t>(F), 0);
+    res.store_canon = rows->canon;
+    for (int f = 0; f < F; ++f) {
+      if (fam[static_cast<size_t>(f)].n <= 0 || fam[static_cast<size_t>(f)].negz) continue;
+      res.canon_io[static_cast<size_t>(f)] = rows->io[f];
+      if (rows->io[f] == 1) res.bitonic_ok[static_cast<size_t>(f)] = 2;
+    }
+  }
   // Column-layout histogram plan (multi-kernel path): per feature group of 32 the largest bin
   // count; row-group copies while they fit the shared-memory budget.
   // Histogram shape for the multi-kernel path: FAMSEER_HIST = atomic (default) | col | rowmajor.
@@ -746,7 +772,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   if (dev_compile) {
     std::vector<ExportJob> jobs(static_cast<size_t>(F));
     for (int f = 0; f < F; ++f) {
-      FamilyModel& m = fo->fams[static_cast<size_t>(f)];
+      FamilyModel& m = fo->fams[static_cast<size_t>(fam_id(f))];
       const FamDesc& fd = fam[static_cast<size_t>(f)];
       const int T = std::max(fd.n > 0 ? fd.trees : 0, 0), D = std::max(fd.depth, 0);
       const int S = (1 << (D + 1)) - 1, nint = (1 << D) - 1, nleaf = 1 << D;
@@ -833,7 +859,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
   htick("results read");
   UploadBatch batch;
   for (int f = 0; f < F; ++f) {
-    FamilyModel& m = fo->fams[static_cast<size_t>(f)];
+    FamilyModel& m = fo->fams[static_cast<size_t>(fam_id(f))];
     const FamDesc& fd = fam[static_cast<size_t>(f)];
     m.lr = fd.lr;
     m.base = fd.n > 0 ? base_h[static_cast<size_t>(f)] : 0.0;

@@ -102,5 +102,22 @@ struct WinRec {
   int32_t maxlc;    // largest left count among the feature's window candidates
 };
 
+// Where a fit's rows live when they do not come packed by seg (fs_store):
+// segment f's rows are x/target rows [row0[f], row0[f] + n[f]) (seg still gives the counts),
+// fam_id[f] is the forest family it refits, and canon (indexed like x rows) holds each family's
+// canonical row order (costmodel.cpp:161-173) as family-relative row ids: io[f] = 1 takes it
+// from there (the sort is skipped), 2 writes the fit's order back, 0 neither.
+struct FitRows {
+  const int64_t* row0 = nullptr;
+  const int32_t* fam_id = nullptr;
+  int64_t span = 0;  // rows addressable in x
+  int32_t* canon = nullptr;
+  const int* io = nullptr;
+  int* negz_out = nullptr;  // per segment: the family holds a -0.0 (its canonical order is not taken)
+};
+
+void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int d, const double* x_d,
+                  const double* target_d, const fs_gbt_params* params, const FitRows* rows = nullptr);
+
 }  // namespace fit
 }  // namespace fs

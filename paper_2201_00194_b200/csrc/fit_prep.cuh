@@ -482,6 +482,22 @@ __global__ void __launch_bounds__(kSortThreads) canonical_kernel(const double* _
     for (int i = threadIdx.x; i < n; i += blockDim.x) canon[fd.pos0 + i] = A[i];
 }
 
+// prep 3b': canonical order exchanged with the caller's training store (FitRows::io): 1 = the
+// store's maintained order is the family's canonical order (its sort was skipped), 2 = record
+// the order just computed in the store.
+__global__ void canon_io_kernel(const FamDesc* __restrict__ fam, int F, int64_t n_tot, const int* __restrict__ io,
+                                int32_t* __restrict__ store_canon, int32_t* __restrict__ canon) {
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n_tot;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int f = family_of_pos(fam, F, p);
+    const int m = io[f];
+    if (m == 0) continue;
+    const int64_t r = fam[f].row0 + (p - fam[f].pos0);
+    if (m == 1) canon[p] = store_canon[r];
+    else store_canon[r] = canon[p];
+  }
+}
+
 // prep 3c: rows into canonical order (codes of reps only, targets) + row->family map
 template <typename CodeT>
 __global__ void gather_canonical_kernel(const double* __restrict__ target, const uint16_t* __restrict__ codes_all,
@@ -579,7 +595,7 @@ __global__ void __launch_bounds__(kSortThreads) canonical_bitonic_kernel(
     const int* __restrict__ eligible, int32_t* __restrict__ canon) {
   extern __shared__ __align__(16) uint32_t ks[];  // [P][W] keys, then [P] row ids
   const int f = blockIdx.x;
-  if (!eligible[f]) return;
+  if (eligible[f] != 1) return;  // 0: LSD passes, 2: order given by the caller (fs_store)
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep;
   int wide = 0;
