@@ -446,6 +446,12 @@ def run_native(args, rank, world, local_rank):
                "train_rows_per_s": N_job * args.steps / (e_total / 1e3), "ms_per_step": e_total / args.steps,
                "api": "fs_score + fs_fit_records + fs_forest_export (host pointers)"}
 
+    # ---- incremental retrain (fs_store): the tuning loop's real pattern ----
+    incremental = None
+    if not args.no_e2e and F:
+        with torch.cuda.stream(stream):
+            incremental = measure_incremental(dev, spaces, W, params, timed, args.steps)
+
     # ---- roofline of the dominant kernel (from the per-kernel replica step) ----
     peak, peak_kind = measured_peak_hbm()
     cands = []
@@ -511,6 +517,7 @@ def run_native(args, rank, world, local_rank):
         "clocks": clock_info,
         "roofline": roofline,
         "e2e": e2e,
+        "incremental": incremental,
     }
     if rank == 0 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(W, forest, x_tr.cpu().numpy(), min_seconds=args.cpu_seconds)
@@ -518,6 +525,76 @@ def run_native(args, rank, world, local_rank):
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def measure_incremental(dev, spaces, W, params, timed, steps, g=64, warm=2):
+    """Retrain as the tuning loop does it (scheduler.cpp:228-235, train_cost_model
+    costmodel.cpp:224-235): every step each family receives g new measurement records and is
+    refit on everything it holds. Two ways through the public API, both timed with CUDA events
+    including the host->device copies: fs_store (the host sends the g new records; the canonical
+    order is merged, the refit skips the sort) and fs_fit_records on the family's full record set
+    each step (the host resends every record; the fit re-sorts). Families start at their bench
+    size minus the held-back batches."""
+    import paper_2201_00194_b200 as fs
+
+    seg = [int(v) for v in W["tr_seg"]]
+    F = len(seg) - 1
+    gf = [min(g, (seg[f + 1] - seg[f]) // (warm + steps + 2)) for f in range(F)]
+    live = [f for f in range(F) if gf[f] > 0]
+    if not live:
+        return None
+    so, asg, lat = W["tr_so"], W["tr_a"], W["tr_lat"]
+    # targets exactly as the store computes them (std::log on the host, costmodel.cpp:232)
+    tmp = fs.Store(dev, 1, 0)
+    tmp.append([0], np.zeros((len(lat), 0)), lat)
+    y = tmp.read(0)[1]
+    tmp.close()
+    start = {f: seg[f + 1] - (warm + steps) * gf[f] for f in live}
+    store = fs.Store(dev, F, PAD)
+    fo_s, fo_f = fs.Forest(dev, F), fs.Forest(dev, F)
+    fam0 = live
+    idx0 = np.concatenate([np.arange(seg[f], start[f]) for f in fam0])
+    sg0 = np.cumsum([0] + [start[f] - seg[f] for f in fam0])
+    store.append_records(spaces, fam0, so[idx0], asg[idx0], lat[idx0], seg=sg0)
+    store.fit(fo_s, families=live, params=params)
+    dev.check()
+    step_no = [0]
+
+    def batch(k):
+        idx = np.concatenate([np.arange(start[f] + k * gf[f], start[f] + (k + 1) * gf[f]) for f in live])
+        sg = np.cumsum([0] + [gf[f] for f in live])
+        return idx, sg
+
+    def store_step():
+        idx, sg = batch(step_no[0])
+        store.append_records(spaces, live, so[idx], asg[idx], lat[idx], seg=sg)
+        store.fit(fo_s, families=live, params=params)
+        step_no[0] += 1
+
+    full_no = [0]
+
+    def full_step():
+        k = full_no[0] + 1
+        idx = np.concatenate([np.arange(seg[f], start[f] + k * gf[f]) for f in live])
+        sg = np.cumsum([0] + [start[f] + k * gf[f] - seg[f] for f in live])
+        fo_f.fit_records(spaces, so[idx], asg[idx], PAD, y[idx], seg=list(sg), params=params)
+        full_no[0] += 1
+
+    for _ in range(warm):
+        store_step()
+        full_step()
+    t_store = timed(store_step, steps)
+    t_full = timed(full_step, steps)
+    # the two paths hold the same rows at the end: identical models
+    same = all(np.array_equal(fo_s.export(f).value, fo_f.export(live.index(f)).value) for f in live)
+    store.close()
+    return {"g_per_family": gf, "families_refit": live, "steps": steps,
+            "rows_start": {f: start[f] - seg[f] for f in live},
+            "store_ms_per_step": statistics.median(t_store), "full_refit_ms_per_step": statistics.median(t_full),
+            "speedup": statistics.median(t_full) / statistics.median(t_store),
+            "h2d_bytes_per_step_store": int(sum(gf[f] for f in live) * (4 + 64 + 8)),
+            "identical_models": bool(same),
+            "api": "fs_store_append_records + fs_store_fit vs fs_fit_records on the whole set"}
 
 
 # ------------------------------------------------------------------------------------------

@@ -37,6 +37,9 @@ struct fs_store {
   double* x = nullptr;       // [cap_total][d] rows, append order within each region
   double* y = nullptr;       // [cap_total] targets (log latency)
   int32_t* canon = nullptr;  // [cap_total] family-relative row ids in canonical order
+  void* stage_h = nullptr;   // pinned staging of one append (grow-only), reusable once up_evt passed
+  size_t stage_cap = 0;
+  cudaEvent_t up_evt = nullptr;
 };
 
 namespace fs {
@@ -68,37 +71,70 @@ __device__ __forceinline__ int row_cmp(const double* __restrict__ x, const doubl
   return 0;
 }
 
-// rank of every new row among the batch (ties by arrival): A[rank] = family-relative row id
-__global__ void batch_rank_kernel(const MergeJob* __restrict__ jobs, const double* __restrict__ x,
-                                  const double* __restrict__ y, int d, int32_t* __restrict__ A) {
+// Every new row of a job (one warp each): its rank among the batch (ties by arrival; lanes over
+// the other batch rows) and its insertion point in the stored order (first stored row not below
+// it) by a 32-ary search - each lane compares one pivot, the ballot count narrows the range ~33x
+// per step, so a few dependent row compares replace log2(n) of them. In rank order: A =
+// family-relative row id, L = insertion point (non-decreasing: lower_bound is monotone in the key).
+__global__ void rank_insert_kernel(const MergeJob* __restrict__ jobs, const double* __restrict__ x,
+                                   const double* __restrict__ y, int d, const int32_t* __restrict__ canon,
+                                   int32_t* __restrict__ A, int32_t* __restrict__ L) {
   const MergeJob jb = jobs[blockIdx.y];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= jb.g) return;
   const int64_t ri = jb.row0 + jb.n_old + i;
   int rank = 0;
-  for (int j = 0; j < jb.g; ++j) {
+  for (int j = lane; j < jb.g; j += 32) {
     if (j == i) continue;
     const int c = row_cmp(x, y, d, jb.row0 + jb.n_old + j, ri);
     rank += c < 0 || (c == 0 && j < i);
   }
-  A[jb.a0 + rank] = jb.n_old + i;
+  rank = __reduce_add_sync(0xffffffffu, rank);
+  int lo = 0, hi = jb.n_old;
+  while (hi > lo) {
+    const int m = hi - lo;
+    if (m <= 32) {
+      const bool lt = lane < m && row_cmp(x, y, d, jb.row0 + canon[jb.row0 + lo + lane], ri) < 0;
+      lo += __popc(__ballot_sync(0xffffffffu, lt));
+      break;
+    }
+    const int q = lo + static_cast<int>((static_cast<int64_t>(lane) + 1) * m / 33);
+    const bool lt = row_cmp(x, y, d, jb.row0 + canon[jb.row0 + q], ri) < 0;
+    const int c = __popc(__ballot_sync(0xffffffffu, lt));  // the pivots below the key form a prefix
+    const int qlo = __shfl_sync(0xffffffffu, q, c > 0 ? c - 1 : 0);
+    const int qhi = __shfl_sync(0xffffffffu, q, c < 32 ? c : 31);
+    if (c > 0) lo = qlo + 1;
+    if (c < 32) hi = qhi;
+  }
+  if (lane == 0) {
+    A[jb.a0 + rank] = jb.n_old + i;
+    L[jb.a0 + rank] = lo;
+  }
 }
 
-// insertion point of every (sorted) new row in the stored order: first stored row not below it
-__global__ void insert_point_kernel(const MergeJob* __restrict__ jobs, const double* __restrict__ x,
-                                    const double* __restrict__ y, int d, const int32_t* __restrict__ canon,
-                                    const int32_t* __restrict__ A, int32_t* __restrict__ L) {
-  const MergeJob jb = jobs[blockIdx.y];
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= jb.g) return;
-  const int64_t key = jb.row0 + A[jb.a0 + r];
-  int lo = 0, hi = jb.n_old;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (row_cmp(x, y, d, jb.row0 + canon[jb.row0 + mid], key) < 0) lo = mid + 1;
-    else hi = mid;
+struct SegDst {
+  int64_t src0;  // first row of the segment in the staged batch
+  int64_t dst;   // its first store row
+};
+
+// staged batch rows (features, targets) into their families' store regions
+__global__ void place_kernel(const SegDst* __restrict__ segs, int nseg, int64_t n, int d, const double* __restrict__ xs,
+                             const double* __restrict__ ys, double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n * (d + 1);
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / (d + 1);
+    const int j = static_cast<int>(e - i * (d + 1));
+    int lo = 0, hi = nseg - 1;  // last segment with src0 <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (segs[mid].src0 <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t r = segs[lo].dst + (i - segs[lo].src0);
+    if (j < d) x[r * d + j] = xs[i * d + j];
+    else y[r] = ys[i];
   }
-  L[jb.a0 + r] = lo;
 }
 
 // merged order: stored row k moves up by the new rows inserted at or before it; new row r lands
@@ -180,10 +216,14 @@ void reserve(fs_store* st, const std::vector<int64_t>& need) {
   st->cap_total = tot;
 }
 
-// Rows [seg[k], seg[k+1]) of the call belong to family fam[k]. `place` writes segment k's rows
-// and targets at the given store rows; then every appended family's canonical order is merged.
-template <class Place>
-void append(fs_store* st, int32_t nseg, const int32_t* fam, const int64_t* seg, const double* latency, Place place) {
+inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
+
+// Rows [seg[k], seg[k+1]) of the call belong to family fam[k]. One pinned staging buffer carries
+// the batch (targets, segment table, merge jobs and either the feature rows or the record
+// descriptors) in one copy; `records` featurizes the descriptors on the device. Then one kernel
+// places the rows and three kernels merge every appended family's canonical order.
+void append(fs_store* st, int32_t nseg, const int32_t* fam, const int64_t* seg, const double* latency,
+            const double* x_h, const fs_spaces* sp, const int32_t* so_h, const int32_t* a_h) {
   fs_device* dev = st->dev;
   cudaStream_t s = dev->stream;
   if (nseg < 1 || !fam || !seg || !latency) fail(FS_EINVAL, "fs_store_append: bad arguments");
@@ -196,26 +236,22 @@ void append(fs_store* st, int32_t nseg, const int32_t* fam, const int64_t* seg, 
     add[static_cast<size_t>(fam[k])] += g;
   }
   const int64_t n_in = seg[nseg];
-  std::vector<double> target(static_cast<size_t>(n_in));
-  for (int64_t i = 0; i < n_in; ++i) {
+  for (int64_t i = 0; i < n_in; ++i)
     if (!(latency[i] > 0.0)) fail(FS_EINVAL, "train_cost_model: non-positive latency");  // :229-231
-    target[static_cast<size_t>(i)] = std::log(latency[i]);                                // :232
-  }
   std::vector<int64_t> need(st->n);
   for (int f = 0; f < st->F; ++f) {
     need[static_cast<size_t>(f)] += add[static_cast<size_t>(f)];
     if (need[static_cast<size_t>(f)] > (1 << 30)) fail(FS_EINVAL, "fs_store_append: family larger than 2^30 rows");
   }
   reserve(st, need);
-  std::vector<int64_t> n_old(st->n), at(st->n);
+  const int d = st->d;
+  // segment destinations, merge jobs
+  std::vector<SegDst> segs(static_cast<size_t>(nseg));
+  std::vector<int64_t> at(st->n);
   for (int k = 0; k < nseg; ++k) {
     const int f = fam[k];
-    const int64_t g = seg[k + 1] - seg[k];
-    const int64_t r = st->row0[static_cast<size_t>(f)] + at[static_cast<size_t>(f)];
-    place(k, r);
-    FS_CUDA(cudaMemcpyAsync(st->y + r, target.data() + seg[k], static_cast<size_t>(g) * sizeof(double),
-                            cudaMemcpyHostToDevice, s));
-    at[static_cast<size_t>(f)] += g;
+    segs[static_cast<size_t>(k)] = {seg[k], st->row0[static_cast<size_t>(f)] + at[static_cast<size_t>(f)]};
+    at[static_cast<size_t>(f)] += seg[k + 1] - seg[k];
   }
   std::vector<MergeJob> jobs;
   int64_t a_tot = 0, b_tot = 0;
@@ -223,6 +259,7 @@ void append(fs_store* st, int32_t nseg, const int32_t* fam, const int64_t* seg, 
   for (int f = 0; f < st->F; ++f) {
     const int64_t g = add[static_cast<size_t>(f)];
     if (g == 0) continue;
+    const int64_t n_old = st->n[static_cast<size_t>(f)];
     st->n[static_cast<size_t>(f)] += g;
     if (!st->sorted[static_cast<size_t>(f)]) continue;
     if (g > kMergeMax) {  // a bulk load: the next fit sorts and records the order
@@ -231,7 +268,7 @@ void append(fs_store* st, int32_t nseg, const int32_t* fam, const int64_t* seg, 
     }
     MergeJob jb;
     jb.row0 = st->row0[static_cast<size_t>(f)];
-    jb.n_old = static_cast<int32_t>(n_old[static_cast<size_t>(f)]);
+    jb.n_old = static_cast<int32_t>(n_old);
     jb.g = static_cast<int32_t>(g);
     jb.a0 = a_tot;
     jb.b0 = b_tot;
@@ -241,25 +278,67 @@ void append(fs_store* st, int32_t nseg, const int32_t* fam, const int64_t* seg, 
     tmax = std::max(tmax, jb.n_old + jb.g);
     jobs.push_back(jb);
   }
-  if (jobs.empty()) return;
-  MergeJob* jobs_d = dev_alloc<MergeJob>(dev, jobs.size());
-  int32_t* A = dev_alloc<int32_t>(dev, static_cast<size_t>(a_tot));
-  int32_t* L = dev_alloc<int32_t>(dev, static_cast<size_t>(a_tot));
-  int32_t* B = dev_alloc<int32_t>(dev, static_cast<size_t>(b_tot));
-  FS_CUDA(cudaMemcpyAsync(jobs_d, jobs.data(), jobs.size() * sizeof(MergeJob), cudaMemcpyHostToDevice, s));
-  const unsigned J = static_cast<unsigned>(jobs.size());
-  const unsigned gb = static_cast<unsigned>((gmax + 127) / 128);
-  batch_rank_kernel<<<dim3(gb, J), 128, 0, s>>>(jobs_d, st->x, st->y, st->d, A);
-  insert_point_kernel<<<dim3(gb, J), 128, 0, s>>>(jobs_d, st->x, st->y, st->d, st->canon, A, L);
-  const unsigned tb = static_cast<unsigned>(std::min(64, (tmax + 255) / 256));
-  merge_kernel<<<dim3(tb, J), 256, 0, s>>>(jobs_d, st->canon, A, L, B);
-  merge_store_kernel<<<dim3(tb, J), 256, 0, s>>>(jobs_d, B, st->canon);
-  dev->count_launch(4);
+  // staging layout (16-byte aligned sections), mirrored on the device
+  const bool rec = sp != nullptr;
+  const size_t o_y = 0, o_seg = al16(o_y + n_in * sizeof(double));
+  const size_t o_job = al16(o_seg + segs.size() * sizeof(SegDst));
+  const size_t o_in = al16(o_job + jobs.size() * sizeof(MergeJob));
+  const size_t in_bytes = rec ? static_cast<size_t>(n_in) * (1 + FS_MAX_KNOBS) * sizeof(int32_t)
+                              : static_cast<size_t>(n_in) * d * sizeof(double);
+  const size_t staged = al16(o_in + in_bytes);
+  if (st->up_evt) FS_CUDA(cudaEventSynchronize(st->up_evt));
+  if (staged > st->stage_cap) {
+    if (st->stage_h) FS_CUDA(cudaFreeHost(st->stage_h));
+    st->stage_h = nullptr;
+    st->stage_cap = std::max<size_t>(staged + staged / 2, 1 << 16);
+    FS_CUDA(cudaHostAlloc(&st->stage_h, st->stage_cap, cudaHostAllocDefault));
+  }
+  auto* h = static_cast<unsigned char*>(st->stage_h);
+  auto* yh = reinterpret_cast<double*>(h + o_y);
+  for (int64_t i = 0; i < n_in; ++i) yh[i] = std::log(latency[i]);  // costmodel.cpp:232 (std::log, host)
+  std::memcpy(h + o_seg, segs.data(), segs.size() * sizeof(SegDst));
+  if (!jobs.empty()) std::memcpy(h + o_job, jobs.data(), jobs.size() * sizeof(MergeJob));
+  if (rec) {
+    std::memcpy(h + o_in, so_h, static_cast<size_t>(n_in) * sizeof(int32_t));
+    std::memcpy(h + o_in + static_cast<size_t>(n_in) * sizeof(int32_t), a_h,
+                static_cast<size_t>(n_in) * FS_MAX_KNOBS * sizeof(int32_t));
+  } else if (in_bytes) {
+    std::memcpy(h + o_in, x_h, in_bytes);
+  }
+  const size_t o_x = al16(staged);  // featurized rows (records form)
+  const size_t o_A = al16(o_x + (rec ? static_cast<size_t>(n_in) * d * sizeof(double) : 0));
+  const size_t o_L = al16(o_A + a_tot * sizeof(int32_t));
+  const size_t o_B = al16(o_L + a_tot * sizeof(int32_t));
+  const size_t dev_bytes = al16(o_B + b_tot * sizeof(int32_t));
+  unsigned char* D = dev_alloc<unsigned char>(dev, dev_bytes);
+  FS_CUDA(cudaMemcpyAsync(D, h, staged, cudaMemcpyHostToDevice, s));
+  if (!st->up_evt) FS_CUDA(cudaEventCreateWithFlags(&st->up_evt, cudaEventDisableTiming));
+  FS_CUDA(cudaEventRecord(st->up_evt, s));
+  const double* xs = reinterpret_cast<const double*>(D + (rec ? o_x : o_in));
+  if (rec) {
+    const auto* so_d = reinterpret_cast<const int32_t*>(D + o_in);
+    launch_featurize(dev, sp, n_in, so_d, so_d + n_in, d, reinterpret_cast<double*>(D + o_x));
+  }
+  const int64_t work = n_in * (d + 1);
+  place_kernel<<<static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, dev->sm_count * 8))),
+                 256, 0, s>>>(reinterpret_cast<const SegDst*>(D + o_seg), nseg, n_in, d, xs,
+                              reinterpret_cast<const double*>(D + o_y), st->x, st->y);
+  dev->count_launch();
+  if (!jobs.empty()) {
+    const auto* jobs_d = reinterpret_cast<const MergeJob*>(D + o_job);
+    auto* A = reinterpret_cast<int32_t*>(D + o_A);
+    auto* L = reinterpret_cast<int32_t*>(D + o_L);
+    auto* B = reinterpret_cast<int32_t*>(D + o_B);
+    const unsigned J = static_cast<unsigned>(jobs.size());
+    rank_insert_kernel<<<dim3(static_cast<unsigned>((gmax + 7) / 8), J), 256, 0, s>>>(jobs_d, st->x, st->y, d,
+                                                                                      st->canon, A, L);
+    const unsigned tb = static_cast<unsigned>(std::min(64, (tmax + 255) / 256));
+    merge_kernel<<<dim3(tb, J), 256, 0, s>>>(jobs_d, st->canon, A, L, B);
+    merge_store_kernel<<<dim3(tb, J), 256, 0, s>>>(jobs_d, B, st->canon);
+    dev->count_launch(3);
+  }
   FS_CUDA(cudaGetLastError());
-  FS_CUDA(cudaFreeAsync(jobs_d, s));
-  FS_CUDA(cudaFreeAsync(A, s));
-  FS_CUDA(cudaFreeAsync(L, s));
-  FS_CUDA(cudaFreeAsync(B, s));
+  FS_CUDA(cudaFreeAsync(D, s));
 }
 
 }  // namespace
@@ -292,6 +371,11 @@ int fs_store_destroy(fs_store* st) {
     if (st->x) FS_CUDA(cudaFreeAsync(st->x, s));
     if (st->y) FS_CUDA(cudaFreeAsync(st->y, s));
     if (st->canon) FS_CUDA(cudaFreeAsync(st->canon, s));
+    if (st->up_evt) {
+      FS_CUDA(cudaEventSynchronize(st->up_evt));
+      FS_CUDA(cudaEventDestroy(st->up_evt));
+    }
+    if (st->stage_h) FS_CUDA(cudaFreeHost(st->stage_h));
     delete st;
   });
 }
@@ -301,12 +385,7 @@ int fs_store_append(fs_store* st, int32_t n_segments, const int32_t* family, con
   return fs::guard([&] {
     if (!st || (!x && st->d > 0)) fs::fail(FS_EINVAL, "fs_store_append: bad arguments");
     st->dev->activate();
-    fs::store::append(st, n_segments, family, seg, latency_ms, [&](int k, int64_t r) {
-      const int64_t g = seg[k + 1] - seg[k];
-      if (st->d > 0)
-        FS_CUDA(cudaMemcpyAsync(st->x + r * st->d, x + seg[k] * st->d, static_cast<size_t>(g) * st->d * sizeof(double),
-                                cudaMemcpyHostToDevice, st->dev->stream));
-    });
+    fs::store::append(st, n_segments, family, seg, latency_ms, x, nullptr, nullptr, nullptr);
   });
 }
 
@@ -324,18 +403,7 @@ int fs_store_append_records(fs_store* st, const fs_spaces* sp, int32_t n_segment
       if (st->d < fs_feature_dim(sp->k_h[static_cast<size_t>(s)]))
         fs::fail(FS_EINVAL, "fs_store_append_records: pad_dim too small");
     }
-    cudaStream_t s = st->dev->stream;
-    int32_t* so_d = fs::store::dev_alloc<int32_t>(st->dev, static_cast<size_t>(n));
-    int32_t* a_d = fs::store::dev_alloc<int32_t>(st->dev, static_cast<size_t>(n) * FS_MAX_KNOBS);
-    FS_CUDA(cudaMemcpyAsync(so_d, space_of, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    FS_CUDA(cudaMemcpyAsync(a_d, assign, static_cast<size_t>(n) * FS_MAX_KNOBS * sizeof(int32_t),
-                            cudaMemcpyHostToDevice, s));
-    fs::store::append(st, n_segments, family, seg, latency_ms, [&](int k, int64_t r) {
-      const int64_t g = seg[k + 1] - seg[k];
-      fs::launch_featurize(st->dev, sp, g, so_d + seg[k], a_d + seg[k] * FS_MAX_KNOBS, st->d, st->x + r * st->d);
-    });
-    FS_CUDA(cudaFreeAsync(so_d, s));
-    FS_CUDA(cudaFreeAsync(a_d, s));
+    fs::store::append(st, n_segments, family, seg, latency_ms, nullptr, sp, space_of, assign);
   });
 }
 
