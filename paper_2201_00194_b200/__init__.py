@@ -126,8 +126,8 @@ class Device:
 
     def counters(self, reset: bool = True) -> dict[str, int]:
         """Device work counters: histogram algorithmic bytes/rows, reference-order folds/nodes."""
-        out = np.zeros(20, np.int64)
-        _check(_lib().fs_device_counters(self.h, _p(out, _capi._i64p), 20, int(reset)))
+        out = np.zeros(24, np.int64)
+        _check(_lib().fs_device_counters(self.h, _p(out, _capi._i64p), 24, int(reset)))
         d = dict(zip(("hist_bytes", "hist_rows", "exact_chains", "exact_nodes"), (int(v) for v in out[:4])))
         names = ("residual", "plan", "hist", "derive", "screen", "tie_class", "decide", "exact_fold", "split",
                  "partition", "leaves", "mse")
@@ -136,6 +136,8 @@ class Device:
         if out[16:20].any():
             d["exact_reasons"] = {k: int(v) for k, v in zip(("multi_candidate_feature", "different_partitions",
                                                                "orders_differ", "uncertain_sign"), out[16:20])}
+        if out[20:24].any():
+            d["probe"] = [int(v) for v in out[20:24]]
         return d
 
     # -- per-kernel CUDA-event timing ------------------------------------------------------------

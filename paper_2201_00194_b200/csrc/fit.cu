@@ -118,6 +118,7 @@ struct ResidentPlan {
   bool pred_smem = false;
   bool pre_smem = false;
   int spec_bufs = 0;  // warps with a speculative exact-fold member buffer
+  int cluster = 1;    // CTAs per family (thread-block cluster sharing the histogram work)
   // column-layout histogram plan for the multi-kernel path (hist_build_col_kernel)
   bool atomic = false;  // limb-atomic histogram (default)
   int colh_max = 1;     // its lane-column height (col_height), max over families
@@ -199,10 +200,27 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                  static_cast<int>(resident.smem)));
     {
       ProfScope prof(dev, "fit_resident");
-      fit_resident_kernel<<<static_cast<unsigned>(resident.families.size()), kResThreads, resident.smem, s>>>(
-          fam_d, st_d, list_d, Dp, reinterpret_cast<const uint8_t*>(codes_c), target_c, base_d, ord, ord_root,
-          rep_orig_d, rep_nb_d, rep_boff_d, vals_d, cle, canon, x_d, d, trees_d, mse_d, max_trees, slots, dev->ctr_d,
-          resident.pred_smem ? 1 : 0, pred, resident.pre_smem ? 1 : 0, resident.spec_bufs);
+      const int cl = resident.cluster;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(resident.families.size() * cl));
+      cfg.blockDim = dim3(kResThreads);
+      cfg.dynamicSmemBytes = resident.smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = static_cast<unsigned>(cl);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      FS_CUDA(cudaLaunchKernelEx(&cfg, fit_resident_kernel, static_cast<const FamDesc*>(fam_d), st_d,
+                                 static_cast<const int*>(list_d), Dp, reinterpret_cast<const uint8_t*>(codes_c),
+                                 static_cast<const double*>(target_c), static_cast<const double*>(base_d),
+                                 static_cast<const int32_t*>(ord), static_cast<const int32_t*>(ord_root),
+                                 rep_orig_d, rep_nb_d, rep_boff_d, static_cast<const double*>(vals_d),
+                                 static_cast<const int32_t*>(cle), static_cast<const int32_t*>(canon), x_d, d, trees_d,
+                                 mse_d, max_trees, slots, dev->ctr_d, resident.pred_smem ? 1 : 0, pred,
+                                 resident.pre_smem ? 1 : 0, resident.spec_bufs));
     }
     dev->count_launch();
     FS_CUDA(cudaGetLastError());
@@ -629,6 +647,31 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
           break;
         }
       }
+    }
+    // FAMSEER_RES_CLUSTER = CTAs per family (1, 2 or 4): the histogram's features are dealt over a
+    // thread-block cluster (needs the running predictions in shared memory and <= 32 features
+    // per CTA)
+    if (res.enabled) {
+      const char* ce = std::getenv("FAMSEER_RES_CLUSTER");
+      // default: the largest of 4 / 2 whose clusters all fit the SMs at once, for families large
+      // enough that the histogram outweighs the per-level cluster exchange (C1's 512 rows: slower)
+      int cl = 1;
+      int nbig = 0;
+      for (int f : res.families) nbig = std::max(nbig, static_cast<int>(fam[static_cast<size_t>(f)].n));
+      if (ce) {
+        cl = std::atoi(ce);
+      } else if (nbig >= kResClusterMinRows) {
+        const int nf = static_cast<int>(res.families.size());
+        for (int c : {kResClusterMax, 2})
+          if (c * nf <= dev->sm_count) {
+            cl = c;
+            break;
+          }
+      }
+      if (cl != 1 && cl != 2 && cl != 4) fail(FS_EINVAL, "FAMSEER_RES_CLUSTER must be 1, 2 or 4");
+      bool ok = res.pred_smem;
+      for (int f : res.families) ok = ok && ceil_div(fam[static_cast<size_t>(f)].nrep, cl) <= 32;
+      res.cluster = ok ? cl : 1;
     }
     if (mode == "resident" && !res.enabled && !res.families.empty())
       fail(FS_EINVAL, "fit: resident path requested but the families do not fit one CTA");

@@ -13,6 +13,8 @@
 #ifndef FS_RES_THREADS
 #define FS_RES_THREADS 512
 #endif
+#include <cooperative_groups.h>
+
 namespace fs {
 namespace fit {
 namespace {
@@ -31,6 +33,8 @@ constexpr int kSpecBufs = 4;  // warps whose single-candidate exact folds use th
 constexpr int kResLimbs = FS_RES_LIMBS;
 constexpr int kResBias = kResLimbs == 3 ? 62 : 40;  // u = v + 2^bias, count = round(U / 2^bias)
 constexpr int kResMaxDepth = 7;  // node ids fit in uint8
+constexpr int kResClusterMax = 4;  // CTAs per family by default (FAMSEER_RES_CLUSTER overrides)
+constexpr int kResClusterMinRows = 1024;  // ... when the largest family has at least this many rows
 
 struct ResNode {
   int32_t n, seg, state, rep, bin, lc, wcount, build;
@@ -90,12 +94,11 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(L.ls) * nr * sizeof(WinRec));
   L.items = o;
   o = res_align(o + static_cast<size_t>(L.ls) * (nr + 1) * sizeof(int));
-  L.rep = o;
-  o = res_align(o + 2 * nr * sizeof(int));
-  L.limb = o;  // lane-column limb histogram [3][colh][32] u32, 4 x 16-bit limbs of sum |v| per level node,
-               // column offset per rep
-  o = res_align(o + std::max<size_t>(static_cast<size_t>(3) * colh * 32 * 4 + static_cast<size_t>(L.ls) * 4 * 4 + nr * 4,
-                                      8 * 512));
+  L.rep = o;  // per rep: bin offset, bin count, lane-column offset; per level node: 4 x 16-bit limbs of sum |v|
+  o = res_align(o + 3 * nr * sizeof(int) + static_cast<size_t>(L.ls) * 4 * 4);
+  L.limb = o;  // lane-column limb histogram [3][colh][32] u32; the tie classes' phi tables
+               // between histograms
+  o = res_align(o + std::max<size_t>(static_cast<size_t>(3) * colh * 32 * 4, 8 * 512));
   L.sbuf = o;  // speculative exact folds: spec_bufs member lists of up to n rows (u16)
   o = res_align(o + static_cast<size_t>(spec_bufs) * n * 2);
   L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
@@ -209,13 +212,26 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
     unsigned long long* __restrict__ ctr, int pred_smem, double* __restrict__ pred_g, int pre_smem, int spec_bufs) {
   extern __shared__ __align__(16) unsigned char sm[];
+  // Optional thread-block cluster of cl_n CTAs per family (FAMSEER_RES_CLUSTER): every CTA holds
+  // the whole per-row state and runs every phase identically, except the histogram, whose
+  // features are dealt round-robin (feature j -> CTA j % cl_n); after each level's histograms
+  // the CTAs pull each other's bins through distributed shared memory. Only CTA rank 0 writes
+  // global results.
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+  const int cl_n = static_cast<int>(cluster.num_blocks());
+  const int cl_r = static_cast<int>(cluster.block_rank());
+  const bool lead = cl_r == 0;
   __shared__ unsigned long long s_red[32];
   __shared__ double s_dred[32];
   __shared__ int s_wsum[32];
   __shared__ int s_shift, s_nitems, s_ctot;
   __shared__ unsigned long long s_cnt[3];  // screened splits, exact nodes, exact folds
   __shared__ unsigned long long s_why[4];  // exact-node reasons
-  const int f = fam_list[blockIdx.x];
+#ifdef FS_RES_HIST_PROBE
+  __shared__ unsigned long long s_probe[4];
+  if (threadIdx.x < 4) s_probe[threadIdx.x] = 0;
+#endif
+  const int f = fam_list[blockIdx.x / cl_n];
   const FamDesc fd = fam[f];
   const int n = fd.n, nrep = fd.nrep, bins = fd.bins, depth = fd.depth;
   const int colh = nrep > 0 ? col_height(nrep, rep_nb + fd.rep0, nullptr) : 1;
@@ -224,8 +240,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   uint8_t* s_codes = sm + Lo.codes;  // [nrep][cs]
   const int cs = Lo.cs;
   uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [3][colh][32]
-  uint32_t* s_absl = s_limb + 3 * colh * 32;                      // [level node][4]
-  int* s_cofs = reinterpret_cast<int*>(s_absl + Lo.ls * 4);        // [nrep]
+  int* s_cofs = reinterpret_cast<int*>(sm + Lo.rep) + 2 * (nrep > 0 ? nrep : 1);       // [nrep]
+  uint32_t* s_absl = reinterpret_cast<uint32_t*>(s_cofs + (nrep > 0 ? nrep : 1));      // [level node][4]
   double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
   int* s_clc = reinterpret_cast<int*>(sm + Lo.clc);           // [level node][bin] left count
   uint16_t* s_binrep = reinterpret_cast<uint16_t*>(sm + Lo.binrep);
@@ -332,6 +348,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       if (lane == 0) s_red[warp] = mx;
     }
+    if (cl_n > 1) cluster.sync();  // the partners finished pulling last round's histograms
     for (int s = tid; s < slots; s += kResThreads) {
       ResNode z;
       memset(&z, 0, sizeof z);
@@ -339,7 +356,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       s_nodes[s] = z;
     }
     TreeRec* tr = trees + fd.tree0 + static_cast<int64_t>(ntrees) * slots_g;
-    for (int s = tid; s < slots_g; s += kResThreads) {
+    for (int s = tid; s < slots_g && lead; s += kResThreads) {
       TreeRec tz;
       memset(&tz, 0, sizeof tz);
       tr[s] = tz;
@@ -394,10 +411,13 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       // arithmetic; the first fold overwrites). sum |v| (the screen bound) is a per-thread
       // 64-bit sum (< 2^61 by the fixed-point shift), warp-reduced, added as 16-bit limbs.
       {
-        const int rpw = nrep <= 32 ? 32 / nrep : 1;  // rows per warp step
-        const int hj = nrep <= 32 ? lane % nrep : lane;
-        const int hm = nrep <= 32 ? lane / nrep : 0;
-        const bool hact = nrep <= 32 ? hm < rpw : true;
+        // this CTA's features: j = jl * cl_n + cl_r (all of them without a cluster)
+        const int nown = (nrep - cl_r + cl_n - 1) / cl_n;
+        const int rpw = nown <= 32 ? 32 / max(nown, 1) : 1;  // rows per warp step
+        const int hjl = nown <= 32 ? lane % max(nown, 1) : lane;
+        const int hj = hjl * cl_n + cl_r;
+        const int hm = nown <= 32 ? lane / max(nown, 1) : 0;
+        const bool hact = nown <= 32 ? nown > 0 && hm < rpw : true;
         const int cpad = 3 * colh * 32;
         for (int k = 0; k < nl; ++k) {
           ResNode& nd = s_nodes[first + k];
@@ -413,8 +433,11 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
 #endif
             const int q_end = min(nv, sub0 + kAtomSub);
             unsigned long long asum = 0;
+#ifdef FS_RES_HIST_PROBE
+            const long long tp0 = clock64();
+#endif
             if (hact) {
-              if (nrep <= 32) {
+              if (nown <= 32) {
                 const uint8_t* hcode = s_codes + static_cast<size_t>(hj) * cs;
                 uint32_t* colp = s_limb + lane;
 #pragma unroll 4
@@ -426,7 +449,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                   atomicAdd(c, static_cast<uint32_t>(u) & kLimbMask);
                   atomicAdd(c + colh * 32, static_cast<uint32_t>(u >> 21) & kLimbMask);
                   if (kResLimbs == 3) atomicAdd(c + 2 * colh * 32, static_cast<uint32_t>(u >> 42));
-                  if (hj == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
+                  if (hjl == 0) asum += static_cast<unsigned long long>(v < 0 ? -v : v);
                 }
               } else {
                 for (int q = sub0 + warp; q < q_end; q += kResWarps) {
@@ -446,6 +469,14 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                 }
               }
             }
+#ifdef FS_RES_HIST_PROBE
+            if (lane == 0 && blockIdx.x == 0) {
+              const unsigned long long dt = static_cast<unsigned long long>(clock64() - tp0);
+              atomicMax(&s_probe[0], dt);
+              atomicAdd(&s_probe[1], dt);
+              if (warp == 0) atomicAdd(&s_probe[3], 1ull);
+            }
+#endif
             for (int o = 16; o > 0; o >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, o);
             if (lane == 0 && asum) {
 #pragma unroll
@@ -459,10 +490,11 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
             int* ck = hc + static_cast<size_t>(k) * bins;
             for (int i = tid; i < bins; i += kResThreads) {
               const int j = s_binrep[i], b = i - s_repb[j];
+              if (cl_n > 1 && j % cl_n != cl_r) continue;  // a partner's feature
               unsigned __int128 U = 0;
-              if (nrep <= 32) {
+              if (nown <= 32) {
                 for (int m = 0; m < rpw; ++m) {
-                  const uint32_t* c = s_limb + b * 32 + j + m * nrep;
+                  const uint32_t* c = s_limb + b * 32 + j / cl_n + m * nown;
                   U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
                        (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
                 }
@@ -490,6 +522,21 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
             RES_PHASE(3);  // limb fold billed to "derive"
 #endif
           }
+        }
+        if (cl_n > 1) {  // the partners' features of every built node, through DSMEM
+          cluster.sync();
+          for (int k = 0; k < nl; ++k) {
+            if (s_nodes[first + k].build != 1) continue;
+            long long* hk = hs + static_cast<size_t>(k) * bins;
+            int* ck = hc + static_cast<size_t>(k) * bins;
+            for (int i = tid; i < bins; i += kResThreads) {
+              const int owner = s_binrep[i] % cl_n;
+              if (owner == cl_r) continue;
+              hk[i] = *cluster.map_shared_rank(hk + i, owner);
+              ck[i] = *cluster.map_shared_rank(ck + i, owner);
+            }
+          }
+          __syncthreads();
         }
       }
       RES_PHASE(2);
@@ -960,7 +1007,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           r.gain = nd.gain;
           r.rep = j;
           r.bin = nd.bin;
-          tr[s] = r;
+          if (lead) tr[s] = r;
           ResNode& a = s_nodes[2 * s + 1];
           ResNode& b = s_nodes[2 * s + 2];
           a.n = nd.lc;
@@ -1065,7 +1112,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         r.gain = 0.0;
         r.rep = -1;
         r.bin = 0;
-        tr[s] = r;
+        if (lead) tr[s] = r;
       }
     }
     __syncthreads();
@@ -1093,7 +1140,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     for (int o = 16; o > 0; o >>= 1) a = fs_add(a, __shfl_down_sync(0xffffffffu, a, o));
     if (lane == 0) s_dred[warp] = a;
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && lead) {
       double t = 0.0;
       for (int w = 0; w < kResThreads / 32; ++w) t = fs_add(t, s_dred[w]);
       mse[static_cast<int64_t>(f) * max_trees + ntrees] = fs_div(t, static_cast<double>(n));
@@ -1102,7 +1149,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     __syncthreads();
       RES_PHASE(11);
   }
-  if (tid == 0) {
+  if (cl_n > 1) cluster.sync();  // no CTA leaves while a partner may still read its shared memory
+  if (tid == 0 && lead) {
     st[f].ntrees = ntrees;
     st[f].active = 0;
     st[f].screened += s_cnt[0];
@@ -1114,6 +1162,10 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     if (blockIdx.x == 0)
       for (int i = 0; i < 12; ++i) atomicAdd(ctr + kCtrPhase0 + i, static_cast<unsigned long long>(s_ph[i]));
     for (int i = 0; i < 4; ++i) atomicAdd(ctr + kCtrPhase0 + 12 + i, s_why[i]);
+#ifdef FS_RES_HIST_PROBE
+    if (blockIdx.x == 0)
+      for (int i = 0; i < 4; ++i) atomicAdd(ctr + kCtrProbe + i, s_probe[i]);
+#endif
   }
 }
 

@@ -67,7 +67,8 @@ enum Counter : int {
   kCtrExactChains,    // reference-order folds run (node totals + feature scans)
   kCtrExactNodes,     // nodes re-evaluated in reference order
   kCtrPhase0,         // resident trainer: SM cycles per phase (kResPhases entries, CTA 0's view)
-  kCtrCount = kCtrPhase0 + 16
+  kCtrProbe = kCtrPhase0 + 16,  // resident trainer A/B probes (FS_RES_HIST_PROBE builds), 4 entries
+  kCtrCount = kCtrProbe + 4
 };
 
 // Grows-only stream-ordered device buffer.
