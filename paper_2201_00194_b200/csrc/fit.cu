@@ -266,9 +266,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   if (resident.phi_smem > 0)
     FS_CUDA(cudaFuncSetAttribute(tieclass_phi_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(resident.phi_smem)));
-  if (resident.atomic)
-    FS_CUDA(cudaFuncSetAttribute(hist_build_atomic_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (resident.atomic) {
+    FS_CUDA(cudaFuncSetAttribute(hist_build_atomic_kernel<CodeT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(resident.atomic_smem)));
+    FS_CUDA(cudaFuncSetAttribute(hist_build_atomic_kernel<CodeT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(resident.atomic_smem)));
+  }
   if (resident.col) {
     col_off_d = ar.upload(resident.col_off);
     col_rg_d = ar.upload(resident.col_rg);
@@ -316,11 +319,17 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
       {
         ProfScope prof(dev, "fit_hist_build");
-        if (resident.atomic)
-          hist_build_atomic_kernel<CodeT><<<dim3(static_cast<unsigned>(ceil_div(n_max, atom_chunk)), pairs, F),
-                                             kAtomThreads, resident.atomic_smem, s>>>(
-              fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
-              resident.colh_max, atom_chunk);
+        if (resident.atomic) {
+          const dim3 grid(static_cast<unsigned>(ceil_div(n_max, atom_chunk)), pairs, F);
+          if (atom_chunk >= kAtomPipeChunk)
+            hist_build_atomic_kernel<CodeT, true><<<grid, kAtomThreads, resident.atomic_smem, s>>>(
+                fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
+                resident.colh_max, atom_chunk);
+          else
+            hist_build_atomic_kernel<CodeT, false><<<grid, kAtomThreads, resident.atomic_smem, s>>>(
+                fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
+                resident.colh_max, atom_chunk);
+        }
         else if (resident.col)
           hist_build_col_kernel<CodeT><<<dim3(chunks, pairs, F), kColWarps * 32, resident.col_smem, s>>>(
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, rep_nb_d, col_off_d, col_rg_d, hsum,

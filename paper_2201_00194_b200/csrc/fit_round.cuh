@@ -322,10 +322,15 @@ constexpr int kAtomThreads = 1024;
 constexpr int kAtomSub = 2048;
 constexpr int kAtomChunk = 8192;  // max rows per CTA (fewer when the batch is small: >= 2 CTAs per SM)
 constexpr int kAtomTile = 128;
+constexpr int kAtomPre = 2;  // uint4 of the next tile's code rows held in registers per thread (kPipe)
+constexpr int kAtomPipeChunk = 8 * kAtomTile;  // rows per CTA from which the pipelined shape is used
 constexpr uint32_t kLimbMask = (1u << 21) - 1u;
 
-template <typename CodeT>
-__global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
+// kPipe: one CTA per SM (64 registers per thread) holding the next tile's gathers in registers
+// (for launches whose CTAs walk many tiles, C5-sized); otherwise two CTAs per SM overlap each
+// other's gather latency (few tiles per CTA, C4-sized).
+template <typename CodeT, bool kPipe>
+__global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, const NodeRec* __restrict__ nodes, int level,
     int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
     const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
@@ -397,17 +402,50 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
     for (int i = tid; i < 3 * colh * 32; i += kAtomThreads) limb[i] = 0;
     __syncthreads();
     const int sub_end = min(rows, sub0 + kAtomSub);
+    // Software pipeline (when a tile's code rows fit kAtomPre uint4 per thread): the next tile's
+    // row gathers are issued into registers before this tile's atomics, so their global-memory
+    // latency hides behind the shared-memory work instead of stalling every tile.
+    const bool pipe = kPipe && kAtomTile * vec_per_row <= kAtomPre * kAtomThreads;
+    uint4 pv[kAtomPre];
+    int64_t pfix = 0;
+#define FS_ATOM_PREFETCH(T0)                                                        \
+  do {                                                                              \
+    const int tr_ = min(kAtomTile, sub_end - (T0));                                 \
+    _Pragma("unroll") for (int q = 0; q < kAtomPre; ++q) {                          \
+      const int i = tid + q * kAtomThreads;                                         \
+      if (i < tr_ * vec_per_row) {                                                  \
+        const int r = i / vec_per_row, v = i - r * vec_per_row;                     \
+        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + (T0) + r];         \
+        pv[q] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];               \
+      }                                                                             \
+    }                                                                               \
+    if (tid < tr_) pfix = rfix[fd.pos0 + ord_cur[fd.pos0 + seg + r0 + (T0) + tid]]; \
+  } while (0)
+    if (pipe) FS_ATOM_PREFETCH(sub0);
     for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
       const int tr = min(kAtomTile, sub_end - t0);
-      for (int i = tid; i < tr * vec_per_row; i += kAtomThreads) {
-        const int r = i / vec_per_row, v = i - r * vec_per_row;
-        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
-        reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+      int64_t v_own = 0;
+      if (pipe) {
+#pragma unroll
+        for (int q = 0; q < kAtomPre; ++q) {
+          const int i = tid + q * kAtomThreads;
+          if (i < tr * vec_per_row) {
+            const int r = i / vec_per_row, v = i - r * vec_per_row;
+            reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = pv[q];
+          }
+        }
+        v_own = pfix;
+      } else {
+        for (int i = tid; i < tr * vec_per_row; i += kAtomThreads) {
+          const int r = i / vec_per_row, v = i - r * vec_per_row;
+          const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+          reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
+        }
+        if (tid < tr) v_own = rfix[fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid]];
       }
       unsigned long long a = 0;
       if (tid < tr) {
-        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid];
-        const int64_t v = rfix[p];
+        const int64_t v = v_own;
         const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
         t_limb[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;
         t_limb[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;
@@ -419,6 +457,7 @@ __global__ void __launch_bounds__(kAtomThreads, 2) hist_build_atomic_kernel(
         if (lane == 0 && a) atomicAdd(&s_abs, a);
       }
       __syncthreads();
+      if (pipe && t0 + kAtomTile < sub_end) FS_ATOM_PREFETCH(t0 + kAtomTile);
       // lane columns: every lane adds into its own bank column -> one wavefront per atomic
       if (hact) {
         uint32_t* colp = limb + lane;
