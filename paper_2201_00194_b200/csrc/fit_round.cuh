@@ -323,6 +323,7 @@ constexpr int kAtomSub = 2048;
 constexpr int kAtomChunk = 8192;  // max rows per CTA (fewer when the batch is small: >= 2 CTAs per SM)
 constexpr int kAtomTile = 128;
 constexpr int kAtomPre = 2;  // uint4 of the next tile's code rows held in registers per thread (kPipe)
+constexpr int kAtomCofRegs = 8;  // lane column offsets kept in registers (nrep <= 256)
 constexpr int kAtomPipeChunk = 8 * kAtomTile;  // rows per CTA from which the pipelined shape is used
 constexpr uint32_t kLimbMask = (1u << 21) - 1u;
 
@@ -398,16 +399,62 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
   const int hm = nrep <= 32 ? lane / nrep : 0;
   const bool hact = nrep <= 32 ? hm < rpw : true;
   const int vec_per_row = Dp * static_cast<int>(sizeof(CodeT)) / 16;
+  // per-lane column offsets of the lane's features (nrep > 32: features lane, lane + 32, ...)
+  int cofr[kAtomCofRegs];
+#pragma unroll
+  for (int t = 0; t < kAtomCofRegs; ++t) cofr[t] = kPipe && lane + 32 * t < nrep ? s_cofs[lane + 32 * t] : 0;
+  // one row of the tile into the lane columns (hact lanes; r = the tile row)
+  auto add_rows = [&](const CodeT* tc, const uint32_t* tl_all, int tr) {
+    if (!hact) return;
+    uint32_t* colp = limb + lane;
+    if (nrep <= 32) {
+      for (int r = warp * rpw + hm; r < tr; r += (kAtomThreads / 32) * rpw) {
+        const uint32_t* tl = tl_all + 3 * r;
+        uint32_t* c = colp + static_cast<int>(tc[r * Dp + hj]) * 32;
+        atomicAdd(c, tl[0]);
+        atomicAdd(c + colh * 32, tl[1]);
+        atomicAdd(c + 2 * colh * 32, tl[2]);
+      }
+    } else if (kPipe && nrep <= 32 * kAtomCofRegs) {  // (registers to spare only in the 1-CTA shape)
+      for (int r = warp; r < tr; r += kAtomThreads / 32) {
+        const uint32_t l0 = tl_all[3 * r], l1 = tl_all[3 * r + 1], l2 = tl_all[3 * r + 2];
+        const CodeT* cr = tc + r * Dp;
+#pragma unroll
+        for (int t = 0; t < kAtomCofRegs; ++t) {
+          const int j = lane + 32 * t;
+          if (j >= nrep) break;
+          uint32_t* c = colp + (cofr[t] + static_cast<int>(cr[j])) * 32;
+          atomicAdd(c, l0);
+          atomicAdd(c + colh * 32, l1);
+          atomicAdd(c + 2 * colh * 32, l2);
+        }
+      }
+    } else {
+      for (int r = warp; r < tr; r += kAtomThreads / 32) {
+        const uint32_t l0 = tl_all[3 * r], l1 = tl_all[3 * r + 1], l2 = tl_all[3 * r + 2];
+        const CodeT* cr = tc + r * Dp;
+        for (int j = lane; j < nrep; j += 32) {
+          uint32_t* c = colp + (s_cofs[j] + static_cast<int>(cr[j])) * 32;
+          atomicAdd(c, l0);
+          atomicAdd(c + colh * 32, l1);
+          atomicAdd(c + 2 * colh * 32, l2);
+        }
+      }
+    }
+  };
   for (int sub0 = 0; sub0 < rows; sub0 += kAtomSub) {
     for (int i = tid; i < 3 * colh * 32; i += kAtomThreads) limb[i] = 0;
     __syncthreads();
     const int sub_end = min(rows, sub0 + kAtomSub);
-    // Software pipeline (when a tile's code rows fit kAtomPre uint4 per thread): the next tile's
-    // row gathers are issued into registers before this tile's atomics, so their global-memory
-    // latency hides behind the shared-memory work instead of stalling every tile.
     const bool pipe = kPipe && kAtomTile * vec_per_row <= kAtomPre * kAtomThreads;
-    uint4 pv[kAtomPre];
-    int64_t pfix = 0;
+    if (pipe) {
+      // Software pipeline, one barrier per tile: registers hold tile t+1's gathered code rows
+      // (and residual); they go to the other tile buffer, tile t+2's gathers are issued into the
+      // same registers, then tile t is accumulated. The buffer written at tile t was last read
+      // at tile t-1, and tile t's buffer was written at tile t-1: the barrier closing each tile
+      // orders both.
+      uint4 pv[kAtomPre];
+      int64_t pfix = 0;
 #define FS_ATOM_PREFETCH(T0)                                                        \
   do {                                                                              \
     const int tr_ = min(kAtomTile, sub_end - (T0));                                 \
@@ -421,68 +468,75 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
     }                                                                               \
     if (tid < tr_) pfix = rfix[fd.pos0 + ord_cur[fd.pos0 + seg + r0 + (T0) + tid]]; \
   } while (0)
-    if (pipe) FS_ATOM_PREFETCH(sub0);
-    for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
-      const int tr = min(kAtomTile, sub_end - t0);
-      int64_t v_own = 0;
-      if (pipe) {
-#pragma unroll
-        for (int q = 0; q < kAtomPre; ++q) {
-          const int i = tid + q * kAtomThreads;
-          if (i < tr * vec_per_row) {
-            const int r = i / vec_per_row, v = i - r * vec_per_row;
-            reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = pv[q];
-          }
+      // the registers' tile into buffer b (codes, limbs, |v| into s_abs)
+#define FS_ATOM_STAGE(T0, B)                                                                        \
+  do {                                                                                              \
+    const int tr_ = min(kAtomTile, sub_end - (T0));                                                 \
+    CodeT* tc_ = t_codes + (B) * (kAtomTile * Dp + 12 * kAtomTile / static_cast<int>(sizeof(CodeT)));  \
+    uint32_t* tl_ = reinterpret_cast<uint32_t*>(tc_ + kAtomTile * Dp);                              \
+    _Pragma("unroll") for (int q = 0; q < kAtomPre; ++q) {                                          \
+      const int i = tid + q * kAtomThreads;                                                         \
+      if (i < tr_ * vec_per_row) {                                                                  \
+        const int r = i / vec_per_row, v = i - r * vec_per_row;                                     \
+        reinterpret_cast<uint4*>(tc_ + r * Dp)[v] = pv[q];                                          \
+      }                                                                                             \
+    }                                                                                               \
+    unsigned long long a_ = 0;                                                                      \
+    if (tid < tr_) {                                                                                \
+      const uint64_t u = static_cast<uint64_t>(pfix) + (1ull << 62);                                \
+      tl_[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;                                          \
+      tl_[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;                                \
+      tl_[3 * tid + 2] = static_cast<uint32_t>(u >> 42);                                            \
+      a_ = static_cast<unsigned long long>(pfix < 0 ? -pfix : pfix);                                \
+    }                                                                                               \
+    if (warp * 32 < tr_) {                                                                          \
+      for (int o = 16; o > 0; o >>= 1) a_ += __shfl_xor_sync(0xffffffffu, a_, o);                   \
+      if (lane == 0 && a_) atomicAdd(&s_abs, a_);                                                   \
+    }                                                                                               \
+  } while (0)
+      FS_ATOM_PREFETCH(sub0);
+      FS_ATOM_STAGE(sub0, 0);
+      if (sub0 + kAtomTile < sub_end) FS_ATOM_PREFETCH(sub0 + kAtomTile);
+      __syncthreads();
+      int buf = 0;
+      for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
+        const int tr = min(kAtomTile, sub_end - t0);
+        if (t0 + kAtomTile < sub_end) {
+          FS_ATOM_STAGE(t0 + kAtomTile, buf ^ 1);
+          if (t0 + 2 * kAtomTile < sub_end) FS_ATOM_PREFETCH(t0 + 2 * kAtomTile);
         }
-        v_own = pfix;
-      } else {
+        const CodeT* tc = t_codes + buf * (kAtomTile * Dp + 12 * kAtomTile / static_cast<int>(sizeof(CodeT)));
+        add_rows(tc, reinterpret_cast<const uint32_t*>(tc + kAtomTile * Dp), tr);
+        __syncthreads();
+        buf ^= 1;
+      }
+#undef FS_ATOM_PREFETCH
+#undef FS_ATOM_STAGE
+    } else {
+      for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
+        const int tr = min(kAtomTile, sub_end - t0);
         for (int i = tid; i < tr * vec_per_row; i += kAtomThreads) {
           const int r = i / vec_per_row, v = i - r * vec_per_row;
           const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
           reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
         }
-        if (tid < tr) v_own = rfix[fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid]];
-      }
-      unsigned long long a = 0;
-      if (tid < tr) {
-        const int64_t v = v_own;
-        const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
-        t_limb[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;
-        t_limb[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;
-        t_limb[3 * tid + 2] = static_cast<uint32_t>(u >> 42);
-        a = static_cast<unsigned long long>(v < 0 ? -v : v);
-      }
-      if (warp * 32 < tr) {
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0 && a) atomicAdd(&s_abs, a);
-      }
-      __syncthreads();
-      if (pipe && t0 + kAtomTile < sub_end) FS_ATOM_PREFETCH(t0 + kAtomTile);
-      // lane columns: every lane adds into its own bank column -> one wavefront per atomic
-      if (hact) {
-        uint32_t* colp = limb + lane;
-        if (nrep <= 32) {
-          for (int r = warp * rpw + hm; r < tr; r += (kAtomThreads / 32) * rpw) {
-            const uint32_t* tl = t_limb + 3 * r;
-            uint32_t* c = colp + static_cast<int>(t_codes[r * Dp + hj]) * 32;
-            atomicAdd(c, tl[0]);
-            atomicAdd(c + colh * 32, tl[1]);
-            atomicAdd(c + 2 * colh * 32, tl[2]);
-          }
-        } else {
-          for (int r = warp; r < tr; r += kAtomThreads / 32) {
-            const uint32_t l0 = t_limb[3 * r], l1 = t_limb[3 * r + 1], l2 = t_limb[3 * r + 2];
-            const CodeT* cr = t_codes + r * Dp;
-            for (int j = lane; j < nrep; j += 32) {
-              uint32_t* c = colp + (s_cofs[j] + static_cast<int>(cr[j])) * 32;
-              atomicAdd(c, l0);
-              atomicAdd(c + colh * 32, l1);
-              atomicAdd(c + 2 * colh * 32, l2);
-            }
-          }
+        unsigned long long a = 0;
+        if (tid < tr) {
+          const int64_t v = rfix[fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid]];
+          const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
+          t_limb[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;
+          t_limb[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;
+          t_limb[3 * tid + 2] = static_cast<uint32_t>(u >> 42);
+          a = static_cast<unsigned long long>(v < 0 ? -v : v);
         }
+        if (warp * 32 < tr) {
+          for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          if (lane == 0 && a) atomicAdd(&s_abs, a);
+        }
+        __syncthreads();
+        add_rows(t_codes, t_limb, tr);
+        __syncthreads();
       }
-      __syncthreads();
     }
     for (int b = tid; b < bins; b += kAtomThreads) {
       const int j = s_binrep[b], bb = b - s_boff[j];
@@ -523,7 +577,7 @@ inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes, int c
   size_t o = (static_cast<size_t>(3) * colh * 32 * 4 + 15) & ~size_t(15);
   o += static_cast<size_t>(bins) * 14 + static_cast<size_t>(nrep) * 12 + 16;
   o = (o + 15) & ~size_t(15);
-  o += static_cast<size_t>(kAtomTile) * Dp * code_bytes + static_cast<size_t>(kAtomTile) * 12 + 16;
+  o += 2 * (static_cast<size_t>(kAtomTile) * Dp * code_bytes + static_cast<size_t>(kAtomTile) * 12) + 16;  // 2 tiles
   return o;
 }
 
