@@ -87,3 +87,25 @@ def test_fit_records_equals_fit_on_featurized_rows(dev, orc):
         assert ea.base == eb.base
         for k in FIELDS:
             assert np.array_equal(getattr(ea, k), getattr(eb, k)), (f, k)
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "4"])
+def test_resident_cluster_sizes_bit_exact(dev, orc, monkeypatch, cluster):
+    """The resident trainer's thread-block-cluster shapes (histogram features dealt over 1, 2 or 4
+    CTAs, bins exchanged through distributed shared memory) all reproduce the oracle's trees."""
+    monkeypatch.setenv("FAMSEER_FIT_PATH", "resident")
+    monkeypatch.setenv("FAMSEER_RES_CLUSTER", cluster)
+    W = bench.build_workload("c2", 1000)
+    x = bench._featurize_host(W, orc)
+    seg, y = W["tr_seg"], W["tr_y"]
+    F = len(W["families"])
+    fo = fs.Forest(dev, F)
+    fo.fit(x, y, seg=list(seg), params=fs.GbtParams(40, 3, 0.1, 2))
+    for f in range(F):
+        a, b = int(seg[f]), int(seg[f + 1])
+        exp = orc.fit(x[a:b], y[a:b], trees=40)
+        got = fo.export(f)
+        assert got.base == exp.base, (cluster, f)
+        for k in FIELDS:
+            assert np.array_equal(getattr(got, k), getattr(exp, k)), (cluster, f, k)
+        np.testing.assert_array_equal(fo.fit_stats(f)[0] + fo.fit_stats(f)[1] > 0, True)
