@@ -375,7 +375,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                                    level_slots_max, small_scratch ? 1 : 0);
         if (small_scratch)
           exact_small_kernel<CodeT><<<kExactSmallCtas, kSortThreads, 0, s>>>(
-              fam_d, nodes, items, n_items, level, Dp, codes_c, resid, nodeid, rep_boff_d, lbuf, win,
+              fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win,
               std::max(nrep_max, 1), level_slots_max, small_scratch, n_max);
       }
       exact_decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt,

@@ -1053,6 +1053,149 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 }
 
 
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = fs_add(a, b);
+  const double bb = fs_sub(s, a);
+  e = fs_add(fs_sub(a, fs_sub(s, bb)), fs_sub(b, bb));
+}
+__device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles -> consecutive ints
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : static_cast<long long>(0x8000000000000000ull) - b;
+}
+__device__ __forceinline__ double ord_dbl(long long o) {
+  return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
+}
+// CTA-wide exact sequential fold of a long gathered chain (sum_residuals, costmodel.cpp:36-40) by
+// midpoint speculation (the warp version is fold_spec): the block's double-double sum of
+// x_0..x_{m-1} estimates the exact prefix P; thread 0 folds x_0..x_{m-1} from 0.0 (the true S_m)
+// while threads t = 1..255 fold x_m..x_{n-1} from the doubles P + (t-128) ulp; the thread whose
+// start is bit-identical to S_m holds S_n. A miss finishes the chain from S_m (same result).
+// All 256 threads must call it; the result is returned to every thread.
+__device__ __forceinline__ double warp_fold_gather_from(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                        int n, double s) {
+  // warp_fold_gather with a per-lane start value: every lane folds the same sequence (loaded
+  // cooperatively, 128 gathers in flight ahead of the adds) from its own start
+  const int lane = threadIdx.x & 31;
+  double x[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = 32 * c + lane;
+    x[c] = i < n ? v[idx[i]] : 0.0;
+  }
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    double y[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 128 + 32 * c + lane;
+      y[c] = i < n ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int base = i0 + 32 * c;
+      if (base >= n) break;
+      const int m = min(32, n - base);
+      if (m == 32) {
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          double t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
+        }
+      } else {
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = y[c];
+  }
+  return s;
+}
+
+__device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
+                                                double* red /* smem [66]: per-warp hi / lo (up to 32 warps), S_m, result */) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = static_cast<int>(blockDim.x >> 5);
+  if (n < 4096 || nw < 2) {  // short chain: warp 0 folds it
+    if (warp == 0) {
+      const double r = warp_fold_gather_from(v, idx, n, 0.0);
+      if (lane == 0) red[64] = r;
+    }
+    __syncthreads();
+    const double r = red[64];
+    __syncthreads();
+    return r;
+  }
+  const int m = n >> 1;
+  // exact-prefix estimate of x_0..x_{m-1}: double-double partial sums (8 gathers in flight)
+  double hi = 0.0, lo = 0.0;
+  for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * blockDim.x;
+      a[k] = i < m ? v[idx[i]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double s, e;
+      two_sum(hi, a[k], s, e);
+      hi = s;
+      lo = fs_add(lo, e);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, e;
+    two_sum(hi, oh, s, e);
+    hi = s;
+    lo = fs_add(fs_add(lo, ol), e);
+  }
+  if (lane == 0) {
+    red[warp] = hi;
+    red[32 + warp] = lo;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double h = 0.0, l = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      double s, e;
+      two_sum(h, red[w], s, e);
+      h = s;
+      l = fs_add(fs_add(l, red[32 + w]), e);
+    }
+    red[65] = fs_add(h, l);
+  }
+  __syncthreads();
+  const double P = red[65];
+  // warp 0 folds the first half from 0.0 (the true S_m); warps 1.. fold the second half from
+  // the candidate starts P + k ulp, k centred on 0 (32 * (nw - 1) candidates)
+  const int cand = tid - 32;  // 0 .. 32*(nw-1)-1
+  const double start = warp == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (cand - 16 * (nw - 1)));
+  const double r = warp == 0 ? warp_fold_gather_from(v, idx, m, 0.0)
+                             : warp_fold_gather_from(v, idx + m, n - m, start);
+  __shared__ int hit;
+  if (tid == 0) {
+    red[64] = r;  // S_m
+    hit = 0;
+  }
+  __syncthreads();
+  if (warp > 0 && __double_as_longlong(start) == __double_as_longlong(red[64])) {
+    red[65] = r;
+    hit = 1;
+  }
+  __syncthreads();
+  if (!hit && warp == 0) {  // speculation missed: finish from the true midpoint
+    const double t = warp_fold_gather_from(v, idx + m, n - m, red[64]);
+    if (lane == 0) red[65] = t;
+  }
+  __syncthreads();
+  const double out = red[65];
+  __syncthreads();
+  return out;
+}
+
 // sum_residuals (costmodel.cpp:36-40) of v[idx[0..n)) in list order by one warp: four chunks of
 // 32 gathers are in flight at once, then each chunk's values are added in lane order (shuffles
 // hoisted ahead of the dependent add chain). Every lane returns the sum.
@@ -1062,6 +1205,7 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 // presorted list restricted to the node (:50-55), recorded at every value boundary.
 // exact folds of nodes below a quarter of the family go through exact_small_kernel
 __device__ __forceinline__ bool exact_is_small(int nv, int n) { return nv < n; }
+constexpr int kExactSpecMin = 4096;  // chains from this length fold speculatively in a CTA (cta_fold_spec)
 
 // Exact reference-order folds for SMALL nodes (nv * 4 < n): instead of scanning the feature's
 // full presorted list for the node's members (exact_kernel; costs O(n) gathers per item however
@@ -1073,25 +1217,42 @@ template <typename CodeT>
 __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
     const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
-    const double* __restrict__ resid, const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_boff,
+    const double* __restrict__ resid, const int32_t* __restrict__ ord, const int32_t* __restrict__ ord_cur,
+    const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_boff,
     double* __restrict__ lbuf, const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
     int32_t* __restrict__ scratch, int n_max) {
   __shared__ SortSmem sm;
   __shared__ int wsum[32];
+  __shared__ double red[66];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = *n_items;
   sort_smem_init(sm);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const ExactItem it = items[w];
-    if (it.rep < 0) continue;
     const FamDesc fd = fam[it.fam];
-    const NodeRec& nd = nodes[fd.node0 + it.slot];
+    NodeRec& nd = nodes[fd.node0 + it.slot];
     const int nv = nd.n, n = fd.n;
-    if (!exact_is_small(nv, n)) continue;
+    if (it.rep < 0) {  // a long node total: speculative CTA fold (exact_kernel folds the short ones)
+      if (nv < kExactSpecMin) continue;
+      const double t = cta_fold_spec(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, nv, red);
+      if (tid == 0) nd.total = t;
+      continue;
+    }
     const int jj = it.rep;
     const int local = it.slot - ((1 << level) - 1);
-    const int need = win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + jj].maxlc;
+    const WinRec& wr = win[(static_cast<int64_t>(it.fam) * level_slots_max + local) * nrep_max + jj];
+    const int need = wr.maxlc;
     double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
+    // one window candidate: only L at its left count is read (exact_decide_kernel), so a long
+    // fold splits speculatively at its midpoint (cta_fold_spec, bit-exact)
+    const bool spec_one = wr.count == 1 && need >= kExactSpecMin;
+    if (!exact_is_small(nv, n)) {
+      if (!spec_one) continue;  // exact_kernel scans the presorted list
+      // the root: every row is a member, the presorted list is the member list
+      const double L = cta_fold_spec(resid + fd.pos0, ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n, need, red);
+      if (tid == 0) out[wr.best_bin] = L;
+      continue;
+    }
     int32_t* A = scratch + static_cast<int64_t>(blockIdx.x) * 2 * n_max;
     int32_t* B = A + n_max;
     // 1. the node's rows in canonical order
@@ -1138,7 +1299,10 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
       __syncthreads();
     }
     // 3. the fold (warp 0; members in list order, boundaries at code changes)
-    if (warp == 0) {
+    if (spec_one) {
+      const double L = cta_fold_spec(resid + fd.pos0, src, need, red);
+      if (tid == 0) out[wr.best_bin] = L;
+    } else if (warp == 0) {
       double left = 0.0;
       int prev = -1;
       for (int i0 = 0; i0 < need; i0 += 32) {
@@ -1190,11 +1354,17 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
     NodeRec& nd = nodes[fd.node0 + it.slot];
     const int n = nd.n;
     if (it.rep < 0) {
+      if (small_path && n >= kExactSpecMin) continue;  // exact_small_kernel: speculative CTA fold
       const double s = warp_fold_gather(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, n);
       if (lane == 0) nd.total = s;
       continue;
     }
     if (exact_is_small(n, fd.n) && small_path) continue;  // exact_small_kernel folds it
+    if (small_path) {
+      const WinRec& wr = win[(static_cast<int64_t>(it.fam) * level_slots_max + (it.slot - ((1 << level) - 1))) *
+                                 nrep_max + it.rep];
+      if (wr.count == 1 && wr.maxlc >= kExactSpecMin) continue;  // exact_small_kernel: speculative fold
+    }
     const int jj = it.rep;
     const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
     const int local = it.slot - ((1 << level) - 1);
@@ -1420,151 +1590,6 @@ __global__ void __launch_bounds__(1024) partition_kernel(
   }
 }
 
-// Leaves: value = (reference-order total) / n (costmodel.cpp:86), prediction += lr * value
-// (:88-90); tree record. One warp per (family, slot).
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-  s = fs_add(a, b);
-  const double bb = fs_sub(s, a);
-  e = fs_add(fs_sub(a, fs_sub(s, bb)), fs_sub(b, bb));
-}
-__device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles -> consecutive ints
-  const long long b = __double_as_longlong(x);
-  return b >= 0 ? b : static_cast<long long>(0x8000000000000000ull) - b;
-}
-__device__ __forceinline__ double ord_dbl(long long o) {
-  return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
-}
-// CTA-wide exact sequential fold of a long gathered chain (sum_residuals, costmodel.cpp:36-40) by
-// midpoint speculation (the warp version is fold_spec): the block's double-double sum of
-// x_0..x_{m-1} estimates the exact prefix P; thread 0 folds x_0..x_{m-1} from 0.0 (the true S_m)
-// while threads t = 1..255 fold x_m..x_{n-1} from the doubles P + (t-128) ulp; the thread whose
-// start is bit-identical to S_m holds S_n. A miss finishes the chain from S_m (same result).
-// All 256 threads must call it; the result is returned to every thread.
-__device__ __forceinline__ double warp_fold_gather_from(const double* __restrict__ v, const int32_t* __restrict__ idx,
-                                                        int n, double s) {
-  // warp_fold_gather with a per-lane start value: every lane folds the same sequence (loaded
-  // cooperatively, 128 gathers in flight ahead of the adds) from its own start
-  const int lane = threadIdx.x & 31;
-  double x[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int i = 32 * c + lane;
-    x[c] = i < n ? v[idx[i]] : 0.0;
-  }
-  for (int i0 = 0; i0 < n; i0 += 128) {
-    double y[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = i0 + 128 + 32 * c + lane;
-      y[c] = i < n ? v[idx[i]] : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int base = i0 + 32 * c;
-      if (base >= n) break;
-      const int m = min(32, n - base);
-      if (m == 32) {
-#pragma unroll
-        for (int l0 = 0; l0 < 32; l0 += 8) {
-          double t[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
-        }
-      } else {
-        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) x[c] = y[c];
-  }
-  return s;
-}
-
-__device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
-                                                double* red /* smem [2*8+2] */) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = static_cast<int>(blockDim.x >> 5);
-  if (n < 4096 || nw < 2) {  // short chain: warp 0 folds it
-    if (warp == 0) {
-      const double r = warp_fold_gather_from(v, idx, n, 0.0);
-      if (lane == 0) red[16] = r;
-    }
-    __syncthreads();
-    const double r = red[16];
-    __syncthreads();
-    return r;
-  }
-  const int m = n >> 1;
-  // exact-prefix estimate of x_0..x_{m-1}: double-double partial sums (8 gathers in flight)
-  double hi = 0.0, lo = 0.0;
-  for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
-    double a[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = i0 + k * blockDim.x;
-      a[k] = i < m ? v[idx[i]] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      double s, e;
-      two_sum(hi, a[k], s, e);
-      hi = s;
-      lo = fs_add(lo, e);
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
-    double s, e;
-    two_sum(hi, oh, s, e);
-    hi = s;
-    lo = fs_add(fs_add(lo, ol), e);
-  }
-  if (lane == 0) {
-    red[warp] = hi;
-    red[8 + warp] = lo;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double h = 0.0, l = 0.0;
-    for (int w = 0; w < nw; ++w) {
-      double s, e;
-      two_sum(h, red[w], s, e);
-      h = s;
-      l = fs_add(fs_add(l, red[8 + w]), e);
-    }
-    red[17] = fs_add(h, l);
-  }
-  __syncthreads();
-  const double P = red[17];
-  // warp 0 folds the first half from 0.0 (the true S_m); warps 1.. fold the second half from
-  // the candidate starts P + k ulp, k centred on 0 (32 * (nw - 1) candidates)
-  const int cand = tid - 32;  // 0 .. 32*(nw-1)-1
-  const double start = warp == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (cand - 16 * (nw - 1)));
-  const double r = warp == 0 ? warp_fold_gather_from(v, idx, m, 0.0)
-                             : warp_fold_gather_from(v, idx + m, n - m, start);
-  __shared__ int hit;
-  if (tid == 0) {
-    red[16] = r;  // S_m
-    hit = 0;
-  }
-  __syncthreads();
-  if (warp > 0 && __double_as_longlong(start) == __double_as_longlong(red[16])) {
-    red[17] = r;
-    hit = 1;
-  }
-  __syncthreads();
-  if (!hit && warp == 0) {  // speculation missed: finish from the true midpoint
-    const double t = warp_fold_gather_from(v, idx + m, n - m, red[16]);
-    if (lane == 0) red[17] = t;
-  }
-  __syncthreads();
-  const double out = red[17];
-  __syncthreads();
-  return out;
-}
-
 // Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
 // the leaf's order-0 segment / n (cta_fold_spec), then pred += lr*value over its rows.
 __global__ void __launch_bounds__(256) leaf_cta_kernel(const FamDesc* __restrict__ fam, int F,
@@ -1572,7 +1597,7 @@ __global__ void __launch_bounds__(256) leaf_cta_kernel(const FamDesc* __restrict
                                                        int slots, const int32_t* __restrict__ ord_cur,
                                                        const double* __restrict__ resid, double* __restrict__ pred,
                                                        TreeRec* __restrict__ trees) {
-  __shared__ double red[18];
+  __shared__ double red[66];
   const int f = blockIdx.y, s = blockIdx.x;
   if (f >= F) return;
   const FamDesc fd = fam[f];
@@ -1615,6 +1640,8 @@ __global__ void __launch_bounds__(256) leaf_cta_kernel(const FamDesc* __restrict
   }
 }
 
+// Leaves: value = (reference-order total) / n (costmodel.cpp:86), prediction += lr * value
+// (:88-90); tree record. One warp per (family, slot).
 __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamState* __restrict__ st,
                             NodeRec* __restrict__ nodes, int slots, const int32_t* __restrict__ ord_cur,
                             const double* __restrict__ resid, double* __restrict__ pred, TreeRec* __restrict__ trees) {
