@@ -88,14 +88,11 @@ void UploadBatch::flush(fs_device* dev) {
 
 void materialize(fs_device* dev, const FamilyModel& m) { materialize(dev, const_cast<FamilyModel&>(m)); }
 
-void materialize(fs_device* dev, FamilyModel& m) {
-  if (!m.pending) return;
+namespace {
+// the pre-order arrays of a pending model from its device export region, already on the host
+void materialize_from(FamilyModel& m, const unsigned char* h) {
   const DevLayout& L = m.lay;
-  const size_t bytes = L.total - L.meta;
-  std::vector<unsigned char> h(bytes);
-  FS_CUDA(cudaMemcpyAsync(h.data(), m.blob_d + L.meta, bytes, cudaMemcpyDeviceToHost, dev->stream));
-  FS_CUDA(cudaStreamSynchronize(dev->stream));
-  auto at = [&](size_t off) { return h.data() + (off - L.meta); };
+  auto at = [&](size_t off) { return h + (off - L.meta); };
   ModelMeta meta;
   std::memcpy(&meta, at(L.meta), sizeof meta);
   const int T = meta.n_trees, S = L.slots;
@@ -131,6 +128,41 @@ void materialize(fs_device* dev, FamilyModel& m) {
   m.mse.assign(mse, mse + T);
   m.n_trees = T;
   m.pending = false;
+}
+}  // namespace
+
+void materialize(fs_device* dev, FamilyModel& m) {
+  if (!m.pending) return;
+  const size_t bytes = m.lay.total - m.lay.meta;
+  std::vector<unsigned char> h(bytes);
+  FS_CUDA(cudaMemcpyAsync(h.data(), m.blob_d + m.lay.meta, bytes, cudaMemcpyDeviceToHost, dev->stream));
+  FS_CUDA(cudaStreamSynchronize(dev->stream));
+  materialize_from(m, h.data());
+}
+
+// Every pending family of a forest in one pinned device->host read and one synchronisation
+// (a fit leaves all its families pending; the first export of any of them fetches them all).
+void materialize_all(fs_device* dev, std::vector<FamilyModel>& fams) {
+  size_t tot = 0;
+  for (const auto& m : fams)
+    if (m.pending) tot += (m.lay.total - m.lay.meta + 15) & ~size_t(15);
+  if (tot == 0) return;
+  auto* h = static_cast<unsigned char*>(dev->pinned(tot));
+  size_t o = 0;
+  for (const auto& m : fams) {
+    if (!m.pending) continue;
+    const size_t bytes = m.lay.total - m.lay.meta;
+    FS_CUDA(cudaMemcpyAsync(h + o, m.blob_d + m.lay.meta, bytes, cudaMemcpyDeviceToHost, dev->stream));
+    o += (bytes + 15) & ~size_t(15);
+  }
+  FS_CUDA(cudaStreamSynchronize(dev->stream));
+  o = 0;
+  for (auto& m : fams) {
+    if (!m.pending) continue;
+    const size_t bytes = m.lay.total - m.lay.meta;
+    materialize_from(m, h + o);
+    o += (bytes + 15) & ~size_t(15);
+  }
 }
 
 void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch) {
@@ -328,7 +360,7 @@ int fs_forest_export(const fs_forest* fo, int32_t family, double* base, int32_t*
     if (!fo || family < 0 || family >= static_cast<int32_t>(fo->fams.size()))
       fs::fail(FS_ERANGE, "fs_forest_export: unknown family id " + std::to_string(family));
     const auto& m = fo->fams[static_cast<size_t>(family)];
-    fs::materialize(fo->dev, m);
+    if (m.pending) fs::materialize_all(fo->dev, const_cast<fs_forest*>(fo)->fams);
     const int T = m.num_trees();
     const int N = m.offsets.back();
     if (base) *base = m.base;

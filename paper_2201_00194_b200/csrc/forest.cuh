@@ -92,6 +92,7 @@ struct UploadBatch {
 // Download a device-compiled fit's pre-order export into the host arrays (no-op otherwise).
 void materialize(fs_device* dev, FamilyModel& m);
 void materialize(fs_device* dev, const FamilyModel& m);
+void materialize_all(fs_device* dev, std::vector<FamilyModel>& fams);
 
 // Build the compiled device form from the pre-order arrays (host transformation of the tree
 // table; O(nodes)). With a batch, the device copy is deferred to batch->flush().
