@@ -396,7 +396,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
                                                                                          ord_cur, resid, pred, trees_d);
       else
-        leaf_cta_kernel<<<dim3(static_cast<unsigned>(slots), F), 256, 0, s>>>(fam_d, F, st_d, nodes, slots, ord_cur,
+        leaf_cta_kernel<<<dim3(static_cast<unsigned>(slots), F), kLeafThreads, 0, s>>>(fam_d, F, st_d, nodes, slots, ord_cur,
                                                                                resid, pred, trees_d);
     }
     mse_partial_kernel<<<dim3(static_cast<unsigned>(mse_blocks), F), 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred,

@@ -1053,6 +1053,8 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 }
 
 
+constexpr int kSpecMulti = 16384;  // cta_fold_spec: chains from this length fold in four segments (three speculated)
+constexpr int kSpecRed = 200;      // cta_fold_spec's shared scratch (doubles)
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
   s = fs_add(a, b);
   const double bb = fs_sub(s, a);
@@ -1114,84 +1116,110 @@ __device__ __forceinline__ double warp_fold_gather_from(const double* __restrict
 }
 
 __device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
-                                                double* red /* smem [66]: per-warp hi / lo (up to 32 warps), S_m, result */) {
+                                                double* red /* smem [kSpecRed] */) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = static_cast<int>(blockDim.x >> 5);
   if (n < 4096 || nw < 2) {  // short chain: warp 0 folds it
     if (warp == 0) {
       const double r = warp_fold_gather_from(v, idx, n, 0.0);
-      if (lane == 0) red[64] = r;
+      if (lane == 0) red[196] = r;
     }
     __syncthreads();
-    const double r = red[64];
+    const double r = red[196];
     __syncthreads();
     return r;
   }
-  const int m = n >> 1;
-  // exact-prefix estimate of x_0..x_{m-1}: double-double partial sums (8 gathers in flight)
-  double hi = 0.0, lo = 0.0;
-  for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
-    double a[8];
+  // G speculative segments after the first: 3 for long chains in CTAs of >= 16 warps, else 1.
+  // Segment g = [b(g), b(g+1)), b(g) = g*n/(G+1); warp 0 folds segment 0 from 0.0, the other
+  // warps are split into G groups and group g folds segment g from the candidate starts
+  // P_g + k ulp around the double-double estimate P_g of the exact prefix up to b(g).
+  const int G = (n >= kSpecMulti && nw >= 16) ? 3 : 1;
+  const int K = G + 1;
+  auto bnd = [&](int g) { return static_cast<int>((static_cast<long long>(g) * n) / K); };
+  // 1. double-double sums of segments 0..G-1 (8 gathers in flight), per-warp partials to smem
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = i0 + k * blockDim.x;
-      a[k] = i < m ? v[idx[i]] : 0.0;
+  for (int g = 0; g < 3; ++g) {
+    if (g >= G) break;
+    double hi = 0.0, lo = 0.0;
+    const int a = bnd(g), e = bnd(g + 1);
+    for (int i0 = a + tid; i0 < e; i0 += 8 * blockDim.x) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * blockDim.x;
+        x[k] = i < e ? v[idx[i]] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        double s, err;
+        two_sum(hi, x[k], s, err);
+        hi = s;
+        lo = fs_add(lo, err);
+      }
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      double s, e;
-      two_sum(hi, a[k], s, e);
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+      double s, err;
+      two_sum(hi, oh, s, err);
       hi = s;
-      lo = fs_add(lo, e);
+      lo = fs_add(fs_add(lo, ol), err);
+    }
+    if (lane == 0) {
+      red[64 * g + warp] = hi;
+      red[64 * g + 32 + warp] = lo;
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
-    double s, e;
-    two_sum(hi, oh, s, e);
-    hi = s;
-    lo = fs_add(fs_add(lo, ol), e);
-  }
-  if (lane == 0) {
-    red[warp] = hi;
-    red[32 + warp] = lo;
-  }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {  // prefix estimates P_1..P_G
     double h = 0.0, l = 0.0;
-    for (int w = 0; w < nw; ++w) {
-      double s, e;
-      two_sum(h, red[w], s, e);
-      h = s;
-      l = fs_add(fs_add(l, red[32 + w]), e);
+    for (int g = 0; g < G; ++g) {
+      for (int w = 0; w < nw; ++w) {
+        double s, err;
+        two_sum(h, red[64 * g + w], s, err);
+        h = s;
+        l = fs_add(fs_add(l, red[64 * g + 32 + w]), err);
+      }
+      red[192 + g] = fs_add(h, l);
     }
-    red[65] = fs_add(h, l);
   }
   __syncthreads();
-  const double P = red[65];
-  // warp 0 folds the first half from 0.0 (the true S_m); warps 1.. fold the second half from
-  // the candidate starts P + k ulp, k centred on 0 (32 * (nw - 1) candidates)
-  const int cand = tid - 32;  // 0 .. 32*(nw-1)-1
-  const double start = warp == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (cand - 16 * (nw - 1)));
-  const double r = warp == 0 ? warp_fold_gather_from(v, idx, m, 0.0)
-                             : warp_fold_gather_from(v, idx + m, n - m, start);
+  // 2. every chain at once: warp 0 from 0.0, group g's threads from P_g + (c - C/2) ulp
+  const int grp = warp == 0 ? 0 : 1 + ((warp - 1) * G) / (nw - 1);
+  int wfirst = 1;
+  while (wfirst < nw && 1 + ((wfirst - 1) * G) / (nw - 1) < grp) ++wfirst;
+  int wlast = wfirst;
+  while (wlast + 1 < nw && 1 + (wlast * G) / (nw - 1) == grp) ++wlast;
+  const int C = 32 * (wlast - wfirst + 1);
+  const double start = grp == 0 ? 0.0 : ord_dbl(dbl_ord(red[192 + grp - 1]) + (tid - 32 * wfirst - C / 2));
+  const int a = bnd(grp), e = bnd(grp + 1);
+  const double r = warp_fold_gather_from(v, idx + a, e - a, start);
   __shared__ int hit;
-  if (tid == 0) {
-    red[64] = r;  // S_m
-    hit = 0;
-  }
+  if (tid == 0) red[196] = r;  // S_1, the true prefix at b(1)
   __syncthreads();
-  if (warp > 0 && __double_as_longlong(start) == __double_as_longlong(red[64])) {
-    red[65] = r;
-    hit = 1;
+  // 3. resolve segment by segment: the thread whose start is bit-identical to the true prefix
+  // holds the next true prefix; a miss finishes the chain sequentially from the true prefix
+  for (int g = 1; g <= G; ++g) {
+    if (tid == 0) hit = 0;
+    __syncthreads();
+    if (grp == g && __double_as_longlong(start) == __double_as_longlong(red[196])) {
+      red[197] = r;
+      hit = 1;
+    }
+    __syncthreads();
+    if (!hit) {
+      if (warp == 0) {
+        const double t = warp_fold_gather_from(v, idx + bnd(g), n - bnd(g), red[196]);
+        if (lane == 0) red[197] = t;
+      }
+      __syncthreads();
+      if (tid == 0) red[196] = red[197];
+      __syncthreads();
+      break;
+    }
+    if (tid == 0) red[196] = red[197];
+    __syncthreads();
   }
-  __syncthreads();
-  if (!hit && warp == 0) {  // speculation missed: finish from the true midpoint
-    const double t = warp_fold_gather_from(v, idx + m, n - m, red[64]);
-    if (lane == 0) red[65] = t;
-  }
-  __syncthreads();
-  const double out = red[65];
+  const double out = red[196];
   __syncthreads();
   return out;
 }
@@ -1223,7 +1251,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     int32_t* __restrict__ scratch, int n_max) {
   __shared__ SortSmem sm;
   __shared__ int wsum[32];
-  __shared__ double red[66];
+  __shared__ double red[kSpecRed];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = *n_items;
   sort_smem_init(sm);
@@ -1590,14 +1618,15 @@ __global__ void __launch_bounds__(1024) partition_kernel(
   }
 }
 
+constexpr int kLeafThreads = 256;  // leaf CTA (1,024 threads with four speculated segments measured slower: C5 leaves 0.59 -> 0.82 s)
 // Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
 // the leaf's order-0 segment / n (cta_fold_spec), then pred += lr*value over its rows.
-__global__ void __launch_bounds__(256) leaf_cta_kernel(const FamDesc* __restrict__ fam, int F,
+__global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* __restrict__ fam, int F,
                                                        const FamState* __restrict__ st, NodeRec* __restrict__ nodes,
                                                        int slots, const int32_t* __restrict__ ord_cur,
                                                        const double* __restrict__ resid, double* __restrict__ pred,
                                                        TreeRec* __restrict__ trees) {
-  __shared__ double red[66];
+  __shared__ double red[kSpecRed];
   const int f = blockIdx.y, s = blockIdx.x;
   if (f >= F) return;
   const FamDesc fd = fam[f];
