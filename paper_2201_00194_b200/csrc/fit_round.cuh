@@ -325,6 +325,7 @@ constexpr int kAtomTile = 128;
 constexpr int kAtomPre = 2;  // uint4 of the next tile's code rows held in registers per thread (kPipe)
 constexpr int kAtomCofRegs = 8;  // lane column offsets kept in registers (nrep <= 256)
 constexpr int kAtomPipeChunk = 8 * kAtomTile;  // rows per CTA from which the pipelined shape is used
+constexpr int kAtomPipeTile = 224;  // pipelined shape: rows per tile (fewer barriers; 224 x 9 uint4 fit 2 per thread)
 constexpr uint32_t kLimbMask = (1u << 21) - 1u;
 
 // kPipe: one CTA per SM (64 registers per thread) holding the next tile's gathers in registers
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
     for (int i = tid; i < 3 * colh * 32; i += kAtomThreads) limb[i] = 0;
     __syncthreads();
     const int sub_end = min(rows, sub0 + kAtomSub);
-    const bool pipe = kPipe && kAtomTile * vec_per_row <= kAtomPre * kAtomThreads;
+    const bool pipe = kPipe && kAtomPipeTile * vec_per_row <= kAtomPre * kAtomThreads;
     if (pipe) {
       // Software pipeline, one barrier per tile: registers hold tile t+1's gathered code rows
       // (and residual); they go to the other tile buffer, tile t+2's gathers are issued into the
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
       int64_t pfix = 0;
 #define FS_ATOM_PREFETCH(T0)                                                        \
   do {                                                                              \
-    const int tr_ = min(kAtomTile, sub_end - (T0));                                 \
+    const int tr_ = min(kAtomPipeTile, sub_end - (T0));                                 \
     _Pragma("unroll") for (int q = 0; q < kAtomPre; ++q) {                          \
       const int i = tid + q * kAtomThreads;                                         \
       if (i < tr_ * vec_per_row) {                                                  \
@@ -471,9 +472,9 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
       // the registers' tile into buffer b (codes, limbs, |v| into s_abs)
 #define FS_ATOM_STAGE(T0, B)                                                                        \
   do {                                                                                              \
-    const int tr_ = min(kAtomTile, sub_end - (T0));                                                 \
-    CodeT* tc_ = t_codes + (B) * (kAtomTile * Dp + 12 * kAtomTile / static_cast<int>(sizeof(CodeT)));  \
-    uint32_t* tl_ = reinterpret_cast<uint32_t*>(tc_ + kAtomTile * Dp);                              \
+    const int tr_ = min(kAtomPipeTile, sub_end - (T0));                                                 \
+    CodeT* tc_ = t_codes + (B) * (kAtomPipeTile * Dp + 12 * kAtomPipeTile / static_cast<int>(sizeof(CodeT)));  \
+    uint32_t* tl_ = reinterpret_cast<uint32_t*>(tc_ + kAtomPipeTile * Dp);                              \
     _Pragma("unroll") for (int q = 0; q < kAtomPre; ++q) {                                          \
       const int i = tid + q * kAtomThreads;                                                         \
       if (i < tr_ * vec_per_row) {                                                                  \
@@ -496,17 +497,17 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
   } while (0)
       FS_ATOM_PREFETCH(sub0);
       FS_ATOM_STAGE(sub0, 0);
-      if (sub0 + kAtomTile < sub_end) FS_ATOM_PREFETCH(sub0 + kAtomTile);
+      if (sub0 + kAtomPipeTile < sub_end) FS_ATOM_PREFETCH(sub0 + kAtomPipeTile);
       __syncthreads();
       int buf = 0;
-      for (int t0 = sub0; t0 < sub_end; t0 += kAtomTile) {
-        const int tr = min(kAtomTile, sub_end - t0);
-        if (t0 + kAtomTile < sub_end) {
-          FS_ATOM_STAGE(t0 + kAtomTile, buf ^ 1);
-          if (t0 + 2 * kAtomTile < sub_end) FS_ATOM_PREFETCH(t0 + 2 * kAtomTile);
+      for (int t0 = sub0; t0 < sub_end; t0 += kAtomPipeTile) {
+        const int tr = min(kAtomPipeTile, sub_end - t0);
+        if (t0 + kAtomPipeTile < sub_end) {
+          FS_ATOM_STAGE(t0 + kAtomPipeTile, buf ^ 1);
+          if (t0 + 2 * kAtomPipeTile < sub_end) FS_ATOM_PREFETCH(t0 + 2 * kAtomPipeTile);
         }
-        const CodeT* tc = t_codes + buf * (kAtomTile * Dp + 12 * kAtomTile / static_cast<int>(sizeof(CodeT)));
-        add_rows(tc, reinterpret_cast<const uint32_t*>(tc + kAtomTile * Dp), tr);
+        const CodeT* tc = t_codes + buf * (kAtomPipeTile * Dp + 12 * kAtomPipeTile / static_cast<int>(sizeof(CodeT)));
+        add_rows(tc, reinterpret_cast<const uint32_t*>(tc + kAtomPipeTile * Dp), tr);
         __syncthreads();
         buf ^= 1;
       }
@@ -577,7 +578,8 @@ inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes, int c
   size_t o = (static_cast<size_t>(3) * colh * 32 * 4 + 15) & ~size_t(15);
   o += static_cast<size_t>(bins) * 14 + static_cast<size_t>(nrep) * 12 + 16;
   o = (o + 15) & ~size_t(15);
-  o += 2 * (static_cast<size_t>(kAtomTile) * Dp * code_bytes + static_cast<size_t>(kAtomTile) * 12) + 16;  // 2 tiles
+  const size_t tile = static_cast<size_t>(std::max(kAtomTile, kAtomPipeTile));
+  o += 2 * (tile * Dp * code_bytes + tile * 12) + 16;  // 2 tiles
   return o;
 }
 
