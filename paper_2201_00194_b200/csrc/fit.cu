@@ -286,6 +286,9 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   const int mse_blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(n_max, kMseRows)));
   double* mse_part = ar.alloc<double>(static_cast<size_t>(F) * mse_blocks);
   const bool fork_totals = std::getenv("FAMSEER_FORK_TOTALS") != nullptr;
+  // chunked partition: left-row count per (family, node at level, 1,024-row chunk)
+  const int part_chunks = static_cast<int>(std::max<int64_t>(1, ceil_div(n_max, kPartChunk)));
+  int32_t* part_cnt = ar.alloc<int32_t>(static_cast<size_t>(F) * level_slots_max * part_chunks);
   // small-node exact folds (exact_small_kernel): per-CTA scratch of two n_max index buffers
   int32_t* small_scratch = std::getenv("FAMSEER_EXACT_SCAN")
                                ? nullptr
@@ -383,9 +386,23 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                                                            std::max(nrep_max, 1), level_slots_max, lbuf);
       {
         ProfScope prof(dev, "fit_partition");
-        partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
-                                                              scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle, ord,
-                                                              canon, x_d, d, trees_d, slots);
+        // few large nodes (C4): a CTA per (node, 1,024-row chunk), two passes; many nodes (C5):
+        // a CTA per node walking its tiles with the next tile's gathers in flight
+        const int64_t p_items = static_cast<int64_t>(F) * lw * part_chunks;
+        if (static_cast<int64_t>(F) * lw * 4 < sm) {
+          const dim3 pg(static_cast<unsigned>(p_items));
+          partition_count_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
+                                                                   scratch, nodeid, rep_orig_d, rep_boff_d, vals_d,
+                                                                   cle, ord, canon, x_d, d, trees_d, slots, part_cnt,
+                                                                   part_chunks, level_slots_max, F);
+          partition_scatter_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
+                                                                     scratch, nodeid, part_cnt, part_chunks,
+                                                                     level_slots_max, F);
+        } else {
+          partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
+                                                                scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle,
+                                                                ord, canon, x_d, d, trees_d, slots);
+        }
       }
       dev->count_launch(10);
     }

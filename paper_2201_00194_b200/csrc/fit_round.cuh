@@ -1620,6 +1620,151 @@ __global__ void __launch_bounds__(1024) partition_kernel(
   }
 }
 
+// Chunked stable partition (costmodel.cpp:94-105 for list 0) for few large nodes (C4): a CTA per
+// (node, 1,024-row chunk) - launched with one CTA per (family, node, chunk) item (the loop then
+// runs once; it also serves a persistent grid). Pass 1 counts each chunk's left rows (and copies the chunk's order-0
+// entries to scratch); pass 2 offsets each chunk by its predecessors' counts and scatters with a
+// block scan - so a 65,536-row root partitions with 64 CTAs instead of one walking 64 tiles.
+constexpr int kPartChunk = 1024;
+
+template <typename CodeT>
+__global__ void __launch_bounds__(kPartChunk) partition_count_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level,
+    int Dp, const CodeT* __restrict__ codes_c, const int32_t* __restrict__ ord_cur, int32_t* __restrict__ scratch,
+    const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_boff,
+    const double* __restrict__ vals, const int32_t* __restrict__ cle, const int32_t* __restrict__ ord,
+    const int32_t* __restrict__ canon, const double* __restrict__ x, int d, TreeRec* __restrict__ trees, int slots,
+    int32_t* __restrict__ part_cnt, int chunks_max, int level_slots_max, int F) {
+  __shared__ int wsum[32];
+  const int nl = 1 << level;
+  const int64_t items = static_cast<int64_t>(F) * nl * chunks_max;  // (family, node, chunk)
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+  const int f = static_cast<int>(w / (static_cast<int64_t>(nl) * chunks_max));
+  const int local = static_cast<int>((w / chunks_max) % nl);
+  const int c = static_cast<int>(w % chunks_max);
+  const FamDesc fd = fam[f];
+  if (!st[f].active) continue;
+  const int s = nl - 1 + local;
+  const NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeSplit) continue;
+  const int r0 = c * kPartChunk;
+  const int jj = nd.rep, bin = nd.bin, n = nd.n, seg = nd.seg, lc = nd.lc;
+  if (r0 >= nd.n) continue;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // (before any row moves: the -0.0 threshold lookup reads the parent's node ids)
+  if (c == 0 && tid == 0) {  // exact threshold, tree record, child records
+    const int orig = rep_orig[fd.rep0 + jj];
+    double thr = vals[fd.bin0 + rep_boff[fd.rep0 + jj] + bin];
+    if (thr == 0.0 && fd.negz) {  // +0.0 and -0.0 share a bin: take the last left element's own value
+      const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
+      for (int i = cle[fd.bin0 + rep_boff[fd.rep0 + jj] + bin] - 1; i >= 0; --i) {
+        if (nodeid[fd.pos0 + L[i]] == s) {
+          thr = x[(fd.row0 + canon[fd.pos0 + L[i]]) * d + orig];
+          break;
+        }
+      }
+    }
+    TreeRec r;
+    r.kind = kNodeSplit;
+    r.feature = orig;
+    r.threshold = thr;
+    r.value = 0.0;
+    r.gain = nd.gain;
+    r.rep = jj;
+    r.bin = bin;
+    trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = r;
+    NodeRec& a = nodes[fd.node0 + 2 * s + 1];
+    NodeRec& b = nodes[fd.node0 + 2 * s + 2];
+    a.n = lc;
+    a.seg = seg;
+    b.n = n - lc;
+    b.seg = seg + lc;
+  }
+
+  const int i = r0 + tid;
+  bool left = false;
+  if (i < nd.n) {
+    const int p = ord_cur[fd.pos0 + nd.seg + i];
+    scratch[fd.pos0 + nd.seg + i] = p;
+    left = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + nd.rep]) <= nd.bin;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, left);
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) part_cnt[(static_cast<int64_t>(f) * level_slots_max + local) * chunks_max + c] = v;
+  }
+  __syncthreads();  // wsum is reused by the next item
+  }
+}
+
+template <typename CodeT>
+__global__ void __launch_bounds__(kPartChunk) partition_scatter_kernel(
+    const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level, int Dp,
+    const CodeT* __restrict__ codes_c, int32_t* __restrict__ ord_cur, const int32_t* __restrict__ scratch,
+    int16_t* __restrict__ nodeid, const int32_t* __restrict__ part_cnt, int chunks_max, int level_slots_max, int F) {
+  __shared__ int wsum[32];
+  __shared__ int s_off;
+  const int nl = 1 << level;
+  const int64_t items = static_cast<int64_t>(F) * nl * chunks_max;  // (family, node, chunk)
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+  const int f = static_cast<int>(w / (static_cast<int64_t>(nl) * chunks_max));
+  const int local = static_cast<int>((w / chunks_max) % nl);
+  const int c = static_cast<int>(w % chunks_max);
+  const FamDesc fd = fam[f];
+  if (!st[f].active) continue;
+  const int s = nl - 1 + local;
+  NodeRec& nd = nodes[fd.node0 + s];
+  if (nd.state != kNodeSplit) continue;
+  const int r0 = c * kPartChunk;
+  const int jj = nd.rep, bin = nd.bin, n = nd.n, seg = nd.seg, lc = nd.lc;
+  if (r0 >= n) continue;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) {  // left rows of the preceding chunks
+    const int32_t* cnt = part_cnt + (static_cast<int64_t>(f) * level_slots_max + local) * chunks_max;
+    int v = 0;
+    for (int k = lane; k < c; k += 32) v += cnt[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s_off = v;
+  }
+  const int i = r0 + tid;
+  int p = 0;
+  bool left = false;
+  if (i < n) {
+    p = scratch[fd.pos0 + seg + i];
+    left = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + jj]) <= bin;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, left);
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    wsum[lane] = incl - v;
+  }
+  __syncthreads();
+  if (i < n) {
+    const int lrank = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+    int32_t* dst = ord_cur + fd.pos0 + seg;
+    const int off_l = s_off, off_r = r0 - s_off;
+    if (left) {
+      dst[off_l + lrank] = p;
+      nodeid[fd.pos0 + p] = static_cast<int16_t>(2 * s + 1);
+    } else {
+      dst[lc + off_r + (i - r0) - lrank] = p;
+      nodeid[fd.pos0 + p] = static_cast<int16_t>(2 * s + 2);
+    }
+  }
+  __syncthreads();  // wsum / s_off are reused by the next item
+  }
+}
+
 constexpr int kLeafThreads = 256;  // leaf CTA (1,024 threads with four speculated segments measured slower: C5 leaves 0.59 -> 0.82 s)
 // Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
 // the leaf's order-0 segment / n (cta_fold_spec), then pred += lr*value over its rows.
