@@ -912,15 +912,42 @@ __global__ void __launch_bounds__(256) tieclass_phi_kernel(
     __syncthreads();  // previous item done with phi
     for (int a = tid; a < nb; a += blockDim.x) phi[a] = 0xFFFFu;
     __syncthreads();
-    for (int i = tid; i < nv; i += blockDim.x) {
-      const int64_t p = rows[i];
-      phi[cb[p * Dp + f0]] = static_cast<uint16_t>(cb[p * Dp + g]);
+    // 8 rows per thread in flight (index gathers, then both code gathers, then the table)
+    for (int i0 = tid; i0 < nv; i0 += 8 * blockDim.x) {
+      int64_t p[8];
+      int cf[8], cg[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * static_cast<int>(blockDim.x);
+        p[k] = i < nv ? rows[i] : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        cf[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + f0]) : 0;
+        cg[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + g]) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (p[k] >= 0) phi[cf[k]] = static_cast<uint16_t>(cg[k]);
     }
     __syncthreads();
     bool bad = false;
-    for (int i = tid; i < nv; i += blockDim.x) {
-      const int64_t p = rows[i];
-      bad |= phi[cb[p * Dp + f0]] != static_cast<uint16_t>(cb[p * Dp + g]);
+    for (int i0 = tid; i0 < nv; i0 += 8 * blockDim.x) {
+      int64_t p[8];
+      int cf[8], cg[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * static_cast<int>(blockDim.x);
+        p[k] = i < nv ? rows[i] : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        cf[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + f0]) : 0;
+        cg[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + g]) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (p[k] >= 0) bad |= phi[cf[k]] != static_cast<uint16_t>(cg[k]);
     }
     if (tid < 32) {  // phi strictly increasing over the present f0 codes
       int carry = -1;
