@@ -1312,26 +1312,38 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     }
     int32_t* A = scratch + static_cast<int64_t>(blockIdx.x) * 2 * n_max;
     int32_t* B = A + n_max;
-    // 1. the node's rows in canonical order
+    // 1. the node's rows in canonical order: each thread tests 8 consecutive rows per pass (8x
+    // fewer block scans than one row per thread), then a block scan of the per-thread counts
     int base = 0;
-    for (int p0 = 0; p0 < n; p0 += blockDim.x) {
-      const int p = p0 + tid;
-      const bool mem = p < n && nodeid[fd.pos0 + p] == it.slot;
-      const unsigned m = __ballot_sync(0xffffffffu, mem);
-      if (lane == 0) wsum[warp] = __popc(m);
+    for (int p0 = 0; p0 < n; p0 += 8 * static_cast<int>(blockDim.x)) {
+      const int pb = p0 + 8 * tid;
+      unsigned bits = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (pb + k < n && nodeid[fd.pos0 + pb + k] == it.slot) bits |= 1u << k;
+      const int cnt = __popc(bits);
+      int incl = cnt;  // warp inclusive scan of the per-thread counts
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wsum[warp] = incl;
       __syncthreads();
       if (warp == 0) {
         const int v = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
-        int incl = v;
+        int wi = v;
         for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
+          const int t = __shfl_up_sync(0xffffffffu, wi, o);
+          if (lane >= o) wi += t;
         }
-        wsum[lane] = incl - v;
-        if (lane == 31) sm.uniform = incl;  // chunk total (borrowed field)
+        wsum[lane] = wi - v;
+        if (lane == 31) sm.uniform = wi;  // pass total (borrowed field)
       }
       __syncthreads();
-      if (mem) A[base + wsum[warp] + __popc(m & ((1u << lane) - 1u))] = p;
+      int dst = base + wsum[warp] + incl - cnt;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (bits >> k & 1u) A[dst++] = pb + k;
       base += sm.uniform;
       __syncthreads();
     }
