@@ -212,7 +212,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = cl > 1 ? 1 : 0;  // no cluster attribute for one CTA per family
       FS_CUDA(cudaLaunchKernelEx(&cfg, fit_resident_kernel, static_cast<const FamDesc*>(fam_d), st_d,
                                  static_cast<const int*>(list_d), Dp, reinterpret_cast<const uint8_t*>(codes_c),
                                  static_cast<const double*>(target_c), static_cast<const double*>(base_d),
