@@ -196,8 +196,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   // ---- resident path: every family fits one CTA's shared memory -> one launch, all rounds ----
   if (std::is_same<CodeT, uint8_t>::value && resident.enabled) {
     int* list_d = ar.upload(resident.families);
-    FS_CUDA(cudaFuncSetAttribute(fit_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(resident.smem)));
+    auto* kfn = resident.cluster > 1 ? fit_resident_kernel<true> : fit_resident_kernel<false>;
+    FS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(resident.smem)));
     {
       ProfScope prof(dev, "fit_resident");
       const int cl = resident.cluster;
@@ -213,7 +213,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = cl > 1 ? 1 : 0;  // no cluster attribute for one CTA per family
-      FS_CUDA(cudaLaunchKernelEx(&cfg, fit_resident_kernel, static_cast<const FamDesc*>(fam_d), st_d,
+      FS_CUDA(cudaLaunchKernelEx(&cfg, kfn, static_cast<const FamDesc*>(fam_d), st_d,
                                  static_cast<const int*>(list_d), Dp, reinterpret_cast<const uint8_t*>(codes_c),
                                  static_cast<const double*>(target_c), static_cast<const double*>(base_d),
                                  static_cast<const int32_t*>(ord), static_cast<const int32_t*>(ord_root),

@@ -203,6 +203,9 @@ __device__ __forceinline__ double fold_spec(const double* __restrict__ v, const 
 
 
 
+// kClu: launched as a thread-block cluster (several CTAs per family); false compiles the
+// single-CTA shape without any cluster arithmetic.
+template <bool kClu>
 __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const FamDesc* __restrict__ fam, FamState* __restrict__ st, const int* __restrict__ fam_list, int Dp,
     const uint8_t* __restrict__ codes_c, const double* __restrict__ target_c, const double* __restrict__ base,
@@ -218,8 +221,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   // the CTAs pull each other's bins through distributed shared memory. Only CTA rank 0 writes
   // global results.
   cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
-  const int cl_n = static_cast<int>(cluster.num_blocks());
-  const int cl_r = static_cast<int>(cluster.block_rank());
+  const int cl_n = kClu ? static_cast<int>(cluster.num_blocks()) : 1;
+  const int cl_r = kClu ? static_cast<int>(cluster.block_rank()) : 0;
   const bool lead = cl_r == 0;
   __shared__ unsigned long long s_red[32];
   __shared__ double s_dred[32];
