@@ -1082,7 +1082,7 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 }
 
 
-constexpr int kSpecMulti = 16384;  // cta_fold_spec: chains from this length fold in four segments (three speculated)
+constexpr int kSpecMulti = 8192;  // cta_fold_spec: chains from this length fold in four segments (three speculated)
 constexpr int kSpecRed = 200;      // cta_fold_spec's shared scratch (doubles)
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
   s = fs_add(a, b);
@@ -1162,7 +1162,7 @@ __device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, co
   // Segment g = [b(g), b(g+1)), b(g) = g*n/(G+1); warp 0 folds segment 0 from 0.0, the other
   // warps are split into G groups and group g folds segment g from the candidate starts
   // P_g + k ulp around the double-double estimate P_g of the exact prefix up to b(g).
-  const int G = (n >= kSpecMulti && nw >= 16) ? 3 : 1;
+  const int G = (n >= kSpecMulti && nw >= 4) ? 3 : 1;
   const int K = G + 1;
   auto bnd = [&](int g) { return static_cast<int>((static_cast<long long>(g) * n) / K); };
   // 1. double-double sums of segments 0..G-1 (8 gathers in flight), per-warp partials to smem
