@@ -114,13 +114,15 @@ int fs_forest_export(const fs_forest* fo, int32_t family, double* base, int32_t*
 
 /* ---- predict (costmodel.cpp:135-143, 237-246) ------------------------------------------------
  * Rows [seg[f], seg[f+1]) are scored with family f's ensemble: score = base, then for every tree
- * in order score = score + lr*leaf (separately rounded, no FMA). leaf_ids (optional, uint8
- * [rows][n_trees_of_family], pre-order node index) is written row-major per segment at
- * leaf_offset[f] (bytes). Non-finite features -> FS_EINVAL. */
+ * in order score = score + lr*leaf (separately rounded, no FMA). leaf_ids (optional, uint16
+ * [rows][n_trees_of_family]: the tree-local pre-order index of the leaf RegressionTree::eval
+ * stops at) is written row-major, segment after segment (segment f starts at element
+ * sum_{g<f} rows_g * n_trees_g). A tree of more than 65,536 nodes cannot report leaf ids
+ * (FS_EINVAL). Non-finite features -> FS_EINVAL. */
 int fs_predict(fs_device* dev, const fs_forest* fo, int32_t n_segments, const int64_t* seg,
-               int32_t d, const double* x, double* scores, uint8_t* leaf_ids);
+               int32_t d, const double* x, double* scores, uint16_t* leaf_ids);
 int fs_predict_d(fs_device* dev, const fs_forest* fo, int32_t n_segments, const int64_t* seg_h,
-                 int32_t d, const double* x_d, double* scores_d, uint8_t* leaf_ids_d);
+                 int32_t d, const double* x_d, double* scores_d, uint16_t* leaf_ids_d);
 
 /* ---- rank (scheduler.cpp:187-192) ------------------------------------------------------------
  * perm[seg[f] + i] = segment-local index of the i-th smallest (score, index) pair: the order

@@ -25,6 +25,7 @@ _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
 _u64p = C.POINTER(C.c_uint64)
 _u8p = C.POINTER(C.c_uint8)
+_u16p = C.POINTER(C.c_uint16)
 
 
 def _p(a, t):
@@ -100,7 +101,7 @@ class _Orc:
         L.orc_last_error.restype = C.c_char_p
         L.orc_featurize.argtypes = [C.c_int, _i32p, _i64p, _i32p, C.c_int64, C.c_int, C.c_int, _dp]
         L.orc_predict.argtypes = [C.c_double, C.c_double, C.c_int, _i32p, _i32p, _dp, _i32p, _i32p, _dp,
-                                  C.c_int64, C.c_int, _dp, _dp, _u8p]
+                                  C.c_int64, C.c_int, _dp, _dp, _u16p]
         L.orc_rank.argtypes = [C.c_int64, _dp, _i64p]
         L.orc_fit.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_double, C.c_int, _dp,
                               C.POINTER(C.c_int), _i32p, _i32p, _dp, _i32p, _i32p, _dp, _dp, _dp, C.c_int64]
@@ -131,11 +132,11 @@ class _Orc:
         if x.ndim == 1:
             x = x[None]
         out = np.zeros(x.shape[0])
-        lo = np.zeros((x.shape[0], max(ens.n_trees, 1)), np.uint8) if leaves else None
+        lo = np.zeros((x.shape[0], max(ens.n_trees, 1)), np.uint16) if leaves else None
         self._chk(self.L.orc_predict(ens.base, ens.lr, ens.n_trees, _p(ens.offsets, _i32p),
                                      _p(ens.feature, _i32p), _p(ens.threshold, _dp), _p(ens.left, _i32p),
                                      _p(ens.right, _i32p), _p(ens.value, _dp), x.shape[0], x.shape[1],
-                                     _p(x, _dp), _p(out, _dp), _p(lo, _u8p)))
+                                     _p(x, _dp), _p(out, _dp), _p(lo, _u16p)))
         return (out, lo[:, : ens.n_trees]) if leaves else out
 
     def rank(self, scores):

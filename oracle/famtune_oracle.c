@@ -58,7 +58,7 @@ int orc_featurize(int k, const int32_t* nvals, const int64_t* values, const int3
 int orc_predict(double base, double lr, int n_trees, const int32_t* offsets,
                 const int32_t* feature, const double* threshold, const int32_t* left,
                 const int32_t* right, const double* value, int64_t p, int d, const double* x,
-                double* out, uint8_t* leaf_out) {
+                double* out, uint16_t* leaf_out) {
   for (int64_t c = 0; c < p; ++c) {
     const double* row = x + c * d;
     for (int j = 0; j < d; ++j)
@@ -68,7 +68,7 @@ int orc_predict(double base, double lr, int n_trees, const int32_t* offsets,
       const int32_t o = offsets[t];
       int idx = 0;
       while (feature[o + idx] >= 0) idx = row[feature[o + idx]] <= threshold[o + idx] ? left[o + idx] : right[o + idx];
-      if (leaf_out) leaf_out[c * n_trees + t] = (uint8_t)idx;
+      if (leaf_out) leaf_out[c * n_trees + t] = (uint16_t)idx;
       const double step = lr * value[o + idx];
       score = score + step;
     }

@@ -29,7 +29,7 @@ int orc_featurize(int k, const int32_t* nvals, const int64_t* values, const int3
 int orc_predict(double base, double lr, int n_trees, const int32_t* offsets,
                 const int32_t* feature, const double* threshold, const int32_t* left,
                 const int32_t* right, const double* value, int64_t p, int d, const double* x,
-                double* out, uint8_t* leaf_out);
+                double* out, uint16_t* leaf_out);
 
 int orc_rank(int64_t p, const double* scores, int64_t* perm);
 

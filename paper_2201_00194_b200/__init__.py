@@ -324,9 +324,9 @@ class Forest:
             total = 0
             for f in range(len(sg) - 1):
                 total += int(sg[f + 1] - sg[f]) * self.export_n_trees(f)
-            lo = np.zeros(max(total, 1), np.uint8)
+            lo = np.zeros(max(total, 1), np.uint16)
         _check(_lib().fs_predict(self.dev.h, self.h, len(sg) - 1, sp, x.shape[1], _p(x, _capi._dp),
-                                 _p(out, _capi._dp), _p(lo, _capi._u8p)))
+                                 _p(out, _capi._dp), _p(lo, _capi._u16p)))
         return (out, lo) if leaves else out
 
     def predict_d(self, x_t, seg, scores_t, leaves_t=None):

@@ -19,6 +19,7 @@ _dp = C.POINTER(C.c_double)
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
 _u8p = C.POINTER(C.c_uint8)
+_u16p = C.POINTER(C.c_uint16)
 _vp = C.c_void_p
 
 
@@ -70,7 +71,7 @@ SIGNATURES = [
                                    _i32p, _dp]),
     ("fs_forest_export", C.c_int, [_vp, C.c_int32, _dp, _i32p, _i32p, _i32p, _i32p, _dp, _i32p, _i32p, _dp, _dp,
                                    _dp]),
-    ("fs_predict", C.c_int, [_vp, _vp, C.c_int32, _i64p, C.c_int32, _dp, _dp, _u8p]),
+    ("fs_predict", C.c_int, [_vp, _vp, C.c_int32, _i64p, C.c_int32, _dp, _dp, _u16p]),
     ("fs_predict_d", C.c_int, [_vp, _vp, C.c_int32, _i64p, C.c_int32, _vp, _vp, _vp]),
     ("fs_rank", C.c_int, [_vp, C.c_int32, _i64p, _dp, _i32p]),
     ("fs_rank_d", C.c_int, [_vp, C.c_int32, _i64p, _vp, _vp]),

@@ -196,6 +196,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   // ---- resident path: every family fits one CTA's shared memory -> one launch, all rounds ----
   if (std::is_same<CodeT, uint8_t>::value && resident.enabled) {
     int* list_d = ar.upload(resident.families);
+    // every round's e = target - pred, [rounds][n] per family, for the exact MSE fold afterwards
+    double* ebuf = ar.alloc<double>(static_cast<size_t>(n_tot) * std::max(max_trees, 1));
     auto* kfn = resident.cluster > 1 ? fit_resident_kernel<true> : fit_resident_kernel<false>;
     FS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(resident.smem)));
     {
@@ -219,11 +221,18 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                  static_cast<const int32_t*>(ord), static_cast<const int32_t*>(ord_root),
                                  rep_orig_d, rep_nb_d, rep_boff_d, static_cast<const double*>(vals_d),
                                  static_cast<const int32_t*>(cle), static_cast<const int32_t*>(canon), x_d, d, trees_d,
-                                 mse_d, max_trees, slots, dev->ctr_d, resident.pred_smem ? 1 : 0, pred,
+                                 ebuf, max_trees, slots, dev->ctr_d, resident.pred_smem ? 1 : 0, pred,
                                  resident.pre_smem ? 1 : 0, resident.spec_bufs));
     }
     dev->count_launch();
     FS_CUDA(cudaGetLastError());
+    if (max_trees > 0) {
+      const int64_t chains = static_cast<int64_t>(F) * max_trees;
+      mse_fold_kernel<<<static_cast<unsigned>(ceil_div(chains, 64)), 64, 0, s>>>(fam_d, st_d, F, ebuf, max_trees, 0, 0,
+                                                                                 max_trees, mse_d, max_trees);
+      dev->count_launch();
+      FS_CUDA(cudaGetLastError());
+    }
     return;
   }
 
@@ -283,8 +292,10 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   // lives on the device in FamState::ntrees), so it is captured once as a CUDA graph and replayed
   // max_trees times; families that stopped early skip their work inside the kernels.
   const int64_t l0 = dev->launches;
-  const int mse_blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(n_max, kMseRows)));
-  double* mse_part = ar.alloc<double>(static_cast<size_t>(F) * mse_blocks);
+  // train_mse_by_round: ring of K rounds of e = target - pred, folded every K rounds (mse_fold_kernel)
+  const int mse_k = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(std::min(max_trees, 64), (int64_t{1} << 30) / std::max<int64_t>(1, n_tot * 8))));
+  double* ebuf = ar.alloc<double>(static_cast<size_t>(mse_k) * n_tot);
   const bool fork_totals = std::getenv("FAMSEER_FORK_TOTALS") != nullptr;
   // chunked partition: left-row count per (family, node at level, 1,024-row chunk)
   const int part_chunks = static_cast<int>(std::max<int64_t>(1, ceil_div(n_max, kPartChunk)));
@@ -416,16 +427,29 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         leaf_cta_kernel<<<dim3(static_cast<unsigned>(slots), F), kLeafThreads, 0, s>>>(fam_d, F, st_d, nodes, slots, ord_cur,
                                                                                resid, pred, trees_d);
     }
-    mse_partial_kernel<<<dim3(static_cast<unsigned>(mse_blocks), F), 256, 0, s>>>(fam_d, st_d, nodes, target_c, pred,
-                                                                              mse_part, mse_blocks);
-    mse_final_kernel<<<F, 1, 0, s>>>(fam_d, st_d, nodes, mse_part, mse_blocks, mse_d, max_trees);
+    mse_stash_kernel<<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, st_d, nodes, rowfam, n_tot, target_c, pred,
+                                                                  ebuf, mse_k);
+    commit_kernel<<<static_cast<unsigned>(ceil_div(F, 128)), 128, 0, s>>>(fam_d, st_d, nodes, F);
     dev->count_launch();
     dev->count_launch(2);
     FS_CUDA(cudaGetLastError());
   };
+  // after round `round` (0-based): fold the ring once it is full or the fit is over
+  auto mse_fold = [&](int round) {
+    if ((round + 1) % mse_k != 0 && round + 1 != max_trees) return;
+    const int t_lo = (round / mse_k) * mse_k, t_hi = round + 1;
+    const int64_t chains = static_cast<int64_t>(F) * (t_hi - t_lo);
+    mse_fold_kernel<<<static_cast<unsigned>(ceil_div(chains, 64)), 64, 0, s>>>(fam_d, st_d, F, ebuf, mse_k, n_tot,
+                                                                               t_lo, t_hi, mse_d, max_trees);
+    dev->count_launch();
+    FS_CUDA(cudaGetLastError());
+  };
   if (max_trees <= 0) return;
   if (std::getenv("FAMSEER_NO_GRAPH") != nullptr) {
-    for (int round = 0; round < max_trees; ++round) round_body();
+    for (int round = 0; round < max_trees; ++round) {
+      round_body();
+      mse_fold(round);
+    }
     return;
   }
   cudaGraph_t graph = nullptr;
@@ -444,8 +468,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   dev->capturing = false;
   const int64_t per_round = dev->launches - l0;
   FS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-  for (int round = 0; round < max_trees; ++round) FS_CUDA(cudaGraphLaunch(exec, s));
-  dev->launches = l0 + per_round * max_trees;
+  const int64_t l1 = dev->launches;
+  for (int round = 0; round < max_trees; ++round) {
+    FS_CUDA(cudaGraphLaunch(exec, s));
+    mse_fold(round);
+  }
+  dev->launches = l0 + per_round * max_trees + (dev->launches - l1);
   FS_CUDA(cudaGraphExecDestroy(exec));
   FS_CUDA(cudaGraphDestroy(graph));
 }
@@ -642,7 +670,9 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
     const std::string mode = envp ? envp : "auto";
     if (mode != "auto" && mode != "resident" && mode != "multi")
       fail(FS_EINVAL, "FAMSEER_FIT_PATH must be auto, resident or multi");
-    if (mode != "multi" && code_bytes == 1 && depth_max <= kResMaxDepth) {
+    // (the resident fit keeps every round's residuals for the MSE fold: n_tot * trees doubles)
+    const bool ebuf_fits = static_cast<double>(seg[F]) * std::max(max_trees, 1) * 8.0 <= 2.0 * (1 << 30);
+    if (mode != "multi" && code_bytes == 1 && depth_max <= kResMaxDepth && ebuf_fits) {
       // Shared-memory staging options, most valuable first: the running predictions (read and
       // updated every round) and the presorted lists (reference-order folds); whatever does not
       // fit stays in global memory (L2-resident).
@@ -861,7 +891,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
       L.meta = put(sizeof(ModelMeta));
       L.nodes = put(static_cast<size_t>(T) * nint * 4);
       L.leafv = put(static_cast<size_t>(T) * nleaf * 8);
-      L.leafid = put(static_cast<size_t>(T) * nleaf);
+      L.leafid = put(static_cast<size_t>(T) * nleaf * 2);
       L.uthr = put(static_cast<size_t>(bins) * 8);
       L.uoff = put(static_cast<size_t>(nrep + 1) * 4);
       L.fmap = put(static_cast<size_t>(nrep) * 4);
@@ -898,7 +928,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
       m.n_trees = T;  // upper bound until materialised (the device meta holds the count)
       m.nodes_d = reinterpret_cast<uint32_t*>(m.blob_d + L.nodes);
       m.leafv_d = reinterpret_cast<double*>(m.blob_d + L.leafv);
-      m.leafid_d = m.blob_d + L.leafid;
+      m.leafid_d = reinterpret_cast<uint16_t*>(m.blob_d + L.leafid);
       m.uthr_d = reinterpret_cast<double*>(m.blob_d + L.uthr);
       m.uoff_d = reinterpret_cast<int32_t*>(m.blob_d + L.uoff);
       m.fmap_d = reinterpret_cast<const int32_t*>(m.blob_d + L.fmap);

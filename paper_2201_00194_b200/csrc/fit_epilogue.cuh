@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(128) export_compile_kernel(
   const uint32_t always_left = jb.code_wide ? 0xFFFFu : 0xFFu;
   uint32_t* nodes = reinterpret_cast<uint32_t*>(B + L.nodes);
   double* leafv = reinterpret_cast<double*>(B + L.leafv);
-  uint8_t* leafid = B + L.leafid;
+  uint16_t* leafid = reinterpret_cast<uint16_t*>(B + L.leafid);
   int32_t* cnt = reinterpret_cast<int32_t*>(B + L.cnt);
   int32_t* feat = reinterpret_cast<int32_t*>(B + L.feat);
   double* thr = reinterpret_cast<double*>(B + L.thr);
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(128) export_compile_kernel(
       int h = nint + q;  // deepest existing ancestor-or-self is the leaf covering this heap leaf
       while (h > 0 && rec[h].kind == 0) h = (h - 1) >> 1;
       leafv[static_cast<size_t>(t) * nleaf + q] = rec[h].value;
-      leafid[static_cast<size_t>(t) * nleaf + q] = static_cast<uint8_t>(pidx[h]);
+      leafid[static_cast<size_t>(t) * nleaf + q] = static_cast<uint16_t>(pidx[h]);
     }
   }
 }

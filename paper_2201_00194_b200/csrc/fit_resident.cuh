@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     const int32_t* __restrict__ ord, const int32_t* __restrict__ ord_root, const int32_t* __restrict__ rep_orig,
     const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ rep_boff, const double* __restrict__ vals,
     const int32_t* __restrict__ cle, const int32_t* __restrict__ canon, const double* __restrict__ x, int d,
-    TreeRec* __restrict__ trees, double* __restrict__ mse, int max_trees, int slots_g,
+    TreeRec* __restrict__ trees, double* __restrict__ ebuf, int max_trees, int slots_g,
     unsigned long long* __restrict__ ctr, int pred_smem, double* __restrict__ pred_g, int pre_smem, int spec_bufs) {
   extern __shared__ __align__(16) unsigned char sm[];
   // Optional thread-block cluster of cl_n CTAs per family (FAMSEER_RES_CLUSTER): every CTA holds
@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const int cl_r = kClu ? static_cast<int>(cluster.block_rank()) : 0;
   const bool lead = cl_r == 0;
   __shared__ unsigned long long s_red[32];
-  __shared__ double s_dred[32];
   __shared__ int s_wsum[32];
   __shared__ int s_shift, s_nitems, s_ctot;
   __shared__ unsigned long long s_cnt[3];  // screened splits, exact nodes, exact folds
@@ -1124,13 +1123,15 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     // its final leaf slot, all threads) fused with the MSE (:215-220); commit or early stop
     // (:212 - the update happens before the reference's stop test too)
     const bool stop = s_nodes[0].state == kNodeLeaf && s_nodes[0].value == 0.0;  // uniform (smem)
-    double a = 0.0;
+    // e of this round in the family's block of ebuf ([rounds][n] at pos0 * max_trees): the
+    // sequential MSE fold over canonical rows runs after the fit (mse_fold_kernel)
+    double* eb = ebuf + fd.pos0 * max_trees + static_cast<int64_t>(ntrees) * n;
     unsigned long long mx = 0;
     for (int p = tid; p < n; p += kResThreads) {
       const double pr = fs_add(s_pred[p], fs_mul(fd.lr, s_nodes[s_node[p]].value));
       s_pred[p] = pr;
       const double e = fs_sub(s_targ[p], pr);  // = the next round's residual (costmodel.cpp:204-206)
-      a = fs_add(a, fs_mul(e, e));
+      if (lead && !stop) eb[p] = e;
       s_resid[p] = e;
       mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(e))));
       s_node[p] = 0;
@@ -1140,14 +1141,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) s_red[warp] = mx;
     have_resid = true;
-    for (int o = 16; o > 0; o >>= 1) a = fs_add(a, __shfl_down_sync(0xffffffffu, a, o));
-    if (lane == 0) s_dred[warp] = a;
     __syncthreads();
-    if (tid == 0 && lead) {
-      double t = 0.0;
-      for (int w = 0; w < kResThreads / 32; ++w) t = fs_add(t, s_dred[w]);
-      mse[static_cast<int64_t>(f) * max_trees + ntrees] = fs_div(t, static_cast<double>(n));
-    }
     ++ntrees;
     __syncthreads();
       RES_PHASE(11);

@@ -1906,61 +1906,87 @@ __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamSta
   }
 }
 
-// Commit the round's tree or stop (costmodel.cpp:212), then MSE over canonical rows (:215-220).
-// The MSE is a fixed-order tree reduction: deterministic, within 1e-15 relative of the
-// reference's sequential fold (it never feeds back into the model).
-// MSE per round (costmodel.cpp:215-220; a fixed-order reduction - it never feeds back):
-// blocks of kMseRows rows per family produce partials (block tree reduction), mse_final_kernel
-// adds them in block order; it also commits the tree or applies the early stop (:212).
-constexpr int kMseRows = 2048;
+// Commit the round's tree or stop (costmodel.cpp:212), then train_mse_by_round (:215-220).
+// The reference folds e*e over the canonical rows sequentially, and so does mse_fold_kernel -
+// but off the round's critical path: every committed round stashes its e = target - pred (the
+// next round's residual) in a ring of K rounds, and every K rounds one launch folds all
+// (family, round) chains of the ring at once, one thread per chain, in canonical order.
 constexpr int kExactSmallCtas = 64;  // CTAs of exact_small_kernel (items loop over them)
 __device__ __forceinline__ bool round_commits(const FamDesc& fd, const FamState& st, const NodeRec* nodes) {
   if (!st.active) return false;
   const NodeRec& root = nodes[fd.node0];
   return !(root.state == kNodeLeaf && root.value == 0.0);
 }
-__global__ void mse_partial_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
-                                   const NodeRec* __restrict__ nodes, const double* __restrict__ target_c,
-                                   const double* __restrict__ pred, double* __restrict__ part, int max_blocks) {
-  __shared__ double red[256];
-  const int f = blockIdx.y;
-  const FamDesc fd = fam[f];
-  const int r0 = blockIdx.x * kMseRows;
-  if (r0 >= fd.n || !round_commits(fd, st[f], nodes)) return;
-  const int r1 = min(fd.n, r0 + kMseRows);
-  double a = 0.0;
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    const double e = fs_sub(target_c[fd.pos0 + i], pred[fd.pos0 + i]);
-    a = fs_add(a, fs_mul(e, e));
+// e of the committing round t = st.ntrees into ring slot t % K ([K][n_tot], canonical rows).
+__global__ void mse_stash_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                 const NodeRec* __restrict__ nodes, const int32_t* __restrict__ rowfam, int64_t n_tot,
+                                 const double* __restrict__ target_c, const double* __restrict__ pred,
+                                 double* __restrict__ ebuf, int K) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_tot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int f = rowfam[i];
+    const FamDesc& fd = fam[f];
+    if (!round_commits(fd, st[f], nodes)) continue;
+    ebuf[static_cast<int64_t>(st[f].ntrees % K) * n_tot + i] = fs_sub(target_c[i], pred[i]);
   }
-  red[threadIdx.x] = a;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] = fs_add(red[threadIdx.x], red[threadIdx.x + o]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[static_cast<int64_t>(f) * max_blocks + blockIdx.x] = red[0];
 }
-__global__ void mse_final_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
-                                 const NodeRec* __restrict__ nodes, const double* __restrict__ part, int max_blocks,
-                                 double* __restrict__ mse, int max_trees) {
+__global__ void commit_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
+                              const NodeRec* __restrict__ nodes, int F) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= gridDim.x * blockDim.x) return;
+  if (f >= F) return;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
   if (!round_commits(fd, st[f], nodes)) {
     st[f].active = 0;  // single leaf of value exactly 0: the reference stops boosting
     return;
   }
-  double a = 0.0;
-  const int nb = (fd.n + kMseRows - 1) / kMseRows;
-  for (int b = 0; b < nb; ++b) a = fs_add(a, part[static_cast<int64_t>(f) * max_blocks + b]);
   const int t = st[f].ntrees;
-  mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(a, static_cast<double>(fd.n));
   st[f].ntrees = t + 1;
   if (t + 1 >= fd.trees) st[f].active = 0;
 }
 
+}  // namespace
+
+// mse[f][t] = (sum over canonical rows p, in order, of e*e) / n (costmodel.cpp:215-220) for
+// every committed round t in [t_lo, t_hi) of every family: one thread per (family, round) chain,
+// every add separately rounded. Round t's e of family f sits at
+//   ring   (ring_stride > 0): ebuf[(t % K) * ring_stride + pos0 + p]
+//   blocks (ring_stride = 0): ebuf[pos0 * K + (t % K) * n + p]   (K = all rounds, resident fit)
+__global__ void mse_fold_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st, int F,
+                                const double* __restrict__ ebuf, int K, int64_t ring_stride, int t_lo, int t_hi,
+                                double* __restrict__ mse, int max_trees) {
+  const int W = t_hi - t_lo;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (W <= 0 || i >= static_cast<int64_t>(F) * W) return;
+  const int f = static_cast<int>(i / W), t = t_lo + static_cast<int>(i % W);
+  const FamDesc fd = fam[f];
+  if (t >= st[f].ntrees || fd.n <= 0) return;
+  const int n = fd.n;
+  const double* e = ring_stride > 0 ? ebuf + static_cast<int64_t>(t % K) * ring_stride + fd.pos0
+                                    : ebuf + fd.pos0 * K + static_cast<int64_t>(t % K) * n;
+  double s = 0.0;
+  int p = 0;
+  if (n >= 8) {  // the next 8 loads are in flight while the current 8 squares are added
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = e[k];
+    for (p = 8; p + 8 <= n; p += 8) {
+      double b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[k] = e[p + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = fs_add(s, fs_mul(a[k], a[k]));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = b[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = fs_add(s, fs_mul(a[k], a[k]));
+  }
+  for (; p < n; ++p) s = fs_add(s, fs_mul(e[p], e[p]));
+  mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(s, static_cast<double>(n));
+}
+
+namespace {
 }  // namespace
 }  // namespace fit
 }  // namespace fs

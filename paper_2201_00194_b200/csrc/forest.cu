@@ -251,7 +251,7 @@ void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch) {
   const int nleaf = 1 << depth;
   std::vector<uint32_t> nodes(static_cast<size_t>(T) * nint, 0);
   std::vector<double> leafv(static_cast<size_t>(T) * nleaf, 0.0);
-  std::vector<uint8_t> leafid(static_cast<size_t>(T) * nleaf, 0);
+  std::vector<uint16_t> leafid(static_cast<size_t>(T) * nleaf, 0);
   struct Place {
     int idx, heap, lvl;
   };
@@ -265,7 +265,7 @@ void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch) {
       const size_t g = static_cast<size_t>(o + c.idx);
       if (c.lvl == depth) {
         leafv[static_cast<size_t>(t) * nleaf + (c.heap - nint)] = m.value[g];
-        leafid[static_cast<size_t>(t) * nleaf + (c.heap - nint)] = static_cast<uint8_t>(c.idx);
+        leafid[static_cast<size_t>(t) * nleaf + (c.heap - nint)] = static_cast<uint16_t>(c.idx);
         continue;
       }
       uint32_t node;
@@ -296,7 +296,7 @@ void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch) {
   pk.commit(m, dev, batch);
   m.nodes_d = pk.at<uint32_t>(m, 0);
   m.leafv_d = pk.at<double>(m, 1);
-  m.leafid_d = pk.at<uint8_t>(m, 2);
+  m.leafid_d = pk.at<uint16_t>(m, 2);
   m.uthr_d = pk.at<double>(m, 3);
   m.n_uthr = static_cast<int>(uthr.size());
   m.uoff_d = pk.at<int32_t>(m, 4);

@@ -54,7 +54,7 @@ struct FamilyModel {
   bool generic = false;  // depth > kMaxHeapDepth: pre-order device arrays instead of heaps
   uint32_t* nodes_d = nullptr;   // [T][2^depth - 1]
   double* leafv_d = nullptr;     // [T][2^depth]
-  uint8_t* leafid_d = nullptr;   // [T][2^depth]
+  uint16_t* leafid_d = nullptr;  // [T][2^depth] pre-order node index of each heap leaf
   double* uthr_d = nullptr;      // unique thresholds, feature-major
   int n_uthr = 0;
   int32_t* uoff_d = nullptr;     // [d_model + 1]

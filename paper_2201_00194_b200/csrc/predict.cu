@@ -1,32 +1,45 @@
 // Kernel (2): GBDT ensemble predict - predict (costmodel.cpp:237-246) with RegressionTree::eval
-// (:135-143) for a whole candidate population, one launch per family segment.
+// (:135-143) for a whole candidate population; every family segment of a call in ONE launch.
 //
-// CTA = a tile of 256 candidates, one per thread.
-//   1. Stage: warps stream the tile's FP64 rows from HBM with coalesced loads (lanes over
-//      features), check finiteness (the reference throws on any non-finite feature) and convert
-//      each value the ensemble actually tests into its threshold code (binary search in the
-//      feature's sorted unique thresholds). Codes land in shared memory transposed
-//      [feature][candidate] so a warp reading one feature hits consecutive bytes.
-//   2. Trees are staged through shared memory in chunks; each thread walks its candidate down
-//      every tree of the chunk (fixed-depth heap, no divergence in trip count) and folds
-//      score = score + lr*leaf in tree order with separately rounded __dmul_rn/__dadd_rn - the
-//      reference's `score += learning_rate * tree.eval(x)` without FMA.
-// HBM traffic per candidate = 8*d (row) + 8 (score) [+ T leaf ids]; the model is read once per
-// CTA from L2.
+// CTA = 256 threads and a tile of TC candidates (TC = 256 .. 32: the host shrinks the tile until
+// the launch covers every SM). Per tile:
+//   1. Stage codes. Each candidate's tested features become threshold codes in shared memory,
+//      row-major [candidate][feature]: code(x) = #{model thresholds of that feature < x}, so
+//      `x <= t_rank` <=> `code(x) <= rank` exactly (SURVEY.md "Bit-exactness rules" 2).
+//      * predict: the tile's FP64 feature rows stream HBM -> shared memory by bulk async copies
+//        (cp.async.bulk, TMA engine, 16 rows per stage, mbarrier-tracked, double-buffered), so
+//        the next stage lands while warps code the current one; every feature of every row is
+//        checked for finiteness (the reference throws on any, costmodel.cpp:238-240);
+//      * score (fused): no feature row exists - a warp per candidate forms
+//        every tested feature from the descriptor exactly as featurize does
+//        (searchspace.cpp:90-118: log2 / position tables built on the host, pair products one
+//        __dmul_rn).
+//   2. Warp-cooperative traversal, 32 trees per pass: the pass's trees are staged in shared
+//      memory (node words transposed [heap node][tree] so 32 lanes at different nodes never
+//      share a bank; lr*leaf precomputed with __dmul_rn), then LANE = TREE: each warp walks its
+//      candidates down the 32 trees at once, the top three levels from registers, and records
+//      the leaf slot (u8) per (tree, candidate).
+//   3. Tree-order fold: thread = candidate adds the 32 leaf values in tree order,
+//      score = score + lr*leaf, separately rounded - the reference's
+//      `score += learning_rate * tree.eval(x)` without FMA.
+// HBM traffic per candidate: 8*d (row) + 8 (score) [+ 2*T leaf ids] for predict, 4*16 + 4 + 8
+// for the fused score; the model is read from L2 once per tile.
 #include <algorithm>
 
 #include "forest.cuh"
 
 namespace {
 
-constexpr int kTile = 256;
-constexpr int kChunk = 64;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kStageRows = 16;  // rows per bulk-copy stage (predict)
+constexpr int kStages = 2;
 
 // One family's compiled ensemble, as the batched kernel sees it.
 struct PredModel {
   const uint32_t* nodes;
   const double* leafv;
-  const uint8_t* leafid;
+  const uint16_t* leafid;
   const double* uthr;
   const int32_t* uoff;
   double base, lr;
@@ -35,9 +48,7 @@ struct PredModel {
   const fs::ModelMeta* meta;  // device-compiled fit: n_trees / base live on the device
 };
 
-// Candidate descriptors for the fused score path (kFused): the kernel computes each tested
-// feature from the assignment exactly as featurize does (searchspace.cpp:90-118; log2/position
-// tables built on the host, pair products one __dmul_rn) instead of reading a feature row.
+// Candidate descriptors for the fused score path.
 struct SpaceTabs {
   const int32_t* space_of;  // [P]
   const int32_t* assign;    // [P][16] value indices
@@ -50,60 +61,111 @@ struct SpaceTabs {
   int pad;
 };
 
-// One CTA's work: a tile of up to kTile rows of one family segment.
+// One CTA's work: a tile of up to TC rows of one family segment.
 struct PredJob {
   int32_t model, rows;
   int64_t row0;   // first row (into x / scores)
-  int64_t leaf0;  // byte offset of row0's leaf ids
+  int64_t leaf0;  // element offset of row0's leaf ids
 };
 
-// Every family segment of a predict call is scored by ONE launch (a family is typically a few
-// hundred tiles; one launch per family left most of the 148 SMs idle). Shared memory is laid out
-// for the largest model of the launch; each CTA uses its own model's shape.
-template <typename CodeT, bool kLeaves, bool kSmemThr, bool kFused>
-__global__ void __launch_bounds__(kTile) predict_heap_kernel(
-    const double* __restrict__ x, int d, const PredModel* __restrict__ models, const PredJob* __restrict__ jobs,
-    int max_dmodel, int max_depth, int max_uthr, double* __restrict__ scores, uint8_t* __restrict__ leaf_out,
-    uint32_t* err, SpaceTabs sp) {
+// Shared-memory carve-up, identical on host and device.
+struct Smem {
+  size_t codes, nodes, lrleaf, leafid, slots, uthr, uoff, rows, bars, total;
+  __host__ __device__ static size_t al(size_t o) { return (o + 15) & ~size_t(15); }
+  __host__ __device__ Smem(int tc, int ds, int code_bytes, int max_depth, bool leaves, int max_uthr, int max_dmodel,
+                           bool smem_thr, int row_doubles) {
+    const size_t mnint = (size_t{1} << max_depth) - 1, mnleaf = size_t{1} << max_depth;
+    size_t o = 0;
+    codes = o;
+    o = al(o + static_cast<size_t>(tc) * ds * code_bytes);
+    nodes = o;  // [heap node][32 trees]
+    o = al(o + mnint * 32 * 4);
+    lrleaf = o;  // [32 trees][leaf]
+    o = al(o + 32 * mnleaf * 8);
+    leafid = o;
+    o = al(o + (leaves ? 32 * mnleaf * 2 : 0));
+    slots = o;  // [32 trees][tc + 4]
+    o = al(o + 32 * static_cast<size_t>(tc + 4));
+    uthr = o;
+    o = al(o + (smem_thr ? static_cast<size_t>(max_uthr) * 8 : 0));
+    uoff = o;
+    o = al(o + (smem_thr ? static_cast<size_t>(max_dmodel + 1) * 4 : 0));
+    rows = o;  // predict: kStages x kStageRows feature rows
+    o = al(o + static_cast<size_t>(row_doubles) * 8);
+    bars = o;
+    o = al(o + kStages * 8);
+    total = o;
+  }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA-engine bulk copy global -> shared, completion counted on the mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// kBulk: predict rows arrive by bulk async copies (rows 16-byte aligned, d even); otherwise warps
+// read them with coalesced loads.
+template <typename CodeT, bool kLeaves, bool kSmemThr, bool kFused, bool kBulk>
+__global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restrict__ x, int d,
+                                                           const PredModel* __restrict__ models,
+                                                           const PredJob* __restrict__ jobs, int tc, int ds,
+                                                           int max_dmodel, int max_depth, int max_uthr,
+                                                           double* __restrict__ scores, uint16_t* __restrict__ leaf_out,
+                                                           uint32_t* err, SpaceTabs sp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const PredJob job = jobs[blockIdx.x];
   const PredModel M = models[job.model];
+  const Smem L(tc, ds, sizeof(CodeT), max_depth, kLeaves, max_uthr, max_dmodel, kSmemThr,
+               kFused || !kBulk ? 0 : kStages * kStageRows * d);
+  CodeT* codes = reinterpret_cast<CodeT*>(smem + L.codes);  // [tc][ds]
+  uint32_t* s_nodes = reinterpret_cast<uint32_t*>(smem + L.nodes);
+  double* s_lrleaf = reinterpret_cast<double*>(smem + L.lrleaf);
+  uint16_t* s_leafid = reinterpret_cast<uint16_t*>(smem + L.leafid);
+  uint8_t* s_slot = smem + L.slots;
+  const int tcp = tc + 4;  // slot row pitch: tcp/4 odd -> lanes (trees) store to distinct banks
+
   const int depth = M.depth, d_model = M.d_model;
   const int n_trees = M.meta ? M.meta->n_trees : M.n_trees;
   const int32_t* fmap = M.fmap;
-  const int nint = (1 << depth) - 1;
-  const int nleaf = 1 << depth;
-  const int mnint = (1 << max_depth) - 1, mnleaf = 1 << max_depth;
-  CodeT* codes = reinterpret_cast<CodeT*>(smem);  // [d_model][kTile]
-  size_t off = (static_cast<size_t>(max_dmodel) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
-  double* s_leafv = reinterpret_cast<double*>(smem + off);  // [kChunk][nleaf]
-  off += static_cast<size_t>(kChunk) * mnleaf * sizeof(double);
-  uint32_t* s_nodes = reinterpret_cast<uint32_t*>(smem + off);  // [kChunk][nint]
-  off += static_cast<size_t>(kChunk) * mnint * sizeof(uint32_t);
-  uint8_t* s_leafid = smem + off;  // [kChunk][nleaf]
-  off += static_cast<size_t>(kChunk) * mnleaf;
-  uint8_t* s_lbuf = smem + off;  // [kTile][kChunk]
-  off += kLeaves ? static_cast<size_t>(kTile) * kChunk : 0;
-  off = (off + 15) & ~size_t(15);
+  const int nint = (1 << depth) - 1, nleaf = 1 << depth;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t row0 = job.row0;
+  const int rows = job.rows;
 
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  // The threshold tables the codes are searched in: staged in shared memory when they fit
-  // (binary-search steps then cost a shared load instead of an L2 round trip).
+  // threshold tables the codes are searched in: staged in shared memory when they fit
   const double* uthr = M.uthr;
   const int32_t* uoff = M.uoff;
   if (kSmemThr) {
-    double* su = reinterpret_cast<double*>(smem + off);
-    int32_t* so = reinterpret_cast<int32_t*>(su + max_uthr);
-    for (int i = tid; i < M.n_uthr; i += kTile) su[i] = __ldg(M.uthr + i);
-    for (int i = tid; i <= d_model; i += kTile) so[i] = __ldg(M.uoff + i);
-    __syncthreads();
+    double* su = reinterpret_cast<double*>(smem + L.uthr);
+    int32_t* so = reinterpret_cast<int32_t*>(smem + L.uoff);
+    for (int i = tid; i < M.n_uthr; i += kThreads) su[i] = __ldg(M.uthr + i);
+    for (int i = tid; i <= d_model; i += kThreads) so[i] = __ldg(M.uoff + i);
     uthr = su;
     uoff = so;
   }
-  const int64_t row0 = job.row0;
-  const int tile_rows = job.rows;
-
   auto code_of = [&](int f, double v) {
     int lo = uoff[f], hi = uoff[f + 1];
     const int first = lo;
@@ -114,10 +176,13 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
     }
     return static_cast<CodeT>(lo - first);
   };
+
+  // ---- 1. codes ---------------------------------------------------------------------------
   if constexpr (kFused) {
+    if (kSmemThr) __syncthreads();
     // warp per candidate: lane k < K fetches knob k's log2 / position; every tested feature is
-    // formed from shuffles (featurize_kernel's arithmetic) and coded - no feature row in HBM
-    for (int c = warp; c < tile_rows; c += kTile / 32) {
+    // formed from shuffles (featurize_kernel's arithmetic) and coded
+    for (int c = warp; c < rows; c += kWarps) {
       const int64_t cand = row0 + c;
       const int s = __ldg(sp.space_of + cand);
       const bool bad_space = s < 0 || s >= sp.n_spaces;
@@ -142,6 +207,7 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
         if (any_bad) atomicOr(err, fs::kErrKnobRange);
         if (sp.pad < dim) atomicOr(err, fs::kErrPadDim);
       }
+      CodeT* crow = codes + static_cast<size_t>(c) * ds;
       for (int base = 0; base < d_model; base += 32) {
         const int f = base + lane;
         const int g = f < d_model && fmap ? __ldg(fmap + f) : f;  // the original feature index
@@ -163,59 +229,111 @@ __global__ void __launch_bounds__(kTile) predict_heap_kernel(
         if (kind == 1) v = la;
         else if (kind == 2) v = pa;
         else if (kind == 3) v = fs_mul(la, lb);
-        if (f < d_model) codes[f * kTile + c] = code_of(f, v);
+        if (f < d_model) crow[f] = code_of(f, v);
       }
     }
   } else {
     bool nonfinite = false;
-    for (int c = warp; c < tile_rows; c += kTile / 32) {
-      const double* xr = x + (row0 + c) * d;
-      for (int f = lane; f < d; f += 32) {
-        const double v = __ldcs(xr + f);  // streamed once
-        nonfinite |= !isfinite(v);
-        if (!fmap && f < d_model) codes[f * kTile + c] = code_of(f, v);
+    double* rbuf = reinterpret_cast<double*>(smem + L.rows);  // [kStages][kStageRows][d]
+    const int nst = (rows + kStageRows - 1) / kStageRows;
+    // warp w codes row r of a stage held in shared memory at `src`
+    auto code_row = [&](const double* src, int c) {
+      for (int f = lane; f < d; f += 32) nonfinite |= !isfinite(src[f]);
+      CodeT* crow = codes + static_cast<size_t>(c) * ds;
+      for (int f = lane; f < d_model; f += 32) crow[f] = code_of(f, src[fmap ? __ldg(fmap + f) : f]);
+    };
+    if constexpr (kBulk) {
+      uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+      auto issue = [&](int st) {
+        const int r0 = st * kStageRows, nr = min(kStageRows, rows - r0);
+        const uint32_t bytes = static_cast<uint32_t>(nr) * d * 8;
+        uint64_t* bar = bars + (st % kStages);
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(rbuf + static_cast<size_t>(st % kStages) * kStageRows * d, x + (row0 + r0) * d, bytes, bar);
+      };
+      if (tid == 0) {
+        for (int b = 0; b < kStages; ++b) mbar_init(bars + b, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < min(kStages, nst); ++st) issue(st);
       }
-      if (fmap)  // compiled features are representatives: gather their original columns (L1 hits)
-        for (int f = lane; f < d_model; f += 32) codes[f * kTile + c] = code_of(f, xr[__ldg(fmap + f)]);
+      __syncthreads();  // barriers initialised (and staged thresholds visible)
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait(bars + (st % kStages), static_cast<uint32_t>((st / kStages) & 1));
+        const double* buf = rbuf + static_cast<size_t>(st % kStages) * kStageRows * d;
+        const int r0 = st * kStageRows, nr = min(kStageRows, rows - r0);
+        for (int r = warp; r < nr; r += kWarps) code_row(buf + static_cast<size_t>(r) * d, r0 + r);
+        __syncthreads();  // every warp is done with this buffer
+        if (tid == 0 && st + kStages < nst) issue(st + kStages);
+      }
+    } else {
+      if (kSmemThr) __syncthreads();
+      // rows read in place: coalesced finiteness pass, tested columns gathered (L1 hits)
+      for (int c = warp; c < rows; c += kWarps) code_row(x + (row0 + c) * d, c);
     }
     if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, fs::kErrNonFinitePredict);
   }
 
+  // ---- 2./3. passes of 32 trees -------------------------------------------------------------
   double score = M.meta ? M.meta->base : M.base;
   const double lr = M.lr;
-  const bool active = tid < tile_rows;
-  for (int t0 = 0; t0 < n_trees; t0 += kChunk) {
-    const int ch = min(kChunk, n_trees - t0);
-    __syncthreads();  // codes ready / previous chunk consumed
-    for (int i = tid; i < ch * nint; i += kTile) s_nodes[i] = __ldg(M.nodes + static_cast<size_t>(t0) * nint + i);
-    for (int i = tid; i < ch * nleaf; i += kTile) {
-      s_leafv[i] = __ldg(M.leafv + static_cast<size_t>(t0) * nleaf + i);
-      s_leafid[i] = __ldg(M.leafid + static_cast<size_t>(t0) * nleaf + i);
+  for (int t0 = 0; t0 < n_trees; t0 += 32) {
+    const int ch = min(32, n_trees - t0);
+    __syncthreads();  // codes ready / the previous pass's fold is done with the tree tables
+    for (int i = tid; i < ch * nint; i += kThreads) {  // [node][tree]
+      const int h = i / ch, t = i - h * ch;
+      s_nodes[h * 32 + t] = __ldg(M.nodes + static_cast<size_t>(t0 + t) * nint + h);
+    }
+    for (int i = tid; i < ch * nleaf; i += kThreads) {
+      s_lrleaf[i] = fs_mul(lr, __ldg(M.leafv + static_cast<size_t>(t0) * nleaf + i));
+      if (kLeaves) s_leafid[i] = __ldg(M.leafid + static_cast<size_t>(t0) * nleaf + i);
     }
     __syncthreads();
-    if (active) {
-      for (int t = 0; t < ch; ++t) {
-        const uint32_t* tn = s_nodes + t * nint;
-        int idx = 0;
-        for (int lv = 0; lv < depth; ++lv) {
-          const uint32_t nd = tn[idx];
-          const uint32_t cv = codes[(nd & 0xFFFFu) * kTile + tid];
-          idx = 2 * idx + 1 + (cv > (nd >> 16) ? 1 : 0);
+    if (lane < ch) {
+      // lane = tree: the top three levels' node words live in registers for the whole pass
+      const uint32_t w0 = nint > 0 ? s_nodes[lane] : 0u;
+      const uint32_t w1 = nint > 1 ? s_nodes[32 + lane] : 0u, w2 = nint > 2 ? s_nodes[64 + lane] : 0u;
+      const uint32_t w3 = nint > 3 ? s_nodes[96 + lane] : 0u, w4 = nint > 4 ? s_nodes[128 + lane] : 0u;
+      const uint32_t w5 = nint > 5 ? s_nodes[160 + lane] : 0u, w6 = nint > 6 ? s_nodes[192 + lane] : 0u;
+      auto walk = [&](const CodeT* r) {
+        if (depth == 0) return 0;
+        const uint32_t b0 = static_cast<uint32_t>(r[w0 & 0xFFFFu]) > (w0 >> 16);
+        if (depth == 1) return static_cast<int>(b0);
+        const uint32_t n1 = b0 ? w2 : w1;
+        const uint32_t b1 = static_cast<uint32_t>(r[n1 & 0xFFFFu]) > (n1 >> 16);
+        if (depth == 2) return static_cast<int>(2 * b0 + b1);
+        const uint32_t n2 = b0 ? (b1 ? w6 : w5) : (b1 ? w4 : w3);
+        const uint32_t b2 = static_cast<uint32_t>(r[n2 & 0xFFFFu]) > (n2 >> 16);
+        int idx = 7 + static_cast<int>(4 * b0 + 2 * b1 + b2);
+        for (int lv = 3; lv < depth; ++lv) {
+          const uint32_t nd = s_nodes[idx * 32 + lane];
+          idx = 2 * idx + 1 + (static_cast<uint32_t>(r[nd & 0xFFFFu]) > (nd >> 16) ? 1 : 0);
         }
-        const int slot = idx - nint;
-        score = fs_add(score, fs_mul(lr, s_leafv[t * nleaf + slot]));
-        if (kLeaves) s_lbuf[tid * kChunk + t] = s_leafid[t * nleaf + slot];
+        return idx - nint;
+      };
+      uint8_t* srow = s_slot + lane * tcp;
+      int c = warp;
+      for (; c + 3 * kWarps < rows; c += 4 * kWarps) {  // four independent walks in flight
+        const int q0 = walk(codes + static_cast<size_t>(c) * ds);
+        const int q1 = walk(codes + static_cast<size_t>(c + kWarps) * ds);
+        const int q2 = walk(codes + static_cast<size_t>(c + 2 * kWarps) * ds);
+        const int q3 = walk(codes + static_cast<size_t>(c + 3 * kWarps) * ds);
+        srow[c] = static_cast<uint8_t>(q0);
+        srow[c + kWarps] = static_cast<uint8_t>(q1);
+        srow[c + 2 * kWarps] = static_cast<uint8_t>(q2);
+        srow[c + 3 * kWarps] = static_cast<uint8_t>(q3);
       }
+      for (; c < rows; c += kWarps) srow[c] = static_cast<uint8_t>(walk(codes + static_cast<size_t>(c) * ds));
     }
-    if (kLeaves) {
-      __syncthreads();
-      for (int i = tid; i < tile_rows * ch; i += kTile) {
-        const int c = i / ch, t = i - c * ch;
-        leaf_out[job.leaf0 + static_cast<int64_t>(c) * n_trees + t0 + t] = s_lbuf[c * kChunk + t];
+    __syncthreads();
+    if (tid < rows) {  // thread = candidate: tree-order fold of the pass's leaf values
+      for (int t = 0; t < ch; ++t) {
+        const int q = s_slot[t * tcp + tid];
+        score = fs_add(score, s_lrleaf[t * nleaf + q]);
+        if (kLeaves) leaf_out[job.leaf0 + static_cast<int64_t>(tid) * n_trees + t0 + t] = s_leafid[t * nleaf + q];
       }
     }
   }
-  if (active) scores[row0 + tid] = score;
+  if (tid < rows) scores[row0 + tid] = score;
 }
 
 // Trees deeper than kMaxHeapDepth: walk the pre-order arrays directly (rare; hand-built models).
@@ -223,7 +341,7 @@ __global__ void predict_generic_kernel(const double* __restrict__ x, int64_t row
                                        double lr, const int32_t* __restrict__ off, const int32_t* __restrict__ feat,
                                        const double* __restrict__ thr, const int32_t* __restrict__ left,
                                        const int32_t* __restrict__ right, const double* __restrict__ val,
-                                       double* __restrict__ scores, uint8_t* __restrict__ leaf_out, uint32_t* err) {
+                                       double* __restrict__ scores, uint16_t* __restrict__ leaf_out, uint32_t* err) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const double* xr = x + r * d;
@@ -236,39 +354,63 @@ __global__ void predict_generic_kernel(const double* __restrict__ x, int64_t row
     int idx = 0;
     while (feat[o + idx] >= 0) idx = xr[feat[o + idx]] <= thr[o + idx] ? left[o + idx] : right[o + idx];
     score = fs_add(score, fs_mul(lr, val[o + idx]));
-    if (leaf_out) leaf_out[r * n_trees + t] = static_cast<uint8_t>(idx);
+    if (leaf_out) leaf_out[r * n_trees + t] = static_cast<uint16_t>(idx);
   }
   scores[r] = score;
 }
 
 struct HeapGroup {
   std::vector<PredModel> models;
-  std::vector<PredJob> jobs;
+  std::vector<int64_t> r0, rows, leaf0;  // per model's segment
   int max_dmodel = 0, max_depth = 0, max_uthr = 0;
 };
 
 template <typename CodeT, bool kLeaves, bool kSmemThr, bool kFused>
-void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, double* scores, uint8_t* leaf_out,
+void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, double* scores, uint16_t* leaf_out,
                   const SpaceTabs& sp) {
-  if (g.jobs.empty()) return;
-  const int mnint = (1 << g.max_depth) - 1, mnleaf = 1 << g.max_depth;
-  size_t smem = (static_cast<size_t>(g.max_dmodel) * kTile * sizeof(CodeT) + 15) & ~size_t(15);
-  smem += static_cast<size_t>(kChunk) * (mnleaf * sizeof(double) + mnint * sizeof(uint32_t) + mnleaf);
-  if (kLeaves) smem += static_cast<size_t>(kTile) * kChunk;
-  smem = (smem + 15) & ~size_t(15);
-  if (kSmemThr) smem += static_cast<size_t>(g.max_uthr) * sizeof(double) + (g.max_dmodel + 1) * sizeof(int32_t);
-  auto* fn = predict_heap_kernel<CodeT, kLeaves, kSmemThr, kFused>;
+  if (g.models.empty()) return;
+  // tile: the largest of 256 / 128 / 64 / 32 candidates whose tiles still cover every SM
+  int tc = 256;
+  int64_t rows_all = 0;
+  for (int64_t r : g.rows) rows_all += r;
+  while (tc > 32) {
+    int64_t tiles = 0;
+    for (int64_t r : g.rows) tiles += fs::ceil_div(r, tc);
+    if (tiles >= dev->sm_count) break;
+    tc /= 2;
+  }
+  const int ds = std::max(4, (g.max_dmodel + 3) & ~3);  // row pitch (elements); >= 4 so feature 0 exists
+  const bool bulk = !kFused && d > 0 && d % 2 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                    static_cast<size_t>(kStages) * kStageRows * d * 8 <= 96 * 1024;
+  const int row_doubles = bulk ? kStages * kStageRows * d : 0;
+  size_t smem = Smem(tc, ds, sizeof(CodeT), g.max_depth, kLeaves, g.max_uthr, g.max_dmodel, kSmemThr, row_doubles).total;
+  while (smem > 227 * 1024 && tc > 32) {
+    tc /= 2;
+    smem = Smem(tc, ds, sizeof(CodeT), g.max_depth, kLeaves, g.max_uthr, g.max_dmodel, kSmemThr, row_doubles).total;
+  }
   if (smem > 227 * 1024) fs::fail(FS_EINVAL, "predict: model too wide for the shared-memory tile");
-  FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const size_t mb = g.models.size() * sizeof(PredModel), jb = g.jobs.size() * sizeof(PredJob);
+  std::vector<PredJob> jobs;
+  jobs.reserve(static_cast<size_t>(fs::ceil_div(rows_all, tc)) + g.models.size());
+  for (size_t mi = 0; mi < g.models.size(); ++mi) {
+    const int T = g.models[mi].n_trees;
+    for (int64_t t = 0; t < g.rows[mi]; t += tc)
+      jobs.push_back({static_cast<int32_t>(mi), static_cast<int32_t>(std::min<int64_t>(tc, g.rows[mi] - t)),
+                      g.r0[mi] + t, g.leaf0[mi] + t * T});
+  }
+  const size_t mb = g.models.size() * sizeof(PredModel), jb = jobs.size() * sizeof(PredJob);
   auto* buf = static_cast<unsigned char*>(dev->scratch(fs::kSlotPredictSeg, mb + jb + 16));
   auto* md = reinterpret_cast<PredModel*>(buf);
   auto* jd = reinterpret_cast<PredJob*>(buf + ((mb + 15) & ~size_t(15)));
   FS_CUDA(cudaMemcpyAsync(md, g.models.data(), mb, cudaMemcpyHostToDevice, dev->stream));
-  FS_CUDA(cudaMemcpyAsync(jd, g.jobs.data(), jb, cudaMemcpyHostToDevice, dev->stream));
+  FS_CUDA(cudaMemcpyAsync(jd, jobs.data(), jb, cudaMemcpyHostToDevice, dev->stream));
   fs::ProfScope prof(dev, kFused ? "score_fused" : "predict");
-  fn<<<static_cast<unsigned>(g.jobs.size()), kTile, smem, dev->stream>>>(
-      x, d, md, jd, g.max_dmodel, g.max_depth, g.max_uthr, scores, leaf_out, dev->err_d, sp);
+  auto launch = [&](auto* fn) {
+    FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    fn<<<static_cast<unsigned>(jobs.size()), kThreads, smem, dev->stream>>>(
+        x, d, md, jd, tc, ds, g.max_dmodel, g.max_depth, g.max_uthr, scores, leaf_out, dev->err_d, sp);
+  };
+  if (bulk) launch(predict_kernel<CodeT, kLeaves, kSmemThr, kFused, true>);
+  else launch(predict_kernel<CodeT, kLeaves, kSmemThr, kFused, false>);
   dev->count_launch();
   FS_CUDA(cudaGetLastError());
 }
@@ -277,12 +419,12 @@ void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, do
 
 namespace fs {
 
-// Scores rows [seg[f], seg[f+1]) with family f. Leaf ids of segment f start at byte
+// Scores rows [seg[f], seg[f+1]) with family f. Leaf ids of segment f start at element
 // sum_{g<f} rows_g * T_g of leaf_out. All heap-form families go out in one launch (per code width
 // / threshold-table placement, normally one); deeper-than-heap models use the generic kernel.
 template <bool kFused>
 void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
-                         const double* x, double* scores, uint8_t* leaf_out, const SpaceTabs& sp) {
+                         const double* x, double* scores, uint16_t* leaf_out, const SpaceTabs& sp) {
   int64_t leaf_off = 0;
   HeapGroup groups[2][2];  // [code_bytes == 2][thresholds in smem]
   for (int f = 0; f < nseg; ++f) {
@@ -297,6 +439,10 @@ void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, cons
     leaf_off += rows * m.n_trees;
     if (m.generic) {
       if (kFused) fail(FS_EINVAL, "score: fused path needs heap-form models");
+      if (leaf_out)
+        for (int t = 0; t < m.num_trees(); ++t)
+          if (m.offsets[static_cast<size_t>(t) + 1] - m.offsets[static_cast<size_t>(t)] > 65536)
+            fail(FS_EINVAL, "predict: leaf ids are uint16; a tree holds more than 65,536 nodes");
       predict_generic_kernel<<<static_cast<int>(ceil_div(rows, 128)), 128, 0, dev->stream>>>(
           x + r0 * d, rows, d, m.n_trees, m.base, m.lr, m.g_off_d, m.g_feat_d, m.g_thr_d, m.g_left_d, m.g_right_d,
           m.g_val_d, scores + r0, leaf_out ? leaf_out + lo : nullptr, dev->err_d);
@@ -306,19 +452,20 @@ void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, cons
     }
     const bool smem_thr = static_cast<size_t>(m.n_uthr) * sizeof(double) <= 48 * 1024;
     HeapGroup& g = groups[m.code_bytes == 2][smem_thr];
-    const int mi = static_cast<int>(g.models.size());
-    g.models.push_back({m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, m.base, m.lr, m.depth, m.n_trees,
-                        m.fmap_d ? m.d_model : std::min(m.d_model, d), m.n_uthr, m.fmap_d, m.meta_d});
-    g.max_dmodel = std::max(g.max_dmodel, m.fmap_d ? m.d_model : std::min(m.d_model, d));
+    const int dm = m.fmap_d ? m.d_model : std::min(m.d_model, d);
+    g.models.push_back({m.nodes_d, m.leafv_d, m.leafid_d, m.uthr_d, m.uoff_d, m.base, m.lr, m.depth, m.n_trees, dm,
+                        m.n_uthr, m.fmap_d, m.meta_d});
+    g.r0.push_back(r0);
+    g.rows.push_back(rows);
+    g.leaf0.push_back(lo);
+    g.max_dmodel = std::max(g.max_dmodel, dm);
     g.max_depth = std::max(g.max_depth, m.depth);
     g.max_uthr = std::max(g.max_uthr, m.n_uthr);
-    for (int64_t t = 0; t < rows; t += kTile)
-      g.jobs.push_back({mi, static_cast<int32_t>(std::min<int64_t>(kTile, rows - t)), r0 + t, lo + t * m.n_trees});
   }
   for (int cb = 0; cb < 2; ++cb)
     for (int st = 0; st < 2; ++st) {
       const HeapGroup& g = groups[cb][st];
-      if (g.jobs.empty()) continue;
+      if (g.models.empty()) continue;
       if (cb == 0) {
         if (leaf_out) st ? launch_group<uint8_t, true, true, kFused>(dev, g, x, d, scores, leaf_out, sp)
                          : launch_group<uint8_t, true, false, kFused>(dev, g, x, d, scores, leaf_out, sp);
@@ -334,7 +481,7 @@ void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, cons
 }
 
 void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
-                    const double* x, double* scores, uint8_t* leaf_out) {
+                    const double* x, double* scores, uint16_t* leaf_out) {
   launch_predict_impl<false>(dev, fo, nseg, seg, d, x, scores, leaf_out, SpaceTabs{});
 }
 
@@ -346,7 +493,7 @@ void launch_score_fused(fs_device* dev, const fs_spaces* spc, const fs_forest* f
   launch_predict_impl<true>(dev, fo, nseg, seg, pad, nullptr, scores, nullptr, sp);
 }
 
-int64_t leaf_bytes(const fs_forest* fo, int32_t nseg, const int64_t* seg) {
+int64_t leaf_count(const fs_forest* fo, int32_t nseg, const int64_t* seg) {
   int64_t b = 0;
   for (int f = 0; f < nseg && f < static_cast<int32_t>(fo->fams.size()); ++f) {
     materialize(fo->dev, fo->fams[static_cast<size_t>(f)]);
@@ -360,7 +507,7 @@ int64_t leaf_bytes(const fs_forest* fo, int32_t nseg, const int64_t* seg) {
 extern "C" {
 
 int fs_predict_d(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d, const double* x_d,
-                 double* scores_d, uint8_t* leaf_d) {
+                 double* scores_d, uint16_t* leaf_d) {
   return fs::guard([&] {
     if (!dev || !fo || nseg < 0 || !seg || d < 0) fs::fail(FS_EINVAL, "fs_predict: bad arguments");
     dev->activate();
@@ -369,7 +516,7 @@ int fs_predict_d(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_
 }
 
 int fs_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d, const double* x,
-               double* scores, uint8_t* leaf_ids) {
+               double* scores, uint16_t* leaf_ids) {
   return fs::guard([&] {
     if (!dev || !fo || nseg < 0 || !seg || d < 0) fs::fail(FS_EINVAL, "fs_predict: bad arguments");
     dev->activate();
@@ -378,12 +525,12 @@ int fs_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t*
     if (seg[0] != 0) fs::fail(FS_EINVAL, "fs_predict: seg[0] must be 0");
     auto* xd = static_cast<double*>(dev->scratch(fs::kSlotH2D0, n * d * sizeof(double)));
     auto* sd = static_cast<double*>(dev->scratch(fs::kSlotD2H0, n * sizeof(double)));
-    const int64_t lb = leaf_ids ? fs::leaf_bytes(fo, nseg, seg) : 0;
-    auto* ld = leaf_ids ? static_cast<uint8_t*>(dev->scratch(fs::kSlotD2H1, std::max<int64_t>(lb, 1))) : nullptr;
+    const int64_t lc = leaf_ids ? fs::leaf_count(fo, nseg, seg) : 0;
+    auto* ld = leaf_ids ? static_cast<uint16_t*>(dev->scratch(fs::kSlotD2H1, std::max<int64_t>(lc, 1) * 2)) : nullptr;
     FS_CUDA(cudaMemcpyAsync(xd, x, n * d * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
     fs::launch_predict(dev, fo, nseg, seg, d, xd, sd, ld);
     FS_CUDA(cudaMemcpyAsync(scores, sd, n * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
-    if (leaf_ids && lb) FS_CUDA(cudaMemcpyAsync(leaf_ids, ld, lb, cudaMemcpyDeviceToHost, dev->stream));
+    if (leaf_ids && lc) FS_CUDA(cudaMemcpyAsync(leaf_ids, ld, lc * 2, cudaMemcpyDeviceToHost, dev->stream));
     fs::raise_deferred(dev->take_errors());
   });
 }

@@ -13,7 +13,7 @@ namespace fs {
 void launch_featurize(fs_device* dev, const fs_spaces* sp, int64_t n, const int32_t* space_of_d,
                       const int32_t* assign_d, int32_t pad, double* out_d);
 void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int64_t* seg, int32_t d,
-                    const double* x, double* scores, uint8_t* leaf_out);
+                    const double* x, double* scores, uint16_t* leaf_out);
 void launch_rank(fs_device* dev, int32_t nseg, const int64_t* seg_h, const double* scores_d, int32_t* perm_d);
 void launch_score_fused(fs_device* dev, const fs_spaces* spc, const fs_forest* fo, int32_t nseg, const int64_t* seg,
                         const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores);

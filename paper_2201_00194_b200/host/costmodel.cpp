@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <list>
 #include <mutex>
 #include <sstream>
 #include <stdexcept>
@@ -88,14 +89,23 @@ Flat flatten(const std::vector<RegressionTree>& trees) {
   return f;
 }
 
+bool same_bits(double a, double b) { return std::memcmp(&a, &b, sizeof(double)) == 0; }
+
 struct Runtime {
   fs_device* dev = nullptr;
+  // Compiled device copies of the models predict()/eval() have seen, keyed by a content digest.
+  // A digest hit is confirmed against the full model content (a 64-bit collision must never
+  // predict with another model); least recently used entries are evicted beyond kCacheCap.
+  static constexpr std::size_t kCacheCap = 512;
   struct Entry {
-    std::uint64_t digest = 0;
     fs_forest* forest = nullptr;
+    double base = 0.0, lr = 0.0;
+    Flat flat;  // the uploaded trees, for the exact comparison on a digest hit
     std::vector<double> gains;  // from the fit that produced this model, if any
+    std::list<std::uint64_t>::iterator lru;
   };
   std::unordered_map<std::uint64_t, Entry> models;  // digest -> compiled model
+  std::list<std::uint64_t> lru;                      // most recently used first
   std::unordered_map<std::uint64_t, fs_spaces*> spaces;
 
   Runtime() { ck(fs_device_create(gpu::device_ordinal(), &dev)); }
@@ -105,27 +115,66 @@ struct Runtime {
     fs_device_destroy(dev);
   }
 
+  static bool same_model(const Entry& e, const CostModelState& m) {
+    if (!same_bits(e.base, m.base_prediction) || !same_bits(e.lr, m.params.learning_rate)) return false;
+    if (e.flat.off.size() != m.trees.size() + 1) return false;
+    std::size_t i = 0;
+    for (std::size_t t = 0; t < m.trees.size(); ++t) {
+      const auto& nodes = m.trees[t].nodes;
+      if (static_cast<std::size_t>(e.flat.off[t + 1] - e.flat.off[t]) != nodes.size()) return false;
+      for (const auto& nd : nodes) {
+        if (e.flat.feat[i] != nd.feature || e.flat.left[i] != nd.left || e.flat.right[i] != nd.right ||
+            !same_bits(e.flat.thr[i], nd.threshold) || !same_bits(e.flat.val[i], nd.value))
+          return false;
+        ++i;
+      }
+    }
+    return true;
+  }
+
   // Compiled device copy of `m`, uploaded on first use (keyed by content).
   fs_forest* forest_for(const CostModelState& m) {
     const std::uint64_t dg = model_digest(m);
     auto it = models.find(dg);
-    if (it != models.end()) return it->second.forest;
-    if (models.size() > 512) {
-      for (auto& kv : models) fs_forest_destroy(kv.second.forest);
-      models.clear();
+    if (it != models.end()) {
+      lru.splice(lru.begin(), lru, it->second.lru);
+      if (same_model(it->second, m)) return it->second.forest;
+      upload(it->second, m);  // digest collision: the slot now holds this model
+      return it->second.forest;
     }
-    fs_forest* fo = nullptr;
-    ck(fs_forest_create(dev, 1, &fo));
-    const Flat f = flatten(m.trees);
-    const int rc = fs_forest_upload(fo, 0, m.base_prediction, m.params.learning_rate,
-                                    static_cast<int32_t>(m.trees.size()), f.off.data(), f.feat.data(), f.thr.data(),
-                                    f.left.data(), f.right.data(), f.val.data());
-    if (rc != FS_OK) {
-      fs_forest_destroy(fo);
-      raise(rc);
+    while (models.size() >= kCacheCap) {  // evict the least recently used model
+      const std::uint64_t victim = lru.back();
+      lru.pop_back();
+      fs_forest_destroy(models[victim].forest);
+      models.erase(victim);
     }
-    models[dg] = {dg, fo, {}};
-    return fo;
+    Entry e;
+    ck(fs_forest_create(dev, 1, &e.forest));
+    try {
+      upload(e, m);
+    } catch (...) {
+      fs_forest_destroy(e.forest);
+      throw;
+    }
+    lru.push_front(dg);
+    e.lru = lru.begin();
+    return (models[dg] = std::move(e)).forest;
+  }
+
+  // the cache entry holding exactly `m`, or nullptr
+  Entry* find(const CostModelState& m) {
+    auto it = models.find(model_digest(m));
+    return it != models.end() && same_model(it->second, m) ? &it->second : nullptr;
+  }
+
+  void upload(Entry& e, const CostModelState& m) {
+    e.gains.clear();
+    e.flat = flatten(m.trees);
+    e.base = m.base_prediction;
+    e.lr = m.params.learning_rate;
+    ck(fs_forest_upload(e.forest, 0, m.base_prediction, m.params.learning_rate, static_cast<int32_t>(m.trees.size()),
+                        e.flat.off.data(), e.flat.feat.data(), e.flat.thr.data(), e.flat.left.data(),
+                        e.flat.right.data(), e.flat.val.data()));
   }
 
   fs_spaces* spaces_for(const SpaceDescriptor& space) {
@@ -218,9 +267,8 @@ void fit_group(std::vector<CostModelState*>& group) {
     std::vector<double> gains;
     export_into(fo, static_cast<int>(g), *group[g], &gains);
     // keep the compiled model for predict: re-upload into a 1-family forest keyed by content
-    fs_forest* one = r.forest_for(*group[g]);
-    (void)one;
-    r.models[model_digest(*group[g])].gains = std::move(gains);
+    r.forest_for(*group[g]);
+    if (auto* e = r.find(*group[g])) e->gains = std::move(gains);
   }
   fs_forest_destroy(fo);
 }
@@ -323,10 +371,9 @@ std::vector<std::int32_t> rank(std::span<const double> scores) {
 
 std::vector<double> split_gains(const CostModelState& model) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
-  auto& models = rt().models;
-  auto it = models.find(model_digest(model));
-  if (it == models.end() || it->second.gains.empty()) return {};
-  return it->second.gains;
+  const auto* e = rt().find(model);
+  if (!e) return {};
+  return e->gains;
 }
 
 }  // namespace gpu
@@ -369,9 +416,9 @@ double RegressionTree::eval(std::span<const double> features) const {
   one.trees.push_back(*this);
   Runtime& r = rt();
   double score = 0.0;
-  uint8_t leaf = 0;
+  uint16_t leaf = 0;
   const int64_t seg[2] = {0, 1};
-  if (nodes.size() > 256) {  // leaf ids are bytes; deeper trees: the value through lr = 1, base 0
+  if (nodes.size() > 65536) {  // leaf ids are uint16; larger trees: the value through lr = 1, base 0
     one.params.learning_rate = 1.0;
     ck(fs_predict(r.dev, r.forest_for(one), 1, seg, static_cast<int32_t>(features.size()), features.data(), &score,
                   nullptr));

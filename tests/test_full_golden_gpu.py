@@ -1,0 +1,120 @@
+"""Full-size parity at the BASELINE.json configurations the small cases cannot reach: C4 (BERT-base
+families, 16,384 rows each, T = 500) and C5 (64 synthetic families of 65,536 rows, T = 1000),
+against models the UNMODIFIED reference fitted on the same inputs (tests/golden/make_golden_full.py,
+oracle/_ref). These sizes run code the small cases never reach: four-segment speculative folds
+(chains >= 8,192), chunk-parallel partition, pipelined 224-row histogram tiles, the MSE ring.
+
+Per family: trees field by field in pre-order, base and train_mse_by_round bit-exact
+(costmodel.cpp:152-222), split gains within 1e-5 relative of the oracle's reference-order replica
+(the north-star bar), and the fused score of the family's candidate pool (fs_score: featurize ->
+predict -> rank, scheduler.cpp:187-192) bit-identical to the reference's predictions and
+std::sort order (sha256 digests + the top 64 + every 97th score)."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import bench
+import paper_2201_00194_b200 as fs
+from common import GOLDEN
+
+pytestmark = pytest.mark.gpu
+TREE_FIELDS = ("offsets", "feature", "threshold", "left", "right", "value")
+_W = {}
+
+
+def workload(cfg):
+    if cfg not in _W:
+        _W[cfg] = bench.build_workload(cfg, seed=1000)
+    return _W[cfg]
+
+
+def golden(cfg):
+    path = os.path.join(GOLDEN, f"full_{cfg}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: run tests/golden/make_golden_full.py where /root/reference exists")
+    return np.load(path)
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def sub_workload(W, fams):
+    """Families `fams` of W as a workload of their own (family independence: a family's model
+    does not depend on which other families share the launch)."""
+    out = dict(W)
+    for key_so, key_a, key_seg in (("pool_so", "pool_a", "pool_seg"), ("tr_so", "tr_a", "tr_seg")):
+        seg = W[key_seg]
+        idx = np.concatenate([np.arange(seg[f], seg[f + 1]) for f in fams])
+        out[key_so], out[key_a] = W[key_so][idx], W[key_a][idx]
+        out[key_seg] = np.concatenate([[0], np.cumsum([seg[f + 1] - seg[f] for f in fams])]).astype(np.int64)
+        if key_seg == "tr_seg":
+            out["tr_y"] = W["tr_y"][idx]
+    return out
+
+
+def check(dev, W, G, fams, positions, trees):
+    sp = fs.Spaces(dev, W["spaces"])
+    fo = fs.Forest(dev, len(W["tr_seg"]) - 1)
+    fo.fit_records(sp, W["tr_so"], W["tr_a"], bench.PAD, W["tr_y"], seg=W["tr_seg"],
+                   params=fs.GbtParams(trees, 3, 0.1, 2))
+    scores, perm = sp.score(fo, W["pool_so"], W["pool_a"], bench.PAD, W["pool_seg"])
+    for f, pos in zip(fams, positions):
+        got = fo.export(pos)
+        assert got.base == float(G[f"f{f}_base"][0]), f
+        for k in TREE_FIELDS:
+            a, b = getattr(got, k), G[f"f{f}_{k}"]
+            assert np.array_equal(a, b), (f, k, np.flatnonzero(a[: len(b)] != b[: len(a)])[:5] if len(a) == len(b) else
+                                          (len(a), len(b)))
+        assert np.array_equal(got.mse, G[f"f{f}_mse"]), (f, np.flatnonzero(got.mse != G[f"f{f}_mse"])[:10])
+        internal = got.feature >= 0
+        np.testing.assert_allclose(got.gain[internal], G[f"f{f}_gain"][internal], rtol=1e-5, atol=0)
+        a, b = int(W["pool_seg"][pos]), int(W["pool_seg"][pos + 1])
+        s, p = scores[a:b], perm[a:b].astype(np.int64)
+        assert np.array_equal(p[:64], G[f"f{f}_top_idx"]), f
+        assert np.array_equal(s[p[:64]], G[f"f{f}_top_score"]), f
+        assert np.array_equal(s[::97], G[f"f{f}_pred_every97"]), f
+        assert digest(s) == str(G[f"f{f}_pred_sha"][0]), f
+        assert digest(p) == str(G[f"f{f}_rank_sha"][0]), f
+    sp.close()
+    fo.close()
+
+
+@pytest.fixture(params=["auto", "multi", "multi_col", "multi_rowmajor"])
+def fit_path(request, monkeypatch):
+    monkeypatch.setenv("FAMSEER_FIT_PATH", "auto" if request.param == "auto" else "multi")
+    if request.param == "multi_col":
+        monkeypatch.setenv("FAMSEER_HIST", "col")
+    elif request.param == "multi_rowmajor":
+        monkeypatch.setenv("FAMSEER_HIST", "rowmajor")
+    return request.param
+
+
+def test_c4_full_size_matches_reference(dev, fit_path):
+    """C4: all three BERT-base families in one fit, T = 500, every trainer shape."""
+    G = golden("c4")
+    W = workload("c4")
+    fams = [int(f) for f in G["families"]]
+    check(dev, W, G, fams, fams, int(G["trees"][0]))
+
+
+def test_c5_full_size_matches_reference(dev):
+    """C5 as the bench runs it: all 64 families in one fit (T = 1000); families 0, 17 and 63
+    are pinned to the reference."""
+    G = golden("c5")
+    W = workload("c5")
+    fams = [int(f) for f in G["families"]]
+    check(dev, W, G, fams, fams, int(G["trees"][0]))
+
+
+@pytest.mark.parametrize("hist", ["col", "rowmajor"])
+def test_c5_pinned_families_other_histograms(dev, monkeypatch, hist):
+    """The pinned C5 families alone, through the other multi-kernel histogram builds."""
+    monkeypatch.setenv("FAMSEER_FIT_PATH", "multi")
+    monkeypatch.setenv("FAMSEER_HIST", hist)
+    G = golden("c5")
+    fams = [int(f) for f in G["families"]]
+    W = sub_workload(workload("c5"), fams)
+    check(dev, W, G, fams, list(range(len(fams))), int(G["trees"][0]))

@@ -75,18 +75,25 @@ def random_forest(rng, d, trees, depth, n_thr=6, ragged=True):
                            np.array(thr), np.array(le, np.int32), np.array(ri, np.int32), np.array(val))
 
 
-@pytest.mark.parametrize("depth,trees,n_thr,d", [(3, 200, 6, 40), (1, 10, 3, 40), (5, 50, 8, 40),
-                                                 (3, 300, 2000, 2), (10, 5, 4, 40), (3, 1200, 40000, 2)])
-def test_random_forests_multi_segment(dev, orc, depth, trees, n_thr, d):
+@pytest.mark.parametrize("depth,trees,n_thr,d,rows", [(3, 200, 6, 40, 700), (1, 10, 3, 40, 700), (5, 50, 8, 40, 700),
+                                                      (3, 300, 2000, 2, 700), (10, 5, 4, 40, 700),
+                                                      (3, 1200, 40000, 2, 700), (7, 30, 6, 40, 700),
+                                                      (8, 20, 6, 40, 700), (4, 64, 6, 41, 700),
+                                                      (3, 100, 6, 164, 40000), (3, 33, 6, 41, 40000)])
+def test_random_forests_multi_segment(dev, orc, depth, trees, n_thr, d, rows):
     # (3, 300, 2000, 2): >254 distinct thresholds per feature -> 16-bit codes
     # (10, 5, 4, 40): deeper than the heap limit -> generic pre-order kernel
     # (3, 1200, 40000, 2): > 6144 unique thresholds -> threshold tables searched in global memory
+    # (7/8, ...): deepest heap trees - pre-order leaf ids above 255 (uint16 leaf ids)
+    # (4, 64, 6, 41): levels below the register-held top three; odd row width (no bulk row copies)
+    # (3, 100, 6, 164, 40000): 256-candidate tiles, bulk-copied rows with a partial last stage;
+    # (3, 33, 6, 41, 40000): the same with coalesced row loads and a partial last tree pass
     rng = np.random.default_rng(depth * 100 + trees)
     ens = [random_forest(rng, d, trees, depth, n_thr) for _ in range(3)]
     fo = fs.Forest(dev, 3)
     for i, e in enumerate(ens):
         fo.upload(i, e)
-    seg = [0, 700, 700 + 1, 700 + 1 + 300]
+    seg = [0, rows, rows + 1, rows + 1 + 300]
     # rows hit thresholds exactly sometimes (x == t must go left)
     x = rng.normal(0, 1, size=(seg[-1], d))
     for f in range(d):

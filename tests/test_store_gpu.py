@@ -1,13 +1,14 @@
 """Device-resident training store (fs_store): the reference's
 train_cost_model appends each measured batch to the family's training set and refits
 (costmodel.cpp:224-235). Every refit from the store must be bit-identical to fs_fit on the same
-rows (which the other suites pin to the oracle), through incremental merges, bulk appends, -0.0
+rows and to the oracle's fit of them (trees, base, train_mse_by_round), through incremental merges, bulk appends, -0.0
 families, multi-family batches and subset refits; the maintained canonical order must be the
 lexicographic (features..., target) order of costmodel.cpp:161-173."""
 import numpy as np
 import pytest
 
 import bench
+import oracle
 import paper_2201_00194_b200 as fs
 
 pytestmark = pytest.mark.gpu
@@ -44,8 +45,15 @@ def _check_store(dev, st, F, tag):
             assert np.array_equal(x[c], x[o]) and np.array_equal(y[c], y[o]), (tag, f)
     fb = fs.Forest(dev, F)
     fb.fit(np.concatenate(xs), np.concatenate(ys), seg=seg, params=P)
+    orc = oracle.orc()
     for f in range(F):
-        _same(fa.export(f), fb.export(f), (tag, f))
+        got = fa.export(f)
+        _same(got, fb.export(f), (tag, f))
+        if len(ys[f]):  # and against the CPU restatement of fit (costmodel.cpp:152-222), not only fs_fit
+            exp = orc.fit(xs[f], ys[f], trees=P.trees, depth=P.depth, lr=P.learning_rate,
+                          min_split=P.min_samples_split)
+            _same(got, exp, (tag, f, "oracle"))
+            assert np.array_equal(got.mse, exp.mse), (tag, f, "mse")
 
 
 def _c3(orc, seed):
