@@ -152,6 +152,20 @@ def build_workload(cfg_name, seed):
     return W
 
 
+def workload_config(W):
+    """The workload the line is quoted on (identical dict in the native and reference arms)."""
+    return {"workload": W["desc"], "config": W["config"], "model": W["model"], "families": W["families"],
+            "candidates_per_step": int(W["pool_seg"][-1]), "train_rows_per_step": int(W["tr_seg"][-1]),
+            "trees": W["trees"], "depth": 3, "learning_rate": 0.1, "pad_dim": PAD, "seed": 1000}
+
+
+def s8d_fit_bytes(rows, trees, depth=3, d=PAD, s_bin=1):
+    """SURVEY.md 8(d) algorithmic bytes of one fit of a family of `rows` rows: one-time binning read
+    N*D*8, per level N*D*s_bin codes + 9N (residual + node id), per round 24N (residual,
+    prediction, leaf update)."""
+    return rows * d * 8 + trees * depth * (rows * d * s_bin + 9 * rows) + trees * 24 * rows
+
+
 def shard_workload(W, rank, world):
     """This rank's families of a global workload (deterministic LPT on rows*T + pool*T,
     paper_2201_00194_b200/sharding.py); records the global unit counts for whole-job rates."""
@@ -274,10 +288,12 @@ def run_native(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.shard == "families":
         # strong scaling: ONE global workload, families LPT-partitioned over ranks
-        W = shard_workload(build_workload(args.config, seed=1000), rank, world)
+        W_global = build_workload(args.config, seed=1000)
+        W = shard_workload(W_global, rank, world)
     else:
         # weak scaling: every rank tunes its own copy of the workload (own seed)
         W = build_workload(args.config, seed=1000 + rank)
+        W_global = W
     dev = fs.Device(local_rank)
     stream = torch.cuda.ExternalStream(dev.stream)
     spaces = fs.Spaces(dev, W["spaces"])
@@ -459,6 +475,8 @@ def run_native(args, rank, world, local_rank):
         n_l, ms = prof_all["fit_hist_build"]
         cands.append(("fit_hist_build", ms, ctr_one["hist_bytes"], n_l,
                       "rows*(nrep*code_bytes + 8 residual + 4 index), rows counted on device", None))
+    fam_rows = [int(W["tr_seg"][f + 1] - W["tr_seg"][f]) for f in range(F)]
+    s8d_fit = sum(s8d_fit_bytes(n, W["trees"]) for n in fam_rows)  # one fit of every family of this rank
     if "fit_resident" in prof_all:
         n_l, ms = prof_all["fit_resident"]
         cands.append(("fit_resident", ms, ctr_one["hist_bytes"], n_l,
@@ -475,8 +493,21 @@ def run_native(args, rank, world, local_rank):
     if cands:
         name, ms, nbytes, n_l, formula, note = max(cands, key=lambda r: r[1])
         ach = nbytes / (ms / 1e3) / 1e9
+        # the same kernel against SURVEY.md 8(d)'s per-unit bytes (every row and feature at every
+        # level, not only the rows the kernel actually histograms)
+        s8d = None
+        if name == "fit_resident":
+            s8d = {"bytes_per_launch": s8d_fit, "formula": "sum_f N_f*D*8 + T*depth*(N_f*D + 9*N_f) + T*24*N_f, "
+                   "D = pad_dim 164, s_bin = 1 (u8 codes), depth 3"}
+        elif name == "fit_hist_build":
+            per_level = sum(n * (PAD + 9) for n in fam_rows)
+            s8d = {"bytes_per_launch": per_level, "formula": "per level: sum_f N_f*D*s_bin + 9*N_f, D = 164, s_bin = 1"}
+        if s8d:
+            a8 = s8d["bytes_per_launch"] * max(n_l, 1) / (ms / 1e3) / 1e9
+            s8d.update({"achieved": round(a8, 2), "frac": round(a8 / peak, 5)})
         roofline = {"bound": "hbm", "kernel": name, "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
-                    "frac": round(ach / peak, 5), "peak_kind": peak_kind, "traffic": ncu_traffic(name),
+                    "frac": round(ach / peak, 5), "frac_s8d": s8d["frac"] if s8d else None, "s8d": s8d,
+                    "peak_kind": peak_kind, "traffic": ncu_traffic(name),
                     "algorithmic_bytes_per_launch": nbytes / max(n_l, 1), "launches": n_l,
                     "avg_launch_ms": ms / max(n_l, 1), "bytes_formula": formula,
                     "measured": "CUDA events on the device stream, one untimed replica step without CUDA graphs",
@@ -499,11 +530,12 @@ def run_native(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (random candidates from the model's knob spaces, quadratic-bowl latencies)",
-        "config": {"workload": W["desc"], "config": args.config, "model": W["model"], "families": W["families"],
-                   "candidates_per_step": P_job, "train_rows_per_step": N_job, "trees": W["trees"],
-                   "depth": 3, "pad_dim": PAD, "parallelism": (f"families LPT-sharded over {world} GPU(s)" if args.shard == "families" else
-                                   f"family-parallel replicas x{world}"),
-                   "l2": "flushed between timed steps (256 MB write)"},
+        "config": workload_config(W_global),
+        "parallelism": (f"families LPT-sharded over {world} GPU(s) (one global workload)" if args.shard == "families"
+                        else f"{world} independent replica(s) of the workload, one per GPU"),
+        "l2": "flushed between timed steps (256 MB write)",
+        "family_ids": fam_ids,
+        "family_model_sha": model_digests(forest, F, fam_ids),
         "train_rows_per_s": N_job * args.steps / (total_ms / 1e3),
         "train_row_rounds_per_s": N_job * W["trees"] * args.steps / (total_ms / 1e3),
         "phases_ms": {"score": score_ms, "fit": fit_ms},
@@ -519,12 +551,52 @@ def run_native(args, rank, world, local_rank):
         "e2e": e2e,
         "incremental": incremental,
     }
+    if dist is not None:  # every rank's family digests on rank 0
+        parts = [None] * world
+        dist.all_gather_object(parts, (fam_ids, result["family_model_sha"]))
+        result["family_ids"] = sorted(i for ids, _ in parts for i in ids)
+        result["family_model_sha"] = {k: v for _, d in parts for k, v in sorted(d.items(), key=lambda kv: int(kv[0]))}
     if rank == 0 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(W, forest, x_tr.cpu().numpy(), min_seconds=args.cpu_seconds)
+    if world == 1 and not args.no_secondary and args.config != "c5":
+        result["secondary_c5"] = secondary_c5()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def secondary_c5():
+    """BASELINE configs[4] (64 families x 65,536 candidates/rows, T = 1000) at N = 1, where the
+    trainer's histogram build - not a latency chain - dominates: its own bench line (a child
+    bench.py, 3 warm-up + 2 timed steps, inputs resident, L2 flushed), kept as a block."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", "c5", "--steps", "2", "--warmup", "3", "--no-e2e",
+           "--no-cpu", "--no-secondary"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
+        d = json.loads(line)
+    except Exception as e:  # pragma: no cover - reported, never fatal for the headline line
+        return {"error": f"{type(e).__name__}: {e}"}
+    keep = ("value", "unit", "ms_per_step", "steps", "warmup", "config", "train_rows_per_s", "train_row_rounds_per_s",
+            "phases_ms", "roofline", "clocks", "gpu_launches", "kernel_ms_one_step", "fit_nodes")
+    return {k: d.get(k) for k in keep}
+
+
+def model_digests(forest, F, fam_ids):
+    """sha256 of every fitted family model (pre-order trees, base, train_mse_by_round), keyed by
+    global family id: equal digests across --gpus N runs show the per-family results do not depend
+    on which GPU computed them."""
+    import hashlib
+
+    out = {}
+    for f in range(F):
+        e = forest.export(f)
+        h = hashlib.sha256(np.float64(e.base).tobytes())
+        for k in ("offsets", "feature", "threshold", "left", "right", "value", "mse"):
+            h.update(np.ascontiguousarray(getattr(e, k)).tobytes())
+        out[str(fam_ids[f])] = h.hexdigest()[:16]
+    return out
 
 
 def measure_incremental(dev, spaces, W, params, timed, steps, g=64, warm=2):
@@ -776,14 +848,33 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (same generator and seed as the native arm's rank 0)",
-            "config": {"workload": W["desc"], "config": args.config, "model": W["model"], "families": W["families"],
-                       "candidates_per_step": P, "train_rows_per_step": N, "trees": W["trees"], "pad_dim": PAD},
+            "config": workload_config(W),
             "train_rows_per_s": N * args.steps / total,
             "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": cores, "kind": "reference",
                              "sample": ("full rounds" if not extrap else f"sampled rounds {plan}, extrapolated")
                              + " of the workload, one thread per family (oracle/_ref)", "extrapolated": extrap,
                              "host_cpu": _cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def self_launch(n):
+    """`bench.py --gpus N` without a launcher: re-exec under torchrun, one rank per GPU (NCCL over
+    NVLink for the top-k all-gather; NCCL's INFO log, which names the communicator's ranks, goes
+    to stderr so stdout keeps the one JSON line)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execvpe(sys.executable, cmd, env)
 
 
 def main():
@@ -796,15 +887,21 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--shard", default="replicate", choices=["replicate", "families"],
-                    help="replicate: every rank tunes its own workload copy (weak scaling); families: one "
-                         "global workload, families LPT-partitioned over ranks (strong scaling)")
+    ap.add_argument("--shard", default=None, choices=["replicate", "families"],
+                    help="families (default for N > 1): one global workload, families LPT-partitioned over "
+                         "ranks (strong scaling, SURVEY 8e); replicate: every rank tunes its own workload copy "
+                         "(weak scaling)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary C5 block at N = 1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args.gpus)  # does not return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.shard is None:
+        args.shard = "families" if world > 1 else "replicate"
     if args.impl == "reference":
         res = run_reference(args, rank, world)
     else:
