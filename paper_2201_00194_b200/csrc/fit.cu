@@ -228,7 +228,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
     FS_CUDA(cudaGetLastError());
     if (max_trees > 0) {
       const int64_t chains = static_cast<int64_t>(F) * max_trees;
-      mse_fold_kernel<<<static_cast<unsigned>(ceil_div(chains, 64)), 64, 0, s>>>(fam_d, st_d, F, ebuf, max_trees, 0, 0,
+      ProfScope prof(dev, "fit_mse");
+      mse_fold_kernel<<<static_cast<unsigned>(ceil_div(chains, 4)), 128, 0, s>>>(fam_d, st_d, F, ebuf, max_trees, 0, 0,
                                                                                  max_trees, mse_d, max_trees);
       dev->count_launch();
       FS_CUDA(cudaGetLastError());
@@ -439,7 +440,8 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
     if ((round + 1) % mse_k != 0 && round + 1 != max_trees) return;
     const int t_lo = (round / mse_k) * mse_k, t_hi = round + 1;
     const int64_t chains = static_cast<int64_t>(F) * (t_hi - t_lo);
-    mse_fold_kernel<<<static_cast<unsigned>(ceil_div(chains, 64)), 64, 0, s>>>(fam_d, st_d, F, ebuf, mse_k, n_tot,
+    ProfScope prof(dev, "fit_mse");
+    mse_fold_kernel<<<static_cast<unsigned>(ceil_div(chains, 4)), 128, 0, s>>>(fam_d, st_d, F, ebuf, mse_k, n_tot,
                                                                                t_lo, t_hi, mse_d, max_trees);
     dev->count_launch();
     FS_CUDA(cudaGetLastError());

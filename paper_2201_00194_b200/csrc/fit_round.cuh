@@ -1948,42 +1948,62 @@ __global__ void commit_kernel(const FamDesc* __restrict__ fam, FamState* __restr
 }  // namespace
 
 // mse[f][t] = (sum over canonical rows p, in order, of e*e) / n (costmodel.cpp:215-220) for
-// every committed round t in [t_lo, t_hi) of every family: one thread per (family, round) chain,
-// every add separately rounded. Round t's e of family f sits at
+// every committed round t in [t_lo, t_hi) of every family: one WARP per (family, round) chain -
+// the warp loads 128 consecutive e's at a time (coalesced, the next 128 in flight), squares them
+// in parallel, and adds the squares in row order (shuffled to every lane; every add separately
+// rounded, so the chain is the reference's). Round t's e of family f sits at
 //   ring   (ring_stride > 0): ebuf[(t % K) * ring_stride + pos0 + p]
 //   blocks (ring_stride = 0): ebuf[pos0 * K + (t % K) * n + p]   (K = all rounds, resident fit)
 __global__ void mse_fold_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st, int F,
                                 const double* __restrict__ ebuf, int K, int64_t ring_stride, int t_lo, int t_hi,
                                 double* __restrict__ mse, int max_trees) {
   const int W = t_hi - t_lo;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (W <= 0 || i >= static_cast<int64_t>(F) * W) return;
-  const int f = static_cast<int>(i / W), t = t_lo + static_cast<int>(i % W);
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (W <= 0 || w >= static_cast<int64_t>(F) * W) return;
+  const int f = static_cast<int>(w / W), t = t_lo + static_cast<int>(w % W);
   const FamDesc fd = fam[f];
   if (t >= st[f].ntrees || fd.n <= 0) return;
   const int n = fd.n;
   const double* e = ring_stride > 0 ? ebuf + static_cast<int64_t>(t % K) * ring_stride + fd.pos0
                                     : ebuf + fd.pos0 * K + static_cast<int64_t>(t % K) * n;
+  double x[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = 32 * c + lane;
+    x[c] = i < n ? e[i] : 0.0;
+  }
   double s = 0.0;
-  int p = 0;
-  if (n >= 8) {  // the next 8 loads are in flight while the current 8 squares are added
-    double a[8];
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    double y[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = e[k];
-    for (p = 8; p + 8 <= n; p += 8) {
-      double b[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) b[k] = e[p + k];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s = fs_add(s, fs_mul(a[k], a[k]));
-#pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] = b[k];
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + 128 + 32 * c + lane;
+      y[c] = i < n ? e[i] : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s = fs_add(s, fs_mul(a[k], a[k]));
+    for (int c = 0; c < 4; ++c) {
+      const int base = i0 + 32 * c;
+      if (base >= n) break;
+      const double sq = fs_mul(x[c], x[c]);
+      const int m = min(32, n - base);
+      if (m == 32) {
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 8) {
+          double q[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) q[k] = __shfl_sync(0xffffffffu, sq, l0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, q[k]);
+        }
+      } else {
+        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, sq, l));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = y[c];
   }
-  for (; p < n; ++p) s = fs_add(s, fs_mul(e[p], e[p]));
-  mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(s, static_cast<double>(n));
+  if (lane == 0) mse[static_cast<int64_t>(f) * max_trees + t] = fs_div(s, static_cast<double>(n));
 }
 
 namespace {
