@@ -4,7 +4,11 @@
 //   engine_ref   - with the reference's own costmodel.o + family.o
 //   engine_b200  - with libfamtune_b200.so in their place (the drop-in: every fit / predict /
 //                  family lookup of the unchanged scheduler runs through the B200 library)
-// tests/test_engine_e2e.py requires the two outputs to be byte-identical.
+//   engine_b200_batched - -DFS_BATCHED_ENGINE: famtune::gpu::BatchedTuningEngine (the batched
+//                  caller, paper_2201_00194_b200/host/batched_engine.cpp) on the drop-in
+// tests/test_engine_e2e.py requires the outputs to be byte-identical. The loop's wall time goes
+// to stderr ("engine_wall_s <seconds>").
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +20,12 @@
 #include "famtune/graph.hpp"
 #include "famtune/scheduler.hpp"
 #include "famtune/simbackend.hpp"
+#ifdef FS_BATCHED_ENGINE
+#include "famtune/batched_engine.hpp"
+using Engine = famtune::gpu::BatchedTuningEngine;
+#else
+using Engine = famtune::TuningEngine;
+#endif
 
 using namespace famtune;
 
@@ -46,8 +56,11 @@ int main(int argc, char** argv) {
   opt.seed = seed;
   opt.cost_model.trees = trees;
   const ClusterAlgo ca = algo == 1 ? ClusterAlgo::ByOpCount : algo == 2 ? ClusterAlgo::ByOpSequence : ClusterAlgo::ByCoreOp;
-  TuningEngine engine(backend, foresee ? make_foresee_policy(ca) : make_baseline_policy(ca), opt);
+  const auto t0 = std::chrono::steady_clock::now();
+  Engine engine(backend, foresee ? make_foresee_policy(ca) : make_baseline_policy(ca), opt);
   const auto state = engine.run();
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::fprintf(stderr, "engine_wall_s %.6f\n", wall);
   std::fputs(curve_to_csv(state).c_str(), stdout);
   std::fputs(engine.registry().to_csv().c_str(), stdout);
   for (const auto& m : engine.models()) {
