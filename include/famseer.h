@@ -135,7 +135,7 @@ int fs_rank_d(fs_device* dev, int32_t n_segments, const int64_t* seg_h, const do
 /* ---- score: the batched tune_step scoring block (scheduler.cpp:187-192) ---------------------
  * featurize -> predict -> rank in one call; the feature matrix never leaves the device.
  * scores[i] and perm[seg[f] + k] as for fs_predict / fs_rank. Either output may be NULL on the
- * host-pointer variant. */
+ * host-pointer variant; fs_score_d with perm_d NULL scores without ranking. */
 int fs_score(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t n_segments,
              const int64_t* seg, const int32_t* space_of, const int32_t* assign, int32_t pad_dim,
              double* scores, int32_t* perm);

@@ -257,7 +257,8 @@ class Spaces:
     def score_d(self, forest: "Forest", space_of_t, assign_t, pad_dim: int, seg, scores_t, perm_t):
         sg, sp = _seg(seg)
         _check(_lib().fs_score_d(self.dev.h, self.h, forest.h, len(sg) - 1, sp, space_of_t.data_ptr(),
-                                 assign_t.data_ptr(), pad_dim, scores_t.data_ptr(), perm_t.data_ptr()))
+                                 assign_t.data_ptr(), pad_dim, scores_t.data_ptr(),
+                                 None if perm_t is None else perm_t.data_ptr()))
 
 
 class Forest:

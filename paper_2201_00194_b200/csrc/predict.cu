@@ -101,6 +101,11 @@ struct Smem {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
                                                            const PredJob* __restrict__ jobs, int tc, int ds,
                                                            int max_dmodel, int max_depth, int max_uthr,
                                                            double* __restrict__ scores, uint16_t* __restrict__ leaf_out,
-                                                           uint32_t* err, SpaceTabs sp) {
+                                                           uint32_t* err, SpaceTabs sp, int fast) {
   extern __shared__ __align__(16) unsigned char smem[];
   const PredJob job = jobs[blockIdx.x];
   const PredModel M = models[job.model];
@@ -146,6 +151,8 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
   uint16_t* s_leafid = reinterpret_cast<uint16_t*>(smem + L.leafid);
   uint8_t* s_slot = smem + L.slots;
   const int tcp = tc + 4;  // slot row pitch: tcp/4 odd -> lanes (trees) store to distinct banks
+  // depth-3 register walk: every model of the launch has depth 3, u8 codes and rows <= 256 bytes
+  const bool kFast = sizeof(CodeT) == 1 && fast != 0;
 
   const int depth = M.depth, d_model = M.d_model;
   const int n_trees = M.meta ? M.meta->n_trees : M.n_trees;
@@ -312,6 +319,36 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
       };
       uint8_t* srow = s_slot + lane * tcp;
       int c = warp;
+      if (kFast) {
+        // depth-3 trees, u8 codes, rows of <= 256 bytes: the seven node words become byte-packed
+        // (code offset, rank) tables in registers, so a level is one byte-permute select, one
+        // shared load and one compare; eight candidates' walks are interleaved level by level
+        const uint32_t o0 = w0 & 0xFFu, k0 = w0 >> 16;
+        const uint32_t o12 = (w1 & 0xFFu) | (w2 & 0xFFu) << 8, k12 = (w1 >> 16) | (w2 >> 16) << 8;
+        const uint32_t o36 = (w3 & 0xFFu) | (w4 & 0xFFu) << 8 | (w5 & 0xFFu) << 16 | (w6 & 0xFFu) << 24;
+        const uint32_t k36 = (w3 >> 16) | (w4 >> 16) << 8 | (w5 >> 16) << 16 | (w6 >> 16) << 24;
+        const uint32_t cb = smem_u32(codes) + static_cast<uint32_t>(c * ds);
+        constexpr int G = 8;
+        for (; c + (G - 1) * kWarps < rows; c += G * kWarps) {
+          const uint32_t rb = cb + static_cast<uint32_t>((c - warp) * ds);
+          uint32_t b0[G], b1[G], v[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) v[g] = lds_u8(rb + static_cast<uint32_t>(g * kWarps * ds) + o0);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            b0[g] = v[g] > k0 ? 1u : 0u;
+            const uint32_t sel = 0x4440u | b0[g];
+            v[g] = lds_u8(rb + static_cast<uint32_t>(g * kWarps * ds) + __byte_perm(o12, 0, sel));
+            b1[g] = v[g] > __byte_perm(k12, 0, sel) ? 1u : 0u;
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t i = 2 * b0[g] + b1[g], sel = 0x4440u | i;
+            v[g] = lds_u8(rb + static_cast<uint32_t>(g * kWarps * ds) + __byte_perm(o36, 0, sel));
+            srow[c + g * kWarps] = static_cast<uint8_t>(2 * i + (v[g] > __byte_perm(k36, 0, sel) ? 1u : 0u));
+          }
+        }
+      }
       for (; c + 3 * kWarps < rows; c += 4 * kWarps) {  // four independent walks in flight
         const int q0 = walk(codes + static_cast<size_t>(c) * ds);
         const int q1 = walk(codes + static_cast<size_t>(c + kWarps) * ds);
@@ -363,6 +400,7 @@ struct HeapGroup {
   std::vector<PredModel> models;
   std::vector<int64_t> r0, rows, leaf0;  // per model's segment
   int max_dmodel = 0, max_depth = 0, max_uthr = 0;
+  bool all_depth3 = true;
 };
 
 template <typename CodeT, bool kLeaves, bool kSmemThr, bool kFused>
@@ -407,7 +445,8 @@ void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, do
   auto launch = [&](auto* fn) {
     FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     fn<<<static_cast<unsigned>(jobs.size()), kThreads, smem, dev->stream>>>(
-        x, d, md, jd, tc, ds, g.max_dmodel, g.max_depth, g.max_uthr, scores, leaf_out, dev->err_d, sp);
+        x, d, md, jd, tc, ds, g.max_dmodel, g.max_depth, g.max_uthr, scores, leaf_out, dev->err_d, sp,
+        sizeof(CodeT) == 1 && g.all_depth3 && ds <= 256 ? 1 : 0);
   };
   if (bulk) launch(predict_kernel<CodeT, kLeaves, kSmemThr, kFused, true>);
   else launch(predict_kernel<CodeT, kLeaves, kSmemThr, kFused, false>);
@@ -460,6 +499,7 @@ void launch_predict_impl(fs_device* dev, const fs_forest* fo, int32_t nseg, cons
     g.leaf0.push_back(lo);
     g.max_dmodel = std::max(g.max_dmodel, dm);
     g.max_depth = std::max(g.max_depth, m.depth);
+    g.all_depth3 = g.all_depth3 && m.depth == 3;
     g.max_uthr = std::max(g.max_uthr, m.n_uthr);
   }
   for (int cb = 0; cb < 2; ++cb)

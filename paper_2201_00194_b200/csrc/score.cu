@@ -37,7 +37,7 @@ static void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* f
     launch_featurize(dev, sp, n, space_of_d, assign_d, pad, x);
     launch_predict(dev, fo, nseg, seg, pad, x, scores_d, nullptr);
   }
-  launch_rank(dev, nseg, seg, scores_d, perm_d);
+  if (perm_d) launch_rank(dev, nseg, seg, scores_d, perm_d);  // perm NULL: scores only
 }
 
 // pairwise_accuracy's pair count (costmodel.cpp:255-276): credit is counted in half units, so

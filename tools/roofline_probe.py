@@ -89,14 +89,25 @@ def main():
         out["featurize"] = {"ms": ms, "bytes": nb, "gbs": nb / ms / 1e6, "frac": nb / ms / 1e6 / peak}
         rng = np.random.default_rng(0)
         xs = x[: min(P, 65536)].cpu().numpy()
+        # predict (feature rows from HBM: P*(8*d + 8) bytes) and the fused score
+        # (descriptors in, score out: P*(64 + 4 + 8)) at the bench's tree counts; rows (688 MB at
+        # 8 x 65,536) exceed L2, so every repetition streams them from HBM
+        for T in sorted({100, args.trees}):
+            fo = fs.Forest(dev, F)
+            for f in range(F):
+                fo.upload(f, random_model(rng, xs, T))
+            fo.predict_d(x, seg, scores)
+            ms = timeit(lambda: fo.predict_d(x, seg, scores))
+            nb = P * (8 * bench.PAD + 8)
+            key = "predict" if T == args.trees else f"predict_T{T}"
+            out[key] = {"ms": ms, "trees": T, "bytes": nb, "gbs": nb / ms / 1e6, "frac": nb / ms / 1e6 / peak,
+                        "node_visits_per_s": P * T * 3 / ms * 1e3}
+            ms = timeit(lambda: sp.score_d(fo, so, asg, bench.PAD, seg, scores, None))  # perm NULL: no rank
+            nb = P * (4 * 16 + 4 + 8)
+            out[f"score_fused_T{T}"] = {"ms": ms, "trees": T, "bytes": nb, "gbs": nb / ms / 1e6,
+                                        "frac": nb / ms / 1e6 / peak, "node_visits_per_s": P * T * 3 / ms * 1e3,
+                                        "note": "featurize -> predict fused (no rank)"}
         fo = fs.Forest(dev, F)
-        for f in range(F):
-            fo.upload(f, random_model(rng, xs, args.trees))
-        fo.predict_d(x, seg, scores)
-        ms = timeit(lambda: fo.predict_d(x, seg, scores))
-        nb = P * (8 * bench.PAD + 8)
-        out["predict"] = {"ms": ms, "trees": args.trees, "bytes": nb, "gbs": nb / ms / 1e6, "frac": nb / ms / 1e6 / peak,
-                          "node_visits_per_s": P * args.trees * 3 / ms * 1e3}
         y = torch.from_numpy(np.resize(W["tr_y"], P)).cuda()
         os.environ["FAMSEER_NO_GRAPH"] = "1"
         dev.profile("fit_hist_build,fit_exact,fit_leaf,fit_screen,fit_partition,fit_rounds")
