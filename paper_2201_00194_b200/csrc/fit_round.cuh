@@ -623,8 +623,8 @@ __global__ void hist_derive_kernel(const FamDesc* __restrict__ fam, const FamSta
 // The reference folds sums sequentially (error <= gamma_n * S each), R = T - L rounds once,
 // then ((L*L)/lc + (R*R)/rc) - (T*T)/n rounds ~5 more times; the screen's sums are exact on
 // the quantised residuals (quantisation <= n * scale / 2). Factor 2 covers both sides.
-__device__ __forceinline__ void screen_gain(int64_t ls, int64_t ts, int lc, int n, double scale, double S, double& g,
-                                            double& lo, double& hi) {
+__device__ __forceinline__ void screen_gain_d(int64_t ls, int64_t ts, int lc, int n, double scale, double S, double& g,
+                                              double& delta) {
   const double u = 1.1102230246251565e-16;
   const double L = static_cast<double>(ls) * scale, T = static_cast<double>(ts) * scale;
   const double R = static_cast<double>(ts - ls) * scale;
@@ -642,7 +642,13 @@ __device__ __forceinline__ void screen_gain(int64_t ls, int64_t ts, int lc, int 
   const double dA = ((2.0 * fabs(L) + EL) * EL + 4.0 * u * aL * aL) * ilc;
   const double dB = ((2.0 * fabs(R) + ER) * ER + 4.0 * u * aR * aR) * irc;
   const double dP = ((2.0 * fabs(T) + ET) * ET + 4.0 * u * aT * aT) * in;
-  const double delta = 2.0 * (dA + dB + dP + 6.0 * u * (A + B + P)) * (1.0 + 8.0 * u) + 1e-300;
+  delta = 2.0 * (dA + dB + dP + 6.0 * u * (A + B + P)) * (1.0 + 8.0 * u) + 1e-300;
+}
+
+__device__ __forceinline__ void screen_gain(int64_t ls, int64_t ts, int lc, int n, double scale, double S, double& g,
+                                            double& lo, double& hi) {
+  double delta;
+  screen_gain_d(ls, ts, lc, n, scale, S, g, delta);
   lo = g - delta;
   hi = g + delta;
 }
