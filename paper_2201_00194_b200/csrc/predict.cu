@@ -25,6 +25,7 @@
 // HBM traffic per candidate: 8*d (row) + 8 (score) [+ 2*T leaf ids] for predict, 4*16 + 4 + 8
 // for the fused score; the model is read from L2 once per tile.
 #include <algorithm>
+#include <cstdlib>
 
 #include "forest.cuh"
 
@@ -70,10 +71,10 @@ struct PredJob {
 
 // Shared-memory carve-up, identical on host and device.
 struct Smem {
-  size_t codes, nodes, lrleaf, leafid, slots, uthr, uoff, rows, bars, total;
+  size_t codes, nodes, lrleaf, leafid, slots, uthr, uoff, rows, bars, fsrc, total;
   __host__ __device__ static size_t al(size_t o) { return (o + 15) & ~size_t(15); }
   __host__ __device__ Smem(int tc, int ds, int code_bytes, int max_depth, bool leaves, int max_uthr, int max_dmodel,
-                           bool smem_thr, int row_doubles) {
+                           bool smem_thr, int row_doubles, bool fused = false) {
     const size_t mnint = (size_t{1} << max_depth) - 1, mnleaf = size_t{1} << max_depth;
     size_t o = 0;
     codes = o;
@@ -88,12 +89,14 @@ struct Smem {
     o = al(o + 32 * static_cast<size_t>(tc + 4));
     uthr = o;
     o = al(o + (smem_thr ? static_cast<size_t>(max_uthr) * 8 : 0));
-    uoff = o;
-    o = al(o + (smem_thr ? static_cast<size_t>(max_dmodel + 1) * 4 : 0));
+    uoff = o;  // per compiled feature: (row column, threshold segment start, length, top step)
+    o = al(o + static_cast<size_t>(max_dmodel + 1) * 16);
     rows = o;  // predict: kStages x kStageRows feature rows
     o = al(o + static_cast<size_t>(row_doubles) * 8);
     bars = o;
     o = al(o + kStages * 8);
+    fsrc = o;  // fused score: per warp, every model feature's descriptor sources for one knob count
+    o = al(o + (fused ? static_cast<size_t>(kWarps) * ds * 4 : 0));
     total = o;
   }
 };
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
   const PredJob job = jobs[blockIdx.x];
   const PredModel M = models[job.model];
   const Smem L(tc, ds, sizeof(CodeT), max_depth, kLeaves, max_uthr, max_dmodel, kSmemThr,
-               kFused || !kBulk ? 0 : kStages * kStageRows * d);
+               kFused || !kBulk ? 0 : kStages * kStageRows * d, kFused);
   CodeT* codes = reinterpret_cast<CodeT*>(smem + L.codes);  // [tc][ds]
   uint32_t* s_nodes = reinterpret_cast<uint32_t*>(smem + L.nodes);
   double* s_lrleaf = reinterpret_cast<double*>(smem + L.lrleaf);
@@ -164,90 +167,169 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
 
   // threshold tables the codes are searched in: staged in shared memory when they fit
   const double* uthr = M.uthr;
-  const int32_t* uoff = M.uoff;
   if (kSmemThr) {
     double* su = reinterpret_cast<double*>(smem + L.uthr);
-    int32_t* so = reinterpret_cast<int32_t*>(smem + L.uoff);
     for (int i = tid; i < M.n_uthr; i += kThreads) su[i] = __ldg(M.uthr + i);
-    for (int i = tid; i <= d_model; i += kThreads) so[i] = __ldg(M.uoff + i);
     uthr = su;
-    uoff = so;
   }
-  auto code_of = [&](int f, double v) {
-    int lo = uoff[f], hi = uoff[f + 1];
-    const int first = lo;
-    while (lo < hi) {  // count of unique thresholds strictly below v
-      const int mid = (lo + hi) >> 1;
-      if (uthr[mid] < v) lo = mid + 1;
-      else hi = mid;
+  // per compiled feature f: its row column, its unique-threshold segment [lo, lo + n) and the
+  // highest power of two <= n, one 16-byte shared load per code
+  int4* s_meta = reinterpret_cast<int4*>(smem + L.uoff);
+  for (int f = tid; f < d_model; f += kThreads) {
+    const int lo = __ldg(M.uoff + f), n = __ldg(M.uoff + f + 1) - lo;
+    s_meta[f] = make_int4(fmap ? __ldg(fmap + f) : f, lo, n, n > 0 ? 1 << (31 - __clz(n)) : 0);
+  }
+  // code(v) = #{unique thresholds of the feature < v} by branchless binary lifting over the
+  // sorted segment (the same step sequence for every value of one feature, so searches of
+  // several rows interleave without divergence)
+  auto code_of = [&](const int4 m, double v) {
+    int pos = 0;
+    for (int step = m.w; step > 0; step >>= 1) {
+      const int q = pos + step;
+      if (q <= m.z && uthr[m.y + q - 1] < v) pos = q;
     }
-    return static_cast<CodeT>(lo - first);
+    return static_cast<CodeT>(pos);
   };
 
   // ---- 1. codes ---------------------------------------------------------------------------
   if constexpr (kFused) {
-    if (kSmemThr) __syncthreads();
-    // warp per candidate: lane k < K fetches knob k's log2 / position; every tested feature is
-    // formed from shuffles (featurize_kernel's arithmetic) and coded
-    for (int c = warp; c < rows; c += kWarps) {
-      const int64_t cand = row0 + c;
+    __syncthreads();  // thresholds / feature table staged
+    // Warp per TWO candidates (their descriptor loads and code searches interleaved). Lane l
+    // holds one table entry per candidate: lanes 0..15 knob l's log2(value), lanes 16..31 knob
+    // (l - 16)'s list position (searchspace.cpp:106-109), so a feature is at most two shuffles:
+    // log / position = one entry, pair product (:111-116) = entry(i) * entry(j) with one
+    // __dmul_rn. Which entries a feature takes depends only on the knob count K: the warp keeps
+    // that map for the K it last saw (shared memory, rebuilt when K changes).
+    int* wsrc = reinterpret_cast<int*>(smem + L.fsrc) + warp * ds;
+    int wk = -1;
+    auto build_src = [&](int k) {
+      __syncwarp();  // every lane is done with the previous map
+      const int dim = 2 * k + k * (k - 1) / 2;
+      for (int f = lane; f < d_model; f += 32) {
+        const int g = fmap ? __ldg(fmap + f) : f;  // the original feature index
+        int a = 0, b = 0, kind = 0;                // 0 zero (padding), 1 one entry, 2 product
+        if (g < k) {
+          kind = 1;
+          a = g;
+        } else if (g < 2 * k) {
+          kind = 1;
+          a = 16 + g - k;
+        } else if (g < dim) {
+          kind = 2;
+          fs::pair_of(k, g - 2 * k, a, b);
+        }
+        wsrc[f] = kind | a << 2 | b << 8;
+      }
+      __syncwarp();
+      wk = k;
+    };
+    struct Desc {
+      double tab;
+      int k;
+    };
+    auto load_desc = [&](int64_t cand) {  // the candidate's table entry in this lane + its K
       const int s = __ldg(sp.space_of + cand);
       const bool bad_space = s < 0 || s >= sp.n_spaces;
       const int k = bad_space ? 0 : __ldg(sp.k + s);
-      const int dim = 2 * k + k * (k - 1) / 2;
-      double lg = 0.0, ps = 0.0;
+      const int j = lane & 15;
+      double t = 0.0;
       bool bad = false;
-      if (lane < k) {
-        const int a = __ldg(sp.assign + cand * FS_MAX_KNOBS + lane);
-        const int m = __ldg(sp.nval + s * FS_MAX_KNOBS + lane);
+      if (j < k) {
+        const int a = __ldg(sp.assign + cand * FS_MAX_KNOBS + j);
+        const int m = __ldg(sp.nval + s * FS_MAX_KNOBS + j);
         if (a < 0 || a >= m) {
           bad = true;
         } else {
-          const int off = __ldg(sp.off + s * FS_MAX_KNOBS + lane);
-          lg = __ldg(sp.log + off + a);
-          ps = __ldg(sp.pos + off + a);
+          const int off = __ldg(sp.off + s * FS_MAX_KNOBS + j);
+          t = lane < 16 ? __ldg(sp.log + off + a) : __ldg(sp.pos + off + a);
         }
       }
       const unsigned any_bad = __ballot_sync(0xffffffffu, bad);
       if (lane == 0) {
         if (bad_space) atomicOr(err, fs::kErrSpaceId);
         if (any_bad) atomicOr(err, fs::kErrKnobRange);
-        if (sp.pad < dim) atomicOr(err, fs::kErrPadDim);
+        if (sp.pad < 2 * k + k * (k - 1) / 2) atomicOr(err, fs::kErrPadDim);
       }
-      CodeT* crow = codes + static_cast<size_t>(c) * ds;
-      for (int base = 0; base < d_model; base += 32) {
-        const int f = base + lane;
-        const int g = f < d_model && fmap ? __ldg(fmap + f) : f;  // the original feature index
-        int src_a = 0, src_b = 0, kind = 0;  // 0 zero (padding), 1 log, 2 pos, 3 product
-        if (g < k) {
-          kind = 1;
-          src_a = g;
-        } else if (g < 2 * k) {
-          kind = 2;
-          src_a = g - k;
-        } else if (g < dim) {
-          kind = 3;
-          fs::pair_of(k, g - 2 * k, src_a, src_b);
+      return Desc{t, k};
+    };
+    auto value = [&](int e, double tab) {
+      const int kind = e & 3;
+      const double x1 = __shfl_sync(0xffffffffu, tab, (e >> 2) & 63);
+      const double x2 = __shfl_sync(0xffffffffu, tab, e >> 8);
+      return kind == 0 ? 0.0 : kind == 1 ? x1 : fs_mul(x1, x2);
+    };
+    for (int c = warp; c < rows; c += 2 * kWarps) {
+      const int c2 = c + kWarps;
+      const bool two = c2 < rows;
+      const Desc A = load_desc(row0 + c);
+      const Desc B = two ? load_desc(row0 + c2) : A;
+      CodeT* ra = codes + static_cast<size_t>(c) * ds;
+      CodeT* rb = codes + static_cast<size_t>(two ? c2 : c) * ds;
+      if (A.k == B.k) {
+        if (A.k != wk) build_src(A.k);
+        for (int fb = 0; fb < d_model; fb += 32) {
+          const int f = fb + lane;
+          const int e = f < d_model ? wsrc[f] : 0;
+          const double va = value(e, A.tab), vb = value(e, B.tab);
+          if (f < d_model) {
+            const int4 m = s_meta[f];
+            int pa = 0, pb = 0;
+            for (int step = m.w; step > 0; step >>= 1) {
+              const int qa = pa + step, qb = pb + step;
+              if (qa <= m.z && uthr[m.y + qa - 1] < va) pa = qa;
+              if (qb <= m.z && uthr[m.y + qb - 1] < vb) pb = qb;
+            }
+            ra[f] = static_cast<CodeT>(pa);
+            rb[f] = static_cast<CodeT>(pb);
+          }
         }
-        const double la = __shfl_sync(0xffffffffu, lg, src_a);
-        const double lb = __shfl_sync(0xffffffffu, lg, src_b);
-        const double pa = __shfl_sync(0xffffffffu, ps, src_a);
-        double v = 0.0;
-        if (kind == 1) v = la;
-        else if (kind == 2) v = pa;
-        else if (kind == 3) v = fs_mul(la, lb);
-        if (f < d_model) crow[f] = code_of(f, v);
+      } else {  // different knob counts: one candidate after the other
+        for (int h = 0; h < 2; ++h) {
+          const Desc& D = h ? B : A;
+          CodeT* r = h ? rb : ra;
+          if (D.k != wk) build_src(D.k);
+          for (int fb = 0; fb < d_model; fb += 32) {
+            const int f = fb + lane;
+            const int e = f < d_model ? wsrc[f] : 0;
+            const double v = value(e, D.tab);
+            if (f < d_model) r[f] = code_of(s_meta[f], v);
+          }
+          __syncwarp();
+        }
       }
     }
   } else {
     bool nonfinite = false;
     double* rbuf = reinterpret_cast<double*>(smem + L.rows);  // [kStages][kStageRows][d]
     const int nst = (rows + kStageRows - 1) / kStageRows;
-    // warp w codes row r of a stage held in shared memory at `src`
-    auto code_row = [&](const double* src, int c) {
-      for (int f = lane; f < d; f += 32) nonfinite |= !isfinite(src[f]);
-      CodeT* crow = codes + static_cast<size_t>(c) * ds;
-      for (int f = lane; f < d_model; f += 32) crow[f] = code_of(f, src[fmap ? __ldg(fmap + f) : f]);
+    // warp w codes rows ca and (when cb >= 0) cb of a stage held in shared memory at sa / sb: every
+    // value checked for finiteness, every model feature coded, the two rows' searches interleaved
+    auto code_rows = [&](const double* sa, int ca, const double* sb, int cb) {
+      if (!kBulk || (d & 1)) {
+        for (int f = lane; f < d; f += 32) nonfinite |= !isfinite(sa[f]) || (cb >= 0 && !isfinite(sb[f]));
+      } else {  // 16-byte aligned rows (bulk stages, d even)
+        const double2* a2 = reinterpret_cast<const double2*>(sa);
+        const double2* b2 = reinterpret_cast<const double2*>(cb >= 0 ? sb : sa);
+        for (int f = lane; f < d / 2; f += 32) {
+          const double2 u = a2[f], w = b2[f];
+          nonfinite |= !isfinite(u.x) || !isfinite(u.y) || !isfinite(w.x) || !isfinite(w.y);
+        }
+      }
+      CodeT* ra = codes + static_cast<size_t>(ca) * ds;
+      CodeT* rb = codes + static_cast<size_t>(cb >= 0 ? cb : ca) * ds;
+      const double* sb_ = cb >= 0 ? sb : sa;
+      for (int f = lane; f < d_model; f += 32) {
+        const int4 m = s_meta[f];
+        const double va = sa[m.x], vb = sb_[m.x];
+        int pa = 0, pb = 0;
+        for (int step = m.w; step > 0; step >>= 1) {
+          const int qa = pa + step, qb = pb + step;
+          if (qa <= m.z && uthr[m.y + qa - 1] < va) pa = qa;
+          if (qb <= m.z && uthr[m.y + qb - 1] < vb) pb = qb;
+        }
+        ra[f] = static_cast<CodeT>(pa);
+        rb[f] = static_cast<CodeT>(pb);
+      }
     };
     if constexpr (kBulk) {
       uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -268,14 +350,21 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
         mbar_wait(bars + (st % kStages), static_cast<uint32_t>((st / kStages) & 1));
         const double* buf = rbuf + static_cast<size_t>(st % kStages) * kStageRows * d;
         const int r0 = st * kStageRows, nr = min(kStageRows, rows - r0);
-        for (int r = warp; r < nr; r += kWarps) code_row(buf + static_cast<size_t>(r) * d, r0 + r);
+        for (int r = warp; r < nr; r += 2 * kWarps) {
+          const int r2 = r + kWarps < nr ? r + kWarps : -1;
+          code_rows(buf + static_cast<size_t>(r) * d, r0 + r, r2 >= 0 ? buf + static_cast<size_t>(r2) * d : nullptr,
+                    r2 >= 0 ? r0 + r2 : -1);
+        }
         __syncthreads();  // every warp is done with this buffer
         if (tid == 0 && st + kStages < nst) issue(st + kStages);
       }
     } else {
-      if (kSmemThr) __syncthreads();
+      __syncthreads();  // thresholds / feature table staged
       // rows read in place: coalesced finiteness pass, tested columns gathered (L1 hits)
-      for (int c = warp; c < rows; c += kWarps) code_row(x + (row0 + c) * d, c);
+      for (int c = warp; c < rows; c += 2 * kWarps) {
+        const int c2 = c + kWarps < rows ? c + kWarps : -1;
+        code_rows(x + (row0 + c) * d, c, c2 >= 0 ? x + (row0 + c2) * d : nullptr, c2);
+      }
     }
     if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, fs::kErrNonFinitePredict);
   }
@@ -409,6 +498,7 @@ void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, do
   if (g.models.empty()) return;
   // tile: the largest of 256 / 128 / 64 / 32 candidates whose tiles still cover every SM
   int tc = 256;
+  if (const char* e = std::getenv("FAMSEER_PREDICT_TC")) tc = std::max(32, std::min(256, std::atoi(e)));  // A/B
   int64_t rows_all = 0;
   for (int64_t r : g.rows) rows_all += r;
   while (tc > 32) {
@@ -421,10 +511,10 @@ void launch_group(fs_device* dev, const HeapGroup& g, const double* x, int d, do
   const bool bulk = !kFused && d > 0 && d % 2 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                     static_cast<size_t>(kStages) * kStageRows * d * 8 <= 96 * 1024;
   const int row_doubles = bulk ? kStages * kStageRows * d : 0;
-  size_t smem = Smem(tc, ds, sizeof(CodeT), g.max_depth, kLeaves, g.max_uthr, g.max_dmodel, kSmemThr, row_doubles).total;
+  size_t smem = Smem(tc, ds, sizeof(CodeT), g.max_depth, kLeaves, g.max_uthr, g.max_dmodel, kSmemThr, row_doubles, kFused).total;
   while (smem > 227 * 1024 && tc > 32) {
     tc /= 2;
-    smem = Smem(tc, ds, sizeof(CodeT), g.max_depth, kLeaves, g.max_uthr, g.max_dmodel, kSmemThr, row_doubles).total;
+    smem = Smem(tc, ds, sizeof(CodeT), g.max_depth, kLeaves, g.max_uthr, g.max_dmodel, kSmemThr, row_doubles, kFused).total;
   }
   if (smem > 227 * 1024) fs::fail(FS_EINVAL, "predict: model too wide for the shared-memory tile");
   std::vector<PredJob> jobs;
