@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
   double* s_lrleaf = reinterpret_cast<double*>(smem + L.lrleaf);
   uint16_t* s_leafid = reinterpret_cast<uint16_t*>(smem + L.leafid);
   uint8_t* s_slot = smem + L.slots;
-  const int tcp = tc + 4;  // slot row pitch: tcp/4 odd -> lanes (trees) store to distinct banks
   // depth-3 register walk: every model of the launch has depth 3, u8 codes and rows <= 256 bytes
   const bool kFast = sizeof(CodeT) == 1 && fast != 0;
 
@@ -372,16 +371,43 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
   // ---- 2./3. passes of 32 trees -------------------------------------------------------------
   double score = M.meta ? M.meta->base : M.base;
   const double lr = M.lr;
+  // depth <= 3: a pass's tree tables (<= 7 x 32 node words, <= 8 x 32 leaves) are one item per
+  // thread, loaded from global memory one pass ahead into registers so the L2 latency hides
+  // behind the current pass's walk and fold
+  const bool pf = depth <= 3;
+  uint32_t pf_node = 0;
+  double pf_leaf = 0.0;
+  uint16_t pf_id = 0;
+  auto prefetch = [&](int tn) {
+    const int chn = min(32, n_trees - tn);
+    const int h = tid >> 5, t = tid & 31;
+    if (h < nint && t < chn) pf_node = __ldg(M.nodes + static_cast<size_t>(tn + t) * nint + h);
+    if (tid < chn * nleaf) {
+      pf_leaf = __ldg(M.leafv + static_cast<size_t>(tn) * nleaf + tid);
+      if (kLeaves) pf_id = __ldg(M.leafid + static_cast<size_t>(tn) * nleaf + tid);
+    }
+  };
+  if (pf && n_trees > 0) prefetch(0);
   for (int t0 = 0; t0 < n_trees; t0 += 32) {
     const int ch = min(32, n_trees - t0);
     __syncthreads();  // codes ready / the previous pass's fold is done with the tree tables
-    for (int i = tid; i < ch * nint; i += kThreads) {  // [node][tree]
-      const int h = i / ch, t = i - h * ch;
-      s_nodes[h * 32 + t] = __ldg(M.nodes + static_cast<size_t>(t0 + t) * nint + h);
-    }
-    for (int i = tid; i < ch * nleaf; i += kThreads) {
-      s_lrleaf[i] = fs_mul(lr, __ldg(M.leafv + static_cast<size_t>(t0) * nleaf + i));
-      if (kLeaves) s_leafid[i] = __ldg(M.leafid + static_cast<size_t>(t0) * nleaf + i);
+    if (pf) {
+      const int h = tid >> 5, t = tid & 31;
+      if (h < nint && t < ch) s_nodes[h * 32 + t] = pf_node;  // [node][tree]
+      if (tid < ch * nleaf) {
+        s_lrleaf[tid] = fs_mul(lr, pf_leaf);
+        if (kLeaves) s_leafid[tid] = pf_id;
+      }
+      if (t0 + 32 < n_trees) prefetch(t0 + 32);
+    } else {
+      for (int i = tid; i < ch * nint; i += kThreads) {  // [node][tree]
+        const int h = i / ch, t = i - h * ch;
+        s_nodes[h * 32 + t] = __ldg(M.nodes + static_cast<size_t>(t0 + t) * nint + h);
+      }
+      for (int i = tid; i < ch * nleaf; i += kThreads) {
+        s_lrleaf[i] = fs_mul(lr, __ldg(M.leafv + static_cast<size_t>(t0) * nleaf + i));
+        if (kLeaves) s_leafid[i] = __ldg(M.leafid + static_cast<size_t>(t0) * nleaf + i);
+      }
     }
     __syncthreads();
     if (lane < ch) {
@@ -406,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
         }
         return idx - nint;
       };
-      uint8_t* srow = s_slot + lane * tcp;
+      uint8_t* srow = s_slot + lane;  // slots [candidate][32 trees]: lane t writes byte 32c + t
       int c = warp;
       if (kFast) {
         // depth-3 trees, u8 codes, rows of <= 256 bytes: the seven node words become byte-packed
@@ -434,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
           for (int g = 0; g < G; ++g) {
             const uint32_t i = 2 * b0[g] + b1[g], sel = 0x4440u | i;
             v[g] = lds_u8(rb + static_cast<uint32_t>(g * kWarps * ds) + __byte_perm(o36, 0, sel));
-            srow[c + g * kWarps] = static_cast<uint8_t>(2 * i + (v[g] > __byte_perm(k36, 0, sel) ? 1u : 0u));
+            srow[(c + g * kWarps) * 32] = static_cast<uint8_t>(2 * i + (v[g] > __byte_perm(k36, 0, sel) ? 1u : 0u));
           }
         }
       }
@@ -443,20 +469,37 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
         const int q1 = walk(codes + static_cast<size_t>(c + kWarps) * ds);
         const int q2 = walk(codes + static_cast<size_t>(c + 2 * kWarps) * ds);
         const int q3 = walk(codes + static_cast<size_t>(c + 3 * kWarps) * ds);
-        srow[c] = static_cast<uint8_t>(q0);
-        srow[c + kWarps] = static_cast<uint8_t>(q1);
-        srow[c + 2 * kWarps] = static_cast<uint8_t>(q2);
-        srow[c + 3 * kWarps] = static_cast<uint8_t>(q3);
+        srow[c * 32] = static_cast<uint8_t>(q0);
+        srow[(c + kWarps) * 32] = static_cast<uint8_t>(q1);
+        srow[(c + 2 * kWarps) * 32] = static_cast<uint8_t>(q2);
+        srow[(c + 3 * kWarps) * 32] = static_cast<uint8_t>(q3);
       }
-      for (; c < rows; c += kWarps) srow[c] = static_cast<uint8_t>(walk(codes + static_cast<size_t>(c) * ds));
+      for (; c < rows; c += kWarps) srow[c * 32] = static_cast<uint8_t>(walk(codes + static_cast<size_t>(c) * ds));
     }
     __syncthreads();
     if (tid < rows) {  // thread = candidate: tree-order fold of the pass's leaf values
-      for (int t = 0; t < ch; ++t) {
-        const int q = s_slot[t * tcp + tid];
-        score = fs_add(score, s_lrleaf[t * nleaf + q]);
-        if (kLeaves) leaf_out[job.leaf0 + static_cast<int64_t>(tid) * n_trees + t0 + t] = s_leafid[t * nleaf + q];
-      }
+      // the candidate's 32 slots in two 16-byte loads; the leaf loads run ahead of the add chain
+      const uint4* s4 = reinterpret_cast<const uint4*>(s_slot + tid * 32);
+      const uint4 sa = s4[0], sb = s4[1];
+      auto fold4 = [&](uint32_t w, int t) {  // trees t .. t+3, slots in the bytes of w
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (t + u < ch) {
+            const int q = static_cast<int>((w >> (8 * u)) & 0xFFu);
+            score = fs_add(score, s_lrleaf[(t + u) * nleaf + q]);
+            if (kLeaves)
+              leaf_out[job.leaf0 + static_cast<int64_t>(tid) * n_trees + t0 + t + u] = s_leafid[(t + u) * nleaf + q];
+          }
+        }
+      };
+      fold4(sa.x, 0);
+      fold4(sa.y, 4);
+      fold4(sa.z, 8);
+      fold4(sa.w, 12);
+      fold4(sb.x, 16);
+      fold4(sb.y, 20);
+      fold4(sb.z, 24);
+      fold4(sb.w, 28);
     }
   }
   if (tid < rows) scores[row0 + tid] = score;
