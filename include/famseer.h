@@ -143,6 +143,19 @@ int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t
                const int64_t* seg_h, const int32_t* space_of_d, const int32_t* assign_d,
                int32_t pad_dim, double* scores_d, int32_t* perm_d);
 
+/* ---- score from linear_index descriptors -------------------------------
+ * As fs_score, but candidate i is (space_of[i], index[i]) with index[i] =
+ * linear_index(space, assignment) (searchspace.cpp:48-54), decoded on the device exactly as
+ * candidate_from_index (:56-66) does (mixed radix, last knob fastest): 4 + 8 bytes per candidate
+ * in instead of 4 + 64. Replaces the per-candidate featurize + predict calls of
+ * scheduler.cpp:187-191 for callers that keep MeasuredSet's u64 keys (reference searchspace.hpp:71-84). */
+int fs_score_index(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t n_segments,
+                   const int64_t* seg, const int32_t* space_of, const uint64_t* index, int32_t pad_dim,
+                   double* scores, int32_t* perm);
+int fs_score_index_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t n_segments,
+                     const int64_t* seg_h, const int32_t* space_of_d, const uint64_t* index_d,
+                     int32_t pad_dim, double* scores_d, int32_t* perm_d);
+
 /* ---- pairwise accuracy (costmodel.cpp:248-277) over precomputed scores ---------------------
  * Pairs with relative latency difference < 1e-6 are excluded, predicted ties score 1/2.
  * FS_EINVAL for m < 2, FS_EDOMAIN when every pair is excluded. */

@@ -109,6 +109,8 @@ class _Orc:
         L.orc_select.argtypes = [C.c_int64, _i64p, C.c_int, C.c_double, C.c_uint64, _i64p]
         L.orc_mix_seed.restype = C.c_uint64
         L.orc_mix_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.orc_linear_index.argtypes = [C.c_int, _i32p, _i32p, C.c_int64, C.c_int, _u64p]
+        L.orc_candidate_from_index.argtypes = [C.c_int, _i32p, _u64p, C.c_int64, C.c_int, _i32p]
         self.L = L
 
     def _chk(self, rc):
@@ -125,6 +127,22 @@ class _Orc:
         out = np.zeros((a.shape[0], pad_dim))
         self._chk(self.L.orc_featurize(len(values_per_knob), _p(nv, _i32p), _p(vals, _i64p), _p(a, _i32p),
                                        a.shape[0], a.shape[1], pad_dim, _p(out, _dp)))
+        return out
+
+    def linear_index(self, nvals, assign):
+        """searchspace.cpp:48-54 for every row of assign (int32 [p][>= k])."""
+        nv = np.ascontiguousarray(nvals, np.int32)
+        a = np.ascontiguousarray(np.atleast_2d(assign), np.int32)
+        out = np.zeros(a.shape[0], np.uint64)
+        self.L.orc_linear_index(len(nv), _p(nv, _i32p), _p(a, _i32p), a.shape[0], a.shape[1], _p(out, _u64p))
+        return out
+
+    def candidate_from_index(self, nvals, index, stride=16):
+        """searchspace.cpp:56-66 for every index: int32 [p][stride] (knobs beyond k are 0)."""
+        nv = np.ascontiguousarray(nvals, np.int32)
+        ix = np.ascontiguousarray(index, np.uint64)
+        out = np.zeros((len(ix), stride), np.int32)
+        self.L.orc_candidate_from_index(len(nv), _p(nv, _i32p), _p(ix, _u64p), len(ix), stride, _p(out, _i32p))
         return out
 
     def predict(self, ens: Ensemble, x, leaves=False):
@@ -226,6 +244,8 @@ class _Ref:
                                C.c_char_p, C.c_int64]
         L.ref_rng_draws.restype = C.c_uint64
         L.ref_rng_draws.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, _u64p]
+        L.ref_linear_index.argtypes = [C.c_int, _i32p, _i64p, _i32p, C.c_int64, C.c_int, _u64p]
+        L.ref_candidate_from_index.argtypes = [C.c_int, _i32p, _i64p, _u64p, C.c_int64, C.c_int, _i32p]
         self.L = L
 
     def _chk(self, rc):
@@ -245,6 +265,24 @@ class _Ref:
         out = np.zeros((a.shape[0], pad_dim))
         self._chk(self.L.ref_featurize(len(values_per_knob), _p(nv, _i32p), _p(vals, _i64p), _p(a, _i32p),
                                        a.shape[0], a.shape[1], pad_dim, _p(out, _dp)))
+        return out
+
+    def linear_index(self, values_per_knob, assign):
+        nv = np.array([len(v) for v in values_per_knob], np.int32)
+        vals = np.ascontiguousarray(np.concatenate([np.asarray(v, np.int64) for v in values_per_knob]))
+        a = np.ascontiguousarray(np.atleast_2d(assign), np.int32)
+        out = np.zeros(a.shape[0], np.uint64)
+        self._chk(self.L.ref_linear_index(len(nv), _p(nv, _i32p), _p(vals, _i64p), _p(a, _i32p), a.shape[0],
+                                          a.shape[1], _p(out, _u64p)))
+        return out
+
+    def candidate_from_index(self, values_per_knob, index, stride=16):
+        nv = np.array([len(v) for v in values_per_knob], np.int32)
+        vals = np.ascontiguousarray(np.concatenate([np.asarray(v, np.int64) for v in values_per_knob]))
+        ix = np.ascontiguousarray(index, np.uint64)
+        out = np.zeros((len(ix), stride), np.int32)
+        self._chk(self.L.ref_candidate_from_index(len(nv), _p(nv, _i32p), _p(vals, _i64p), _p(ix, _u64p), len(ix),
+                                                  stride, _p(out, _i32p)))
         return out
 
     # -- models ----------------------------------------------------------------------------

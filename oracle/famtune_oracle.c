@@ -21,6 +21,28 @@ const char* orc_last_error(void) { return g_err; }
 /* searchspace.cpp:86-88 */
 int orc_feature_dim(int k) { return 2 * k + k * (k - 1) / 2; }
 
+/* searchspace.cpp:48-54: mixed-radix rank of an assignment (knob 0 most significant). */
+void orc_linear_index(int k, const int32_t* nvals, const int32_t* assign, int64_t p, int assign_stride,
+                      uint64_t* out) {
+  for (int64_t c = 0; c < p; ++c) {
+    uint64_t idx = 0;
+    for (int i = 0; i < k; ++i) idx = idx * (uint64_t)nvals[i] + (uint64_t)assign[c * assign_stride + i];
+    out[c] = idx;
+  }
+}
+
+/* searchspace.cpp:56-66: the inverse, last knob first (index % m, index /= m). */
+void orc_candidate_from_index(int k, const int32_t* nvals, const uint64_t* index, int64_t p, int assign_stride,
+                              int32_t* out) {
+  for (int64_t c = 0; c < p; ++c) {
+    uint64_t idx = index[c];
+    for (int i = k; i-- > 0;) {
+      out[c * assign_stride + i] = (int32_t)(idx % (uint64_t)nvals[i]);
+      idx /= (uint64_t)nvals[i];
+    }
+  }
+}
+
 /* searchspace.cpp:90-118: log2(value) per knob, idx/(m-1) per knob, then log2_i*log2_j for
  * i<j in row-major pair order, zero padding to pad_dim. */
 int orc_featurize(int k, const int32_t* nvals, const int64_t* values, const int32_t* assign,

@@ -23,6 +23,10 @@ const char* orc_last_error(void);
 
 int orc_feature_dim(int k);
 
+void orc_linear_index(int k, const int32_t* nvals, const int32_t* assign, int64_t p, int assign_stride,
+                      uint64_t* out);
+void orc_candidate_from_index(int k, const int32_t* nvals, const uint64_t* index, int64_t p, int assign_stride,
+                              int32_t* out);
 int orc_featurize(int k, const int32_t* nvals, const int64_t* values, const int32_t* assign,
                   int64_t p, int assign_stride, int pad_dim, double* out);
 

@@ -113,6 +113,26 @@ int ref_featurize_checked(int k, const int32_t* nvals, const int64_t* values,
 
 int ref_feature_dim(int k) { return feature_dim(k); }
 
+int ref_linear_index(int k, const int32_t* nvals, const int64_t* values, const int32_t* assign, int64_t p,
+                     int assign_stride, uint64_t* out) {
+  return guarded([&] {
+    const auto space = space_from(k, nvals, values);
+    for (int64_t i = 0; i < p; ++i)
+      out[i] = linear_index(space, std::span<const int32_t>(assign + i * assign_stride, static_cast<std::size_t>(k)));
+  });
+}
+
+int ref_candidate_from_index(int k, const int32_t* nvals, const int64_t* values, const uint64_t* index, int64_t p,
+                             int assign_stride, int32_t* out) {
+  return guarded([&] {
+    const auto space = space_from(k, nvals, values);
+    for (int64_t i = 0; i < p; ++i) {
+      const auto c = candidate_from_index(space, 0, index[i]);
+      std::copy(c.assignment.begin(), c.assignment.end(), out + i * assign_stride);
+    }
+  });
+}
+
 ref_model* ref_model_new(int family_id, int trees, int depth, double lr, int min_split) {
   auto* m = new ref_model;
   GbtParams p;

@@ -254,6 +254,24 @@ class Spaces:
                                _p(a, _capi._i32p), pad_dim, _p(scores, _capi._dp), _p(perm, _capi._i32p)))
         return scores, perm
 
+    def score_index(self, forest: "Forest", space_of, index, pad_dim: int, seg):
+        """fs_score from (space id, linear_index) descriptors (searchspace.cpp:48-66): the device
+        decodes each u64 mixed-radix index like candidate_from_index. Returns (scores, perm)."""
+        so = np.ascontiguousarray(space_of, np.int32)
+        ix = np.ascontiguousarray(index, np.uint64)
+        sg, sp = _seg(seg)
+        scores = np.empty(len(so), np.float64)
+        perm = np.empty(len(so), np.int32)
+        _check(_lib().fs_score_index(self.dev.h, self.h, forest.h, len(sg) - 1, sp, _p(so, _capi._i32p),
+                                     _p(ix, _capi._u64p), pad_dim, _p(scores, _capi._dp), _p(perm, _capi._i32p)))
+        return scores, perm
+
+    def score_index_d(self, forest: "Forest", space_of_t, index_t, pad_dim: int, seg, scores_t, perm_t):
+        sg, sp = _seg(seg)
+        _check(_lib().fs_score_index_d(self.dev.h, self.h, forest.h, len(sg) - 1, sp, space_of_t.data_ptr(),
+                                       index_t.data_ptr(), pad_dim, scores_t.data_ptr(),
+                                       None if perm_t is None else perm_t.data_ptr()))
+
     def score_d(self, forest: "Forest", space_of_t, assign_t, pad_dim: int, seg, scores_t, perm_t):
         sg, sp = _seg(seg)
         _check(_lib().fs_score_d(self.dev.h, self.h, forest.h, len(sg) - 1, sp, space_of_t.data_ptr(),

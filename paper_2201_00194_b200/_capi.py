@@ -18,6 +18,7 @@ FS_MAX_KNOBS = 16
 _dp = C.POINTER(C.c_double)
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
+_u64p = C.POINTER(C.c_uint64)
 _u8p = C.POINTER(C.c_uint8)
 _u16p = C.POINTER(C.c_uint16)
 _vp = C.c_void_p
@@ -59,6 +60,8 @@ SIGNATURES = [
     ("fs_store_fit", C.c_int, [_vp, _vp, C.c_int32, _i32p, C.POINTER(GbtParams)]),
     ("fs_score", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _i32p, C.c_int32, _dp, _i32p]),
     ("fs_score_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp]),
+    ("fs_score_index", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _u64p, C.c_int32, _dp, _i32p]),
+    ("fs_score_index_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp]),
     ("fs_feature_dim", C.c_int, [C.c_int32]),
     ("fs_spaces_create", C.c_int, [_vp, C.c_int32, _i32p, _i32p, _i64p, C.POINTER(_vp)]),
     ("fs_spaces_destroy", C.c_int, [_vp]),

@@ -138,6 +138,16 @@ int fs_spaces_create(fs_device* dev, int32_t n_spaces, const int32_t* n_knobs, c
         }
       }
     }
+    // mixed-radix strides of linear_index (searchspace.cpp:48-54): idx = sum_j a_j * prod_{k>j} m_k
+    // (wraps modulo 2^64 like the reference's unsigned arithmetic once a space exceeds 2^64)
+    std::vector<uint64_t> stride(static_cast<size_t>(n_spaces) * FS_MAX_KNOBS, 0);
+    for (int s = 0; s < n_spaces; ++s) {
+      uint64_t st = 1;
+      for (int i = sp->k_h[static_cast<size_t>(s)] - 1; i >= 0; --i) {
+        stride[static_cast<size_t>(s) * FS_MAX_KNOBS + i] = st;
+        st *= static_cast<uint64_t>(nval[static_cast<size_t>(s) * FS_MAX_KNOBS + i]);
+      }
+    }
     auto up = [&](auto*& dst, const auto& vec) {
       using T = std::remove_reference_t<decltype(*dst)>;
       FS_CUDA(cudaMalloc(&dst, std::max<size_t>(1, vec.size()) * sizeof(T)));
@@ -149,6 +159,7 @@ int fs_spaces_create(fs_device* dev, int32_t n_spaces, const int32_t* n_knobs, c
     up(sp->off_d, off);
     up(sp->log_d, lg);
     up(sp->pos_d, ps);
+    up(sp->stride_d, stride);
     FS_CUDA(cudaStreamSynchronize(dev->stream));
     *out = sp.release();
   });
@@ -164,6 +175,7 @@ int fs_spaces_destroy(fs_spaces* sp) {
     cudaFree(sp->off_d);
     cudaFree(sp->log_d);
     cudaFree(sp->pos_d);
+    cudaFree(sp->stride_d);
     delete sp;
   });
 }

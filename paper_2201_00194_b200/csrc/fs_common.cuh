@@ -160,6 +160,7 @@ enum Slot : int {
   kSlotScoreX,
   kSlotScoreS,
   kSlotScoreP,
+  kSlotScoreA,  // assignments decoded from linear_index descriptors (unfused score fallback)
   kSlotFitX,    // featurized training records (fs_fit_records)
   kSlotFitIn,   // their descriptors / targets (host-pointer form)
   kSlotCount
@@ -191,6 +192,8 @@ struct fs_spaces {
   int32_t* off_d = nullptr;  // [n*16] offset into log/pos tables
   double* log_d = nullptr;
   double* pos_d = nullptr;
+  // linear_index descriptors (searchspace.cpp:48-66): stride[s][j] = prod_{k>j} m_k
+  uint64_t* stride_d = nullptr;  // [n*16]
 };
 
 namespace fs {

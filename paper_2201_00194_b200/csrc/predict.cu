@@ -60,6 +60,8 @@ struct SpaceTabs {
   const double* pos;
   int n_spaces;
   int pad;
+  const uint64_t* index = nullptr;   // [P] linear_index descriptors (nullptr: assign)
+  const uint64_t* stride = nullptr;  // [n_spaces][16]
 };
 
 // One CTA's work: a tile of up to TC rows of one family segment.
@@ -234,8 +236,15 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const double* __restr
       double t = 0.0;
       bool bad = false;
       if (j < k) {
-        const int a = __ldg(sp.assign + cand * FS_MAX_KNOBS + j);
         const int m = __ldg(sp.nval + s * FS_MAX_KNOBS + j);
+        int a;
+        if (sp.index) {  // candidate_from_index (searchspace.cpp:56-66): a_j = (idx / stride_j) % m_j
+          const uint64_t idx = __ldg(reinterpret_cast<const unsigned long long*>(sp.index) + cand);
+          const uint64_t q = idx / __ldg(reinterpret_cast<const unsigned long long*>(sp.stride) + s * FS_MAX_KNOBS + j);
+          a = static_cast<int>(q % static_cast<uint64_t>(m));
+        } else {
+          a = __ldg(sp.assign + cand * FS_MAX_KNOBS + j);
+        }
         if (a < 0 || a >= m) {
           bad = true;
         } else {
@@ -661,8 +670,10 @@ void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int
 // Fused featurize -> predict: candidates come as (space id, value indices)
 // descriptors; no feature matrix is written or read. pad plays the row width d.
 void launch_score_fused(fs_device* dev, const fs_spaces* spc, const fs_forest* fo, int32_t nseg, const int64_t* seg,
-                        const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores) {
-  const SpaceTabs sp{space_of_d, assign_d, spc->k_d, spc->nval_d, spc->off_d, spc->log_d, spc->pos_d, spc->n, pad};
+                        const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores,
+                        const uint64_t* index_d) {
+  const SpaceTabs sp{space_of_d, assign_d, spc->k_d, spc->nval_d, spc->off_d, spc->log_d,
+                     spc->pos_d, spc->n,   pad,      index_d,     spc->stride_d};
   launch_predict_impl<true>(dev, fo, nseg, seg, pad, nullptr, scores, nullptr, sp);
 }
 

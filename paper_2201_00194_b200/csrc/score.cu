@@ -16,11 +16,30 @@ void launch_predict(fs_device* dev, const fs_forest* fo, int32_t nseg, const int
                     const double* x, double* scores, uint16_t* leaf_out);
 void launch_rank(fs_device* dev, int32_t nseg, const int64_t* seg_h, const double* scores_d, int32_t* perm_d);
 void launch_score_fused(fs_device* dev, const fs_spaces* spc, const fs_forest* fo, int32_t nseg, const int64_t* seg,
-                        const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores);
+                        const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores,
+                        const uint64_t* index_d);
 
+// candidate_from_index (searchspace.cpp:56-66) on the device: assignment[j] = (idx / prod_{k>j}
+// m_k) % m_j, thread per (candidate, knob). Only the unfused fallback needs the assignments.
+__global__ void decode_index_kernel(const int32_t* __restrict__ space_of, const uint64_t* __restrict__ index, int64_t n,
+                                    const int32_t* __restrict__ k_d, const int32_t* __restrict__ nval,
+                                    const uint64_t* __restrict__ stride, int n_spaces, int32_t* __restrict__ assign) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * FS_MAX_KNOBS) return;
+  const int64_t c = i / FS_MAX_KNOBS;
+  const int j = static_cast<int>(i - c * FS_MAX_KNOBS);
+  const int s = space_of[c];
+  int a = 0;
+  if (s >= 0 && s < n_spaces && j < k_d[s])
+    a = static_cast<int>((index[c] / stride[s * FS_MAX_KNOBS + j]) % static_cast<uint64_t>(nval[s * FS_MAX_KNOBS + j]));
+  assign[i] = a;
+}
+
+// index_d != nullptr: candidates are (space id, linear_index) descriptors (SURVEY.md 8f row 1:
+// 4 + 8 bytes per candidate in, instead of the 4 + 64 of an int32[16] assignment)
 static void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg,
                          const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores_d,
-                         int32_t* perm_d) {
+                         int32_t* perm_d, const uint64_t* index_d = nullptr) {
   const int64_t n = seg[nseg];
   if (n <= 0) return;
   if (seg[0] != 0) fail(FS_EINVAL, "score: seg[0] must be 0");
@@ -31,8 +50,16 @@ static void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* f
   for (int f = 0; f < nseg && fused; ++f)
     if (f < static_cast<int32_t>(fo->fams.size()) && fo->fams[static_cast<size_t>(f)].generic) fused = false;
   if (fused) {
-    launch_score_fused(dev, sp, fo, nseg, seg, space_of_d, assign_d, pad, scores_d);
+    launch_score_fused(dev, sp, fo, nseg, seg, space_of_d, assign_d, pad, scores_d, index_d);
   } else {
+    if (index_d) {
+      auto* as = static_cast<int32_t*>(dev->scratch(kSlotScoreA, static_cast<size_t>(n) * FS_MAX_KNOBS * sizeof(int32_t)));
+      decode_index_kernel<<<static_cast<unsigned>(ceil_div(n * FS_MAX_KNOBS, 256)), 256, 0, dev->stream>>>(
+          space_of_d, index_d, n, sp->k_d, sp->nval_d, sp->stride_d, sp->n, as);
+      dev->count_launch();
+      FS_CUDA(cudaGetLastError());
+      assign_d = as;
+    }
     auto* x = static_cast<double*>(dev->scratch(kSlotScoreX, static_cast<size_t>(n) * pad * sizeof(double)));
     launch_featurize(dev, sp, n, space_of_d, assign_d, pad, x);
     launch_predict(dev, fo, nseg, seg, pad, x, scores_d, nullptr);
@@ -192,6 +219,36 @@ int fs_score(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t n
     FS_CUDA(cudaMemcpyAsync(so, space_of, n * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
     FS_CUDA(cudaMemcpyAsync(as, assign, n * FS_MAX_KNOBS * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
     fs::score_device(dev, sp, fo, nseg, seg, so, as, pad_dim, sd, pd);
+    if (scores) FS_CUDA(cudaMemcpyAsync(scores, sd, n * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
+    if (perm) FS_CUDA(cudaMemcpyAsync(perm, pd, n * sizeof(int32_t), cudaMemcpyDeviceToHost, dev->stream));
+    fs::raise_deferred(dev->take_errors());
+  });
+}
+
+int fs_score_index_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg_h,
+                     const int32_t* space_of_d, const uint64_t* index_d, int32_t pad_dim, double* scores_d,
+                     int32_t* perm_d) {
+  return fs::guard([&] {
+    if (!dev || !sp || !fo || nseg < 0 || !seg_h || pad_dim < 0) fs::fail(FS_EINVAL, "fs_score_index: bad arguments");
+    dev->activate();
+    fs::score_device(dev, sp, fo, nseg, seg_h, space_of_d, nullptr, pad_dim, scores_d, perm_d, index_d);
+  });
+}
+
+int fs_score_index(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg,
+                   const int32_t* space_of, const uint64_t* index, int32_t pad_dim, double* scores, int32_t* perm) {
+  return fs::guard([&] {
+    if (!dev || !sp || !fo || nseg < 0 || !seg || pad_dim < 0) fs::fail(FS_EINVAL, "fs_score_index: bad arguments");
+    dev->activate();
+    const int64_t n = seg[nseg];
+    if (n <= 0) return;
+    auto* so = static_cast<int32_t*>(dev->scratch(fs::kSlotH2D0, n * sizeof(int32_t)));
+    auto* ix = static_cast<uint64_t*>(dev->scratch(fs::kSlotH2D1, n * sizeof(uint64_t)));
+    auto* sd = static_cast<double*>(dev->scratch(fs::kSlotScoreS, n * sizeof(double)));
+    auto* pd = static_cast<int32_t*>(dev->scratch(fs::kSlotScoreP, n * sizeof(int32_t)));
+    FS_CUDA(cudaMemcpyAsync(so, space_of, n * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
+    FS_CUDA(cudaMemcpyAsync(ix, index, n * sizeof(uint64_t), cudaMemcpyHostToDevice, dev->stream));
+    fs::score_device(dev, sp, fo, nseg, seg, so, nullptr, pad_dim, sd, pd, ix);
     if (scores) FS_CUDA(cudaMemcpyAsync(scores, sd, n * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
     if (perm) FS_CUDA(cudaMemcpyAsync(perm, pd, n * sizeof(int32_t), cudaMemcpyDeviceToHost, dev->stream));
     fs::raise_deferred(dev->take_errors());

@@ -129,3 +129,32 @@ def test_fit_differential_vs_reference(orc, ref):
 def test_rng_stream_matches_reference(ref):
     assert np.array_equal(ref.rng_draws(42, 0xD4, 0, 64, 1000), G["rng_below"])
     assert np.array_equal(ref.rng_draws(42, 0xD4, 0, 16), G["rng_raw"])
+
+
+def test_linear_index_pinned(orc):
+    """linear_index / candidate_from_index (searchspace.cpp:48-66) against the reference's own
+    outputs on every subgraph space of two model files (tests/golden/make_golden_index.py)."""
+    L = np.load(f"{GOLDEN}/linear_index.npz")
+    names = sorted({k.rsplit("_", 1)[0] for k in L.files})
+    assert len(names) == 39
+    for name in names:
+        model, sid = name.rsplit("_", 1)
+        knobs = load_spaces(model)["subgraphs"][int(sid)]["knobs"]
+        nv = [len(v) for v in knobs]
+        a = L[f"{name}_assign"]
+        assert np.array_equal(orc.linear_index(nv, a[:, : len(nv)]), L[f"{name}_index"]), name
+        assert np.array_equal(orc.candidate_from_index(nv, L[f"{name}_index"]), L[f"{name}_back"]), name
+        assert np.array_equal(L[f"{name}_back"], a), name  # round trip
+        assert int(L[f"{name}_index"][0]) == 0 and int(L[f"{name}_index"][-1]) == int(np.prod(nv)) - 1
+
+
+def test_linear_index_differential_vs_reference(orc, ref):
+    rng = np.random.default_rng(11)
+    for k in (1, 5, 16):
+        knobs = [[1 << i for i in range(int(rng.integers(1, 9)))] for _ in range(k)]
+        nv = [len(v) for v in knobs]
+        a = np.stack([rng.integers(0, m, 200) for m in nv], 1).astype(np.int32)
+        idx = ref.linear_index(knobs, a)
+        assert np.array_equal(orc.linear_index(nv, a), idx)
+        assert np.array_equal(orc.candidate_from_index(nv, idx)[:, :k], a)
+        assert np.array_equal(ref.candidate_from_index(knobs, idx)[:, :k], a)
