@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   const bool lead = cl_r == 0;
   __shared__ unsigned long long s_red[32];
   __shared__ int s_wsum[32];
-  __shared__ int s_shift, s_nitems, s_ctot;
+  __shared__ int s_nitems, s_ctot;
   __shared__ unsigned long long s_cnt[3];  // screened splits, exact nodes, exact folds
   __shared__ unsigned long long s_why[4];  // exact-node reasons
 #ifdef FS_RES_HIST_PROBE
@@ -364,13 +364,15 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       tr[s] = tz;
     }
     __syncthreads();
-    if (tid == 0) {
+    // every thread reduces the per-warp maxima itself (broadcast loads): no serial section and
+    // no extra barrier
+    int shift;
+    {
       unsigned long long m = 0;
+#pragma unroll
       for (int w = 0; w < kResThreads / 32; ++w) m = max(m, s_red[w]);
-      s_shift = kResLimbs == 3 ? fix_shift(m, n) : fix_shift(m, n) - 22;  // n*|v| < 2^61 resp. 2^39
+      shift = kResLimbs == 3 ? fix_shift(m, n) : fix_shift(m, n) - 22;  // n*|v| < 2^61 resp. 2^39
     }
-    __syncthreads();
-    const int shift = s_shift;
     const double scale = ldexp(1.0, -shift);
     for (int p = tid; p < n; p += kResThreads) s_fix[p] = __double2ll_rn(ldexp(s_resid[p], shift));
     __syncthreads();
@@ -670,29 +672,38 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       // any fold. Check order equivalence against the lowest window feature in parallel.
       if (tid == 0) s_neq = 0;
       __syncthreads();
-      if (tid < nl) {
-        const int k = tid;
+      // warp per node, lanes over its features: the window is one candidate per feature, all at
+      // the same left count, and the lowest window feature's lower bound is positive
+      for (int k = warp; k < nl; k += kResWarps) {
         ResNode& nd = s_nodes[first + k];
-        nd.eqf0 = -1;
-        if (nd.state == 0 && nd.build != 0 && nd.wcount >= 2) {
-          const WinRec* w = s_win + k * nrep;
-          int f0 = -1, lc0 = -1;
-          bool ok = true;
-          for (int j = 0; j < nrep && ok; ++j) {
-            if (!w[j].flag) continue;
-            if (w[j].count != 1) ok = false;
-            if (f0 < 0) {
-              f0 = j;
-              lc0 = w[j].best_lc;
-            } else if (w[j].best_lc != lc0) {
-              ok = false;
-            }
-          }
-          if (ok && f0 >= 0 && w[f0].best_lo > 0.0) {
-            nd.eqf0 = f0;
-            for (int j = f0 + 1; j < nrep; ++j)
-              if (w[j].flag) s_items[atomicAdd(&s_neq, 1)] = (first + k) << 16 | j;
-          }
+        if (!(nd.state == 0 && nd.build != 0 && nd.wcount >= 2)) {
+          if (lane == 0) nd.eqf0 = -1;
+          continue;
+        }
+        const WinRec* w = s_win + k * nrep;
+        int f0 = -1;
+        for (int j0 = 0; j0 < nrep && f0 < 0; j0 += 32) {
+          const unsigned m = __ballot_sync(0xffffffffu, j0 + lane < nrep && w[j0 + lane].flag);
+          if (m) f0 = j0 + __ffs(m) - 1;
+        }
+        const int lc0 = f0 >= 0 ? w[f0].best_lc : -1;
+        bool bad = false;
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          const bool fl = j < nrep && w[j].flag;
+          bad |= __any_sync(0xffffffffu, fl && (w[j].count != 1 || w[j].best_lc != lc0));
+        }
+        const bool ok = !bad && f0 >= 0 && w[f0].best_lo > 0.0;
+        if (lane == 0) nd.eqf0 = ok ? f0 : -1;
+        if (!ok) continue;
+        for (int j0 = 0; j0 < nrep; j0 += 32) {
+          const int j = j0 + lane;
+          const bool put = j < nrep && j > f0 && w[j].flag;
+          const unsigned m = __ballot_sync(0xffffffffu, put);
+          int base = 0;
+          if (lane == 0 && m) base = atomicAdd(&s_neq, __popc(m));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (put) s_items[base + __popc(m & ((1u << lane) - 1u))] = (first + k) << 16 | j;
         }
       }
       __syncthreads();
