@@ -105,8 +105,8 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
   L.clc = o;  // left count per (node at level, bin)
   o = res_align(o + static_cast<size_t>(L.ls) * bins * 4);
-  L.binrep = o;  // feature (rep) of every bin
-  o = res_align(o + static_cast<size_t>(bins) * 2);
+  L.binrep = o;  // feature (rep) of every bin, then this CTA's owned bins in order (histogram fold)
+  o = res_align(o + static_cast<size_t>(bins) * 4);
   L.vals = o;  // threshold value of every bin + original feature of every rep (split records)
   o = res_align(o + static_cast<size_t>(bins) * 8 + nr * 4);
   L.cand = o;  // screened (gain, bound) per (node at level, bin)
@@ -247,6 +247,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
   int* s_clc = reinterpret_cast<int*>(sm + Lo.clc);           // [level node][bin] left count
   uint16_t* s_binrep = reinterpret_cast<uint16_t*>(sm + Lo.binrep);
+  uint16_t* s_own = s_binrep + bins;  // bins of this CTA's histogram features (j % cl_n == cl_r)
+  __shared__ int s_nown;
   double* s_vals = reinterpret_cast<double*>(sm + Lo.vals);
   int* s_rorig = reinterpret_cast<int*>(s_vals + bins);
   __shared__ int s_neq;
@@ -330,6 +332,15 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   for (int p = tid; p < n; p += kResThreads) s_pred[p] = b0;
   if (pre_smem)
     for (int i = tid; i < n * nrep; i += kResThreads) s_pre[i] = static_cast<uint16_t>(g_pre[i]);
+  // limb cells start zeroed; every fold zeroes the cells it reads (and the tie classes' phi
+  // tables, which overlay them, are zeroed again), so no zeroing pass per histogram
+  for (int i = tid; i < 3 * colh * 32; i += kResThreads) s_limb[i] = 0;
+  if (tid == 0) {
+    int no = 0;
+    for (int j = cl_r; j < nrep; j += cl_n)
+      for (int b = 0; b < rep_nb[fd.rep0 + j]; ++b) s_own[no++] = static_cast<uint16_t>(rep_boff[fd.rep0 + j] + b);
+    s_nown = no;
+  }
   __syncthreads();
 
   int ntrees = 0;
@@ -381,6 +392,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     for (int level = 0; level <= depth; ++level) {
       const int first = (1 << level) - 1, nl = 1 << level;
       // ---- plan (level_plan_kernel) --------------------------------------------------------
+      if (level < depth && tid < 4 * nl) s_absl[tid] = 0;  // the level's sum |v| limb counters
       if (tid < nl) {
         const int s = first + tid;
         ResNode& nd = s_nodes[s];
@@ -422,19 +434,12 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         const int hj = hjl * cl_n + cl_r;
         const int hm = nown <= 32 ? lane / max(nown, 1) : 0;
         const bool hact = nown <= 32 ? nown > 0 && hm < rpw : true;
-        const int cpad = 3 * colh * 32;
         for (int k = 0; k < nl; ++k) {
           ResNode& nd = s_nodes[first + k];
           if (nd.build != 1) continue;
           const int nv = nd.n;
           const uint16_t* rows = s_ord0 + nd.seg;
           for (int sub0 = 0; sub0 < nv; sub0 += kAtomSub) {
-            for (int i = tid; i < cpad; i += kResThreads) s_limb[i] = 0;
-            if (tid < 4) s_absl[4 * k + tid] = 0;
-            __syncthreads();
-#ifdef FS_RES_HIST_SPLIT
-            RES_PHASE(1);  // A/B probe: zeroing billed to "plan"
-#endif
             const int q_end = min(nv, sub0 + kAtomSub);
             unsigned long long asum = 0;
 #ifdef FS_RES_HIST_PROBE
@@ -492,33 +497,55 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
 #endif
             long long* hk = hs + static_cast<size_t>(k) * bins;
             int* ck = hc + static_cast<size_t>(k) * bins;
-            for (int i = tid; i < bins; i += kResThreads) {
+            // four threads per owned bin, each summing a quarter of the bin's lane copies (the
+            // cells are zeroed as they are read), combined by two xor shuffles within the group
+            const int nown_b = s_nown;
+            for (int i4 = tid; i4 < 4 * nown_b; i4 += kResThreads) {
+              const int i = s_own[i4 >> 2], sub = i4 & 3;
               const int j = s_binrep[i], b = i - s_repb[j];
-              if (cl_n > 1 && j % cl_n != cl_r) continue;  // a partner's feature
-              unsigned __int128 U = 0;
+              unsigned long long ulo = 0, uhi = 0;  // 128-bit partial sum of u over the copies
+              auto add_cell = [&](uint32_t* c) {
+                const unsigned __int128 v = static_cast<unsigned __int128>(c[0]) +
+                                            (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
+                                            (kResLimbs == 3 ? static_cast<unsigned __int128>(c[2 * colh * 32]) << 42 : 0);
+                c[0] = 0;
+                c[colh * 32] = 0;
+                if (kResLimbs == 3) c[2 * colh * 32] = 0;
+                const unsigned __int128 t = ((static_cast<unsigned __int128>(uhi) << 64) | ulo) + v;
+                ulo = static_cast<unsigned long long>(t);
+                uhi = static_cast<unsigned long long>(t >> 64);
+              };
               if (nown <= 32) {
-                for (int m = 0; m < rpw; ++m) {
-                  const uint32_t* c = s_limb + b * 32 + j / cl_n + m * nown;
-                  U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
-                       (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
-                }
-              } else {
-                const uint32_t* c = s_limb + (s_cofs[j] + b) * 32 + (j & 31);
-                U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
-                    (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+                for (int m = sub; m < rpw; m += 4) add_cell(s_limb + b * 32 + j / cl_n + m * nown);
+              } else if (sub == 0) {
+                add_cell(s_limb + (s_cofs[j] + b) * 32 + (j & 31));
               }
-              const uint64_t cnt =
-                  static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << (kResBias - 1))) >> kResBias);
-              const long long hv =
-                  static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << kResBias)));
-              hk[i] = (sub0 == 0 ? 0ll : hk[i]) + hv;
-              ck[i] = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
+              // lanes of this warp inside the loop bound (a prefix: whole groups of four)
+              const int lim = 4 * nown_b - (i4 - lane);
+              const unsigned grp = lim >= 32 ? 0xffffffffu : (1u << lim) - 1u;
+#pragma unroll
+              for (int o = 1; o < 4; o <<= 1) {
+                const unsigned long long olo = __shfl_xor_sync(grp, ulo, o), ohi = __shfl_xor_sync(grp, uhi, o);
+                const unsigned __int128 t = ((static_cast<unsigned __int128>(uhi) << 64) | ulo) +
+                                            ((static_cast<unsigned __int128>(ohi) << 64) | olo);
+                ulo = static_cast<unsigned long long>(t);
+                uhi = static_cast<unsigned long long>(t >> 64);
+              }
+              if (sub == 0) {
+                const unsigned __int128 U = (static_cast<unsigned __int128>(uhi) << 64) | ulo;
+                const uint64_t cnt =
+                    static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << (kResBias - 1))) >> kResBias);
+                const long long hv =
+                    static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << kResBias)));
+                hk[i] = (sub0 == 0 ? 0ll : hk[i]) + hv;
+                ck[i] = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
+              }
             }
-            if (tid == 0) {
+            if (tid == 0) {  // the node's sum |v| over its chunks so far (counters zeroed by the plan)
               unsigned long long add = 0;
 #pragma unroll
               for (int t = 0; t < 4; ++t) add += static_cast<unsigned long long>(s_absl[4 * k + t]) << (16 * t);
-              nd.absfix = (sub0 == 0 ? 0ull : nd.absfix) + add;
+              nd.absfix = add;
               if (sub0 == 0) c_hist_rows += nv;
             }
             __syncthreads();
@@ -764,6 +791,10 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           }
           __syncthreads();
         }
+        // the phi tables overlaid the limb cells: zero them again for the next histograms (the
+        // decide phase's barriers order these stores before any accumulate)
+        if (neq > 0)
+          for (int i = tid; i < min(3 * colh * 32, min(cap, neq) * 128); i += kResThreads) s_limb[i] = 0;
       }
       RES_PHASE(5);
       // ---- decide (decide_kernel) ------------------------------------------------------------
