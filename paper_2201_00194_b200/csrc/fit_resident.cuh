@@ -35,6 +35,26 @@ constexpr int kResBias = kResLimbs == 3 ? 62 : 40;  // u = v + 2^bias, count = r
 constexpr int kResMaxDepth = 7;  // node ids fit in uint8
 constexpr int kResClusterMax = 4;  // CTAs per family by default (FAMSEER_RES_CLUSTER overrides)
 constexpr int kResClusterMinRows = 1024;  // ... when the largest family has at least this many rows
+// Histogram rings: level L's bins live in ring L % 3. With a cluster, the owner of a feature
+// pushes its bins into the partners' ring as soon as it folds them; a partner last read that
+// ring at level L - 3 (screen, decisions) or L - 2 (as the parent in the sibling subtraction),
+// both before it arrived at level L - 1's exchange barrier, which the pusher has passed.
+constexpr int kResRings = 3;
+
+// distributed shared memory: the 32-bit shared::cluster address of the same offset in CTA rank
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st(uint32_t a, long long v) {
+  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st(uint32_t a, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 
 struct ResNode {
   int32_t n, seg, state, rep, bin, lc, wcount, build;
@@ -46,8 +66,8 @@ struct ResNode {
 
 struct ResLayout {
   int ls, slots, cs;
-  size_t codes, resid, pred, predv, targ, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, sbuf, stage, clc, binrep,
-      vals, cand, total;
+  size_t codes, resid, pred, predv, targ, fix, node, ord0, scratch, hsum, hcnt, lbuf, nodes, win, items, rep, limb, sbuf, stage, binrep,
+      vals, total;
 };
 
 __host__ __device__ inline size_t res_align(size_t v) { return (v + 15) & ~size_t(15); }
@@ -82,10 +102,10 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   o = res_align(o + static_cast<size_t>(n) * 2);
   L.scratch = o;
   o = res_align(o + static_cast<size_t>(n) * 2);
-  L.hsum = o;
-  o = res_align(o + static_cast<size_t>(2) * L.ls * bins * 8);
+  L.hsum = o;  // three level rings (kResRings)
+  o = res_align(o + static_cast<size_t>(kResRings) * L.ls * bins * 8);
   L.hcnt = o;
-  o = res_align(o + static_cast<size_t>(2) * L.ls * bins * 4);
+  o = res_align(o + static_cast<size_t>(kResRings) * L.ls * bins * 4);
   L.lbuf = o;
   o = res_align(o + static_cast<size_t>(L.ls) * bins * 8);
   L.nodes = o;
@@ -99,18 +119,15 @@ __host__ __device__ inline ResLayout res_layout(int n, int nrep, int bins, int d
   L.limb = o;  // lane-column limb histogram [3][colh][32] u32; the tie classes' phi tables
                // between histograms
   o = res_align(o + std::max<size_t>(static_cast<size_t>(3) * colh * 32 * 4, 8 * 512));
-  L.sbuf = o;  // speculative exact folds: spec_bufs member lists of up to n rows (u16)
-  o = res_align(o + static_cast<size_t>(spec_bufs) * n * 2);
+  L.sbuf = o;  // speculative exact folds: spec_bufs member lists of up to n rows (u16); during the
+               // screen: (gain, bound) doubles and the left count per (node at level, bin)
+  o = res_align(o + std::max(static_cast<size_t>(spec_bufs) * n * 2, static_cast<size_t>(L.ls) * bins * 20));
   L.stage = o;  // exact-fold staging: per warp 32 doubles + 32 codes
   o = res_align(o + static_cast<size_t>(kResWarps) * 32 * 9);
-  L.clc = o;  // left count per (node at level, bin)
-  o = res_align(o + static_cast<size_t>(L.ls) * bins * 4);
   L.binrep = o;  // feature (rep) of every bin, then this CTA's owned bins in order (histogram fold)
   o = res_align(o + static_cast<size_t>(bins) * 4);
   L.vals = o;  // threshold value of every bin + original feature of every rep (split records)
   o = res_align(o + static_cast<size_t>(bins) * 8 + nr * 4);
-  L.cand = o;  // screened (gain, bound) per (node at level, bin)
-  o = res_align(o + static_cast<size_t>(L.ls) * bins * 16);
   L.total = o;
   return L;
 }
@@ -244,8 +261,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
   uint32_t* s_limb = reinterpret_cast<uint32_t*>(sm + Lo.limb);  // [3][colh][32]
   int* s_cofs = reinterpret_cast<int*>(sm + Lo.rep) + 2 * (nrep > 0 ? nrep : 1);       // [nrep]
   uint32_t* s_absl = reinterpret_cast<uint32_t*>(s_cofs + (nrep > 0 ? nrep : 1));      // [level node][4]
-  double* s_cand = reinterpret_cast<double*>(sm + Lo.cand);  // [level node][bin] x (g, delta)
-  int* s_clc = reinterpret_cast<int*>(sm + Lo.clc);           // [level node][bin] left count
+  double* s_cand = reinterpret_cast<double*>(sm + Lo.sbuf);  // [level node][bin] x (g, delta), screen only
+  int* s_clc = reinterpret_cast<int*>(s_cand + 2 * static_cast<size_t>(Lo.ls) * bins);  // left counts
   uint16_t* s_binrep = reinterpret_cast<uint16_t*>(sm + Lo.binrep);
   uint16_t* s_own = s_binrep + bins;  // bins of this CTA's histogram features (j % cl_n == cl_r)
   __shared__ int s_nown;
@@ -416,7 +433,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
       __syncthreads();
       RES_PHASE(1);
       if (level == depth || nrep == 0) break;
-      const int ring = level & 1;
+      const int ring = level % kResRings;
       long long* hs = s_hsum + static_cast<size_t>(ring) * ls * bins;
       int* hc = s_hcnt + static_cast<size_t>(ring) * ls * bins;
       // ---- histograms of every directly built node of the level, one node at a time, in lane
@@ -537,8 +554,16 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                     static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << (kResBias - 1))) >> kResBias);
                 const long long hv =
                     static_cast<long long>(static_cast<uint64_t>(U - (static_cast<unsigned __int128>(cnt) << kResBias)));
-                hk[i] = (sub0 == 0 ? 0ll : hk[i]) + hv;
-                ck[i] = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
+                const long long hsv = (sub0 == 0 ? 0ll : hk[i]) + hv;
+                const int hcv = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
+                hk[i] = hsv;
+                ck[i] = hcv;
+                if (kClu && sub0 + kAtomSub >= nv)  // the node's final bin: push it to the partners
+                  for (int r = 1; r < cl_n; ++r) {
+                    const int rr = (cl_r + r) % cl_n;
+                    dsmem_st(dsmem_addr(hk + i, rr), hsv);
+                    dsmem_st(dsmem_addr(ck + i, rr), hcv);
+                  }
               }
             }
             if (tid == 0) {  // the node's sum |v| over its chunks so far (counters zeroed by the plan)
@@ -554,27 +579,14 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
 #endif
           }
         }
-        if (cl_n > 1) {  // the partners' features of every built node, through DSMEM
-          cluster.sync();
-          for (int k = 0; k < nl; ++k) {
-            if (s_nodes[first + k].build != 1) continue;
-            long long* hk = hs + static_cast<size_t>(k) * bins;
-            int* ck = hc + static_cast<size_t>(k) * bins;
-            for (int i = tid; i < bins; i += kResThreads) {
-              const int owner = s_binrep[i] % cl_n;
-              if (owner == cl_r) continue;
-              hk[i] = *cluster.map_shared_rank(hk + i, owner);
-              ck[i] = *cluster.map_shared_rank(ck + i, owner);
-            }
-          }
-          __syncthreads();
-        }
+        if (cl_n > 1) cluster.sync();  // the partners' pushed bins visible (arrive.release / wait.acquire)
       }
       RES_PHASE(2);
       // ---- siblings by exact subtraction --------------------------------------------------------
       if (level > 0) {
-        const long long* hp = s_hsum + static_cast<size_t>(ring ^ 1) * ls * bins;
-        const int* cp = s_hcnt + static_cast<size_t>(ring ^ 1) * ls * bins;
+        const int pring = (level + kResRings - 1) % kResRings;
+        const long long* hp = s_hsum + static_cast<size_t>(pring) * ls * bins;
+        const int* cp = s_hcnt + static_cast<size_t>(pring) * ls * bins;
         const int pfirst = (1 << (level - 1)) - 1;
         for (int k2 = 0; k2 < nl / 2; ++k2) {
           const int parent = pfirst + k2;

@@ -8,5 +8,5 @@ import json,sys; d=json.loads(sys.stdin.read()); p=d['resident_phase_cycles_cta0
   python -c "
 import json; d=json.load(open('gpurun_out/ab.json')); print('value', round(d['value']), 'ms', round(d['ms_per_step'],3), 'fit_resident', d['kernel_ms_one_step'].get('fit_resident'))"
 }
-for lib in paper_2201_00194_b200/libfamseer.so var/*/libfamseer.so; do abrun $lib ""; done
+for lib in paper_2201_00194_b200/libfamseer.so var/*/libfamseer.so; do [ -f "$lib" ] && abrun $lib ""; done
 for e in ${AB_ENVS}; do abrun paper_2201_00194_b200/libfamseer.so "$e"; done
