@@ -220,6 +220,75 @@ __device__ __forceinline__ double fold_spec(const double* __restrict__ v, const 
 
 
 
+// The fold chain s = start + x_0 + x_1 + ... (separately rounded) over a CONTIGUOUS array x[0..n): 16-byte loads (two elements per shared load),
+// eight elements in flight ahead of the dependent adds.
+__device__ __forceinline__ double fold_c(const double* __restrict__ x, int n, double s) {
+  int i = 0;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) && n > 0) s = fs_add(s, x[i++]);  // align to 16 bytes
+  const double2* x2 = reinterpret_cast<const double2*>(x + i);
+  const int n2 = (n - i) >> 1;
+  int k = 0;
+  if (n2 >= 4) {
+    double2 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = x2[u];
+    for (k = 4; k + 4 <= n2; k += 4) {
+      double2 b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = x2[k + u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s = fs_add(s, a[u].x);
+        s = fs_add(s, a[u].y);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = b[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s = fs_add(s, a[u].x);
+      s = fs_add(s, a[u].y);
+    }
+  }
+  for (; k < n2; ++k) {
+    const double2 a = x2[k];
+    s = fs_add(s, a.x);
+    s = fs_add(s, a.y);
+  }
+  for (i += 2 * n2; i < n; ++i) s = fs_add(s, x[i]);
+  return s;
+}
+
+// fold_spec over a contiguous array (warp-collective; lane 0 exact first half, lanes 1..31 the
+// second half from P - 15 .. P + 15 ulp)
+__device__ __forceinline__ double fold_spec_c(const double* __restrict__ x, int n) {
+  const int lane = threadIdx.x & 31;
+  if (n < 192) return fold_c(x, n, 0.0);
+  const int m = n >> 1;
+  double hi = 0.0, lo = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    double s, e;
+    two_sum(hi, x[i], s, e);
+    hi = s;
+    lo = fs_add(lo, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, e;
+    two_sum(hi, oh, s, e);
+    hi = s;
+    lo = fs_add(fs_add(lo, ol), e);
+  }
+  const double P = fs_add(hi, lo);
+  const double start = lane == 0 ? 0.0 : ord_dbl(dbl_ord(P) + (lane - 16));
+  // one call with per-lane arguments (two call sites would run the halves one after the other)
+  const double s = fold_c(lane == 0 ? x : x + m, lane == 0 ? m : n - m, start);
+  const double Sm = __shfl_sync(0xffffffffu, s, 0);
+  const unsigned hit = __ballot_sync(0xffffffffu, lane != 0 && __double_as_longlong(start) == __double_as_longlong(Sm));
+  if (hit) return __shfl_sync(0xffffffffu, s, __ffs(hit) - 1);
+  return fold_c(x + m, n - m, Sm);  // speculation missed: finish from the true midpoint
+}
+
 // kClu: launched as a thread-block cluster (several CTAs per family); false compiles the
 // single-CTA shape without any cluster arithmetic.
 template <bool kClu>
@@ -1151,12 +1220,18 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     }
       RES_PHASE(1);
     // ---- leaves (leaf_kernel): reference-order total / n, prediction update ------------------
-    for (int s = warp; s < slots; s += kResThreads / 32) {
+    // residuals in order-0 list order, contiguous (every leaf's rows are a contiguous segment of
+    // the list): the chains read two elements per 16-byte load instead of two loads per element.
+    // The fixed-point residuals' buffer is free after the last histogram.
+    double* s_gath = reinterpret_cast<double*>(s_fix);
+    for (int i = tid; i < n; i += kResThreads) s_gath[i] = s_resid[s_ord0[i]];
+    __syncthreads();
+    for (int s = warp; s < slots; s += kResWarps) {
       ResNode& nd = s_nodes[s];
       if (nd.state != kNodeLeaf || nd.n == 0) continue;
       if (s > 0 && s_nodes[(s - 1) >> 1].state != kNodeSplit) continue;
       const int nv = nd.n;
-      const double sum = fold_spec(s_resid, s_ord0 + nd.seg, nv);  // warp-collective
+      const double sum = fold_spec_c(s_gath + nd.seg, nv);  // warp-collective
       const double value = fs_div(sum, static_cast<double>(nv));
       if (lane == 0) {
         nd.value = value;
