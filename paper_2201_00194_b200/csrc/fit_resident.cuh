@@ -627,12 +627,6 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                 const int hcv = (sub0 == 0 ? 0 : ck[i]) + static_cast<int>(cnt);
                 hk[i] = hsv;
                 ck[i] = hcv;
-                if (kClu && sub0 + kAtomSub >= nv)  // the node's final bin: push it to the partners
-                  for (int r = 1; r < cl_n; ++r) {
-                    const int rr = (cl_r + r) % cl_n;
-                    dsmem_st(dsmem_addr(hk + i, rr), hsv);
-                    dsmem_st(dsmem_addr(ck + i, rr), hcv);
-                  }
               }
             }
             if (tid == 0) {  // the node's sum |v| over its chunks so far (counters zeroed by the plan)
@@ -648,10 +642,44 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
 #endif
           }
         }
-        if (cl_n > 1) cluster.sync();  // the partners' pushed bins visible (arrive.release / wait.acquire)
+        // prefix form: the owner turns each of its features' bins of every directly built node
+        // into inclusive prefix sums over the feature's bins (warp per (node, feature), lanes
+        // over bins) and pushes them to the partners. Sums and counts are exact integers and
+        // prefix is linear: siblings derive prefix from prefix, the screen reads a candidate's
+        // left sum / count and the node total in O(1), the exact decision needs no count scan.
+        const int nown_f = (nrep - cl_r + cl_n - 1) / cl_n;
+        for (int it = warp; it < nl * nown_f; it += kResWarps) {
+          const int k = it / nown_f, j = (it - k * nown_f) * cl_n + cl_r;
+          if (s_nodes[first + k].build != 1) continue;
+          long long* h = hs + static_cast<size_t>(k) * bins + s_repb[j];
+          int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+          const int nb = s_repn[j];
+          long long hcar = 0;
+          int ccar = 0;
+          for (int b0 = 0; b0 < nb; b0 += 32) {
+            const int b = b0 + lane;
+            const long long hv = warp_incl_scan(b < nb ? h[b] : 0ll, lane) + hcar;
+            const int cv = warp_incl_scan(b < nb ? c[b] : 0, lane) + ccar;
+            if (b < nb) {
+              h[b] = hv;
+              c[b] = cv;
+              if (kClu)
+                for (int r = 1; r < cl_n; ++r) {
+                  const int rr = (cl_r + r) % cl_n;
+                  dsmem_st(dsmem_addr(h + b, rr), hv);
+                  dsmem_st(dsmem_addr(c + b, rr), cv);
+                }
+            }
+            hcar = __shfl_sync(0xffffffffu, hv, 31);
+            ccar = __shfl_sync(0xffffffffu, cv, 31);
+          }
+        }
+        // the partners' pushed prefix sums visible (arrive.release / wait.acquire)
+        if (cl_n > 1) cluster.sync();
+        else __syncthreads();
       }
       RES_PHASE(2);
-      // ---- siblings by exact subtraction --------------------------------------------------------
+      // ---- siblings by exact subtraction (of prefix sums) ------------------------------------
       if (level > 0) {
         const int pring = (level + kResRings - 1) % kResRings;
         const long long* hp = s_hsum + static_cast<size_t>(pring) * ls * bins;
@@ -716,18 +744,12 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                   z.best_bin = -1;
                   s_win[k * nrep + j] = z;
                 }
-                long long is = 0, ts = 0;
-                for (int t = 0; t < nb; ++t) {
-                  const long long hv = h[t];
-                  ts += hv;
-                  if (t <= b) {
-                    is += hv;
-                    ic += c[t];
-                  }
-                }
+                const long long is = h[b], ts = h[nb - 1];  // prefix form
+                ic = c[b];
+                const int cb = ic - (b > 0 ? c[b - 1] : 0);
                 s_clc[ci] = ic;
                 const int nv = ndp->n;
-                if (c[b] > 0 && ic < nv) {
+                if (cb > 0 && ic < nv) {
                   const double S = static_cast<double>(ndp->absfix) * scale * (1.0 + 1e-12);
                   double g, hi;
                   screen_gain(is, ts, ic, nv, scale, S, g, lo, hi);
@@ -1063,8 +1085,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           int carry = 0;
           for (int b0 = 0; b0 < nb && carry < lim; b0 += 32) {
             const int b = b0 + lane;
-            const int cb = b < nb ? c[b] : 0;
-            const int cum = warp_incl_scan(cb, lane) + carry;
+            const int cum = b < nb ? c[b] : 0;  // prefix form
+            const int cb = b < nb ? cum - (b > 0 ? c[b - 1] : 0) : 0;
             if (cb > 0 && cum < nv && cum <= lim) {  // folds stop at the last window candidate
               const double L = lb[b];
               const double R = fs_sub(T, L);
@@ -1079,7 +1101,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
                 blc = cum;
               }
             }
-            carry = __shfl_sync(0xffffffffu, cum, 31);
+            carry = c[min(b0 + 31, nb - 1)];
           }
         }
         for (int o = 16; o > 0; o >>= 1) {
