@@ -726,7 +726,7 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
             break;
           }
       }
-      if (cl != 1 && cl != 2 && cl != 4) fail(FS_EINVAL, "FAMSEER_RES_CLUSTER must be 1, 2 or 4");
+      if (cl != 1 && cl != 2 && cl != 4 && cl != 8) fail(FS_EINVAL, "FAMSEER_RES_CLUSTER must be 1, 2, 4 or 8");
       bool ok = res.pred_smem;
       for (int f : res.families) ok = ok && ceil_div(fam[static_cast<size_t>(f)].nrep, cl) <= 32;
       res.cluster = ok ? cl : 1;

@@ -89,7 +89,7 @@ def test_fit_records_equals_fit_on_featurized_rows(dev, orc):
             assert np.array_equal(getattr(ea, k), getattr(eb, k)), (f, k)
 
 
-@pytest.mark.parametrize("cluster", ["1", "2", "4"])
+@pytest.mark.parametrize("cluster", ["1", "2", "4", "8"])
 def test_resident_cluster_sizes_bit_exact(dev, orc, monkeypatch, cluster):
     """The resident trainer's thread-block-cluster shapes (histogram features dealt over 1, 2 or 4
     CTAs, bins exchanged through distributed shared memory) all reproduce the oracle's trees."""
