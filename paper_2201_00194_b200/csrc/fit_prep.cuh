@@ -653,30 +653,41 @@ __global__ void __launch_bounds__(kSortThreads) canonical_bitonic_kernel(
 __global__ void base_kernel(const FamDesc* __restrict__ fam, const double* __restrict__ target_c,
                             double* __restrict__ base, double* __restrict__ pred, const int32_t* __restrict__ ord,
                             int32_t* __restrict__ ord_root) {
+  // sequential mean in canonical order (costmodel.cpp:185-188): the targets are staged into
+  // shared memory 2,048 at a time by the whole CTA (coalesced), and thread 0 folds each stage
+  // from shared memory (L2 latency only once per stage instead of once per 8 elements)
+  constexpr int kStage = 2048;
+  __shared__ double st[kStage];
   const FamDesc fd = fam[blockIdx.x];
-  if (threadIdx.x == 0) {  // sequential mean in canonical order (costmodel.cpp:185-188)
-    const double* t = target_c + fd.pos0;
-    double s = 0.0;
-    int i = 0;
-    if (fd.n >= 8) {  // the next 8 loads are in flight while 8 dependent adds run
-      double a[8];
+  const double* t = target_c + fd.pos0;
+  double s = 0.0;
+  for (int c0 = 0; c0 < fd.n; c0 += kStage) {
+    const int m = min(kStage, fd.n - c0);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) st[i] = t[c0 + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int i = 0;
+      if (m >= 8) {  // the next 8 loads are in flight while 8 dependent adds run
+        double a[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] = t[k];
-      for (i = 8; i + 8 <= fd.n; i += 8) {
-        double b[8];
+        for (int k = 0; k < 8; ++k) a[k] = st[k];
+        for (i = 8; i + 8 <= m; i += 8) {
+          double b[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) b[k] = t[i + k];
+          for (int k = 0; k < 8; ++k) b[k] = st[i + k];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[k] = b[k];
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) a[k] = b[k];
       }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s = fs_add(s, a[k]);
+      for (; i < m; ++i) s = fs_add(s, st[i]);
     }
-    for (; i < fd.n; ++i) s = fs_add(s, t[i]);
-    base[blockIdx.x] = fd.n ? fs_div(s, static_cast<double>(fd.n)) : 0.0;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) base[blockIdx.x] = fd.n ? fs_div(s, static_cast<double>(fd.n)) : 0.0;
   __syncthreads();
   const double b = base[blockIdx.x];
   for (int i = threadIdx.x; i < fd.n; i += blockDim.x) {
