@@ -350,12 +350,16 @@ def run_native(args, rank, world, local_rank):
         return out
 
     def step():
-        if F:
+        # one tuning round: score every pool with the current models + refit every family; by
+        # default through fs_tune_step_d (the scoring overlaps the refit on a second stream,
+        # identical results), --no-overlap issues fs_score_d then fs_fit_d
+        if F and not args.no_overlap:
+            forest.tune_step_d(spaces, pool_so, pool_a, PAD, pool_seg, scores, perm, x_tr, y_tr, tr_seg, params)
+        elif F:
             spaces.score_d(forest, pool_so, pool_a, PAD, pool_seg, scores, perm)
+            forest.fit_d(x_tr, y_tr, tr_seg, params)
         if dist is not None:
             topk_allgather()
-        if F:
-            forest.fit_d(x_tr, y_tr, tr_seg, params)
 
     def timed(fn, k, flush_between=True):
         times = []
@@ -436,8 +440,11 @@ def run_native(args, rank, world, local_rank):
             if not F:
                 d2h[0] = 0
                 return
-            s_h, p_h = spaces.score(forest, h_so, h_a, PAD, pool_seg)
-            forest.fit_records(spaces, h_tso, h_ta, PAD, h_y, seg=tr_seg, params=params)
+            if args.no_overlap:
+                s_h, p_h = spaces.score(forest, h_so, h_a, PAD, pool_seg)
+                forest.fit_records(spaces, h_tso, h_ta, PAD, h_y, seg=tr_seg, params=params)
+            else:
+                s_h, p_h = forest.tune_step(spaces, h_so, h_a, PAD, pool_seg, h_tso, h_ta, h_y, tr_seg, params=params)
             nbytes = s_h.nbytes + p_h.nbytes
             for f in range(F):
                 e = forest.export(f)
@@ -460,7 +467,8 @@ def run_native(args, rank, world, local_rank):
         e2e = {"value": P_job * args.steps / (e_total / 1e3), "unit": "candidates/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
                "train_rows_per_s": N_job * args.steps / (e_total / 1e3), "ms_per_step": e_total / args.steps,
-               "api": "fs_score + fs_fit_records + fs_forest_export (host pointers)"}
+               "api": ("fs_score + fs_fit_records" if args.no_overlap else "fs_tune_step (score + fit_records, overlapped)")
+               + " + fs_forest_export (host pointers)"}
 
     # ---- incremental retrain (fs_store): the tuning loop's real pattern ----
     incremental = None
@@ -885,6 +893,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="score then refit as two calls instead of one fs_tune_step (scoring forked onto a second stream)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--shard", default=None, choices=["replicate", "families"],

@@ -143,6 +143,26 @@ int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t
                const int64_t* seg_h, const int32_t* space_of_d, const int32_t* assign_d,
                int32_t pad_dim, double* scores_d, int32_t* perm_d);
 
+/* ---- one tuning round: score + refit, overlapped (scheduler.cpp:187-192 + :233-238) ---------
+ * fs_score of the pools with the forest's CURRENT models and a refit of every fit segment, as
+ * one call: the scoring runs on the device's second stream concurrently with the refit's
+ * preparation and boosting rounds, and the refit writes the new models only after the scoring
+ * has read the old ones - results identical to fs_score followed by fs_fit_d / fs_fit_records.
+ * fs_tune_step_d: device pointers, training rows as features (fs_fit_d's x/target); returns
+ * like fs_fit_d (deferred errors of the scoring surface at the next fs_device_check).
+ * fs_tune_step: host pointers, training rows as measurement records featurized on the device
+ * (fs_fit_records); scores/perm are complete and every error raised on return. */
+int fs_tune_step_d(fs_device* dev, const fs_spaces* sp, fs_forest* fo, int32_t n_pool_segments,
+                   const int64_t* pool_seg_h, const int32_t* pool_space_of_d, const int32_t* pool_assign_d,
+                   int32_t pad_dim, double* scores_d, int32_t* perm_d, int32_t n_fit_segments,
+                   const int64_t* fit_seg_h, const double* x_d, const double* target_d,
+                   const fs_gbt_params* params);
+int fs_tune_step(fs_device* dev, const fs_spaces* sp, fs_forest* fo, int32_t n_pool_segments,
+                 const int64_t* pool_seg, const int32_t* pool_space_of, const int32_t* pool_assign,
+                 int32_t pad_dim, double* scores, int32_t* perm, int32_t n_fit_segments,
+                 const int64_t* fit_seg, const int32_t* fit_space_of, const int32_t* fit_assign,
+                 const double* fit_target, const fs_gbt_params* params);
+
 /* ---- score from linear_index descriptors -------------------------------
  * As fs_score, but candidate i is (space_of[i], index[i]) with index[i] =
  * linear_index(space, assignment) (searchspace.cpp:48-54), decoded on the device exactly as

@@ -399,6 +399,38 @@ class Forest:
         _check(_lib().fs_fit_records_d(self.dev.h, self.h, spaces.h, nf, sp, space_of_t.data_ptr(),
                                        assign_t.data_ptr(), pad_dim, target_t.data_ptr(), pa))
 
+    def tune_step_d(self, spaces: "Spaces", pool_so_t, pool_a_t, pad_dim: int, pool_seg, scores_t, perm_t, x_t,
+                    target_t, fit_seg, params=None):
+        """One tuning round, overlapped (fs_tune_step_d): score the pools with the CURRENT models
+        (scheduler.cpp:187-192) while refitting every fit segment (:233-238); same results as
+        Spaces.score_d followed by fit_d."""
+        psg, psp = _seg(pool_seg)
+        fsg, fsp = _seg(fit_seg)
+        pa = _params_array(params, len(fsg) - 1)
+        _check(_lib().fs_tune_step_d(self.dev.h, spaces.h, self.h, len(psg) - 1, psp, pool_so_t.data_ptr(),
+                                     pool_a_t.data_ptr(), pad_dim, scores_t.data_ptr(),
+                                     None if perm_t is None else perm_t.data_ptr(), len(fsg) - 1, fsp,
+                                     x_t.data_ptr(), target_t.data_ptr(), pa))
+
+    def tune_step(self, spaces: "Spaces", pool_so, pool_a, pad_dim: int, pool_seg, tr_so, tr_a, tr_target, fit_seg,
+                  params=None):
+        """fs_tune_step, host buffers: returns (scores, perm) of the pools under the models as
+        they were, then the forest holds the refit models (training rows as records)."""
+        so = np.ascontiguousarray(pool_so, np.int32)
+        a = np.ascontiguousarray(pool_a, np.int32)
+        tso = np.ascontiguousarray(tr_so, np.int32)
+        ta = np.ascontiguousarray(tr_a, np.int32)
+        ty = np.ascontiguousarray(tr_target, np.float64)
+        psg, psp = _seg(pool_seg)
+        fsg, fsp = _seg(fit_seg)
+        pa = _params_array(params, len(fsg) - 1)
+        scores = np.empty(len(so), np.float64)
+        perm = np.empty(len(so), np.int32)
+        _check(_lib().fs_tune_step(self.dev.h, spaces.h, self.h, len(psg) - 1, psp, _p(so, _capi._i32p),
+                                   _p(a, _capi._i32p), pad_dim, _p(scores, _capi._dp), _p(perm, _capi._i32p),
+                                   len(fsg) - 1, fsp, _p(tso, _capi._i32p), _p(ta, _capi._i32p), _p(ty, _capi._dp), pa))
+        return scores, perm
+
     def fit_stats(self, family: int):
         a, b = C.c_int64(), C.c_int64()
         _check(_lib().fs_forest_fit_stats(self.h, family, C.byref(a), C.byref(b)))

@@ -60,6 +60,10 @@ SIGNATURES = [
     ("fs_store_fit", C.c_int, [_vp, _vp, C.c_int32, _i32p, C.POINTER(GbtParams)]),
     ("fs_score", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _i32p, C.c_int32, _dp, _i32p]),
     ("fs_score_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp]),
+    ("fs_tune_step_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp, C.c_int32, _i64p,
+                                  _vp, _vp, _vp]),
+    ("fs_tune_step", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _i32p, C.c_int32, _dp, _i32p, C.c_int32,
+                                _i64p, _i32p, _i32p, _dp, _vp]),
     ("fs_score_index", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _u64p, C.c_int32, _dp, _i32p]),
     ("fs_score_index_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp]),
     ("fs_feature_dim", C.c_int, [C.c_int32]),

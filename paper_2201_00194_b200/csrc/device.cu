@@ -114,6 +114,8 @@ cudaStream_t fs_device::aux_stream() {
     FS_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
     FS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     FS_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    FS_CUDA(cudaMalloc(&err_aux_d, sizeof(uint32_t)));
+    FS_CUDA(cudaMemsetAsync(err_aux_d, 0, sizeof(uint32_t), stream));
   }
   return aux;
 }
@@ -187,6 +189,7 @@ int fs_device_destroy(fs_device* d) {
       if (b.p) cudaFreeAsync(b.p, d->stream);
     cudaStreamSynchronize(d->stream);
     if (d->err_d) cudaFree(d->err_d);
+    if (d->err_aux_d) cudaFree(d->err_aux_d);
     if (d->ctr_d) cudaFree(d->ctr_d);
     if (d->err_h) cudaFreeHost(d->err_h);
     if (d->pinned_h) cudaFreeHost(d->pinned_h);

@@ -865,6 +865,11 @@ void fit_families(fs_device* dev, fs_forest* fo, int F, const int64_t* seg, int 
 
   // ---- results: heap-slot records -> pre-order CostModelState layout ------------------------
   htick("rounds launched");
+  // a forked reader of the current models (fs_tune_step's scoring) must finish first
+  if (dev->epilogue_wait) {
+    FS_CUDA(cudaStreamWaitEvent(s, dev->epilogue_wait, 0));
+    dev->epilogue_wait = nullptr;
+  }
   // Epilogue. Default: export + compile on the device straight into each family's model blob
   // (no host round trip; the host pre-order arrays are materialised when first asked for).
   // FAMSEER_HOST_COMPILE=1 (or trees deeper than the device compile handles): read the tree
@@ -1084,6 +1089,151 @@ int fs_fit_records(fs_device* dev, fs_forest* fo, const fs_spaces* sp, int32_t n
     auto* xd = static_cast<double*>(dev->scratch(fs::kSlotFitX, std::max<int64_t>(n * pad, 1) * sizeof(double)));
     fs::launch_featurize(dev, sp, n, sd, ad, pad, xd);
     fs::fit::fit_families(dev, fo, nseg, seg, pad, xd, td, params);
+  });
+}
+
+}  // extern "C"
+
+namespace fs {
+void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg,
+                  const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores_d, int32_t* perm_d,
+                  const uint64_t* index_d);
+namespace {
+__global__ void merge_err_kernel(uint32_t* err, uint32_t* err_aux) {
+  if (*err_aux) {
+    *err |= *err_aux;
+    *err_aux = 0;
+  }
+}
+
+// One tuning round (tune_step's scoring, scheduler.cpp:187-192, and train_and_charge's refit,
+// :233-238) with the two halves overlapped: the pools are scored with the forest's CURRENT
+// models on the device's aux stream (forked after the main stream's prior work, own error word)
+// while the main stream runs the refit; the refit's epilogue - the first write of any model
+// blob - waits for the scoring. `prefix` (host-pointer variant: the pool's H2D copies) and
+// `suffix` (its D2H copies) run on the aux stream around the scoring; `fit` runs on the main
+// stream. On return the main stream is joined with the fork and the fork's deferred errors are
+// merged into the device's error word.
+template <class Pre, class Score, class Post, class Fit>
+void tune_step(fs_device* dev, Pre prefix, Score score, Post suffix, Fit fit) {
+  cudaStream_t main = dev->stream, aux = dev->aux_stream();
+  uint32_t* err_main = dev->err_d;
+  FS_CUDA(cudaEventRecord(dev->ev_fork, main));
+  FS_CUDA(cudaStreamWaitEvent(aux, dev->ev_fork, 0));
+  dev->stream = aux;
+  dev->err_d = dev->err_aux_d;
+  try {
+    prefix();
+    score();
+    suffix();
+  } catch (...) {
+    dev->stream = main;
+    dev->err_d = err_main;
+    FS_CUDA(cudaEventRecord(dev->ev_join, aux));
+    FS_CUDA(cudaStreamWaitEvent(main, dev->ev_join, 0));
+    throw;
+  }
+  dev->stream = main;
+  dev->err_d = err_main;
+  FS_CUDA(cudaEventRecord(dev->ev_join, aux));
+  dev->epilogue_wait = dev->ev_join;
+  auto join = [&] {
+    dev->epilogue_wait = nullptr;
+    FS_CUDA(cudaStreamWaitEvent(main, dev->ev_join, 0));
+    merge_err_kernel<<<1, 1, 0, main>>>(dev->err_d, dev->err_aux_d);
+    FS_CUDA(cudaGetLastError());
+  };
+  try {
+    fit();
+  } catch (...) {
+    join();
+    throw;
+  }
+  join();
+}
+}  // namespace
+}  // namespace fs
+
+extern "C" {
+
+int fs_tune_step_d(fs_device* dev, const fs_spaces* sp, fs_forest* fo, int32_t n_pool_segments,
+                   const int64_t* pool_seg_h, const int32_t* pool_space_of_d, const int32_t* pool_assign_d,
+                   int32_t pad_dim, double* scores_d, int32_t* perm_d, int32_t n_fit_segments,
+                   const int64_t* fit_seg_h, const double* x_d, const double* target_d,
+                   const fs_gbt_params* params) {
+  return fs::guard([&] {
+    if (!dev || !sp || !fo || n_pool_segments < 0 || !pool_seg_h || pad_dim < 0 || n_fit_segments < 0 ||
+        !fit_seg_h || !params)
+      fs::fail(FS_EINVAL, "fs_tune_step: bad arguments");
+    dev->activate();
+    fs::tune_step(
+        dev, [] {},
+        [&] {
+          if (pool_seg_h[n_pool_segments] > 0)
+            fs::score_device(dev, sp, fo, n_pool_segments, pool_seg_h, pool_space_of_d, pool_assign_d, pad_dim,
+                             scores_d, perm_d, nullptr);
+        },
+        [] {}, [&] { fs::fit::fit_families(dev, fo, n_fit_segments, fit_seg_h, pad_dim, x_d, target_d, params); });
+  });
+}
+
+int fs_tune_step(fs_device* dev, const fs_spaces* sp, fs_forest* fo, int32_t n_pool_segments, const int64_t* pool_seg,
+                 const int32_t* pool_space_of, const int32_t* pool_assign, int32_t pad_dim, double* scores,
+                 int32_t* perm, int32_t n_fit_segments, const int64_t* fit_seg, const int32_t* fit_space_of,
+                 const int32_t* fit_assign, const double* fit_target, const fs_gbt_params* params) {
+  return fs::guard([&] {
+    if (!dev || !sp || !fo || n_pool_segments < 0 || !pool_seg || pad_dim < 0 || n_fit_segments < 0 || !fit_seg ||
+        !params)
+      fs::fail(FS_EINVAL, "fs_tune_step: bad arguments");
+    if (pool_seg[0] != 0 || fit_seg[0] != 0) fs::fail(FS_EINVAL, "fs_tune_step: seg[0] must be 0");
+    dev->activate();
+    const int64_t P = pool_seg[n_pool_segments], n = fit_seg[n_fit_segments];
+    for (int64_t i = 0; i < n; ++i) {  // the reference validates every record's dimension (searchspace.cpp:94-101)
+      const int s = fit_space_of[i];
+      if (s < 0 || s >= sp->n) fs::fail(FS_EINVAL, "fit_records: unknown space id");
+      if (pad_dim < fs_feature_dim(sp->k_h[static_cast<size_t>(s)])) fs::fail(FS_EINVAL, "fit_records: pad_dim too small");
+    }
+    int32_t *so = nullptr, *as = nullptr, *pd = nullptr;
+    double* sd = nullptr;
+    fs::tune_step(
+        dev,
+        [&] {  // pool descriptors in, on the fork
+          if (P <= 0) return;
+          so = static_cast<int32_t*>(dev->scratch(fs::kSlotH2D0, P * sizeof(int32_t)));
+          as = static_cast<int32_t*>(dev->scratch(fs::kSlotH2D1, P * FS_MAX_KNOBS * sizeof(int32_t)));
+          sd = static_cast<double*>(dev->scratch(fs::kSlotScoreS, P * sizeof(double)));
+          pd = static_cast<int32_t*>(dev->scratch(fs::kSlotScoreP, P * sizeof(int32_t)));
+          FS_CUDA(cudaMemcpyAsync(so, pool_space_of, P * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
+          FS_CUDA(cudaMemcpyAsync(as, pool_assign, P * FS_MAX_KNOBS * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                  dev->stream));
+        },
+        [&] {
+          if (P > 0) fs::score_device(dev, sp, fo, n_pool_segments, pool_seg, so, as, pad_dim, sd, pd, nullptr);
+        },
+        [&] {  // scores and permutation out, on the fork
+          if (P <= 0) return;
+          if (scores) FS_CUDA(cudaMemcpyAsync(scores, sd, P * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
+          if (perm) FS_CUDA(cudaMemcpyAsync(perm, pd, P * sizeof(int32_t), cudaMemcpyDeviceToHost, dev->stream));
+        },
+        [&] {  // records in, featurized on the device (simbackend.cpp:185), refit (costmodel.cpp:224-235)
+          const size_t b_so = static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(int32_t);
+          const size_t b_a = static_cast<size_t>(std::max<int64_t>(n, 1)) * FS_MAX_KNOBS * sizeof(int32_t);
+          const size_t b_t = static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(double);
+          auto* in = static_cast<unsigned char*>(dev->scratch(fs::kSlotFitIn, b_t + b_so + b_a + 32));
+          auto* td = reinterpret_cast<double*>(in);
+          auto* tsd = reinterpret_cast<int32_t*>(in + b_t);
+          auto* tad = reinterpret_cast<int32_t*>(in + b_t + b_so);
+          if (n) {
+            FS_CUDA(cudaMemcpyAsync(td, fit_target, n * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+            FS_CUDA(cudaMemcpyAsync(tsd, fit_space_of, n * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
+            FS_CUDA(cudaMemcpyAsync(tad, fit_assign, n * FS_MAX_KNOBS * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                    dev->stream));
+          }
+          auto* xd = static_cast<double*>(dev->scratch(fs::kSlotFitX, std::max<int64_t>(n * pad_dim, 1) * sizeof(double)));
+          fs::launch_featurize(dev, sp, n, tsd, tad, pad_dim, xd);
+          fs::fit::fit_families(dev, fo, n_fit_segments, fit_seg, pad_dim, xd, td, params);
+        });
+    fs::raise_deferred(dev->take_errors());  // the host outputs are complete (main joined the fork)
   });
 }
 

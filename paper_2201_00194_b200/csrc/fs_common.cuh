@@ -110,7 +110,9 @@ struct fs_device {
   cudaEvent_t up_evt = nullptr;    // recorded after the last upload from up_h
   void* pinned_upload(size_t bytes);  // waits until the previous upload from it has been read
   void upload_done();                 // record up_evt on the stream after issuing the copies
-  cudaStream_t aux = nullptr;      // forked work inside a round (trainer node totals)
+  cudaStream_t aux = nullptr;      // forked work: trainer node totals / the tune step's scoring
+  cudaEvent_t epilogue_wait = nullptr;  // fit_families waits for it before writing any model blob
+  uint32_t* err_aux_d = nullptr;   // error word of the tune step's forked scoring
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t aux_stream();       // lazily created (non-blocking) + its fork/join events
   void* scratch(int slot, size_t bytes);  // stream-ordered grow; contents undefined

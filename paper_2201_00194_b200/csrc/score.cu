@@ -37,9 +37,9 @@ __global__ void decode_index_kernel(const int32_t* __restrict__ space_of, const 
 
 // index_d != nullptr: candidates are (space id, linear_index) descriptors (SURVEY.md 8f row 1:
 // 4 + 8 bytes per candidate in, instead of the 4 + 64 of an int32[16] assignment)
-static void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg,
-                         const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores_d,
-                         int32_t* perm_d, const uint64_t* index_d = nullptr) {
+void score_device(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t nseg, const int64_t* seg,
+                  const int32_t* space_of_d, const int32_t* assign_d, int32_t pad, double* scores_d, int32_t* perm_d,
+                  const uint64_t* index_d) {
   const int64_t n = seg[nseg];
   if (n <= 0) return;
   if (seg[0] != 0) fail(FS_EINVAL, "score: seg[0] must be 0");
@@ -201,7 +201,7 @@ int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t
   return fs::guard([&] {
     if (!dev || !sp || !fo || nseg < 0 || !seg_h || pad_dim < 0) fs::fail(FS_EINVAL, "fs_score: bad arguments");
     dev->activate();
-    fs::score_device(dev, sp, fo, nseg, seg_h, space_of_d, assign_d, pad_dim, scores_d, perm_d);
+    fs::score_device(dev, sp, fo, nseg, seg_h, space_of_d, assign_d, pad_dim, scores_d, perm_d, nullptr);
   });
 }
 
@@ -218,7 +218,7 @@ int fs_score(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t n
     auto* pd = static_cast<int32_t*>(dev->scratch(fs::kSlotScoreP, n * sizeof(int32_t)));
     FS_CUDA(cudaMemcpyAsync(so, space_of, n * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
     FS_CUDA(cudaMemcpyAsync(as, assign, n * FS_MAX_KNOBS * sizeof(int32_t), cudaMemcpyHostToDevice, dev->stream));
-    fs::score_device(dev, sp, fo, nseg, seg, so, as, pad_dim, sd, pd);
+    fs::score_device(dev, sp, fo, nseg, seg, so, as, pad_dim, sd, pd, nullptr);
     if (scores) FS_CUDA(cudaMemcpyAsync(scores, sd, n * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
     if (perm) FS_CUDA(cudaMemcpyAsync(perm, pd, n * sizeof(int32_t), cudaMemcpyDeviceToHost, dev->stream));
     fs::raise_deferred(dev->take_errors());
