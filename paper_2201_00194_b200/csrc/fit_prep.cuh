@@ -589,6 +589,8 @@ __device__ __forceinline__ bool key_less(const uint32_t* a, const uint32_t* b, i
   return false;
 }
 
+constexpr int kBitonicE = 4;  // canonical_bitonic_kernel: sequence elements per thread in registers (P <= 4 T)
+
 __global__ void __launch_bounds__(kSortThreads) canonical_bitonic_kernel(
     const double* __restrict__ target, const uint16_t* __restrict__ codes_all, int d,
     const FamDesc* __restrict__ fam, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_nb,
@@ -625,26 +627,87 @@ __global__ void __launch_bounds__(kSortThreads) canonical_bitonic_kernel(
     k[W - 1] = static_cast<uint32_t>(tk);
   }
   __syncthreads();
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        uint32_t* a = ks + static_cast<size_t>(lo) * W;
-        uint32_t* b = ks + static_cast<size_t>(hi) * W;
-        if (key_less(b, a, W) == up) {
-          for (int w = 0; w < W; ++w) {
-            const uint32_t t = a[w];
-            a[w] = b[w];
-            b[w] = t;
+  // Bitonic sort of ROW IDS (the keys stay in place): element i of the sequence lives in thread
+  // i % T, register slot i / T (E = P / T slots, E <= kBitonicE). A compare-exchange keeps the
+  // smaller or larger of (key, row) - a total order, so both partners agree. Partners within a
+  // warp exchange by shuffle, partners in the same thread by register, others through shared
+  // memory (ids[] doubles as the exchange buffer): barriers only for strides in [32, T).
+  const int T = blockDim.x, E = P / T;
+  if (E >= 1 && E <= kBitonicE && (T & 31) == 0) {
+    const int lane = threadIdx.x & 31;
+    uint32_t v[kBitonicE];
+#pragma unroll
+    for (int e = 0; e < kBitonicE; ++e) v[e] = e < E ? static_cast<uint32_t>(threadIdx.x + e * T) : 0u;
+    auto less_rows = [&](uint32_t a, uint32_t b) {  // (key, row) order
+      const uint32_t* ka = ks + static_cast<size_t>(a) * W;
+      const uint32_t* kb = ks + static_cast<size_t>(b) * W;
+      for (int w = 0; w < W; ++w)
+        if (ka[w] != kb[w]) return ka[w] < kb[w];
+      return a < b;
+    };
+    for (int size = 2; size <= P; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        uint32_t pv[kBitonicE];
+        if (stride < 32) {
+#pragma unroll
+          for (int e = 0; e < kBitonicE; ++e) pv[e] = __shfl_xor_sync(0xffffffffu, v[e], stride);
+        } else if (stride >= T) {
+          const int es = stride / T;
+#pragma unroll
+          for (int e = 0; e < kBitonicE; ++e) {
+            pv[e] = v[0];
+#pragma unroll
+            for (int q = 0; q < kBitonicE; ++q)
+              if (q == (e ^ es)) pv[e] = v[q];
           }
-          const uint32_t t = ids[lo];
-          ids[lo] = ids[hi];
-          ids[hi] = t;
+        } else {
+#pragma unroll
+          for (int e = 0; e < kBitonicE; ++e)
+            if (e < E) ids[threadIdx.x + e * T] = v[e];
+          __syncthreads();
+#pragma unroll
+          for (int e = 0; e < kBitonicE; ++e)
+            if (e < E) pv[e] = ids[(threadIdx.x + e * T) ^ stride];
+          __syncthreads();
+        }
+#pragma unroll
+        for (int e = 0; e < kBitonicE; ++e) {
+          if (e >= E) continue;
+          const int i = threadIdx.x + e * T;
+          const bool up = (i & size) == 0, lower = (i & stride) == 0;
+          const bool pl = less_rows(pv[e], v[e]);  // partner smaller
+          // the lower position of an ascending pair keeps the smaller element, etc.
+          if (pl == (up == lower)) v[e] = pv[e];
         }
       }
-      __syncthreads();
+    }
+#pragma unroll
+    for (int e = 0; e < kBitonicE; ++e)
+      if (e < E) ids[threadIdx.x + e * T] = v[e];
+    __syncthreads();
+    (void)lane;
+  } else {
+    for (int size = 2; size <= P; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          uint32_t* a = ks + static_cast<size_t>(lo) * W;
+          uint32_t* b = ks + static_cast<size_t>(hi) * W;
+          if (key_less(b, a, W) == up) {
+            for (int w = 0; w < W; ++w) {
+              const uint32_t t = a[w];
+              a[w] = b[w];
+              b[w] = t;
+            }
+            const uint32_t t = ids[lo];
+            ids[lo] = ids[hi];
+            ids[hi] = t;
+          }
+        }
+        __syncthreads();
+      }
     }
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) canon[fd.pos0 + i] = static_cast<int32_t>(ids[i]);
