@@ -451,9 +451,14 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
     for (int s = tid; s < slots; s += kResThreads) {
       ResNode z;
       memset(&z, 0, sizeof z);
-      if (s == 0) z.n = n;
+      if (s == 0) {  // the root's plan (level_plan_kernel, level 0)
+        z.n = n;
+        if (nrep > 0 && node_needs_split(fd, 0, n)) z.build = 1;
+        else z.state = kNodeLeaf;
+      }
       s_nodes[s] = z;
     }
+    if (tid < 4) s_absl[tid] = 0;  // the root's sum |v| limb counters
     TreeRec* tr = trees + fd.tree0 + static_cast<int64_t>(ntrees) * slots_g;
     for (int s = tid; s < slots_g && lead; s += kResThreads) {
       TreeRec tz;
@@ -477,29 +482,7 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
 
     for (int level = 0; level <= depth; ++level) {
       const int first = (1 << level) - 1, nl = 1 << level;
-      // ---- plan (level_plan_kernel) --------------------------------------------------------
-      if (level < depth && tid < 4 * nl) s_absl[tid] = 0;  // the level's sum |v| limb counters
-      if (tid < nl) {
-        const int s = first + tid;
-        ResNode& nd = s_nodes[s];
-        if (level == 0) {
-          if (nrep > 0 && node_needs_split(fd, 0, nd.n)) nd.build = 1;
-          else nd.state = kNodeLeaf;
-        } else if (s_nodes[(s - 1) >> 1].state == kNodeSplit) {
-          const bool need = nrep > 0 && node_needs_split(fd, level, nd.n);
-          if (!need) nd.state = kNodeLeaf;
-          if (s & 1) {
-            const int sib = s + 1;
-            const bool need_sib = nrep > 0 && node_needs_split(fd, level, s_nodes[sib].n);
-            if (need || need_sib) {
-              const int small = nd.n <= s_nodes[sib].n ? s : sib;
-              s_nodes[small].build = 1;
-              s_nodes[small == s ? sib : s].build = 2;
-            }
-          }
-        }
-      }
-      __syncthreads();
+      // (the level's plan - leaf / build flags - was made when its parents split: split records)
       RES_PHASE(1);
       if (level == depth || nrep == 0) break;
       const int ring = level % kResRings;
@@ -635,6 +618,10 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
               for (int t = 0; t < 4; ++t) add += static_cast<unsigned long long>(s_absl[4 * k + t]) << (16 * t);
               nd.absfix = add;
               if (sub0 == 0) c_hist_rows += nv;
+              if (level > 0 && sub0 + kAtomSub >= nv) {  // the derived sibling's sum |v|
+                const int s = first + k, sib = (s & 1) ? s + 1 : s - 1;
+                if (s_nodes[sib].build == 2) s_nodes[sib].absfix = s_nodes[(s - 1) >> 1].absfix - add;
+              }
             }
             __syncthreads();
 #ifdef FS_RES_HIST_SPLIT
@@ -647,12 +634,26 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         // over bins) and pushes them to the partners. Sums and counts are exact integers and
         // prefix is linear: siblings derive prefix from prefix, the screen reads a candidate's
         // left sum / count and the node total in O(1), the exact decision needs no count scan.
+        // The owner also derives the sibling (build 2) of every built node for its features by
+        // exact subtraction of prefix sums (parent - built; the parent's prefix of an owned
+        // feature is always local) and pushes it too, so no CTA derives after the exchange.
         const int nown_f = (nrep - cl_r + cl_n - 1) / cl_n;
+        const int pring = (level + kResRings - 1) % kResRings;
+        const long long* hpar = s_hsum + static_cast<size_t>(pring) * ls * bins;
+        const int* cpar = s_hcnt + static_cast<size_t>(pring) * ls * bins;
+        const int pfirst = level > 0 ? (1 << (level - 1)) - 1 : 0;
         for (int it = warp; it < nl * nown_f; it += kResWarps) {
           const int k = it / nown_f, j = (it - k * nown_f) * cl_n + cl_r;
-          if (s_nodes[first + k].build != 1) continue;
-          long long* h = hs + static_cast<size_t>(k) * bins + s_repb[j];
-          int* c = hc + static_cast<size_t>(k) * bins + s_repb[j];
+          const int s = first + k;
+          if (s_nodes[s].build != 1) continue;
+          const int sib = level > 0 ? ((s & 1) ? s + 1 : s - 1) : -1;
+          const bool dsib = sib >= 0 && s_nodes[sib].build == 2;
+          const int bo = s_repb[j];
+          long long* h = hs + static_cast<size_t>(k) * bins + bo;
+          int* c = hc + static_cast<size_t>(k) * bins + bo;
+          long long* ho = dsib ? hs + static_cast<size_t>(sib - first) * bins + bo : nullptr;
+          int* co = dsib ? hc + static_cast<size_t>(sib - first) * bins + bo : nullptr;
+          const size_t pb = dsib ? static_cast<size_t>(((s - 1) >> 1) - pfirst) * bins + bo : 0;
           const int nb = s_repn[j];
           long long hcar = 0;
           int ccar = 0;
@@ -663,11 +664,23 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
             if (b < nb) {
               h[b] = hv;
               c[b] = cv;
+              long long ov = 0;
+              int oc = 0;
+              if (dsib) {
+                ov = hpar[pb + b] - hv;
+                oc = cpar[pb + b] - cv;
+                ho[b] = ov;
+                co[b] = oc;
+              }
               if (kClu)
                 for (int r = 1; r < cl_n; ++r) {
                   const int rr = (cl_r + r) % cl_n;
                   dsmem_st(dsmem_addr(h + b, rr), hv);
                   dsmem_st(dsmem_addr(c + b, rr), cv);
+                  if (dsib) {
+                    dsmem_st(dsmem_addr(ho + b, rr), ov);
+                    dsmem_st(dsmem_addr(co + b, rr), oc);
+                  }
                 }
             }
             hcar = __shfl_sync(0xffffffffu, hv, 31);
@@ -679,37 +692,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         else __syncthreads();
       }
       RES_PHASE(2);
-      // ---- siblings by exact subtraction (of prefix sums) ------------------------------------
-      if (level > 0) {
-        const int pring = (level + kResRings - 1) % kResRings;
-        const long long* hp = s_hsum + static_cast<size_t>(pring) * ls * bins;
-        const int* cp = s_hcnt + static_cast<size_t>(pring) * ls * bins;
-        const int pfirst = (1 << (level - 1)) - 1;
-        for (int k2 = 0; k2 < nl / 2; ++k2) {
-          const int parent = pfirst + k2;
-          if (s_nodes[parent].state != kNodeSplit) continue;
-          const int c1 = 2 * parent + 1, c2 = c1 + 1;
-          int built, other;
-          if (s_nodes[c1].build == 1 && s_nodes[c2].build == 2) {
-            built = c1;
-            other = c2;
-          } else if (s_nodes[c2].build == 1 && s_nodes[c1].build == 2) {
-            built = c2;
-            other = c1;
-          } else {
-            continue;
-          }
-          const size_t ob = static_cast<size_t>(other - first) * bins, bb = static_cast<size_t>(built - first) * bins;
-          const size_t pb = static_cast<size_t>(k2) * bins;
-          for (int b = tid; b < bins; b += kResThreads) {
-            hs[ob + b] = hp[pb + b] - hs[bb + b];
-            hc[ob + b] = cp[pb + b] - hc[bb + b];
-          }
-          if (tid == 0) s_nodes[other].absfix = s_nodes[parent].absfix - s_nodes[built].absfix;
-        }
-        __syncthreads();
+      // (siblings were derived by the feature owners, above)
       RES_PHASE(3);
-      }
       // ---- screen: thread per candidate (level node k, bin). Pass 0: the feature's prefix
       // count / sum up to the bin by a short loop over its bins, the screened gain and its bound
       // (cached), the node's max lower bound (segmented warp max, then one 64-bit atomicMax per
@@ -1130,7 +1114,8 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
         }
       }
       __syncthreads();
-      // ---- split records: threshold, tree record, children -------------------------------------
+      // ---- split records: threshold, tree record, children and their plan -----------------------
+      if (level + 1 < depth && tid < 8 * nl) s_absl[tid] = 0;  // the next level's sum |v| counters
       if (tid < nl) {
         const int s = first + tid;
         ResNode& nd = s_nodes[s];
@@ -1161,6 +1146,18 @@ __global__ void __launch_bounds__(kResThreads, 1) fit_resident_kernel(
           a.seg = nd.seg;
           b.n = nd.n - nd.lc;
           b.seg = nd.seg + nd.lc;
+          // the children's plan (level_plan_kernel): a child that cannot split is a leaf; when
+          // either can, the smaller is built directly (1) and the other derived (2)
+          const bool na = nrep > 0 && node_needs_split(fd, level + 1, a.n);
+          const bool nb2 = nrep > 0 && node_needs_split(fd, level + 1, b.n);
+          if (!na) a.state = kNodeLeaf;
+          if (!nb2) b.state = kNodeLeaf;
+          if (na || nb2) {
+            ResNode& small = a.n <= b.n ? a : b;
+            ResNode& big = a.n <= b.n ? b : a;
+            small.build = 1;
+            big.build = 2;
+          }
         }
       }
       __syncthreads();
