@@ -252,6 +252,18 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   ExactItem* items = ar.alloc<ExactItem>(static_cast<size_t>(F) * level_slots_max * (nrep_max + 1));
   int* n_items = ar.alloc<int>(1);
   (void)total_tree;
+  // column-major codes (the presorted lists' layout) for the kernels that read one feature's code
+  // of scattered rows: tie classes, exact folds, partition
+  CodeT* codes_cm = ar.alloc<CodeT>(static_cast<size_t>(std::max<int64_t>(total_ord, 1)));
+  if (total_ord > 0) {
+    const size_t tsm = static_cast<size_t>(128) * (Dp + 1) * sizeof(CodeT);
+    FS_CUDA(cudaFuncSetAttribute(codes_colmajor_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(tsm)));
+    codes_colmajor_kernel<CodeT><<<dim3(static_cast<unsigned>(ceil_div(n_max, 128)), F), 256, tsm, s>>>(
+        fam_d, Dp, codes_c, codes_cm);
+    dev->count_launch();
+    FS_CUDA(cudaGetLastError());
+  }
 
   // histogram launch shape
   const int per_group_min = std::max(1, std::min(min_nrep_hint, kHistThreads));
@@ -371,11 +383,11 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       tieclass_prep_kernel<<<dim3(grid1(lw, 4, 1 << 20), F), 128, 0, s>>>(  // warp per node
           fam_d, st_d, nodes, level, win, std::max(nrep_max, 1), level_slots_max, items, n_items);
       if (resident.phi_smem > 0)
-        tieclass_phi_kernel<CodeT><<<sm * 4, 256, resident.phi_smem, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c,
+        tieclass_phi_kernel<CodeT><<<sm * 4, 256, resident.phi_smem, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_cm,
                                                                  ord_cur, rep_nb_d, win, std::max(nrep_max, 1),
                                                                  level_slots_max);
       else
-        tieclass_check_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, ord,
+        tieclass_check_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_cm, ord,
                                                              nodeid, win, std::max(nrep_max, 1), level_slots_max);
       dev->count_launch(2);
       FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
@@ -385,12 +397,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       if (fork_totals) FS_CUDA(cudaStreamWaitEvent(s, dev->ev_join, 0));  // join: totals ready
       {
         ProfScope prof(dev, "fit_exact");
-        exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord,
+        exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_cm, resid, ord,
                                                    ord_cur, nodeid, rep_boff_d, lbuf, win, std::max(nrep_max, 1),
                                                    level_slots_max, small_scratch ? 1 : 0);
         if (small_scratch)
           exact_small_kernel<CodeT><<<kExactSmallCtas, kSortThreads, 0, s>>>(
-              fam_d, nodes, items, n_items, level, Dp, codes_c, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win,
+              fam_d, nodes, items, n_items, level, Dp, codes_cm, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win,
               std::max(nrep_max, 1), level_slots_max, small_scratch, n_max);
       }
       exact_decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt,
@@ -403,15 +415,15 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         const int64_t p_items = static_cast<int64_t>(F) * lw * part_chunks;
         if (static_cast<int64_t>(F) * lw * 4 < sm) {
           const dim3 pg(static_cast<unsigned>(p_items));
-          partition_count_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
+          partition_count_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_cm, ord_cur,
                                                                    scratch, nodeid, rep_orig_d, rep_boff_d, vals_d,
                                                                    cle, ord, canon, x_d, d, trees_d, slots, part_cnt,
                                                                    part_chunks, level_slots_max, F);
-          partition_scatter_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
+          partition_scatter_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_cm, ord_cur,
                                                                      scratch, nodeid, part_cnt, part_chunks,
                                                                      level_slots_max, F);
         } else {
-          partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_c, ord_cur,
+          partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_cm, ord_cur,
                                                                 scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle,
                                                                 ord, canon, x_d, d, trees_d, slots);
         }

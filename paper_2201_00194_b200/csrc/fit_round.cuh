@@ -755,6 +755,30 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
   }
 }
 
+// Column-major copy of the canonical codes for the multi-kernel round: codes_cm[ord0 + j * n + p]
+// (the presorted lists' layout). Tiles of 128 rows come in as 16-byte row vectors and go out as
+// 128-byte column runs.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) codes_colmajor_kernel(const FamDesc* __restrict__ fam, int Dp,
+                                                             const CodeT* __restrict__ codes_c,
+                                                             CodeT* __restrict__ codes_cm) {
+  extern __shared__ __align__(16) unsigned char tile_raw[];
+  CodeT* tile = reinterpret_cast<CodeT*>(tile_raw);  // [128][Dp + 1]
+  const FamDesc fd = fam[blockIdx.y];
+  const int r0 = blockIdx.x * 128;
+  if (r0 >= fd.n || fd.nrep <= 0) return;
+  const int rows = min(128, fd.n - r0), pitch = Dp + 1;
+  for (int i = threadIdx.x; i < rows * Dp; i += blockDim.x) {
+    const int r = i / Dp, j = i - r * Dp;
+    tile[r * pitch + j] = codes_c[(fd.pos0 + r0 + r) * Dp + j];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < fd.nrep * rows; i += blockDim.x) {
+    const int j = i / rows, r = i - j * rows;
+    codes_cm[fd.ord0 + static_cast<int64_t>(j) * fd.n + r0 + r] = tile[r * pitch + j];
+  }
+}
+
 struct ExactItem {
   int32_t fam;
   int16_t slot;
@@ -900,7 +924,7 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
 template <typename CodeT>
 __global__ void __launch_bounds__(256) tieclass_phi_kernel(
     const FamDesc* __restrict__ fam, const NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
-    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_cm,
     const int32_t* __restrict__ ord_cur, const int32_t* __restrict__ rep_nb, WinRec* __restrict__ win,
     int nrep_max, int level_slots_max) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -914,7 +938,10 @@ __global__ void __launch_bounds__(256) tieclass_phi_kernel(
     const int f0 = nd.eqf0, g = it.rep, nv = nd.n;
     const int nb = rep_nb[fd.rep0 + f0];
     const int32_t* rows = ord_cur + fd.pos0 + nd.seg;
-    const CodeT* cb = codes_c + fd.pos0 * Dp;
+    // column-major codes (codes_cm[ord0 + rep * n + row], built once per fit): a node's rows
+    // gather from one feature's column (L2-resident) instead of one 32-byte sector per row
+    const CodeT* cm_f0 = codes_cm + fd.ord0 + static_cast<int64_t>(f0) * fd.n;
+    const CodeT* cm_g = codes_cm + fd.ord0 + static_cast<int64_t>(g) * fd.n;
     __syncthreads();  // previous item done with phi
     for (int a = tid; a < nb; a += blockDim.x) phi[a] = 0xFFFFu;
     __syncthreads();
@@ -929,8 +956,8 @@ __global__ void __launch_bounds__(256) tieclass_phi_kernel(
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        cf[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + f0]) : 0;
-        cg[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + g]) : 0;
+        cf[k] = p[k] >= 0 ? static_cast<int>(cm_f0[p[k]]) : 0;
+        cg[k] = p[k] >= 0 ? static_cast<int>(cm_g[p[k]]) : 0;
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
@@ -948,8 +975,8 @@ __global__ void __launch_bounds__(256) tieclass_phi_kernel(
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        cf[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + f0]) : 0;
-        cg[k] = p[k] >= 0 ? static_cast<int>(cb[p[k] * Dp + g]) : 0;
+        cf[k] = p[k] >= 0 ? static_cast<int>(cm_f0[p[k]]) : 0;
+        cg[k] = p[k] >= 0 ? static_cast<int>(cm_g[p[k]]) : 0;
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
@@ -978,7 +1005,7 @@ __global__ void __launch_bounds__(256) tieclass_phi_kernel(
 template <typename CodeT>
 __global__ void __launch_bounds__(256) tieclass_check_kernel(
     const FamDesc* __restrict__ fam, const NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
-    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_cm,
     const int32_t* __restrict__ ord, const int16_t* __restrict__ nodeid, WinRec* __restrict__ win, int nrep_max,
     int level_slots_max) {
   const int lane = threadIdx.x & 31;
@@ -998,8 +1025,8 @@ __global__ void __launch_bounds__(256) tieclass_check_kernel(
       const int p = p_next;
       p_next = i + 32 < n ? L[i + 32] : 0;
       const bool mem = i < n && nodeid[fd.pos0 + p] == it.slot;
-      const int a = mem ? static_cast<int>(codes_c[(fd.pos0 + p) * Dp + f0]) : 0;
-      const int b = mem ? static_cast<int>(codes_c[(fd.pos0 + p) * Dp + g]) : 0;
+      const int a = mem ? static_cast<int>(codes_cm[fd.ord0 + static_cast<int64_t>(f0) * n + p]) : 0;
+      const int b = mem ? static_cast<int>(codes_cm[fd.ord0 + static_cast<int64_t>(g) * n + p]) : 0;
       const unsigned m = __ballot_sync(0xffffffffu, mem);
       seen += __popc(m);
       const unsigned lt = m & ((1u << lane) - 1u);
@@ -1279,7 +1306,7 @@ constexpr int kExactSpecMin = 4096;  // chains from this length fold speculative
 template <typename CodeT>
 __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
-    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_c,
+    const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_cm,
     const double* __restrict__ resid, const int32_t* __restrict__ ord, const int32_t* __restrict__ ord_cur,
     const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_boff,
     double* __restrict__ lbuf, const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
@@ -1354,11 +1381,11 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
       __syncthreads();
     }
     // 2. stable sort by the feature's code: (code, canonical position) = presorted order
-    const CodeT* cj = codes_c + static_cast<int64_t>(fd.pos0) * Dp + jj;
+    const CodeT* cj = codes_cm + fd.ord0 + static_cast<int64_t>(jj) * fd.n;  // column-major
     int32_t* src = A;
     int32_t* dst = B;
     if (stable_digit_pass([&](int i) { return src[i]; }, dst, nv,
-                          [&](int p) { return static_cast<int>(cj[static_cast<int64_t>(p) * Dp] & 255u); }, sm)) {
+                          [&](int p) { return static_cast<int>(cj[p] & 255u); }, sm)) {
       int32_t* t = src;
       src = dst;
       dst = t;
@@ -1366,7 +1393,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     __syncthreads();
     if (sizeof(CodeT) == 2) {
       if (stable_digit_pass([&](int i) { return src[i]; }, dst, nv,
-                            [&](int p) { return static_cast<int>(cj[static_cast<int64_t>(p) * Dp] >> 8); }, sm)) {
+                            [&](int p) { return static_cast<int>(cj[p] >> 8); }, sm)) {
         int32_t* t = src;
         src = dst;
         dst = t;
@@ -1383,7 +1410,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
       for (int i0 = 0; i0 < need; i0 += 32) {
         const int i = i0 + lane;
         const int p = i < need ? src[i] : 0;
-        const int code = i < need ? static_cast<int>(cj[static_cast<int64_t>(p) * Dp]) : 0;
+        const int code = i < need ? static_cast<int>(cj[p]) : 0;
         const double rv = i < need ? resid[fd.pos0 + p] : 0.0;
         const int cnt = min(32, need - i0);
         for (int l0 = 0; l0 < cnt; l0 += 8) {
@@ -1413,7 +1440,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
 template <typename CodeT>
 __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes,
                                                     const ExactItem* __restrict__ items, const int* __restrict__ n_items,
-                                                    int level, int Dp, const CodeT* __restrict__ codes_c,
+                                                    int level, int Dp, const CodeT* __restrict__ codes_cm,
                                                     const double* __restrict__ resid, const int32_t* __restrict__ ord,
                                                     const int32_t* __restrict__ ord_cur,
                                                     const int16_t* __restrict__ nodeid,
@@ -1460,7 +1487,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
       for (int c = 0; c < 4; ++c) mem[c] = p[c] >= 0 && nodeid[fd.pos0 + p[c]] == it.slot;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        code[c] = mem[c] ? static_cast<int>(codes_c[(fd.pos0 + p[c]) * Dp + jj]) : 0;
+        code[c] = mem[c] ? static_cast<int>(codes_cm[fd.ord0 + static_cast<int64_t>(jj) * fd.n + p[c]]) : 0;
         rv[c] = mem[c] ? resid[fd.pos0 + p[c]] : 0.0;
       }
 #pragma unroll
@@ -1568,7 +1595,7 @@ __global__ void exact_decide_kernel(const FamDesc* __restrict__ fam, const FamSt
 template <typename CodeT>
 __global__ void __launch_bounds__(1024) partition_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level, int Dp,
-    const CodeT* __restrict__ codes_c, int32_t* __restrict__ ord_cur, int32_t* __restrict__ scratch,
+    const CodeT* __restrict__ codes_cm, int32_t* __restrict__ ord_cur, int32_t* __restrict__ scratch,
     int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_boff,
     const double* __restrict__ vals, const int32_t* __restrict__ cle, const int32_t* __restrict__ ord,
     const int32_t* __restrict__ canon, const double* __restrict__ x, int d, TreeRec* __restrict__ trees, int slots) {
@@ -1622,14 +1649,14 @@ __global__ void __launch_bounds__(1024) partition_kernel(
   const int16_t cl = static_cast<int16_t>(2 * s + 1), cr = static_cast<int16_t>(2 * s + 2);
   // the next chunk's index and code gathers are issued before this chunk's scan and scatter
   int p_nx = tid < n ? src[tid] : 0;
-  int c_nx = tid < n ? static_cast<int>(codes_c[(fd.pos0 + p_nx) * Dp + jj]) : 0;
+  int c_nx = tid < n ? static_cast<int>(codes_cm[fd.ord0 + static_cast<int64_t>(jj) * fd.n + p_nx]) : 0;
   for (int t0 = 0; t0 < n; t0 += blockDim.x) {
     const int i = t0 + tid;
     const int p = p_nx;
     const bool left = i < n && c_nx <= bin;
     if (i + static_cast<int>(blockDim.x) < n) {
       p_nx = src[i + blockDim.x];
-      c_nx = static_cast<int>(codes_c[(fd.pos0 + p_nx) * Dp + jj]);
+      c_nx = static_cast<int>(codes_cm[fd.ord0 + static_cast<int64_t>(jj) * fd.n + p_nx]);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, left);
     if (lane == 0) wsum[warp] = __popc(bal);
@@ -1675,7 +1702,7 @@ constexpr int kPartChunk = 1024;
 template <typename CodeT>
 __global__ void __launch_bounds__(kPartChunk) partition_count_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level,
-    int Dp, const CodeT* __restrict__ codes_c, const int32_t* __restrict__ ord_cur, int32_t* __restrict__ scratch,
+    int Dp, const CodeT* __restrict__ codes_cm, const int32_t* __restrict__ ord_cur, int32_t* __restrict__ scratch,
     const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_boff,
     const double* __restrict__ vals, const int32_t* __restrict__ cle, const int32_t* __restrict__ ord,
     const int32_t* __restrict__ canon, const double* __restrict__ x, int d, TreeRec* __restrict__ trees, int slots,
@@ -1731,7 +1758,7 @@ __global__ void __launch_bounds__(kPartChunk) partition_count_kernel(
   if (i < nd.n) {
     const int p = ord_cur[fd.pos0 + nd.seg + i];
     scratch[fd.pos0 + nd.seg + i] = p;
-    left = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + nd.rep]) <= nd.bin;
+    left = static_cast<int>(codes_cm[fd.ord0 + static_cast<int64_t>(nd.rep) * fd.n + p]) <= nd.bin;
   }
   const unsigned bal = __ballot_sync(0xffffffffu, left);
   if (lane == 0) wsum[warp] = __popc(bal);
@@ -1748,7 +1775,7 @@ __global__ void __launch_bounds__(kPartChunk) partition_count_kernel(
 template <typename CodeT>
 __global__ void __launch_bounds__(kPartChunk) partition_scatter_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level, int Dp,
-    const CodeT* __restrict__ codes_c, int32_t* __restrict__ ord_cur, const int32_t* __restrict__ scratch,
+    const CodeT* __restrict__ codes_cm, int32_t* __restrict__ ord_cur, const int32_t* __restrict__ scratch,
     int16_t* __restrict__ nodeid, const int32_t* __restrict__ part_cnt, int chunks_max, int level_slots_max, int F) {
   __shared__ int wsum[32];
   __shared__ int s_off;
@@ -1779,7 +1806,7 @@ __global__ void __launch_bounds__(kPartChunk) partition_scatter_kernel(
   bool left = false;
   if (i < n) {
     p = scratch[fd.pos0 + seg + i];
-    left = static_cast<int>(codes_c[(fd.pos0 + p) * Dp + jj]) <= bin;
+    left = static_cast<int>(codes_cm[fd.ord0 + static_cast<int64_t>(jj) * fd.n + p]) <= bin;
   }
   const unsigned bal = __ballot_sync(0xffffffffu, left);
   if (lane == 0) wsum[warp] = __popc(bal);
