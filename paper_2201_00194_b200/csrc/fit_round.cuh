@@ -1290,6 +1290,157 @@ __device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, co
 // 32 gathers are in flight at once, then each chunk's values are added in lane order (shuffles
 // hoisted ahead of the dependent add chain). Every lane returns the sum.
 
+// cta_fold_spec with the chains' elements staged through shared memory: the K segments advance
+// in lockstep, kStageCh elements at a time gathered cooperatively (every thread one element per
+// pass) into stage[K][kStageCh], and every thread folds its segment's run from shared memory
+// with 16-byte broadcast loads - half a shared load per element instead of two shuffles per
+// element and warp (the speculating warps all read the same run: the shuffle broadcast made the
+// leaf kernels MIO-bound with many CTAs per SM). A missed segment is re-folded alone from the
+// true prefix (by warp 0) and the next segment is still checked against the new value.
+constexpr int kStageCh = 1024;
+__device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                       int n, double* red /* smem [kSpecRed] */,
+                                                       double* stage /* smem [4][kStageCh], >= blockDim doubles */) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = static_cast<int>(blockDim.x >> 5);
+  if (n < 4096 || nw < 2) return cta_fold_spec(v, idx, n, red);
+  const int G = (n >= kSpecMulti && nw >= 4) ? 3 : 1;
+  const int K = G + 1;
+  auto bnd = [&](int g) { return static_cast<int>((static_cast<long long>(g) * n) / K); };
+  // 1. double-double estimates of the exact prefix sums at the segment starts
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    if (g >= G) break;
+    double hi = 0.0, lo = 0.0;
+    const int a = bnd(g), e = bnd(g + 1);
+    for (int i0 = a + tid; i0 < e; i0 += 8 * blockDim.x) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * blockDim.x;
+        x[k] = i < e ? v[idx[i]] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        double s, err;
+        two_sum(hi, x[k], s, err);
+        hi = s;
+        lo = fs_add(lo, err);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+      double s, err;
+      two_sum(hi, oh, s, err);
+      hi = s;
+      lo = fs_add(fs_add(lo, ol), err);
+    }
+    if (lane == 0) {
+      red[64 * g + warp] = hi;
+      red[64 * g + 32 + warp] = lo;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double h = 0.0, l = 0.0;
+    for (int g = 0; g < G; ++g) {
+      for (int w = 0; w < nw; ++w) {
+        double s, err;
+        two_sum(h, red[64 * g + w], s, err);
+        h = s;
+        l = fs_add(fs_add(l, red[64 * g + 32 + w]), err);
+      }
+      red[192 + g] = fs_add(h, l);
+    }
+  }
+  __syncthreads();
+  // 2. warp 0 folds segment 0 from 0.0; the other warps split into G groups, group g folding
+  // segment g from P_g + (c - C/2) ulp
+  const int grp = warp == 0 ? 0 : 1 + ((warp - 1) * G) / (nw - 1);
+  int wfirst = 1;
+  while (wfirst < nw && 1 + ((wfirst - 1) * G) / (nw - 1) < grp) ++wfirst;
+  int wlast = wfirst;
+  while (wlast + 1 < nw && 1 + (wlast * G) / (nw - 1) == grp) ++wlast;
+  const int C = 32 * (wlast - wfirst + 1);
+  const double start = grp == 0 ? 0.0 : ord_dbl(dbl_ord(red[192 + grp - 1]) + (tid - 32 * wfirst - C / 2));
+  const int seg_len = bnd(grp + 1) - bnd(grp);
+  int lmax = 0;
+  for (int g = 0; g < K; ++g) lmax = max(lmax, bnd(g + 1) - bnd(g));
+  double s = start;
+  for (int c0 = 0; c0 < lmax; c0 += kStageCh) {
+    for (int t0 = tid; t0 < K * kStageCh; t0 += 8 * blockDim.x) {  // 8 gathers in flight per thread
+      int ix[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * blockDim.x;
+        const int q = t / kStageCh, o = t - q * kStageCh;
+        ix[u] = t < K * kStageCh && c0 + o < bnd(q + 1) - bnd(q) ? idx[bnd(q) + c0 + o] : -1;
+      }
+      double xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = ix[u] >= 0 ? v[ix[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (ix[u] >= 0) stage[t0 + u * blockDim.x] = xv[u];
+    }
+    __syncthreads();
+    const int m = min(kStageCh, seg_len - c0);
+    if (m > 0) {  // this thread's run: two elements per 16-byte (broadcast) load, 8 in flight
+      const double2* x2 = reinterpret_cast<const double2*>(stage + grp * kStageCh);
+      const int m2 = m >> 1;
+      int k = 0;
+      for (; k + 4 <= m2; k += 4) {
+        double2 a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = x2[k + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          s = fs_add(s, a[u].x);
+          s = fs_add(s, a[u].y);
+        }
+      }
+      for (; k < m2; ++k) {
+        const double2 a = x2[k];
+        s = fs_add(s, a.x);
+        s = fs_add(s, a.y);
+      }
+      if (m & 1) s = fs_add(s, stage[grp * kStageCh + m - 1]);
+    }
+    __syncthreads();
+  }
+  // 3. resolve segment by segment (every chain result parked in the stage buffer)
+  stage[tid] = s;
+  if (tid == 0) red[196] = s;  // S_1: the true prefix at bnd(1)
+  __shared__ int hit;
+  __syncthreads();
+  for (int g = 1; g <= G; ++g) {
+    if (tid == 0) {
+      int w0 = 1;  // first warp of group g
+      while (w0 < nw && 1 + ((w0 - 1) * G) / (nw - 1) < g) ++w0;
+      int w1 = w0;
+      while (w1 + 1 < nw && 1 + (w1 * G) / (nw - 1) == g) ++w1;
+      const int Cg = 32 * (w1 - w0 + 1);
+      const double S = red[196];
+      const long long k = dbl_ord(S) - dbl_ord(red[192 + g - 1]) + Cg / 2;
+      hit = k >= 0 && k < Cg && __double_as_longlong(ord_dbl(dbl_ord(S))) == __double_as_longlong(S);
+      if (hit) red[197] = stage[32 * w0 + k];
+    }
+    __syncthreads();
+    if (!hit) {  // re-fold segment g alone from the true prefix
+      if (warp == 0) {
+        const double t = warp_fold_gather_from(v, idx + bnd(g), bnd(g + 1) - bnd(g), red[196]);
+        if (lane == 0) red[197] = t;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) red[196] = red[197];
+    __syncthreads();
+  }
+  const double out = red[196];
+  __syncthreads();
+  return out;
+}
+
 // One warp per item: reference-order folds. Item rep < 0: node total over the order-0 list
 // (sum_residuals(order[0]), costmodel.cpp:47). Item rep j: best_split's left sums over feature j's
 // presorted list restricted to the node (:50-55), recorded at every value boundary.
@@ -1846,6 +1997,7 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
                                                        const double* __restrict__ resid, double* __restrict__ pred,
                                                        TreeRec* __restrict__ trees) {
   __shared__ double red[kSpecRed];
+  __shared__ __align__(16) double stage[4 * kStageCh];
   const int f = blockIdx.y, s = blockIdx.x;
   if (f >= F) return;
   const FamDesc fd = fam[f];
@@ -1855,7 +2007,7 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
   if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
   const int n = nd.n;
   const int32_t* L = ord_cur + fd.pos0 + nd.seg;
-  const double sum = nd.pad_ ? nd.total : cta_fold_spec(resid + fd.pos0, L, n, red);
+  const double sum = nd.pad_ ? nd.total : cta_fold_spec_staged(resid + fd.pos0, L, n, red, stage);
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
   // prediction update, 8 rows per thread in flight (index and prediction gathers issued before
