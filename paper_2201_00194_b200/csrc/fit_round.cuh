@@ -1297,10 +1297,12 @@ __device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, co
 // element and warp (the speculating warps all read the same run: the shuffle broadcast made the
 // leaf kernels MIO-bound with many CTAs per SM). A missed segment is re-folded alone from the
 // true prefix (by warp 0) and the next segment is still checked against the new value.
-constexpr int kStageCh = 1024;
+constexpr int kStageCh = 1024;      // leaf CTAs (256 threads)
+constexpr int kStageChSmall = 256;  // exact_small CTAs (1,024 threads: the stage doubles as their result slots)
 __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict__ v, const int32_t* __restrict__ idx,
                                                        int n, double* red /* smem [kSpecRed] */,
-                                                       double* stage /* smem [4][kStageCh], >= blockDim doubles */) {
+                                                       double* stage /* smem [4][ch], >= blockDim doubles */,
+                                                       int ch) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = static_cast<int>(blockDim.x >> 5);
   if (n < 4096 || nw < 2) return cta_fold_spec(v, idx, n, red);
@@ -1367,14 +1369,14 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
   int lmax = 0;
   for (int g = 0; g < K; ++g) lmax = max(lmax, bnd(g + 1) - bnd(g));
   double s = start;
-  for (int c0 = 0; c0 < lmax; c0 += kStageCh) {
-    for (int t0 = tid; t0 < K * kStageCh; t0 += 8 * blockDim.x) {  // 8 gathers in flight per thread
+  for (int c0 = 0; c0 < lmax; c0 += ch) {
+    for (int t0 = tid; t0 < K * ch; t0 += 8 * blockDim.x) {  // 8 gathers in flight per thread
       int ix[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int t = t0 + u * blockDim.x;
-        const int q = t / kStageCh, o = t - q * kStageCh;
-        ix[u] = t < K * kStageCh && c0 + o < bnd(q + 1) - bnd(q) ? idx[bnd(q) + c0 + o] : -1;
+        const int q = t / ch, o = t - q * ch;
+        ix[u] = t < K * ch && c0 + o < bnd(q + 1) - bnd(q) ? idx[bnd(q) + c0 + o] : -1;
       }
       double xv[8];
 #pragma unroll
@@ -1384,9 +1386,9 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
         if (ix[u] >= 0) stage[t0 + u * blockDim.x] = xv[u];
     }
     __syncthreads();
-    const int m = min(kStageCh, seg_len - c0);
+    const int m = min(ch, seg_len - c0);
     if (m > 0) {  // this thread's run: two elements per 16-byte (broadcast) load, 8 in flight
-      const double2* x2 = reinterpret_cast<const double2*>(stage + grp * kStageCh);
+      const double2* x2 = reinterpret_cast<const double2*>(stage + grp * ch);
       const int m2 = m >> 1;
       int k = 0;
       for (; k + 4 <= m2; k += 4) {
@@ -1404,7 +1406,7 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
         s = fs_add(s, a.x);
         s = fs_add(s, a.y);
       }
-      if (m & 1) s = fs_add(s, stage[grp * kStageCh + m - 1]);
+      if (m & 1) s = fs_add(s, stage[grp * ch + m - 1]);
     }
     __syncthreads();
   }
@@ -1465,6 +1467,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
   __shared__ SortSmem sm;
   __shared__ int wsum[32];
   __shared__ double red[kSpecRed];
+  __shared__ __align__(16) double stage[4 * kStageChSmall];  // 8 KB (static shared memory is 48 KB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = *n_items;
   sort_smem_init(sm);
@@ -1475,7 +1478,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const int nv = nd.n, n = fd.n;
     if (it.rep < 0) {  // a long node total: speculative CTA fold (exact_kernel folds the short ones)
       if (nv < kExactSpecMin) continue;
-      const double t = cta_fold_spec(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, nv, red);
+      const double t = cta_fold_spec_staged(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, nv, red, stage, kStageChSmall);
       if (tid == 0) nd.total = t;
       continue;
     }
@@ -1490,7 +1493,8 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     if (!exact_is_small(nv, n)) {
       if (!spec_one) continue;  // exact_kernel scans the presorted list
       // the root: every row is a member, the presorted list is the member list
-      const double L = cta_fold_spec(resid + fd.pos0, ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n, need, red);
+      const double L = cta_fold_spec_staged(resid + fd.pos0, ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n, need, red,
+                                            stage, kStageChSmall);
       if (tid == 0) out[wr.best_bin] = L;
       continue;
     }
@@ -1553,7 +1557,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     }
     // 3. the fold (warp 0; members in list order, boundaries at code changes)
     if (spec_one) {
-      const double L = cta_fold_spec(resid + fd.pos0, src, need, red);
+      const double L = cta_fold_spec_staged(resid + fd.pos0, src, need, red, stage, kStageChSmall);
       if (tid == 0) out[wr.best_bin] = L;
     } else if (warp == 0) {
       double left = 0.0;
@@ -2007,7 +2011,7 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
   if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
   const int n = nd.n;
   const int32_t* L = ord_cur + fd.pos0 + nd.seg;
-  const double sum = nd.pad_ ? nd.total : cta_fold_spec_staged(resid + fd.pos0, L, n, red, stage);
+  const double sum = nd.pad_ ? nd.total : cta_fold_spec_staged(resid + fd.pos0, L, n, red, stage, kStageCh);
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
   // prediction update, 8 rows per thread in flight (index and prediction gathers issued before
