@@ -362,6 +362,10 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
   const int local = s - ((1 << level) - 1);
   const int64_t hbase = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + local) * fd.bins;
   const int nrep = fd.nrep, bins = fd.bins;
+  // the i-th row of the node: at the root every row belongs, and integer sums do not depend on
+  // the order, so the root streams rows in canonical order (coalesced tiles) instead of
+  // gathering them through the order-0 list
+  auto row_at = [&](int i) -> int64_t { return level == 0 ? i : ord_cur[fd.pos0 + i]; };
   // layout: limbs[3][colh_max][32] u32 (lane columns, see col_height) | acc_sum[bins] i64 |
   // acc_cnt[bins] i32 | binrep[bins] u16 | boff[nrep] | cofs[nrep] | tile codes | tile limbs
   uint32_t* limb = reinterpret_cast<uint32_t*>(smem);
@@ -463,11 +467,11 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
       const int i = tid + q * kAtomThreads;                                         \
       if (i < tr_ * vec_per_row) {                                                  \
         const int r = i / vec_per_row, v = i - r * vec_per_row;                     \
-        const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + (T0) + r];         \
+        const int64_t p = fd.pos0 + row_at(seg + r0 + (T0) + r);                      \
         pv[q] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];               \
       }                                                                             \
     }                                                                               \
-    if (tid < tr_) pfix = rfix[fd.pos0 + ord_cur[fd.pos0 + seg + r0 + (T0) + tid]]; \
+    if (tid < tr_) pfix = rfix[fd.pos0 + row_at(seg + r0 + (T0) + tid)];           \
   } while (0)
       // the registers' tile into buffer b (codes, limbs, |v| into s_abs)
 #define FS_ATOM_STAGE(T0, B)                                                                        \
@@ -518,12 +522,12 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
         const int tr = min(kAtomTile, sub_end - t0);
         for (int i = tid; i < tr * vec_per_row; i += kAtomThreads) {
           const int r = i / vec_per_row, v = i - r * vec_per_row;
-          const int64_t p = fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + r];
+          const int64_t p = fd.pos0 + row_at(seg + r0 + t0 + r);
           reinterpret_cast<uint4*>(t_codes + r * Dp)[v] = reinterpret_cast<const uint4*>(codes_c + p * Dp)[v];
         }
         unsigned long long a = 0;
         if (tid < tr) {
-          const int64_t v = rfix[fd.pos0 + ord_cur[fd.pos0 + seg + r0 + t0 + tid]];
+          const int64_t v = rfix[fd.pos0 + row_at(seg + r0 + t0 + tid)];
           const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
           t_limb[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;
           t_limb[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;
