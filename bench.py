@@ -169,12 +169,13 @@ def s8d_fit_bytes(rows, trees, depth=3, d=PAD, s_bin=1):
 def shard_workload(W, rank, world):
     """This rank's families of a global workload (deterministic LPT on rows*T + pool*T,
     paper_2201_00194_b200/sharding.py); records the global unit counts for whole-job rates."""
-    from paper_2201_00194_b200 import sharding
+    import paper_2201_00194_b200 as fs
 
     F = len(W["families"])
     ps, ts = W["pool_seg"], W["tr_seg"]
-    costs = [sharding.family_cost(int(ts[f + 1] - ts[f]), int(ps[f + 1] - ps[f]), W["trees"]) for f in range(F)]
-    owner = sharding.assign_families(costs, world)
+    # the product's partition (fs_shard_families, include/famseer.h); sharding.assign_families is
+    # its host-side restatement (tests/test_multigpu_gloo.py checks they agree)
+    owner = fs.shard_families(np.diff(ts), np.diff(ps), np.full(F, W["trees"], np.int32), world)
     mine = [f for f in range(F) if owner[f] == rank]
     out = dict(W)
     for key_so, key_a, key_seg in (("pool_so", "pool_a", "pool_seg"), ("tr_so", "tr_a", "tr_seg")):
@@ -325,8 +326,22 @@ def run_native(args, rank, world, local_rank):
     fam_base = rank * F if args.shard != "families" else 0
     fam_ids = W.get("family_ids", list(range(F)))
 
+    comm = None
+    if dist is not None and not share:
+        # the product's exchange (fs_comm over NCCL): rank 0 makes the id, torch.distributed
+        # carries its bytes to the other ranks
+        cid = [fs.Comm.new_id() if rank == 0 else None]
+        dist.broadcast_object_list(cid, src=0)
+        comm = fs.Comm(dev, world, rank, cid[0])
+        n_fam_all = len(W_global["families"]) * (world if args.shard != "families" else 1)
+        merged = torch.empty((n_fam_all, G_TOP, 3), dtype=torch.float64, device="cuda")
+
     def topk_allgather():
-        # per-family top-g records {family, pool index, score}; the only collective (NCCL)
+        # per-family top-g records {family, pool index, score}; the only collective
+        if comm is not None:  # fs_topk_allgather: pack -> ncclAllGather -> merge, on the device
+            comm.topk_allgather([fam_base + f for f in fam_ids], pool_seg, scores, perm, G_TOP,
+                                W.get("fam_cap", F), n_fam_all, merged)
+            return merged
         idx = []
         for f in range(F):
             a, b = int(pool_seg[f]), int(pool_seg[f + 1])

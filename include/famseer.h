@@ -176,6 +176,30 @@ int fs_score_index_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, i
                      const int64_t* seg_h, const int32_t* space_of_d, const uint64_t* index_d,
                      int32_t pad_dim, double* scores_d, int32_t* perm_d);
 
+/* ---- multi-GPU: family-parallel tuning on the GPUs of one node ---------------
+ * Families share nothing (scheduler.cpp:123-130), so each rank (one process per GPU) owns a
+ * deterministic set of families and calls fs_score / fs_fit / fs_tune_step on its own device;
+ * per-family results are bit-identical on any rank. fs_shard_families: LPT partition on
+ * rows*T + pool*T (ties: lower family id first, then the least-loaded lower rank), host only.
+ * fs_comm: an NCCL communicator (libnccl.so.2 loaded at run time; FS_ENCCL when it is missing or
+ * a call fails): rank 0 makes the id with fs_comm_id and the caller broadcasts the
+ * FS_COMM_ID_BYTES bytes to every rank (any side channel). fs_topk_allgather: the per-round
+ * exchange - every local family's first g ranked candidates (tune_step's by-score picks,
+ * scheduler.cpp:196-201) as records {family id, pool index, score} (float64), all-gathered over
+ * NVLink and merged on the device into merged_d[n_families][g][3] in family-id order (missing
+ * entries -1). fam_cap: the largest local family count of any rank (the same on every rank).
+ * Stream-ordered on the device's stream. */
+#define FS_COMM_ID_BYTES 128
+typedef struct fs_comm fs_comm;
+int fs_shard_families(int32_t n_families, const int64_t* rows, const int64_t* pool, const int32_t* trees,
+                      int32_t world, int32_t* owner);
+int fs_comm_id(uint8_t* id /* FS_COMM_ID_BYTES */);
+int fs_comm_create(fs_device* dev, int32_t world, int32_t rank, const uint8_t* id, fs_comm** out);
+int fs_comm_destroy(fs_comm* comm);
+int fs_topk_allgather(fs_comm* comm, int32_t n_local, const int32_t* family_ids, const int64_t* seg_h,
+                      const double* scores_d, const int32_t* perm_d, int32_t g, int32_t fam_cap,
+                      int32_t n_families, double* merged_d);
+
 /* ---- pairwise accuracy (costmodel.cpp:248-277) over precomputed scores ---------------------
  * Pairs with relative latency difference < 1e-6 are excluded, predicted ties score 1/2.
  * FS_EINVAL for m < 2, FS_EDOMAIN when every pair is excluded. */

@@ -23,7 +23,7 @@ import numpy as np
 from . import _capi
 from ._capi import FS_MAX_KNOBS, GbtParams
 
-__all__ = ["Device", "Spaces", "Forest", "Store", "Ensemble", "GbtParams", "FamseerError", "InvalidArgument",
+__all__ = ["Device", "Spaces", "Forest", "Store", "Comm", "shard_families", "Ensemble", "GbtParams", "FamseerError", "InvalidArgument",
            "DomainError", "OutOfRange", "feature_dim", "FS_MAX_KNOBS"]
 
 
@@ -520,3 +520,55 @@ def _params_array(params, n):
         params = [params] * n
     arr = (GbtParams * n)(*params)
     return arr
+
+
+# ---- multi-GPU: family-parallel tuning -------------------------------------------
+def shard_families(rows, pool, trees, world: int) -> list[int]:
+    """fs_shard_families: deterministic LPT owner rank per family (cost rows*T + pool*T)."""
+    r = np.ascontiguousarray(rows, np.int64)
+    p = np.ascontiguousarray(pool, np.int64)
+    t = np.ascontiguousarray(trees, np.int32)
+    owner = np.zeros(len(r), np.int32)
+    _check(_lib().fs_shard_families(len(r), _p(r, _capi._i64p), _p(p, _capi._i64p), _p(t, _capi._i32p), world,
+                                    _p(owner, _capi._i32p)))
+    return owner.tolist()
+
+
+class Comm:
+    """fs_comm: the NCCL communicator of one rank (one process per GPU). Rank 0 makes the id
+    (Comm.new_id()); the caller broadcasts the bytes to the other ranks."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def new_id() -> bytes:
+        buf = (C.c_uint8 * Comm.ID_BYTES)()
+        _check(_lib().fs_comm_id(buf))
+        return bytes(buf)
+
+    def __init__(self, dev: Device, world: int, rank: int, comm_id: bytes):
+        self.dev = dev
+        buf = (C.c_uint8 * Comm.ID_BYTES).from_buffer_copy(comm_id)
+        h = C.c_void_p()
+        _check(_lib().fs_comm_create(dev.h, world, rank, buf, C.byref(h)))
+        self.h = h.value
+
+    def topk_allgather(self, family_ids, seg, scores_t, perm_t, g: int, fam_cap: int, n_families: int, merged_t):
+        """Every local family's first g ranked candidates, all-gathered and merged on the device
+        into merged_t [n_families][g][3] (family id, pool index, score; -1 where absent)."""
+        ids = np.ascontiguousarray(family_ids, np.int32)
+        sg = np.ascontiguousarray(seg, np.int64)
+        _check(_lib().fs_topk_allgather(self.h, len(ids), _p(ids, _capi._i32p), _p(sg, _capi._i64p),
+                                        scores_t.data_ptr(), perm_t.data_ptr(), g, fam_cap, n_families,
+                                        merged_t.data_ptr()))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().fs_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -64,6 +64,11 @@ SIGNATURES = [
                                   _vp, _vp, _vp]),
     ("fs_tune_step", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _i32p, C.c_int32, _dp, _i32p, C.c_int32,
                                 _i64p, _i32p, _i32p, _dp, _vp]),
+    ("fs_shard_families", C.c_int, [C.c_int32, _i64p, _i64p, _i32p, C.c_int32, _i32p]),
+    ("fs_comm_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("fs_comm_create", C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
+    ("fs_comm_destroy", C.c_int, [_vp]),
+    ("fs_topk_allgather", C.c_int, [_vp, C.c_int32, _i32p, _i64p, _vp, _vp, C.c_int32, C.c_int32, C.c_int32, _vp]),
     ("fs_score_index", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _i32p, _u64p, C.c_int32, _dp, _i32p]),
     ("fs_score_index_d", C.c_int, [_vp, _vp, _vp, C.c_int32, _i64p, _vp, _vp, C.c_int32, _vp, _vp]),
     ("fs_feature_dim", C.c_int, [C.c_int32]),

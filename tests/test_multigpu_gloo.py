@@ -108,3 +108,22 @@ def test_bench_family_sharding_covers_global_workload():
                 assert np.array_equal(S["tr_y"][sa:sb], W["tr_y"][a:b])
         assert sorted(seen) == list(range(len(W["families"])))
         assert rows == int(W["tr_seg"][-1]) and pool == int(W["pool_seg"][-1])
+
+
+def test_capi_shard_families_matches_host_logic():
+    """fs_shard_families (the product's C ABI, include/famseer.h) computes the same deterministic
+    LPT partition as the host sharding module, ties included."""
+    import paper_2201_00194_b200 as fs
+
+    rng = np.random.default_rng(3)
+    for trial in range(50):
+        F = int(rng.integers(1, 70))
+        rows = rng.integers(1, 5000, F)
+        pool = rng.integers(1, 3000, F)
+        if trial % 5 == 0:  # equal costs: the tie-breaks decide
+            rows[:] = 100
+            pool[:] = 50
+        trees = np.full(F, int(rng.integers(1, 1000)), np.int32)
+        for world in (1, 2, 3, 4, 8):
+            costs = [sharding.family_cost(int(r), int(p), int(trees[0])) for r, p in zip(rows, pool)]
+            assert fs.shard_families(rows, pool, trees, world) == sharding.assign_families(costs, world)
