@@ -111,6 +111,26 @@ inline unsigned grid1(int64_t n, int block, int cap) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, block), cap)));
 }
 
+// A boosting round's kernels go out with programmatic stream serialization (PDL): the next kernel
+// is scheduled while its predecessor drains and waits in FS_PDL_WAIT() for its completion, which
+// hides the launch gap between the round's ~40 small dependent kernels (inside the CUDA graph the
+// dependencies become programmatic edges). FAMSEER_NO_PDL=1 launches them plainly.
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  static const bool off = std::getenv("FAMSEER_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  FS_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 struct ResidentPlan {
   bool enabled = false;
   std::vector<int> families;
@@ -250,7 +270,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   double* lbuf = ar.alloc<double>(total_lbuf);
   WinRec* win = ar.alloc<WinRec>(static_cast<size_t>(F) * level_slots_max * std::max(nrep_max, 1));
   ExactItem* items = ar.alloc<ExactItem>(static_cast<size_t>(F) * level_slots_max * (nrep_max + 1));
-  int* n_items = ar.alloc<int>(1);
+  int* n_items = ar.alloc<int>(2);  // [0] tie-class items, [1] exact items (zeroed by hist_zero_kernel)
   (void)total_tree;
   // column-major codes (the presorted lists' layout) for the kernels that read one feature's code
   // of scattered rows: tie classes, exact folds, partition
@@ -319,15 +339,14 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                                : ar.alloc<int32_t>(static_cast<size_t>(kExactSmallCtas) * 2 * std::max(n_max, 1));
   cudaStream_t aux = fork_totals ? dev->aux_stream() : nullptr;
   auto round_body = [&]() {
-    round_init_kernel<<<F, 256, 0, s>>>(fam_d, st_d, nodes, slots, trees_d);
-    FS_CUDA(cudaMemsetAsync(node_abs, 0, static_cast<size_t>(F) * slots * sizeof(int64_t), s));
-    residual_kernel<<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, F, n_tot, st_d, rowfam, target_c, pred, resid,
-                                                                 ord_root, ord_cur, nodeid);
-    fixed_kernel<<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, n_tot, st_d, rowfam, resid, rfix);
+    launch_pdl(round_init_kernel, dim3(F), dim3(256), 0, s, fam_d, st_d, nodes, slots, trees_d, node_abs);
+    launch_pdl(residual_kernel, dim3(grid1(n_tot, 256, sm * 16)), dim3(256), 0, s, fam_d, F, n_tot, st_d, rowfam,
+               target_c, pred, resid, ord_root, ord_cur, nodeid);
+    launch_pdl(fixed_kernel, dim3(grid1(n_tot, 256, sm * 16)), dim3(256), 0, s, fam_d, n_tot, st_d, rowfam, resid, rfix);
     dev->count_launch(3);
     for (int level = 0; level <= depth_max; ++level) {
       const unsigned lw = 1u << level;
-      level_plan_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level);
+      launch_pdl(level_plan_kernel, dim3(grid1(lw, 128, 1 << 20), F), dim3(128), 0, s, fam_d, st_d, nodes, level);
       dev->count_launch();
       if (level == depth_max || nrep_max == 0) continue;
       // Optional fork (FAMSEER_FORK_TOTALS=1): every screened node's total on a side stream while
@@ -341,21 +360,21 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         FS_CUDA(cudaEventRecord(dev->ev_join, aux));
         dev->count_launch();
       }
-      hist_zero_kernel<<<dim3(grid1(static_cast<int64_t>(lw) * max_bins, 256, 64), F), 256, 0, s>>>(fam_d, st_d, level,
-                                                                                                  hsum, hcnt);
+      launch_pdl(hist_zero_kernel, dim3(grid1(static_cast<int64_t>(lw) * max_bins, 256, 64), F), dim3(256), 0, s, fam_d,
+                 st_d, level, hsum, hcnt, n_items);
       const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
       {
         ProfScope prof(dev, "fit_hist_build");
         if (resident.atomic) {
           const dim3 grid(static_cast<unsigned>(ceil_div(n_max, atom_chunk)), pairs, F);
           if (atom_chunk >= kAtomPipeChunk)
-            hist_build_atomic_kernel<CodeT, true><<<grid, kAtomThreads, resident.atomic_smem, s>>>(
-                fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
-                resident.colh_max, atom_chunk);
+            launch_pdl(hist_build_atomic_kernel<CodeT, true>, grid, dim3(kAtomThreads), resident.atomic_smem, s, fam_d,
+                       st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
+                       resident.colh_max, atom_chunk);
           else
-            hist_build_atomic_kernel<CodeT, false><<<grid, kAtomThreads, resident.atomic_smem, s>>>(
-                fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
-                resident.colh_max, atom_chunk);
+            launch_pdl(hist_build_atomic_kernel<CodeT, false>, grid, dim3(kAtomThreads), resident.atomic_smem, s, fam_d,
+                       st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, dev->ctr_d,
+                       resident.colh_max, atom_chunk);
         }
         else if (resident.col)
           hist_build_col_kernel<CodeT><<<dim3(chunks, pairs, F), kColWarps * 32, resident.col_smem, s>>>(
@@ -369,45 +388,41 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, groups,
               dev->ctr_d);
       }
-      hist_derive_kernel<<<dim3(grid1(max_bins, 256, 16), pairs, F), 256, 0, s>>>(fam_d, st_d, nodes, level, hsum,
-                                                                                  hcnt, node_abs);
+      launch_pdl(hist_derive_kernel, dim3(grid1(max_bins, 256, 16), pairs, F), dim3(256), 0, s, fam_d, st_d, nodes,
+                 level, hsum, hcnt, node_abs);
       const dim3 sg(grid1(nrep_max, 4, 1 << 20), lw, F);  // 4 warps (reps) per 128-thread block
       {
         ProfScope prof(dev, "fit_screen");
-        screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
-                                          std::max(nrep_max, 1), level_slots_max, 0);
-        screen_kernel<<<sg, 128, 0, s>>>(fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d, rep_nb_d, win,
-                                          std::max(nrep_max, 1), level_slots_max, 1);
+        launch_pdl(screen_kernel, sg, dim3(128), 0, s, fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d,
+                   rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, 0);
+        launch_pdl(screen_kernel, sg, dim3(128), 0, s, fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d,
+                   rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, 1);
       }
-      FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
-      tieclass_prep_kernel<<<dim3(grid1(lw, 4, 1 << 20), F), 128, 0, s>>>(  // warp per node
-          fam_d, st_d, nodes, level, win, std::max(nrep_max, 1), level_slots_max, items, n_items);
+      // (n_items[0]: tie-class items, n_items[1]: exact items; both zeroed by hist_zero_kernel)
+      launch_pdl(tieclass_prep_kernel, dim3(grid1(lw, 4, 1 << 20), F), dim3(128), 0, s,  // warp per node
+                 fam_d, st_d, nodes, level, win, std::max(nrep_max, 1), level_slots_max, items, n_items);
       if (resident.phi_smem > 0)
-        tieclass_phi_kernel<CodeT><<<sm * 4, 256, resident.phi_smem, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_cm,
-                                                                 ord_cur, rep_nb_d, win, std::max(nrep_max, 1),
-                                                                 level_slots_max);
+        launch_pdl(tieclass_phi_kernel<CodeT>, dim3(sm * 4), dim3(256), resident.phi_smem, s, fam_d, nodes, items,
+                   n_items, level, Dp, codes_cm, ord_cur, rep_nb_d, win, std::max(nrep_max, 1), level_slots_max);
       else
-        tieclass_check_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_cm, ord,
-                                                             nodeid, win, std::max(nrep_max, 1), level_slots_max);
+        launch_pdl(tieclass_check_kernel<CodeT>, dim3(sm * 2), dim3(256), 0, s, fam_d, nodes, items, n_items, level, Dp,
+                   codes_cm, ord, nodeid, win, std::max(nrep_max, 1), level_slots_max);
       dev->count_launch(2);
-      FS_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int), s));
-      decide_kernel<<<dim3(grid1(lw, 4, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt, rep_boff_d, win,
-                                                                     std::max(nrep_max, 1), level_slots_max, items,
-                                                                     n_items, dev->ctr_d);
+      launch_pdl(decide_kernel, dim3(grid1(lw, 4, 1 << 20), F), dim3(128), 0, s, fam_d, st_d, nodes, level, hcnt,
+                 rep_boff_d, win, std::max(nrep_max, 1), level_slots_max, items, n_items + 1, dev->ctr_d);
       if (fork_totals) FS_CUDA(cudaStreamWaitEvent(s, dev->ev_join, 0));  // join: totals ready
       {
         ProfScope prof(dev, "fit_exact");
-        exact_kernel<CodeT><<<sm * 2, 256, 0, s>>>(fam_d, nodes, items, n_items, level, Dp, codes_cm, resid, ord,
-                                                   ord_cur, nodeid, rep_boff_d, lbuf, win, std::max(nrep_max, 1),
-                                                   level_slots_max, small_scratch ? 1 : 0);
+        launch_pdl(exact_kernel<CodeT>, dim3(sm * 2), dim3(256), 0, s, fam_d, nodes, items, n_items + 1, level, Dp,
+                   codes_cm, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win, std::max(nrep_max, 1), level_slots_max,
+                   small_scratch ? 1 : 0);
         if (small_scratch)
-          exact_small_kernel<CodeT><<<kExactSmallCtas, kSortThreads, 0, s>>>(
-              fam_d, nodes, items, n_items, level, Dp, codes_cm, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win,
-              std::max(nrep_max, 1), level_slots_max, small_scratch, n_max);
+          launch_pdl(exact_small_kernel<CodeT>, dim3(kExactSmallCtas), dim3(kSortThreads), 0, s, fam_d, nodes, items,
+                     n_items + 1, level, Dp, codes_cm, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win,
+                     std::max(nrep_max, 1), level_slots_max, small_scratch, n_max);
       }
-      exact_decide_kernel<<<dim3(grid1(lw, 128, 1 << 20), F), 128, 0, s>>>(fam_d, st_d, nodes, level, hcnt,
-                                                                           rep_boff_d, rep_nb_d, win,
-                                                                           std::max(nrep_max, 1), level_slots_max, lbuf);
+      launch_pdl(exact_decide_kernel, dim3(grid1(lw, 128, 1 << 20), F), dim3(128), 0, s, fam_d, st_d, nodes, level,
+                 hcnt, rep_boff_d, rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, lbuf);
       {
         ProfScope prof(dev, "fit_partition");
         // few large nodes (C4): a CTA per (node, 1,024-row chunk), two passes; many nodes (C5):
@@ -415,17 +430,14 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         const int64_t p_items = static_cast<int64_t>(F) * lw * part_chunks;
         if (static_cast<int64_t>(F) * lw * 4 < sm) {
           const dim3 pg(static_cast<unsigned>(p_items));
-          partition_count_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_cm, ord_cur,
-                                                                   scratch, nodeid, rep_orig_d, rep_boff_d, vals_d,
-                                                                   cle, ord, canon, x_d, d, trees_d, slots, part_cnt,
-                                                                   part_chunks, level_slots_max, F);
-          partition_scatter_kernel<CodeT><<<pg, kPartChunk, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_cm, ord_cur,
-                                                                     scratch, nodeid, part_cnt, part_chunks,
-                                                                     level_slots_max, F);
+          launch_pdl(partition_count_kernel<CodeT>, pg, dim3(kPartChunk), 0, s, fam_d, st_d, nodes, level, Dp, codes_cm,
+                     ord_cur, scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle, ord, canon, x_d, d, trees_d, slots,
+                     part_cnt, part_chunks, level_slots_max, F);
+          launch_pdl(partition_scatter_kernel<CodeT>, pg, dim3(kPartChunk), 0, s, fam_d, st_d, nodes, level, Dp,
+                     codes_cm, ord_cur, scratch, nodeid, part_cnt, part_chunks, level_slots_max, F);
         } else {
-          partition_kernel<CodeT><<<dim3(lw, F), 1024, 0, s>>>(fam_d, st_d, nodes, level, Dp, codes_cm, ord_cur,
-                                                                scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle,
-                                                                ord, canon, x_d, d, trees_d, slots);
+          launch_pdl(partition_kernel<CodeT>, dim3(lw, F), dim3(1024), 0, s, fam_d, st_d, nodes, level, Dp, codes_cm,
+                     ord_cur, scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle, ord, canon, x_d, d, trees_d, slots);
         }
       }
       dev->count_launch(10);
@@ -437,12 +449,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
                                                                                          ord_cur, resid, pred, trees_d);
       else
-        leaf_cta_kernel<<<dim3(static_cast<unsigned>(slots), F), kLeafThreads, 0, s>>>(fam_d, F, st_d, nodes, slots, ord_cur,
-                                                                               resid, pred, trees_d);
+        launch_pdl(leaf_cta_kernel, dim3(static_cast<unsigned>(slots), F), dim3(kLeafThreads), 0, s, fam_d, F, st_d, nodes,
+                   slots, ord_cur, resid, pred, trees_d);
     }
-    mse_stash_kernel<<<grid1(n_tot, 256, sm * 16), 256, 0, s>>>(fam_d, st_d, nodes, rowfam, n_tot, target_c, pred,
-                                                                  ebuf, mse_k);
-    commit_kernel<<<static_cast<unsigned>(ceil_div(F, 128)), 128, 0, s>>>(fam_d, st_d, nodes, F);
+    launch_pdl(mse_stash_kernel, dim3(grid1(n_tot, 256, sm * 16)), dim3(256), 0, s, fam_d, st_d, nodes, rowfam, n_tot,
+               target_c, pred, ebuf, mse_k);
+    launch_pdl(commit_kernel, dim3(static_cast<unsigned>(ceil_div(F, 128))), dim3(128), 0, s, fam_d, st_d, nodes, F);
     dev->count_launch();
     dev->count_launch(2);
     FS_CUDA(cudaGetLastError());

@@ -763,9 +763,11 @@ __global__ void base_kernel(const FamDesc* __restrict__ fam, const double* __res
 // boosting rounds
 // ------------------------------------------------------------------------------------------
 __global__ void round_init_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st, NodeRec* __restrict__ nodes,
-                                  int slots, TreeRec* __restrict__ trees) {
+                                  int slots, TreeRec* __restrict__ trees, int64_t* __restrict__ node_abs) {
+  FS_PDL_WAIT();
   const int f = blockIdx.x;
   const FamDesc fd = fam[f];
+  for (int s = threadIdx.x; s < slots; s += blockDim.x) node_abs[fd.node0 + s] = 0;
   if (!st[f].active) return;
   NodeRec* nd = nodes + fd.node0;
   for (int s = threadIdx.x; s < slots; s += blockDim.x) {
@@ -785,6 +787,7 @@ __global__ void residual_kernel(const FamDesc* __restrict__ fam, int F, int64_t 
                                 const double* __restrict__ pred, double* __restrict__ resid,
                                 const int32_t* __restrict__ ord_root, int32_t* __restrict__ ord_cur,
                                 int16_t* __restrict__ nodeid) {
+  FS_PDL_WAIT();
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n_tot;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int f = rowfam[p];
@@ -819,6 +822,7 @@ __device__ __forceinline__ int fix_shift(uint64_t maxabs_bits, int n) {
 __global__ void fixed_kernel(const FamDesc* __restrict__ fam, int64_t n_tot, FamState* __restrict__ st,
                              const int32_t* __restrict__ rowfam, const double* __restrict__ resid,
                              int64_t* __restrict__ rfix) {
+  FS_PDL_WAIT();
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n_tot;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int f = rowfam[p];

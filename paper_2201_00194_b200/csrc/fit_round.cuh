@@ -10,6 +10,7 @@ namespace {
 // Which nodes at `level` are screened, which histograms are built directly / derived.
 __global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                                   NodeRec* __restrict__ nodes, int level) {
+  FS_PDL_WAIT();
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
@@ -39,7 +40,10 @@ __global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamStat
 }
 
 __global__ void hist_zero_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st, int level,
-                                 int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt) {
+                                 int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt, int* __restrict__ n_items) {
+  FS_PDL_WAIT();
+  // the level's two work-list counters (tie-class items, exact items)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) n_items[threadIdx.x] = 0;
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
   if (!st[f].active || level >= max(fd.depth, 1)) return;
@@ -65,6 +69,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_build_kernel(
     int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
     const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
     int64_t* __restrict__ node_abs, int groups, unsigned long long* __restrict__ ctr) {
+  FS_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
@@ -184,6 +189,7 @@ __global__ void __launch_bounds__(kColWarps * 32) hist_build_col_kernel(
     const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb, const int32_t* __restrict__ grp_off,
     const int32_t* __restrict__ grp_rg, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
     int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr) {
+  FS_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
@@ -337,6 +343,7 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
     int Dp, const CodeT* __restrict__ codes_c, const int64_t* __restrict__ rfix, const int32_t* __restrict__ ord_cur,
     const int32_t* __restrict__ rep_boff, int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt,
     int64_t* __restrict__ node_abs, unsigned long long* __restrict__ ctr, int colh_max, int chunk) {
+  FS_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
@@ -591,6 +598,7 @@ inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes, int c
 __global__ void hist_derive_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                                    const NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
                                    int32_t* __restrict__ hcnt, int64_t* __restrict__ node_abs) {
+  FS_PDL_WAIT();
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
   if (!st[f].active || level == 0) return;
@@ -673,6 +681,7 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
                               const int32_t* __restrict__ hcnt, const int64_t* __restrict__ node_abs,
                               const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
                               WinRec* __restrict__ win, int nrep_max, int level_slots_max, int pass) {
+  FS_PDL_WAIT();
   // warp per (node, rep), lanes over the rep's bins: coalesced histogram reads, warp prefix
   // scans for the left count / sum, every candidate's screen in parallel
   const int f = blockIdx.z;
@@ -815,6 +824,7 @@ __global__ void tieclass_prep_kernel(const FamDesc* __restrict__ fam, const FamS
                                      NodeRec* __restrict__ nodes, int level, const WinRec* __restrict__ win,
                                      int nrep_max, int level_slots_max, ExactItem* __restrict__ items,
                                      int* __restrict__ n_items) {
+  FS_PDL_WAIT();
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
@@ -853,6 +863,7 @@ __global__ void decide_kernel(const FamDesc* __restrict__ fam, const FamState* _
                               const int32_t* __restrict__ rep_boff, const WinRec* __restrict__ win, int nrep_max,
                               int level_slots_max, ExactItem* __restrict__ items, int* __restrict__ n_items,
                               unsigned long long* __restrict__ ctr) {
+  FS_PDL_WAIT();
   (void)hcnt;
   (void)rep_boff;
   const int f = blockIdx.y;
@@ -931,6 +942,7 @@ __global__ void __launch_bounds__(256) tieclass_phi_kernel(
     const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_cm,
     const int32_t* __restrict__ ord_cur, const int32_t* __restrict__ rep_nb, WinRec* __restrict__ win,
     int nrep_max, int level_slots_max) {
+  FS_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* phi = reinterpret_cast<uint16_t*>(smem);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -1012,6 +1024,7 @@ __global__ void __launch_bounds__(256) tieclass_check_kernel(
     const int* __restrict__ n_items, int level, int Dp, const CodeT* __restrict__ codes_cm,
     const int32_t* __restrict__ ord, const int16_t* __restrict__ nodeid, WinRec* __restrict__ win, int nrep_max,
     int level_slots_max) {
+  FS_PDL_WAIT();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int total = *n_items;
@@ -1104,6 +1117,7 @@ __device__ __forceinline__ double warp_fold_gather(const double* __restrict__ v,
 __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
                               NodeRec* __restrict__ nodes, int level, const int32_t* __restrict__ ord_cur,
                               const double* __restrict__ resid) {
+  FS_PDL_WAIT();
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
@@ -1468,6 +1482,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_boff,
     double* __restrict__ lbuf, const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
     int32_t* __restrict__ scratch, int n_max) {
+  FS_PDL_WAIT();
   __shared__ SortSmem sm;
   __shared__ int wsum[32];
   __shared__ double red[kSpecRed];
@@ -1606,6 +1621,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
                                                     const int32_t* __restrict__ rep_boff, double* __restrict__ lbuf,
                                                     const WinRec* __restrict__ win, int nrep_max,
                                                     int level_slots_max, int small_path) {
+  FS_PDL_WAIT();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int total = *n_items;
@@ -1685,6 +1701,7 @@ __global__ void exact_decide_kernel(const FamDesc* __restrict__ fam, const FamSt
                                     const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
                                     const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
                                     const double* __restrict__ lbuf) {
+  FS_PDL_WAIT();
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
@@ -1758,6 +1775,7 @@ __global__ void __launch_bounds__(1024) partition_kernel(
     int16_t* __restrict__ nodeid, const int32_t* __restrict__ rep_orig, const int32_t* __restrict__ rep_boff,
     const double* __restrict__ vals, const int32_t* __restrict__ cle, const int32_t* __restrict__ ord,
     const int32_t* __restrict__ canon, const double* __restrict__ x, int d, TreeRec* __restrict__ trees, int slots) {
+  FS_PDL_WAIT();
   __shared__ int wsum[32];
   __shared__ int base_l, base_r;
   const int f = blockIdx.y;
@@ -1866,6 +1884,7 @@ __global__ void __launch_bounds__(kPartChunk) partition_count_kernel(
     const double* __restrict__ vals, const int32_t* __restrict__ cle, const int32_t* __restrict__ ord,
     const int32_t* __restrict__ canon, const double* __restrict__ x, int d, TreeRec* __restrict__ trees, int slots,
     int32_t* __restrict__ part_cnt, int chunks_max, int level_slots_max, int F) {
+  FS_PDL_WAIT();
   __shared__ int wsum[32];
   const int nl = 1 << level;
   const int64_t items = static_cast<int64_t>(F) * nl * chunks_max;  // (family, node, chunk)
@@ -1936,6 +1955,7 @@ __global__ void __launch_bounds__(kPartChunk) partition_scatter_kernel(
     const FamDesc* __restrict__ fam, const FamState* __restrict__ st, NodeRec* __restrict__ nodes, int level, int Dp,
     const CodeT* __restrict__ codes_cm, int32_t* __restrict__ ord_cur, const int32_t* __restrict__ scratch,
     int16_t* __restrict__ nodeid, const int32_t* __restrict__ part_cnt, int chunks_max, int level_slots_max, int F) {
+  FS_PDL_WAIT();
   __shared__ int wsum[32];
   __shared__ int s_off;
   const int nl = 1 << level;
@@ -2004,6 +2024,7 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
                                                        int slots, const int32_t* __restrict__ ord_cur,
                                                        const double* __restrict__ resid, double* __restrict__ pred,
                                                        TreeRec* __restrict__ trees) {
+  FS_PDL_WAIT();
   __shared__ double red[kSpecRed];
   __shared__ __align__(16) double stage[4 * kStageCh];
   const int f = blockIdx.y, s = blockIdx.x;
@@ -2053,6 +2074,7 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
 __global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamState* __restrict__ st,
                             NodeRec* __restrict__ nodes, int slots, const int32_t* __restrict__ ord_cur,
                             const double* __restrict__ resid, double* __restrict__ pred, TreeRec* __restrict__ trees) {
+  FS_PDL_WAIT();
   const int lane = threadIdx.x & 31;
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int f = static_cast<int>(w / slots), s = static_cast<int>(w % slots);
@@ -2115,6 +2137,7 @@ __global__ void mse_stash_kernel(const FamDesc* __restrict__ fam, const FamState
                                  const NodeRec* __restrict__ nodes, const int32_t* __restrict__ rowfam, int64_t n_tot,
                                  const double* __restrict__ target_c, const double* __restrict__ pred,
                                  double* __restrict__ ebuf, int K) {
+  FS_PDL_WAIT();
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_tot;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int f = rowfam[i];
@@ -2125,6 +2148,7 @@ __global__ void mse_stash_kernel(const FamDesc* __restrict__ fam, const FamState
 }
 __global__ void commit_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
                               const NodeRec* __restrict__ nodes, int F) {
+  FS_PDL_WAIT();
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   const FamDesc fd = fam[f];
@@ -2150,6 +2174,7 @@ __global__ void commit_kernel(const FamDesc* __restrict__ fam, FamState* __restr
 __global__ void mse_fold_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st, int F,
                                 const double* __restrict__ ebuf, int K, int64_t ring_stride, int t_lo, int t_hi,
                                 double* __restrict__ mse, int max_trees) {
+  FS_PDL_WAIT();
   const int W = t_hi - t_lo;
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;

@@ -32,6 +32,13 @@ inline void cuda_check(cudaError_t e, const char* what) {
   }
 }
 #define FS_CUDA(x) ::fs::cuda_check((x), #x)
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream serialization
+// may be scheduled while its predecessor drains; it waits here for the predecessor's completion
+// (and memory visibility) before touching anything it produced. A no-op for a normal launch.
+// Programmatic dependent launch: wait for the preceding kernel on the stream to complete (and its
+// writes to be visible), then let the next PDL launch start scheduling (its CTAs park in their
+// own FS_PDL_WAIT). Harmless no-ops when the launch carried no PDL attribute.
+#define FS_PDL_WAIT() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
 
 template <class F>
 int guard(F&& f) {
