@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "fit.cuh"
+#include "fold_est.cuh"
 
 namespace fs {
 void launch_featurize(fs_device* dev, const fs_spaces* sp, int64_t n, const int32_t* space_of_d,

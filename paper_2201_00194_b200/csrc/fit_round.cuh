@@ -1135,18 +1135,7 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 
 constexpr int kSpecMulti = 8192;  // cta_fold_spec: chains from this length fold in four segments (three speculated)
 constexpr int kSpecRed = 200;      // cta_fold_spec's shared scratch (doubles)
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-  s = fs_add(a, b);
-  const double bb = fs_sub(s, a);
-  e = fs_add(fs_sub(a, fs_sub(s, bb)), fs_sub(b, bb));
-}
-__device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles -> consecutive ints
-  const long long b = __double_as_longlong(x);
-  return b >= 0 ? b : static_cast<long long>(0x8000000000000000ull) - b;
-}
-__device__ __forceinline__ double ord_dbl(long long o) {
-  return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
-}
+// (two_sum, dbl_ord, ord_dbl: fold_est.cuh)
 // CTA-wide exact sequential fold of a long gathered chain (sum_residuals, costmodel.cpp:36-40) by
 // midpoint speculation (the warp version is fold_spec): the block's double-double sum of
 // x_0..x_{m-1} estimates the exact prefix P; thread 0 folds x_0..x_{m-1} from 0.0 (the true S_m)
@@ -1200,11 +1189,17 @@ __device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, co
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = static_cast<int>(blockDim.x >> 5);
   if (n < 4096 || nw < 2) {  // short chain: warp 0 folds it
+#ifdef FS_SPEC_PROBE
+    const long long q0 = clock64();
+#endif
     if (warp == 0) {
       const double r = warp_fold_gather_from(v, idx, n, 0.0);
       if (lane == 0) red[196] = r;
     }
     __syncthreads();
+#ifdef FS_SPEC_PROBE
+    if (tid == 0) printf("SPEC short n=%d nt=%d cyc=%lld\n", n, blockDim.x, clock64() - q0);
+#endif
     const double r = red[196];
     __syncthreads();
     return r;
@@ -1327,6 +1322,10 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
   const int G = (n >= kSpecMulti && nw >= 4) ? 3 : 1;
   const int K = G + 1;
   auto bnd = [&](int g) { return static_cast<int>((static_cast<long long>(g) * n) / K); };
+#ifdef FS_SPEC_PROBE
+  long long pc0 = clock64(), pc1 = 0, pc2 = 0;
+  int pmiss = 0;
+#endif
   // 1. double-double estimates of the exact prefix sums at the segment starts
 #pragma unroll
   for (int g = 0; g < 3; ++g) {
@@ -1429,6 +1428,9 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
     __syncthreads();
   }
   // 3. resolve segment by segment (every chain result parked in the stage buffer)
+#ifdef FS_SPEC_PROBE
+  pc1 = clock64();
+#endif
   stage[tid] = s;
   if (tid == 0) red[196] = s;  // S_1: the true prefix at bnd(1)
   __shared__ int hit;
@@ -1446,6 +1448,13 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
       if (hit) red[197] = stage[32 * w0 + k];
     }
     __syncthreads();
+#ifdef FS_SPEC_PROBE
+    if (tid == 0 && !hit) {
+      const long long k = dbl_ord(red[196]) - dbl_ord(red[192 + g - 1]);
+      printf("SPECMISS n=%d g=%d off=%lld S=%.17g P=%.17g\n", n, g, k, red[196], red[192 + g - 1]);
+      ++pmiss;
+    }
+#endif
     if (!hit) {  // re-fold segment g alone from the true prefix
       if (warp == 0) {
         const double t = warp_fold_gather_from(v, idx + bnd(g), bnd(g + 1) - bnd(g), red[196]);
@@ -1457,6 +1466,12 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
     __syncthreads();
   }
   const double out = red[196];
+#ifdef FS_SPEC_PROBE
+  pc2 = clock64();
+  if (tid == 0)
+    printf("SPEC staged n=%d G=%d nt=%d miss=%d est+fold=%lld resolve=%lld\n", n, G, blockDim.x, pmiss, pc1 - pc0,
+           pc2 - pc1);
+#endif
   __syncthreads();
   return out;
 }
@@ -1483,13 +1498,27 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     double* __restrict__ lbuf, const WinRec* __restrict__ win, int nrep_max, int level_slots_max,
     int32_t* __restrict__ scratch, int n_max) {
   FS_PDL_WAIT();
-  __shared__ SortSmem sm;
+  // the sort's and the speculative folds' shared memory overlap (never live together; the sort
+  // state is re-initialised after a fold)
+  union FoldOrSort {
+    SortSmem sort;
+    struct {
+      double stage[fold_est_stage_doubles(kSortThreads, 2)];
+      double scr[fold_est_scratch_doubles(kSortThreads)];
+    } fold;
+  };
+  __shared__ __align__(16) FoldOrSort u;
+  SortSmem& sm = u.sort;
   __shared__ int wsum[32];
-  __shared__ double red[kSpecRed];
-  __shared__ __align__(16) double stage[4 * kStageChSmall];  // 8 KB (static shared memory is 48 KB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = *n_items;
   sort_smem_init(sm);
+  auto fold_at = [&](int64_t pos0, const int32_t* list, int len) {
+    __syncthreads();  // the sort state is dead
+    const double r = cta_fold_est<2>(resid + pos0, list, len, 0.0, u.fold.stage, u.fold.scr);
+    sort_smem_init(sm);
+    return r;
+  };
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const ExactItem it = items[w];
     const FamDesc fd = fam[it.fam];
@@ -1497,7 +1526,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const int nv = nd.n, n = fd.n;
     if (it.rep < 0) {  // a long node total: speculative CTA fold (exact_kernel folds the short ones)
       if (nv < kExactSpecMin) continue;
-      const double t = cta_fold_spec_staged(resid + fd.pos0, ord_cur + fd.pos0 + nd.seg, nv, red, stage, kStageChSmall);
+      const double t = fold_at(fd.pos0, ord_cur + fd.pos0 + nd.seg, nv);
       if (tid == 0) nd.total = t;
       continue;
     }
@@ -1512,8 +1541,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     if (!exact_is_small(nv, n)) {
       if (!spec_one) continue;  // exact_kernel scans the presorted list
       // the root: every row is a member, the presorted list is the member list
-      const double L = cta_fold_spec_staged(resid + fd.pos0, ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n, need, red,
-                                            stage, kStageChSmall);
+      const double L = fold_at(fd.pos0, ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n, need);
       if (tid == 0) out[wr.best_bin] = L;
       continue;
     }
@@ -1576,7 +1604,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     }
     // 3. the fold (warp 0; members in list order, boundaries at code changes)
     if (spec_one) {
-      const double L = cta_fold_spec_staged(resid + fd.pos0, src, need, red, stage, kStageChSmall);
+      const double L = fold_at(fd.pos0, src, need);
       if (tid == 0) out[wr.best_bin] = L;
     } else if (warp == 0) {
       double left = 0.0;
@@ -2016,6 +2044,7 @@ __global__ void __launch_bounds__(kPartChunk) partition_scatter_kernel(
   }
 }
 
+constexpr int kLeafEstMin = 384;   // leaf chains from this length fold through cta_fold_est (fold_est.cuh)
 constexpr int kLeafThreads = 256;  // leaf CTA (1,024 threads with four speculated segments measured slower: C5 leaves 0.59 -> 0.82 s)
 // Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
 // the leaf's order-0 segment / n (cta_fold_spec), then pred += lr*value over its rows.
@@ -2025,8 +2054,8 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
                                                        const double* __restrict__ resid, double* __restrict__ pred,
                                                        TreeRec* __restrict__ trees) {
   FS_PDL_WAIT();
-  __shared__ double red[kSpecRed];
-  __shared__ __align__(16) double stage[4 * kStageCh];
+  __shared__ __align__(16) double stage[fold_est_stage_doubles(kLeafThreads)];
+  __shared__ double fscr[fold_est_scratch_doubles(kLeafThreads)];
   const int f = blockIdx.y, s = blockIdx.x;
   if (f >= F) return;
   const FamDesc fd = fam[f];
@@ -2036,7 +2065,19 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
   if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
   const int n = nd.n;
   const int32_t* L = ord_cur + fd.pos0 + nd.seg;
-  const double sum = nd.pad_ ? nd.total : cta_fold_spec_staged(resid + fd.pos0, L, n, red, stage, kStageCh);
+  double sum;
+  if (nd.pad_) {
+    sum = nd.total;
+  } else if (n < kLeafEstMin) {  // short chain: warp 0
+    if (threadIdx.x < 32) {
+      const double t = warp_fold_gather(resid + fd.pos0, L, n);
+      if (threadIdx.x == 0) fscr[0] = t;
+    }
+    __syncthreads();
+    sum = fscr[0];
+  } else {
+    sum = cta_fold_est<16>(resid + fd.pos0, L, n, 0.0, stage, fscr);
+  }
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
   // prediction update, 8 rows per thread in flight (index and prediction gathers issued before
