@@ -1481,7 +1481,7 @@ __device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict_
 // presorted list restricted to the node (:50-55), recorded at every value boundary.
 // exact folds of nodes below a quarter of the family go through exact_small_kernel
 __device__ __forceinline__ bool exact_is_small(int nv, int n) { return nv < n; }
-constexpr int kExactSpecMin = 4096;  // chains from this length fold speculatively in a CTA (cta_fold_spec)
+constexpr int kExactSpecMin = 1024;  // chains from this length fold in a CTA (cta_fold_est / cta_fold_est_rec)
 
 // Exact reference-order folds for SMALL nodes (nv * 4 < n): instead of scanning the feature's
 // full presorted list for the node's members (exact_kernel; costs O(n) gathers per item however
@@ -1505,6 +1505,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     struct {
       double stage[fold_est_stage_doubles(kSortThreads, 2)];
       double scr[fold_est_scratch_doubles(kSortThreads)];
+      CodeT cst[2 * kSortThreads];
     } fold;
   };
   __shared__ __align__(16) FoldOrSort u;
@@ -1518,6 +1519,11 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const double r = cta_fold_est<2>(resid + pos0, list, len, 0.0, u.fold.stage, u.fold.scr);
     sort_smem_init(sm);
     return r;
+  };
+  auto fold_rec = [&](int64_t pos0, const int32_t* list, int len, const CodeT* cj, double* out) {
+    __syncthreads();
+    cta_fold_est_rec<2, CodeT>(resid + pos0, list, len, cj, out, u.fold.stage, u.fold.cst, u.fold.scr);
+    sort_smem_init(sm);
   };
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const ExactItem it = items[w];
@@ -1538,11 +1544,17 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     // one window candidate: only L at its left count is read (exact_decide_kernel), so a long
     // fold splits speculatively at its midpoint (cta_fold_spec, bit-exact)
     const bool spec_one = wr.count == 1 && need >= kExactSpecMin;
+    const CodeT* cj = codes_cm + fd.ord0 + static_cast<int64_t>(jj) * fd.n;  // column-major
     if (!exact_is_small(nv, n)) {
-      if (!spec_one) continue;  // exact_kernel scans the presorted list
+      if (need < kExactSpecMin) continue;  // exact_kernel scans the presorted list
       // the root: every row is a member, the presorted list is the member list
-      const double L = fold_at(fd.pos0, ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n, need);
-      if (tid == 0) out[wr.best_bin] = L;
+      const int32_t* lst = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;
+      if (spec_one) {
+        const double L = fold_at(fd.pos0, lst, need);
+        if (tid == 0) out[wr.best_bin] = L;
+      } else {
+        fold_rec(fd.pos0, lst, need, cj, out);
+      }
       continue;
     }
     int32_t* A = scratch + static_cast<int64_t>(blockIdx.x) * 2 * n_max;
@@ -1583,7 +1595,6 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
       __syncthreads();
     }
     // 2. stable sort by the feature's code: (code, canonical position) = presorted order
-    const CodeT* cj = codes_cm + fd.ord0 + static_cast<int64_t>(jj) * fd.n;  // column-major
     int32_t* src = A;
     int32_t* dst = B;
     if (stable_digit_pass([&](int i) { return src[i]; }, dst, nv,
@@ -1606,6 +1617,8 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     if (spec_one) {
       const double L = fold_at(fd.pos0, src, need);
       if (tid == 0) out[wr.best_bin] = L;
+    } else if (need >= kExactSpecMin) {
+      fold_rec(fd.pos0, src, need, cj, out);
     } else if (warp == 0) {
       double left = 0.0;
       int prev = -1;
@@ -1668,7 +1681,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const FamDesc* __restrict__ 
     if (small_path) {
       const WinRec& wr = win[(static_cast<int64_t>(it.fam) * level_slots_max + (it.slot - ((1 << level) - 1))) *
                                  nrep_max + it.rep];
-      if (wr.count == 1 && wr.maxlc >= kExactSpecMin) continue;  // exact_small_kernel: speculative fold
+      if (wr.maxlc >= kExactSpecMin) continue;  // exact_small_kernel: CTA fold of the presorted list
     }
     const int jj = it.rep;
     const int32_t* L = ord + fd.ord0 + static_cast<int64_t>(jj) * fd.n;

@@ -67,7 +67,7 @@ __device__ __forceinline__ void warp_sum_dd(double& h, double& l) {
 // doubles keep the sub-block accesses conflict-free while the folds read runs of 16-byte words
 // in order.
 __host__ __device__ constexpr int fold_est_stage_doubles(int threads, int emax = 16) { return threads * (emax + 2); }
-__host__ __device__ constexpr int fold_est_scratch_doubles(int threads) { return threads + 32 + 4 * (threads / 32) + 8; }
+__host__ __device__ constexpr int fold_est_scratch_doubles(int threads) { return threads + 64 + 4 * (threads / 32) + 8; }
 
 // Fold s through `nblk` whole sub-blocks of E elements (pitch P) starting at sb, then `tail`
 // more elements; the next sub-block's loads are issued before the current adds.
@@ -109,10 +109,12 @@ __device__ __forceinline__ double fold_run_e(int E, const double* __restrict__ s
 // fold_est_scratch_doubles(blockDim) doubles. blockDim a multiple of 32, at most 1024; EMAX a
 // power of two in [2, 16] (the longest sub-block per thread and super-segment).
 // ctr (optional): [0] += segments resolved by a hit, [1] += segments re-folded after a miss.
-template <int EMAX = 16>
-__device__ __noinline__ double cta_fold_est(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
-                                            double start, double* __restrict__ stage, double* __restrict__ scr,
-                                            unsigned long long* ctr = nullptr) {
+template <int EMAX, typename CodeT, bool kRec>
+__device__ __forceinline__ double cta_fold_est_impl(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
+                                                    double start, const CodeT* __restrict__ codes,
+                                                    double* __restrict__ out, double* __restrict__ stage,
+                                                    CodeT* __restrict__ cst, double* __restrict__ scr,
+                                                    unsigned long long* ctr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = blockDim.x, nw = T >> 5;
   double* res = scr;              // [T] chain results
@@ -120,8 +122,10 @@ __device__ __noinline__ double cta_fold_est(const double* __restrict__ v, const 
   double* wt = cen + 32;          // [2 nw] warp prefix-sum totals (double-double)
   double* dt = wt + 2 * nw;       // [nw] warp rounding-error totals
   double* bcast = dt + 2 * nw;    // [1]
+  double* tst = bcast + 8;        // [32] (kRec) true start of every segment
   constexpr int kFoldE = EMAX, kFoldPitch = EMAX + 2;
   double S = start;  // true value at the current super-segment's start (every thread)
+  int last_code = -1;  // (kRec) code of the element before the super-segment
 #ifdef FOLD_EST_PROBE
   long long tq = clock64();
 #define FE_MARK(k)                                                       \
@@ -158,6 +162,13 @@ __device__ __noinline__ double cta_fold_est(const double* __restrict__ v, const 
 #pragma unroll
       for (int u = 0; u < 8; ++u)
         if (j0 + u < E) xv[u] = v[ii[u]];
+      if (kRec) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int p = (j0 + u) * T + tid;
+          if (j0 + u < E && p < L) cst[p] = codes[ii[u]];
+        }
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int p = (j0 + u) * T + tid;
@@ -252,9 +263,11 @@ __device__ __noinline__ double cta_fold_est(const double* __restrict__ v, const 
     if (tid == 0) {
       double cur = res[0];
       unsigned long long hits = 0, misses = 0;
+      if (kRec) tst[0] = S;
       for (int k = 1; k < nw; ++k) {
         const int a0 = k * 32 * E;
         if (a0 >= L) break;
+        if (kRec) tst[k] = cur;
         const long long off = dbl_ord(cur) - (dbl_ord(cen[k]) - 16);
         if (off >= 0 && off < 32 && __double_as_longlong(ord_dbl(dbl_ord(cur))) == __double_as_longlong(cur)) {
           cur = res[32 * k + static_cast<int>(off)];
@@ -272,12 +285,50 @@ __device__ __noinline__ double cta_fold_est(const double* __restrict__ v, const 
       }
     }
     __syncthreads();
+    if (kRec) {  // 5. every segment re-folded from its true start by one thread, recording
+      // S_i (the fold of x_0..x_{i-1}) at out[c_{i-1}] wherever c_i != c_{i-1}
+      const int a0 = warp * 32 * E;
+      if (lane == 0 && a0 < L) {
+        const int a1 = min(a0 + 32 * E, L);
+        double cur = tst[warp];
+        int prev = a0 == 0 ? last_code : static_cast<int>(cst[a0 - 1]);
+        for (int i = a0; i < a1; ++i) {
+          const int c = static_cast<int>(cst[i]);
+          if (prev >= 0 && c != prev) out[prev] = cur;
+          cur = fs_add(cur, stage[(i >> lgE) * kFoldPitch + (i & (E - 1))]);
+          prev = c;
+        }
+      }
+      last_code = static_cast<int>(cst[L - 1]);
+      __syncthreads();
+    }
     S = bcast[0];
     FE_MARK(7)
     base += L;
   }
 #undef FE_MARK
+  if (kRec && tid == 0 && n > 0) out[last_code] = S;
   return S;
+}
+
+// The chain's fold only (x_i = v[idx[i]], or v[i] when idx is nullptr), from `start`.
+template <int EMAX = 16>
+__device__ __noinline__ double cta_fold_est(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
+                                            double start, double* __restrict__ stage, double* __restrict__ scr,
+                                            unsigned long long* ctr = nullptr) {
+  return cta_fold_est_impl<EMAX, uint8_t, false>(v, idx, n, start, nullptr, nullptr, stage, nullptr, scr, ctr);
+}
+
+// best_split's recorded fold (costmodel.cpp:50-69): the chain x_i = v[idx[i]] with codes
+// c_i = codes[idx[i]] (non-decreasing along the list); out[c] = the fold of every element before
+// the first element whose code differs from c, i.e. the left sum at each value boundary, and the
+// last code's entry holds the full fold. cst: EMAX * blockDim CodeT of smem. Returns the fold.
+template <int EMAX, typename CodeT>
+__device__ __noinline__ double cta_fold_est_rec(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
+                                                const CodeT* __restrict__ codes, double* __restrict__ out,
+                                                double* __restrict__ stage, CodeT* __restrict__ cst,
+                                                double* __restrict__ scr) {
+  return cta_fold_est_impl<EMAX, CodeT, true>(v, idx, n, 0.0, codes, out, stage, cst, scr, nullptr);
 }
 
 }  // namespace fs
