@@ -271,7 +271,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   double* lbuf = ar.alloc<double>(total_lbuf);
   WinRec* win = ar.alloc<WinRec>(static_cast<size_t>(F) * level_slots_max * std::max(nrep_max, 1));
   ExactItem* items = ar.alloc<ExactItem>(static_cast<size_t>(F) * level_slots_max * (nrep_max + 1));
-  int* n_items = ar.alloc<int>(2);  // [0] tie-class items, [1] exact items (zeroed by hist_zero_kernel)
+  int* n_items = ar.alloc<int>(2);  // [0] tie-class items, [1] exact items (zeroed by level_prep_kernel)
   (void)total_tree;
   // column-major codes (the presorted lists' layout) for the kernels that read one feature's code
   // of scattered rows: tie classes, exact folds, partition
@@ -347,9 +347,15 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
     dev->count_launch(3);
     for (int level = 0; level <= depth_max; ++level) {
       const unsigned lw = 1u << level;
-      launch_pdl(level_plan_kernel, dim3(grid1(lw, 128, 1 << 20), F), dim3(128), 0, s, fam_d, st_d, nodes, level);
+      if (level == depth_max || nrep_max == 0) {
+        launch_pdl(level_plan_kernel, dim3(grid1(lw, 128, 1 << 20), F), dim3(128), 0, s, fam_d, st_d, nodes, level);
+        dev->count_launch();
+        continue;
+      }
+      // the level's plan, zeroed histogram slots and work-list counters
+      launch_pdl(level_prep_kernel, dim3(grid1(static_cast<int64_t>(lw) * max_bins, 256, 64), F), dim3(256), 0, s,
+                 fam_d, st_d, nodes, level, hsum, hcnt, n_items);
       dev->count_launch();
-      if (level == depth_max || nrep_max == 0) continue;
       // Optional fork (FAMSEER_FORK_TOTALS=1): every screened node's total on a side stream while
       // this level's histogram..decide kernels run; joined before the exact folds. Measured
       // slower at C4 (the root chain outlasts the level's other kernels and the join then
@@ -361,8 +367,6 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         FS_CUDA(cudaEventRecord(dev->ev_join, aux));
         dev->count_launch();
       }
-      launch_pdl(hist_zero_kernel, dim3(grid1(static_cast<int64_t>(lw) * max_bins, 256, 64), F), dim3(256), 0, s, fam_d,
-                 st_d, level, hsum, hcnt, n_items);
       const unsigned pairs = level == 0 ? 1u : (1u << (level - 1));
       {
         ProfScope prof(dev, "fit_hist_build");
@@ -389,8 +393,6 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
               fam_d, st_d, nodes, level, Dp, codes_c, rfix, ord_cur, rep_boff_d, hsum, hcnt, node_abs, groups,
               dev->ctr_d);
       }
-      launch_pdl(hist_derive_kernel, dim3(grid1(max_bins, 256, 16), pairs, F), dim3(256), 0, s, fam_d, st_d, nodes,
-                 level, hsum, hcnt, node_abs);
       const dim3 sg(grid1(nrep_max, 4, 1 << 20), lw, F);  // 4 warps (reps) per 128-thread block
       {
         ProfScope prof(dev, "fit_screen");
@@ -399,7 +401,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
         launch_pdl(screen_kernel, sg, dim3(128), 0, s, fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d,
                    rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, 1);
       }
-      // (n_items[0]: tie-class items, n_items[1]: exact items; both zeroed by hist_zero_kernel)
+      // (n_items[0]: tie-class items, n_items[1]: exact items; both zeroed by level_prep_kernel)
       launch_pdl(tieclass_prep_kernel, dim3(grid1(lw, 4, 1 << 20), F), dim3(128), 0, s,  // warp per node
                  fam_d, st_d, nodes, level, win, std::max(nrep_max, 1), level_slots_max, items, n_items);
       if (resident.phi_smem > 0)
@@ -441,7 +443,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                      ord_cur, scratch, nodeid, rep_orig_d, rep_boff_d, vals_d, cle, ord, canon, x_d, d, trees_d, slots);
         }
       }
-      dev->count_launch(10);
+      dev->count_launch(8);
     }
     const int64_t leaf_threads = static_cast<int64_t>(F) * slots * 32;
     {

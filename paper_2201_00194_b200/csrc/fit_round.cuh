@@ -7,16 +7,9 @@ namespace fs {
 namespace fit {
 namespace {
 
-// Which nodes at `level` are screened, which histograms are built directly / derived.
-__global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
-                                  NodeRec* __restrict__ nodes, int level) {
-  FS_PDL_WAIT();
-  const int f = blockIdx.y;
-  const FamDesc fd = fam[f];
-  if (!st[f].active) return;
+// Which nodes at `level` are screened, which histograms are built directly / derived (one node).
+__device__ __forceinline__ void plan_node(const FamDesc& fd, NodeRec* __restrict__ nodes, int level, int local) {
   const int first = (1 << level) - 1;
-  const int local = blockIdx.x * blockDim.x + threadIdx.x;
-  if (local >= (1 << level)) return;
   NodeRec* nd = nodes + fd.node0;
   const int s = first + local;
   if (level == 0) {
@@ -39,14 +32,29 @@ __global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamStat
   }
 }
 
-__global__ void hist_zero_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st, int level,
-                                 int64_t* __restrict__ hsum, int32_t* __restrict__ hcnt, int* __restrict__ n_items) {
+__global__ void level_plan_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                  NodeRec* __restrict__ nodes, int level) {
   FS_PDL_WAIT();
-  // the level's two work-list counters (tie-class items, exact items)
+  const int f = blockIdx.y;
+  const FamDesc fd = fam[f];
+  if (!st[f].active) return;
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;
+  if (local < (1 << level)) plan_node(fd, nodes, level, local);
+}
+
+// A level's preparation in one launch: the node plan (block 0 of each family), the level's
+// histogram slots zeroed, the level's two work-list counters (tie-class items, exact items).
+__global__ void level_prep_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
+                                  NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
+                                  int32_t* __restrict__ hcnt, int* __restrict__ n_items) {
+  FS_PDL_WAIT();
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) n_items[threadIdx.x] = 0;
   const int f = blockIdx.y;
   const FamDesc fd = fam[f];
-  if (!st[f].active || level >= max(fd.depth, 1)) return;
+  if (!st[f].active) return;
+  if (blockIdx.x == 0)
+    for (int local = threadIdx.x; local < (1 << level); local += blockDim.x) plan_node(fd, nodes, level, local);
+  if (level >= max(fd.depth, 1)) return;
   const int64_t base = fd.hist0 + static_cast<int64_t>(level & 1) * fd.level_slots * fd.bins;
   const int64_t cnt = static_cast<int64_t>(min(1 << level, fd.level_slots)) * fd.bins;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
@@ -594,42 +602,6 @@ inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes, int c
   return o;
 }
 
-// sibling = parent - built child (exact: integer histograms)
-__global__ void hist_derive_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
-                                   const NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
-                                   int32_t* __restrict__ hcnt, int64_t* __restrict__ node_abs) {
-  FS_PDL_WAIT();
-  const int f = blockIdx.z;
-  const FamDesc fd = fam[f];
-  if (!st[f].active || level == 0) return;
-  const NodeRec* nd = nodes + fd.node0;
-  const int k = blockIdx.y;
-  if (k >= (1 << (level - 1))) return;
-  const int parent = (1 << (level - 1)) - 1 + k;
-  if (nd[parent].state != kNodeSplit) return;
-  const int c1 = 2 * parent + 1, c2 = c1 + 1;
-  int built, other;
-  if (nd[c1].build == 1 && nd[c2].build == 2) {
-    built = c1;
-    other = c2;
-  } else if (nd[c2].build == 1 && nd[c1].build == 2) {
-    built = c2;
-    other = c1;
-  } else {
-    return;
-  }
-  const int first = (1 << level) - 1, pfirst = (1 << (level - 1)) - 1;
-  const int64_t hb = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + (built - first)) * fd.bins;
-  const int64_t ho = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + (other - first)) * fd.bins;
-  const int64_t hp = fd.hist0 + (static_cast<int64_t>((level - 1) & 1) * fd.level_slots + (parent - pfirst)) * fd.bins;
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < fd.bins; b += gridDim.x * blockDim.x) {
-    hsum[ho + b] = hsum[hp + b] - hsum[hb + b];
-    hcnt[ho + b] = hcnt[hp + b] - hcnt[hb + b];
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    node_abs[fd.node0 + other] = node_abs[fd.node0 + parent] - node_abs[fd.node0 + built];
-}
-
 // Screened gain of one candidate plus a rigorous bound on |reference gain - screened gain|.
 // ls/ts: fixed-point left/total sums; S: sum|r| of the node (real units); scale = 2^-shift.
 // The reference folds sums sequentially (error <= gamma_n * S each), R = T - L rounds once,
@@ -677,8 +649,8 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
 // One thread per (family, node at level, rep). pass 0: max lower bound per node. pass 1:
 // window membership (hi >= LO and hi > 0), per-feature best candidate, node window count.
 __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
-                              NodeRec* __restrict__ nodes, int level, const int64_t* __restrict__ hsum,
-                              const int32_t* __restrict__ hcnt, const int64_t* __restrict__ node_abs,
+                              NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
+                              int32_t* __restrict__ hcnt, int64_t* __restrict__ node_abs,
                               const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
                               WinRec* __restrict__ win, int nrep_max, int level_slots_max, int pass) {
   FS_PDL_WAIT();
@@ -700,7 +672,25 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
                      rep_boff[fd.rep0 + jj];
   const int nb = rep_nb[fd.rep0 + jj];
   const double scale = ldexp(1.0, -st[f].shift);
-  const double S = static_cast<double>(node_abs[fd.node0 + s]) * scale * (1.0 + 1e-12);
+  int64_t nabs = node_abs[fd.node0 + s];
+  if (pass == 0 && nd.build == 2) {
+    // the sibling-derived histogram (parent - built sibling), this warp's feature: written here
+    // for the pass-1 screen and the next level's derivations (no separate derive launch)
+    const int parent = (s - 1) >> 1, sib = (s & 1) ? s + 1 : s - 1;
+    const int first = (1 << level) - 1, pfirst = (1 << (level - 1)) - 1;
+    const int64_t hs = fd.hist0 + (static_cast<int64_t>(level & 1) * fd.level_slots + (sib - first)) * fd.bins +
+                       rep_boff[fd.rep0 + jj];
+    const int64_t hp = fd.hist0 + (static_cast<int64_t>((level - 1) & 1) * fd.level_slots + (parent - pfirst)) * fd.bins +
+                       rep_boff[fd.rep0 + jj];
+    for (int b = lane; b < nb; b += 32) {
+      hsum[hb + b] = hsum[hp + b] - hsum[hs + b];
+      hcnt[hb + b] = hcnt[hp + b] - hcnt[hs + b];
+    }
+    __syncwarp();
+    nabs = node_abs[fd.node0 + parent] - node_abs[fd.node0 + sib];
+    if (jj == 0 && lane == 0) node_abs[fd.node0 + s] = nabs;
+  }
+  const double S = static_cast<double>(nabs) * scale * (1.0 + 1e-12);
   int64_t ts = 0;
   for (int b = lane; b < nb; b += 32) ts += hsum[hb + b];
   for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);

@@ -16,9 +16,12 @@
 // cta_fold_est (all threads of the CTA call it; every thread gets the result):
 //   per super-segment of up to kFoldE * blockDim elements (sub-blocks of E <= kFoldE elements
 //   per thread, held in registers and staged in shared memory):
-//     1. every thread sums its sub-block in double-double; CTA exclusive scan -> P at every
-//        sub-block start (anchored at the exact start of the super-segment)
-//     2. every thread re-walks its sub-block accumulating e^_i; CTA exclusive scan -> D^
+//     1. every thread sums its sub-block; warp scan + warp totals -> the prefix P at every
+//        sub-block start (anchored at the exact start of the super-segment; plain doubles, a few
+//        ulps off - the window absorbs that, and a step's rounding error depends only on the
+//        running sum's binade and grid, which a few ulps do not change)
+//     2. every thread re-walks its sub-block as a rounded fold from its P, accumulating each
+//        step's rounding error (TwoSum); warp totals -> D^ at every segment start
 //     3. warp k folds segment k (32 sub-blocks) from the 32 doubles fl(P_k + D^_k) - 16 .. +15
 //        ulp (warp 0 from the exact start); 16-byte broadcast loads from the stage
 //     4. thread 0 walks the segments: the lane whose start is bit-identical to the true end of
@@ -44,25 +47,6 @@ __device__ __forceinline__ long long dbl_ord(double x) {  // consecutive doubles
 __device__ __forceinline__ double ord_dbl(long long o) {
   return __longlong_as_double(o >= 0 ? o : static_cast<long long>(0x8000000000000000ull) - o);
 }
-// double-double sum, renormalised (|lo| <= ulp(hi) / 2)
-__device__ __forceinline__ void dd_add(double ah, double al, double bh, double bl, double& rh, double& rl) {
-  double s, e;
-  two_sum(ah, bh, s, e);
-  e = fs_add(e, fs_add(al, bl));
-  rh = fs_add(s, e);
-  rl = fs_sub(e, fs_sub(rh, s));
-}
-
-// Warp-wide sum of double-doubles (every lane gets it; xor butterfly, the same order on every
-// lane, so the result is lane-independent).
-__device__ __forceinline__ void warp_sum_dd(double& h, double& l) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double oh = __shfl_xor_sync(0xffffffffu, h, o), ol = __shfl_xor_sync(0xffffffffu, l, o);
-    dd_add(h, l, oh, ol, h, l);
-  }
-}
-
 // Stage layout: thread t's sub-block (E <= EMAX elements) at t * (EMAX + 2): the two pad
 // doubles keep the sub-block accesses conflict-free while the folds read runs of 16-byte words
 // in order.
@@ -189,52 +173,36 @@ __device__ __forceinline__ double cta_fold_est_impl(const double* __restrict__ v
     }
     FE_MARK(0)
     // 1. double-double sum of the sub-block; warp scan + warp totals -> exact prefix at b0
-    double h = 0.0, l = 0.0;
+    double h = 0.0;
 #pragma unroll
-    for (int u = 0; u < kFoldE; ++u) {
-      if (u < cnt) {
-        double s, e;
-        two_sum(h, x[u], s, e);
-        h = s;
-        l = fs_add(l, e);
-      }
-    }
-    double ih = h, il = l;
+    for (int u = 0; u < kFoldE; ++u)
+      if (u < cnt) h = fs_add(h, x[u]);
+    double ih = h;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const double oh = __shfl_up_sync(0xffffffffu, ih, o), ol = __shfl_up_sync(0xffffffffu, il, o);
-      if (lane >= o) dd_add(oh, ol, ih, il, ih, il);
+      const double oh = __shfl_up_sync(0xffffffffu, ih, o);
+      if (lane >= o) ih = fs_add(oh, ih);
     }
-    if (lane == 31) {
-      wt[2 * warp] = ih;
-      wt[2 * warp + 1] = il;
-    }
-    double xh = __shfl_up_sync(0xffffffffu, ih, 1), xl = __shfl_up_sync(0xffffffffu, il, 1);
-    if (lane == 0) xh = xl = 0.0;
+    if (lane == 31) wt[2 * warp] = ih;
+    double xh = __shfl_up_sync(0xffffffffu, ih, 1);
+    if (lane == 0) xh = 0.0;
     FE_MARK(1)
     __syncthreads();
-    double wh = lane < warp ? wt[2 * lane] : 0.0, wl = lane < warp ? wt[2 * lane + 1] : 0.0;
-    warp_sum_dd(wh, wl);  // the warps before this one
-    double ph, pl;
-    dd_add(S, 0.0, wh, wl, ph, pl);  // prefix at the segment (warp) start
-    const double seg_h = ph, seg_l = pl;
-    dd_add(ph, pl, xh, xl, ph, pl);  // prefix at this thread's sub-block
+    double wh = lane < warp ? wt[2 * lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wh = fs_add(wh, __shfl_xor_sync(0xffffffffu, wh, o));
+    const double seg_pre = fs_add(S, wh);
     FE_MARK(2)
-    // 2. estimated rounding errors over the sub-block; warp totals
     double d = 0.0;
     {
-      double qh = ph, ql = pl;
+      double q = fs_add(seg_pre, xh);
 #pragma unroll
       for (int u = 0; u < kFoldE; ++u) {
         if (u < cnt) {
-          const double sh = fs_add(qh, ql);
           double y, err;
-          two_sum(sh, x[u], y, err);  // y + err == sh + x exactly: the rounding error is -err
+          two_sum(q, x[u], y, err);  // the rounding error of this step is -err
           d = fs_sub(d, err);
-          double s, e;
-          two_sum(qh, x[u], s, e);
-          qh = s;
-          ql = fs_add(ql, e);
+          q = y;
         }
       }
     }
@@ -246,9 +214,7 @@ __device__ __forceinline__ double cta_fold_est_impl(const double* __restrict__ v
     double dw = lane < warp ? dt[lane] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dw = fs_add(dw, __shfl_xor_sync(0xffffffffu, dw, o));
-    double eh, el;
-    dd_add(seg_h, seg_l, dw, 0.0, eh, el);
-    const double est_k = fs_add(eh, el);  // the same on every lane of the warp
+    const double est_k = fs_add(seg_pre, dw);
     FE_MARK(4)
     // 3. speculative folds: warp 0 from the exact start, warp k from est_k - 16 .. + 15 ulp
     const int seg0 = min(warp * 32 * E, L), seg_n = min(L - seg0, 32 * E);
