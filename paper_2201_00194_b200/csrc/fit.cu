@@ -445,20 +445,12 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       }
       dev->count_launch(8);
     }
-    const int64_t leaf_threads = static_cast<int64_t>(F) * slots * 32;
     {
       ProfScope prof(dev, "fit_leaf");
-      if (std::getenv("FAMSEER_LEAF_WARP"))
-        leaf_kernel<<<static_cast<unsigned>(ceil_div(leaf_threads, 256)), 256, 0, s>>>(fam_d, F, st_d, nodes, slots,
-                                                                                         ord_cur, resid, pred, trees_d);
-      else
-        launch_pdl(leaf_cta_kernel, dim3(static_cast<unsigned>(slots), F), dim3(kLeafThreads), 0, s, fam_d, F, st_d, nodes,
-                   slots, ord_cur, resid, pred, trees_d);
+      launch_pdl(leaf_cta_kernel, dim3(static_cast<unsigned>(slots), F), dim3(kLeafThreads), 0, s, fam_d, F, st_d, nodes,
+                 slots, ord_cur, resid, pred, trees_d, target_c, ebuf, mse_k, n_tot);
     }
-    launch_pdl(mse_stash_kernel, dim3(grid1(n_tot, 256, sm * 16)), dim3(256), 0, s, fam_d, st_d, nodes, rowfam, n_tot,
-               target_c, pred, ebuf, mse_k);
     launch_pdl(commit_kernel, dim3(static_cast<unsigned>(ceil_div(F, 128))), dim3(128), 0, s, fam_d, st_d, nodes, F);
-    dev->count_launch();
     dev->count_launch(2);
     FS_CUDA(cudaGetLastError());
   };

@@ -2055,7 +2055,8 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
                                                        const FamState* __restrict__ st, NodeRec* __restrict__ nodes,
                                                        int slots, const int32_t* __restrict__ ord_cur,
                                                        const double* __restrict__ resid, double* __restrict__ pred,
-                                                       TreeRec* __restrict__ trees) {
+                                                       TreeRec* __restrict__ trees, const double* __restrict__ target_c,
+                                                       double* __restrict__ ebuf, int K, int64_t n_tot) {
   FS_PDL_WAIT();
   __shared__ __align__(16) double stage[fold_est_stage_doubles(kLeafThreads)];
   __shared__ double fscr[fold_est_scratch_doubles(kLeafThreads)];
@@ -2083,21 +2084,32 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
   }
   const double value = fs_div(sum, static_cast<double>(n));
   const double step = fs_mul(fd.lr, value);
+  // the round commits unless the tree is a single leaf of value exactly 0 (round_commits); then
+  // e = target - prediction of each row goes to the MSE ring slot of this round (mse_stash)
+  const bool commits = !(s == 0 && value == 0.0);
+  double* eb = ebuf + static_cast<int64_t>(st[f].ntrees % K) * n_tot;
   // prediction update, 8 rows per thread in flight (index and prediction gathers issued before
   // the stores: the compiler cannot prove the arrays do not alias)
   for (int i0 = 0; i0 < n; i0 += 8 * static_cast<int>(blockDim.x)) {
     int64_t pp[8];
-    double pv[8];
+    double pv[8], tv[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int i = i0 + k * blockDim.x + threadIdx.x;
       pp[k] = i < n ? fd.pos0 + L[i] : -1;
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) pv[k] = pp[k] >= 0 ? pred[pp[k]] : 0.0;
+    for (int k = 0; k < 8; ++k) {
+      pv[k] = pp[k] >= 0 ? pred[pp[k]] : 0.0;
+      tv[k] = pp[k] >= 0 ? target_c[pp[k]] : 0.0;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (pp[k] >= 0) pred[pp[k]] = fs_add(pv[k], step);
+      if (pp[k] >= 0) {
+        const double np = fs_add(pv[k], step);
+        pred[pp[k]] = np;
+        if (commits) eb[pp[k]] = fs_sub(tv[k], np);  // this round's MSE term (costmodel.cpp:215-220)
+      }
   }
   if (threadIdx.x == 0) {
     nd.value = value;
@@ -2113,57 +2125,6 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
   }
 }
 
-// Leaves: value = (reference-order total) / n (costmodel.cpp:86), prediction += lr * value
-// (:88-90); tree record. One warp per (family, slot).
-__global__ void leaf_kernel(const FamDesc* __restrict__ fam, int F, const FamState* __restrict__ st,
-                            NodeRec* __restrict__ nodes, int slots, const int32_t* __restrict__ ord_cur,
-                            const double* __restrict__ resid, double* __restrict__ pred, TreeRec* __restrict__ trees) {
-  FS_PDL_WAIT();
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int f = static_cast<int>(w / slots), s = static_cast<int>(w % slots);
-  if (f >= F) return;
-  const FamDesc fd = fam[f];
-  if (!st[f].active) return;
-  NodeRec& nd = nodes[fd.node0 + s];
-  if (nd.state != kNodeLeaf || nd.n == 0) return;
-  // a slot is a leaf of this tree only if its parent split (or it is the root)
-  if (s > 0 && nodes[fd.node0 + ((s - 1) >> 1)].state != kNodeSplit) return;
-  const int n = nd.n;
-  const int32_t* L = ord_cur + fd.pos0 + nd.seg;
-  // the same fold as the node total when totals_kernel already produced it (costmodel.cpp:86)
-  const double sum = nd.pad_ ? nd.total : warp_fold_gather(resid + fd.pos0, L, n);
-  const double value = fs_div(sum, static_cast<double>(n));
-  const double step = fs_mul(fd.lr, value);
-  // prediction update, 8 rows per lane in flight (a plain loop serialises on L2 latency:
-  // the compiler cannot prove the index and prediction arrays do not alias)
-  for (int i0 = 0; i0 < n; i0 += 256) {
-    int64_t pp[8];
-    double pv[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = i0 + 32 * k + lane;
-      pp[k] = i < n ? fd.pos0 + L[i] : -1;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) pv[k] = pp[k] >= 0 ? pred[pp[k]] : 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (pp[k] >= 0) pred[pp[k]] = fs_add(pv[k], step);
-  }
-  if (lane == 0) {
-    nd.value = value;
-    TreeRec r;
-    r.kind = kNodeLeaf;
-    r.feature = -1;
-    r.threshold = 0.0;
-    r.value = value;
-    r.gain = 0.0;
-    r.rep = -1;
-    r.bin = 0;
-    trees[fd.tree0 + static_cast<int64_t>(st[f].ntrees) * slots + s] = r;
-  }
-}
 
 // Commit the round's tree or stop (costmodel.cpp:212), then train_mse_by_round (:215-220).
 // The reference folds e*e over the canonical rows sequentially, and so does mse_fold_kernel -
@@ -2175,20 +2136,6 @@ __device__ __forceinline__ bool round_commits(const FamDesc& fd, const FamState&
   if (!st.active) return false;
   const NodeRec& root = nodes[fd.node0];
   return !(root.state == kNodeLeaf && root.value == 0.0);
-}
-// e of the committing round t = st.ntrees into ring slot t % K ([K][n_tot], canonical rows).
-__global__ void mse_stash_kernel(const FamDesc* __restrict__ fam, const FamState* __restrict__ st,
-                                 const NodeRec* __restrict__ nodes, const int32_t* __restrict__ rowfam, int64_t n_tot,
-                                 const double* __restrict__ target_c, const double* __restrict__ pred,
-                                 double* __restrict__ ebuf, int K) {
-  FS_PDL_WAIT();
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_tot;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int f = rowfam[i];
-    const FamDesc& fd = fam[f];
-    if (!round_commits(fd, st[f], nodes)) continue;
-    ebuf[static_cast<int64_t>(st[f].ntrees % K) * n_tot + i] = fs_sub(target_c[i], pred[i]);
-  }
 }
 __global__ void commit_kernel(const FamDesc* __restrict__ fam, FamState* __restrict__ st,
                               const NodeRec* __restrict__ nodes, int F) {
