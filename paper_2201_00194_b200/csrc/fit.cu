@@ -338,6 +338,9 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   int32_t* small_scratch = std::getenv("FAMSEER_EXACT_SCAN")
                                ? nullptr
                                : ar.alloc<int32_t>(static_cast<size_t>(kExactSmallCtas) * 2 * std::max(n_max, 1));
+  if (small_scratch)
+    FS_CUDA(cudaFuncSetAttribute(exact_small_kernel<CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(exact_small_smem<CodeT>())));
   cudaStream_t aux = fork_totals ? dev->aux_stream() : nullptr;
   auto round_body = [&]() {
     launch_pdl(round_init_kernel, dim3(F), dim3(256), 0, s, fam_d, st_d, nodes, slots, trees_d, node_abs);
@@ -420,7 +423,7 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
                    codes_cm, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win, std::max(nrep_max, 1), level_slots_max,
                    small_scratch ? 1 : 0);
         if (small_scratch)
-          launch_pdl(exact_small_kernel<CodeT>, dim3(kExactSmallCtas), dim3(kSortThreads), 0, s, fam_d, nodes, items,
+          launch_pdl(exact_small_kernel<CodeT>, dim3(kExactSmallCtas), dim3(kSortThreads), exact_small_smem<CodeT>(), s, fam_d, nodes, items,
                      n_items + 1, level, Dp, codes_cm, resid, ord, ord_cur, nodeid, rep_boff_d, lbuf, win,
                      std::max(nrep_max, 1), level_slots_max, small_scratch, n_max);
       }

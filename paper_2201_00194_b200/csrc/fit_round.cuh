@@ -1479,6 +1479,13 @@ constexpr int kExactSpecMin = 1024;  // chains from this length fold in a CTA (c
 // node ids), stable-sorts them by the feature's code (the presorted order restricted to the
 // node is exactly (code, canonical position) order), and warp 0 folds them - the same adds in
 // the same order as best_split (costmodel.cpp:50-69), stopping at the last window candidate.
+constexpr int kExactFoldE = 8;  // exact_small's fold sub-blocks (8 elements x 1,024 threads per super-segment)
+template <typename CodeT>
+constexpr size_t exact_small_smem() {
+  const size_t fold = (static_cast<size_t>(fold_est_stage_doubles(kSortThreads, kExactFoldE)) +
+                       fold_est_scratch_doubles(kSortThreads)) * 8 + static_cast<size_t>(kExactFoldE) * kSortThreads * sizeof(CodeT);
+  return fold > sizeof(SortSmem) ? fold : sizeof(SortSmem);
+}
 template <typename CodeT>
 __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const FamDesc* __restrict__ fam, NodeRec* __restrict__ nodes, const ExactItem* __restrict__ items,
@@ -1493,12 +1500,13 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
   union FoldOrSort {
     SortSmem sort;
     struct {
-      double stage[fold_est_stage_doubles(kSortThreads, 2)];
+      double stage[fold_est_stage_doubles(kSortThreads, kExactFoldE)];
       double scr[fold_est_scratch_doubles(kSortThreads)];
-      CodeT cst[2 * kSortThreads];
+      CodeT cst[kExactFoldE * kSortThreads];
     } fold;
   };
-  __shared__ __align__(16) FoldOrSort u;
+  extern __shared__ __align__(16) unsigned char xs_raw[];  // exact_small_smem<CodeT>() bytes
+  FoldOrSort& u = *reinterpret_cast<FoldOrSort*>(xs_raw);
   SortSmem& sm = u.sort;
   __shared__ int wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1506,13 +1514,13 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
   sort_smem_init(sm);
   auto fold_at = [&](int64_t pos0, const int32_t* list, int len) {
     __syncthreads();  // the sort state is dead
-    const double r = cta_fold_est<2>(resid + pos0, list, len, 0.0, u.fold.stage, u.fold.scr);
+    const double r = cta_fold_est<kExactFoldE>(resid + pos0, list, len, 0.0, u.fold.stage, u.fold.scr);
     sort_smem_init(sm);
     return r;
   };
   auto fold_rec = [&](int64_t pos0, const int32_t* list, int len, const CodeT* cj, double* out) {
     __syncthreads();
-    cta_fold_est_rec<2, CodeT>(resid + pos0, list, len, cj, out, u.fold.stage, u.fold.cst, u.fold.scr);
+    cta_fold_est_rec<kExactFoldE, CodeT>(resid + pos0, list, len, cj, out, u.fold.stage, u.fold.cst, u.fold.scr);
     sort_smem_init(sm);
   };
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
