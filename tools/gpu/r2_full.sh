@@ -10,6 +10,8 @@ timeout 900 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.er
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_c2.json 2> gpurun_out/bench_ref_c2.err; echo ref=$?
 for c in c1 c3; do timeout 600 python bench.py --config $c --no-secondary > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo $c=$?; done
 timeout 900 python bench.py --config c4 --steps 3 --warmup 3 --no-secondary > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo c4=$?
+timeout 1500 python bench.py --config c5 --steps 2 --warmup 3 --no-cpu --no-e2e --no-secondary > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo c5=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4_fit20.csv python tools/fit_once.py c4 20 > /dev/null 2>&1; echo ncu_c4=$?
 FAMSEER_BENCH_SHARE_GPU=1 timeout 600 python bench.py --gpus 2 --no-cpu --no-e2e --no-secondary > gpurun_out/bench_n2_shared.json 2> gpurun_out/bench_n2_shared.err; echo n2=$?
 timeout 600 python tools/roofline_probe.py --families 8 --rows 65536 --trees 1000 > gpurun_out/roofline_probe.json 2> gpurun_out/roofline_probe.err; echo probe=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-secondary > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
