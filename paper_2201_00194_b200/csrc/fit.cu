@@ -118,7 +118,7 @@ inline unsigned grid1(int64_t n, int block, int cap) {
 // dependencies become programmatic edges). FAMSEER_NO_PDL=1 launches them plainly.
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
-  static const bool off = std::getenv("FAMSEER_NO_PDL") != nullptr;
+  const bool off = std::getenv("FAMSEER_NO_PDL") != nullptr;  // read per launch (a test toggles it)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

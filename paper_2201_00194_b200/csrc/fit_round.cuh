@@ -1123,348 +1123,7 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 }
 
 
-constexpr int kSpecMulti = 8192;  // cta_fold_spec: chains from this length fold in four segments (three speculated)
-constexpr int kSpecRed = 200;      // cta_fold_spec's shared scratch (doubles)
-// (two_sum, dbl_ord, ord_dbl: fold_est.cuh)
-// CTA-wide exact sequential fold of a long gathered chain (sum_residuals, costmodel.cpp:36-40) by
-// midpoint speculation (the warp version is fold_spec): the block's double-double sum of
-// x_0..x_{m-1} estimates the exact prefix P; thread 0 folds x_0..x_{m-1} from 0.0 (the true S_m)
-// while threads t = 1..255 fold x_m..x_{n-1} from the doubles P + (t-128) ulp; the thread whose
-// start is bit-identical to S_m holds S_n. A miss finishes the chain from S_m (same result).
-// All 256 threads must call it; the result is returned to every thread.
-__device__ __forceinline__ double warp_fold_gather_from(const double* __restrict__ v, const int32_t* __restrict__ idx,
-                                                        int n, double s) {
-  // warp_fold_gather with a per-lane start value: every lane folds the same sequence (loaded
-  // cooperatively, 128 gathers in flight ahead of the adds) from its own start
-  const int lane = threadIdx.x & 31;
-  double x[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int i = 32 * c + lane;
-    x[c] = i < n ? v[idx[i]] : 0.0;
-  }
-  for (int i0 = 0; i0 < n; i0 += 128) {
-    double y[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = i0 + 128 + 32 * c + lane;
-      y[c] = i < n ? v[idx[i]] : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int base = i0 + 32 * c;
-      if (base >= n) break;
-      const int m = min(32, n - base);
-      if (m == 32) {
-#pragma unroll
-        for (int l0 = 0; l0 < 32; l0 += 8) {
-          double t[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, x[c], l0 + k);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) s = fs_add(s, t[k]);
-        }
-      } else {
-        for (int l = 0; l < m; ++l) s = fs_add(s, __shfl_sync(0xffffffffu, x[c], l));
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) x[c] = y[c];
-  }
-  return s;
-}
-
-__device__ __forceinline__ double cta_fold_spec(const double* __restrict__ v, const int32_t* __restrict__ idx, int n,
-                                                double* red /* smem [kSpecRed] */) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = static_cast<int>(blockDim.x >> 5);
-  if (n < 4096 || nw < 2) {  // short chain: warp 0 folds it
-#ifdef FS_SPEC_PROBE
-    const long long q0 = clock64();
-#endif
-    if (warp == 0) {
-      const double r = warp_fold_gather_from(v, idx, n, 0.0);
-      if (lane == 0) red[196] = r;
-    }
-    __syncthreads();
-#ifdef FS_SPEC_PROBE
-    if (tid == 0) printf("SPEC short n=%d nt=%d cyc=%lld\n", n, blockDim.x, clock64() - q0);
-#endif
-    const double r = red[196];
-    __syncthreads();
-    return r;
-  }
-  // G speculative segments after the first: 3 for long chains in CTAs of >= 16 warps, else 1.
-  // Segment g = [b(g), b(g+1)), b(g) = g*n/(G+1); warp 0 folds segment 0 from 0.0, the other
-  // warps are split into G groups and group g folds segment g from the candidate starts
-  // P_g + k ulp around the double-double estimate P_g of the exact prefix up to b(g).
-  const int G = (n >= kSpecMulti && nw >= 4) ? 3 : 1;
-  const int K = G + 1;
-  auto bnd = [&](int g) { return static_cast<int>((static_cast<long long>(g) * n) / K); };
-  // 1. double-double sums of segments 0..G-1 (8 gathers in flight), per-warp partials to smem
-#pragma unroll
-  for (int g = 0; g < 3; ++g) {
-    if (g >= G) break;
-    double hi = 0.0, lo = 0.0;
-    const int a = bnd(g), e = bnd(g + 1);
-    for (int i0 = a + tid; i0 < e; i0 += 8 * blockDim.x) {
-      double x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = i0 + k * blockDim.x;
-        x[k] = i < e ? v[idx[i]] : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        double s, err;
-        two_sum(hi, x[k], s, err);
-        hi = s;
-        lo = fs_add(lo, err);
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
-      double s, err;
-      two_sum(hi, oh, s, err);
-      hi = s;
-      lo = fs_add(fs_add(lo, ol), err);
-    }
-    if (lane == 0) {
-      red[64 * g + warp] = hi;
-      red[64 * g + 32 + warp] = lo;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {  // prefix estimates P_1..P_G
-    double h = 0.0, l = 0.0;
-    for (int g = 0; g < G; ++g) {
-      for (int w = 0; w < nw; ++w) {
-        double s, err;
-        two_sum(h, red[64 * g + w], s, err);
-        h = s;
-        l = fs_add(fs_add(l, red[64 * g + 32 + w]), err);
-      }
-      red[192 + g] = fs_add(h, l);
-    }
-  }
-  __syncthreads();
-  // 2. every chain at once: warp 0 from 0.0, group g's threads from P_g + (c - C/2) ulp
-  const int grp = warp == 0 ? 0 : 1 + ((warp - 1) * G) / (nw - 1);
-  int wfirst = 1;
-  while (wfirst < nw && 1 + ((wfirst - 1) * G) / (nw - 1) < grp) ++wfirst;
-  int wlast = wfirst;
-  while (wlast + 1 < nw && 1 + (wlast * G) / (nw - 1) == grp) ++wlast;
-  const int C = 32 * (wlast - wfirst + 1);
-  const double start = grp == 0 ? 0.0 : ord_dbl(dbl_ord(red[192 + grp - 1]) + (tid - 32 * wfirst - C / 2));
-  const int a = bnd(grp), e = bnd(grp + 1);
-  const double r = warp_fold_gather_from(v, idx + a, e - a, start);
-  __shared__ int hit;
-  if (tid == 0) red[196] = r;  // S_1, the true prefix at b(1)
-  __syncthreads();
-  // 3. resolve segment by segment: the thread whose start is bit-identical to the true prefix
-  // holds the next true prefix; a miss finishes the chain sequentially from the true prefix
-  for (int g = 1; g <= G; ++g) {
-    if (tid == 0) hit = 0;
-    __syncthreads();
-    if (grp == g && __double_as_longlong(start) == __double_as_longlong(red[196])) {
-      red[197] = r;
-      hit = 1;
-    }
-    __syncthreads();
-    if (!hit) {
-      if (warp == 0) {
-        const double t = warp_fold_gather_from(v, idx + bnd(g), n - bnd(g), red[196]);
-        if (lane == 0) red[197] = t;
-      }
-      __syncthreads();
-      if (tid == 0) red[196] = red[197];
-      __syncthreads();
-      break;
-    }
-    if (tid == 0) red[196] = red[197];
-    __syncthreads();
-  }
-  const double out = red[196];
-  __syncthreads();
-  return out;
-}
-
-// sum_residuals (costmodel.cpp:36-40) of v[idx[0..n)) in list order by one warp: four chunks of
-// 32 gathers are in flight at once, then each chunk's values are added in lane order (shuffles
-// hoisted ahead of the dependent add chain). Every lane returns the sum.
-
-// cta_fold_spec with the chains' elements staged through shared memory: the K segments advance
-// in lockstep, kStageCh elements at a time gathered cooperatively (every thread one element per
-// pass) into stage[K][kStageCh], and every thread folds its segment's run from shared memory
-// with 16-byte broadcast loads - half a shared load per element instead of two shuffles per
-// element and warp (the speculating warps all read the same run: the shuffle broadcast made the
-// leaf kernels MIO-bound with many CTAs per SM). A missed segment is re-folded alone from the
-// true prefix (by warp 0) and the next segment is still checked against the new value.
-constexpr int kStageCh = 1024;      // leaf CTAs (256 threads)
-constexpr int kStageChSmall = 256;  // exact_small CTAs (1,024 threads: the stage doubles as their result slots)
-__device__ __forceinline__ double cta_fold_spec_staged(const double* __restrict__ v, const int32_t* __restrict__ idx,
-                                                       int n, double* red /* smem [kSpecRed] */,
-                                                       double* stage /* smem [4][ch], >= blockDim doubles */,
-                                                       int ch) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = static_cast<int>(blockDim.x >> 5);
-  if (n < 4096 || nw < 2) return cta_fold_spec(v, idx, n, red);
-  const int G = (n >= kSpecMulti && nw >= 4) ? 3 : 1;
-  const int K = G + 1;
-  auto bnd = [&](int g) { return static_cast<int>((static_cast<long long>(g) * n) / K); };
-#ifdef FS_SPEC_PROBE
-  long long pc0 = clock64(), pc1 = 0, pc2 = 0;
-  int pmiss = 0;
-#endif
-  // 1. double-double estimates of the exact prefix sums at the segment starts
-#pragma unroll
-  for (int g = 0; g < 3; ++g) {
-    if (g >= G) break;
-    double hi = 0.0, lo = 0.0;
-    const int a = bnd(g), e = bnd(g + 1);
-    for (int i0 = a + tid; i0 < e; i0 += 8 * blockDim.x) {
-      double x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = i0 + k * blockDim.x;
-        x[k] = i < e ? v[idx[i]] : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        double s, err;
-        two_sum(hi, x[k], s, err);
-        hi = s;
-        lo = fs_add(lo, err);
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
-      double s, err;
-      two_sum(hi, oh, s, err);
-      hi = s;
-      lo = fs_add(fs_add(lo, ol), err);
-    }
-    if (lane == 0) {
-      red[64 * g + warp] = hi;
-      red[64 * g + 32 + warp] = lo;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double h = 0.0, l = 0.0;
-    for (int g = 0; g < G; ++g) {
-      for (int w = 0; w < nw; ++w) {
-        double s, err;
-        two_sum(h, red[64 * g + w], s, err);
-        h = s;
-        l = fs_add(fs_add(l, red[64 * g + 32 + w]), err);
-      }
-      red[192 + g] = fs_add(h, l);
-    }
-  }
-  __syncthreads();
-  // 2. warp 0 folds segment 0 from 0.0; the other warps split into G groups, group g folding
-  // segment g from P_g + (c - C/2) ulp
-  const int grp = warp == 0 ? 0 : 1 + ((warp - 1) * G) / (nw - 1);
-  int wfirst = 1;
-  while (wfirst < nw && 1 + ((wfirst - 1) * G) / (nw - 1) < grp) ++wfirst;
-  int wlast = wfirst;
-  while (wlast + 1 < nw && 1 + (wlast * G) / (nw - 1) == grp) ++wlast;
-  const int C = 32 * (wlast - wfirst + 1);
-  const double start = grp == 0 ? 0.0 : ord_dbl(dbl_ord(red[192 + grp - 1]) + (tid - 32 * wfirst - C / 2));
-  const int seg_len = bnd(grp + 1) - bnd(grp);
-  int lmax = 0;
-  for (int g = 0; g < K; ++g) lmax = max(lmax, bnd(g + 1) - bnd(g));
-  double s = start;
-  for (int c0 = 0; c0 < lmax; c0 += ch) {
-    for (int t0 = tid; t0 < K * ch; t0 += 8 * blockDim.x) {  // 8 gathers in flight per thread
-      int ix[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = t0 + u * blockDim.x;
-        const int q = t / ch, o = t - q * ch;
-        ix[u] = t < K * ch && c0 + o < bnd(q + 1) - bnd(q) ? idx[bnd(q) + c0 + o] : -1;
-      }
-      double xv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) xv[u] = ix[u] >= 0 ? v[ix[u]] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (ix[u] >= 0) stage[t0 + u * blockDim.x] = xv[u];
-    }
-    __syncthreads();
-    const int m = min(ch, seg_len - c0);
-    if (m > 0) {  // this thread's run: two elements per 16-byte (broadcast) load, 8 in flight
-      const double2* x2 = reinterpret_cast<const double2*>(stage + grp * ch);
-      const int m2 = m >> 1;
-      int k = 0;
-      for (; k + 4 <= m2; k += 4) {
-        double2 a[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] = x2[k + u];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          s = fs_add(s, a[u].x);
-          s = fs_add(s, a[u].y);
-        }
-      }
-      for (; k < m2; ++k) {
-        const double2 a = x2[k];
-        s = fs_add(s, a.x);
-        s = fs_add(s, a.y);
-      }
-      if (m & 1) s = fs_add(s, stage[grp * ch + m - 1]);
-    }
-    __syncthreads();
-  }
-  // 3. resolve segment by segment (every chain result parked in the stage buffer)
-#ifdef FS_SPEC_PROBE
-  pc1 = clock64();
-#endif
-  stage[tid] = s;
-  if (tid == 0) red[196] = s;  // S_1: the true prefix at bnd(1)
-  __shared__ int hit;
-  __syncthreads();
-  for (int g = 1; g <= G; ++g) {
-    if (tid == 0) {
-      int w0 = 1;  // first warp of group g
-      while (w0 < nw && 1 + ((w0 - 1) * G) / (nw - 1) < g) ++w0;
-      int w1 = w0;
-      while (w1 + 1 < nw && 1 + (w1 * G) / (nw - 1) == g) ++w1;
-      const int Cg = 32 * (w1 - w0 + 1);
-      const double S = red[196];
-      const long long k = dbl_ord(S) - dbl_ord(red[192 + g - 1]) + Cg / 2;
-      hit = k >= 0 && k < Cg && __double_as_longlong(ord_dbl(dbl_ord(S))) == __double_as_longlong(S);
-      if (hit) red[197] = stage[32 * w0 + k];
-    }
-    __syncthreads();
-#ifdef FS_SPEC_PROBE
-    if (tid == 0 && !hit) {
-      const long long k = dbl_ord(red[196]) - dbl_ord(red[192 + g - 1]);
-      printf("SPECMISS n=%d g=%d off=%lld S=%.17g P=%.17g\n", n, g, k, red[196], red[192 + g - 1]);
-      ++pmiss;
-    }
-#endif
-    if (!hit) {  // re-fold segment g alone from the true prefix
-      if (warp == 0) {
-        const double t = warp_fold_gather_from(v, idx + bnd(g), bnd(g + 1) - bnd(g), red[196]);
-        if (lane == 0) red[197] = t;
-      }
-      __syncthreads();
-    }
-    if (tid == 0) red[196] = red[197];
-    __syncthreads();
-  }
-  const double out = red[196];
-#ifdef FS_SPEC_PROBE
-  pc2 = clock64();
-  if (tid == 0)
-    printf("SPEC staged n=%d G=%d nt=%d miss=%d est+fold=%lld resolve=%lld\n", n, G, blockDim.x, pmiss, pc1 - pc0,
-           pc2 - pc1);
-#endif
-  __syncthreads();
-  return out;
-}
+// (two_sum, dbl_ord, ord_dbl and the CTA-wide folds: fold_est.cuh)
 
 // One warp per item: reference-order folds. Item rep < 0: node total over the order-0 list
 // (sum_residuals(order[0]), costmodel.cpp:47). Item rep j: best_split's left sums over feature j's
@@ -1540,7 +1199,7 @@ __global__ void __launch_bounds__(kSortThreads) exact_small_kernel(
     const int need = wr.maxlc;
     double* out = lbuf + fd.lbuf0 + static_cast<int64_t>(local) * fd.bins + rep_boff[fd.rep0 + jj];
     // one window candidate: only L at its left count is read (exact_decide_kernel), so a long
-    // fold splits speculatively at its midpoint (cta_fold_spec, bit-exact)
+    // fold needs only the fold up to that count (cta_fold_est, bit-exact)
     const bool spec_one = wr.count == 1 && need >= kExactSpecMin;
     const CodeT* cj = codes_cm + fd.ord0 + static_cast<int64_t>(jj) * fd.n;  // column-major
     if (!exact_is_small(nv, n)) {
@@ -2058,7 +1717,7 @@ __global__ void __launch_bounds__(kPartChunk) partition_scatter_kernel(
 constexpr int kLeafEstMin = 384;   // leaf chains from this length fold through cta_fold_est (fold_est.cuh)
 constexpr int kLeafThreads = 256;  // leaf CTA (1,024 threads with four speculated segments measured slower: C5 leaves 0.59 -> 0.82 s)
 // Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
-// the leaf's order-0 segment / n (cta_fold_spec), then pred += lr*value over its rows.
+// the leaf's order-0 segment / n (cta_fold_est), then pred += lr*value over its rows.
 __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* __restrict__ fam, int F,
                                                        const FamState* __restrict__ st, NodeRec* __restrict__ nodes,
                                                        int slots, const int32_t* __restrict__ ord_cur,

@@ -82,13 +82,16 @@ def check(dev, W, G, fams, positions, trees):
     fo.close()
 
 
-@pytest.fixture(params=["auto", "multi", "multi_col", "multi_rowmajor"])
+@pytest.fixture(params=["auto", "multi", "multi_col", "multi_rowmajor", "multi_nopdl_nograph"])
 def fit_path(request, monkeypatch):
     monkeypatch.setenv("FAMSEER_FIT_PATH", "auto" if request.param == "auto" else "multi")
     if request.param == "multi_col":
         monkeypatch.setenv("FAMSEER_HIST", "col")
     elif request.param == "multi_rowmajor":
         monkeypatch.setenv("FAMSEER_HIST", "rowmajor")
+    elif request.param == "multi_nopdl_nograph":  # plain launches, round by round (no graph)
+        monkeypatch.setenv("FAMSEER_NO_PDL", "1")
+        monkeypatch.setenv("FAMSEER_NO_GRAPH", "1")
     return request.param
 
 
