@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_build_kernel(
   int64_t* s_sum = reinterpret_cast<int64_t*>(smem);
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_sum + (kGlobal ? 0 : static_cast<int64_t>(groups) * bins));
   unsigned char* tail = reinterpret_cast<unsigned char*>(s_cnt + (kGlobal ? 0 : static_cast<int64_t>(groups) * bins));
-  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  tail = smem + ((static_cast<size_t>(tail - smem) + 15) & ~size_t(15));  // (stays a shared-space pointer: LDS, not generic loads)
   CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                          // [kHistTileRows][Dp]
   int64_t* t_fix = reinterpret_cast<int64_t*>(t_codes + kHistTileRows * Dp);  // [kHistTileRows]
   __shared__ unsigned long long s_abs;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kColWarps * 32) hist_build_col_kernel(
   int64_t* s_sum = reinterpret_cast<int64_t*>(smem);                        // [rg][gsz]
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_sum + static_cast<int64_t>(rg) * gsz);
   unsigned char* tail = reinterpret_cast<unsigned char*>(s_cnt + static_cast<int64_t>(rg) * gsz);
-  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  tail = smem + ((static_cast<size_t>(tail - smem) + 15) & ~size_t(15));  // (stays a shared-space pointer: LDS, not generic loads)
   CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                            // [kHistTileRows][Dp]
   int64_t* t_fix = reinterpret_cast<int64_t*>(t_codes + kHistTileRows * Dp);  // [kHistTileRows]
   __shared__ unsigned long long s_abs;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
   int32_t* s_cofs = s_boff + nrep;
   int32_t* s_nbv = s_cofs + nrep;
   unsigned char* tail = reinterpret_cast<unsigned char*>(s_nbv + nrep);
-  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  tail = smem + ((static_cast<size_t>(tail - smem) + 15) & ~size_t(15));  // (stays a shared-space pointer: LDS, not generic loads)
   CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                              // [kAtomTile][Dp]
   uint32_t* t_limb = reinterpret_cast<uint32_t*>(t_codes + kAtomTile * Dp);     // [kAtomTile][3]
   __shared__ unsigned long long s_abs;
