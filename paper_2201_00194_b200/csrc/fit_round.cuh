@@ -381,7 +381,8 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
   // the order, so the root streams rows in canonical order (coalesced tiles) instead of
   // gathering them through the order-0 list
   auto row_at = [&](int i) -> int64_t { return level == 0 ? i : ord_cur[fd.pos0 + i]; };
-  // layout: limbs[3][colh_max][32] u32 (lane columns, see col_height) | acc_sum[bins] i64 |
+  // layout: limbs[colh_max][3][32] u32 (lane columns, see col_height; a cell's three limbs 128 B
+  // apart, so one address + immediate offsets per (row, feature)) | acc_sum[bins] i64 |
   // acc_cnt[bins] i32 | binrep[bins] u16 | boff[nrep] | cofs[nrep] | tile codes | tile limbs
   uint32_t* limb = reinterpret_cast<uint32_t*>(smem);
   int64_t* acc_sum =
@@ -430,10 +431,10 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
     if (nrep <= 32) {
       for (int r = warp * rpw + hm; r < tr; r += (kAtomThreads / 32) * rpw) {
         const uint32_t* tl = tl_all + 3 * r;
-        uint32_t* c = colp + static_cast<int>(tc[r * Dp + hj]) * 32;
+        uint32_t* c = colp + static_cast<int>(tc[r * Dp + hj]) * 96;
         atomicAdd(c, tl[0]);
-        atomicAdd(c + colh * 32, tl[1]);
-        atomicAdd(c + 2 * colh * 32, tl[2]);
+        atomicAdd(c + 32, tl[1]);
+        atomicAdd(c + 64, tl[2]);
       }
     } else if (kPipe && nrep <= 32 * kAtomCofRegs) {  // (registers to spare only in the 1-CTA shape)
       for (int r = warp; r < tr; r += kAtomThreads / 32) {
@@ -443,10 +444,10 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
         for (int t = 0; t < kAtomCofRegs; ++t) {
           const int j = lane + 32 * t;
           if (j >= nrep) break;
-          uint32_t* c = colp + (cofr[t] + static_cast<int>(cr[j])) * 32;
+          uint32_t* c = colp + (cofr[t] + static_cast<int>(cr[j])) * 96;
           atomicAdd(c, l0);
-          atomicAdd(c + colh * 32, l1);
-          atomicAdd(c + 2 * colh * 32, l2);
+          atomicAdd(c + 32, l1);
+          atomicAdd(c + 64, l2);
         }
       }
     } else {
@@ -454,10 +455,10 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
         const uint32_t l0 = tl_all[3 * r], l1 = tl_all[3 * r + 1], l2 = tl_all[3 * r + 2];
         const CodeT* cr = tc + r * Dp;
         for (int j = lane; j < nrep; j += 32) {
-          uint32_t* c = colp + (s_cofs[j] + static_cast<int>(cr[j])) * 32;
+          uint32_t* c = colp + (s_cofs[j] + static_cast<int>(cr[j])) * 96;
           atomicAdd(c, l0);
-          atomicAdd(c + colh * 32, l1);
-          atomicAdd(c + 2 * colh * 32, l2);
+          atomicAdd(c + 32, l1);
+          atomicAdd(c + 64, l2);
         }
       }
     }
@@ -563,14 +564,14 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
       unsigned __int128 U = 0;
       if (nrep <= 32) {
         for (int m = 0; m < rpw; ++m) {
-          const uint32_t* c = limb + bb * 32 + j + m * nrep;
-          U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
-               (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+          const uint32_t* c = limb + bb * 96 + j + m * nrep;
+          U += static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[32]) << 21) +
+               (static_cast<unsigned __int128>(c[64]) << 42);
         }
       } else {
-        const uint32_t* c = limb + (s_cofs[j] + bb) * 32 + (j & 31);
-        U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[colh * 32]) << 21) +
-            (static_cast<unsigned __int128>(c[2 * colh * 32]) << 42);
+        const uint32_t* c = limb + (s_cofs[j] + bb) * 96 + (j & 31);
+        U = static_cast<unsigned __int128>(c[0]) + (static_cast<unsigned __int128>(c[32]) << 21) +
+            (static_cast<unsigned __int128>(c[64]) << 42);
       }
       const uint64_t c = static_cast<uint64_t>((U + (static_cast<unsigned __int128>(1) << 61)) >> 62);
       const unsigned __int128 sv = U - (static_cast<unsigned __int128>(c) << 62);
