@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
   unsigned char* tail = reinterpret_cast<unsigned char*>(s_nbv + nrep);
   tail = smem + ((static_cast<size_t>(tail - smem) + 15) & ~size_t(15));  // (stays a shared-space pointer: LDS, not generic loads)
   CodeT* t_codes = reinterpret_cast<CodeT*>(tail);                              // [kAtomTile][Dp]
-  uint32_t* t_limb = reinterpret_cast<uint32_t*>(t_codes + kAtomTile * Dp);     // [kAtomTile][3]
+  uint32_t* t_limb = reinterpret_cast<uint32_t*>(t_codes + kAtomTile * Dp);     // [kAtomTile][4] (3 limbs + pad: one 16-byte load)
   __shared__ unsigned long long s_abs;
   __shared__ int s_colh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -430,15 +430,16 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
     uint32_t* colp = limb + lane;
     if (nrep <= 32) {
       for (int r = warp * rpw + hm; r < tr; r += (kAtomThreads / 32) * rpw) {
-        const uint32_t* tl = tl_all + 3 * r;
+        const uint4 lv = reinterpret_cast<const uint4*>(tl_all)[r];
         uint32_t* c = colp + static_cast<int>(tc[r * Dp + hj]) * 96;
-        atomicAdd(c, tl[0]);
-        atomicAdd(c + 32, tl[1]);
-        atomicAdd(c + 64, tl[2]);
+        atomicAdd(c, lv.x);
+        atomicAdd(c + 32, lv.y);
+        atomicAdd(c + 64, lv.z);
       }
     } else if (kPipe && nrep <= 32 * kAtomCofRegs) {  // (registers to spare only in the 1-CTA shape)
       for (int r = warp; r < tr; r += kAtomThreads / 32) {
-        const uint32_t l0 = tl_all[3 * r], l1 = tl_all[3 * r + 1], l2 = tl_all[3 * r + 2];
+        const uint4 lv = reinterpret_cast<const uint4*>(tl_all)[r];
+        const uint32_t l0 = lv.x, l1 = lv.y, l2 = lv.z;
         const CodeT* cr = tc + r * Dp;
 #pragma unroll
         for (int t = 0; t < kAtomCofRegs; ++t) {
@@ -452,7 +453,8 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
       }
     } else {
       for (int r = warp; r < tr; r += kAtomThreads / 32) {
-        const uint32_t l0 = tl_all[3 * r], l1 = tl_all[3 * r + 1], l2 = tl_all[3 * r + 2];
+        const uint4 lv = reinterpret_cast<const uint4*>(tl_all)[r];
+        const uint32_t l0 = lv.x, l1 = lv.y, l2 = lv.z;
         const CodeT* cr = tc + r * Dp;
         for (int j = lane; j < nrep; j += 32) {
           uint32_t* c = colp + (s_cofs[j] + static_cast<int>(cr[j])) * 96;
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
 #define FS_ATOM_STAGE(T0, B)                                                                        \
   do {                                                                                              \
     const int tr_ = min(kAtomPipeTile, sub_end - (T0));                                                 \
-    CodeT* tc_ = t_codes + (B) * (kAtomPipeTile * Dp + 12 * kAtomPipeTile / static_cast<int>(sizeof(CodeT)));  \
+    CodeT* tc_ = t_codes + (B) * (kAtomPipeTile * Dp + 16 * kAtomPipeTile / static_cast<int>(sizeof(CodeT)));  \
     uint32_t* tl_ = reinterpret_cast<uint32_t*>(tc_ + kAtomPipeTile * Dp);                              \
     _Pragma("unroll") for (int q = 0; q < kAtomPre; ++q) {                                          \
       const int i = tid + q * kAtomThreads;                                                         \
@@ -505,9 +507,9 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
     unsigned long long a_ = 0;                                                                      \
     if (tid < tr_) {                                                                                \
       const uint64_t u = static_cast<uint64_t>(pfix) + (1ull << 62);                                \
-      tl_[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;                                          \
-      tl_[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;                                \
-      tl_[3 * tid + 2] = static_cast<uint32_t>(u >> 42);                                            \
+      reinterpret_cast<uint4*>(tl_)[tid] = make_uint4(static_cast<uint32_t>(u) & kLimbMask,          \
+                                                      static_cast<uint32_t>(u >> 21) & kLimbMask,    \
+                                                      static_cast<uint32_t>(u >> 42), 0u);           \
       a_ = static_cast<unsigned long long>(pfix < 0 ? -pfix : pfix);                                \
     }                                                                                               \
     if (warp * 32 < tr_) {                                                                          \
@@ -526,7 +528,7 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
           FS_ATOM_STAGE(t0 + kAtomPipeTile, buf ^ 1);
           if (t0 + 2 * kAtomPipeTile < sub_end) FS_ATOM_PREFETCH(t0 + 2 * kAtomPipeTile);
         }
-        const CodeT* tc = t_codes + buf * (kAtomPipeTile * Dp + 12 * kAtomPipeTile / static_cast<int>(sizeof(CodeT)));
+        const CodeT* tc = t_codes + buf * (kAtomPipeTile * Dp + 16 * kAtomPipeTile / static_cast<int>(sizeof(CodeT)));
         add_rows(tc, reinterpret_cast<const uint32_t*>(tc + kAtomPipeTile * Dp), tr);
         __syncthreads();
         buf ^= 1;
@@ -545,9 +547,9 @@ __global__ void __launch_bounds__(kAtomThreads, kPipe ? 1 : 2) hist_build_atomic
         if (tid < tr) {
           const int64_t v = rfix[fd.pos0 + row_at(seg + r0 + t0 + tid)];
           const uint64_t u = static_cast<uint64_t>(v) + (1ull << 62);
-          t_limb[3 * tid] = static_cast<uint32_t>(u) & kLimbMask;
-          t_limb[3 * tid + 1] = static_cast<uint32_t>(u >> 21) & kLimbMask;
-          t_limb[3 * tid + 2] = static_cast<uint32_t>(u >> 42);
+          reinterpret_cast<uint4*>(t_limb)[tid] = make_uint4(static_cast<uint32_t>(u) & kLimbMask,
+                                                             static_cast<uint32_t>(u >> 21) & kLimbMask,
+                                                             static_cast<uint32_t>(u >> 42), 0u);
           a = static_cast<unsigned long long>(v < 0 ? -v : v);
         }
         if (warp * 32 < tr) {
@@ -599,7 +601,7 @@ inline size_t hist_atomic_smem(int bins, int nrep, int Dp, int code_bytes, int c
   o += static_cast<size_t>(bins) * 14 + static_cast<size_t>(nrep) * 12 + 16;
   o = (o + 15) & ~size_t(15);
   const size_t tile = static_cast<size_t>(std::max(kAtomTile, kAtomPipeTile));
-  o += 2 * (tile * Dp * code_bytes + tile * 12) + 16;  // 2 tiles
+  o += 2 * (tile * Dp * code_bytes + tile * 16) + 16;  // 2 tiles
   return o;
 }
 
