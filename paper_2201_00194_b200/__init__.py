@@ -312,23 +312,20 @@ class Forest:
                                        _p(le, _capi._i32p), _p(ri, _capi._i32p), _p(va, _capi._dp)))
 
     def export(self, family: int, lr: float = 0.1) -> Ensemble:
-        L = _lib()
-        base = C.c_double()
-        nt, nn = C.c_int32(), C.c_int32()
-        _check(L.fs_forest_export(self.h, family, C.byref(base), C.byref(nt), C.byref(nn), *([None] * 9)))
-        t, n = nt.value, nn.value
-        off = np.zeros(t + 1, np.int32)
-        feat = np.zeros(n, np.int32)
-        thr = np.zeros(n)
-        le = np.zeros(n, np.int32)
-        ri = np.zeros(n, np.int32)
-        va = np.zeros(n)
-        gain = np.zeros(n)
-        mse = np.zeros(max(t, 1))
-        _check(L.fs_forest_export(self.h, family, C.byref(base), None, None, _p(off, _capi._i32p),
-                                  _p(feat, _capi._i32p), _p(thr, _capi._dp), _p(le, _capi._i32p),
-                                  _p(ri, _capi._i32p), _p(va, _capi._dp), _p(gain, _capi._dp), _p(mse, _capi._dp)))
-        return Ensemble(base.value, lr, off, feat, thr, le, ri, va, gain, mse[:t])
+        raw = _lib().fs_forest_export_raw
+        hdr = np.zeros(4, np.float64)  # base | n_trees, n_nodes (int32 pair in the second word)
+        a0 = hdr.ctypes.data
+        _check(raw(self.h, family, a0, a0 + 8, a0 + 12, *([None] * 8)))
+        t, n = int(hdr[1:2].view(np.int32)[0]), int(hdr[1:2].view(np.int32)[1])
+        # one int32 and one float64 buffer, the arrays as views
+        ib = np.empty(t + 1 + 3 * n, np.int32)
+        db = np.empty(3 * n + max(t, 1), np.float64)
+        ia, da = ib.ctypes.data, db.ctypes.data
+        _check(raw(self.h, family, a0, None, None, ia, ia + 4 * (t + 1), da, ia + 4 * (t + 1 + n),
+                   ia + 4 * (t + 1 + 2 * n), da + 8 * n, da + 16 * n, da + 24 * n))
+        off, feat, le, ri = ib[:t + 1], ib[t + 1:t + 1 + n], ib[t + 1 + n:t + 1 + 2 * n], ib[t + 1 + 2 * n:]
+        thr, va, gain, mse = db[:n], db[n:2 * n], db[2 * n:3 * n], db[3 * n:3 * n + t]
+        return Ensemble(float(hdr[0]), lr, off, feat, thr, le, ri, va, gain, mse)
 
     def predict(self, x, seg=None, leaves: bool = False):
         x = np.ascontiguousarray(x, np.float64)

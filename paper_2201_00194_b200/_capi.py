@@ -107,5 +107,11 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    # the same export entry with raw addresses (the hot per-family export avoids building a
+    # ctypes pointer object per array)
+    raw = lib["fs_forest_export"]
+    raw.restype = C.c_int
+    raw.argtypes = [_vp, C.c_int32] + [C.c_void_p] * 11
+    lib.fs_forest_export_raw = raw
     _lib = lib
     return lib

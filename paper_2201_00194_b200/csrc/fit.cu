@@ -1255,7 +1255,12 @@ int fs_tune_step(fs_device* dev, const fs_spaces* sp, fs_forest* fo, int32_t n_p
           fs::launch_featurize(dev, sp, n, tsd, tad, pad_dim, xd);
           fs::fit::fit_families(dev, fo, n_fit_segments, fit_seg, pad_dim, xd, td, params);
         });
-    fs::raise_deferred(dev->take_errors());  // the host outputs are complete (main joined the fork)
+    // the refit models' host copies ride on the same synchronisation (the next export reads them
+    // without another round trip)
+    const bool staged = fs::materialize_enqueue(dev, fo->fams);
+    const uint32_t bits = dev->take_errors();  // the host outputs are complete (main joined the fork)
+    if (staged && !bits) fs::materialize_parse(dev, fo->fams);
+    fs::raise_deferred(bits);
   });
 }
 

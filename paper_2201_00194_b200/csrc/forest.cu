@@ -142,11 +142,14 @@ void materialize(fs_device* dev, FamilyModel& m) {
 
 // Every pending family of a forest in one pinned device->host read and one synchronisation
 // (a fit leaves all its families pending; the first export of any of them fetches them all).
-void materialize_all(fs_device* dev, std::vector<FamilyModel>& fams) {
+// Split in two so a caller that synchronises anyway (fs_tune_step) can enqueue the read before
+// its own synchronisation: materialize_enqueue stages the copies in the device's pinned buffer
+// (nothing else may use it until materialize_parse), materialize_parse reads them afterwards.
+bool materialize_enqueue(fs_device* dev, std::vector<FamilyModel>& fams) {
   size_t tot = 0;
   for (const auto& m : fams)
     if (m.pending) tot += (m.lay.total - m.lay.meta + 15) & ~size_t(15);
-  if (tot == 0) return;
+  if (tot == 0) return false;
   auto* h = static_cast<unsigned char*>(dev->pinned(tot));
   size_t o = 0;
   for (const auto& m : fams) {
@@ -155,14 +158,22 @@ void materialize_all(fs_device* dev, std::vector<FamilyModel>& fams) {
     FS_CUDA(cudaMemcpyAsync(h + o, m.blob_d + m.lay.meta, bytes, cudaMemcpyDeviceToHost, dev->stream));
     o += (bytes + 15) & ~size_t(15);
   }
-  FS_CUDA(cudaStreamSynchronize(dev->stream));
-  o = 0;
+  return true;
+}
+void materialize_parse(fs_device* dev, std::vector<FamilyModel>& fams) {
+  const auto* h = static_cast<const unsigned char*>(dev->pinned_h);
+  size_t o = 0;
   for (auto& m : fams) {
     if (!m.pending) continue;
     const size_t bytes = m.lay.total - m.lay.meta;
     materialize_from(m, h + o);
     o += (bytes + 15) & ~size_t(15);
   }
+}
+void materialize_all(fs_device* dev, std::vector<FamilyModel>& fams) {
+  if (!materialize_enqueue(dev, fams)) return;
+  FS_CUDA(cudaStreamSynchronize(dev->stream));
+  materialize_parse(dev, fams);
 }
 
 void compile_model(fs_device* dev, FamilyModel& m, UploadBatch* batch) {

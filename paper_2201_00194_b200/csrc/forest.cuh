@@ -93,6 +93,8 @@ struct UploadBatch {
 void materialize(fs_device* dev, FamilyModel& m);
 void materialize(fs_device* dev, const FamilyModel& m);
 void materialize_all(fs_device* dev, std::vector<FamilyModel>& fams);
+bool materialize_enqueue(fs_device* dev, std::vector<FamilyModel>& fams);  // copies into dev->pinned; true if any
+void materialize_parse(fs_device* dev, std::vector<FamilyModel>& fams);    // after the stream synchronised
 
 // Build the compiled device form from the pre-order arrays (host transformation of the tree
 // table; O(nodes)). With a batch, the device copy is deferred to batch->flush().
