@@ -268,6 +268,9 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
   int64_t* node_abs = ar.alloc<int64_t>(static_cast<size_t>(F) * slots);
   int64_t* hsum = ar.alloc<int64_t>(total_hist);
   int32_t* hcnt = ar.alloc<int32_t>(total_hist);
+  // screen pass 0's per-candidate (gain, bound) and left count, read by pass 1 (same cells)
+  double2* scr_gd = ar.alloc<double2>(total_hist);
+  int32_t* scr_ic = ar.alloc<int32_t>(total_hist);
   double* lbuf = ar.alloc<double>(total_lbuf);
   WinRec* win = ar.alloc<WinRec>(static_cast<size_t>(F) * level_slots_max * std::max(nrep_max, 1));
   ExactItem* items = ar.alloc<ExactItem>(static_cast<size_t>(F) * level_slots_max * (nrep_max + 1));
@@ -400,9 +403,9 @@ void run_rounds(const ResidentPlan& resident, fs_device* dev, Arena& ar, int F, 
       {
         ProfScope prof(dev, "fit_screen");
         launch_pdl(screen_kernel, sg, dim3(128), 0, s, fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d,
-                   rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, 0);
+                   rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, 0, scr_gd, scr_ic);
         launch_pdl(screen_kernel, sg, dim3(128), 0, s, fam_d, st_d, nodes, level, hsum, hcnt, node_abs, rep_boff_d,
-                   rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, 1);
+                   rep_nb_d, win, std::max(nrep_max, 1), level_slots_max, 1, scr_gd, scr_ic);
       }
       // (n_items[0]: tie-class items, n_items[1]: exact items; both zeroed by level_prep_kernel)
       launch_pdl(tieclass_prep_kernel, dim3(grid1(lw, 4, 1 << 20), F), dim3(128), 0, s,  // warp per node

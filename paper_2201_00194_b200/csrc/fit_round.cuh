@@ -655,10 +655,12 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
                               NodeRec* __restrict__ nodes, int level, int64_t* __restrict__ hsum,
                               int32_t* __restrict__ hcnt, int64_t* __restrict__ node_abs,
                               const int32_t* __restrict__ rep_boff, const int32_t* __restrict__ rep_nb,
-                              WinRec* __restrict__ win, int nrep_max, int level_slots_max, int pass) {
+                              WinRec* __restrict__ win, int nrep_max, int level_slots_max, int pass,
+                              double2* __restrict__ gcache, int32_t* __restrict__ icache) {
   FS_PDL_WAIT();
   // warp per (node, rep), lanes over the rep's bins: coalesced histogram reads, warp prefix
-  // scans for the left count / sum, every candidate's screen in parallel
+  // scans for the left count / sum, every candidate's screen in parallel (pass 0); pass 1 reads
+  // each candidate's (gain, bound) and left count back from pass 0's cache (the histogram's cells)
   const int f = blockIdx.z;
   const FamDesc fd = fam[f];
   if (!st[f].active) return;
@@ -693,26 +695,42 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
     nabs = node_abs[fd.node0 + parent] - node_abs[fd.node0 + sib];
     if (jj == 0 && lane == 0) node_abs[fd.node0 + s] = nabs;
   }
-  const double S = static_cast<double>(nabs) * scale * (1.0 + 1e-12);
-  int64_t ts = 0;
-  for (int b = lane; b < nb; b += 32) ts += hsum[hb + b];
-  for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
-  const double LO = pass ? lo_from_key(nd.lokey) : 0.0;
   double best_lo = -INFINITY, bg = -INFINITY, bl = 0.0;
-  int bb = 0x7fffffff, blc = 0, count = 0, mlc = 0, carry_c = 0;
-  int64_t carry_s = 0;
-  for (int b0 = 0; b0 < nb; b0 += 32) {
-    const int b = b0 + lane;
-    const int cc = b < nb ? hcnt[hb + b] : 0;
-    const int64_t sv = b < nb ? hsum[hb + b] : 0;
-    const int ic = warp_incl_scan(cc, lane) + carry_c;
-    const int64_t is = warp_incl_scan(sv, lane) + carry_s;
-    if (b < nb && cc > 0 && ic < n) {  // a boundary after bin b (a later bin is non-empty)
-      double g, lo, hi;
-      screen_gain(is, ts, ic, n, scale, S, g, lo, hi);
-      if (!pass) {
-        best_lo = fmax(best_lo, lo);
-      } else if (hi >= LO && hi > 0.0) {
+  int bb = 0x7fffffff, blc = 0, count = 0, mlc = 0;
+  if (!pass) {
+    const double S = static_cast<double>(nabs) * scale * (1.0 + 1e-12);
+    int64_t ts = 0;
+    for (int b = lane; b < nb; b += 32) ts += hsum[hb + b];
+    for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+    int carry_c = 0;
+    int64_t carry_s = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int b = b0 + lane;
+      const int cc = b < nb ? hcnt[hb + b] : 0;
+      const int64_t sv = b < nb ? hsum[hb + b] : 0;
+      const int ic = warp_incl_scan(cc, lane) + carry_c;
+      const int64_t is = warp_incl_scan(sv, lane) + carry_s;
+      if (b < nb) {
+        double g = NAN, delta = 0.0;
+        if (cc > 0 && ic < n) {  // a boundary after bin b (a later bin is non-empty)
+          screen_gain_d(is, ts, ic, n, scale, S, g, delta);
+          best_lo = fmax(best_lo, g - delta);
+        }
+        gcache[hb + b] = make_double2(g, delta);
+        icache[hb + b] = ic;
+      }
+      carry_c = __shfl_sync(0xffffffffu, ic, 31);
+      carry_s = __shfl_sync(0xffffffffu, is, 31);
+    }
+  } else {
+    const double LO = lo_from_key(nd.lokey);
+    for (int b = lane; b < nb; b += 32) {
+      const double2 gd = gcache[hb + b];
+      const double g = gd.x;
+      if (isnan(g)) continue;
+      const double lo = g - gd.y, hi = g + gd.y;  // = screen_gain's lo / hi
+      if (hi >= LO && hi > 0.0) {
+        const int ic = icache[hb + b];
         ++count;
         mlc = max(mlc, ic);
         if (g > bg || (g == bg && b < bb)) {
@@ -723,8 +741,6 @@ __global__ void screen_kernel(const FamDesc* __restrict__ fam, const FamState* _
         }
       }
     }
-    carry_c = __shfl_sync(0xffffffffu, ic, 31);
-    carry_s = __shfl_sync(0xffffffffu, is, 31);
   }
   if (!pass) {
     for (int o = 16; o > 0; o >>= 1) best_lo = fmax(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
