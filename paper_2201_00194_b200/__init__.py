@@ -418,14 +418,15 @@ class Forest:
         tso = np.ascontiguousarray(tr_so, np.int32)
         ta = np.ascontiguousarray(tr_a, np.int32)
         ty = np.ascontiguousarray(tr_target, np.float64)
-        psg, psp = _seg(pool_seg)
-        fsg, fsp = _seg(fit_seg)
+        psg = np.ascontiguousarray(pool_seg, np.int64)
+        fsg = np.ascontiguousarray(fit_seg, np.int64)
         pa = _params_array(params, len(fsg) - 1)
         scores = np.empty(len(so), np.float64)
         perm = np.empty(len(so), np.int32)
-        _check(_lib().fs_tune_step(self.dev.h, spaces.h, self.h, len(psg) - 1, psp, _p(so, _capi._i32p),
-                                   _p(a, _capi._i32p), pad_dim, _p(scores, _capi._dp), _p(perm, _capi._i32p),
-                                   len(fsg) - 1, fsp, _p(tso, _capi._i32p), _p(ta, _capi._i32p), _p(ty, _capi._dp), pa))
+        # raw addresses (the per-step call builds no ctypes pointer objects)
+        _check(_lib().fs_tune_step_raw(self.dev.h, spaces.h, self.h, len(psg) - 1, psg.ctypes.data, so.ctypes.data,
+                                       a.ctypes.data, pad_dim, scores.ctypes.data, perm.ctypes.data, len(fsg) - 1,
+                                       fsg.ctypes.data, tso.ctypes.data, ta.ctypes.data, ty.ctypes.data, pa))
         return scores, perm
 
     def fit_stats(self, family: int):

@@ -113,5 +113,10 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     raw.restype = C.c_int
     raw.argtypes = [_vp, C.c_int32] + [C.c_void_p] * 11
     lib.fs_forest_export_raw = raw
+    raw = lib["fs_tune_step"]
+    raw.restype = C.c_int
+    raw.argtypes = [_vp, _vp, _vp, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                    C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, _vp]
+    lib.fs_tune_step_raw = raw
     _lib = lib
     return lib
