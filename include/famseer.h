@@ -151,7 +151,9 @@ int fs_score_d(fs_device* dev, const fs_spaces* sp, const fs_forest* fo, int32_t
  * fs_tune_step_d: device pointers, training rows as features (fs_fit_d's x/target); returns
  * like fs_fit_d (deferred errors of the scoring surface at the next fs_device_check).
  * fs_tune_step: host pointers, training rows as measurement records featurized on the device
- * (fs_fit_records); scores/perm are complete and every error raised on return. */
+ * (fs_fit_records); scores/perm are complete and every error raised on return, and the refit
+ * models' host copies were fetched in the same synchronisation (fs_forest_export right after
+ * needs no device round trip). */
 int fs_tune_step_d(fs_device* dev, const fs_spaces* sp, fs_forest* fo, int32_t n_pool_segments,
                    const int64_t* pool_seg_h, const int32_t* pool_space_of_d, const int32_t* pool_assign_d,
                    int32_t pad_dim, double* scores_d, int32_t* perm_d, int32_t n_fit_segments,
