@@ -1,7 +1,8 @@
 """fold_est.cuh's CTA folds (cta_fold_est / cta_fold_est_rec) bit-identical to the one-thread
 sequential fold (sum_residuals and best_split's boundary recording, costmodel.cpp:36-69) on
-adversarial chains: builds tools/fold_bench.cu with nvcc for the two CTA shapes the trainer uses
-(256 threads x 16-element sub-blocks: leaves; 1,024 threads x 2: exact_small) and runs it."""
+adversarial chains: builds tools/fold_bench.cu with nvcc for the CTA shapes the trainer uses
+(256 threads x 16-element sub-blocks: leaves; 1,024 threads x 8: exact_small) and two others,
+and runs it."""
 import os
 import subprocess
 
@@ -12,7 +13,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("threads,em", [(256, 16), (1024, 2), (512, 16)])
+@pytest.mark.parametrize("threads,em", [(256, 16), (1024, 8), (1024, 2), (512, 16)])
 def test_fold_est_bit_exact(tmp_path, threads, em):
     exe = tmp_path / f"fold_bench_{threads}_{em}"
     subprocess.run(
