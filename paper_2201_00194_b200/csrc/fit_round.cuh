@@ -1149,7 +1149,10 @@ __global__ void totals_kernel(const FamDesc* __restrict__ fam, const FamState* _
 // presorted list restricted to the node (:50-55), recorded at every value boundary.
 // exact folds of nodes below a quarter of the family go through exact_small_kernel
 __device__ __forceinline__ bool exact_is_small(int nv, int n) { return nv < n; }
-constexpr int kExactSpecMin = 1024;  // chains from this length fold in a CTA (cta_fold_est / cta_fold_est_rec)
+#ifndef FS_EXACT_SPEC_MIN
+#define FS_EXACT_SPEC_MIN 128
+#endif
+constexpr int kExactSpecMin = FS_EXACT_SPEC_MIN;  // chains from this length fold in a CTA (cta_fold_est / cta_fold_est_rec); 1,024 / 512 / 256 measured slower
 
 // Exact reference-order folds for SMALL nodes (nv * 4 < n): instead of scanning the feature's
 // full presorted list for the node's members (exact_kernel; costs O(n) gathers per item however
@@ -1733,7 +1736,10 @@ __global__ void __launch_bounds__(kPartChunk) partition_scatter_kernel(
   }
 }
 
-constexpr int kLeafEstMin = 384;   // leaf chains from this length fold through cta_fold_est (fold_est.cuh)
+#ifndef FS_LEAF_EST_MIN
+#define FS_LEAF_EST_MIN 384
+#endif
+constexpr int kLeafEstMin = FS_LEAF_EST_MIN;   // leaf chains from this length fold through cta_fold_est (fold_est.cuh)
 constexpr int kLeafThreads = 256;  // leaf CTA (1,024 threads with four speculated segments measured slower: C5 leaves 0.59 -> 0.82 s)
 // Leaves (costmodel.cpp:85-91): a CTA per (family, heap slot) - value = reference-order fold of
 // the leaf's order-0 segment / n (cta_fold_est), then pred += lr*value over its rows.
