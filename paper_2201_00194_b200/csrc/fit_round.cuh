@@ -1160,7 +1160,10 @@ constexpr int kExactSpecMin = FS_EXACT_SPEC_MIN;  // chains from this length fol
 // node ids), stable-sorts them by the feature's code (the presorted order restricted to the
 // node is exactly (code, canonical position) order), and warp 0 folds them - the same adds in
 // the same order as best_split (costmodel.cpp:50-69), stopping at the last window candidate.
-constexpr int kExactFoldE = 8;  // exact_small's fold sub-blocks (8 elements x 1,024 threads per super-segment)
+#ifndef FS_EXACT_FOLD_E
+#define FS_EXACT_FOLD_E 8
+#endif
+constexpr int kExactFoldE = FS_EXACT_FOLD_E;  // exact_small's fold sub-blocks (8 elements x 1,024 threads per super-segment)
 template <typename CodeT>
 constexpr size_t exact_small_smem() {
   const size_t fold = (static_cast<size_t>(fold_est_stage_doubles(kSortThreads, kExactFoldE)) +
@@ -1823,7 +1826,10 @@ __global__ void __launch_bounds__(kLeafThreads) leaf_cta_kernel(const FamDesc* _
 // but off the round's critical path: every committed round stashes its e = target - pred (the
 // next round's residual) in a ring of K rounds, and every K rounds one launch folds all
 // (family, round) chains of the ring at once, one thread per chain, in canonical order.
-constexpr int kExactSmallCtas = 64;  // CTAs of exact_small_kernel (items loop over them)
+#ifndef FS_EXACT_SMALL_CTAS
+#define FS_EXACT_SMALL_CTAS 64
+#endif
+constexpr int kExactSmallCtas = FS_EXACT_SMALL_CTAS;  // CTAs of exact_small_kernel (items loop over them)
 __device__ __forceinline__ bool round_commits(const FamDesc& fd, const FamState& st, const NodeRec* nodes) {
   if (!st.active) return false;
   const NodeRec& root = nodes[fd.node0];
